@@ -1,0 +1,171 @@
+/*
+ * hsb200.h -- C ABI of the B200 hot path of the block Jacobi sweeping
+ * preconditioner (arXiv 2209.10886) for the 2D Helmholtz interface problem
+ * (I - S) g = b on an N1 x N2 checkerboard.
+ *
+ * The reference (`helmsweep`, pure Python over SciPy's SuperLU) has no FFI of
+ * its own; its only language boundary is Python -> SuperLU's C code.  Each
+ * entry point below replaces one reference interface (file:line relative to
+ * /root/reference/pkg/src/helmsweep/ unless it names SPEC.md):
+ *
+ *   hs_create / hs_set_dirichlet / hs_factor
+ *       InterfaceSystem.__init__            interface_system.py:73-89
+ *       LocalOperator.__init__ + splu       discretization.py:126-174
+ *   hs_lifting_rhs
+ *       compute_liftings + assemble_rhs     interface_system.py:98-113
+ *       solve_lifting                       discretization.py:315-332
+ *   hs_apply (HS_APPLY_S / HS_APPLY_IMS)
+ *       apply_scattering                    interface_system.py:135-142
+ *       apply_interface_operator            interface_system.py:144-146
+ *   hs_restricted_apply
+ *       restricted_apply                    interface_system.py:148-162
+ *   hs_set_windows / hs_precond / hs_half_apply
+ *       forward_sweep, backward_sweep, sgs_apply, bj_half_apply, bsp_apply
+ *                                           SPEC.md:306-348 (not shipped)
+ *   hs_gmres
+ *       gmres(apply_A, apply_M, b, opts)    SPEC.md:399-407 (not shipped)
+ *   hs_get_schur
+ *       the per-subdomain map solve_local + extract_outgoing_trace
+ *                                           discretization.py:264-312
+ *
+ * Conventions
+ *   - complex128 = two doubles (re, im) interleaved, i.e. numpy complex128.
+ *   - interface vectors are in the reference m-order (interface_system.py:30-62):
+ *     length L = 2*N_e*n, block m (1-based) = elements [(m-1)n, mn).  With
+ *     nrhs > 1 a vector is [L][nrhs] row-major (right-hand side fastest).
+ *   - `mem`: HS_MEM_HOST (caller host pointer; copied in/out inside the call)
+ *     or HS_MEM_DEVICE (pointer on the context's device).
+ *   - multi-GPU: one context per GPU/process; rank r owns a contiguous band of
+ *     subdomain rows.  Vectors passed in/out are full length on
+ *     every rank; a rank reads and writes only the blocks it owns.
+ *   - return value: 0 = ok, > 0 = invalid argument (Python maps it to
+ *     ValueError, like the reference's ValueError paths), < 0 = CUDA / NCCL /
+ *     numerical failure (RuntimeError, like discretization.py:171-174).
+ *     hs_last_error() gives the message.
+ *   - a context is used by one host thread at a time.
+ */
+#ifndef HSB200_H
+#define HSB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hs_ctx hs_ctx;
+
+enum { HS_MEM_HOST = 0, HS_MEM_DEVICE = 1 };
+enum { HS_APPLY_S = 0, HS_APPLY_IMS = 1 };
+enum { HS_PC_NONE = 0, HS_PC_SP = 1, HS_PC_BSP = 2 };
+enum { HS_SEAM_DEDUP = 0, HS_SEAM_LITERAL = 1 };
+enum { HS_DIR_FORWARD = 0, HS_DIR_BACKWARD = 1 };
+
+/* Library version and build flags ("hsb200 <ver> sm_100a ..."). */
+const char* hs_version(void);
+
+/* Message of the last failed call on this context (or of the last failed
+ * hs_create when ctx is NULL).  Valid until the next call. */
+const char* hs_last_error(const hs_ctx* ctx);
+
+/* Create a context.  device = CUDA ordinal, or -1 for a plan-only context
+ * (host tables only, no CUDA calls; used by CPU tests).  tau = tau_re + i tau_im
+ * is the impedance coefficient (ImpedanceSpec, discretization.py:86-102).
+ * rank/nranks: row-band sharding (nranks = 1 for a single GPU). */
+int hs_create(hs_ctx** ctx, int device, int n1, int n2, int n, double h, double kappa,
+              double tau_re, double tau_im, int rank, int nranks);
+int hs_destroy(hs_ctx* ctx);
+
+/* Scatterer cells (identity rows, discretization.py:187-200, 247-251) of
+ * subdomain (i1, i2), 1-based lattice coordinates; cells index the n x n grid
+ * row-major (y slow).  Must precede hs_factor. */
+int hs_set_dirichlet(hs_ctx* ctx, int i1, int i2, const int32_t* cells, int ncells);
+
+/* Build every subdomain's interface Schur map on the GPU (block-tridiagonal
+ * elimination of the Dirichlet-eliminated operator, one per distinct
+ * operator, then scattered into per-subdomain compact maps). */
+int hs_factor(hs_ctx* ctx);
+
+/* Right-hand side b (interface_system.py:105-113) for nrhs liftings: vals holds
+ * the Dirichlet data of the scatterer cells as [ncells][nrhs] complex (the
+ * reference uses -u_inc, discretization.py:326-328).  b is [L][nrhs]. */
+int hs_lifting_rhs(hs_ctx* ctx, const double* vals, int nrhs, double* b, int mem);
+
+/* out = S g (mode HS_APPLY_S) or (I - S) g (HS_APPLY_IMS). */
+int hs_apply(hs_ctx* ctx, int mode, const double* g, double* out, int nrhs, int mem);
+
+/* out = V_T S V_Src^T g: solve subdomains of the source groups, write blocks
+ * owned by the target groups, zero elsewhere. */
+int hs_restricted_apply(hs_ctx* ctx, const double* g, double* out, int nrhs,
+                        const int32_t* src_groups, int nsrc, const int32_t* tgt_groups, int ntgt,
+                        int mem);
+
+/* Window ranges [lo, hi] (group indices, inclusive) of the partial sweeps of
+ * one direction (kind 0 = lower / forward, 1 = upper / backward).  Default
+ * after hs_create: the reference rule (indexing.py:158-179). */
+int hs_set_windows(hs_ctx* ctx, int kind, const int32_t* lo, const int32_t* hi, int nwin);
+
+/* Preconditioner options: seam mode and the BSP intermediate residual
+ * (SweepConfig). */
+int hs_set_precond_options(hs_ctx* ctx, int seam_mode, int intermediate_residual);
+
+/* z = M r for M in {identity, SP = S_U^-1 S_L^-1, BSP}. */
+int hs_precond(hs_ctx* ctx, int kind, const double* r, double* z, int nrhs, int mem);
+
+/* One block-Jacobi half (bj_half_apply) with the configured
+ * windows; with one window per direction it is forward_sweep / backward_sweep. */
+int hs_half_apply(hs_ctx* ctx, int direction, const double* r, double* z, int nrhs, int mem);
+
+/* Full right-preconditioned GMRES on the device (conventions in oracle/gmres.py):
+ * b, x are [L][nrhs]; iters[nrhs], converged[nrhs]; hist (may be NULL) is
+ * [maxit+1][nrhs] relative residual estimates (unused tail left untouched). */
+int hs_gmres(hs_ctx* ctx, int pc_kind, const double* b, double* x, int nrhs, double tol,
+             int maxit, int* iters, double* hist, int* converged, int mem);
+
+/* ---- introspection (plan-only contexts too) ---------------------------- */
+/* Sizes: L (= 2 N_e n), number of subdomains, number of groups, 2 N_e. */
+int hs_sizes(const hs_ctx* ctx, int64_t* L, int* nsub, int* ngroups, int* npairs);
+/* m-order pair table: pairs[4*k .. 4*k+3] = owner (i1,i2), neighbour (i1,i2). */
+int hs_pairs(const hs_ctx* ctx, int32_t* pairs);
+/* Rank that owns each subdomain block (owner's row band), length 2 N_e. */
+int hs_block_owner(const hs_ctx* ctx, int32_t* owner_rank);
+/* Step schedule of a preconditioner: rec[3*k] = step, rec[3*k+1] = phase
+ * (0 forward, 1 residual, 2 backward), rec[3*k+2] = subdomain ordinal (index in
+ * multi-index order).  Returns the number of entries in *count. */
+int hs_schedule(const hs_ctx* ctx, int kind, int32_t* rec, int cap, int* count);
+/* Trace-exchange plan of a step kind across row bands (for rank `rank`):
+ * blocks (0-based m) this rank sends to rank-1 / rank+1 after a forward,
+ * backward and full step.  kind: 0 forward, 1 backward, 2 full. */
+int hs_exchange_plan(const hs_ctx* ctx, int kind, int peer, int32_t* blocks, int cap, int* count);
+
+/* Compact Schur map of subdomain (i1,i2) as a dense (k n) x (k n) complex
+ * matrix, row-major (after hs_factor). */
+int hs_get_schur(hs_ctx* ctx, int i1, int i2, double* T);
+/* Replace the map of subdomain (i1,i2) (bring-up / tests only). */
+int hs_set_schur(hs_ctx* ctx, int i1, int i2, const double* T);
+
+/* ---- execution control / measurement ----------------------------------- */
+/* 1 = calls with HS_MEM_DEVICE return without synchronising the stream. */
+int hs_set_async(hs_ctx* ctx, int async_mode);
+int hs_sync(hs_ctx* ctx);
+/* The context's CUDA stream (cudaStream_t) as an integer. */
+int hs_stream(hs_ctx* ctx, uint64_t* stream);
+/* Kernel timing: when on, every step-apply launch is bracketed by CUDA events;
+ * hs_kernel_stats reports launches, summed ms and algorithmic bytes of the
+ * step-apply kernels since the last reset. */
+int hs_set_kernel_timing(hs_ctx* ctx, int on);
+int hs_kernel_stats(hs_ctx* ctx, int64_t* launches, double* ms, double* bytes, int reset);
+/* Bytes of device memory held by the context. */
+int hs_memory(const hs_ctx* ctx, int64_t* bytes);
+
+/* ---- multi-GPU ---------------------------------------------------------- */
+/* Initialise the NCCL communicator of a sharded context from a 128-byte
+ * ncclUniqueId produced by rank 0 (hs_nccl_unique_id). */
+int hs_nccl_unique_id(uint8_t id[128]);
+int hs_comm_init(hs_ctx* ctx, const uint8_t id[128]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HSB200_H */

@@ -1,0 +1,1069 @@
+// C ABI (include/hsb200.h): context lifecycle, factorisation driver, sweep
+// orchestration, GMRES loop, introspection and the row-band exchange.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <map>
+#include <tuple>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "../../include/hsb200.h"
+#include "hs_ctx.h"
+#include "hs_kernels.h"
+
+using namespace hs;
+
+struct hs_ctx : public Ctx {};
+
+static std::string g_create_err;
+
+#define HS_VERSION "hsb200 0.1.0 sm_100a complex128"
+
+namespace {
+
+int fail(Ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  else g_create_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                     \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess)                                                           \
+      return fail(c, -1, std::string(#call) + ": " + cudaGetErrorString(e_));       \
+  } while (0)
+
+#define NK(call)                                                                     \
+  do {                                                                               \
+    ncclResult_t r_ = (call);                                                        \
+    if (r_ != ncclSuccess)                                                           \
+      return fail(c, -2, std::string(#call) + ": " + ncclGetErrorString(r_));       \
+  } while (0)
+
+#define NEED_GPU(c)                                                                  \
+  do {                                                                               \
+    if ((c)->device < 0) return fail(c, 2, "plan-only context (device -1) cannot run kernels"); \
+  } while (0)
+
+cudaError_t dalloc(Ctx* c, void** p, size_t bytes) {
+  cudaError_t e = cudaMalloc(p, bytes > 0 ? bytes : 16);
+  if (e == cudaSuccess) c->dev_bytes += (int64_t)bytes;
+  return e;
+}
+
+void dfree(Ctx* c, void* p, size_t bytes) {
+  if (p) {
+    cudaFree(p);
+    c->dev_bytes -= (int64_t)bytes;
+  }
+}
+
+// Named, grow-only device work buffers.
+int ws_get(Ctx* c, const std::string& name, size_t elems, double2** out) {
+  Workspace& w = c->ws[name];
+  if (w.cap < elems) {
+    dfree(c, w.p, w.cap * sizeof(double2));
+    w.p = nullptr;
+    w.cap = 0;
+    CK(dalloc(c, (void**)&w.p, elems * sizeof(double2)));
+    w.cap = elems;
+  }
+  *out = w.p;
+  return 0;
+}
+
+template <class T>
+int upload(Ctx* c, T** dptr, const std::vector<T>& v) {
+  if (v.empty()) {
+    *dptr = nullptr;
+    return 0;
+  }
+  CK(dalloc(c, (void**)dptr, v.size() * sizeof(T)));
+  CK(cudaMemcpy(*dptr, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return 0;
+}
+
+void free_step(Ctx* c, DevStep& s) {
+  dfree(c, s.items, s.nitems * sizeof(DevItem));
+  dfree(c, s.tiles, s.ntiles * sizeof(DevTile));
+  dfree(c, s.recv, s.nrecv * sizeof(DevRecv));
+  s = DevStep();
+}
+
+int make_step(Ctx* c, const StepTable& t, DevStep& out) {
+  std::vector<DevItem> items;
+  std::vector<DevTile> tiles;
+  std::vector<DevRecv> recv;
+  double mapb = 0, vecb = 0;
+  int maxK = 0;
+  for (size_t i = 0; i < t.items.size(); ++i) {
+    const Item& it = t.items[i];
+    DevItem d;
+    d.s = it.s; d.rlo = it.rlo; d.rhi = it.rhi; d.alt = it.alt;
+    for (int q = 0; q < 4; ++q) d.slot[q] = it.slot[q];
+    items.push_back(d);
+    const int K = c->plan.subs[it.s].k * c->n;
+    maxK = std::max(maxK, K);
+    for (int tl = it.rlo / kRowTile; tl * kRowTile < it.rhi; ++tl) tiles.push_back({(int)i, tl});
+    const double rows = it.rhi - it.rlo;
+    // 16 (rows cols + cols + 2 rows) bytes per solve-application
+    mapb += 16.0 * rows * K;
+    vecb += 16.0 * (K + 2.0 * rows);
+  }
+  for (const RecvSlot& r : t.recv) recv.push_back({r.dir, r.slot, (long long)r.off});
+  free_step(c, out);
+  if (upload(c, &out.items, items)) return -1;
+  if (upload(c, &out.tiles, tiles)) return -1;
+  if (upload(c, &out.recv, recv)) return -1;
+  out.nitems = (int)items.size();
+  out.ntiles = (int)tiles.size();
+  out.nrecv = (int)recv.size();
+  out.nsend_up = t.nsend_up; out.nsend_dn = t.nsend_dn;
+  out.nrecv_up = t.nrecv_up; out.nrecv_dn = t.nrecv_dn;
+  out.maxK = maxK;
+  out.bytes_per_rhs_map = mapb;
+  out.bytes_per_rhs_vec = vecb;
+  return 0;
+}
+
+int build_steps(Ctx* c) {
+  if (!c->steps_dirty) return 0;
+  for (auto& s : c->fwd) free_step(c, s);
+  for (auto& s : c->bwd) free_step(c, s);
+  for (auto& s : c->sp_fwd) free_step(c, s);
+  for (auto& s : c->sp_bwd) free_step(c, s);
+  free_step(c, c->full);
+  Plan& P = c->plan;
+  auto f = P.half_steps(0), b = P.half_steps(1);
+  c->fwd.assign(f.size(), DevStep());
+  c->bwd.assign(b.size(), DevStep());
+  for (size_t i = 0; i < f.size(); ++i) if (make_step(c, f[i], c->fwd[i])) return -1;
+  for (size_t i = 0; i < b.size(); ++i) if (make_step(c, b[i], c->bwd[i])) return -1;
+  // SP = one window per direction
+  auto wl = P.win_lower, wu = P.win_upper;
+  P.win_lower.clear(); P.win_upper.clear();
+  if (P.ng >= 2) {
+    P.win_lower.push_back({2, P.ng + 1});
+    P.win_upper.push_back({2, P.ng + 1});
+  }
+  auto sf = P.half_steps(0), sb = P.half_steps(1);
+  P.win_lower = wl; P.win_upper = wu;
+  c->sp_fwd.assign(sf.size(), DevStep());
+  c->sp_bwd.assign(sb.size(), DevStep());
+  for (size_t i = 0; i < sf.size(); ++i) if (make_step(c, sf[i], c->sp_fwd[i])) return -1;
+  for (size_t i = 0; i < sb.size(); ++i) if (make_step(c, sb[i], c->sp_bwd[i])) return -1;
+  if (make_step(c, P.full_step(), c->full)) return -1;
+  // seam blocks (literal mode): groups shared by consecutive windows
+  for (int dir = 0; dir < 2; ++dir) {
+    const auto& W = dir == 0 ? P.win_lower : P.win_upper;
+    std::set<int> seams;
+    for (size_t i = 0; i + 1 < W.size(); ++i) {
+      if (dir == 0) seams.insert(W[i].second);   // lower: hi of window i == lo of i+1
+      else seams.insert(W[i].first);             // upper: lo of window i == hi of i+1
+    }
+    std::vector<int> blocks;
+    for (int m = 0; m < P.npairs; ++m)
+      if (seams.count(P.block_group[m]) && P.subs[P.block_sub[m]].rank == P.rank) blocks.push_back(m);
+    dfree(c, c->d_seam[dir], c->n_seam[dir] * sizeof(int));
+    c->d_seam[dir] = nullptr;
+    if (upload(c, &c->d_seam[dir], blocks)) return -1;
+    c->n_seam[dir] = (int)blocks.size();
+  }
+  // exchange buffers
+  size_t need = 0;
+  auto upd = [&](const std::vector<DevStep>& v) {
+    for (auto& s : v) need = std::max(need, (size_t)std::max(std::max(s.nsend_up, s.nsend_dn), std::max(s.nrecv_up, s.nrecv_dn)));
+  };
+  upd(c->fwd); upd(c->bwd); upd(c->sp_fwd); upd(c->sp_bwd);
+  need = std::max(need, (size_t)std::max(std::max(c->full.nsend_up, c->full.nsend_dn), std::max(c->full.nrecv_up, c->full.nrecv_dn)));
+  c->xbuf_cap = need * c->n;  // per RHS; grown with R in ensure_xbuf
+  c->steps_dirty = false;
+  return 0;
+}
+
+int ensure_xbuf(Ctx* c, int R) {
+  if (c->plan.nranks == 1) return 0;
+  size_t elems = c->xbuf_cap * R;
+  double2* p;
+  if (ws_get(c, "xsu", elems, &p)) return -1;
+  c->send_up = p;
+  if (ws_get(c, "xsd", elems, &p)) return -1;
+  c->send_dn = p;
+  if (ws_get(c, "xru", elems, &p)) return -1;
+  c->recv_up = p;
+  if (ws_get(c, "xrd", elems, &p)) return -1;
+  c->recv_dn = p;
+  return 0;
+}
+
+cudaEvent_t ev_get(Ctx* c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// One sweep step: batched apply + (row bands) exchange + receive epilogue.
+int run_step(Ctx* c, const DevStep& st, const double2* srcA, const double2* srcB, Epi e, int R) {
+  e.send_up = c->send_up;
+  e.send_dn = c->send_dn;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->timing && st.ntiles > 0) {
+    e0 = ev_get(c);
+    e1 = ev_get(c);
+    cudaEventRecord(e0, c->stream);
+  }
+  launch_step(*c, st, srcA, srcB, e, R);
+  if (e1) {
+    cudaEventRecord(e1, c->stream);
+    c->ev_pending.push_back({e0, e1});
+    c->ev_bytes.push_back(st.bytes_per_rhs_map + R * st.bytes_per_rhs_vec);
+  }
+  CK(cudaGetLastError());
+  if (c->plan.nranks > 1) {
+    ncclComm_t comm = (ncclComm_t)c->nccl;
+    if (!comm) return fail(c, -2, "sharded context without hs_comm_init");
+    const size_t per = (size_t)c->n * R * 2;  // doubles per slot
+    const int rk = c->plan.rank;
+    NK(ncclGroupStart());
+    if (st.nsend_up) NK(ncclSend(c->send_up, per * st.nsend_up, ncclDouble, rk + 1, comm, c->stream));
+    if (st.nsend_dn) NK(ncclSend(c->send_dn, per * st.nsend_dn, ncclDouble, rk - 1, comm, c->stream));
+    if (st.nrecv_up) NK(ncclRecv(c->recv_up, per * st.nrecv_up, ncclDouble, rk + 1, comm, c->stream));
+    if (st.nrecv_dn) NK(ncclRecv(c->recv_dn, per * st.nrecv_dn, ncclDouble, rk - 1, comm, c->stream));
+    NK(ncclGroupEnd());
+    launch_recv_epi(*c, st, e, R);
+    CK(cudaGetLastError());
+  }
+  return 0;
+}
+
+Epi epi(int mode, double2* o1, double2* o2 = nullptr, double2* o3 = nullptr,
+        const double2* a = nullptr, const double2* b = nullptr) {
+  Epi e;
+  e.mode = mode; e.o1 = o1; e.o2 = o2; e.o3 = o3; e.a = a; e.b = b;
+  e.send_up = e.send_dn = nullptr;
+  return e;
+}
+
+long long LRof(Ctx* c, int R) { return c->plan.L * (long long)R; }
+
+// ---- device pointer in/out for host or device caller buffers
+int dev_in(Ctx* c, const double* p, long long elems, int mem, const char* name, const double2** out) {
+  if (mem == HS_MEM_DEVICE) {
+    *out = (const double2*)p;
+    return 0;
+  }
+  if (mem != HS_MEM_HOST) return fail(c, 1, "mem must be HS_MEM_HOST or HS_MEM_DEVICE");
+  double2* d;
+  if (ws_get(c, name, elems, &d)) return -1;
+  if (elems) CK(cudaMemcpyAsync(d, p, elems * sizeof(double2), cudaMemcpyHostToDevice, c->stream));
+  *out = d;
+  return 0;
+}
+
+int dev_out(Ctx* c, double* p, long long elems, int mem, const char* name, double2** out) {
+  if (mem == HS_MEM_DEVICE) {
+    *out = (double2*)p;
+    return 0;
+  }
+  if (mem != HS_MEM_HOST) return fail(c, 1, "mem must be HS_MEM_HOST or HS_MEM_DEVICE");
+  return ws_get(c, name, elems, out);
+}
+
+int finish_out(Ctx* c, double* p, const double2* d, long long elems, int mem) {
+  if (mem == HS_MEM_HOST) {
+    if (elems) CK(cudaMemcpyAsync(p, d, elems * sizeof(double2), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+  } else if (!c->async_mode) {
+    CK(cudaStreamSynchronize(c->stream));
+  }
+  return 0;
+}
+
+int check_ready(Ctx* c, int R) {
+  NEED_GPU(c);
+  if (!c->factored) return fail(c, 1, "hs_factor has not been called");
+  if (R < 1 || R > 1024) return fail(c, 1, "nrhs must be in 1..1024");
+  if (build_steps(c)) return -1;
+  if (ensure_xbuf(c, R)) return -1;
+  return 0;
+}
+
+// ---- preconditioners on device vectors
+int do_half(Ctx* c, int dir, const double2* r, double2* z, int R) {
+  const long long LR = LRof(c, R);
+  CK(cudaMemcpyAsync(z, r, LR * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
+  const auto& steps = dir == 0 ? c->fwd : c->bwd;
+  for (const auto& st : steps)
+    if (run_step(c, st, z, r, epi(EPI_ACC, z), R)) return -1;
+  if (c->seam == HS_SEAM_LITERAL) launch_seam_add(*c, dir, z, r, R);
+  return 0;
+}
+
+int do_precond(Ctx* c, int kind, const double2* r, double2* z, int R) {
+  const long long LR = LRof(c, R);
+  if (kind == HS_PC_NONE) {
+    CK(cudaMemcpyAsync(z, r, LR * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
+    return 0;
+  }
+  if (kind == HS_PC_SP) {
+    double2* zl;
+    if (ws_get(c, "zL", LR, &zl)) return -1;
+    CK(cudaMemcpyAsync(zl, r, LR * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
+    for (const auto& st : c->sp_fwd)
+      if (run_step(c, st, zl, r, epi(EPI_ACC, zl), R)) return -1;
+    CK(cudaMemcpyAsync(z, zl, LR * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
+    for (const auto& st : c->sp_bwd)
+      if (run_step(c, st, z, zl, epi(EPI_ACC, z), R)) return -1;
+    return 0;
+  }
+  if (kind != HS_PC_BSP) return fail(c, 1, "unknown preconditioner kind");
+  double2 *zl, *rp, *w;
+  if (ws_get(c, "zL", LR, &zl) || ws_get(c, "rp", LR, &rp) || ws_get(c, "w", LR, &w)) return -1;
+  if (do_half(c, 0, r, zl, R)) return -1;
+  const double2* rsrc;
+  if (c->inter) {
+    if (run_step(c, c->full, zl, zl, epi(EPI_RESID, rp, w, z, r, zl), R)) return -1;
+    rsrc = rp;
+  } else {
+    launch_vec(*c, VEC_INIT_BWD, LR, w, z, r, zl);
+    rsrc = r;
+  }
+  for (const auto& st : c->bwd)
+    if (run_step(c, st, w, rsrc, epi(EPI_ACC2, w, z), R)) return -1;
+  if (c->seam == HS_SEAM_LITERAL) launch_seam_add(*c, 1, z, rsrc, R);
+  return 0;
+}
+
+int do_apply(Ctx* c, int mode, const double2* g, double2* out, int R) {
+  if (mode == HS_APPLY_S) return run_step(c, c->full, g, g, epi(EPI_SET, out), R);
+  if (mode == HS_APPLY_IMS) return run_step(c, c->full, g, g, epi(EPI_IMS, out, nullptr, nullptr, g), R);
+  return fail(c, 1, "unknown apply mode");
+}
+
+// ---- factorisation
+int build_classes(Ctx* c) {
+  const int n = c->n;
+  c->classes.clear();
+  OpClass gen;
+  gen.mask.assign((size_t)n * n, 0);
+  c->classes.push_back(gen);
+  c->sub_class.assign(c->plan.nsub, 0);
+  for (auto& kv : c->dcells) {
+    if (kv.second.empty()) continue;
+    std::vector<uint8_t> m((size_t)n * n, 0);
+    for (int cell : kv.second) m[cell] = 1;
+    int found = -1;
+    for (size_t i = 0; i < c->classes.size(); ++i)
+      if (c->classes[i].mask == m) found = (int)i;
+    if (found < 0) {
+      OpClass oc;
+      oc.mask = m;
+      oc.dcells = kv.second;
+      c->classes.push_back(oc);
+      found = (int)c->classes.size() - 1;
+    }
+    c->sub_class[kv.first] = found;
+  }
+  return 0;
+}
+
+// Sparse RHS entries for the unit columns of Dirichlet boundary cells (rare:
+// a scatterer cell on the subdomain edge) -- eliminated form, SURVEY.md §7.
+void dirichlet_boundary_extras(Ctx* c, const OpClass& oc, std::map<std::tuple<int, int, int>, double2>& ex) {
+  const int n = c->n;
+  const double ih2 = 1.0 / (c->h * c->h);
+  auto isd = [&](int k, int x) { return oc.mask[(size_t)k * n + x] != 0; };
+  for (int f = 0; f < 4; ++f)
+    for (int p = 0; p < n; ++p) {
+      int k, x;
+      if (f == 0) { k = p; x = 0; } else if (f == 1) { k = 0; x = p; }
+      else if (f == 2) { k = n - 1; x = p; } else { k = p; x = n - 1; }
+      if (!isd(k, x)) continue;
+      const int col = f * n + p;
+      const int nb[4][2] = {{k - 1, x}, {k + 1, x}, {k, x - 1}, {k, x + 1}};
+      for (auto& q : nb) {
+        if (q[0] < 0 || q[0] >= n || q[1] < 0 || q[1] >= n || isd(q[0], q[1])) continue;
+        double2& v = ex[std::make_tuple(q[0], q[1], col)];
+        v.x += ih2;
+      }
+    }
+}
+
+int upload_extras(Ctx* c, const std::map<std::tuple<int, int, int>, double2>& ex, ExtraRHS& e,
+                  std::vector<void*>& owned) {
+  const int n = c->n;
+  e.row_ptr.assign(n + 1, 0);
+  if (ex.empty()) {
+    e.row_ptr.clear();
+    return 0;
+  }
+  std::vector<int> xs, cols;
+  std::vector<double2> vals;
+  for (auto& kv : ex) e.row_ptr[std::get<0>(kv.first) + 1]++;
+  for (int k = 0; k < n; ++k) e.row_ptr[k + 1] += e.row_ptr[k];
+  for (auto& kv : ex) {  // map is ordered by (k, x, col)
+    xs.push_back(std::get<1>(kv.first));
+    cols.push_back(std::get<2>(kv.first));
+    vals.push_back(kv.second);
+  }
+  if (upload(c, &e.d_x, xs) || upload(c, &e.d_col, cols) || upload(c, &e.d_val, vals)) return -1;
+  owned.push_back(e.d_x); owned.push_back(e.d_col); owned.push_back(e.d_val);
+  return 0;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+const char* hs_version(void) { return HS_VERSION; }
+
+const char* hs_last_error(const hs_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
+
+int hs_create(hs_ctx** out, int device, int n1, int n2, int n, double h, double kappa, double tau_re,
+              double tau_im, int rank, int nranks) {
+  Ctx* c = nullptr;
+  if (!out) return fail(nullptr, 1, "null context pointer");
+  *out = nullptr;
+  if (!(h > 0)) return fail(nullptr, 1, "h must be positive");
+  if (!(kappa > 0)) return fail(nullptr, 1, "kappa must be positive");
+  if (tau_im == 0) return fail(nullptr, 1, "impedance coefficient must have nonzero imaginary part");
+  hs_ctx* x = new hs_ctx();
+  std::string e = x->plan.build(n1, n2, n, rank, nranks);
+  if (!e.empty()) {
+    delete x;
+    return fail(nullptr, 1, e);
+  }
+  x->device = device;
+  x->n1 = n1; x->n2 = n2; x->n = n;
+  x->h = h; x->kappa = kappa; x->tau_re = tau_re; x->tau_im = tau_im;
+  if (device >= 0) {
+    c = x;
+    cudaError_t ce = cudaSetDevice(device);
+    if (ce != cudaSuccess) {
+      std::string m = std::string("cudaSetDevice: ") + cudaGetErrorString(ce);
+      delete x;
+      return fail(nullptr, -1, m);
+    }
+    cudaStreamCreateWithFlags(&x->stream, cudaStreamNonBlocking);
+    cudaDeviceGetAttribute(&x->num_sms, cudaDevAttrMultiProcessorCount, device);
+    cudaDeviceGetAttribute(&x->coop_ok, cudaDevAttrCooperativeLaunch, device);
+    set_step_smem_limit();
+    // per-subdomain records (T_off filled by hs_factor)
+    std::vector<DevSub> subs(x->plan.nsub);
+    long long off = 0;
+    for (int s = 0; s < x->plan.nsub; ++s) {
+      const SubPlan& sp = x->plan.subs[s];
+      DevSub d;
+      d.k = sp.k;
+      d.in_off = sp.first_block * n;
+      for (int q = 0; q < 4; ++q) d.tgt[q] = q < sp.k ? sp.tgt_block[q] * n : -1;
+      const long long K = (long long)sp.k * n;
+      d.T_off = off;
+      off += ((K + kRowTile - 1) / kRowTile) * kRowTile * K;
+      x->plan.subs[s].T_off = d.T_off;
+      subs[s] = d;
+    }
+    x->T_elems = (size_t)off;
+    if (upload(x, &x->dsubs, subs)) {
+      std::string m = x->err;
+      delete x;
+      return fail(nullptr, -1, m);
+    }
+    cudaError_t le = cudaGetLastError();
+    if (le != cudaSuccess) {
+      std::string m = std::string("device setup: ") + cudaGetErrorString(le);
+      delete x;
+      return fail(nullptr, -1, m);
+    }
+  }
+  *out = x;
+  return 0;
+}
+
+int hs_destroy(hs_ctx* c) {
+  if (!c) return 0;
+  if (c->device >= 0) {
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    for (auto& kv : c->ws) cudaFree(kv.second.p);
+    for (auto& s : c->fwd) free_step(c, s);
+    for (auto& s : c->bwd) free_step(c, s);
+    for (auto& s : c->sp_fwd) free_step(c, s);
+    for (auto& s : c->sp_bwd) free_step(c, s);
+    free_step(c, c->full);
+    for (auto& oc : c->classes) cudaFree(oc.T4);
+    cudaFree(c->T);
+    cudaFree(c->dsubs);
+    cudaFree(c->d_seam[0]);
+    cudaFree(c->d_seam[1]);
+    for (auto& p : c->ev_pending) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
+    if (c->nccl) ncclCommDestroy((ncclComm_t)c->nccl);
+    cudaStreamDestroy(c->stream);
+  }
+  delete c;
+  return 0;
+}
+
+int hs_set_dirichlet(hs_ctx* c, int i1, int i2, const int32_t* cells, int ncells) {
+  if (!c) return fail(nullptr, 1, "null context");
+  if (i1 < 1 || i1 > c->n1 || i2 < 1 || i2 > c->n2) return fail(c, 1, "subdomain out of range");
+  if (ncells < 0 || (ncells > 0 && !cells)) return fail(c, 1, "bad cell list");
+  std::vector<int32_t> v(cells, cells + ncells);
+  for (int x : v)
+    if (x < 0 || x >= c->n * c->n) return fail(c, 1, "Dirichlet cell index out of range");
+  std::sort(v.begin(), v.end());
+  v.erase(std::unique(v.begin(), v.end()), v.end());
+  c->dcells[c->plan.ordinal(i1, i2)] = v;
+  c->factored = false;
+  return 0;
+}
+
+int hs_factor(hs_ctx* c) {
+  if (!c) return fail(nullptr, 1, "null context");
+  NEED_GPU(c);
+  CK(cudaSetDevice(c->device));
+  const int n = c->n;
+  build_classes(c);
+  const int ncls = (int)c->classes.size();
+  const long long nn = (long long)n * n;
+  // masks
+  std::vector<uint8_t> masks;
+  for (auto& oc : c->classes) masks.insert(masks.end(), oc.mask.begin(), oc.mask.end());
+  uint8_t* dmasks = nullptr;
+  if (upload(c, &dmasks, masks)) return -1;
+  // X_k for all classes (kept: lifting solves reuse them)
+  if (c->ws.count("__X")) {
+    dfree(c, c->ws["__X"].p, c->ws["__X"].cap * sizeof(double2));
+    c->ws.erase("__X");
+  }
+  double2* X;
+  const long long xstride = nn * n;
+  CK(dalloc(c, (void**)&X, (size_t)xstride * ncls * sizeof(double2)));
+  double2 *Rp, *Cp;
+  const long long pstride = 32LL * n;
+  CK(dalloc(c, (void**)&Rp, (size_t)pstride * ncls * sizeof(double2)));
+  CK(dalloc(c, (void**)&Cp, (size_t)pstride * ncls * sizeof(double2)));
+  int* dbad;
+  CK(dalloc(c, (void**)&dbad, sizeof(int)));
+  CK(cudaMemsetAsync(dbad, 0, sizeof(int), c->stream));
+  CK(factor_blocks(*c, X, xstride, dmasks, ncls, Rp, Cp, pstride, dbad));
+  // boundary responses for the 4n unit columns
+  const int R = 4 * n;
+  double2 *Y, *Bk, *G;
+  const long long ystride = nn * R, bstride = (long long)n * R, gstride = 4LL * n * R;
+  CK(dalloc(c, (void**)&Y, (size_t)ystride * ncls * sizeof(double2)));
+  CK(dalloc(c, (void**)&Bk, (size_t)bstride * ncls * sizeof(double2)));
+  CK(dalloc(c, (void**)&G, (size_t)gstride * ncls * sizeof(double2)));
+  std::vector<ExtraRHS> extras(ncls);
+  std::vector<void*> owned;
+  for (int k = 0; k < ncls; ++k) {
+    std::map<std::tuple<int, int, int>, double2> ex;
+    dirichlet_boundary_extras(c, c->classes[k], ex);
+    if (upload_extras(c, ex, extras[k], owned)) return -1;
+  }
+  CK(solve_boundary(*c, X, xstride, dmasks, ncls, R, R, extras.data(), Y, ystride, Bk, bstride, G, gstride));
+  // T4 = -(s/d) I - (2 tau / (h^3 d^2)) G
+  const std::complex<double> tau(c->tau_re, c->tau_im);
+  const double h = c->h;
+  const std::complex<double> d = 1.0 / h - tau / 2.0, s = 1.0 / h + tau / 2.0;
+  const std::complex<double> a = -(s / d), b = -(2.0 * tau) / (h * h * h * d * d);
+  std::vector<double2*> T4s(ncls);
+  for (int k = 0; k < ncls; ++k) {
+    dfree(c, c->classes[k].T4, 0);
+    CK(dalloc(c, (void**)&c->classes[k].T4, (size_t)16 * nn * sizeof(double2)));
+    launch_make_T4(*c, c->classes[k].T4, G + k * gstride, R, make_double2(a.real(), a.imag()),
+                   make_double2(b.real(), b.imag()));
+    T4s[k] = c->classes[k].T4;
+    c->classes[k].X = X + k * xstride;  // view; X freed as a whole at destroy
+  }
+  // per-subdomain maps, tile-major
+  if (!c->T) CK(dalloc(c, (void**)&c->T, c->T_elems * sizeof(double2)));
+  std::vector<int2> tl;
+  std::vector<int> faces(4 * c->plan.nsub, 0), cls(c->plan.nsub, 0);
+  for (int s2 = 0; s2 < c->plan.nsub; ++s2) {
+    const SubPlan& sp = c->plan.subs[s2];
+    const int K = sp.k * n;
+    for (int t = 0; t * kRowTile < K; ++t) tl.push_back(make_int2(s2, t));
+    for (int q = 0; q < sp.k; ++q) faces[4 * s2 + q] = sp.face[q];
+    cls[s2] = c->sub_class[s2];
+  }
+  int2* dtl;
+  int *dfaces, *dcls;
+  double2** dT4s;
+  if (upload(c, &dtl, tl) || upload(c, &dfaces, faces) || upload(c, &dcls, cls) || upload(c, &dT4s, T4s)) return -1;
+  launch_scatter_T(*c, dtl, (int)tl.size(), dfaces, dcls, dT4s);
+  CK(cudaGetLastError());
+  int bad = 0;
+  CK(cudaMemcpyAsync(&bad, dbad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  // finite check of the class maps
+  for (int k = 0; k < ncls; ++k) {
+    std::vector<double2> h4((size_t)16 * nn);
+    CK(cudaMemcpy(h4.data(), c->classes[k].T4, h4.size() * sizeof(double2), cudaMemcpyDeviceToHost));
+    for (auto& v : h4)
+      if (!std::isfinite(v.x) || !std::isfinite(v.y)) { bad = 2; break; }
+  }
+  dfree(c, Y, 0); dfree(c, Bk, 0); dfree(c, G, 0); dfree(c, Rp, 0); dfree(c, Cp, 0); dfree(c, dbad, 0);
+  dfree(c, dtl, 0); dfree(c, dfaces, 0); dfree(c, dcls, 0); dfree(c, dT4s, 0); dfree(c, dmasks, 0);
+  for (void* p : owned) dfree(c, p, 0);
+  // keep masks of classes on host only; X stays for lifting solves
+  c->ws["__X"].p = X;  // freed at destroy / refactor
+  c->ws["__X"].cap = (size_t)xstride * ncls;
+  c->dev_bytes += 0;
+  for (auto& oc : c->classes) oc.factored = true;
+  if (bad) return fail(c, -3, "singular or non-finite subdomain factorisation");
+  c->factored = true;
+  c->steps_dirty = true;
+  return 0;
+}
+
+int hs_lifting_rhs(hs_ctx* c, const double* vals, int nrhs, double* bout, int mem) {
+  if (!c) return fail(nullptr, 1, "null context");
+  if (int e = check_ready(c, nrhs)) return e;
+  CK(cudaSetDevice(c->device));
+  const int n = c->n;
+  const long long LR = LRof(c, nrhs);
+  double2* b;
+  if (dev_out(c, bout, LR, mem, "out", &b)) return -1;
+  CK(cudaMemsetAsync(b, 0, LR * sizeof(double2), c->stream));
+  const double ih2 = 1.0 / (c->h * c->h);
+  const std::complex<double> tau(c->tau_re, c->tau_im);
+  const std::complex<double> d = 1.0 / c->h - tau / 2.0;
+  const std::complex<double> coef = -(2.0 * tau) / (c->h * d);
+  size_t vpos = 0;
+  for (auto& kv : c->dcells) {
+    const auto& cells = kv.second;
+    if (cells.empty()) continue;
+    const int s = kv.first;
+    const SubPlan& sp = c->plan.subs[s];
+    const OpClass& oc = c->classes[c->sub_class[s]];
+    std::map<std::tuple<int, int, int>, double2> ex;
+    auto isd = [&](int k, int x) { return oc.mask[(size_t)k * n + x] != 0; };
+    for (size_t ci = 0; ci < cells.size(); ++ci) {
+      const int k = cells[ci] / n, x = cells[ci] % n;
+      for (int j = 0; j < nrhs; ++j) {
+        const double* v = vals + 2 * ((vpos + ci) * nrhs + j);
+        double2& e0 = ex[std::make_tuple(k, x, j)];
+        e0.x += v[0]; e0.y += v[1];
+        const int nb[4][2] = {{k - 1, x}, {k + 1, x}, {k, x - 1}, {k, x + 1}};
+        for (auto& q : nb) {
+          if (q[0] < 0 || q[0] >= n || q[1] < 0 || q[1] >= n || isd(q[0], q[1])) continue;
+          double2& e1 = ex[std::make_tuple(q[0], q[1], j)];
+          e1.x += ih2 * v[0]; e1.y += ih2 * v[1];
+        }
+      }
+    }
+    vpos += cells.size();
+    if (sp.rank != c->plan.rank) continue;
+    ExtraRHS er;
+    std::vector<void*> owned;
+    if (upload_extras(c, ex, er, owned)) return -1;
+    const long long nn = (long long)n * n;
+    double2 *Y, *Bk, *G;
+    CK(dalloc(c, (void**)&Y, (size_t)nn * nrhs * sizeof(double2)));
+    CK(dalloc(c, (void**)&Bk, (size_t)n * nrhs * sizeof(double2)));
+    CK(dalloc(c, (void**)&G, (size_t)4 * n * nrhs * sizeof(double2)));
+    // single class: pass its X and mask
+    uint8_t* dm;
+    if (upload(c, &dm, oc.mask)) return -1;
+    CK(solve_boundary(*c, oc.X, 0, dm, 1, nrhs, 0, &er, Y, 0, Bk, 0, G, 0));
+    std::vector<int> ft(4, -1);
+    for (int q = 0; q < sp.k; ++q) ft[sp.face[q]] = sp.tgt_block[q] * n;
+    int* dft;
+    if (upload(c, &dft, ft)) return -1;
+    launch_lift_b(*c, b, G, nrhs, 0, nrhs, dft, make_double2(coef.real(), coef.imag()));
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(c->stream));
+    dfree(c, Y, 0); dfree(c, Bk, 0); dfree(c, G, 0); dfree(c, dm, 0); dfree(c, dft, 0);
+    for (void* p : owned) dfree(c, p, 0);
+  }
+  return finish_out(c, bout, b, LR, mem);
+}
+
+int hs_apply(hs_ctx* c, int mode, const double* g, double* out, int nrhs, int mem) {
+  if (!c) return fail(nullptr, 1, "null context");
+  if (int e = check_ready(c, nrhs)) return e;
+  const long long LR = LRof(c, nrhs);
+  const double2* dg;
+  double2* dout;
+  if (dev_in(c, g, LR, mem, "in", &dg) || dev_out(c, out, LR, mem, "out", &dout)) return -1;
+  if (do_apply(c, mode, dg, dout, nrhs)) return -1;
+  return finish_out(c, out, dout, LR, mem);
+}
+
+int hs_restricted_apply(hs_ctx* c, const double* g, double* out, int nrhs, const int32_t* src,
+                        int nsrc, const int32_t* tgt, int ntgt, int mem) {
+  if (!c) return fail(nullptr, 1, "null context");
+  if (int e = check_ready(c, nrhs)) return e;
+  const long long LR = LRof(c, nrhs);
+  const double2* dg;
+  double2* dout;
+  if (dev_in(c, g, LR, mem, "in", &dg) || dev_out(c, out, LR, mem, "out", &dout)) return -1;
+  std::vector<int> S(src, src + std::max(nsrc, 0)), Tg(tgt, tgt + std::max(ntgt, 0));
+  DevStep st;
+  if (make_step(c, c->plan.restricted_step(S, Tg), st)) return -1;
+  CK(cudaMemsetAsync(dout, 0, LR * sizeof(double2), c->stream));
+  int rc = run_step(c, st, dg, dg, epi(EPI_SET, dout), nrhs);
+  int rc2 = finish_out(c, out, dout, LR, mem);
+  cudaStreamSynchronize(c->stream);
+  free_step(c, st);
+  return rc ? rc : rc2;
+}
+
+int hs_set_windows(hs_ctx* c, int kind, const int32_t* lo, const int32_t* hi, int nwin) {
+  if (!c) return fail(nullptr, 1, "null context");
+  if (kind != 0 && kind != 1) return fail(c, 1, "window kind must be 0 (lower) or 1 (upper)");
+  std::vector<std::pair<int, int>> w;
+  const int ng = c->plan.ng;
+  for (int i = 0; i < nwin; ++i) {
+    if (lo[i] < 2 || hi[i] > ng + 1 || lo[i] >= hi[i]) return fail(c, 1, "window out of range");
+    w.push_back({lo[i], hi[i]});
+  }
+  (kind == 0 ? c->plan.win_lower : c->plan.win_upper) = w;
+  c->steps_dirty = true;
+  return 0;
+}
+
+int hs_set_precond_options(hs_ctx* c, int seam_mode, int inter) {
+  if (!c) return fail(nullptr, 1, "null context");
+  if (seam_mode != HS_SEAM_DEDUP && seam_mode != HS_SEAM_LITERAL) return fail(c, 1, "bad seam mode");
+  c->seam = seam_mode;
+  c->inter = inter ? 1 : 0;
+  return 0;
+}
+
+int hs_precond(hs_ctx* c, int kind, const double* r, double* z, int nrhs, int mem) {
+  if (!c) return fail(nullptr, 1, "null context");
+  if (int e = check_ready(c, nrhs)) return e;
+  const long long LR = LRof(c, nrhs);
+  const double2* dr;
+  double2* dz;
+  if (dev_in(c, r, LR, mem, "in", &dr) || dev_out(c, z, LR, mem, "out", &dz)) return -1;
+  if (do_precond(c, kind, dr, dz, nrhs)) return -1;
+  return finish_out(c, z, dz, LR, mem);
+}
+
+int hs_half_apply(hs_ctx* c, int direction, const double* r, double* z, int nrhs, int mem) {
+  if (!c) return fail(nullptr, 1, "null context");
+  if (direction != 0 && direction != 1) return fail(c, 1, "direction must be 0 or 1");
+  if (int e = check_ready(c, nrhs)) return e;
+  const long long LR = LRof(c, nrhs);
+  const double2* dr;
+  double2* dz;
+  if (dev_in(c, r, LR, mem, "in", &dr) || dev_out(c, z, LR, mem, "out", &dz)) return -1;
+  if (do_half(c, direction, dr, dz, nrhs)) return -1;
+  return finish_out(c, z, dz, LR, mem);
+}
+
+int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, int maxit,
+             int* iters, double* hist, int* converged, int mem) {
+  if (!c) return fail(nullptr, 1, "null context");
+  if (int e = check_ready(c, R)) return e;
+  if (!(tol > 0) || maxit < 1) return fail(c, 1, "tol must be > 0 and maxit >= 1");
+  if (pc < HS_PC_NONE || pc > HS_PC_BSP) return fail(c, 1, "unknown preconditioner kind");
+  if (c->plan.nranks > 1) return fail(c, 3, "hs_gmres across row bands is not implemented yet");
+  if (R & (R - 1)) return fail(c, 1, "batched GMRES needs nrhs a power of two");
+  const long long LR = LRof(c, R);
+  if (LR == 0) {  // empty interface system (1 x 1 lattice): 0 iterations
+    for (int r = 0; r < R; ++r) {
+      if (iters) iters[r] = 0;
+      if (converged) converged[r] = 1;
+      if (hist) hist[r] = 1.0;
+    }
+    return 0;
+  }
+  const double2* db;
+  double2* dx;
+  if (dev_in(c, b, LR, mem, "gin", &db) || dev_out(c, x, LR, mem, "gout", &dx)) return -1;
+  int chunk = 0;
+  int grid = gmres_coop_grid(*c, LR, R, &chunk);
+  if (grid <= 0) return fail(c, 3, "interface vector too large for the cooperative Arnoldi kernel");
+  GmresDev G;
+  G.LR = LR; G.R = R; G.tol = tol;
+  double2 *V, *Z;
+  if (ws_get(c, "V", (size_t)(maxit + 1) * LR, &V) || ws_get(c, "Z", LR, &Z)) return -1;
+  G.V = V;
+  const long long hsz = (long long)R * ((long long)maxit * (maxit + 3) / 2 + 2);
+  double2 *H, *sn, *g, *part, *y;
+  double2* scal;
+  if (ws_get(c, "H", hsz, &H) || ws_get(c, "sn", (size_t)maxit * R, &sn) ||
+      ws_get(c, "g", (size_t)(maxit + 1) * R, &g) || ws_get(c, "part", (size_t)2 * (grid + 2 * c->num_sms) * R, &part) ||
+      ws_get(c, "y", (size_t)maxit * R, &y) ||
+      ws_get(c, "scal", (size_t)(maxit + 1) * R + 4 * R + (size_t)maxit * R, &scal))
+    return -1;
+  int* ints;
+  double2* iw;
+  if (ws_get(c, "gint", (size_t)(5 * R + 1) / 4 + 2, &iw)) return -1;
+  ints = (int*)iw;
+  G.H = H; G.sn = sn; G.g = g; G.partial = part; G.y = y;
+  double* sd = (double*)scal;
+  G.hist = sd;
+  G.beta = sd + (size_t)(maxit + 1) * R;
+  G.wnorm0 = G.beta + R;
+  G.cs = G.wnorm0 + R;
+  G.active = ints; G.iters = ints + R; G.conv = ints + 2 * R; G.brk = ints + 3 * R; G.nactive = ints + 4 * R;
+  CK(gmres_init(*c, G, db));
+  int nact = 0;
+  CK(cudaMemcpyAsync(&nact, G.nactive, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  int kdone = 0;
+  for (int k = 0; k < maxit && nact > 0; ++k) {
+    double2* vk = V + (long long)k * LR;
+    double2* w = V + (long long)(k + 1) * LR;
+    const double2* zin = vk;
+    if (pc != HS_PC_NONE) {
+      if (do_precond(c, pc, vk, Z, R)) return -1;
+      zin = Z;
+    }
+    if (do_apply(c, HS_APPLY_IMS, zin, w, R)) return -1;
+    CK(gmres_arnoldi(*c, G, k, grid, chunk));
+    CK(gmres_givens(*c, G, k));
+    CK(cudaMemcpyAsync(&nact, G.nactive, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    kdone = k + 1;
+  }
+  if (kdone > 0) {
+    double2* u;
+    if (ws_get(c, "U", LR, &u)) return -1;
+    CK(gmres_finish(*c, G, kdone, u));
+    if (pc != HS_PC_NONE) {
+      if (do_precond(c, pc, u, dx, R)) return -1;
+    } else {
+      CK(cudaMemcpyAsync(dx, u, LR * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
+    }
+  } else {
+    CK(cudaMemsetAsync(dx, 0, LR * sizeof(double2), c->stream));
+  }
+  std::vector<int> hi(5 * R);
+  CK(cudaMemcpyAsync(hi.data(), ints, 5 * R * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  if (hist) CK(cudaMemcpyAsync(hist, G.hist, (size_t)(kdone + 1) * R * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  if (int e = finish_out(c, x, dx, LR, mem)) return e;
+  CK(cudaStreamSynchronize(c->stream));
+  for (int r = 0; r < R; ++r) {
+    if (iters) iters[r] = hi[R + r];
+    if (converged) converged[r] = hi[2 * R + r];
+  }
+  return 0;
+}
+
+// ---- introspection ---------------------------------------------------------
+int hs_sizes(const hs_ctx* c, int64_t* L, int* nsub, int* ngroups, int* npairs) {
+  if (!c) return 1;
+  if (L) *L = c->plan.L;
+  if (nsub) *nsub = c->plan.nsub;
+  if (ngroups) *ngroups = c->plan.ng;
+  if (npairs) *npairs = c->plan.npairs;
+  return 0;
+}
+
+int hs_pairs(const hs_ctx* c, int32_t* pairs) {
+  if (!c) return 1;
+  const Plan& P = c->plan;
+  for (int m = 0; m < P.npairs; ++m) {
+    const SubPlan& o = P.subs[P.block_sub[m]];
+    const int q = m - o.first_block;
+    const SubPlan& nb = P.subs[o.nbr[q]];
+    pairs[4 * m] = o.i1; pairs[4 * m + 1] = o.i2; pairs[4 * m + 2] = nb.i1; pairs[4 * m + 3] = nb.i2;
+  }
+  return 0;
+}
+
+int hs_block_owner(const hs_ctx* c, int32_t* owner) {
+  if (!c) return 1;
+  for (int m = 0; m < c->plan.npairs; ++m) owner[m] = c->plan.subs[c->plan.block_sub[m]].rank;
+  return 0;
+}
+
+int hs_schedule(const hs_ctx* cc, int kind, int32_t* rec, int cap, int* count) {
+  if (!cc) return 1;
+  hs_ctx* c = const_cast<hs_ctx*>(cc);
+  Plan P = c->plan;  // copy: full (unsharded) schedule
+  P.nranks = 1; P.rank = 0;
+  for (auto& s : P.subs) s.rank = 0;
+  std::vector<int32_t> out;
+  auto emit = [&](const std::vector<StepTable>& steps, int phase, int& step) {
+    for (auto& st : steps) {
+      ++step;
+      std::set<int> seen;
+      for (auto& it : st.items)
+        if (seen.insert(it.s).second) { out.push_back(step); out.push_back(phase); out.push_back(it.s); }
+    }
+  };
+  int step = 0;
+  if (kind == HS_PC_SP) {
+    P.win_lower.clear(); P.win_upper.clear();
+    if (P.ng >= 2) { P.win_lower.push_back({2, P.ng + 1}); P.win_upper.push_back({2, P.ng + 1}); }
+    emit(P.half_steps(0), 0, step);
+    emit(P.half_steps(1), 2, step);
+  } else if (kind == HS_PC_BSP) {
+    emit(P.half_steps(0), 0, step);
+    emit(P.half_steps(1), 2, step);
+  } else if (kind != HS_PC_NONE) {
+    return fail(c, 1, "unknown preconditioner kind");
+  }
+  *count = (int)(out.size() / 3);
+  if (rec) {
+    if (cap < *count) return fail(c, 1, "schedule buffer too small");
+    std::copy(out.begin(), out.end(), rec);
+  }
+  return 0;
+}
+
+int hs_exchange_plan(const hs_ctx* cc, int kind, int peer, int32_t* blocks, int cap, int* count) {
+  if (!cc) return 1;
+  hs_ctx* c = const_cast<hs_ctx*>(cc);
+  const Plan& P = c->plan;
+  std::vector<StepTable> steps;
+  if (kind == 0) steps = P.half_steps(0);
+  else if (kind == 1) steps = P.half_steps(1);
+  else if (kind == 2) steps.push_back(P.full_step());
+  else return fail(c, 1, "kind must be 0, 1 or 2");
+  std::vector<int32_t> out;
+  for (size_t t = 0; t < steps.size(); ++t)
+    for (auto& it : steps[t].items) {
+      const SubPlan& sp = P.subs[it.s];
+      for (int q = 0; q < sp.k; ++q) {
+        const int sl = it.slot[q];
+        if (sl == -1) continue;
+        const int dst = sl >= 0 ? P.rank + 1 : P.rank - 1;
+        if (dst != peer) continue;
+        out.push_back((int32_t)t);
+        out.push_back(sp.tgt_block[q]);
+      }
+    }
+  *count = (int)(out.size() / 2);
+  if (blocks) {
+    if (cap < *count) return fail(c, 1, "buffer too small");
+    std::copy(out.begin(), out.end(), blocks);
+  }
+  return 0;
+}
+
+int hs_get_schur(hs_ctx* c, int i1, int i2, double* T) {
+  if (!c) return fail(nullptr, 1, "null context");
+  NEED_GPU(c);
+  if (!c->factored || !c->T) return fail(c, 1, "no maps (call hs_factor)");
+  if (i1 < 1 || i1 > c->n1 || i2 < 1 || i2 > c->n2) return fail(c, 1, "subdomain out of range");
+  const SubPlan& sp = c->plan.subs[c->plan.ordinal(i1, i2)];
+  const long long K = (long long)sp.k * c->n;
+  const long long nt = (K + kRowTile - 1) / kRowTile;
+  std::vector<double2> tm((size_t)nt * kRowTile * K);
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaMemcpy(tm.data(), c->T + sp.T_off, tm.size() * sizeof(double2), cudaMemcpyDeviceToHost));
+  for (long long r = 0; r < K; ++r)
+    for (long long col = 0; col < K; ++col) {
+      const double2 v = tm[(size_t)((r / kRowTile) * K + col) * kRowTile + r % kRowTile];
+      T[2 * (r * K + col)] = v.x;
+      T[2 * (r * K + col) + 1] = v.y;
+    }
+  return 0;
+}
+
+int hs_set_schur(hs_ctx* c, int i1, int i2, const double* T) {
+  if (!c) return fail(nullptr, 1, "null context");
+  NEED_GPU(c);
+  if (i1 < 1 || i1 > c->n1 || i2 < 1 || i2 > c->n2) return fail(c, 1, "subdomain out of range");
+  if (!c->T) CK(dalloc(c, (void**)&c->T, c->T_elems * sizeof(double2)));
+  const SubPlan& sp = c->plan.subs[c->plan.ordinal(i1, i2)];
+  const long long K = (long long)sp.k * c->n;
+  const long long nt = (K + kRowTile - 1) / kRowTile;
+  std::vector<double2> tm((size_t)nt * kRowTile * K, make_double2(0, 0));
+  for (long long r = 0; r < K; ++r)
+    for (long long col = 0; col < K; ++col)
+      tm[(size_t)((r / kRowTile) * K + col) * kRowTile + r % kRowTile] =
+          make_double2(T[2 * (r * K + col)], T[2 * (r * K + col) + 1]);
+  CK(cudaMemcpy(c->T + sp.T_off, tm.data(), tm.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  c->factored = true;  // bring-up: maps supplied by the caller
+  return 0;
+}
+
+int hs_set_async(hs_ctx* c, int a) {
+  if (!c) return 1;
+  c->async_mode = a ? 1 : 0;
+  return 0;
+}
+
+int hs_sync(hs_ctx* c) {
+  if (!c) return 1;
+  NEED_GPU(c);
+  CK(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int hs_stream(hs_ctx* c, uint64_t* s) {
+  if (!c) return 1;
+  NEED_GPU(c);
+  *s = (uint64_t)(uintptr_t)c->stream;
+  return 0;
+}
+
+int hs_set_kernel_timing(hs_ctx* c, int on) {
+  if (!c) return 1;
+  c->timing = on != 0;
+  return 0;
+}
+
+int hs_kernel_stats(hs_ctx* c, int64_t* launches, double* ms, double* bytes, int reset) {
+  if (!c) return 1;
+  NEED_GPU(c);
+  CK(cudaStreamSynchronize(c->stream));
+  for (size_t i = 0; i < c->ev_pending.size(); ++i) {
+    float t = 0;
+    cudaEventElapsedTime(&t, c->ev_pending[i].first, c->ev_pending[i].second);
+    c->k_ms += t;
+    c->k_bytes += c->ev_bytes[i];
+    c->k_launches++;
+    c->ev_pool.push_back(c->ev_pending[i].first);
+    c->ev_pool.push_back(c->ev_pending[i].second);
+  }
+  c->ev_pending.clear();
+  c->ev_bytes.clear();
+  if (launches) *launches = c->k_launches;
+  if (ms) *ms = c->k_ms;
+  if (bytes) *bytes = c->k_bytes;
+  if (reset) { c->k_launches = 0; c->k_ms = 0; c->k_bytes = 0; }
+  return 0;
+}
+
+int hs_memory(const hs_ctx* c, int64_t* bytes) {
+  if (!c) return 1;
+  *bytes = c->dev_bytes;
+  return 0;
+}
+
+int hs_nccl_unique_id(uint8_t id[128]) {
+  Ctx* c = nullptr;
+  ncclUniqueId u;
+  NK(ncclGetUniqueId(&u));
+  static_assert(sizeof(u) == 128, "ncclUniqueId size");
+  std::memcpy(id, &u, 128);
+  return 0;
+}
+
+int hs_comm_init(hs_ctx* c, const uint8_t id[128]) {
+  if (!c) return fail(nullptr, 1, "null context");
+  NEED_GPU(c);
+  CK(cudaSetDevice(c->device));
+  ncclUniqueId u;
+  std::memcpy(&u, id, 128);
+  ncclComm_t comm;
+  NK(ncclCommInitRank(&comm, c->plan.nranks, u, c->plan.rank));
+  c->nccl = comm;
+  return 0;
+}
+
+}  // extern "C"

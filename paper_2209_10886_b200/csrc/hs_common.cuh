@@ -1,0 +1,64 @@
+// Device helpers shared by the kernels.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "hs_ctx.h"
+
+namespace hs {
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// acc += a * b
+__device__ __forceinline__ void cfma(double2& acc, double2 a, double2 b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+}
+// acc += conj(a) * b
+__device__ __forceinline__ void cfma_conj(double2& acc, double2 a, double2 b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(-a.y, b.x, acc.y);
+}
+
+// Streaming 128-bit load of a map element: read-only path, no L1 allocation.
+__device__ __forceinline__ double2 ld_stream(const double2* p) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void epi_apply(const Epi& e, long long t, double2 y) {
+  switch (e.mode) {
+    case EPI_SET: e.o1[t] = y; break;
+    case EPI_ACC: e.o1[t] = cadd(e.o1[t], y); break;
+    case EPI_IMS: e.o1[t] = csub(e.a[t], y); break;
+    case EPI_RESID: {
+      // r' = b - (zL - S zL)  (SPEC.md:343 with interface_system.py:144-146 order)
+      double2 zl = e.b[t];
+      double2 v = csub(e.a[t], csub(zl, y));
+      e.o1[t] = v;
+      e.o2[t] = v;
+      e.o3[t] = cadd(zl, v);
+    } break;
+    case EPI_ACC2:
+      e.o1[t] = cadd(e.o1[t], y);
+      e.o2[t] = cadd(e.o2[t], y);
+      break;
+  }
+}
+
+// Send-buffer routing of a face's output (row-band exchange); returns true if routed.
+__device__ __forceinline__ bool epi_route(const Epi& e, int slot, long long p, double2 y) {
+  if (slot == -1) return false;
+  if (slot >= 0) e.send_up[p + 0] = y;
+  else e.send_dn[p + 0] = y;
+  return true;
+}
+
+}  // namespace hs

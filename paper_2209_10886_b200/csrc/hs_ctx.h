@@ -1,0 +1,130 @@
+// Context of one GPU (or plan-only) instance and the device data structures
+// shared by the kernels.  See include/hsb200.h for the C ABI.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "hs_plan.h"
+
+namespace hs {
+
+constexpr int kRowTile = 32;  // rows per tile of the tile-major map layout
+
+// Per-subdomain record on the device.  Maps are stored tile-major:
+// T_s[tile][col][lane] = T_s(tile*32 + lane, col), rows padded to a multiple of
+// 32 with zeros, so a 32-row strip of a map is one contiguous K*512-byte run.
+struct DevSub {
+  long long T_off;  // element offset of the map
+  int in_off;       // element offset of the incoming slab m(s, .) (block * n)
+  int k;            // interface faces; K = k * n columns
+  int tgt[4];       // element offset (block * n) of the block written by each face
+};
+
+struct DevItem {
+  int s, rlo, rhi, alt;
+  int slot[4];
+};
+
+struct DevTile {
+  int item, tile;
+};
+
+struct DevRecv {
+  int dir, slot;
+  long long off;
+};
+
+// Epilogue of a step: what to do with output row values y at element t.
+enum EpiMode {
+  EPI_SET = 0,    // o1[t] = y
+  EPI_ACC = 1,    // o1[t] += y                       (sweep step, one state)
+  EPI_IMS = 2,    // o1[t] = a[t] - y                 ((I - S) g)
+  EPI_RESID = 3,  // v = a[t] - b[t] + y; o1 = v; o2 = v; o3 = b[t] + v   (BSP residual)
+  EPI_ACC2 = 4,   // o1[t] += y; o2[t] += y           (BSP backward step)
+};
+
+struct Epi {
+  int mode;
+  double2* o1;
+  double2* o2;
+  double2* o3;
+  const double2* a;
+  const double2* b;
+  double2* send_up;
+  double2* send_dn;
+};
+
+// A step uploaded to the device: items + tiles + receive list.
+struct DevStep {
+  DevItem* items = nullptr;
+  DevTile* tiles = nullptr;
+  DevRecv* recv = nullptr;
+  int nitems = 0, ntiles = 0, nrecv = 0;
+  int nsend_up = 0, nsend_dn = 0, nrecv_up = 0, nrecv_dn = 0;
+  int maxK = 0;
+  double bytes_per_rhs_map = 0, bytes_per_rhs_vec = 0;  // algorithmic bytes: map part, per-RHS vector part
+};
+
+// One distinct subdomain operator (Dirichlet mask) and its factor.
+struct OpClass {
+  std::vector<uint8_t> mask;          // n*n, 1 = Dirichlet cell
+  std::vector<int32_t> dcells;        // sorted Dirichlet cells
+  double2* X = nullptr;               // n x (n x n) inverses of the block-LU pivots
+  double2* T4 = nullptr;              // full 4n x 4n map (row-major)
+  bool factored = false;
+};
+
+struct Workspace {
+  double2* p = nullptr;
+  size_t cap = 0;  // elements
+};
+
+struct Ctx {
+  int device = -1;
+  int n1 = 0, n2 = 0, n = 0;
+  double h = 0, kappa = 0, tau_re = 0, tau_im = 0;
+  Plan plan;
+  std::string err;
+  // per-subdomain Dirichlet cells (host) and classes
+  std::map<int, std::vector<int32_t>> dcells;  // ordinal -> cells
+  std::vector<OpClass> classes;
+  std::vector<int> sub_class;
+  bool factored = false;
+  // device state
+  cudaStream_t stream = nullptr;
+  double2* T = nullptr;
+  size_t T_elems = 0;
+  DevSub* dsubs = nullptr;
+  // windows / precond options
+  int seam = 0, inter = 1;
+  bool steps_dirty = true;
+  std::vector<DevStep> fwd, bwd, sp_fwd, sp_bwd;
+  DevStep full;
+  std::vector<std::vector<int>> seam_blocks;  // [dir] blocks of seam groups (literal mode)
+  int* d_seam[2] = {nullptr, nullptr};
+  int n_seam[2] = {0, 0};
+  // vectors (grown on demand): named work buffers
+  std::map<std::string, Workspace> ws;
+  // exchange buffers
+  double2* send_up = nullptr; double2* send_dn = nullptr;
+  double2* recv_up = nullptr; double2* recv_dn = nullptr;
+  size_t xbuf_cap = 0;
+  void* nccl = nullptr;  // ncclComm_t
+  // execution control / timing
+  int async_mode = 0;
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pending;
+  std::vector<double> ev_bytes;
+  std::vector<cudaEvent_t> ev_pool;
+  int64_t k_launches = 0;
+  double k_ms = 0, k_bytes = 0;
+  int64_t dev_bytes = 0;
+  int num_sms = 148;
+  int coop_ok = 0;
+};
+
+}  // namespace hs

@@ -1,0 +1,73 @@
+// Kernel launchers (host-callable), implemented in hs_apply.cu, hs_schur.cu, hs_krylov.cu.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "hs_ctx.h"
+
+namespace hs {
+
+enum VecOp { VEC_ADD = 0, VEC_COPY2 = 1, VEC_INIT_BWD = 2 };
+
+// Sparse right-hand-side additions of one operator class, grouped by grid row.
+struct ExtraRHS {
+  std::vector<int> row_ptr;  // n + 1 (empty = none)
+  int* d_x = nullptr;
+  int* d_col = nullptr;
+  double2* d_val = nullptr;
+};
+
+// ---- step apply (hs_apply.cu)
+void launch_step(Ctx& c, const DevStep& st, const double2* srcA, const double2* srcB, const Epi& e,
+                 int R);
+void launch_recv_epi(Ctx& c, const DevStep& st, const Epi& e, int R);
+void launch_vec(Ctx& c, int op, long long len, double2* o1, double2* o2, const double2* a,
+                const double2* b);
+void launch_seam_add(Ctx& c, int dir, double2* z, const double2* r, int R);
+cudaError_t set_step_smem_limit();
+
+// ---- factorisation (hs_schur.cu)
+cudaError_t factor_blocks(Ctx& c, double2* X, long long xstride, const uint8_t* dmasks, int ncls,
+                          double2* Rp, double2* Cp, long long pstride, int* dbad);
+cudaError_t solve_boundary(Ctx& c, const double2* X, long long xstride, const uint8_t* dmasks,
+                           int ncls, int R, int nunit, const ExtraRHS* extras, double2* Y,
+                           long long ystride, double2* Bk, long long bstride, double2* G,
+                           long long gstride);
+void zgemm(cudaStream_t st, int M, int N, int K, double2 alpha, const double2* A, int lda,
+           long long sa, const double2* B, int ldb, long long sb, double2 beta, double2* C, int ldc,
+           long long sc, int batch);
+void launch_make_T4(Ctx& c, double2* T4, const double2* G, int R, double2 a, double2 b);
+void launch_scatter_T(Ctx& c, const int2* tl, int ntiles, const int* sub_faces, const int* sub_cls,
+                      double2* const* T4s);
+void launch_lift_b(Ctx& c, double2* b, const double2* G, int Rtot, int col0, int nrhs,
+                   const int* face_tgt, double2 coef);
+
+// ---- GMRES (hs_krylov.cu)
+struct GmresDev {
+  double2* V;        // (maxit+1) x LR basis
+  long long LR;      // L * R
+  int R;
+  double2* H;        // packed columns: column k at offset R * k(k+3)/2, length (k+2) x R
+  double* cs;        // maxit x R
+  double2* sn;       // maxit x R
+  double2* g;        // (maxit+1) x R
+  double* hist;      // (maxit+1) x R
+  double* beta;      // R
+  double* wnorm0;    // R
+  int* active;       // R: 1 while iterating
+  int* iters;        // R
+  int* conv;         // R
+  int* brk;          // R
+  int* nactive;      // 1
+  double2* partial;  // 2 x grid x R
+  double2* y;        // maxit x R
+  double tol;
+};
+cudaError_t gmres_init(Ctx& c, GmresDev& G, const double2* b);
+cudaError_t gmres_arnoldi(Ctx& c, GmresDev& G, int k, int grid, int chunk);
+cudaError_t gmres_givens(Ctx& c, GmresDev& G, int k);
+cudaError_t gmres_finish(Ctx& c, GmresDev& G, int maxit, double2* u);
+int gmres_coop_grid(Ctx& c, long long LR, int R, int* chunk);
+
+}  // namespace hs

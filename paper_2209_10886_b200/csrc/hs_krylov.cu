@@ -1,0 +1,330 @@
+// GMRES on the device: right-preconditioned, full (no restart), modified
+// Gram-Schmidt Arnoldi, complex Givens rotations (the
+// conventions are written out in oracle/gmres.py and mirrored here exactly).
+//
+// The Arnoldi step of iteration k is ONE cooperative kernel: each CTA keeps
+// its slice of w = A M v_k in shared memory, and for j = 0..k computes its
+// partial <v_j, w>, meets the other CTAs at a grid barrier, reduces the
+// partials in a fixed order (deterministic, no atomics) and subtracts
+// h_jk v_j.  HBM traffic is one read of each v_j plus one read/write of w.
+// Multi-RHS (R columns, RHS fastest) runs R independent processes in lockstep
+// (batched GMRES); a thread always sees the same column r = e mod R.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "hs_common.cuh"
+#include "hs_kernels.h"
+
+namespace cg = cooperative_groups;
+
+namespace hs {
+
+__device__ __forceinline__ long long hoff(int k, int R) { return (long long)R * ((long long)k * (k + 3) / 2); }
+
+// Block-level per-column reduction: red[tid] holds a thread value, threads
+// with equal tid % R share a column; P = blockDim / R is a power of two.
+__device__ void block_colsum(double2* red, int R) {
+  const int tid = threadIdx.x;
+  for (int s = blockDim.x / 2; s >= R; s >>= 1) {
+    __syncthreads();
+    if (tid < s) red[tid] = cadd(red[tid], red[tid + s]);
+  }
+  __syncthreads();
+}
+
+// Grid-level reduction of partials[b][r] (b < nblk) into out[r] (shared),
+// fixed summation order.  Uses red (blockDim) as scratch.
+__device__ void grid_colsum(const double2* partials, int nblk, int R, double2* red, double2* out) {
+  const int tid = threadIdx.x;
+  const int r = tid % R, i = tid / R, P = blockDim.x / R;
+  double2 acc = make_double2(0, 0);
+  for (int b = i; b < nblk; b += P) acc = cadd(acc, partials[(long long)b * R + r]);
+  red[tid] = acc;
+  block_colsum(red, R);
+  if (tid < R) out[tid] = red[tid];
+  __syncthreads();
+}
+
+__global__ void k_mgs(GmresDev G, int k, int chunk) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double2 sm[];
+  const int R = G.R;
+  double2* ws = sm;                    // chunk
+  double2* red = ws + chunk;           // blockDim
+  double2* hsh = red + blockDim.x;     // R
+  const long long LR = G.LR;
+  const long long e0 = (long long)blockIdx.x * chunk;
+  const int cnt = (int)max(0LL, min((long long)chunk, LR - e0));
+  const int tid = threadIdx.x;
+  const int nblk = gridDim.x;
+  double2* w = G.V + (long long)(k + 1) * LR;
+  double2* part = G.partial;
+  int pb = 0;
+  for (int i = tid; i < cnt; i += blockDim.x) ws[i] = w[e0 + i];
+  // ||w|| before orthogonalisation (breakdown test)
+  {
+    double2 acc = make_double2(0, 0);
+    for (int i = tid; i < cnt; i += blockDim.x) acc.x += ws[i].x * ws[i].x + ws[i].y * ws[i].y;
+    red[tid] = acc;
+    block_colsum(red, R);
+    if (tid < R) part[(long long)pb * nblk * R + (long long)blockIdx.x * R + tid] = red[tid];
+    grid.sync();
+    grid_colsum(part + (long long)pb * nblk * R, nblk, R, red, hsh);
+    if (blockIdx.x == 0 && tid < R) G.wnorm0[tid] = sqrt(hsh[tid].x);
+    pb ^= 1;
+  }
+  double2* Hk = G.H + hoff(k, R);
+  for (int j = 0; j <= k; ++j) {
+    const double2* v = G.V + (long long)j * LR + e0;
+    double2 acc = make_double2(0, 0);
+    for (int i = tid; i < cnt; i += blockDim.x) cfma_conj(acc, v[i], ws[i]);
+    red[tid] = acc;
+    block_colsum(red, R);
+    if (tid < R) part[(long long)pb * nblk * R + (long long)blockIdx.x * R + tid] = red[tid];
+    grid.sync();
+    grid_colsum(part + (long long)pb * nblk * R, nblk, R, red, hsh);
+    pb ^= 1;
+    if (blockIdx.x == 0 && tid < R) Hk[(long long)j * R + tid] = hsh[tid];
+    for (int i = tid; i < cnt; i += blockDim.x) {
+      const double2 h = hsh[(int)((e0 + i) % R)];
+      double2 vv = v[i];
+      // w = w - h v   (oracle: w - H[j,k] * V[j])
+      ws[i] = csub(ws[i], cmul(h, vv));
+    }
+    __syncthreads();
+  }
+  {
+    double2 acc = make_double2(0, 0);
+    for (int i = tid; i < cnt; i += blockDim.x) acc.x += ws[i].x * ws[i].x + ws[i].y * ws[i].y;
+    red[tid] = acc;
+    block_colsum(red, R);
+    if (tid < R) part[(long long)pb * nblk * R + (long long)blockIdx.x * R + tid] = red[tid];
+    grid.sync();
+    grid_colsum(part + (long long)pb * nblk * R, nblk, R, red, hsh);
+  }
+  if (tid < R) {
+    double hn = sqrt(hsh[tid].x);
+    hsh[tid].x = hn;
+    if (blockIdx.x == 0) Hk[(long long)(k + 1) * R + tid] = make_double2(hn, 0);
+  }
+  __syncthreads();
+  for (int i = tid; i < cnt; i += blockDim.x) {
+    const double hn = hsh[(int)((e0 + i) % R)].x;
+    w[e0 + i] = hn > 0 ? make_double2(ws[i].x / hn, ws[i].y / hn) : make_double2(0, 0);
+  }
+}
+
+// Givens update of column k for every active right-hand side.
+__global__ void k_givens(GmresDev G, int k) {
+  const int R = G.R;
+  const double eps = 2.220446049250313e-16;
+  __shared__ int cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  for (int r = threadIdx.x; r < R; r += blockDim.x) {
+    if (!G.active[r]) continue;
+    double2* Hk = G.H + hoff(k, R);
+    const double hn = Hk[(long long)(k + 1) * R + r].x;
+    for (int j = 0; j < k; ++j) {
+      const double c = G.cs[(long long)j * R + r];
+      const double2 s = G.sn[(long long)j * R + r];
+      const double2 a = Hk[(long long)j * R + r], b = Hk[(long long)(j + 1) * R + r];
+      // t = c a + s b ;  b' = -conj(s) a + c b
+      double2 t = cadd(make_double2(c * a.x, c * a.y), cmul(s, b));
+      double2 sc = make_double2(-s.x, s.y);  // -conj(s)
+      double2 b2 = cadd(cmul(sc, a), make_double2(c * b.x, c * b.y));
+      Hk[(long long)j * R + r] = t;
+      Hk[(long long)(j + 1) * R + r] = b2;
+    }
+    const double2 a = Hk[(long long)k * R + r];
+    const double bb = Hk[(long long)(k + 1) * R + r].x;
+    double c;
+    double2 s;
+    const double aa = hypot(a.x, a.y);
+    if (aa == 0.0) {
+      c = 0.0;
+      s = make_double2(1.0, 0.0);
+    } else {
+      const double rho = hypot(aa, fabs(bb));
+      c = aa / rho;
+      // s = (a/|a|) * conj(b) / rho, b real
+      s = make_double2(a.x / aa * bb / rho, a.y / aa * bb / rho);
+    }
+    G.cs[(long long)k * R + r] = c;
+    G.sn[(long long)k * R + r] = s;
+    Hk[(long long)k * R + r] = cadd(make_double2(c * a.x, c * a.y), make_double2(s.x * bb, s.y * bb));
+    Hk[(long long)(k + 1) * R + r] = make_double2(0, 0);
+    const double2 gk = G.g[(long long)k * R + r];
+    // g[k+1] = -conj(s) g[k];  g[k] = c g[k]
+    G.g[(long long)(k + 1) * R + r] = cmul(make_double2(-s.x, s.y), gk);
+    G.g[(long long)k * R + r] = make_double2(c * gk.x, c * gk.y);
+    const double2 gn = G.g[(long long)(k + 1) * R + r];
+    const double res = hypot(gn.x, gn.y) / G.beta[r];
+    G.hist[(long long)(k + 1) * R + r] = res;
+    G.iters[r] = k + 1;
+    if (res <= G.tol) {
+      G.conv[r] = 1;
+      G.active[r] = 0;
+    } else if (hn <= 16 * eps * G.wnorm0[r]) {
+      G.brk[r] = 1;
+      G.active[r] = 0;
+    } else {
+      atomicAdd(&cnt, 1);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *G.nactive = cnt;
+}
+
+// beta = ||b|| per column (two-pass deterministic), V0 = b / beta, state init.
+__global__ void k_colnorm_partial(const double2* x, long long LR, int R, int chunk, double2* part) {
+  extern __shared__ double2 red[];
+  const long long e0 = (long long)blockIdx.x * chunk;
+  const int cnt = (int)max(0LL, min((long long)chunk, LR - e0));
+  double2 acc = make_double2(0, 0);
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    double2 v = x[e0 + i];
+    acc.x += v.x * v.x + v.y * v.y;
+  }
+  red[threadIdx.x] = acc;
+  block_colsum(red, R);
+  if (threadIdx.x < R) part[(long long)blockIdx.x * R + threadIdx.x] = red[threadIdx.x];
+}
+
+__global__ void k_gmres_init(GmresDev G, int nblk) {
+  extern __shared__ double2 red[];
+  double2* out = red + blockDim.x;
+  grid_colsum(G.partial, nblk, G.R, red, out);
+  __shared__ int cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  for (int r = threadIdx.x; r < G.R; r += blockDim.x) {
+    double b = sqrt(out[r].x);
+    G.beta[r] = b;
+    G.g[r] = make_double2(b, 0);
+    G.hist[r] = 1.0;
+    G.iters[r] = 0;
+    G.brk[r] = 0;
+    G.conv[r] = b == 0.0 ? 1 : 0;
+    G.active[r] = b == 0.0 ? 0 : 1;
+    if (b != 0.0) atomicAdd(&cnt, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *G.nactive = cnt;
+}
+
+__global__ void k_scale_cols(double2* V, const double2* b, const double* beta, long long LR, int R) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < LR;
+       i += (long long)gridDim.x * blockDim.x) {
+    double bt = beta[i % R];
+    double2 v = b[i];
+    V[i] = bt > 0 ? make_double2(v.x / bt, v.y / bt) : make_double2(0, 0);
+  }
+}
+
+// Back substitution H y = g (rotated, upper triangular, m = iters[r]).
+__global__ void k_trisolve(GmresDev G) {
+  const int R = G.R;
+  for (int r = threadIdx.x; r < R; r += blockDim.x) {
+    const int m = G.iters[r];
+    for (int i = m - 1; i >= 0; --i) {
+      double2 acc = G.g[(long long)i * R + r];
+      for (int j = i + 1; j < m; ++j) {
+        const double2 hij = G.H[hoff(j, R) + (long long)i * R + r];
+        acc = csub(acc, cmul(hij, G.y[(long long)j * R + r]));
+      }
+      const double2 d = G.H[hoff(i, R) + (long long)i * R + r];
+      const double den = d.x * d.x + d.y * d.y;
+      G.y[(long long)i * R + r] =
+          make_double2((acc.x * d.x + acc.y * d.y) / den, (acc.y * d.x - acc.x * d.y) / den);
+    }
+  }
+}
+
+// u = sum_{j < m_r} y_j v_j
+__global__ void k_combine(GmresDev G, int mmax, double2* u) {
+  const long long LR = G.LR;
+  const int R = G.R;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < LR;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(e % R);
+    const int m = G.iters[r];
+    double2 acc = make_double2(0, 0);
+    for (int j = 0; j < mmax && j < m; ++j) cfma(acc, G.y[(long long)j * R + r], G.V[(long long)j * LR + e]);
+    u[e] = acc;
+  }
+}
+
+static int pow2_floor(int x) {
+  int p = 1;
+  while (p * 2 <= x) p *= 2;
+  return p;
+}
+
+static int coop_block(int R) { return R * pow2_floor(1024 / R); }
+
+int gmres_coop_grid(Ctx& c, long long LR, int R, int* chunk) {
+  const int bs = coop_block(R);
+  int dev = c.device;
+  int per_sm = 1;
+  // aim for 1 CTA per SM with <= 160 KB of w slice
+  long long nb = c.num_sms;
+  long long ch = (LR + nb - 1) / nb;
+  ch = ((ch + R - 1) / R) * R;
+  size_t smem = (size_t)(ch + bs + R) * sizeof(double2);
+  if (smem > 200 * 1024) {
+    per_sm = 2;
+    nb = (long long)c.num_sms * 2;
+    ch = ((LR + nb - 1) / nb + R - 1) / R * R;
+    smem = (size_t)(ch + bs + R) * sizeof(double2);
+    if (smem > 110 * 1024) return -1;
+  }
+  (void)dev;
+  (void)per_sm;
+  *chunk = (int)ch;
+  return (int)((LR + ch - 1) / ch);
+}
+
+cudaError_t gmres_init(Ctx& c, GmresDev& G, const double2* b) {
+  const int R = G.R;
+  const int bs = coop_block(R);
+  long long nb = c.num_sms * 2;
+  long long ch = ((G.LR + nb - 1) / nb + R - 1) / R * R;
+  int nblk = (int)((G.LR + ch - 1) / ch);
+  k_colnorm_partial<<<nblk, bs, bs * sizeof(double2), c.stream>>>(b, G.LR, R, (int)ch, G.partial);
+  k_gmres_init<<<1, bs, (bs + R) * sizeof(double2), c.stream>>>(G, nblk);
+  int g2 = (int)std::min<long long>((G.LR + 255) / 256, (long long)c.num_sms * 8);
+  k_scale_cols<<<g2 > 0 ? g2 : 1, 256, 0, c.stream>>>(G.V, b, G.beta, G.LR, R);
+  return cudaGetLastError();
+}
+
+cudaError_t gmres_arnoldi(Ctx& c, GmresDev& G, int k, int grid, int chunk) {
+  const int bs = coop_block(G.R);
+  size_t smem = (size_t)(chunk + bs + G.R) * sizeof(double2);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_mgs, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+    attr_set = true;
+  }
+  void* args[] = {(void*)&G, (void*)&k, (void*)&chunk};
+  return cudaLaunchCooperativeKernel((const void*)k_mgs, dim3(grid), dim3(bs), args, smem, c.stream);
+}
+
+cudaError_t gmres_givens(Ctx& c, GmresDev& G, int k) {
+  int bs = G.R < 1024 ? ((G.R + 31) / 32) * 32 : 1024;
+  k_givens<<<1, bs, 0, c.stream>>>(G, k);
+  return cudaGetLastError();
+}
+
+cudaError_t gmres_finish(Ctx& c, GmresDev& G, int mmax, double2* u) {
+  int bs = G.R < 1024 ? ((G.R + 31) / 32) * 32 : 1024;
+  k_trisolve<<<1, bs, 0, c.stream>>>(G);
+  int g2 = (int)std::min<long long>((G.LR + 255) / 256, (long long)c.num_sms * 8);
+  k_combine<<<g2 > 0 ? g2 : 1, 256, 0, c.stream>>>(G, mmax, u);
+  return cudaGetLastError();
+}
+
+}  // namespace hs

@@ -1,0 +1,505 @@
+// One-shot subdomain factorisation on the GPU: interface Schur maps.
+//
+// Replaces LocalOperator.__init__ + splu (discretization.py:126-174) and the
+// per-apply solve_local + extract_outgoing_trace (discretization.py:264-312)
+// by the dense map
+//     T = -(s/d) I - (2 tau / (h^3 d^2)) E^T A^{-1} E
+// (SURVEY.md §7), computed once per DISTINCT operator: the matrix depends
+// only on (n, h, kappa, tau, Dirichlet cells) (discretization.py:221-256), so
+// every subdomain without scatterer cells shares one operator.
+//
+// A is taken row-block by row-block (grid rows y = k, n cells each): it is
+// block tridiagonal, A = tridiag(C_{k-1}, D_k, C_k) with diagonal couplings
+// C_k = -1/h^2 (zero at Dirichlet cells, which are eliminated: identity rows
+// AND columns, their known value moved to the right-hand side).  Natural-order
+// block elimination without inter-block pivoting (accurate for these
+// operators, SURVEY.md §7 hard part 1):
+//     S_0 = D_0,   S_k = D_k - C_{k-1} X_{k-1} C_{k-1},   X_k = S_k^{-1}
+// X_k by blocked in-place Gauss-Jordan (32-wide panels, partial pivoting
+// inside the diagonal panel block).  Then for the R right-hand sides (one unit
+// vector per boundary cell, plus lifting data):
+//     Y_0 = X_0 F_0,  Y_k = X_k (F_k - C_{k-1} Y_{k-1})         (forward)
+//     U_{n-1} = Y_{n-1},  U_k = Y_k - X_k C_k U_{k+1}            (backward)
+// and the boundary rows of U give E^T A^{-1} E.  All dense work is batched
+// over the distinct operators; the products are complex GEMMs.
+#include <cuda_runtime.h>
+
+#include <cmath>
+
+#include "hs_common.cuh"
+#include "hs_kernels.h"
+
+namespace hs {
+
+struct OpParams {
+  int n;
+  double ih2;      // 1/h^2
+  double dre, dim; // diagonal base: (4/h^2 - kappa^2) - (1/h^2)(s/d) per ghost: dre + g * (gre, gim)
+  double gre, gim; // -(1/h^2)(s/d)
+};
+
+__device__ __forceinline__ bool dmask(const uint8_t* m, int n, int k, int x) { return m[k * n + x] != 0; }
+
+// coupling between row k and k+1 at column x
+__device__ __forceinline__ double coupling(const uint8_t* m, int n, int k, int x, double ih2) {
+  return (dmask(m, n, k, x) || dmask(m, n, k + 1, x)) ? 0.0 : -ih2;
+}
+
+// S_k = D_k - C X_{k-1} C  written into X_k.   grid (n, ncls), block 256
+__global__ void k_formS(double2* X, long long xstride, const uint8_t* masks, OpParams P, int k) {
+  const int n = P.n;
+  const int i = blockIdx.x;
+  const int c = blockIdx.y;
+  const uint8_t* m = masks + (long long)c * n * n;
+  double2* Xk = X + c * xstride + (long long)k * n * n;
+  const double2* Xp = Xk - (long long)n * n;
+  const bool di = dmask(m, n, k, i);
+  const double ci = k > 0 ? coupling(m, n, k - 1, i, P.ih2) : 0.0;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    double2 v = make_double2(0, 0);
+    const bool dj = dmask(m, n, k, j);
+    if (i == j) {
+      if (di) v = make_double2(1, 0);
+      else {
+        double g = (i == 0) + (i == n - 1) + (k == 0) + (k == n - 1);
+        v = make_double2(P.dre + g * P.gre, g * P.gim);
+      }
+    } else if ((j == i + 1 || j == i - 1) && !di && !dj) {
+      v = make_double2(-P.ih2, 0);
+    }
+    if (k > 0 && ci != 0.0) {
+      const double cj = coupling(m, n, k - 1, j, P.ih2);
+      if (cj != 0.0) {
+        double2 xv = Xp[(long long)i * n + j];
+        v.x -= ci * xv.x * cj;
+        v.y -= ci * xv.y * cj;
+      }
+    }
+    Xk[(long long)i * n + j] = v;
+  }
+}
+
+// Panel step of blocked Gauss-Jordan on A = X_k (n x n, in place), panel
+// columns J = [j0, j0+nb).  Each CTA inverts P = A[J,J] in shared memory
+// (GJ with partial pivoting), then writes row panel Rp[:, cols] = P^{-1} A[J, cols]
+// (cols outside J) or P^{-1}[:, cols-j0] (cols inside J) for its column tile,
+// and copies part of the column panel Cp = A[:, J].
+// grid (ceil(n/64), ncls), block 256
+__global__ void __launch_bounds__(256) k_gj_panel(const double2* X, long long xstride, int k, int n,
+                                                  int j0, int nb, double2* Rp, double2* Cp,
+                                                  long long pstride, int* bad) {
+  __shared__ double2 Aug[32][65];   // [P | I]
+  __shared__ double2 fcol[32];
+  __shared__ int piv;
+  const int c = blockIdx.y;
+  const double2* A = X + c * xstride + (long long)k * n * n;
+  double2* R = Rp + c * pstride;
+  double2* Cpp = Cp + c * pstride;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < 32 * 64; i += 256) {
+    int r = i / 64, q = i % 64;
+    double2 v = make_double2(0, 0);
+    if (r < nb) {
+      if (q < nb) v = A[(long long)(j0 + r) * n + j0 + q];
+      else if (q - 32 == r) v = make_double2(1, 0);
+    } else if (q == r || q - 32 == r) {
+      v = make_double2(q == r ? 1 : 0, 0);  // pad rows: identity, never pivoted into
+    }
+    Aug[r][q] = v;
+  }
+  __syncthreads();
+  for (int p = 0; p < nb; ++p) {
+    if (tid < 32) {
+      double best = -1.0;
+      int bi = p;
+      if (tid >= p && tid < nb) {
+        best = fabs(Aug[tid][p].x) + fabs(Aug[tid][p].y);
+        bi = tid;
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      if (tid == 0) {
+        piv = bi;
+        if (!(best > 0.0) && bad) atomicExch(bad, 1);
+      }
+    }
+    __syncthreads();
+    const int pr = piv;
+    if (pr != p) {
+      for (int q = tid; q < 64; q += 256) {
+        double2 t = Aug[p][q];
+        Aug[p][q] = Aug[pr][q];
+        Aug[pr][q] = t;
+      }
+      __syncthreads();
+    }
+    double2 d = Aug[p][p];
+    double den = d.x * d.x + d.y * d.y;
+    double2 inv = make_double2(d.x / den, -d.y / den);
+    __syncthreads();
+    for (int q = tid; q < 64; q += 256) Aug[p][q] = cmul(Aug[p][q], inv);
+    if (tid < 32) fcol[tid] = Aug[tid][p];
+    __syncthreads();
+    for (int i = tid; i < 32 * 64; i += 256) {
+      int r = i / 64, q = i % 64;
+      if (r == p || r >= nb) continue;
+      double2 f = fcol[r];
+      if (f.x == 0.0 && f.y == 0.0) continue;
+      double2 pv = Aug[p][q];
+      Aug[r][q] = csub(Aug[r][q], cmul(f, pv));
+    }
+    __syncthreads();
+  }
+  // Aug[:, 32:32+nb] = P^{-1}.  Thread owns column q of the 64-column tile and
+  // rows r = (tid >> 6) + 4 i; the original A[J, col] column is read once.
+  const int col0 = blockIdx.x * 64;
+  {
+    const int q = tid & 63, col = col0 + q;
+    if (col < n) {
+      const bool inJ = col >= j0 && col < j0 + nb;
+      double2 bcol[32];
+      if (!inJ) {
+#pragma unroll
+        for (int t = 0; t < 32; ++t) bcol[t] = t < nb ? A[(long long)(j0 + t) * n + col] : make_double2(0, 0);
+      }
+      for (int r = tid >> 6; r < nb; r += 4) {
+        double2 v;
+        if (inJ) {
+          v = Aug[r][32 + col - j0];
+        } else {
+          v = make_double2(0, 0);
+#pragma unroll
+          for (int t = 0; t < 32; ++t) cfma(v, Aug[r][32 + t], bcol[t]);
+        }
+        R[(long long)r * n + col] = v;
+      }
+    }
+  }
+  // column panel copy: rows split across CTAs
+  for (int i = blockIdx.x * 256 + tid; i < n * nb; i += gridDim.x * 256) {
+    int r = i / nb, t = i % nb;
+    Cpp[(long long)r * 32 + t] = A[(long long)r * n + j0 + t];
+  }
+}
+
+// Trailing update of the GJ panel step.  grid (ceil(n/32), ceil(n/32), ncls), block 256
+__global__ void __launch_bounds__(256) k_gj_update(double2* X, long long xstride, int k, int n,
+                                                   int j0, int nb, const double2* Rp,
+                                                   const double2* Cp, long long pstride) {
+  __shared__ double2 Cs[32][33];
+  __shared__ double2 Rs[32][33];
+  const int c = blockIdx.z;
+  double2* A = X + c * xstride + (long long)k * n * n;
+  const double2* R = Rp + c * pstride;
+  const double2* C = Cp + c * pstride;
+  const int r0 = blockIdx.y * 32, q0 = blockIdx.x * 32;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < 32 * 32; i += 256) {
+    int a = i / 32, b = i % 32;
+    Cs[a][b] = (r0 + a < n && b < nb) ? C[(long long)(r0 + a) * 32 + b] : make_double2(0, 0);
+    Rs[a][b] = (a < nb && q0 + b < n) ? R[(long long)a * n + q0 + b] : make_double2(0, 0);
+  }
+  __syncthreads();
+  const int ql = tid & 31;
+  const int q = q0 + ql;
+  for (int a = tid >> 5; a < 32; a += 8) {
+    const int r = r0 + a;
+    if (r >= n || q >= n) continue;
+    double2 v;
+    if (r >= j0 && r < j0 + nb) {
+      v = Rs[r - j0][ql];
+    } else {
+      v = (q >= j0 && q < j0 + nb) ? make_double2(0, 0) : A[(long long)r * n + q];
+      double2 s = make_double2(0, 0);
+      for (int t = 0; t < nb; ++t) cfma(s, Cs[a][t], Rs[t][ql]);
+      v = csub(v, s);
+    }
+    A[(long long)r * n + q] = v;
+  }
+}
+
+// Complex GEMM, batched over blockIdx.z:  C = alpha * A * B + beta * C
+// A: M x K (lda), B: K x N (ldb), C: M x N (ldc); 64 x 64 tiles, 256 threads,
+// 4 x 4 complex outputs per thread (rows ty + 16 i, cols tx + 16 j).
+__global__ void __launch_bounds__(256) k_zgemm(int M, int N, int K, double2 alpha,
+                                               const double2* A, int lda, long long sa,
+                                               const double2* B, int ldb, long long sb,
+                                               double2 beta, double2* C, int ldc, long long sc) {
+  __shared__ double2 As[16][64];
+  __shared__ double2 Bs[16][64];
+  const int z = blockIdx.z;
+  A += z * sa;
+  B += z * sb;
+  C += z * sc;
+  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  double2 acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = make_double2(0, 0);
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    for (int i = tid; i < 16 * 64; i += 256) {
+      int kk = i & 15, mm = i >> 4;  // A tile: 64 rows x 16 k
+      int gr = m0 + mm, gk = k0 + kk;
+      As[kk][mm] = (gr < M && gk < K) ? A[(long long)gr * lda + gk] : make_double2(0, 0);
+      int kb = i >> 6, nn = i & 63;  // B tile: 16 k x 64 cols
+      int bk = k0 + kb, bc = n0 + nn;
+      Bs[kb][nn] = (bk < K && bc < N) ? B[(long long)bk * ldb + bc] : make_double2(0, 0);
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int kk = 0; kk < 16; ++kk) {
+      double2 a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) cfma(acc[i][j], a[i], b[j]);
+    }
+    __syncthreads();
+  }
+  const bool zero_beta = beta.x == 0.0 && beta.y == 0.0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int r = m0 + ty + 16 * i;
+    if (r >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int q = n0 + tx + 16 * j;
+      if (q >= N) continue;
+      double2 v = cmul(alpha, acc[i][j]);
+      long long o = (long long)r * ldc + q;
+      if (!zero_beta) v = cadd(v, cmul(beta, C[o]));
+      C[o] = v;
+    }
+  }
+}
+
+// Forward right-hand side of row k: B = F_k - C_{k-1} Y_{k-1}; F_k's unit part
+// for the 4n boundary columns (faces W,S,N,E, position p) is analytic.
+// grid (n, ncls), block 256
+__global__ void k_rhs_fwd(double2* Bk, long long bstride, const double2* Y, long long ystride,
+                          const uint8_t* masks, int n, int R, int nunit, double ih2, int k) {
+  const int x = blockIdx.x, c = blockIdx.y;
+  const uint8_t* m = masks + (long long)c * n * n;
+  const double cx = k > 0 ? coupling(m, n, k - 1, x, ih2) : 0.0;
+  const double2* Yp = Y + c * ystride + ((long long)(k - 1) * n + x) * R;
+  double2* B = Bk + c * bstride + (long long)x * R;
+  for (int col = threadIdx.x; col < R; col += blockDim.x) {
+    double2 v = make_double2(0, 0);
+    if (col < nunit) {
+      int f = col / n, p = col - f * n;
+      bool hit = (f == 0 && k == p && x == 0) || (f == 1 && k == 0 && x == p) ||
+                 (f == 2 && k == n - 1 && x == p) || (f == 3 && k == p && x == n - 1);
+      if (hit) v.x = 1.0;
+    }
+    if (cx != 0.0) {
+      double2 y = Yp[col];
+      v.x -= cx * y.x;
+      v.y -= cx * y.y;
+    }
+    B[col] = v;
+  }
+}
+
+// Sparse additions to F_k (Dirichlet data and its coupling to free cells).
+__global__ void k_rhs_extra(double2* Bk, long long bstride, int R, const int* ex_x, const int* ex_col,
+                            const double2* ex_val, int cnt, int c) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cnt) return;
+  double2* B = Bk + c * bstride;
+  long long o = (long long)ex_x[i] * R + ex_col[i];
+  B[o] = cadd(B[o], ex_val[i]);
+}
+
+// Backward: B = C_k U_{k+1}.  grid (n, ncls)
+__global__ void k_rhs_bwd(double2* Bk, long long bstride, const double2* Y, long long ystride,
+                          const uint8_t* masks, int n, int R, double ih2, int k) {
+  const int x = blockIdx.x, c = blockIdx.y;
+  const uint8_t* m = masks + (long long)c * n * n;
+  const double cx = coupling(m, n, k, x, ih2);
+  const double2* Yn = Y + c * ystride + ((long long)(k + 1) * n + x) * R;
+  double2* B = Bk + c * bstride + (long long)x * R;
+  for (int col = threadIdx.x; col < R; col += blockDim.x) {
+    double2 y = Yn[col];
+    B[col] = make_double2(cx * y.x, cx * y.y);
+  }
+}
+
+// Boundary values G[4n][R] (faces W,S,N,E; increasing coordinate) of U.
+__global__ void k_extract(double2* G, long long gstride, const double2* Y, long long ystride, int n,
+                          int R) {
+  const int row = blockIdx.x, c = blockIdx.y;
+  const int f = row / n, p = row - f * n;
+  int k, x;
+  if (f == 0) { k = p; x = 0; }
+  else if (f == 1) { k = 0; x = p; }
+  else if (f == 2) { k = n - 1; x = p; }
+  else { k = p; x = n - 1; }
+  const double2* src = Y + c * ystride + ((long long)k * n + x) * R;
+  double2* dst = G + c * gstride + (long long)row * R;
+  for (int col = threadIdx.x; col < R; col += blockDim.x) dst[col] = src[col];
+}
+
+// T4 = a I + b G[:, :4n]   (a = -s/d, b = -2 tau/(h^3 d^2))
+__global__ void k_make_T4(double2* T4, const double2* G, int n4, int R, double2 a, double2 b) {
+  const int row = blockIdx.x;
+  for (int col = threadIdx.x; col < n4; col += blockDim.x) {
+    double2 v = cmul(b, G[(long long)row * R + col]);
+    if (row == col) v = cadd(v, a);
+    T4[(long long)row * n4 + col] = v;
+  }
+}
+
+// Scatter compact per-subdomain maps (tile-major) from the class maps.
+// One CTA per (sub, tile) via the tile list; face[] maps compact -> global face.
+__global__ void __launch_bounds__(256) k_scatter_T(const int2* tl, const DevSub* subs,
+                                                   const int* sub_faces, const int* sub_cls,
+                                                   double2* const* T4s, double2* T, int n) {
+  __shared__ double2 buf[32][33];
+  const int2 st = tl[blockIdx.x];
+  const int s = st.x, tile = st.y;
+  const DevSub sb = subs[s];
+  const int K = sb.k * n;
+  const int n4 = 4 * n;
+  const double2* T4 = T4s[sub_cls[s]];
+  const int* fc = sub_faces + 4 * s;
+  double2* out = T + sb.T_off + (long long)tile * K * kRowTile;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int c0 = 0; c0 < K; c0 += 32) {
+    // read rows (tile) x cols c0..c0+31 coalesced along columns
+    for (int a = warp; a < 32; a += 8) {
+      int r = tile * 32 + a;
+      int col = c0 + lane;
+      double2 v = make_double2(0, 0);
+      if (r < K && col < K) {
+        int gr = fc[r / n] * n + r % n;
+        int gc = fc[col / n] * n + col % n;
+        v = T4[(long long)gr * n4 + gc];
+      }
+      buf[a][lane] = v;
+    }
+    __syncthreads();
+    for (int cc = warp; cc < 32; cc += 8) {
+      int col = c0 + cc;
+      if (col < K) out[(long long)col * kRowTile + lane] = buf[lane][cc];
+    }
+    __syncthreads();
+  }
+}
+
+// Lifting traces of the home subdomain into b: b[m(j,home)] = coef * U_face(lift col).
+__global__ void k_lift_b(double2* b, const double2* G, int Rtot, int col0, int nrhs, int n,
+                         const int* face_tgt /*4: element offsets or -1*/, double2 coef) {
+  const int row = blockIdx.x;  // 0..4n
+  const int f = row / n, p = row - f * n;
+  const int off = face_tgt[f];
+  if (off < 0) return;
+  for (int j = threadIdx.x; j < nrhs; j += blockDim.x) {
+    double2 g = G[(long long)row * Rtot + col0 + j];
+    b[((long long)off + p) * nrhs + j] = cmul(coef, g);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host drivers
+
+static OpParams op_params(const Ctx& c) {
+  OpParams P;
+  P.n = c.n;
+  P.ih2 = 1.0 / (c.h * c.h);
+  // d = 1/h - tau/2, s = 1/h + tau/2, ratio = s/d (discretization.py:139-140, 245)
+  double dr = 1.0 / c.h - c.tau_re / 2, di = -c.tau_im / 2;
+  double sr = 1.0 / c.h + c.tau_re / 2, si = c.tau_im / 2;
+  double den = dr * dr + di * di;
+  double rr = (sr * dr + si * di) / den, ri = (si * dr - sr * di) / den;
+  P.dre = 4.0 * P.ih2 - c.kappa * c.kappa;
+  P.dim = 0;
+  P.gre = -P.ih2 * rr;
+  P.gim = -P.ih2 * ri;
+  return P;
+}
+
+// X_k = S_k^{-1} for all rows and all classes (batched over the classes).
+cudaError_t factor_blocks(Ctx& c, double2* X, long long xstride, const uint8_t* dmasks, int ncls,
+                          double2* Rp, double2* Cp, long long pstride, int* dbad) {
+  const int n = c.n;
+  OpParams P = op_params(c);
+  for (int k = 0; k < n; ++k) {
+    k_formS<<<dim3(n, ncls), 128, 0, c.stream>>>(X, xstride, dmasks, P, k);
+    for (int j0 = 0; j0 < n; j0 += 32) {
+      int nb = n - j0 < 32 ? n - j0 : 32;
+      k_gj_panel<<<dim3((n + 63) / 64, ncls), 256, 0, c.stream>>>(X, xstride, k, n, j0, nb, Rp, Cp,
+                                                                  pstride, dbad);
+      k_gj_update<<<dim3((n + 31) / 32, (n + 31) / 32, ncls), 256, 0, c.stream>>>(
+          X, xstride, k, n, j0, nb, Rp, Cp, pstride);
+    }
+  }
+  return cudaGetLastError();
+}
+
+void zgemm(cudaStream_t st, int M, int N, int K, double2 alpha, const double2* A, int lda,
+           long long sa, const double2* B, int ldb, long long sb, double2 beta, double2* C, int ldc,
+           long long sc, int batch) {
+  dim3 grid((N + 63) / 64, (M + 63) / 64, batch);
+  k_zgemm<<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, sa, B, ldb, sb, beta, C, ldc, sc);
+}
+
+// Solve the factored block-tridiagonal systems for R right-hand sides and
+// extract the boundary values G (4n x R) per class.
+cudaError_t solve_boundary(Ctx& c, const double2* X, long long xstride, const uint8_t* dmasks,
+                           int ncls, int R, int nunit, const ExtraRHS* extras, double2* Y,
+                           long long ystride, double2* Bk, long long bstride, double2* G,
+                           long long gstride) {
+  const int n = c.n;
+  const double ih2 = 1.0 / (c.h * c.h);
+  const long long nn = (long long)n * n;
+  const int rthreads = R < 256 ? ((R + 31) / 32) * 32 : 256;
+  for (int k = 0; k < n; ++k) {
+    k_rhs_fwd<<<dim3(n, ncls), rthreads, 0, c.stream>>>(Bk, bstride, Y, ystride, dmasks, n, R, nunit,
+                                                        ih2, k);
+    for (int cl = 0; cl < ncls; ++cl) {
+      const ExtraRHS& e = extras[cl];
+      if (e.row_ptr.empty()) continue;
+      int b0 = e.row_ptr[k], b1 = e.row_ptr[k + 1];
+      if (b1 > b0)
+        k_rhs_extra<<<(b1 - b0 + 255) / 256, 256, 0, c.stream>>>(Bk, bstride, R, e.d_x + b0,
+                                                                 e.d_col + b0, e.d_val + b0, b1 - b0,
+                                                                 cl);
+    }
+    zgemm(c.stream, n, R, n, make_double2(1, 0), X + k * nn, n, xstride, Bk, R, bstride,
+          make_double2(0, 0), Y + (long long)k * n * R, R, ystride, ncls);
+  }
+  for (int k = n - 2; k >= 0; --k) {
+    k_rhs_bwd<<<dim3(n, ncls), rthreads, 0, c.stream>>>(Bk, bstride, Y, ystride, dmasks, n, R, ih2, k);
+    zgemm(c.stream, n, R, n, make_double2(-1, 0), X + k * nn, n, xstride, Bk, R, bstride,
+          make_double2(1, 0), Y + (long long)k * n * R, R, ystride, ncls);
+  }
+  k_extract<<<dim3(4 * n, ncls), rthreads, 0, c.stream>>>(G, gstride, Y, ystride, n, R);
+  return cudaGetLastError();
+}
+
+void launch_make_T4(Ctx& c, double2* T4, const double2* G, int R, double2 a, double2 b) {
+  k_make_T4<<<4 * c.n, 256, 0, c.stream>>>(T4, G, 4 * c.n, R, a, b);
+}
+
+void launch_scatter_T(Ctx& c, const int2* tl, int ntiles, const int* sub_faces, const int* sub_cls,
+                      double2* const* T4s) {
+  if (ntiles > 0)
+    k_scatter_T<<<ntiles, 256, 0, c.stream>>>(tl, c.dsubs, sub_faces, sub_cls, T4s, c.T, c.n);
+}
+
+void launch_lift_b(Ctx& c, double2* b, const double2* G, int Rtot, int col0, int nrhs,
+                   const int* face_tgt, double2 coef) {
+  int th = nrhs < 32 ? 32 : (nrhs > 256 ? 256 : nrhs);
+  k_lift_b<<<4 * c.n, th, 0, c.stream>>>(b, G, Rtot, col0, nrhs, c.n, face_tgt, coef);
+}
+
+}  // namespace hs

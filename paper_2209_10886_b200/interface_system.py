@@ -1,0 +1,340 @@
+"""The interface problem (I - S) g = b on the GPU, with the reference API.
+
+`GpuInterfaceSystem(spec, partition, imp=None, workers=1, ...)` is the drop-in
+for `InterfaceSystem` (interface_system.py:65-175): same constructor
+arguments, attributes (`spec`, `partition`, `imp`, `layout`, `operators`)
+and methods (`compute_liftings`, `assemble_rhs`, `apply_scattering`,
+`apply_interface_operator`, `restricted_apply`, `materialize_dense`), plus
+the specified-but-unshipped preconditioner and GMRES entry points
+(SPEC.md:306-407).  Every numerical operation runs in libhsb200 on the GPU:
+one batched kernel per sweep step over all subdomains of the step.
+
+Vectors are numpy complex128 (host; copied in/out inside the call) or torch
+complex128 CUDA tensors (device; zero-copy), of shape (L,) or (L, R) for R
+right-hand sides; results come back as the same kind.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import native
+from .discretization import ImpedanceSpec, SubdomainInfo, lifting_data, scatterer_cells
+from .indexing import MultiIndex, Partition, window_ranges
+
+DENSE_GUARD = 6000
+
+
+class TraceLayout:
+    """interface_system.py:30-62: 2 N_e blocks of n in m-order."""
+
+    def __init__(self, partition: Partition, n: int):
+        self.partition = partition
+        self.n = n
+        self.size = len(partition.pairs) * n
+
+    def zeros(self) -> np.ndarray:
+        return np.zeros(self.size, dtype=complex)
+
+    def block(self, m: int) -> slice:
+        return slice((m - 1) * self.n, m * self.n)
+
+    def block_of(self, owner, neighbor) -> slice:
+        return self.block(self.partition.m_index((owner, neighbor)))
+
+    def group_indices(self, groups) -> np.ndarray:
+        groups = set(groups)
+        ms = [m for m, p in enumerate(self.partition.pairs, start=1) if p.owner.group in groups]
+        if not ms:
+            return np.empty(0, dtype=np.intp)
+        return np.concatenate([np.arange((m - 1) * self.n, m * self.n) for m in ms])
+
+    def check(self, g):
+        shape = tuple(getattr(g, "shape", np.shape(g)))
+        if len(shape) == 0 or shape[0] != self.size or len(shape) > 2:
+            n = shape[0] if shape else 0
+            raise ValueError(f"interface vector has length {n}, expected {self.size}")
+        return g
+
+
+@dataclass
+class SweepConfig:
+    """SPEC.md:296-299 (+ the block count of SURVEY.md §8d)."""
+
+    kind: str = "bsp"  # none | sp | bsp
+    bsp_seam: str = "dedup"
+    bsp_intermediate_residual: bool = True
+    count_residual_steps: bool = False
+    blocks: int | None = None
+
+
+@dataclass
+class GmresOptions:
+    tol: float = 1e-6
+    maxit: int = 200
+    record_history: bool = True
+
+
+@dataclass
+class GmresResult:
+    solution: object
+    history: list = field(default_factory=list)
+    iterations: int = 0
+    converged: bool = False
+    wall_time: float = 0.0
+
+
+_PC = {"none": native.HS_PC_NONE, "sp": native.HS_PC_SP, "bsp": native.HS_PC_BSP}
+
+
+class _Vec:
+    """Caller buffer <-> (pointer, mem kind, output allocator)."""
+
+    def __init__(self, x, L):
+        self.torch = None
+        try:
+            import torch
+            if isinstance(x, torch.Tensor):
+                self.torch = torch
+        except ImportError:  # pragma: no cover
+            pass
+        if self.torch is not None:
+            t = x
+            if t.dtype != self.torch.complex128:
+                t = t.to(self.torch.complex128)
+            t = t.contiguous()
+            self.cpu = not t.is_cuda
+            if self.cpu:
+                self.arr = np.ascontiguousarray(t.numpy())
+            else:
+                self.torch.cuda.current_stream(t.device).synchronize()
+                self.t = t
+        else:
+            self.cpu = True
+            self.arr = np.ascontiguousarray(np.asarray(x), dtype=np.complex128)
+        shape = self.arr.shape if self.cpu else tuple(self.t.shape)
+        if len(shape) not in (1, 2) or shape[0] != L:
+            raise ValueError(f"interface vector has length {shape[0] if shape else 0}, expected {L}")
+        self.shape = shape
+        self.R = 1 if len(shape) == 1 else shape[1]
+
+    @property
+    def ptr(self):
+        return self.arr.ctypes.data if self.cpu else self.t.data_ptr()
+
+    @property
+    def mem(self):
+        return native.HS_MEM_HOST if self.cpu else native.HS_MEM_DEVICE
+
+    def empty(self):
+        if self.cpu:
+            out = np.empty(self.shape, dtype=np.complex128)
+            return out, out.ctypes.data
+        out = self.torch.empty(self.shape, dtype=self.torch.complex128, device=self.t.device)
+        return out, out.data_ptr()
+
+    def wrap(self, out):
+        if self.torch is not None and self.cpu:
+            return self.torch.from_numpy(out)
+        return out
+
+
+class GpuInterfaceSystem:
+    """Subdomain Schur maps + matrix-free S on one GPU (or one row band)."""
+
+    def __init__(self, spec, partition: Partition, imp: ImpedanceSpec | None = None, workers: int = 1,
+                 device: int = 0, rank: int = 0, nranks: int = 1, nccl_id: bytes | None = None,
+                 sweep: SweepConfig | None = None):
+        if workers < 1:
+            raise ValueError(f"workers must be >= 1, got {workers}")
+        self.spec = spec
+        self.partition = partition
+        self.imp = imp if imp is not None else ImpedanceSpec.for_problem(spec)
+        self.workers = workers  # accepted for API parity; the GPU batches every solve of a step
+        self.layout = TraceLayout(partition, spec.cells_per_side)
+        self.n = spec.cells_per_side
+        self.rank, self.nranks = rank, nranks
+        self.ctx = native.Context(device, partition.n1, partition.n2, self.n, spec.h, spec.kappa,
+                                  complex(self.imp.coefficient), rank, nranks)
+        if nranks > 1:
+            if nccl_id is None:
+                raise ValueError("a sharded system needs the NCCL unique id of rank 0")
+            buf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+            self.ctx.call("hs_comm_init", buf)
+        self.home, cells = scatterer_cells(spec, partition)
+        if self.home is not None:
+            c = native.i32(cells)
+            self.ctx.call("hs_set_dirichlet", self.home.i1, self.home.i2, native.iptr(c), len(c))
+        t0 = time.perf_counter()
+        self.ctx.call("hs_factor")
+        self.setup_time = time.perf_counter() - t0
+        self._operators = None
+        self.sweep = SweepConfig()
+        self.configure(sweep or SweepConfig())
+
+    # ---- reference attributes
+    @property
+    def operators(self):
+        if self._operators is None:
+            self._operators = {i: SubdomainInfo.build(self.spec, self.imp, self.partition, i)
+                               for i in self.partition.subdomains}
+        return self._operators
+
+    def configure(self, sweep: SweepConfig):
+        """Windows and seam/residual options of the preconditioner."""
+        P = self.partition
+        for k, kind in ((0, "lower"), (1, "upper")):
+            w = window_ranges(P.n1, P.n2, kind, sweep.blocks)
+            lo, hi = native.i32([a for a, _ in w]), native.i32([b for _, b in w])
+            self.ctx.call("hs_set_windows", k, native.iptr(lo), native.iptr(hi), len(w))
+        seam = native.HS_SEAM_LITERAL if sweep.bsp_seam == "literal" else native.HS_SEAM_DEDUP
+        if sweep.bsp_seam not in ("dedup", "literal"):
+            raise ValueError(f"bsp_seam must be 'dedup' or 'literal', got {sweep.bsp_seam!r}")
+        self.ctx.call("hs_set_precond_options", seam, int(bool(sweep.bsp_intermediate_residual)))
+        self.sweep = sweep
+
+    def _call_io(self, fn, g, pre=(), post=()):
+        v = _Vec(self.layout.check(g), self.layout.size)
+        out, optr = v.empty()
+        self.ctx.call(fn, *pre, C.c_void_p(v.ptr), C.c_void_p(optr), v.R, *post, v.mem)
+        return v.wrap(out)
+
+    # ---- interface_system.py:98-162
+    def compute_liftings(self, directions=None):
+        """Lifting traces of the scatterer subdomain -> b (discretization.py:315-332,
+        interface_system.py:98-113).  `directions`: list of incident directions for
+        several right-hand sides (config 4)."""
+        return {"b": self.rhs(directions), "directions": directions}
+
+    def assemble_rhs(self, liftings) -> np.ndarray:
+        return np.array(liftings["b"], copy=True)
+
+    def rhs(self, directions=None) -> np.ndarray:
+        home, data = lifting_data(self.spec, self.partition, directions)
+        R = data.shape[1]
+        out = np.zeros((self.layout.size, R), dtype=np.complex128)
+        if home is not None:
+            d = np.ascontiguousarray(data, dtype=np.complex128)
+            self.ctx.call("hs_lifting_rhs", C.c_void_p(d.ctypes.data), R, C.c_void_p(out.ctypes.data),
+                          native.HS_MEM_HOST)
+        return out[:, 0] if directions is None else out
+
+    def apply_scattering(self, g):
+        return self._call_io("hs_apply", g, pre=(native.HS_APPLY_S,))
+
+    def apply_interface_operator(self, g):
+        return self._call_io("hs_apply", g, pre=(native.HS_APPLY_IMS,))
+
+    def restricted_apply(self, g, source_groups, target_groups):
+        src, tgt = native.i32(sorted(set(source_groups))), native.i32(sorted(set(target_groups)))
+        v = _Vec(self.layout.check(g), self.layout.size)
+        out, optr = v.empty()
+        self.ctx.call("hs_restricted_apply", C.c_void_p(v.ptr), C.c_void_p(optr), v.R,
+                      native.iptr(src), len(src), native.iptr(tgt), len(tgt), v.mem)
+        return v.wrap(out)
+
+    def materialize_dense(self) -> np.ndarray:
+        size = self.layout.size
+        if size > DENSE_GUARD:
+            raise ValueError(f"dense guard exceeded: {size} > {DENSE_GUARD}")
+        out = np.zeros((size, size), dtype=complex)
+        for c0 in range(0, size, 512):
+            c1 = min(size, c0 + 512)
+            R = 1 << (c1 - c0 - 1).bit_length()
+            E = np.zeros((size, R), dtype=complex)
+            E[np.arange(c0, c1), np.arange(c1 - c0)] = 1.0
+            out[:, c0:c1] = self.apply_scattering(E)[:, :c1 - c0]
+        return out
+
+    def schur_map(self, i) -> np.ndarray:
+        """Compact (k n) x (k n) map of subdomain i (faces W,S,N,E)."""
+        i = MultiIndex(*i)
+        k = len(self.partition.neighbors[i])
+        K = k * self.n
+        T = np.zeros((K, K), dtype=np.complex128)
+        self.ctx.call("hs_get_schur", i.i1, i.i2, C.c_void_p(T.ctypes.data))
+        return T
+
+    # ---- SPEC.md:306-348
+    def precondition(self, r, kind: str | None = None):
+        kind = self.sweep.kind if kind is None else kind
+        return self._call_io("hs_precond", r, pre=(_PC[kind],))
+
+    def bsp_apply(self, b):
+        return self.precondition(b, "bsp")
+
+    def sgs_apply(self, r):
+        return self.precondition(r, "sp")
+
+    def bj_half_apply(self, r, direction: str):
+        d = {"forward": 0, "backward": 1}[direction]
+        return self._call_io("hs_half_apply", r, pre=(d,))
+
+    def _single_window(self):
+        ng = self.partition.n_groups
+        one = native.i32([2]), native.i32([ng + 1])
+        for k in (0, 1):
+            self.ctx.call("hs_set_windows", k, native.iptr(one[0]), native.iptr(one[1]), 1 if ng >= 2 else 0)
+
+    def forward_sweep(self, r):
+        self._single_window()
+        try:
+            return self.bj_half_apply(r, "forward")
+        finally:
+            self.configure(self.sweep)
+
+    def backward_sweep(self, r):
+        self._single_window()
+        try:
+            return self.bj_half_apply(r, "backward")
+        finally:
+            self.configure(self.sweep)
+
+    def step_schedule(self, kind: str | None = None):
+        """[(step, phase, [MultiIndex])]."""
+        kind = self.sweep.kind if kind is None else kind
+        return schedule_records(self.ctx, self.partition, kind, self.sweep)
+
+    # ---- SPEC.md:399-407 on the device
+    def gmres(self, b, kind: str | None = None, tol: float = 1e-6, maxit: int = 200) -> GmresResult:
+        kind = self.sweep.kind if kind is None else kind
+        v = _Vec(self.layout.check(b), self.layout.size)
+        out, optr = v.empty()
+        R = v.R
+        iters = np.zeros(R, dtype=np.int32)
+        conv = np.zeros(R, dtype=np.int32)
+        hist = np.zeros((maxit + 1, R), dtype=np.float64)
+        t0 = time.perf_counter()
+        self.ctx.call("hs_gmres", _PC[kind], C.c_void_p(v.ptr), C.c_void_p(optr), R, float(tol), int(maxit),
+                      native.iptr(iters), hist.ctypes.data_as(C.POINTER(C.c_double)), native.iptr(conv), v.mem)
+        wall = time.perf_counter() - t0
+        if R == 1:
+            h = list(hist[:iters[0] + 1, 0]) if iters[0] > 0 else []
+            return GmresResult(v.wrap(out), h, int(iters[0]), bool(conv[0]), wall)
+        return GmresResult(v.wrap(out), [list(hist[:iters[r] + 1, r]) for r in range(R)], iters.tolist(),
+                           conv.astype(bool).tolist(), wall)
+
+
+InterfaceSystem = GpuInterfaceSystem
+
+
+def schedule_records(ctx, partition, kind, sweep):
+    recs = []
+    subs = partition.subdomains
+    raw = ctx.schedule(_PC[kind])
+    phases = {0: "forward", 1: "residual", 2: "backward"}
+    cur = None
+    for step, ph, s in raw:
+        if cur is None or cur[0] != step:
+            cur = (int(step), phases[int(ph)], [])
+            recs.append(cur)
+        cur[2].append(subs[int(s)])
+    if kind == "bsp" and sweep.bsp_intermediate_residual and sweep.count_residual_steps:
+        nf = sum(1 for r in recs if r[1] == "forward")
+        res = (nf + 1, "residual", list(subs))
+        recs = recs[:nf] + [res] + [(t + 1, ph, ss) for t, ph, ss in recs[nf:]]
+    return recs

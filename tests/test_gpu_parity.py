@@ -1,0 +1,174 @@
+"""GPU parity: libhsb200 (through the reference-shaped API / C ABI) against the
+oracle and the golden vectors produced by the real reference.
+
+Tolerances (relative L2 unless stated):
+  * Schur maps vs the accurate CPU oracle (Dirichlet-eliminated SuperLU): 1e-11
+  * S g, (I-S) g, restricted blocks vs reference goldens: 1e-10 (the
+    reference's own SuperLU error on the scatterer subdomain is 1e-11..4e-11
+    at n = 32..64)
+  * SP / BSP applies vs the SPEC restatement on the reference S: 1e-10
+  * GMRES: iterations within +-1 (exact expected), x within 1e-8, final
+    true relative residual < tol (BASELINE.json north_star).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import cvec, golden, oracle_problem, product_problem, relerr
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2209_10886_b200.configs import CONFIGS, small_case  # noqa: E402
+from paper_2209_10886_b200.interface_system import GpuInterfaceSystem, SweepConfig  # noqa: E402
+
+CASES = {
+    "small_2x2": small_case(2, 2, 8),
+    "small_3x3": small_case(3, 3, 8),
+    "small_3x2": small_case(3, 2, 12),
+    "small_1x4": small_case(1, 4, 8),
+    "cfg1": CONFIGS[1],
+    "cfg2": CONFIGS[2],
+}
+
+_SYS = {}
+
+
+def system(name, sweep=None):
+    key = name
+    if key not in _SYS:
+        spec, part = product_problem(CASES[name])
+        _SYS[key] = GpuInterfaceSystem(spec, part)
+    s = _SYS[key]
+    s.configure(sweep or SweepConfig(blocks=CASES[name].get("blocks")))
+    return s
+
+
+@pytest.mark.parametrize("name", ["small_2x2", "small_3x3", "small_3x2", "cfg1", "cfg2"])
+def test_schur_maps_vs_oracle(name):
+    from oracle.schur import schur_maps_for
+    c = CASES[name]
+    prob, lat = oracle_problem(c)
+    s = system(name)
+    picks = [lat.subs[0], lat.subs[len(lat.subs) // 2], lat.subs[-1]]
+    if prob.home(lat) is not None:
+        picks.append(prob.home(lat))
+    ref = schur_maps_for(prob, lat, picks)
+    for sub in picks:
+        T = s.schur_map(sub)
+        assert T.shape == ref[sub].shape
+        assert relerr(T, ref[sub]) < 1e-11, (sub, relerr(T, ref[sub]))
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_apply_vs_reference_golden(name):
+    G = golden(name)
+    s = system(name)
+    assert relerr(s.apply_scattering(G["g"]), G["Sg"]) < 1e-10
+    assert relerr(s.apply_interface_operator(G["g"]), G["Ag"]) < 1e-10
+    for key in G.files:
+        if key.startswith("R_"):
+            _, a, b = key.split("_")
+            out = s.restricted_apply(G["g"], {int(a)}, {int(b)})
+            assert relerr(out, G[key]) < 1e-10, key
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_rhs_vs_reference_golden(name):
+    G = golden(name)
+    s = system(name)
+    assert relerr(s.rhs(), G["b"]) < 1e-10
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_preconditioners_vs_golden(name):
+    G = golden(name)
+    c = CASES[name]
+    s = system(name)
+    r = G["r"]
+    assert relerr(s.sgs_apply(r), G["M_sp"]) < 1e-10
+    s.configure(SweepConfig())
+    assert relerr(s.bsp_apply(r), G["M_bsp"]) < 1e-10
+    assert relerr(s.bj_half_apply(r, "forward"), G["half_fwd"]) < 1e-10
+    assert relerr(s.bj_half_apply(r, "backward"), G["half_bwd"]) < 1e-10
+    s.configure(SweepConfig(bsp_seam="literal"))
+    assert relerr(s.bsp_apply(r), G["M_bsp_literal"]) < 1e-10
+    s.configure(SweepConfig(bsp_intermediate_residual=False))
+    assert relerr(s.bsp_apply(r), G["M_bsp_nores"]) < 1e-10
+    s.configure(SweepConfig(blocks=1))
+    assert relerr(s.bsp_apply(r), G["M_bsp1"]) < 1e-10
+    if c.get("blocks"):
+        s.configure(SweepConfig(blocks=c["blocks"]))
+        assert relerr(s.bsp_apply(r), G[f"M_bsp{c['blocks']}"]) < 1e-10
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_gmres_vs_golden(name):
+    G = golden(name)
+    c = CASES[name]
+    s = system(name, SweepConfig(blocks=c.get("blocks")))
+    b = G["b"]
+    res = s.gmres(b, "bsp", tol=1e-6, maxit=1000)
+    assert abs(res.iterations - int(G["gm_iters"])) <= 1, (res.iterations, int(G["gm_iters"]))
+    assert res.converged
+    assert relerr(res.solution, G["gm_x"]) < 1e-8
+    true_res = relerr(s.apply_interface_operator(res.solution), b)
+    assert true_res < 1e-6
+    n = min(len(res.history), len(G["gm_hist"]))
+    np.testing.assert_allclose(res.history[:n], G["gm_hist"][:n], rtol=1e-6, atol=1e-12)
+
+
+def test_multi_rhs_matches_single():
+    s = system("cfg1")
+    L = s.layout.size
+    X = cvec(11, L, 8)
+    Y = s.apply_scattering(X)
+    for r in range(8):
+        assert relerr(Y[:, r], s.apply_scattering(np.ascontiguousarray(X[:, r]))) < 1e-14
+    Z = s.bsp_apply(X)
+    for r in (0, 5):
+        assert relerr(Z[:, r], s.bsp_apply(np.ascontiguousarray(X[:, r]))) < 1e-13
+
+
+def test_torch_device_io_zero_copy():
+    s = system("cfg1")
+    g = cvec(3, s.layout.size)
+    gt = torch.from_numpy(g).cuda()
+    out = s.apply_interface_operator(gt)
+    assert out.is_cuda and out.dtype == torch.complex128
+    assert relerr(out.cpu().numpy(), s.apply_interface_operator(g)) < 1e-15
+    z = s.bsp_apply(gt)
+    assert relerr(z.cpu().numpy(), s.bsp_apply(g)) < 1e-15
+
+
+def test_determinism_bitwise():
+    s = system("cfg2")
+    g = cvec(5, s.layout.size)
+    a = s.bsp_apply(g)
+    b = s.bsp_apply(g)
+    assert np.array_equal(a, b)
+    r1 = s.gmres(s.rhs(), "bsp", tol=1e-6, maxit=200)
+    r2 = s.gmres(s.rhs(), "bsp", tol=1e-6, maxit=200)
+    assert np.array_equal(r1.solution, r2.solution) and r1.iterations == r2.iterations
+
+
+def test_degenerate_1x1():
+    spec, part = product_problem(small_case(1, 1, 8))
+    s = GpuInterfaceSystem(spec, part)
+    assert s.layout.size == 0
+    res = s.gmres(np.zeros(0, dtype=complex), "bsp")
+    assert res.iterations == 0 and res.converged
+
+
+def test_no_scatterer_zero_rhs():
+    c = dict(small_case(2, 2, 8))
+    c["center"] = None
+    spec, part = product_problem(c)
+    s = GpuInterfaceSystem(spec, part)
+    b = s.rhs()
+    assert np.all(b == 0)
+    res = s.gmres(b, "bsp")
+    assert res.iterations == 0 and np.all(res.solution == 0)
