@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 hot path (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl ours|reference]
+
+A *step* is one block-Jacobi sweeping-preconditioner (BSP) apply z = M r over
+one synthetic interface vector (seeded complex normal) of the configured
+problem -- by default BASELINE config 5 (32x16 subdomains of 256x256 cells,
+8 blocks, 7.9 GB of Schur maps: far larger than the 126 MB L2, so no flush
+is needed between steps).  `value` is applies/s of the whole job with the
+vector resident in HBM (CUDA events on the library's stream, max over
+ranks); `e2e` is the same through the C ABI with pinned host buffers
+(host->device copy of r and device->host copy of z inside every step).
+The line also reports the roofline of the dominant kernel (the batched
+step-apply, timed per launch with CUDA events), GMRES time-to-solution, the
+CPU baseline (the oracle port of the reference path on the host cores) and
+the SM clocks seen during the timed region.
+
+`--impl reference` times the reference algorithm on the host cores instead
+(oracle port: SciPy SuperLU subdomain solves, all cores via a process pool),
+as a bounded sample per step projected to applies/s.
+Under torchrun with N > 1 the subdomain rows are sharded over the ranks
+(strong scaling: the apply is split; traces cross band edges over NCCL).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GMRES time-to-solution; preconditioner applies/s and % of HBM roofline"
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def problem(cfgno):
+    from paper_2209_10886_b200.configs import CONFIGS
+    from paper_2209_10886_b200.discretization import ProblemSpec, Scatterer
+    from paper_2209_10886_b200.indexing import Partition
+    c = CONFIGS[cfgno]
+    ang = c["angle"] if c["angle"] is not None else 0.0
+    spec = ProblemSpec(kappa=c["kappa"], cells_per_side=c["n"], subdomain_side=c["side"],
+                       scatterer=Scatterer(tuple(c["center"]), c["radius"]),
+                       incident_direction=(float(np.cos(ang)), float(np.sin(ang))))
+    return c, spec, Partition(c["n1"], c["n2"])
+
+
+def config_json(c, world):
+    return {"workload": f"{c['name']}: BSP apply, {c['n1']}x{c['n2']} subdomains of {c['n']}x{c['n']} cells, "
+                        f"{'reference' if c['blocks'] is None else c['blocks']} blocks, {c['nrhs']} RHS",
+            "lattice": [c["n1"], c["n2"]], "cells_per_side": c["n"], "grid": [c["n1"] * c["n"], c["n2"] * c["n"]],
+            "kappa": c["kappa"], "blocks": c["blocks"], "nrhs": c["nrhs"], "tol": c["tol"],
+            "parallelism": f"rowbands{world}" if world > 1 else "single",
+            "l2": "inputs larger than L2 (Schur maps 7.9 GB at cfg5 >> 126 MB); no flush" if c["n"] >= 128
+                  else "L2 flushed between steps"}
+
+
+# ---------------------------------------------------------------- clocks
+class Clocks:
+    def __init__(self, dev):
+        self.p = None
+        self.dev = dev
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(dev), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.p.terminate()
+        try:
+            out, _ = self.p.communicate(timeout=5)
+        except Exception:
+            self.p.kill()
+            out = ""
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- CPU baseline (oracle port)
+def _cpu_worker_init(cfgno):
+    global _W
+    from paper_2209_10886_b200.configs import CONFIGS
+    from oracle.fd import Problem, Subdomain
+    from oracle.lattice import Lattice
+    c = CONFIGS[cfgno]
+    prob = Problem(kappa=c["kappa"], n=c["n"], side=c["side"], center=tuple(c["center"]), radius=c["radius"])
+    lat = Lattice(c["n1"], c["n2"])
+    sub = (c["n1"] // 2 + 1, c["n2"] // 2 - 1) if c["n2"] > 3 else lat.subs[0]  # interior, no scatterer
+    op = Subdomain(prob, lat, sub)
+    rng = np.random.default_rng(0)
+    tr = {f: rng.standard_normal(c["n"]) + 1j * rng.standard_normal(c["n"]) for f in op.iface}
+    _W = (op, tr)
+
+
+def _cpu_worker_solves(nsolves):
+    op, tr = _W
+    t0 = time.perf_counter()
+    for _ in range(nsolves):
+        u = op.solve(tr)
+        for f in op.iface:
+            op.outgoing(u, tr[f], f)
+    return nsolves, time.perf_counter() - t0
+
+
+def solves_per_apply(system):
+    """Subdomain solves of one BSP apply in the reference path: one per item of
+    every forward/backward step (schedule) plus N_dom for the residual."""
+    recs = system.step_schedule("bsp")
+    return sum(len(s) for _, _, s in recs) + system.partition.n_subdomains
+
+
+def cpu_baseline(cfgno, n_solves_apply, budget_s=20.0):
+    """Single-core sample of the reference arithmetic (SuperLU solve + outgoing
+    traces of one interior subdomain), projected to one BSP apply."""
+    t0 = time.perf_counter()
+    _cpu_worker_init(cfgno)
+    t_fac = time.perf_counter() - t0
+    n, dt = _cpu_worker_solves(1)
+    k = max(1, int(budget_s / max(dt, 1e-4)) - 1)
+    k = min(k, 400)
+    n2, dt2 = _cpu_worker_solves(k)
+    t_solve = dt2 / n2
+    return {"value": 1.0 / (n_solves_apply * t_solve), "unit": "applies/s", "cores": 1, "kind": "port",
+            "sample": f"{n2} SuperLU solves + outgoing traces of one interior subdomain "
+                      f"({t_solve * 1e3:.2f} ms each; factor {t_fac:.2f} s), projected to one BSP apply = "
+                      f"{n_solves_apply} subdomain solves",
+            "t_solve_s": t_solve}
+
+
+def run_reference(args):
+    """--impl reference: the reference path (oracle port) on all host cores."""
+    rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)
+    if rank != 0:
+        return 0
+    import multiprocessing as mp
+    from paper_2209_10886_b200.configs import CONFIGS
+    c = CONFIGS[args.config]
+    from oracle.lattice import Lattice
+    from oracle.sweeps import step_schedule as _  # noqa: F401  (schedule below is structural)
+    from paper_2209_10886_b200.indexing import window_ranges
+    lat = Lattice(c["n1"], c["n2"])
+    nfw = sum(len([s for s in lat.subs if s[0] + s[1] == lo + t - 1])
+              for lo, hi in window_ranges(c["n1"], c["n2"], "lower", c["blocks"]) for t in range(1, hi - lo + 1))
+    nbw = sum(len([s for s in lat.subs if s[0] + s[1] == hi - t + 1])
+              for lo, hi in window_ranges(c["n1"], c["n2"], "upper", c["blocks"]) for t in range(1, hi - lo + 1))
+    nsol = nfw + nbw + len(lat.subs)
+    procs = os.cpu_count() or 1
+    ctx = mp.get_context("fork")
+    with ctx.Pool(procs, initializer=_cpu_worker_init, initargs=(args.config,)) as pool:
+        pool.map(_cpu_worker_solves, [1] * procs)
+        t0 = time.perf_counter()
+        pool.map(_cpu_worker_solves, [1] * procs)
+        per = max(1, int(1.5 / max((time.perf_counter() - t0), 1e-3)))
+        for _ in range(args.warmup):
+            pool.map(_cpu_worker_solves, [per] * procs)
+        times = []
+        total = 0
+        for _ in range(args.steps):
+            t0 = time.perf_counter()
+            res = pool.map(_cpu_worker_solves, [per] * procs)
+            times.append(time.perf_counter() - t0)
+            total += sum(r[0] for r in res)
+    wall = sum(times)
+    solves_s = total / wall
+    value = solves_s / nsol
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "applies/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / len(times),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic", "config": config_json(c, 1),
+            "cpu_baseline": {"value": value, "unit": "applies/s", "cores": procs, "kind": "port",
+                             "sample": f"each step: {procs} processes x {per} SuperLU solves + outgoing traces of "
+                                       f"an interior {c['n']}x{c['n']} subdomain; applies/s = solves/s / {nsol} "
+                                       f"solves per BSP apply"},
+            "e2e": {"value": value, "unit": "applies/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-gmres", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import ctypes as C
+    import torch
+    from paper_2209_10886_b200 import native
+    from paper_2209_10886_b200.interface_system import GpuInterfaceSystem, SweepConfig
+
+    rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)
+    local = env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    dist = None
+    nccl_id = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        obj = [native.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+
+    c, spec, part = problem(args.config)
+    sweep = SweepConfig(blocks=c["blocks"])
+    t0 = time.perf_counter()
+    system = GpuInterfaceSystem(spec, part, device=local, rank=rank, nranks=world, nccl_id=nccl_id, sweep=sweep)
+    setup_s = time.perf_counter() - t0
+    ctx = system.ctx
+    L = system.layout.size
+    gen = torch.Generator(device="cpu").manual_seed(1234)
+    r_host = torch.complex(torch.randn(L, generator=gen, dtype=torch.float64),
+                           torch.randn(L, generator=gen, dtype=torch.float64))
+    r = r_host.cuda()
+    z = torch.empty_like(r)
+    torch.cuda.synchronize()
+    stream = torch.cuda.ExternalStream(ctx.stream())
+    ctx.call("hs_set_async", 1)
+
+    def apply_dev():
+        ctx.call("hs_precond", native.HS_PC_BSP, C.c_void_p(r.data_ptr()), C.c_void_p(z.data_ptr()), 1,
+                 native.HS_MEM_DEVICE)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    for _ in range(max(args.warmup, 3)):
+        apply_dev()
+    ctx.call("hs_sync")
+    ctx.kernel_stats(reset=True)
+    ctx.call("hs_set_kernel_timing", 1)
+    barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    time.sleep(0.25)
+    l0 = ctx.launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        apply_dev()
+    ev1.record(stream)
+    ev1.synchronize()
+    launches = ctx.launches() - l0
+    clk = clocks.stop()
+    barrier()
+    torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1)
+    ctx.call("hs_set_kernel_timing", 0)
+    kl, kms, kbytes = ctx.kernel_stats(reset=True)
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per = ms / args.steps
+    value = 1e3 / ms_per
+
+    # roofline of the step-apply kernel
+    peak, peak_kind = load_peaks()
+    ach = (kbytes / (kms * 1e-3)) / 1e9 if kms > 0 else None
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"ncu_step_kernel_cfg{args.config}.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    share = kms / ms if ms > 0 else None
+
+    # e2e through the C ABI with pinned host buffers
+    rh = r_host.numpy().copy()
+    r_pin = torch.from_numpy(rh).pin_memory()
+    z_pin = torch.empty_like(r_pin).pin_memory()
+    ctx.call("hs_set_async", 0)
+
+    def apply_host():
+        ctx.call("hs_precond", native.HS_PC_BSP, C.c_void_p(r_pin.data_ptr()), C.c_void_p(z_pin.data_ptr()), 1,
+                 native.HS_MEM_HOST)
+
+    for _ in range(2):
+        apply_host()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ke = max(3, args.steps // 3)
+    e0.record(stream)
+    for _ in range(ke):
+        apply_host()
+    e1.record(stream)
+    e1.synchronize()
+    ems = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ems], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ems = float(t.item())
+    e2e = {"value": 1e3 * ke / ems, "unit": "applies/s", "h2d_bytes_per_step": int(L * 16),
+           "d2h_bytes_per_step": int(L * 16)}
+
+    # GMRES time-to-solution (single GPU; GMRES phase only)
+    gm = None
+    if world == 1 and not args.no_gmres:
+        b = system.rhs()
+        system.gmres(b, "bsp", tol=c["tol"], maxit=1000)  # warm (workspace allocation)
+        t1 = time.perf_counter()
+        res = system.gmres(b, "bsp", tol=c["tol"], maxit=1000)
+        tts = time.perf_counter() - t1
+        true_res = float(np.linalg.norm(system.apply_interface_operator(res.solution) - b) / np.linalg.norm(b))
+        gm = {"time_to_solution_s": tts, "iterations": res.iterations, "converged": res.converged,
+              "true_relative_residual": true_res, "setup_s": setup_s}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(args.config, solves_per_apply(system))
+        except Exception as e:  # report, do not fail the bench
+            cpu = {"value": None, "unit": "applies/s", "cores": 1, "kind": "port", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "applies/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+                "config": config_json(c, world),
+                "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                             "frac": (ach / peak) if ach else None, "traffic": traffic,
+                             "kernel": "k_step1 (batched step-apply ZGEMV)", "peak_source": peak_kind,
+                             "launches": kl, "kernel_ms_share_of_step": share,
+                             "algorithmic_bytes_per_apply": kbytes / max(args.steps, 1)},
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+                "gmres": gm, "setup_s": setup_s}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

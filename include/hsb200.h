@@ -156,6 +156,8 @@ int hs_stream(hs_ctx* ctx, uint64_t* stream);
  * step-apply kernels since the last reset. */
 int hs_set_kernel_timing(hs_ctx* ctx, int on);
 int hs_kernel_stats(hs_ctx* ctx, int64_t* launches, double* ms, double* bytes, int reset);
+/* Number of kernels this context has launched (all kinds). */
+int hs_launch_count(const hs_ctx* ctx, int64_t* n);
 /* Bytes of device memory held by the context. */
 int hs_memory(const hs_ctx* ctx, int64_t* bytes);
 

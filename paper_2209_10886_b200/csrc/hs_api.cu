@@ -1039,6 +1039,12 @@ int hs_kernel_stats(hs_ctx* c, int64_t* launches, double* ms, double* bytes, int
   return 0;
 }
 
+int hs_launch_count(const hs_ctx* c, int64_t* n) {
+  if (!c) return 1;
+  *n = c->launches;
+  return 0;
+}
+
 int hs_memory(const hs_ctx* c, int64_t* bytes) {
   if (!c) return 1;
   *bytes = c->dev_bytes;

@@ -178,9 +178,11 @@ void launch_step(Ctx& c, const DevStep& st, const double2* srcA, const double2* 
     if (R == 1) {
       constexpr int NW = 8;
       size_t smem = (size_t)(st.maxK + NW * 32) * sizeof(double2);
+      c.launches++;
       k_step1<NW><<<st.ntiles, NW * 32, smem, c.stream>>>(st.tiles, st.items, c.dsubs, c.T, srcA,
                                                           srcB, e, c.n);
     } else {
+      c.launches++;
       k_stepR<<<st.ntiles, 256, 0, c.stream>>>(st.tiles, st.items, c.dsubs, c.T, srcA, srcB, e,
                                               c.n, R);
     }
@@ -190,6 +192,7 @@ void launch_step(Ctx& c, const DevStep& st, const double2* srcA, const double2* 
 void launch_recv_epi(Ctx& c, const DevStep& st, const Epi& e, int R) {
   if (st.nrecv == 0) return;
   long long len = (long long)st.nrecv * c.n * R;
+  c.launches++;
   k_recv_epi<<<grid_for(len, c.num_sms), 256, 0, c.stream>>>(st.recv, st.nrecv, c.recv_dn,
                                                              c.recv_up, e, c.n, R);
 }
@@ -197,12 +200,14 @@ void launch_recv_epi(Ctx& c, const DevStep& st, const Epi& e, int R) {
 void launch_vec(Ctx& c, int op, long long len, double2* o1, double2* o2, const double2* a,
                 const double2* b) {
   if (len <= 0) return;
+  c.launches++;
   k_vec<<<grid_for(len, c.num_sms), 256, 0, c.stream>>>(op, len, o1, o2, a, b);
 }
 
 void launch_seam_add(Ctx& c, int dir, double2* z, const double2* r, int R) {
   if (c.n_seam[dir] == 0) return;
   long long len = (long long)c.n_seam[dir] * c.n * R;
+  c.launches++;
   k_seam_add<<<grid_for(len, c.num_sms), 256, 0, c.stream>>>(c.d_seam[dir], c.n_seam[dir], z, r,
                                                              c.n, R);
 }

@@ -121,6 +121,7 @@ struct Ctx {
   std::vector<double> ev_bytes;
   std::vector<cudaEvent_t> ev_pool;
   int64_t k_launches = 0;
+  int64_t launches = 0;  // every kernel this context launched
   double k_ms = 0, k_bytes = 0;
   int64_t dev_bytes = 0;
   int num_sms = 148;

@@ -294,6 +294,7 @@ cudaError_t gmres_init(Ctx& c, GmresDev& G, const double2* b) {
   long long nb = c.num_sms * 2;
   long long ch = ((G.LR + nb - 1) / nb + R - 1) / R * R;
   int nblk = (int)((G.LR + ch - 1) / ch);
+  c.launches += 3;
   k_colnorm_partial<<<nblk, bs, bs * sizeof(double2), c.stream>>>(b, G.LR, R, (int)ch, G.partial);
   k_gmres_init<<<1, bs, (bs + R) * sizeof(double2), c.stream>>>(G, nblk);
   int g2 = (int)std::min<long long>((G.LR + 255) / 256, (long long)c.num_sms * 8);
@@ -309,18 +310,21 @@ cudaError_t gmres_arnoldi(Ctx& c, GmresDev& G, int k, int grid, int chunk) {
     cudaFuncSetAttribute(k_mgs, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
     attr_set = true;
   }
+  c.launches++;
   void* args[] = {(void*)&G, (void*)&k, (void*)&chunk};
   return cudaLaunchCooperativeKernel((const void*)k_mgs, dim3(grid), dim3(bs), args, smem, c.stream);
 }
 
 cudaError_t gmres_givens(Ctx& c, GmresDev& G, int k) {
   int bs = G.R < 1024 ? ((G.R + 31) / 32) * 32 : 1024;
+  c.launches++;
   k_givens<<<1, bs, 0, c.stream>>>(G, k);
   return cudaGetLastError();
 }
 
 cudaError_t gmres_finish(Ctx& c, GmresDev& G, int mmax, double2* u) {
   int bs = G.R < 1024 ? ((G.R + 31) / 32) * 32 : 1024;
+  c.launches += 2;
   k_trisolve<<<1, bs, 0, c.stream>>>(G);
   int g2 = (int)std::min<long long>((G.LR + 255) / 256, (long long)c.num_sms * 8);
   k_combine<<<g2 > 0 ? g2 : 1, 256, 0, c.stream>>>(G, mmax, u);

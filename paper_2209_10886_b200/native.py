@@ -62,6 +62,7 @@ _SIGS = {
     "hs_set_kernel_timing": (_I, [_P, _I]),
     "hs_kernel_stats": (_I, [_P, C.POINTER(C.c_int64), C.POINTER(_D), C.POINTER(_D), _I]),
     "hs_memory": (_I, [_P, C.POINTER(C.c_int64)]),
+    "hs_launch_count": (_I, [_P, C.POINTER(C.c_int64)]),
     "hs_nccl_unique_id": (_I, [C.POINTER(C.c_uint8)]),
     "hs_comm_init": (_I, [_P, C.POINTER(C.c_uint8)]),
 }
@@ -158,6 +159,11 @@ class Context:
         n, ms, by = C.c_int64(), _D(), _D()
         self.call("hs_kernel_stats", C.byref(n), C.byref(ms), C.byref(by), int(reset))
         return n.value, ms.value, by.value
+
+    def launches(self) -> int:
+        v = C.c_int64()
+        self.call("hs_launch_count", C.byref(v))
+        return v.value
 
     def memory(self) -> int:
         b = C.c_int64()
