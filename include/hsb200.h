@@ -134,10 +134,12 @@ int hs_block_owner(const hs_ctx* ctx, int32_t* owner_rank);
  * (0 forward, 1 residual, 2 backward), rec[3*k+2] = subdomain ordinal (index in
  * multi-index order).  Returns the number of entries in *count. */
 int hs_schedule(const hs_ctx* ctx, int kind, int32_t* rec, int cap, int* count);
-/* Trace-exchange plan of a step kind across row bands (for rank `rank`):
- * blocks (0-based m) this rank sends to rank-1 / rank+1 after a forward,
- * backward and full step.  kind: 0 forward, 1 backward, 2 full. */
-int hs_exchange_plan(const hs_ctx* ctx, int kind, int peer, int32_t* blocks, int cap, int* count);
+/* Trace-exchange plan of a step kind across row bands, for this rank: recv = 0
+ * lists what it sends to `peer`, recv = 1 what it receives from `peer`, as
+ * triples (step index, 0-based block m, buffer slot) in slot order, for the
+ * steps of kind 0 (forward half), 1 (backward half) or 2 (full apply). */
+int hs_exchange_plan(const hs_ctx* ctx, int kind, int peer, int recv, int32_t* triples, int cap,
+                     int* count);
 
 /* Compact Schur map of subdomain (i1,i2) as a dense (k n) x (k n) complex
  * matrix, row-major (after hs_factor). */

@@ -127,6 +127,18 @@ def step_schedule(pc: Preconditioner):
     return recs
 
 
+class SchedulePlan:
+    """Schedule-only view of a preconditioner (no operators): for step counts
+    and wavefront records without factorising anything."""
+
+    def __init__(self, lat, kind="bsp", blocks=None, intermediate_residual=True, count_residual_steps=False):
+        self.lat, self.kind = lat, kind
+        self.ng = lat.n_groups
+        self.inter, self.count_res = intermediate_residual, count_residual_steps
+        self.lower = make_windows(lat.n1, lat.n2, "lower", blocks)
+        self.upper = make_windows(lat.n1, lat.n2, "upper", blocks)
+
+
 def format_trace(recs) -> str:
     """StepTrace text lines."""
     return "".join(

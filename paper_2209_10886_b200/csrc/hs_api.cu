@@ -923,7 +923,8 @@ int hs_schedule(const hs_ctx* cc, int kind, int32_t* rec, int cap, int* count) {
   return 0;
 }
 
-int hs_exchange_plan(const hs_ctx* cc, int kind, int peer, int32_t* blocks, int cap, int* count) {
+int hs_exchange_plan(const hs_ctx* cc, int kind, int peer, int recv, int32_t* blocks, int cap,
+                     int* count) {
   if (!cc) return 1;
   hs_ctx* c = const_cast<hs_ctx*>(cc);
   const Plan& P = c->plan;
@@ -933,7 +934,17 @@ int hs_exchange_plan(const hs_ctx* cc, int kind, int peer, int32_t* blocks, int 
   else if (kind == 2) steps.push_back(P.full_step());
   else return fail(c, 1, "kind must be 0, 1 or 2");
   std::vector<int32_t> out;
-  for (size_t t = 0; t < steps.size(); ++t)
+  for (size_t t = 0; t < steps.size(); ++t) {
+    if (recv) {
+      for (auto& rs : steps[t].recv) {
+        const int src = rs.dir == 0 ? P.rank - 1 : P.rank + 1;
+        if (src != peer) continue;
+        out.push_back((int32_t)t);
+        out.push_back((int32_t)(rs.off / c->n));
+        out.push_back(rs.slot);
+      }
+      continue;
+    }
     for (auto& it : steps[t].items) {
       const SubPlan& sp = P.subs[it.s];
       for (int q = 0; q < sp.k; ++q) {
@@ -943,9 +954,11 @@ int hs_exchange_plan(const hs_ctx* cc, int kind, int peer, int32_t* blocks, int 
         if (dst != peer) continue;
         out.push_back((int32_t)t);
         out.push_back(sp.tgt_block[q]);
+        out.push_back(sl >= 0 ? sl : -sl - 2);
       }
     }
-  *count = (int)(out.size() / 2);
+  }
+  *count = (int)(out.size() / 3);
   if (blocks) {
     if (cap < *count) return fail(c, 1, "buffer too small");
     std::copy(out.begin(), out.end(), blocks);

@@ -53,7 +53,7 @@ _SIGS = {
     "hs_pairs": (_I, [_P, _pI32]),
     "hs_block_owner": (_I, [_P, _pI32]),
     "hs_schedule": (_I, [_P, _I, _pI32, _I, C.POINTER(_I)]),
-    "hs_exchange_plan": (_I, [_P, _I, _I, _pI32, _I, C.POINTER(_I)]),
+    "hs_exchange_plan": (_I, [_P, _I, _I, _I, _pI32, _I, C.POINTER(_I)]),
     "hs_get_schur": (_I, [_P, _I, _I, _P]),
     "hs_set_schur": (_I, [_P, _I, _I, _P]),
     "hs_set_async": (_I, [_P, _I]),
@@ -143,11 +143,12 @@ class Context:
         self.call("hs_schedule", int(kind), iptr(out), cnt.value, C.byref(cnt))
         return out[:cnt.value]
 
-    def exchange_plan(self, kind: int, peer: int) -> np.ndarray:
+    def exchange_plan(self, kind: int, peer: int, recv: bool = False) -> np.ndarray:
+        """(step, block, slot) triples sent to / received from `peer`."""
         cnt = _I()
-        self.call("hs_exchange_plan", int(kind), int(peer), None, 0, C.byref(cnt))
-        out = np.zeros((max(cnt.value, 1), 2), dtype=np.int32)
-        self.call("hs_exchange_plan", int(kind), int(peer), iptr(out), cnt.value, C.byref(cnt))
+        self.call("hs_exchange_plan", int(kind), int(peer), int(recv), None, 0, C.byref(cnt))
+        out = np.zeros((max(cnt.value, 1), 3), dtype=np.int32)
+        self.call("hs_exchange_plan", int(kind), int(peer), int(recv), iptr(out), cnt.value, C.byref(cnt))
         return out[:cnt.value]
 
     def stream(self) -> int:

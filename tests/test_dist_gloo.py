@@ -1,0 +1,198 @@
+"""CPU, multi-process (gloo): the row-band sharded BSP / (I - S) applies.
+
+Each rank owns a band of subdomain rows, applies only its
+subdomains' Schur maps (oracle, test infrastructure) and exchanges the outputs
+that cross a band edge with its neighbours using the native exchange plan
+(hs_exchange_plan: the same slot order the NCCL send/recv path of libhsb200
+uses), applying the epilogue on receipt exactly like k_recv_epi.  The owned
+blocks must equal the single-process result.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import oracle_problem
+from paper_2209_10886_b200.configs import small_case
+
+CASE = small_case(4, 6, 8)
+CASE5 = dict(small_case(5, 7, 8), center=(2.5, 5.0), radius=0.9)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+class Band:
+    def __init__(self, case, rank, world, blocks):
+        from oracle import Interface
+        from oracle.lattice import windows
+        from paper_2209_10886_b200 import native
+        from paper_2209_10886_b200.indexing import window_ranges
+        self.prob, self.lat = oracle_problem(case)
+        self.itf = Interface(self.prob, self.lat, backend="schur")
+        self.n = self.prob.n
+        self.rank, self.world = rank, world
+        self.ctx = native.Context(-1, case["n1"], case["n2"], self.n, 0.1, 1.0, 1j, rank=rank, nranks=world)
+        for k, kd in ((0, "lower"), (1, "upper")):
+            w = window_ranges(case["n1"], case["n2"], kd, blocks)
+            lo, hi = native.i32([a for a, _ in w]), native.i32([b for _, b in w])
+            self.ctx.call("hs_set_windows", k, native.iptr(lo), native.iptr(hi), len(w))
+        self.lower = windows(case["n1"], case["n2"], "lower", blocks)
+        self.upper = windows(case["n1"], case["n2"], "upper", blocks)
+        self.owner = self.ctx.block_owner()
+        self.sub_rank = {s: int(self.owner[self.lat.first_block[s] - 1]) for s in self.lat.subs}
+
+    def blk(self, m):
+        return slice(m * self.n, (m + 1) * self.n)
+
+    def outputs(self, s, src, faces):
+        """(target block, y) for the given compact faces of subdomain s."""
+        T = self.itf.T[s]
+        x = src[self.itf.in_slice(s)]
+        out = []
+        for q in faces:
+            f, j = self.lat.faces[s][q]
+            y = T[q * self.n:(q + 1) * self.n] @ x
+            out.append((self.lat.m_index(j, s) - 1, y))
+        return out
+
+    def exchange(self, kind, t, remote, apply):
+        """Send raw outputs in plan slot order, receive, apply epilogue."""
+        reqs, recvs = [], []
+        for peer in (self.rank - 1, self.rank + 1):
+            if not 0 <= peer < self.world:
+                continue
+            plan = self.ctx.exchange_plan(kind, peer)
+            plan = plan[plan[:, 0] == t] if len(plan) else plan
+            if len(plan):
+                buf = np.zeros((len(plan), self.n), dtype=complex)
+                for _, b, slot in plan:
+                    buf[slot] = remote[int(b)]
+                reqs.append(dist.isend(torch.view_as_real(torch.from_numpy(buf)).contiguous(), peer))
+            rplan = self.ctx.exchange_plan(kind, peer, recv=True)
+            rplan = rplan[rplan[:, 0] == t] if len(rplan) else rplan
+            if len(rplan):
+                rb = torch.zeros((len(rplan), self.n, 2), dtype=torch.float64)
+                reqs.append(dist.irecv(rb, peer))
+                recvs.append((rplan, rb))
+        for r in reqs:
+            r.wait()
+        for rplan, rb in recvs:
+            vals = torch.view_as_complex(rb).numpy()
+            for _, b, slot in rplan:
+                apply(int(b), vals[slot])
+
+    def run_step(self, kind, t, items, apply):
+        remote = {}
+        for s, src, faces in items:
+            if self.sub_rank[s] != self.rank:
+                continue
+            for b, y in self.outputs(s, src, faces):
+                if self.owner[b] == self.rank:
+                    apply(b, y)
+                else:
+                    remote[b] = y
+        self.exchange(kind, t, remote, apply)
+
+    def half_items(self, direction, t, state, inp):
+        wins = self.lower if direction == 0 else self.upper
+        items = []
+        for lo, hi in wins:
+            if t > hi - lo:
+                continue
+            g = lo + t - 1 if direction == 0 else hi - t + 1
+            src = inp if t == 1 else state
+            for s in self.lat.groups.get(g, []):
+                nl = sum(1 for f, _ in self.lat.faces[s] if f in (0, 1))
+                k = len(self.lat.faces[s])
+                faces = range(nl, k) if direction == 0 else range(0, nl)
+                if len(faces):
+                    items.append((s, src, faces))
+        return items
+
+    def bsp(self, b):
+        zl = b.copy()
+        depth = max(hi - lo for lo, hi in self.lower)
+        for t in range(1, depth + 1):
+            def acc(blk, y):
+                zl[self.blk(blk)] += y
+            self.run_step(0, t - 1, self.half_items(0, t, zl, b), acc)
+        rp, w, z = np.zeros_like(b), np.zeros_like(b), np.zeros_like(b)
+
+        def resid(blk, y):
+            sl = self.blk(blk)
+            v = b[sl] - (zl[sl] - y)
+            rp[sl], w[sl], z[sl] = v, v, zl[sl] + v
+        full = [(s, zl, range(len(self.lat.faces[s]))) for s in self.lat.subs]
+        self.run_step(2, 0, full, resid)
+        depth = max(hi - lo for lo, hi in self.upper)
+        for t in range(1, depth + 1):
+            def acc2(blk, y):
+                w[self.blk(blk)] += y
+                z[self.blk(blk)] += y
+            self.run_step(1, t - 1, self.half_items(1, t, w, rp), acc2)
+        return z
+
+    def apply_A(self, g):
+        out = np.zeros_like(g)
+
+        def ims(blk, y):
+            out[self.blk(blk)] = g[self.blk(blk)] - y
+        full = [(s, g, range(len(self.lat.faces[s]))) for s in self.lat.subs]
+        self.run_step(2, 0, full, ims)
+        return out
+
+    def owned_mask(self):
+        return np.repeat(self.owner == self.rank, self.n)
+
+
+def _worker(rank, world, port, case, blocks, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import Interface, Preconditioner
+        band = Band(case, rank, world, blocks)
+        rng = np.random.default_rng(7)
+        r = rng.standard_normal(band.itf.size) + 1j * rng.standard_normal(band.itf.size)
+        z = band.bsp(r)
+        a = band.apply_A(r)
+        ref_itf = Interface(band.prob, band.lat, backend="schur")
+        zr = Preconditioner(ref_itf, "bsp", blocks=blocks)(r)
+        ar = ref_itf.apply_A(r)
+        m = band.owned_mask()
+        q.put((rank, float(np.abs(z[m] - zr[m]).max() / np.abs(zr).max()),
+               float(np.abs(a[m] - ar[m]).max() / np.abs(ar).max()), int(m.sum())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case,world,blocks", [(CASE, 2, None), (CASE, 3, 2), (CASE5, 2, 4), (CASE5, 3, None)])
+def test_sharded_bsp_matches_single_process(case, world, blocks):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, case, blocks, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    L = None
+    total = 0
+    for rank, ez, ea, owned in res:
+        assert ez < 1e-13, (rank, ez)
+        assert ea < 1e-13, (rank, ea)
+        total += owned
+    from oracle.lattice import Lattice
+    assert total == Lattice(case["n1"], case["n2"]).n_pairs * case["n"]
