@@ -75,8 +75,19 @@ def config_json(c, world):
             "lattice": [c["n1"], c["n2"]], "cells_per_side": c["n"], "grid": [c["n1"] * c["n"], c["n2"] * c["n"]],
             "kappa": c["kappa"], "blocks": c["blocks"], "nrhs": c["nrhs"], "tol": c["tol"],
             "parallelism": f"rowbands{world}" if world > 1 else "single",
-            "l2": "inputs larger than L2 (Schur maps 7.9 GB at cfg5 >> 126 MB); no flush" if c["n"] >= 128
-                  else "L2 flushed between steps"}
+            "l2": (f"inputs larger than L2: Schur maps {schur_bytes(c) / 1e9:.2f} GB >> 126 MB L2, no flush"
+                   if schur_bytes(c) > 4 * 126e6 else "L2 NOT flushed: maps fit in L2 (report as L2-resident)")}
+
+
+def schur_bytes(c):
+    """Bytes of the per-subdomain maps: 16 n^2 sum_i k_i^2."""
+    n1, n2, n = c["n1"], c["n2"], c["n"]
+    tot = 0
+    for a in range(1, n1 + 1):
+        for b in range(1, n2 + 1):
+            k = (a > 1) + (a < n1) + (b > 1) + (b < n2)
+            tot += k * k
+    return 16.0 * n * n * tot
 
 
 # ---------------------------------------------------------------- clocks
@@ -309,11 +320,16 @@ def main():
     # roofline of the step-apply kernel
     peak, peak_kind = load_peaks()
     ach = (kbytes / (kms * 1e-3)) / 1e9 if kms > 0 else None
-    traffic = None
+    traffic, traffic_src = None, None
     prof = os.path.join(ROOT, "profiles", f"ncu_step_kernel_cfg{args.config}.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof) and kl > 0:
         with open(prof) as f:
-            traffic = json.load(f).get("dram_bytes_per_launch")
+            pj = json.load(f)
+        # ncu DRAM bytes / algorithmic bytes of the captured launches, applied to
+        # this run's average launch (the same per-launch unit as `achieved`)
+        traffic = pj["traffic_over_algorithmic"] * kbytes / kl
+        traffic_src = (f"profiles/{os.path.basename(prof)}: dram/algorithmic = "
+                       f"{pj['traffic_over_algorithmic']:.4f} over {len(pj['launches'])} captured launches")
     share = kms / ms if ms > 0 else None
 
     # e2e through the C ABI with pinned host buffers
@@ -369,7 +385,7 @@ def main():
                 "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
                 "config": config_json(c, world),
                 "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                             "frac": (ach / peak) if ach else None, "traffic": traffic,
+                             "frac": (ach / peak) if ach else None, "traffic": traffic, "traffic_source": traffic_src,
                              "kernel": "k_step1 (batched step-apply ZGEMV)", "peak_source": peak_kind,
                              "launches": kl, "kernel_ms_share_of_step": share,
                              "algorithmic_bytes_per_apply": kbytes / max(args.steps, 1)},
