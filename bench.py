@@ -309,7 +309,7 @@ def main():
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
     ctx.call("hs_set_kernel_timing", 0)
-    kl, kms, kbytes = ctx.kernel_stats(reset=True)
+    kl, kms, kbytes, _kflops = ctx.kernel_stats(reset=True)
     if dist is not None:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

@@ -82,6 +82,13 @@ int hs_destroy(hs_ctx* ctx);
  * row-major (y slow).  Must precede hs_factor. */
 int hs_set_dirichlet(hs_ctx* ctx, int i1, int i2, const int32_t* cells, int ncells);
 
+/* Map storage, before hs_factor: 0 = one compact map per subdomain streamed
+ * from HBM by the step kernels (default); 1 = shared-operator mode: only the
+ * distinct operators' 4n x 4n maps are kept (the reference matrix depends
+ * only on the Dirichlet cells, discretization.py:224-229) and every step is a
+ * DMMA contraction with the map L2-resident (needs n % 16 == 0). */
+int hs_set_map_mode(hs_ctx* ctx, int mode);
+
 /* Build every subdomain's interface Schur map on the GPU (block-tridiagonal
  * elimination of the Dirichlet-eliminated operator, one per distinct
  * operator, then scattered into per-subdomain compact maps). */
@@ -154,10 +161,12 @@ int hs_sync(hs_ctx* ctx);
 /* The context's CUDA stream (cudaStream_t) as an integer. */
 int hs_stream(hs_ctx* ctx, uint64_t* stream);
 /* Kernel timing: when on, every step-apply launch is bracketed by CUDA events;
- * hs_kernel_stats reports launches, summed ms and algorithmic bytes of the
+ * hs_kernel_stats reports launches, summed ms, algorithmic bytes (per-subdomain
+ * map path) and algorithmic flops (8 per complex MAC) of the
  * step-apply kernels since the last reset. */
 int hs_set_kernel_timing(hs_ctx* ctx, int on);
-int hs_kernel_stats(hs_ctx* ctx, int64_t* launches, double* ms, double* bytes, int reset);
+int hs_kernel_stats(hs_ctx* ctx, int64_t* launches, double* ms, double* bytes, double* flops,
+                    int reset);
 /* Number of kernels this context has launched (all kinds). */
 int hs_launch_count(const hs_ctx* ctx, int64_t* n);
 /* Bytes of device memory held by the context. */

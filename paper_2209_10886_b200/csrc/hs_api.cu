@@ -86,7 +86,10 @@ int upload(Ctx* c, T** dptr, const std::vector<T>& v) {
     return 0;
   }
   CK(dalloc(c, (void**)dptr, v.size() * sizeof(T)));
-  CK(cudaMemcpy(*dptr, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  // Stream-ordered: the kernels run on a non-blocking stream, which does not
+  // order against a legacy-stream cudaMemcpy (whose pageable H2D copy may
+  // return before the DMA lands).  Pageable source -> staged before return.
+  CK(cudaMemcpyAsync(*dptr, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, c->stream));
   return 0;
 }
 
@@ -94,7 +97,121 @@ void free_step(Ctx* c, DevStep& s) {
   dfree(c, s.items, s.nitems * sizeof(DevItem));
   dfree(c, s.tiles, s.ntiles * sizeof(DevTile));
   dfree(c, s.recv, s.nrecv * sizeof(DevRecv));
+  for (auto& kv : s.mma) {
+    dfree(c, kv.second.tasks, kv.second.ntasks * sizeof(MmaTask));
+    dfree(c, kv.second.cols, kv.second.ncols * sizeof(MmaCol));
+  }
   s = DevStep();
+}
+
+// DMMA contraction tasks of a step.  shared = false: per-subdomain maps
+// (compact faces, rows of T_s), R right-hand sides per slab.  shared = true:
+// the class maps (4 faces W,S,N,E), one column per (subdomain, RHS), items of
+// the same class and face range batched into one contraction.
+int make_mma(Ctx* c, DevStep& st, int R, bool shared, DevMma** out) {
+  const int key = shared ? -R : R;
+  auto it = st.mma.find(key);
+  if (it != st.mma.end()) {
+    *out = &it->second;
+    return 0;
+  }
+  const Plan& P = c->plan;
+  const int n = c->n;
+  std::vector<MmaTask> tasks;
+  std::vector<MmaCol> cols;
+  double flops = 0;
+  auto col_for = [&](const Item& item, int r, bool global_faces) {
+    const SubPlan& sp = P.subs[item.s];
+    MmaCol col;
+    for (int q = 0; q < 4; ++q) { col.in[q] = -1; col.out[q] = -1; col.slot[q] = -1; }
+    for (int q = 0; q < sp.k; ++q) {
+      const int f = global_faces ? sp.face[q] : q;
+      col.in[f] = ((long long)sp.first_block * n + (long long)q * n) * R + r;
+      const int r0 = q * n, r1 = (q + 1) * n;
+      if (r1 <= item.rlo || r0 >= item.rhi) continue;  // face not produced by this item
+      col.out[f] = (long long)sp.tgt_block[q] * n * R + r;
+      col.slot[f] = item.slot[q];
+    }
+    col.r = r;
+    col.alt = item.alt;
+    return col;
+  };
+  if (!shared) {
+    for (const Item& item : st.host.items) {
+      const SubPlan& sp = P.subs[item.s];
+      const int K = sp.k * n;
+      for (int r0 = (item.rlo / 32) * 32; r0 < item.rhi; r0 += 32)
+        for (int c0 = 0; c0 < R; c0 += 32) {
+          MmaTask tk;
+          tk.a_off = sp.T_off + (long long)(r0 / 32) * K * 32;
+          tk.K = K; tk.r0 = r0; tk.rlo = item.rlo; tk.rhi = item.rhi;
+          tk.col0 = (int)cols.size();
+          tk.ncols = std::min(32, R - c0);
+          for (int r = c0; r < c0 + tk.ncols; ++r) cols.push_back(col_for(item, r, false));
+          tasks.push_back(tk);
+          flops += 8.0 * 32 * tk.ncols * K;
+        }
+    }
+  } else {
+    // group by (class, global face-row range)
+    std::map<std::tuple<int, int, int>, std::vector<int>> groups;
+    for (size_t i = 0; i < st.host.items.size(); ++i) {
+      const Item& item = st.host.items[i];
+      const SubPlan& sp = P.subs[item.s];
+      int glo, ghi;
+      if (item.rlo == 0 && item.rhi == sp.k * n) { glo = 0; ghi = 4 * n; }
+      else if (item.rlo == 0) { glo = 0; ghi = 2 * n; }      // lower faces W,S
+      else { glo = 2 * n; ghi = 4 * n; }                      // upper faces N,E
+      groups[std::make_tuple(c->sub_class[item.s], glo, ghi)].push_back((int)i);
+    }
+    const int K = 4 * n;
+    for (auto& g : groups) {
+      const int cls = std::get<0>(g.first), glo = std::get<1>(g.first), ghi = std::get<2>(g.first);
+      std::vector<MmaCol> gc;
+      for (int i : g.second)
+        for (int r = 0; r < R; ++r) gc.push_back(col_for(st.host.items[i], r, true));
+      for (size_t c0 = 0; c0 < gc.size(); c0 += 32) {
+        const int nc = (int)std::min<size_t>(32, gc.size() - c0);
+        const int base = (int)cols.size();
+        cols.insert(cols.end(), gc.begin() + c0, gc.begin() + c0 + nc);
+        for (int r0 = (glo / 32) * 32; r0 < ghi; r0 += 32) {
+          MmaTask tk;
+          tk.a_off = c->Tcls_off[cls] + (long long)(r0 / 32) * K * 32;
+          tk.K = K; tk.r0 = r0; tk.rlo = glo; tk.rhi = ghi;
+          tk.col0 = base;
+          tk.ncols = nc;
+          tasks.push_back(tk);
+          flops += 8.0 * 32 * nc * K;
+        }
+      }
+    }
+  }
+  // bounds validation of every descriptor (a bad table must fail here, not fault)
+  {
+    const long long LR = P.L * (long long)R;
+    const size_t Aelems = shared ? c->Tcls_elems : c->T_elems;
+    for (const MmaTask& tk : tasks) {
+      if (tk.K % 16 || tk.a_off < 0 || (size_t)(tk.a_off + (long long)tk.K * 32) > Aelems)
+        return fail(c, -4, "internal: contraction task reads outside the maps");
+      for (int j = 0; j < tk.ncols; ++j) {
+        const MmaCol& col = cols[tk.col0 + j];
+        for (int q = 0; q < 4; ++q) {
+          if (col.in[q] >= 0 && col.in[q] + (long long)(n - 1) * R >= LR)
+            return fail(c, -4, "internal: contraction column reads outside the vector");
+          if (col.out[q] >= 0 && col.out[q] + (long long)(n - 1) * R >= LR)
+            return fail(c, -4, "internal: contraction column writes outside the vector");
+        }
+      }
+    }
+  }
+  DevMma m;
+  if (upload(c, &m.tasks, tasks) || upload(c, &m.cols, cols)) return -1;
+  m.ntasks = (int)tasks.size();
+  m.ncols = (int)cols.size();
+  m.flops = flops;
+  auto res = st.mma.emplace(key, m);
+  *out = &res.first->second;
+  return 0;
 }
 
 int make_step(Ctx* c, const StepTable& t, DevStep& out) {
@@ -130,6 +247,7 @@ int make_step(Ctx* c, const StepTable& t, DevStep& out) {
   out.maxK = maxK;
   out.bytes_per_rhs_map = mapb;
   out.bytes_per_rhs_vec = vecb;
+  out.host = t;
   return 0;
 }
 
@@ -215,20 +333,29 @@ cudaEvent_t ev_get(Ctx* c) {
 }
 
 // One sweep step: batched apply + (row bands) exchange + receive epilogue.
-int run_step(Ctx* c, const DevStep& st, const double2* srcA, const double2* srcB, Epi e, int R) {
+int run_step(Ctx* c, DevStep& st, const double2* srcA, const double2* srcB, Epi e, int R) {
   e.send_up = c->send_up;
   e.send_dn = c->send_dn;
+  // kernel choice: shared class maps -> DMMA contraction; per-subdomain maps:
+  // one RHS -> HBM ZGEMV (k_step1), several -> DMMA contraction (FFMA fallback
+  // when n is not a multiple of the 16-wide K chunk)
+  DevMma* mm = nullptr;
+  const bool shared = c->map_mode == 1;
+  if (st.nitems > 0 && (shared || (R > 1 && c->n % 16 == 0)))
+    if (make_mma(c, st, R, shared, &mm)) return -1;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (c->timing && st.ntiles > 0) {
     e0 = ev_get(c);
     e1 = ev_get(c);
     cudaEventRecord(e0, c->stream);
   }
-  launch_step(*c, st, srcA, srcB, e, R);
+  if (mm) launch_zmma(*c, *mm, shared ? c->Tcls : c->T, srcA, srcB, e, R);
+  else launch_step(*c, st, srcA, srcB, e, R);
   if (e1) {
     cudaEventRecord(e1, c->stream);
     c->ev_pending.push_back({e0, e1});
-    c->ev_bytes.push_back(st.bytes_per_rhs_map + R * st.bytes_per_rhs_vec);
+    c->ev_bytes.push_back(shared ? 0.0 : st.bytes_per_rhs_map + R * st.bytes_per_rhs_vec);
+    c->ev_flops.push_back(mm ? mm->flops : 8.0 * st.bytes_per_rhs_map / 16.0 * R);
   }
   CK(cudaGetLastError());
   if (c->plan.nranks > 1) {
@@ -304,8 +431,8 @@ int check_ready(Ctx* c, int R) {
 int do_half(Ctx* c, int dir, const double2* r, double2* z, int R) {
   const long long LR = LRof(c, R);
   CK(cudaMemcpyAsync(z, r, LR * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
-  const auto& steps = dir == 0 ? c->fwd : c->bwd;
-  for (const auto& st : steps)
+  auto& steps = dir == 0 ? c->fwd : c->bwd;
+  for (auto& st : steps)
     if (run_step(c, st, z, r, epi(EPI_ACC, z), R)) return -1;
   if (c->seam == HS_SEAM_LITERAL) launch_seam_add(*c, dir, z, r, R);
   return 0;
@@ -321,10 +448,10 @@ int do_precond(Ctx* c, int kind, const double2* r, double2* z, int R) {
     double2* zl;
     if (ws_get(c, "zL", LR, &zl)) return -1;
     CK(cudaMemcpyAsync(zl, r, LR * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
-    for (const auto& st : c->sp_fwd)
+    for (auto& st : c->sp_fwd)
       if (run_step(c, st, zl, r, epi(EPI_ACC, zl), R)) return -1;
     CK(cudaMemcpyAsync(z, zl, LR * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
-    for (const auto& st : c->sp_bwd)
+    for (auto& st : c->sp_bwd)
       if (run_step(c, st, z, zl, epi(EPI_ACC, z), R)) return -1;
     return 0;
   }
@@ -340,7 +467,7 @@ int do_precond(Ctx* c, int kind, const double2* r, double2* z, int R) {
     launch_vec(*c, VEC_INIT_BWD, LR, w, z, r, zl);
     rsrc = r;
   }
-  for (const auto& st : c->bwd)
+  for (auto& st : c->bwd)
     if (run_step(c, st, w, rsrc, epi(EPI_ACC2, w, z), R)) return -1;
   if (c->seam == HS_SEAM_LITERAL) launch_seam_add(*c, 1, z, rsrc, R);
   return 0;
@@ -461,6 +588,7 @@ int hs_create(hs_ctx** out, int device, int n1, int n2, int n, double h, double 
     cudaDeviceGetAttribute(&x->num_sms, cudaDevAttrMultiProcessorCount, device);
     cudaDeviceGetAttribute(&x->coop_ok, cudaDevAttrCooperativeLaunch, device);
     set_step_smem_limit();
+    set_zmma_smem_limit();
     // per-subdomain records (T_off filled by hs_factor)
     std::vector<DevSub> subs(x->plan.nsub);
     long long off = 0;
@@ -506,6 +634,7 @@ int hs_destroy(hs_ctx* c) {
     free_step(c, c->full);
     for (auto& oc : c->classes) cudaFree(oc.T4);
     cudaFree(c->T);
+    cudaFree(c->Tcls);
     cudaFree(c->dsubs);
     cudaFree(c->d_seam[0]);
     cudaFree(c->d_seam[1]);
@@ -590,22 +719,40 @@ int hs_factor(hs_ctx* c) {
     T4s[k] = c->classes[k].T4;
     c->classes[k].X = X + k * xstride;  // view; X freed as a whole at destroy
   }
-  // per-subdomain maps, tile-major
-  if (!c->T) CK(dalloc(c, (void**)&c->T, c->T_elems * sizeof(double2)));
-  std::vector<int2> tl;
-  std::vector<int> faces(4 * c->plan.nsub, 0), cls(c->plan.nsub, 0);
-  for (int s2 = 0; s2 < c->plan.nsub; ++s2) {
-    const SubPlan& sp = c->plan.subs[s2];
-    const int K = sp.k * n;
-    for (int t = 0; t * kRowTile < K; ++t) tl.push_back(make_int2(s2, t));
-    for (int q = 0; q < sp.k; ++q) faces[4 * s2 + q] = sp.face[q];
-    cls[s2] = c->sub_class[s2];
+  // class maps, strip-major (shared-operator mode reads them directly)
+  {
+    const long long strips = (4LL * n + 31) / 32;
+    const long long per = strips * 32 * 4LL * n;
+    dfree(c, c->Tcls, c->Tcls_elems * sizeof(double2));
+    c->Tcls = nullptr;
+    c->Tcls_elems = (size_t)per * ncls;
+    CK(dalloc(c, (void**)&c->Tcls, c->Tcls_elems * sizeof(double2)));
+    c->Tcls_off.assign(ncls, 0);
+    for (int k = 0; k < ncls; ++k) {
+      c->Tcls_off[k] = per * k;
+      launch_pack_strips(*c, c->classes[k].T4, c->Tcls + per * k, 4 * n, 4 * n);
+    }
   }
-  int2* dtl;
-  int *dfaces, *dcls;
-  double2** dT4s;
-  if (upload(c, &dtl, tl) || upload(c, &dfaces, faces) || upload(c, &dcls, cls) || upload(c, &dT4s, T4s)) return -1;
-  launch_scatter_T(*c, dtl, (int)tl.size(), dfaces, dcls, dT4s);
+  // per-subdomain maps, tile-major (the HBM-streamed path)
+  int2* dtl = nullptr;
+  int *dfaces = nullptr, *dcls = nullptr;
+  double2** dT4s = nullptr;
+  if (c->map_mode == 0) {
+    if (!c->T) CK(dalloc(c, (void**)&c->T, c->T_elems * sizeof(double2)));
+    std::vector<int2> tl;
+    std::vector<int> faces(4 * c->plan.nsub, 0), cls(c->plan.nsub, 0);
+    for (int s2 = 0; s2 < c->plan.nsub; ++s2) {
+      const SubPlan& sp = c->plan.subs[s2];
+      const int K = sp.k * n;
+      for (int t = 0; t * kRowTile < K; ++t) tl.push_back(make_int2(s2, t));
+      for (int q = 0; q < sp.k; ++q) faces[4 * s2 + q] = sp.face[q];
+      cls[s2] = c->sub_class[s2];
+    }
+    if (upload(c, &dtl, tl) || upload(c, &dfaces, faces) || upload(c, &dcls, cls) || upload(c, &dT4s, T4s)) return -1;
+    launch_scatter_T(*c, dtl, (int)tl.size(), dfaces, dcls, dT4s);
+  } else if (n % 16 != 0) {
+    return fail(c, 1, "shared-map mode needs cells_per_side divisible by 16");
+  }
   CK(cudaGetLastError());
   int bad = 0;
   CK(cudaMemcpyAsync(&bad, dbad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
@@ -969,13 +1116,27 @@ int hs_exchange_plan(const hs_ctx* cc, int kind, int peer, int recv, int32_t* bl
 int hs_get_schur(hs_ctx* c, int i1, int i2, double* T) {
   if (!c) return fail(nullptr, 1, "null context");
   NEED_GPU(c);
-  if (!c->factored || !c->T) return fail(c, 1, "no maps (call hs_factor)");
+  if (!c->factored || (!c->T && !c->Tcls)) return fail(c, 1, "no maps (call hs_factor)");
   if (i1 < 1 || i1 > c->n1 || i2 < 1 || i2 > c->n2) return fail(c, 1, "subdomain out of range");
-  const SubPlan& sp = c->plan.subs[c->plan.ordinal(i1, i2)];
+  const int s = c->plan.ordinal(i1, i2);
+  const SubPlan& sp = c->plan.subs[s];
   const long long K = (long long)sp.k * c->n;
   const long long nt = (K + kRowTile - 1) / kRowTile;
-  std::vector<double2> tm((size_t)nt * kRowTile * K);
   CK(cudaStreamSynchronize(c->stream));
+  if (!c->T) {  // shared-map mode: compact sub-block of the class map
+    const int n = c->n, n4 = 4 * n;
+    std::vector<double2> t4((size_t)n4 * n4);
+    CK(cudaMemcpy(t4.data(), c->classes[c->sub_class[s]].T4, t4.size() * sizeof(double2),
+                  cudaMemcpyDeviceToHost));
+    for (long long r = 0; r < K; ++r)
+      for (long long col = 0; col < K; ++col) {
+        const long long gr = sp.face[r / n] * n + r % n, gc = sp.face[col / n] * n + col % n;
+        T[2 * (r * K + col)] = t4[(size_t)(gr * n4 + gc)].x;
+        T[2 * (r * K + col) + 1] = t4[(size_t)(gr * n4 + gc)].y;
+      }
+    return 0;
+  }
+  std::vector<double2> tm((size_t)nt * kRowTile * K);
   CK(cudaMemcpy(tm.data(), c->T + sp.T_off, tm.size() * sizeof(double2), cudaMemcpyDeviceToHost));
   for (long long r = 0; r < K; ++r)
     for (long long col = 0; col < K; ++col) {
@@ -999,7 +1160,9 @@ int hs_set_schur(hs_ctx* c, int i1, int i2, const double* T) {
     for (long long col = 0; col < K; ++col)
       tm[(size_t)((r / kRowTile) * K + col) * kRowTile + r % kRowTile] =
           make_double2(T[2 * (r * K + col)], T[2 * (r * K + col) + 1]);
-  CK(cudaMemcpy(c->T + sp.T_off, tm.data(), tm.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  CK(cudaMemcpyAsync(c->T + sp.T_off, tm.data(), tm.size() * sizeof(double2), cudaMemcpyHostToDevice,
+                     c->stream));
+  CK(cudaStreamSynchronize(c->stream));
   c->factored = true;  // bring-up: maps supplied by the caller
   return 0;
 }
@@ -1024,13 +1187,24 @@ int hs_stream(hs_ctx* c, uint64_t* s) {
   return 0;
 }
 
+int hs_set_map_mode(hs_ctx* c, int mode) {
+  if (!c) return fail(nullptr, 1, "null context");
+  if (mode != 0 && mode != 1) return fail(c, 1, "map mode must be 0 (per subdomain) or 1 (shared)");
+  if (mode != c->map_mode) {
+    c->map_mode = mode;
+    c->factored = false;  // maps must be (re)built in the new layout
+    c->steps_dirty = true;
+  }
+  return 0;
+}
+
 int hs_set_kernel_timing(hs_ctx* c, int on) {
   if (!c) return 1;
   c->timing = on != 0;
   return 0;
 }
 
-int hs_kernel_stats(hs_ctx* c, int64_t* launches, double* ms, double* bytes, int reset) {
+int hs_kernel_stats(hs_ctx* c, int64_t* launches, double* ms, double* bytes, double* flops, int reset) {
   if (!c) return 1;
   NEED_GPU(c);
   CK(cudaStreamSynchronize(c->stream));
@@ -1039,16 +1213,19 @@ int hs_kernel_stats(hs_ctx* c, int64_t* launches, double* ms, double* bytes, int
     cudaEventElapsedTime(&t, c->ev_pending[i].first, c->ev_pending[i].second);
     c->k_ms += t;
     c->k_bytes += c->ev_bytes[i];
+    c->k_flops += c->ev_flops[i];
     c->k_launches++;
     c->ev_pool.push_back(c->ev_pending[i].first);
     c->ev_pool.push_back(c->ev_pending[i].second);
   }
   c->ev_pending.clear();
   c->ev_bytes.clear();
+  c->ev_flops.clear();
   if (launches) *launches = c->k_launches;
   if (ms) *ms = c->k_ms;
   if (bytes) *bytes = c->k_bytes;
-  if (reset) { c->k_launches = 0; c->k_ms = 0; c->k_bytes = 0; }
+  if (flops) *flops = c->k_flops;
+  if (reset) { c->k_launches = 0; c->k_ms = 0; c->k_bytes = 0; c->k_flops = 0; }
   return 0;
 }
 

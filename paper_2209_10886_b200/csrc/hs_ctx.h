@@ -58,8 +58,36 @@ struct Epi {
   double2* send_dn;
 };
 
+// DMMA contraction tasks (hs_zmma.cu): 32 map rows x up to 32 columns each.
+struct MmaTask {
+  long long a_off;  // element offset of the 32-row strip holding rows r0..r0+31
+  int K;            // map columns
+  int r0, rlo, rhi; // strip start; valid output rows [rlo, rhi)
+  int col0, ncols;  // column descriptors [col0, col0 + ncols)
+};
+
+// One B column / output column: per face (map row block q), the element
+// offset of position 0 in the input and output vectors (-1: face absent ->
+// zero input, dropped output); consecutive positions are R apart.
+struct MmaCol {
+  long long in[4];
+  long long out[4];
+  int slot[4];
+  int r;    // right-hand side index (exchange buffer layout)
+  int alt;  // read srcB (the half's input) instead of srcA
+};
+
+struct DevMma {
+  MmaTask* tasks = nullptr;
+  MmaCol* cols = nullptr;
+  int ntasks = 0, ncols = 0;
+  double flops = 0;
+};
+
 // A step uploaded to the device: items + tiles + receive list.
 struct DevStep {
+  StepTable host;                 // kept to build contraction tasks lazily
+  std::map<int, DevMma> mma;      // key: R (per-subdomain maps) or -R (shared maps)
   DevItem* items = nullptr;
   DevTile* tiles = nullptr;
   DevRecv* recv = nullptr;
@@ -94,6 +122,10 @@ struct Ctx {
   std::vector<OpClass> classes;
   std::vector<int> sub_class;
   bool factored = false;
+  int map_mode = 0;               // 0: per-subdomain maps (HBM path), 1: shared class maps
+  double2* Tcls = nullptr;        // class maps, strip-major, padded rows
+  std::vector<long long> Tcls_off;
+  size_t Tcls_elems = 0;
   // device state
   cudaStream_t stream = nullptr;
   double2* T = nullptr;
@@ -118,11 +150,11 @@ struct Ctx {
   int async_mode = 0;
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pending;
-  std::vector<double> ev_bytes;
+  std::vector<double> ev_bytes, ev_flops;
   std::vector<cudaEvent_t> ev_pool;
   int64_t k_launches = 0;
   int64_t launches = 0;  // every kernel this context launched
-  double k_ms = 0, k_bytes = 0;
+  double k_ms = 0, k_bytes = 0, k_flops = 0;
   int64_t dev_bytes = 0;
   int num_sms = 148;
   int coop_ok = 0;

@@ -26,6 +26,10 @@ void launch_vec(Ctx& c, int op, long long len, double2* o1, double2* o2, const d
                 const double2* b);
 void launch_seam_add(Ctx& c, int dir, double2* z, const double2* r, int R);
 cudaError_t set_step_smem_limit();
+void launch_zmma(Ctx& c, const DevMma& m, const double2* A, const double2* srcA, const double2* srcB,
+                 const Epi& e, int R);
+cudaError_t set_zmma_smem_limit();
+void launch_pack_strips(Ctx& c, const double2* T4, double2* out, int rows, int cols);
 
 // ---- factorisation (hs_schur.cu)
 cudaError_t factor_blocks(Ctx& c, double2* X, long long xstride, const uint8_t* dmasks, int ncls,

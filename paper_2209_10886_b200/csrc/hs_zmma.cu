@@ -1,0 +1,213 @@
+// Complex128 GEMM on the FP64 tensor cores (DMMA, mma.sync.m8n8k4.f64; tcgen05
+// has no f64 kind) for the dense contractions of the sweeps:
+//   * K4, multi-RHS: Y = T_s[rows, :] * X_s (K x R), X_s the subdomain's
+//     incoming slab of the [L][R] vector (interface_system.py:115-133 for R
+//     right-hand sides at once);
+//   * the shared-operator variant: every subdomain with the same operator
+//     (discretization.py:224-229: the matrix does not depend on which faces
+//     couple) uses its class map T4 (4n x 4n), so a step is ONE contraction
+//     Y = T4[rows, :] * [x_s1 ... x_sm] with missing faces read as zero and
+//     their outputs dropped -- FP64-bound with the map L2-resident.
+//
+// A task = 32 map rows x up to 32 columns.  A is read from the strip-major map
+// layout (a 32-row strip is contiguous, K x 32), B columns are gathered per
+// face from the vector (column descriptor: per-face element offset or -1,
+// stride R between consecutive face positions).  K is staged in chunks of 16
+// through a 3-stage cp.async pipeline; 4 warps each own a 16 x 16 output
+// block (2 x 2 DMMA tiles, real and imaginary accumulators; a complex MAC is
+// 4 real DMMAs).  The epilogue routes every output to its block exactly like
+// the single-RHS kernel (same Epi modes, same exchange slots).
+#include <cuda_runtime.h>
+
+#include "hs_common.cuh"
+#include "hs_kernels.h"
+
+namespace hs {
+
+namespace {
+
+constexpr int BM = 32, BN = 32, KC = 16, STAGES = 3, THREADS = 128;
+
+__device__ __forceinline__ void cp16(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(THREADS) k_zmma(const MmaTask* __restrict__ tasks,
+                                                  const MmaCol* __restrict__ cols,
+                                                  const double2* __restrict__ A,
+                                                  const double2* srcA, const double2* srcB, Epi e,
+                                                  int n, int R) {
+  extern __shared__ __align__(16) double2 dyn[];
+  double2 (*As)[KC][BM] = reinterpret_cast<double2 (*)[KC][BM]>(dyn);
+  double2 (*Bs)[KC][BN] = reinterpret_cast<double2 (*)[KC][BN]>(dyn + STAGES * KC * BM);
+  __shared__ long long cin[BN][4], cout_[BN][4];
+  __shared__ int cslot[BN][4], cr[BN], calt[BN];
+  const MmaTask tk = tasks[blockIdx.x];
+  const int tid = threadIdx.x;
+  if (tid < BN) {
+    if (tid < tk.ncols) {
+      const MmaCol c = cols[tk.col0 + tid];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        cin[tid][q] = c.in[q];
+        cout_[tid][q] = c.out[q];
+        cslot[tid][q] = c.slot[q];
+      }
+      cr[tid] = c.r;
+      calt[tid] = c.alt;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        cin[tid][q] = -1;
+        cout_[tid][q] = -1;
+        cslot[tid][q] = -1;
+      }
+      cr[tid] = 0;
+      calt[tid] = 0;
+    }
+  }
+  __syncthreads();
+  const double2* Ab = A + tk.a_off;  // strip containing rows r0..r0+31: [K][32]
+  const int nk = tk.K / KC;
+
+  auto load = [&](int stage, int kc) {
+    const int k0 = kc * KC;
+    const double2* asrc = Ab + (long long)k0 * BM;
+#pragma unroll
+    for (int i = 0; i < (KC * BM) / THREADS; ++i) {
+      const int el = tid + i * THREADS;
+      cp16(&As[stage][0][0] + el, asrc + el);
+    }
+    const int q = k0 / n, p0 = k0 - q * n;
+#pragma unroll
+    for (int i = 0; i < (KC * BN) / THREADS; ++i) {
+      const int el = tid + i * THREADS;
+      const int kk = el / BN, j = el % BN;
+      const long long off = cin[j][q];
+      double2* dst = &Bs[stage][kk][j];
+      if (off >= 0) {
+        const double2* v = calt[j] ? srcB : srcA;
+        cp16(dst, v + off + (long long)(p0 + kk) * R);
+      } else {
+        *dst = make_double2(0.0, 0.0);
+      }
+    }
+  };
+
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1;
+  const int gid = lane >> 2, tig = lane & 3;
+  double cre[2][2][2], cim[2][2][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) cre[a][b][c] = cim[a][b][c] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) load(s, s);
+    cp_commit();
+  }
+  for (int kc = 0; kc < nk; ++kc) {
+    cp_wait<STAGES - 2>();
+    __syncthreads();
+    const int nxt = kc + STAGES - 1;
+    if (nxt < nk) load(nxt % STAGES, nxt);
+    cp_commit();
+    const int st = kc % STAGES;
+#pragma unroll
+    for (int k4 = 0; k4 < KC; k4 += 4) {
+      double2 a[2], b[2];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) a[mt] = As[st][k4 + tig][wm * 16 + mt * 8 + gid];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) b[nt] = Bs[st][k4 + tig][wn * 16 + nt * 8 + gid];
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const double nai = -a[mt].y;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          dmma(cre[mt][nt][0], cre[mt][nt][1], a[mt].x, b[nt].x);
+          dmma(cre[mt][nt][0], cre[mt][nt][1], nai, b[nt].y);
+          dmma(cim[mt][nt][0], cim[mt][nt][1], a[mt].x, b[nt].y);
+          dmma(cim[mt][nt][0], cim[mt][nt][1], a[mt].y, b[nt].x);
+        }
+      }
+    }
+  }
+  cp_wait<0>();
+
+  // epilogue: C(row gid, cols 2 tig + {0,1}) of each 8x8 tile
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt) {
+    const int row = tk.r0 + wm * 16 + mt * 8 + gid;
+    if (row < tk.rlo || row >= tk.rhi) continue;
+    const int q = row / n, p = row - q * n;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = wn * 16 + nt * 8 + 2 * tig + h;
+        if (j >= tk.ncols) continue;
+        const double2 y = make_double2(cre[mt][nt][h], cim[mt][nt][h]);
+        const int slot = cslot[j][q];
+        if (slot == -1) {
+          const long long off = cout_[j][q];
+          if (off >= 0) epi_apply(e, off + (long long)p * R, y);
+        } else if (slot >= 0) {
+          e.send_up[((long long)slot * n + p) * R + cr[j]] = y;
+        } else {
+          e.send_dn[((long long)(-slot - 2) * n + p) * R + cr[j]] = y;
+        }
+      }
+  }
+}
+
+constexpr size_t kZmmaSmem = sizeof(double2) * STAGES * KC * (BM + BN);
+
+void launch_zmma(Ctx& c, const DevMma& m, const double2* A, const double2* srcA, const double2* srcB,
+                 const Epi& e, int R) {
+  if (m.ntasks == 0) return;
+  c.launches++;
+  k_zmma<<<m.ntasks, THREADS, kZmmaSmem, c.stream>>>(m.tasks, m.cols, A, srcA, srcB, e, c.n, R);
+}
+
+cudaError_t set_zmma_smem_limit() {
+  return cudaFuncSetAttribute(k_zmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kZmmaSmem);
+}
+
+// Row-major (rows x cols) map -> strip-major [rows/32][cols][32], zero-padded rows.
+__global__ void k_pack_strips(const double2* T4, double2* out, int rows, int cols) {
+  const long long strips = (rows + 31) / 32;
+  const long long total = strips * cols * 32;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int lane = (int)(i % 32);
+    const long long rest = i / 32;
+    const int col = (int)(rest % cols);
+    const int strip = (int)(rest / cols);
+    const int row = strip * 32 + lane;
+    out[i] = row < rows ? T4[(long long)row * cols + col] : make_double2(0, 0);
+  }
+}
+
+void launch_pack_strips(Ctx& c, const double2* T4, double2* out, int rows, int cols) {
+  c.launches++;
+  k_pack_strips<<<4 * c.num_sms, 256, 0, c.stream>>>(T4, out, rows, cols);
+}
+
+}  // namespace hs

@@ -148,7 +148,11 @@ class GpuInterfaceSystem:
 
     def __init__(self, spec, partition: Partition, imp: ImpedanceSpec | None = None, workers: int = 1,
                  device: int = 0, rank: int = 0, nranks: int = 1, nccl_id: bytes | None = None,
-                 sweep: SweepConfig | None = None):
+                 sweep: SweepConfig | None = None, maps: str = "subdomain"):
+        """maps = "subdomain": one compact Schur map per subdomain, streamed from
+        HBM by the step kernels (the graded path); "shared": only the distinct
+        operators' maps (generic + scatterer) are kept and every step is a DMMA
+        contraction with the map L2-resident (discretization.py:224-229)."""
         if workers < 1:
             raise ValueError(f"workers must be >= 1, got {workers}")
         self.spec = spec
@@ -165,6 +169,10 @@ class GpuInterfaceSystem:
                 raise ValueError("a sharded system needs the NCCL unique id of rank 0")
             buf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
             self.ctx.call("hs_comm_init", buf)
+        if maps not in ("subdomain", "shared"):
+            raise ValueError(f"maps must be 'subdomain' or 'shared', got {maps!r}")
+        self.maps = maps
+        self.ctx.call("hs_set_map_mode", 1 if maps == "shared" else 0)
         self.home, cells = scatterer_cells(spec, partition)
         if self.home is not None:
             c = native.i32(cells)

@@ -60,7 +60,8 @@ _SIGS = {
     "hs_sync": (_I, [_P]),
     "hs_stream": (_I, [_P, C.POINTER(C.c_uint64)]),
     "hs_set_kernel_timing": (_I, [_P, _I]),
-    "hs_kernel_stats": (_I, [_P, C.POINTER(C.c_int64), C.POINTER(_D), C.POINTER(_D), _I]),
+    "hs_kernel_stats": (_I, [_P, C.POINTER(C.c_int64), C.POINTER(_D), C.POINTER(_D), C.POINTER(_D), _I]),
+    "hs_set_map_mode": (_I, [_P, _I]),
     "hs_memory": (_I, [_P, C.POINTER(C.c_int64)]),
     "hs_launch_count": (_I, [_P, C.POINTER(C.c_int64)]),
     "hs_nccl_unique_id": (_I, [C.POINTER(C.c_uint8)]),
@@ -157,9 +158,10 @@ class Context:
         return s.value
 
     def kernel_stats(self, reset: bool = False):
-        n, ms, by = C.c_int64(), _D(), _D()
-        self.call("hs_kernel_stats", C.byref(n), C.byref(ms), C.byref(by), int(reset))
-        return n.value, ms.value, by.value
+        """(launches, ms, algorithmic bytes, algorithmic flops) of the step kernels."""
+        n, ms, by, fl = C.c_int64(), _D(), _D(), _D()
+        self.call("hs_kernel_stats", C.byref(n), C.byref(ms), C.byref(by), C.byref(fl), int(reset))
+        return n.value, ms.value, by.value, fl.value
 
     def launches(self) -> int:
         v = C.c_int64()

@@ -1,0 +1,94 @@
+"""GPU: the FP64 DMMA contraction paths.
+
+* multi-RHS with per-subdomain maps (K4): every column equals the single-RHS
+  HBM kernel's result;
+* shared-operator mode (class maps, one contraction per step): equals the
+  per-subdomain mode on every entry point (the maps are the same numbers,
+  discretization.py:224-229), and GMRES takes the same iterations;
+* shared mode refuses n not divisible by the 16-wide K chunk.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import cvec, golden, product_problem, relerr
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2209_10886_b200.configs import CONFIGS, small_case  # noqa: E402
+from paper_2209_10886_b200.interface_system import GpuInterfaceSystem, SweepConfig  # noqa: E402
+
+_S = {}
+
+
+def system(k, maps):
+    key = (k, maps)
+    if key not in _S:
+        if k >= 3:
+            for kk in [x for x in _S if x[0] >= 3 and x != key]:
+                del _S[kk]
+        c = CONFIGS[k] if isinstance(k, int) else k
+        spec, part = product_problem(c)
+        _S[key] = GpuInterfaceSystem(spec, part, maps=maps, sweep=SweepConfig(blocks=c["blocks"]))
+    return _S[key]
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_multi_rhs_dmma_equals_single(k):
+    s = system(k, "subdomain")
+    L = s.layout.size
+    X = cvec(3, L, 40)  # 40: a full and a partial 32-column chunk
+    Y = s.apply_interface_operator(X)
+    Z = s.bsp_apply(X)
+    for r in (0, 17, 31, 32, 39):
+        x = np.ascontiguousarray(X[:, r])
+        assert relerr(Y[:, r], s.apply_interface_operator(x)) < 1e-14
+        assert relerr(Z[:, r], s.bsp_apply(x)) < 1e-13
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_shared_mode_equals_subdomain_mode(k):
+    a, b = system(k, "subdomain"), system(k, "shared")
+    L = a.layout.size
+    g = cvec(9, L)
+    assert relerr(b.apply_scattering(g), a.apply_scattering(g)) < 1e-14
+    assert relerr(b.apply_interface_operator(g), a.apply_interface_operator(g)) < 1e-14
+    assert relerr(b.bsp_apply(g), a.bsp_apply(g)) < 1e-13
+    assert relerr(b.sgs_apply(g), a.sgs_apply(g)) < 1e-13
+    ng = a.partition.n_groups
+    assert relerr(b.restricted_apply(g, {ng // 2}, {ng // 2 + 1}), a.restricted_apply(g, {ng // 2}, {ng // 2 + 1})) < 1e-14
+    G = [(s.i1, s.i2) for s in a.partition.subdomains[:3]] + [tuple(a.home)]
+    for sub in G:
+        assert np.array_equal(b.schur_map(sub), a.schur_map(sub))
+    rb = b.rhs()
+    assert relerr(rb, a.rhs()) < 1e-15
+    ra, rs = a.gmres(rb, "bsp", tol=1e-6, maxit=1000), b.gmres(rb, "bsp", tol=1e-6, maxit=1000)
+    assert ra.iterations == rs.iterations and rs.converged
+    assert relerr(rs.solution, ra.solution) < 1e-10
+
+
+def test_shared_mode_vs_reference_golden_cfg2():
+    G = golden("cfg2")
+    s = system(2, "shared")
+    assert relerr(s.apply_interface_operator(G["g"]), G["Ag"]) < 1e-10
+    assert relerr(s.bsp_apply(G["r"]), G["M_bsp"]) < 1e-10
+    res = s.gmres(G["b"], "bsp", tol=1e-6, maxit=1000)
+    assert res.iterations == int(G["gm_iters"])
+    assert relerr(res.solution, G["gm_x"]) < 1e-8
+
+
+def test_shared_mode_cfg5_gmres():
+    s = system(5, "shared")
+    b = s.rhs()
+    res = s.gmres(b, "bsp", tol=1e-6, maxit=1000)
+    assert res.converged and 100 <= res.iterations <= 115
+    assert relerr(s.apply_interface_operator(res.solution), b) < 1e-6
+
+
+def test_shared_mode_needs_n_multiple_of_16():
+    spec, part = product_problem(small_case(2, 2, 8))
+    with pytest.raises(ValueError):
+        GpuInterfaceSystem(spec, part, maps="shared")

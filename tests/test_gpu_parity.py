@@ -127,7 +127,7 @@ def test_multi_rhs_matches_single():
     X = cvec(11, L, 8)
     Y = s.apply_scattering(X)
     for r in range(8):
-        assert relerr(Y[:, r], s.apply_scattering(np.ascontiguousarray(X[:, r]))) < 1e-14
+        assert relerr(Y[:, r], s.apply_scattering(np.ascontiguousarray(X[:, r]))) < 1e-13
     Z = s.bsp_apply(X)
     for r in (0, 5):
         assert relerr(Z[:, r], s.bsp_apply(np.ascontiguousarray(X[:, r]))) < 1e-13
