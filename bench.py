@@ -141,7 +141,9 @@ def _cpu_worker_init(cfgno):
     c = CONFIGS[cfgno]
     prob = Problem(kappa=c["kappa"], n=c["n"], side=c["side"], center=tuple(c["center"]), radius=c["radius"])
     lat = Lattice(c["n1"], c["n2"])
-    sub = (c["n1"] // 2 + 1, c["n2"] // 2 - 1) if c["n2"] > 3 else lat.subs[0]  # interior, no scatterer
+    home = prob.home(lat)
+    interior = [s for s in lat.subs if len(lat.faces[s]) == 4 and s != home]
+    sub = interior[len(interior) // 2] if interior else next(s for s in lat.subs if s != home)
     op = Subdomain(prob, lat, sub)
     rng = np.random.default_rng(0)
     tr = {f: rng.standard_normal(c["n"]) + 1j * rng.standard_normal(c["n"]) for f in op.iface}
@@ -156,13 +158,6 @@ def _cpu_worker_solves(nsolves):
         for f in op.iface:
             op.outgoing(u, tr[f], f)
     return nsolves, time.perf_counter() - t0
-
-
-def solves_per_apply(system):
-    """Subdomain solves of one BSP apply in the reference path: one per item of
-    every forward/backward step (schedule) plus N_dom for the residual."""
-    recs = system.step_schedule("bsp")
-    return sum(len(s) for _, _, s in recs) + system.partition.n_subdomains
 
 
 def cpu_baseline(cfgno, n_solves_apply, budget_s=20.0):
@@ -191,15 +186,9 @@ def run_reference(args):
     import multiprocessing as mp
     from paper_2209_10886_b200.configs import CONFIGS
     c = CONFIGS[args.config]
-    from oracle.lattice import Lattice
-    from oracle.sweeps import step_schedule as _  # noqa: F401  (schedule below is structural)
-    from paper_2209_10886_b200.indexing import window_ranges
-    lat = Lattice(c["n1"], c["n2"])
-    nfw = sum(len([s for s in lat.subs if s[0] + s[1] == lo + t - 1])
-              for lo, hi in window_ranges(c["n1"], c["n2"], "lower", c["blocks"]) for t in range(1, hi - lo + 1))
-    nbw = sum(len([s for s in lat.subs if s[0] + s[1] == hi - t + 1])
-              for lo, hi in window_ranges(c["n1"], c["n2"], "upper", c["blocks"]) for t in range(1, hi - lo + 1))
-    nsol = nfw + nbw + len(lat.subs)
+    # the reference solves every subdomain of a step that has an output face
+    # (interface_system.py:122-124), once per right-hand side
+    nsol = solves_per_apply_cfg(c) * int(c["nrhs"])
     procs = os.cpu_count() or 1
     ctx = mp.get_context("fork")
     with ctx.Pool(procs, initializer=_cpu_worker_init, initargs=(args.config,)) as pool:
@@ -242,6 +231,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gmres", action="store_true")
+    ap.add_argument("--no-variants", action="store_true", help="skip the shared-operator variant")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -264,82 +254,126 @@ def main():
         nccl_id = obj[0]
 
     c, spec, part = problem(args.config)
+    R = int(c["nrhs"])
     sweep = SweepConfig(blocks=c["blocks"])
     t0 = time.perf_counter()
     system = GpuInterfaceSystem(spec, part, device=local, rank=rank, nranks=world, nccl_id=nccl_id, sweep=sweep)
     setup_s = time.perf_counter() - t0
-    ctx = system.ctx
     L = system.layout.size
     gen = torch.Generator(device="cpu").manual_seed(1234)
-    r_host = torch.complex(torch.randn(L, generator=gen, dtype=torch.float64),
-                           torch.randn(L, generator=gen, dtype=torch.float64))
-    r = r_host.cuda()
-    z = torch.empty_like(r)
-    torch.cuda.synchronize()
-    stream = torch.cuda.ExternalStream(ctx.stream())
-    ctx.call("hs_set_async", 1)
-
-    def apply_dev():
-        ctx.call("hs_precond", native.HS_PC_BSP, C.c_void_p(r.data_ptr()), C.c_void_p(z.data_ptr()), 1,
-                 native.HS_MEM_DEVICE)
+    shape = (L,) if R == 1 else (L, R)
+    r_host = torch.complex(torch.randn(shape, generator=gen, dtype=torch.float64),
+                           torch.randn(shape, generator=gen, dtype=torch.float64))
 
     def barrier():
         if dist is not None:
             dist.barrier()
 
-    for _ in range(max(args.warmup, 3)):
-        apply_dev()
-    ctx.call("hs_sync")
-    ctx.kernel_stats(reset=True)
-    ctx.call("hs_set_kernel_timing", 1)
-    barrier()
-    torch.cuda.synchronize()
-    clocks = Clocks(local)
-    time.sleep(0.25)
-    l0 = ctx.launches()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    for _ in range(args.steps):
-        apply_dev()
-    ev1.record(stream)
-    ev1.synchronize()
-    launches = ctx.launches() - l0
-    clk = clocks.stop()
-    barrier()
-    torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1)
-    ctx.call("hs_set_kernel_timing", 0)
-    kl, kms, kbytes, _kflops = ctx.kernel_stats(reset=True)
-    if dist is not None:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    ms_per = ms / args.steps
-    value = 1e3 / ms_per
+        return float(t.item())
 
-    # roofline of the step-apply kernel
-    peak, peak_kind = load_peaks()
-    ach = (kbytes / (kms * 1e-3)) / 1e9 if kms > 0 else None
-    traffic, traffic_src = None, None
-    prof = os.path.join(ROOT, "profiles", f"ncu_step_kernel_cfg{args.config}.json")
-    if os.path.exists(prof) and kl > 0:
-        with open(prof) as f:
-            pj = json.load(f)
-        # ncu DRAM bytes / algorithmic bytes of the captured launches, applied to
-        # this run's average launch (the same per-launch unit as `achieved`)
-        traffic = pj["traffic_over_algorithmic"] * kbytes / kl
-        traffic_src = (f"profiles/{os.path.basename(prof)}: dram/algorithmic = "
-                       f"{pj['traffic_over_algorithmic']:.4f} over {len(pj['launches'])} captured launches")
-    share = kms / ms if ms > 0 else None
+    def measure(sysm, steps, warmup, with_clocks):
+        """Device-resident BSP applies, CUDA events on the library stream."""
+        ctx = sysm.ctx
+        r = r_host.cuda()
+        z = torch.empty_like(r)
+        torch.cuda.synchronize()
+        stream = torch.cuda.ExternalStream(ctx.stream())
+        ctx.call("hs_set_async", 1)
+
+        def apply_dev():
+            ctx.call("hs_precond", native.HS_PC_BSP, C.c_void_p(r.data_ptr()), C.c_void_p(z.data_ptr()), R,
+                     native.HS_MEM_DEVICE)
+
+        for _ in range(max(warmup, 3)):
+            apply_dev()
+        ctx.call("hs_sync")
+        ctx.kernel_stats(reset=True)
+        ctx.call("hs_set_kernel_timing", 1)
+        barrier()
+        torch.cuda.synchronize()
+        clocks = Clocks(local) if with_clocks else None
+        if clocks:
+            time.sleep(0.25)
+        l0 = ctx.launches()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(steps):
+            apply_dev()
+        ev1.record(stream)
+        ev1.synchronize()
+        launches = ctx.launches() - l0
+        clk = clocks.stop() if clocks else None
+        barrier()
+        torch.cuda.synchronize()
+        ms = max_over_ranks(ev0.elapsed_time(ev1))
+        ctx.call("hs_set_kernel_timing", 0)
+        kl, kms, kbytes, kflops = ctx.kernel_stats(reset=True)
+        ctx.call("hs_set_async", 0)
+        return {"ms_per": ms / steps, "ms": ms, "launches": launches, "clk": clk, "kl": kl, "kms": kms,
+                "kbytes": kbytes, "kflops": kflops}
+
+    def gmres_tts(sysm):
+        if R == 1:
+            b = sysm.rhs()
+        else:
+            from paper_2209_10886_b200.configs import angles
+            b = sysm.rhs(directions=[(float(np.cos(t)), float(np.sin(t))) for t in angles(c)])
+        sysm.gmres(b, "bsp", tol=c["tol"], maxit=1000)  # warm (workspace allocation)
+        t1 = time.perf_counter()
+        res = sysm.gmres(b, "bsp", tol=c["tol"], maxit=1000)
+        tts = time.perf_counter() - t1
+        resid = np.linalg.norm(sysm.apply_interface_operator(res.solution) - b, axis=0) / np.linalg.norm(b, axis=0)
+        its = res.iterations if R == 1 else max(res.iterations)
+        conv = res.converged if R == 1 else all(res.converged)
+        return {"time_to_solution_s": tts, "iterations": its, "converged": bool(conv),
+                "true_relative_residual": float(np.max(resid))}
+
+    m = measure(system, args.steps, args.warmup, True)
+    ms_per = m["ms_per"]
+    value = 1e3 / ms_per
+    share = m["kms"] / m["ms"] if m["ms"] > 0 else None
+    if R == 1:
+        # roofline of the HBM-bound step-apply kernel (per-subdomain maps)
+        peak, peak_kind = load_peaks()
+        ach = (m["kbytes"] / (m["kms"] * 1e-3)) / 1e9 if m["kms"] > 0 else None
+        traffic, traffic_src = None, None
+        prof = os.path.join(ROOT, "profiles", f"ncu_step_kernel_cfg{args.config}.json")
+        if os.path.exists(prof) and m["kl"] > 0:
+            with open(prof) as f:
+                pj = json.load(f)
+            # ncu DRAM bytes / algorithmic bytes of the captured launches, applied to
+            # this run's average launch (the same per-launch unit as `achieved`)
+            traffic = pj["traffic_over_algorithmic"] * m["kbytes"] / m["kl"]
+            traffic_src = (f"profiles/{os.path.basename(prof)}: dram/algorithmic = "
+                           f"{pj['traffic_over_algorithmic']:.4f} over {len(pj['launches'])} captured launches")
+        roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": (ach / peak) if ach else None, "traffic": traffic, "traffic_source": traffic_src,
+                "kernel": "k_step1 (batched step-apply ZGEMV, per-subdomain maps)", "peak_source": peak_kind,
+                "launches": m["kl"], "kernel_ms_share_of_step": share,
+                "algorithmic_bytes_per_apply": m["kbytes"] / max(args.steps, 1)}
+    else:
+        peak = fp64_peak()
+        ach = (m["kflops"] / (m["kms"] * 1e-3)) / 1e12 if m["kms"] > 0 else None
+        roof = {"bound": "fp64", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                "frac": (ach / peak) if ach else None, "traffic": None,
+                "kernel": "k_zmma (FP64 DMMA complex contraction, per-subdomain maps x R RHS)",
+                "peak_source": "measured DMMA m8n8k4 peak, profiles/fp64_peak_b200.json",
+                "launches": m["kl"], "kernel_ms_share_of_step": share,
+                "algorithmic_flops_per_apply": m["kflops"] / max(args.steps, 1)}
 
     # e2e through the C ABI with pinned host buffers
-    rh = r_host.numpy().copy()
-    r_pin = torch.from_numpy(rh).pin_memory()
+    ctx = system.ctx
+    stream = torch.cuda.ExternalStream(ctx.stream())
+    r_pin = torch.from_numpy(r_host.numpy().copy()).pin_memory()
     z_pin = torch.empty_like(r_pin).pin_memory()
-    ctx.call("hs_set_async", 0)
 
     def apply_host():
-        ctx.call("hs_precond", native.HS_PC_BSP, C.c_void_p(r_pin.data_ptr()), C.c_void_p(z_pin.data_ptr()), 1,
+        ctx.call("hs_precond", native.HS_PC_BSP, C.c_void_p(r_pin.data_ptr()), C.c_void_p(z_pin.data_ptr()), R,
                  native.HS_MEM_HOST)
 
     for _ in range(2):
@@ -352,30 +386,37 @@ def main():
         apply_host()
     e1.record(stream)
     e1.synchronize()
-    ems = e0.elapsed_time(e1)
-    if dist is not None:
-        t = torch.tensor([ems], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ems = float(t.item())
-    e2e = {"value": 1e3 * ke / ems, "unit": "applies/s", "h2d_bytes_per_step": int(L * 16),
-           "d2h_bytes_per_step": int(L * 16)}
+    ems = max_over_ranks(e0.elapsed_time(e1))
+    e2e = {"value": 1e3 * ke / ems, "unit": "applies/s", "h2d_bytes_per_step": int(L * R * 16),
+           "d2h_bytes_per_step": int(L * R * 16)}
 
-    # GMRES time-to-solution (single GPU; GMRES phase only)
     gm = None
+    variants = {}
     if world == 1 and not args.no_gmres:
-        b = system.rhs()
-        system.gmres(b, "bsp", tol=c["tol"], maxit=1000)  # warm (workspace allocation)
-        t1 = time.perf_counter()
-        res = system.gmres(b, "bsp", tol=c["tol"], maxit=1000)
-        tts = time.perf_counter() - t1
-        true_res = float(np.linalg.norm(system.apply_interface_operator(res.solution) - b) / np.linalg.norm(b))
-        gm = {"time_to_solution_s": tts, "iterations": res.iterations, "converged": res.converged,
-              "true_relative_residual": true_res, "setup_s": setup_s}
+        gm = gmres_tts(system)
+        gm["setup_s"] = setup_s
+    if world == 1 and not args.no_variants and c["n"] % 16 == 0:
+        # shared-operator variant: class maps only, every step one DMMA contraction
+        del system
+        torch.cuda.empty_cache()
+        t0 = time.perf_counter()
+        sh = GpuInterfaceSystem(spec, part, device=local, sweep=sweep, maps="shared")
+        sh_setup = time.perf_counter() - t0
+        ms_sh = measure(sh, max(10, args.steps), args.warmup, False)
+        fl = ms_sh["kflops"] / (ms_sh["kms"] * 1e-3) / 1e12 if ms_sh["kms"] > 0 else None
+        variants["shared_maps"] = {
+            "what": "generic subdomains share one 4n x 4n map (discretization.py:224-229); each sweep step is "
+                    "one FP64 DMMA contraction (k_zmma) with the map L2-resident",
+            "applies_per_s": 1e3 / ms_sh["ms_per"], "ms_per_apply": ms_sh["ms_per"],
+            "roofline": {"bound": "fp64", "achieved": fl, "peak": fp64_peak(), "unit": "TFLOP/s",
+                         "frac": fl / fp64_peak() if fl else None},
+            "setup_s": sh_setup, "gmres": None if args.no_gmres else gmres_tts(sh),
+            "map_bytes": sh.ctx.memory()}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_baseline(args.config, solves_per_apply(system))
+            cpu = cpu_baseline(args.config, solves_per_apply_cfg(c) * R)
         except Exception as e:  # report, do not fail the bench
             cpu = {"value": None, "unit": "applies/s", "cores": 1, "kind": "port", "sample": f"failed: {e}"}
 
@@ -383,19 +424,38 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "applies/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-                "config": config_json(c, world),
-                "roofline": {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                             "frac": (ach / peak) if ach else None, "traffic": traffic, "traffic_source": traffic_src,
-                             "kernel": "k_step1 (batched step-apply ZGEMV)", "peak_source": peak_kind,
-                             "launches": kl, "kernel_ms_share_of_step": share,
-                             "algorithmic_bytes_per_apply": kbytes / max(args.steps, 1)},
-                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
-                "gmres": gm, "setup_s": setup_s}
+                "config": config_json(c, world), "roofline": roof,
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": m["launches"], "clocks": m["clk"],
+                "gmres": gm, "setup_s": setup_s, "variants": variants}
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def fp64_peak():
+    p = os.path.join(ROOT, "profiles", "fp64_peak_b200.json")
+    with open(p) as f:
+        return float(json.load(f)["dmma_m8n8k4_tflops"])
+
+
+def solves_per_apply_cfg(c):
+    """Subdomain solves of one BSP apply in the reference path: one per
+    subdomain of every forward / backward step (windows) plus N_dom for the
+    intermediate residual."""
+    from oracle.lattice import Lattice
+    from paper_2209_10886_b200.indexing import window_ranges
+    lat = Lattice(c["n1"], c["n2"])
+
+    def nl(s):
+        return sum(1 for f, _ in lat.faces[s] if f in (0, 1))
+
+    nfw = sum(1 for lo, hi in window_ranges(c["n1"], c["n2"], "lower", c["blocks"]) for t in range(1, hi - lo + 1)
+              for s in lat.groups.get(lo + t - 1, []) if len(lat.faces[s]) > nl(s))
+    nbw = sum(1 for lo, hi in window_ranges(c["n1"], c["n2"], "upper", c["blocks"]) for t in range(1, hi - lo + 1)
+              for s in lat.groups.get(hi - t + 1, []) if nl(s) > 0)
+    return nfw + nbw + len(lat.subs)
 
 
 if __name__ == "__main__":

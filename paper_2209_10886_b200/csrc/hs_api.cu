@@ -209,6 +209,8 @@ int make_mma(Ctx* c, DevStep& st, int R, bool shared, DevMma** out) {
   m.ntasks = (int)tasks.size();
   m.ncols = (int)cols.size();
   m.flops = flops;
+  m.minK = tasks.empty() ? 0 : tasks[0].K;
+  for (const MmaTask& tk : tasks) m.minK = std::min(m.minK, tk.K);
   auto res = st.mma.emplace(key, m);
   *out = &res.first->second;
   return 0;

@@ -81,6 +81,7 @@ struct DevMma {
   MmaTask* tasks = nullptr;
   MmaCol* cols = nullptr;
   int ntasks = 0, ncols = 0;
+  int minK = 0;  // smallest K of the tasks (split-K decision)
   double flops = 0;
 };
 

@@ -13,20 +13,27 @@
 // layout (a 32-row strip is contiguous, K x 32), B columns are gathered per
 // face from the vector (column descriptor: per-face element offset or -1,
 // stride R between consecutive face positions).  K is staged in chunks of 16
-// through a 3-stage cp.async pipeline; 4 warps each own a 16 x 16 output
-// block (2 x 2 DMMA tiles, real and imaginary accumulators; a complex MAC is
-// 4 real DMMAs).  The epilogue routes every output to its block exactly like
-// the single-RHS kernel (same Epi modes, same exchange slots).
+// through a 4-stage cp.async pipeline.  8 warps: 4 output quadrants (16 x 16 =
+// 2 x 2 DMMA tiles, real and imaginary accumulators; a complex MAC is 4 real
+// DMMAs) x 2 halves of every K chunk, reduced through shared memory.  When a
+// step has few tasks the K range is also split over a thread-block cluster of
+// KS CTAs whose partial tiles are summed by rank 0 through distributed shared
+// memory in rank order (deterministic).  The epilogue routes every output to
+// its block exactly like the single-RHS kernel (same Epi modes and slots).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "hs_common.cuh"
 #include "hs_kernels.h"
 
+namespace cg = cooperative_groups;
+
 namespace hs {
 
 namespace {
 
-constexpr int BM = 32, BN = 32, KC = 16, STAGES = 3, THREADS = 128;
+constexpr int BM = 32, BN = 32, KC = 16, STAGES = 4, THREADS = 256;
+constexpr int kStageElems = KC * (BM + BN);
 
 __device__ __forceinline__ void cp16(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -44,17 +51,17 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 
 }  // namespace
 
+// grid = ntasks * KS, cluster (KS, 1, 1); task = blockIdx.x / KS
 __global__ void __launch_bounds__(THREADS) k_zmma(const MmaTask* __restrict__ tasks,
                                                   const MmaCol* __restrict__ cols,
                                                   const double2* __restrict__ A,
                                                   const double2* srcA, const double2* srcB, Epi e,
-                                                  int n, int R) {
+                                                  int n, int R, int KS) {
   extern __shared__ __align__(16) double2 dyn[];
-  double2 (*As)[KC][BM] = reinterpret_cast<double2 (*)[KC][BM]>(dyn);
-  double2 (*Bs)[KC][BN] = reinterpret_cast<double2 (*)[KC][BN]>(dyn + STAGES * KC * BM);
   __shared__ long long cin[BN][4], cout_[BN][4];
   __shared__ int cslot[BN][4], cr[BN], calt[BN];
-  const MmaTask tk = tasks[blockIdx.x];
+  const int rank = KS > 1 ? (int)cg::this_cluster().block_rank() : 0;
+  const MmaTask tk = tasks[blockIdx.x / KS];
   const int tid = threadIdx.x;
   if (tid < BN) {
     if (tid < tk.ncols) {
@@ -80,7 +87,12 @@ __global__ void __launch_bounds__(THREADS) k_zmma(const MmaTask* __restrict__ ta
   }
   __syncthreads();
   const double2* Ab = A + tk.a_off;  // strip containing rows r0..r0+31: [K][32]
-  const int nk = tk.K / KC;
+  const int nk_all = tk.K / KC;
+  const int kc0 = (int)((long long)nk_all * rank / KS), kc1 = (int)((long long)nk_all * (rank + 1) / KS);
+  const int nk = kc1 - kc0;
+
+  auto As = [&](int st, int k, int m) -> double2& { return dyn[st * kStageElems + k * BM + m]; };
+  auto Bs = [&](int st, int k, int j) -> double2& { return dyn[st * kStageElems + KC * BM + k * BN + j]; };
 
   auto load = [&](int stage, int kc) {
     const int k0 = kc * KC;
@@ -88,7 +100,7 @@ __global__ void __launch_bounds__(THREADS) k_zmma(const MmaTask* __restrict__ ta
 #pragma unroll
     for (int i = 0; i < (KC * BM) / THREADS; ++i) {
       const int el = tid + i * THREADS;
-      cp16(&As[stage][0][0] + el, asrc + el);
+      cp16(&dyn[stage * kStageElems + el], asrc + el);
     }
     const int q = k0 / n, p0 = k0 - q * n;
 #pragma unroll
@@ -96,7 +108,7 @@ __global__ void __launch_bounds__(THREADS) k_zmma(const MmaTask* __restrict__ ta
       const int el = tid + i * THREADS;
       const int kk = el / BN, j = el % BN;
       const long long off = cin[j][q];
-      double2* dst = &Bs[stage][kk][j];
+      double2* dst = &Bs(stage, kk, j);
       if (off >= 0) {
         const double2* v = calt[j] ? srcB : srcA;
         cp16(dst, v + off + (long long)(p0 + kk) * R);
@@ -107,7 +119,8 @@ __global__ void __launch_bounds__(THREADS) k_zmma(const MmaTask* __restrict__ ta
   };
 
   const int lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 1, wn = warp & 1;
+  const int wk = warp >> 2, wq = warp & 3;
+  const int wm = wq >> 1, wn = wq & 1;
   const int gid = lane >> 2, tig = lane & 3;
   double cre[2][2][2], cim[2][2][2];
 #pragma unroll
@@ -119,23 +132,23 @@ __global__ void __launch_bounds__(THREADS) k_zmma(const MmaTask* __restrict__ ta
 
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nk) load(s, s);
+    if (s < nk) load(s, kc0 + s);
     cp_commit();
   }
-  for (int kc = 0; kc < nk; ++kc) {
+  for (int i = 0; i < nk; ++i) {
     cp_wait<STAGES - 2>();
     __syncthreads();
-    const int nxt = kc + STAGES - 1;
-    if (nxt < nk) load(nxt % STAGES, nxt);
+    const int nxt = i + STAGES - 1;
+    if (nxt < nk) load(nxt % STAGES, kc0 + nxt);
     cp_commit();
-    const int st = kc % STAGES;
+    const int st = i % STAGES;
 #pragma unroll
-    for (int k4 = 0; k4 < KC; k4 += 4) {
+    for (int k4 = wk * 8; k4 < wk * 8 + 8; k4 += 4) {
       double2 a[2], b[2];
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt) a[mt] = As[st][k4 + tig][wm * 16 + mt * 8 + gid];
+      for (int mt = 0; mt < 2; ++mt) a[mt] = As(st, k4 + tig, wm * 16 + mt * 8 + gid);
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) b[nt] = Bs[st][k4 + tig][wn * 16 + nt * 8 + gid];
+      for (int nt = 0; nt < 2; ++nt) b[nt] = Bs(st, k4 + tig, wn * 16 + nt * 8 + gid);
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
         const double nai = -a[mt].y;
@@ -150,6 +163,65 @@ __global__ void __launch_bounds__(THREADS) k_zmma(const MmaTask* __restrict__ ta
     }
   }
   cp_wait<0>();
+  __syncthreads();
+
+  // reduce the two K halves: the wk = 1 warps hand their tiles to wk = 0
+  double2* red = dyn;  // 4 quadrants x 16 values per lane x 32 lanes
+  if (wk == 1) {
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          red[(wq * 8 + (mt * 4 + nt * 2 + h)) * 32 + lane] = make_double2(cre[mt][nt][h], cim[mt][nt][h]);
+  }
+  __syncthreads();
+  if (wk == 0) {
+#pragma unroll
+    for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const double2 o = red[(wq * 8 + (mt * 4 + nt * 2 + h)) * 32 + lane];
+          cre[mt][nt][h] += o.x;
+          cim[mt][nt][h] += o.y;
+        }
+  }
+  if (KS > 1) {
+    // cluster split-K: ranks > 0 publish their tile, rank 0 sums in rank order
+    cg::cluster_group cl = cg::this_cluster();
+    __syncthreads();
+    if (wk == 0 && rank > 0) {
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            red[(wq * 8 + (mt * 4 + nt * 2 + h)) * 32 + lane] = make_double2(cre[mt][nt][h], cim[mt][nt][h]);
+    }
+    cl.sync();
+    if (rank == 0 && wk == 0) {
+      for (int src = 1; src < KS; ++src) {
+        const double2* rem = cl.map_shared_rank(red, src);
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const double2 o = rem[(wq * 8 + (mt * 4 + nt * 2 + h)) * 32 + lane];
+              cre[mt][nt][h] += o.x;
+              cim[mt][nt][h] += o.y;
+            }
+      }
+    }
+    cl.sync();  // keep remote shared memory alive until rank 0 has read it
+    if (rank != 0) return;
+  }
+  if (wk != 0) return;
 
   // epilogue: C(row gid, cols 2 tig + {0,1}) of each 8x8 tile
 #pragma unroll
@@ -177,13 +249,30 @@ __global__ void __launch_bounds__(THREADS) k_zmma(const MmaTask* __restrict__ ta
   }
 }
 
-constexpr size_t kZmmaSmem = sizeof(double2) * STAGES * KC * (BM + BN);
+constexpr size_t kZmmaSmem = sizeof(double2) * STAGES * kStageElems;
 
 void launch_zmma(Ctx& c, const DevMma& m, const double2* A, const double2* srcA, const double2* srcB,
                  const Epi& e, int R) {
   if (m.ntasks == 0) return;
+  // split K over a cluster when the step has too few tasks to fill the GPU
+  const int minK = m.minK;
+  int KS = 1;
+  while (KS < 4 && (long long)m.ntasks * KS < 2LL * c.num_sms && minK / KC >= 4 * KS * 2) KS *= 2;
   c.launches++;
-  k_zmma<<<m.ntasks, THREADS, kZmmaSmem, c.stream>>>(m.tasks, m.cols, A, srcA, srcB, e, c.n, R);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(m.ntasks * KS);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = kZmmaSmem;
+  cfg.stream = c.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = KS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k_zmma, (const MmaTask*)m.tasks, (const MmaCol*)m.cols, A, srcA, srcB, e,
+                     c.n, R, KS);
 }
 
 cudaError_t set_zmma_smem_limit() {
