@@ -86,7 +86,7 @@ int hs_set_dirichlet(hs_ctx* ctx, int i1, int i2, const int32_t* cells, int ncel
  * from HBM by the step kernels (default); 1 = shared-operator mode: only the
  * distinct operators' 4n x 4n maps are kept (the reference matrix depends
  * only on the Dirichlet cells, discretization.py:224-229) and every step is a
- * DMMA contraction with the map L2-resident (needs n % 16 == 0). */
+ * DMMA contraction with the map L2-resident (needs n % 32 == 0). */
 int hs_set_map_mode(hs_ctx* ctx, int mode);
 
 /* Build every subdomain's interface Schur map on the GPU (block-tridiagonal

@@ -343,7 +343,7 @@ int run_step(Ctx* c, DevStep& st, const double2* srcA, const double2* srcB, Epi 
   // when n is not a multiple of the 16-wide K chunk)
   DevMma* mm = nullptr;
   const bool shared = c->map_mode == 1;
-  if (st.nitems > 0 && (shared || (R > 1 && c->n % 16 == 0)))
+  if (st.nitems > 0 && (shared || (R > 1 && c->n % 32 == 0)))
     if (make_mma(c, st, R, shared, &mm)) return -1;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (c->timing && st.ntiles > 0) {
@@ -752,8 +752,8 @@ int hs_factor(hs_ctx* c) {
     }
     if (upload(c, &dtl, tl) || upload(c, &dfaces, faces) || upload(c, &dcls, cls) || upload(c, &dT4s, T4s)) return -1;
     launch_scatter_T(*c, dtl, (int)tl.size(), dfaces, dcls, dT4s);
-  } else if (n % 16 != 0) {
-    return fail(c, 1, "shared-map mode needs cells_per_side divisible by 16");
+  } else if (n % 32 != 0) {
+    return fail(c, 1, "shared-map mode needs cells_per_side divisible by 32");
   }
   CK(cudaGetLastError());
   int bad = 0;

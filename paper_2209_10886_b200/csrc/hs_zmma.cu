@@ -12,8 +12,8 @@
 // A task = 32 map rows x up to 32 columns.  A is read from the strip-major map
 // layout (a 32-row strip is contiguous, K x 32), B columns are gathered per
 // face from the vector (column descriptor: per-face element offset or -1,
-// stride R between consecutive face positions).  K is staged in chunks of 16
-// through a 4-stage cp.async pipeline.  8 warps: 4 output quadrants (16 x 16 =
+// stride R between consecutive face positions).  K is staged in chunks of 32
+// through a 3-stage cp.async pipeline.  8 warps: 4 output quadrants (16 x 16 =
 // 2 x 2 DMMA tiles, real and imaginary accumulators; a complex MAC is 4 real
 // DMMAs) x 2 halves of every K chunk, reduced through shared memory.  When a
 // step has few tasks the K range is also split over a thread-block cluster of
@@ -32,8 +32,11 @@ namespace hs {
 
 namespace {
 
-constexpr int BM = 32, BN = 32, KC = 16, STAGES = 4, THREADS = 256;
-constexpr int kStageElems = KC * (BM + BN);
+constexpr int BM = 32, BN = 32, KC = 32, STAGES = 3, THREADS = 256;
+// row stride 34 (not 32): the 8 lanes of a 128-bit shared-load phase (4 k rows x
+// 2 columns) then hit 8 distinct 16-byte bank groups
+constexpr int SA = BM + 2, SB = BN + 2;
+constexpr int kStageElems = KC * (SA + SB);
 
 __device__ __forceinline__ void cp16(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -91,8 +94,8 @@ __global__ void __launch_bounds__(THREADS) k_zmma(const MmaTask* __restrict__ ta
   const int kc0 = (int)((long long)nk_all * rank / KS), kc1 = (int)((long long)nk_all * (rank + 1) / KS);
   const int nk = kc1 - kc0;
 
-  auto As = [&](int st, int k, int m) -> double2& { return dyn[st * kStageElems + k * BM + m]; };
-  auto Bs = [&](int st, int k, int j) -> double2& { return dyn[st * kStageElems + KC * BM + k * BN + j]; };
+  auto As = [&](int st, int k, int m) -> double2& { return dyn[st * kStageElems + k * SA + m]; };
+  auto Bs = [&](int st, int k, int j) -> double2& { return dyn[st * kStageElems + KC * SA + k * SB + j]; };
 
   auto load = [&](int stage, int kc) {
     const int k0 = kc * KC;
@@ -100,7 +103,7 @@ __global__ void __launch_bounds__(THREADS) k_zmma(const MmaTask* __restrict__ ta
 #pragma unroll
     for (int i = 0; i < (KC * BM) / THREADS; ++i) {
       const int el = tid + i * THREADS;
-      cp16(&dyn[stage * kStageElems + el], asrc + el);
+      cp16(&As(stage, el / BM, el % BM), asrc + el);
     }
     const int q = k0 / n, p0 = k0 - q * n;
 #pragma unroll
@@ -142,23 +145,39 @@ __global__ void __launch_bounds__(THREADS) k_zmma(const MmaTask* __restrict__ ta
     if (nxt < nk) load(nxt % STAGES, kc0 + nxt);
     cp_commit();
     const int st = i % STAGES;
+    const int kb = wk * (KC / 2);
+    double2 a[2], b[2], an[2], bn[2];
 #pragma unroll
-    for (int k4 = wk * 8; k4 < wk * 8 + 8; k4 += 4) {
-      double2 a[2], b[2];
+    for (int mt = 0; mt < 2; ++mt) a[mt] = As(st, kb + tig, wm * 16 + mt * 8 + gid);
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt) a[mt] = As(st, k4 + tig, wm * 16 + mt * 8 + gid);
+    for (int nt = 0; nt < 2; ++nt) b[nt] = Bs(st, kb + tig, wn * 16 + nt * 8 + gid);
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) b[nt] = Bs(st, k4 + tig, wn * 16 + nt * 8 + gid);
+    for (int k4 = 0; k4 < KC / 2; k4 += 4) {
+      if (k4 + 4 < KC / 2) {  // prefetch the next fragments before issuing this step's DMMAs
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) an[mt] = As(st, kb + k4 + 4 + tig, wm * 16 + mt * 8 + gid);
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) bn[nt] = Bs(st, kb + k4 + 4 + tig, wn * 16 + nt * 8 + gid);
+      }
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
         const double nai = -a[mt].y;
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) {
           dmma(cre[mt][nt][0], cre[mt][nt][1], a[mt].x, b[nt].x);
-          dmma(cre[mt][nt][0], cre[mt][nt][1], nai, b[nt].y);
           dmma(cim[mt][nt][0], cim[mt][nt][1], a[mt].x, b[nt].y);
+        }
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          dmma(cre[mt][nt][0], cre[mt][nt][1], nai, b[nt].y);
           dmma(cim[mt][nt][0], cim[mt][nt][1], a[mt].y, b[nt].x);
         }
+      }
+      if (k4 + 4 < KC / 2) {
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) a[mt] = an[mt];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) b[nt] = bn[nt];
       }
     }
   }
@@ -257,7 +276,7 @@ void launch_zmma(Ctx& c, const DevMma& m, const double2* A, const double2* srcA,
   // split K over a cluster when the step has too few tasks to fill the GPU
   const int minK = m.minK;
   int KS = 1;
-  while (KS < 4 && (long long)m.ntasks * KS < 2LL * c.num_sms && minK / KC >= 4 * KS * 2) KS *= 2;
+  while (KS < 4 && (long long)m.ntasks * KS < 2LL * c.num_sms && minK / KC >= 2 * KS * 2) KS *= 2;
   c.launches++;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(m.ntasks * KS);

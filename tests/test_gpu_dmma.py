@@ -88,7 +88,7 @@ def test_shared_mode_cfg5_gmres():
     assert relerr(s.apply_interface_operator(res.solution), b) < 1e-6
 
 
-def test_shared_mode_needs_n_multiple_of_16():
+def test_shared_mode_needs_n_multiple_of_32():
     spec, part = product_problem(small_case(2, 2, 8))
     with pytest.raises(ValueError):
         GpuInterfaceSystem(spec, part, maps="shared")
