@@ -130,6 +130,12 @@ int hs_half_apply(hs_ctx* ctx, int direction, const double* r, double* z, int nr
 int hs_gmres(hs_ctx* ctx, int pc_kind, const double* b, double* x, int nrhs, double tol,
              int maxit, int* iters, double* hist, int* converged, int mem);
 
+/* Arnoldi implementation: 0 = auto (one cooperative MGS kernel per iteration
+ * on a single GPU; host-driven MGS with one ncclAllReduce per inner product
+ * across row bands), 1 = force the host-driven MGS (single-GPU test of the
+ * sharded algorithm). */
+int hs_set_gmres_mode(hs_ctx* ctx, int mode);
+
 /* ---- introspection (plan-only contexts too) ---------------------------- */
 /* Sizes: L (= 2 N_e n), number of subdomains, number of groups, 2 N_e. */
 int hs_sizes(const hs_ctx* ctx, int64_t* L, int* nsub, int* ngroups, int* npairs);

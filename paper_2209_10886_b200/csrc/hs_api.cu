@@ -21,6 +21,18 @@ using namespace hs;
 
 struct hs_ctx : public Ctx {};
 
+namespace hs {
+// One in-place sum over the ranks of the context (GMRES inner products).
+cudaError_t allreduce_sum_doubles(Ctx& c, double* buf, size_t count, void* comm) {
+  ncclResult_t r = ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, (ncclComm_t)comm, c.stream);
+  if (r != ncclSuccess) {
+    c.err = std::string("ncclAllReduce: ") + ncclGetErrorString(r);
+    return cudaErrorUnknown;
+  }
+  return cudaSuccess;
+}
+}  // namespace hs
+
 static std::string g_create_err;
 
 #define HS_VERSION "hsb200 0.1.0 sm_100a complex128"
@@ -637,6 +649,7 @@ int hs_destroy(hs_ctx* c) {
     for (auto& oc : c->classes) cudaFree(oc.T4);
     cudaFree(c->T);
     cudaFree(c->Tcls);
+    cudaFree(c->d_owned);
     cudaFree(c->dsubs);
     cudaFree(c->d_seam[0]);
     cudaFree(c->d_seam[1]);
@@ -924,8 +937,10 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
   if (int e = check_ready(c, R)) return e;
   if (!(tol > 0) || maxit < 1) return fail(c, 1, "tol must be > 0 and maxit >= 1");
   if (pc < HS_PC_NONE || pc > HS_PC_BSP) return fail(c, 1, "unknown preconditioner kind");
-  if (c->plan.nranks > 1) return fail(c, 3, "hs_gmres across row bands is not implemented yet");
   if (R & (R - 1)) return fail(c, 1, "batched GMRES needs nrhs a power of two");
+  // Arnoldi: one cooperative kernel per iteration on one GPU; across row bands
+  // (or when forced) the host-driven MGS over owned blocks + allreduce per dot
+  const bool dist = c->plan.nranks > 1 || c->gmres_mode == 1;
   const long long LR = LRof(c, R);
   if (LR == 0) {  // empty interface system (1 x 1 lattice): 0 iterations
     for (int r = 0; r < R; ++r) {
@@ -939,8 +954,19 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
   double2* dx;
   if (dev_in(c, b, LR, mem, "gin", &db) || dev_out(c, x, LR, mem, "gout", &dx)) return -1;
   int chunk = 0;
-  int grid = gmres_coop_grid(*c, LR, R, &chunk);
+  int grid = dist ? 2 * c->num_sms : gmres_coop_grid(*c, LR, R, &chunk);
   if (grid <= 0) return fail(c, 3, "interface vector too large for the cooperative Arnoldi kernel");
+  double2 *part2 = nullptr, *mgsout = nullptr;
+  if (dist) {
+    if (!c->d_owned) {
+      std::vector<int> owned;
+      for (int m = 0; m < c->plan.npairs; ++m)
+        if (c->plan.subs[c->plan.block_sub[m]].rank == c->plan.rank) owned.push_back(m);
+      if (upload(c, &c->d_owned, owned)) return -1;
+      c->n_owned = (int)owned.size();
+    }
+    if (ws_get(c, "part2", (size_t)grid * 2 * R, &part2) || ws_get(c, "mgsout", (size_t)2 * R, &mgsout)) return -1;
+  }
   GmresDev G;
   G.LR = LR; G.R = R; G.tol = tol;
   double2 *V, *Z;
@@ -965,7 +991,8 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
   G.wnorm0 = G.beta + R;
   G.cs = G.wnorm0 + R;
   G.active = ints; G.iters = ints + R; G.conv = ints + 2 * R; G.brk = ints + 3 * R; G.nactive = ints + 4 * R;
-  CK(gmres_init(*c, G, db));
+  if (dist) CK(gmres_init_dist(*c, G, db, c->d_owned, c->n_owned, part2, mgsout, c->nccl));
+  else CK(gmres_init(*c, G, db));
   int nact = 0;
   CK(cudaMemcpyAsync(&nact, G.nactive, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
@@ -979,7 +1006,8 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
       zin = Z;
     }
     if (do_apply(c, HS_APPLY_IMS, zin, w, R)) return -1;
-    CK(gmres_arnoldi(*c, G, k, grid, chunk));
+    if (dist) CK(gmres_arnoldi_dist(*c, G, k, c->d_owned, c->n_owned, part2, mgsout, c->nccl));
+    else CK(gmres_arnoldi(*c, G, k, grid, chunk));
     CK(gmres_givens(*c, G, k));
     CK(cudaMemcpyAsync(&nact, G.nactive, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
@@ -1186,6 +1214,13 @@ int hs_stream(hs_ctx* c, uint64_t* s) {
   if (!c) return 1;
   NEED_GPU(c);
   *s = (uint64_t)(uintptr_t)c->stream;
+  return 0;
+}
+
+int hs_set_gmres_mode(hs_ctx* c, int mode) {
+  if (!c) return fail(nullptr, 1, "null context");
+  if (mode != 0 && mode != 1) return fail(c, 1, "gmres mode must be 0 (auto) or 1 (host-driven MGS)");
+  c->gmres_mode = mode;
   return 0;
 }
 

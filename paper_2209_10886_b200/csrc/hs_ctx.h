@@ -147,6 +147,9 @@ struct Ctx {
   double2* recv_up = nullptr; double2* recv_dn = nullptr;
   size_t xbuf_cap = 0;
   void* nccl = nullptr;  // ncclComm_t
+  int gmres_mode = 0;    // 0 auto (cooperative MGS on one rank), 1 host-driven MGS over owned blocks
+  int* d_owned = nullptr;  // this rank's blocks (host-driven MGS)
+  int n_owned = 0;
   // execution control / timing
   int async_mode = 0;
   bool timing = false;

@@ -73,5 +73,12 @@ cudaError_t gmres_arnoldi(Ctx& c, GmresDev& G, int k, int grid, int chunk);
 cudaError_t gmres_givens(Ctx& c, GmresDev& G, int k);
 cudaError_t gmres_finish(Ctx& c, GmresDev& G, int maxit, double2* u);
 int gmres_coop_grid(Ctx& c, long long LR, int R, int* chunk);
+// host-driven MGS over owned blocks (+ one ncclAllReduce per inner product when comm != null)
+cudaError_t gmres_arnoldi_dist(Ctx& c, GmresDev& G, int k, const int* blocks, int nb, double2* part,
+                               double2* out, void* nccl_comm);
+cudaError_t gmres_init_dist(Ctx& c, GmresDev& G, const double2* b, const int* blocks, int nb,
+                            double2* part, double2* out, void* nccl_comm);
+// in-place sum over ranks (implemented next to the NCCL calls in hs_api.cu)
+cudaError_t allreduce_sum_doubles(Ctx& c, double* buf, size_t count, void* nccl_comm);
 
 }  // namespace hs

@@ -194,10 +194,16 @@ __global__ void k_colnorm_partial(const double2* x, long long LR, int R, int chu
   if (threadIdx.x < R) part[(long long)blockIdx.x * R + threadIdx.x] = red[threadIdx.x];
 }
 
-__global__ void k_gmres_init(GmresDev G, int nblk) {
+// nblk >= 0: reduce G.partial[nblk][R]; nblk < 0: pre[r].x already holds |b_r|^2
+__global__ void k_gmres_init(GmresDev G, int nblk, const double2* pre) {
   extern __shared__ double2 red[];
   double2* out = red + blockDim.x;
-  grid_colsum(G.partial, nblk, G.R, red, out);
+  if (nblk >= 0) {
+    grid_colsum(G.partial, nblk, G.R, red, out);
+  } else {
+    for (int r = threadIdx.x; r < G.R; r += blockDim.x) out[r] = pre[r];
+    __syncthreads();
+  }
   __shared__ int cnt;
   if (threadIdx.x == 0) cnt = 0;
   __syncthreads();
@@ -296,7 +302,7 @@ cudaError_t gmres_init(Ctx& c, GmresDev& G, const double2* b) {
   int nblk = (int)((G.LR + ch - 1) / ch);
   c.launches += 3;
   k_colnorm_partial<<<nblk, bs, bs * sizeof(double2), c.stream>>>(b, G.LR, R, (int)ch, G.partial);
-  k_gmres_init<<<1, bs, (bs + R) * sizeof(double2), c.stream>>>(G, nblk);
+  k_gmres_init<<<1, bs, (bs + R) * sizeof(double2), c.stream>>>(G, nblk, nullptr);
   int g2 = (int)std::min<long long>((G.LR + 255) / 256, (long long)c.num_sms * 8);
   k_scale_cols<<<g2 > 0 ? g2 : 1, 256, 0, c.stream>>>(G.V, b, G.beta, G.LR, R);
   return cudaGetLastError();
@@ -319,6 +325,146 @@ cudaError_t gmres_givens(Ctx& c, GmresDev& G, int k) {
   int bs = G.R < 1024 ? ((G.R + 31) / 32) * 32 : 1024;
   c.launches++;
   k_givens<<<1, bs, 0, c.stream>>>(G, k);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// MGS across row bands (and the single-GPU host-driven variant of the same
+// algorithm): each rank owns whole blocks of every Krylov vector.  For every j
+// one kernel applies the previous projection and forms this rank's partial
+// inner products over its owned blocks (fixed-order block reduction), one
+// CTA reduces the partials in a fixed order, and -- with several ranks -- one
+// ncclAllReduce of R complex values makes h_jk identical on every rank, so
+// the Givens rotations (k_givens) stay replicated.  No host round trip per j.
+
+// mode 0: out = (|w|^2, <v_j, w>)            (j = 0; |w| before orthogonalisation)
+// mode 1: w -= h v_{j-1}; out = <v_j, w>      (1 <= j <= k)
+// mode 2: w -= h v_k; out = |w|^2
+// mode 3: w /= |w| (h = allreduced |w|^2), writes H[k+1] and wnorm0 handled by caller
+__global__ void k_mgs_dist(GmresDev G, const int* __restrict__ blocks, int nb, int nR, int k, int j,
+                           int mode, const double2* __restrict__ h, double2* part) {
+  extern __shared__ double2 red[];
+  const int R = G.R;
+  const long long LR = G.LR;
+  double2* w = G.V + (long long)(k + 1) * LR;
+  const double2* vj = G.V + (long long)j * LR;
+  const double2* vp = mode == 1 ? G.V + (long long)(j - 1) * LR : (mode == 2 ? G.V + (long long)k * LR : nullptr);
+  const long long total = (long long)nb * nR;
+  double2 a0 = make_double2(0, 0), a1 = make_double2(0, 0);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long e = (long long)blocks[i / nR] * nR + i % nR;
+    const int r = (int)(e % R);
+    double2 x = w[e];
+    if (mode == 1 || mode == 2) {
+      x = csub(x, cmul(h[r], vp[e]));
+      w[e] = x;
+    } else if (mode == 3) {
+      const double hn = sqrt(h[r].x);
+      w[e] = hn > 0 ? make_double2(x.x / hn, x.y / hn) : make_double2(0, 0);
+      continue;
+    }
+    if (mode == 0) {
+      a0.x += x.x * x.x + x.y * x.y;
+      cfma_conj(a1, vj[e], x);
+    } else if (mode == 1) {
+      cfma_conj(a1, vj[e], x);
+    } else {
+      a0.x += x.x * x.x + x.y * x.y;
+    }
+  }
+  if (mode == 3) return;
+  // per-column block reduction (thread's column fixed: blockDim % R == 0, nR % R == 0)
+  red[threadIdx.x] = a0;
+  block_colsum(red, R);
+  if (threadIdx.x < R) part[(long long)blockIdx.x * 2 * R + threadIdx.x] = red[threadIdx.x];
+  __syncthreads();
+  red[threadIdx.x] = a1;
+  block_colsum(red, R);
+  if (threadIdx.x < R) part[(long long)blockIdx.x * 2 * R + R + threadIdx.x] = red[threadIdx.x];
+}
+
+// out[0..2R) = fixed-order sum of part[g][0..2R) over g < ngrid
+__global__ void k_mgs_reduce(const double2* part, int ngrid, int R, double2* out) {
+  for (int t = threadIdx.x; t < 2 * R; t += blockDim.x) {
+    double2 s = make_double2(0, 0);
+    for (int g = 0; g < ngrid; ++g) s = cadd(s, part[(long long)g * 2 * R + t]);
+    out[t] = s;
+  }
+}
+
+// record the allreduced values: j == 0 -> wnorm0 and H[0]; 1..k -> H[j]; j == k+1 -> H[k+1] = |w|
+__global__ void k_mgs_commit(GmresDev G, int k, int j, const double2* out) {
+  const int R = G.R;
+  double2* Hk = G.H + hoff(k, R);
+  for (int r = threadIdx.x; r < R; r += blockDim.x) {
+    if (j == 0) {
+      G.wnorm0[r] = sqrt(out[r].x);
+      Hk[r] = out[R + r];
+    } else if (j <= k) {
+      Hk[(long long)j * R + r] = out[R + r];
+    } else {
+      Hk[(long long)(k + 1) * R + r] = make_double2(sqrt(out[r].x), 0);
+    }
+  }
+}
+
+cudaError_t gmres_arnoldi_dist(Ctx& c, GmresDev& G, int k, const int* blocks, int nb, double2* part,
+                               double2* out, void* nccl_comm) {
+  const int R = G.R;
+  const int bs = coop_block(R);
+  const int nR = c.n * R;
+  const int grid = c.num_sms * 2;
+  const size_t smem = bs * sizeof(double2);
+  auto allreduce = [&]() -> cudaError_t {
+    if (!nccl_comm) return cudaSuccess;
+    return allreduce_sum_doubles(c, (double*)out, 4 * R, nccl_comm);
+  };
+  // j = 0: (|w|^2, <v_0, w>)
+  c.launches += 3;
+  k_mgs_dist<<<grid, bs, smem, c.stream>>>(G, blocks, nb, nR, k, 0, 0, out, part);
+  k_mgs_reduce<<<1, 256, 0, c.stream>>>(part, grid, R, out);
+  if (cudaError_t e = allreduce()) return e;
+  k_mgs_commit<<<1, 256, 0, c.stream>>>(G, k, 0, out);
+  for (int j = 1; j <= k; ++j) {
+    // h_{j-1} = out[R..2R)
+    c.launches += 3;
+    k_mgs_dist<<<grid, bs, smem, c.stream>>>(G, blocks, nb, nR, k, j, 1, out + R, part);
+    k_mgs_reduce<<<1, 256, 0, c.stream>>>(part, grid, R, out);
+    if (cudaError_t e = allreduce()) return e;
+    k_mgs_commit<<<1, 256, 0, c.stream>>>(G, k, j, out);
+  }
+  c.launches += 4;
+  k_mgs_dist<<<grid, bs, smem, c.stream>>>(G, blocks, nb, nR, k, k, 2, out + R, part);
+  k_mgs_reduce<<<1, 256, 0, c.stream>>>(part, grid, R, out);
+  if (cudaError_t e = allreduce()) return e;
+  k_mgs_commit<<<1, 256, 0, c.stream>>>(G, k, k + 1, out);
+  k_mgs_dist<<<grid, bs, smem, c.stream>>>(G, blocks, nb, nR, k, k, 3, out, part);
+  return cudaGetLastError();
+}
+
+// beta over owned blocks (+ allreduce), then the usual init
+cudaError_t gmres_init_dist(Ctx& c, GmresDev& G, const double2* b, const int* blocks, int nb,
+                            double2* part, double2* out, void* nccl_comm) {
+  const int R = G.R;
+  const int bs = coop_block(R);
+  const int nR = c.n * R;
+  const int grid = c.num_sms * 2;
+  // |b|^2 via mode 2 on a scratch copy is avoidable: reuse k_mgs_dist on V[0] = b
+  cudaError_t e = cudaMemcpyAsync(G.V, b, G.LR * sizeof(double2), cudaMemcpyDeviceToDevice, c.stream);
+  if (e != cudaSuccess) return e;
+  // mode 0 with k = -1: w = V[0], v_j = V[0] -> out[0..R) = |b|^2
+  c.launches += 2;
+  k_mgs_dist<<<grid, bs, bs * sizeof(double2), c.stream>>>(G, blocks, nb, nR, -1, 0, 0, out, part);
+  k_mgs_reduce<<<1, 256, 0, c.stream>>>(part, grid, R, out);
+  if (nccl_comm) {
+    e = allreduce_sum_doubles(c, (double*)out, 4 * R, nccl_comm);
+    if (e != cudaSuccess) return e;
+  }
+  c.launches += 2;
+  k_gmres_init<<<1, bs, (bs + R) * sizeof(double2), c.stream>>>(G, -1, out);
+  int g2 = (int)std::min<long long>((G.LR + 255) / 256, (long long)c.num_sms * 8);
+  k_scale_cols<<<g2 > 0 ? g2 : 1, 256, 0, c.stream>>>(G.V, b, G.beta, G.LR, R);
   return cudaGetLastError();
 }
 

@@ -308,8 +308,15 @@ class GpuInterfaceSystem:
         return schedule_records(self.ctx, self.partition, kind, self.sweep)
 
     # ---- SPEC.md:399-407 on the device
-    def gmres(self, b, kind: str | None = None, tol: float = 1e-6, maxit: int = 200) -> GmresResult:
+    def gmres(self, b, kind: str | None = None, tol: float = 1e-6, maxit: int = 200,
+              arnoldi: str = "auto") -> GmresResult:
+        """arnoldi = "auto" (one cooperative MGS kernel per iteration; host-driven
+        MGS with an allreduce per inner product across row bands) or "hostloop"
+        (force the sharded algorithm on one GPU)."""
         kind = self.sweep.kind if kind is None else kind
+        if arnoldi not in ("auto", "hostloop"):
+            raise ValueError(f"arnoldi must be 'auto' or 'hostloop', got {arnoldi!r}")
+        self.ctx.call("hs_set_gmres_mode", 1 if arnoldi == "hostloop" else 0)
         v = _Vec(self.layout.check(b), self.layout.size)
         out, optr = v.empty()
         R = v.R

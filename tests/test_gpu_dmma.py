@@ -92,3 +92,28 @@ def test_shared_mode_needs_n_multiple_of_32():
     spec, part = product_problem(small_case(2, 2, 8))
     with pytest.raises(ValueError):
         GpuInterfaceSystem(spec, part, maps="shared")
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_hostloop_mgs_equals_cooperative(k):
+    """The sharded Arnoldi (host-driven MGS over owned blocks, the algorithm run
+    across row bands with one allreduce per inner product) on one GPU."""
+    s = system(k, "subdomain")
+    b = s.rhs()
+    a = s.gmres(b, "bsp", tol=1e-6, maxit=1000, arnoldi="auto")
+    h = s.gmres(b, "bsp", tol=1e-6, maxit=1000, arnoldi="hostloop")
+    assert h.iterations == a.iterations and h.converged
+    assert relerr(h.solution, a.solution) < 1e-12
+    np.testing.assert_allclose(h.history, a.history, rtol=1e-10)
+
+
+def test_hostloop_mgs_batched_cfg4():
+    import math
+    from paper_2209_10886_b200.configs import angles
+    s = system(4, "subdomain")
+    dirs = [(math.cos(t), math.sin(t)) for t in angles(CONFIGS[4])][:8]
+    B = s.rhs(directions=dirs)
+    a = s.gmres(B, "bsp", tol=1e-6, maxit=1000)
+    h = s.gmres(B, "bsp", tol=1e-6, maxit=1000, arnoldi="hostloop")
+    assert h.iterations == a.iterations
+    assert relerr(h.solution, a.solution) < 1e-12
