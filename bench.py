@@ -324,14 +324,17 @@ def main():
             from paper_2209_10886_b200.configs import angles
             b = sysm.rhs(directions=[(float(np.cos(t)), float(np.sin(t))) for t in angles(c)])
         sysm.gmres(b, "bsp", tol=c["tol"], maxit=1000)  # warm (workspace allocation)
+        barrier()
         t1 = time.perf_counter()
         res = sysm.gmres(b, "bsp", tol=c["tol"], maxit=1000)
-        tts = time.perf_counter() - t1
-        resid = np.linalg.norm(sysm.apply_interface_operator(res.solution) - b, axis=0) / np.linalg.norm(b, axis=0)
+        tts = max_over_ranks(time.perf_counter() - t1)  # synchronous call: host time brackets the device work
         its = res.iterations if R == 1 else max(res.iterations)
         conv = res.converged if R == 1 else all(res.converged)
-        return {"time_to_solution_s": tts, "iterations": its, "converged": bool(conv),
-                "true_relative_residual": float(np.max(resid))}
+        out = {"time_to_solution_s": tts, "iterations": its, "converged": bool(conv)}
+        if world == 1:  # with row bands each rank holds only its own blocks of x
+            resid = np.linalg.norm(sysm.apply_interface_operator(res.solution) - b, axis=0) / np.linalg.norm(b, axis=0)
+            out["true_relative_residual"] = float(np.max(resid))
+        return out
 
     m = measure(system, args.steps, args.warmup, True)
     ms_per = m["ms_per"]
@@ -392,7 +395,7 @@ def main():
 
     gm = None
     variants = {}
-    if world == 1 and not args.no_gmres:
+    if not args.no_gmres:
         gm = gmres_tts(system)
         gm["setup_s"] = setup_s
     if world == 1 and not args.no_variants and c["n"] % 16 == 0:

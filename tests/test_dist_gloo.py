@@ -155,8 +155,54 @@ class Band:
     def owned_mask(self):
         return np.repeat(self.owner == self.rank, self.n)
 
+    def gmres(self, b, tol=1e-6, maxit=200):
+        """Right-preconditioned MGS GMRES with every inner product reduced over
+        the ranks (the algorithm of gmres_arnoldi_dist: partial dots over owned
+        blocks, one all-reduce each, Givens replicated on every rank)."""
+        from oracle.gmres import givens
+        m = self.owned_mask()
 
-def _worker(rank, world, port, case, blocks, q):
+        def dot(u, v):
+            t = torch.tensor([complex(np.vdot(u[m], v[m]))], dtype=torch.complex128)
+            t = torch.view_as_real(t).contiguous()
+            dist.all_reduce(t)
+            return complex(t[0, 0].item(), t[0, 1].item())
+
+        beta = abs(dot(b, b)) ** 0.5
+        V = [np.where(m, b / beta, 0)]
+        H = np.zeros((maxit + 1, maxit), complex)
+        cs, sn = np.zeros(maxit), np.zeros(maxit, complex)
+        g = np.zeros(maxit + 1, complex)
+        g[0] = beta
+        k_done = 0
+        for k in range(maxit):
+            w = self.apply_A(self.bsp(V[k]))
+            w = np.where(m, w, 0)
+            for j in range(k + 1):
+                H[j, k] = dot(V[j], w)
+                w = w - H[j, k] * V[j]
+            hn = abs(dot(w, w)) ** 0.5
+            H[k + 1, k] = hn
+            for j in range(k):
+                t = cs[j] * H[j, k] + sn[j] * H[j + 1, k]
+                H[j + 1, k] = -np.conj(sn[j]) * H[j, k] + cs[j] * H[j + 1, k]
+                H[j, k] = t
+            c, s_ = givens(H[k, k], H[k + 1, k].real)
+            cs[k], sn[k] = c, s_
+            H[k, k] = c * H[k, k] + s_ * H[k + 1, k]
+            H[k + 1, k] = 0
+            g[k + 1] = -np.conj(s_) * g[k]
+            g[k] = c * g[k]
+            k_done = k + 1
+            if abs(g[k + 1]) / beta <= tol:
+                break
+            V.append(w / hn)
+        y = np.linalg.solve(np.triu(H[:k_done, :k_done]), g[:k_done])
+        u = sum(y[i] * V[i] for i in range(k_done))
+        return self.bsp(u), k_done
+
+
+def _worker(rank, world, port, case, blocks, q, with_gmres=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -170,8 +216,19 @@ def _worker(rank, world, port, case, blocks, q):
         zr = Preconditioner(ref_itf, "bsp", blocks=blocks)(r)
         ar = ref_itf.apply_A(r)
         m = band.owned_mask()
-        q.put((rank, float(np.abs(z[m] - zr[m]).max() / np.abs(zr).max()),
-               float(np.abs(a[m] - ar[m]).max() / np.abs(ar).max()), int(m.sum())))
+        res = [rank, float(np.abs(z[m] - zr[m]).max() / np.abs(zr).max()),
+               float(np.abs(a[m] - ar[m]).max() / np.abs(ar).max()), int(m.sum())]
+        if with_gmres:
+            from oracle.gmres import gmres
+            from oracle.schur import lifting_traces
+            home, tr = lifting_traces(band.prob, band.lat)
+            b = np.zeros(ref_itf.size, complex)
+            for f, j in band.lat.faces[home]:
+                b[ref_itf.block(band.lat.m_index(j, home))] = tr[f]
+            x, its = band.gmres(b)
+            ref = gmres(ref_itf.apply_A, Preconditioner(ref_itf, "bsp", blocks=blocks), b, tol=1e-6, maxit=200)
+            res += [its, ref.iterations, float(np.abs(x[m] - ref.x[m]).max() / np.abs(ref.x).max())]
+        q.put(tuple(res))
     finally:
         dist.destroy_process_group()
 
@@ -190,9 +247,29 @@ def test_sharded_bsp_matches_single_process(case, world, blocks):
         assert p.exitcode == 0
     L = None
     total = 0
-    for rank, ez, ea, owned in res:
+    for rank, ez, ea, owned in [r[:4] for r in res]:
         assert ez < 1e-13, (rank, ez)
         assert ea < 1e-13, (rank, ea)
         total += owned
     from oracle.lattice import Lattice
     assert total == Lattice(case["n1"], case["n2"]).n_pairs * case["n"]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_gmres_matches_single_process(world):
+    """Row-band GMRES (inner products all-reduced over the ranks, as in
+    gmres_arnoldi_dist) converges in the same iterations to the same x."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, CASE5, None, q, True)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in res:
+        its, ref_its, ex = r[4], r[5], r[6]
+        assert its == ref_its, (its, ref_its)
+        assert ex < 1e-10, ex
