@@ -99,6 +99,15 @@ int hs_factor(hs_ctx* ctx);
  * reference uses -u_inc, discretization.py:326-328).  b is [L][nrhs]. */
 int hs_lifting_rhs(hs_ctx* ctx, const double* vals, int nrhs, double* b, int mem);
 
+/* Field reconstruction (the driver's reconstruct_solution):
+ * u_i = v_i + w_i for every subdomain this rank owns, where v_i solves the
+ * subdomain with its incoming traces from g (solve_local,
+ * discretization.py:264-293) and w_i is the lifting with Dirichlet data
+ * lift_vals (as for hs_lifting_rhs; NULL -> no lifting), computed with the
+ * stored block factors; stitched into field, (N2 n) x (N1 n) complex, y slow
+ * (cells of other ranks' subdomains are zero). */
+int hs_reconstruct(hs_ctx* ctx, const double* g, const double* lift_vals, double* field, int mem);
+
 /* out = S g (mode HS_APPLY_S) or (I - S) g (HS_APPLY_IMS). */
 int hs_apply(hs_ctx* ctx, int mode, const double* g, double* out, int nrhs, int mem);
 

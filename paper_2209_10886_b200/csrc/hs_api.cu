@@ -856,6 +856,89 @@ int hs_lifting_rhs(hs_ctx* c, const double* vals, int nrhs, double* bout, int me
   return finish_out(c, bout, b, LR, mem);
 }
 
+int hs_reconstruct(hs_ctx* c, const double* g, const double* lift_vals, double* field, int mem) {
+  if (!c) return fail(nullptr, 1, "null context");
+  if (int e = check_ready(c, 1)) return e;
+  const int n = c->n;
+  const long long L = c->plan.L;
+  const long long F = (long long)c->n1 * c->n2 * n * n;
+  const double2* dg;
+  double2* df;
+  if (dev_in(c, g, L, mem, "rin", &dg) || dev_out(c, field, F, mem, "rout", &df)) return -1;
+  CK(cudaMemsetAsync(df, 0, F * sizeof(double2), c->stream));
+  const double ih2 = 1.0 / (c->h * c->h);
+  const std::complex<double> tau(c->tau_re, c->tau_im);
+  const std::complex<double> d = 1.0 / c->h - tau / 2.0;
+  const std::complex<double> rc = 1.0 / (c->h * c->h * d);  // rhs_coeff, discretization.py:141
+  // lifting data of each Dirichlet subdomain, ordinal order (as hs_lifting_rhs)
+  std::map<int, size_t> vstart;
+  size_t vpos = 0;
+  for (auto& kv : c->dcells) {
+    vstart[kv.first] = vpos;
+    vpos += kv.second.size();
+  }
+  for (size_t cl = 0; cl < c->classes.size(); ++cl) {
+    const OpClass& oc = c->classes[cl];
+    std::vector<int> face_off, col_ab, members;
+    for (int s = 0; s < c->plan.nsub; ++s) {
+      if (c->sub_class[s] != (int)cl || c->plan.subs[s].rank != c->plan.rank) continue;
+      const SubPlan& sp = c->plan.subs[s];
+      int fo[4] = {-1, -1, -1, -1};
+      for (int q = 0; q < sp.k; ++q) fo[sp.face[q]] = (sp.first_block + q) * n;
+      face_off.insert(face_off.end(), fo, fo + 4);
+      col_ab.push_back(sp.i1);
+      col_ab.push_back(sp.i2);
+      members.push_back(s);
+    }
+    const int R = (int)members.size();
+    if (R == 0) continue;
+    // lifting: Dirichlet data at the scatterer cells and its coupling into the
+    // free neighbours (eliminated form); Dirichlet cells on a face are not
+    // supported here (the disk must clear the subdomain edge by half a cell)
+    std::map<std::tuple<int, int, int>, double2> ex;
+    for (int col = 0; col < R; ++col) {
+      auto it = c->dcells.find(members[col]);
+      if (it == c->dcells.end() || it->second.empty()) continue;
+      for (int cell : it->second) {
+        const int k = cell / n, x = cell % n;
+        if (k == 0 || k == n - 1 || x == 0 || x == n - 1)
+          return fail(c, 1, "reconstruction: scatterer cells on a subdomain face are not supported");
+      }
+      if (!lift_vals) continue;
+      auto isd = [&](int k, int x) { return oc.mask[(size_t)k * n + x] != 0; };
+      const size_t v0 = vstart[members[col]];
+      for (size_t ci = 0; ci < it->second.size(); ++ci) {
+        const int k = it->second[ci] / n, x = it->second[ci] % n;
+        const double* v = lift_vals + 2 * (v0 + ci);
+        double2& e0 = ex[std::make_tuple(k, x, col)];
+        e0.x += v[0]; e0.y += v[1];
+        const int nb[4][2] = {{k - 1, x}, {k + 1, x}, {k, x - 1}, {k, x + 1}};
+        for (auto& q : nb) {
+          if (isd(q[0], q[1])) continue;
+          double2& e1 = ex[std::make_tuple(q[0], q[1], col)];
+          e1.x += ih2 * v[0]; e1.y += ih2 * v[1];
+        }
+      }
+    }
+    ExtraRHS er;
+    std::vector<void*> owned;
+    if (upload_extras(c, ex, er, owned)) return -1;
+    int *dfo, *dab;
+    uint8_t* dm;
+    if (upload(c, &dfo, face_off) || upload(c, &dab, col_ab) || upload(c, &dm, oc.mask)) return -1;
+    double2 *Y, *Bk;
+    CK(dalloc(c, (void**)&Y, (size_t)n * n * R * sizeof(double2)));
+    CK(dalloc(c, (void**)&Bk, (size_t)n * R * sizeof(double2)));
+    CK(solve_fields(*c, oc.X, dm, R, dg, dfo, make_double2(rc.real(), rc.imag()), er, Y, Bk));
+    launch_scatter_field(*c, df, c->n1 * n, Y, R, dab, 0);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(c->stream));
+    dfree(c, Y, 0); dfree(c, Bk, 0); dfree(c, dfo, 0); dfree(c, dab, 0); dfree(c, dm, 0);
+    for (void* p : owned) dfree(c, p, 0);
+  }
+  return finish_out(c, field, df, F, mem);
+}
+
 int hs_apply(hs_ctx* c, int mode, const double* g, double* out, int nrhs, int mem) {
   if (!c) return fail(nullptr, 1, "null context");
   if (int e = check_ready(c, nrhs)) return e;

@@ -42,6 +42,10 @@ void zgemm(cudaStream_t st, int M, int N, int K, double2 alpha, const double2* A
            long long sa, const double2* B, int ldb, long long sb, double2 beta, double2* C, int ldc,
            long long sc, int batch);
 void launch_make_T4(Ctx& c, double2* T4, const double2* G, int R, double2 a, double2 b);
+cudaError_t solve_fields(Ctx& c, const double2* X, const uint8_t* dmask, int R, const double2* g,
+                         const int* face_off, double2 coeff, const ExtraRHS& extras, double2* Y, double2* Bk);
+void launch_scatter_field(Ctx& c, double2* field, int nx_total, const double2* Y, int R, const int* col_ab,
+                          int accumulate);
 void launch_scatter_T(Ctx& c, const int2* tl, int ntiles, const int* sub_faces, const int* sub_cls,
                       double2* const* T4s);
 void launch_lift_b(Ctx& c, double2* b, const double2* G, int Rtot, int col0, int nrhs,

@@ -309,6 +309,50 @@ __global__ void k_rhs_fwd(double2* Bk, long long bstride, const double2* Y, long
   }
 }
 
+// Forward right-hand side of row k for the field solves of several subdomains
+// (one column each): F_k = rhs_coeff * (incoming traces scattered to the face
+// cells, corners get two faces; discretization.py:278-285) - C_{k-1} Y_{k-1}.
+// face_off[4 * col + f]: element offset of the subdomain's incoming block for
+// face f (W,S,N,E) in g, or -1.   grid (n, 1), block <= 256
+__global__ void k_rhs_traces(double2* Bk, const double2* Y, const uint8_t* mask, int n, int R, double ih2,
+                             int k, const double2* g, const int* face_off, double2 coeff) {
+  const int x = blockIdx.x;
+  const double cx = k > 0 ? coupling(mask, n, k - 1, x, ih2) : 0.0;
+  const double2* Yp = Y + ((long long)(k - 1) * n + x) * R;
+  double2* B = Bk + (long long)x * R;
+  for (int col = threadIdx.x; col < R; col += blockDim.x) {
+    const int* fo = face_off + 4 * col;
+    double2 t = make_double2(0, 0);
+    if (x == 0 && fo[0] >= 0) t = cadd(t, g[fo[0] + k]);          // W, position k
+    if (k == 0 && fo[1] >= 0) t = cadd(t, g[fo[1] + x]);          // S, position x
+    if (k == n - 1 && fo[2] >= 0) t = cadd(t, g[fo[2] + x]);      // N, position x
+    if (x == n - 1 && fo[3] >= 0) t = cadd(t, g[fo[3] + k]);      // E, position k
+    double2 v = cmul(coeff, t);
+    if (cx != 0.0) {
+      const double2 y = Yp[col];
+      v.x -= cx * y.x;
+      v.y -= cx * y.y;
+    }
+    B[col] = v;
+  }
+}
+
+// Stitch solved fields Y[k][x][col] into the global grid (y slow):
+// field[(b-1) n + k][(a-1) n + x] (+)= Y, one column per subdomain.
+__global__ void k_scatter_field(double2* field, int nx_total, const double2* Y, int n, int R,
+                                const int* col_ab, int accumulate) {
+  const long long total = (long long)n * n * R;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int col = (int)(i % R);
+    const long long cell = i / R;
+    const int k = (int)(cell / n), x = (int)(cell % n);
+    const int a = col_ab[2 * col], b = col_ab[2 * col + 1];
+    const long long o = ((long long)(b - 1) * n + k) * nx_total + (long long)(a - 1) * n + x;
+    field[o] = accumulate ? cadd(field[o], Y[i]) : Y[i];
+  }
+}
+
 // Sparse additions to F_k (Dirichlet data and its coupling to free cells).
 __global__ void k_rhs_extra(double2* Bk, long long bstride, int R, const int* ex_x, const int* ex_col,
                             const double2* ex_val, int cnt, int c) {
@@ -484,6 +528,44 @@ cudaError_t solve_boundary(Ctx& c, const double2* X, long long xstride, const ui
   }
   k_extract<<<dim3(4 * n, ncls), rthreads, 0, c.stream>>>(G, gstride, Y, ystride, n, R);
   return cudaGetLastError();
+}
+
+// Full fields of R subdomains of one operator class driven by their incoming
+// traces in g (+ sparse extras: the lifting's Dirichlet data), Y = n x n x R.
+cudaError_t solve_fields(Ctx& c, const double2* X, const uint8_t* dmask, int R, const double2* g,
+                         const int* face_off, double2 coeff, const ExtraRHS& extras, double2* Y, double2* Bk) {
+  const int n = c.n;
+  const double ih2 = 1.0 / (c.h * c.h);
+  const long long nn = (long long)n * n;
+  const int rthreads = R < 256 ? ((R + 31) / 32) * 32 : 256;
+  for (int k = 0; k < n; ++k) {
+    c.launches++;
+    k_rhs_traces<<<n, rthreads, 0, c.stream>>>(Bk, Y, dmask, n, R, ih2, k, g, face_off, coeff);
+    if (!extras.row_ptr.empty()) {
+      const int b0 = extras.row_ptr[k], b1 = extras.row_ptr[k + 1];
+      if (b1 > b0) {
+        c.launches++;
+        k_rhs_extra<<<(b1 - b0 + 255) / 256, 256, 0, c.stream>>>(Bk, 0, R, extras.d_x + b0, extras.d_col + b0,
+                                                                 extras.d_val + b0, b1 - b0, 0);
+      }
+    }
+    c.launches++;
+    zgemm(c.stream, n, R, n, make_double2(1, 0), X + k * nn, n, 0, Bk, R, 0, make_double2(0, 0),
+          Y + (long long)k * n * R, R, 0, 1);
+  }
+  for (int k = n - 2; k >= 0; --k) {
+    c.launches += 2;
+    k_rhs_bwd<<<dim3(n, 1), rthreads, 0, c.stream>>>(Bk, 0, Y, 0, dmask, n, R, ih2, k);
+    zgemm(c.stream, n, R, n, make_double2(-1, 0), X + k * nn, n, 0, Bk, R, 0, make_double2(1, 0),
+          Y + (long long)k * n * R, R, 0, 1);
+  }
+  return cudaGetLastError();
+}
+
+void launch_scatter_field(Ctx& c, double2* field, int nx_total, const double2* Y, int R, const int* col_ab,
+                          int accumulate) {
+  c.launches++;
+  k_scatter_field<<<4 * c.num_sms, 256, 0, c.stream>>>(field, nx_total, Y, c.n, R, col_ab, accumulate);
 }
 
 void launch_make_T4(Ctx& c, double2* T4, const double2* G, int R, double2 a, double2 b) {

@@ -258,6 +258,26 @@ class GpuInterfaceSystem:
             out[:, c0:c1] = self.apply_scattering(E)[:, :c1 - c0]
         return out
 
+    def reconstruct_solution(self, g, with_lifting: bool = True) -> np.ndarray:
+        """Stitched global field u_i = v_i + w_i as an
+        (N2 n) x (N1 n) complex array, y slow, computed on the GPU from the
+        stored block factors (v_i: solve_local with the incoming traces of g,
+        discretization.py:264-293; w_i: the lifting, :315-332)."""
+        g = np.ascontiguousarray(np.asarray(self.layout.check(g)), dtype=np.complex128)
+        if g.ndim != 1:
+            raise ValueError("reconstruct_solution takes one right-hand side")
+        n, P = self.n, self.partition
+        field = np.zeros((P.n2 * n, P.n1 * n), dtype=np.complex128)
+        lift = None
+        if with_lifting:
+            home, data = lifting_data(self.spec, P)
+            if home is not None:
+                lift = np.ascontiguousarray(data[:, 0])
+        self.ctx.call("hs_reconstruct", C.c_void_p(g.ctypes.data),
+                      C.c_void_p(lift.ctypes.data) if lift is not None else None,
+                      C.c_void_p(field.ctypes.data), native.HS_MEM_HOST)
+        return field
+
     def schur_map(self, i) -> np.ndarray:
         """Compact (k n) x (k n) map of subdomain i (faces W,S,N,E)."""
         i = MultiIndex(*i)

@@ -43,6 +43,7 @@ _SIGS = {
     "hs_factor": (_I, [_P]),
     "hs_lifting_rhs": (_I, [_P, _P, _I, _P, _I]),
     "hs_apply": (_I, [_P, _I, _P, _P, _I, _I]),
+    "hs_reconstruct": (_I, [_P, _P, _P, _P, _I]),
     "hs_restricted_apply": (_I, [_P, _P, _P, _I, _pI32, _I, _pI32, _I, _I]),
     "hs_set_windows": (_I, [_P, _I, _pI32, _pI32, _I]),
     "hs_set_precond_options": (_I, [_P, _I, _I]),
