@@ -145,6 +145,11 @@ int hs_gmres(hs_ctx* ctx, int pc_kind, const double* b, double* x, int nrhs, dou
  * sharded algorithm). */
 int hs_set_gmres_mode(hs_ctx* ctx, int mode);
 
+/* 1 (default) = run a BSP apply with one RHS as a single persistent dataflow
+ * launch (per-block completion counters instead of one launch per step);
+ * 0 = one launch per sweep step.  Both give bitwise identical results. */
+int hs_set_fused(hs_ctx* ctx, int on);
+
 /* ---- introspection (plan-only contexts too) ---------------------------- */
 /* Sizes: L (= 2 N_e n), number of subdomains, number of groups, 2 N_e. */
 int hs_sizes(const hs_ctx* ctx, int64_t* L, int* nsub, int* ngroups, int* npairs);

@@ -265,8 +265,76 @@ int make_step(Ctx* c, const StepTable& t, DevStep& out) {
   return 0;
 }
 
+void free_fused(Ctx* c) {
+  DevFused& f = c->fused;
+  dfree(c, f.items, f.nitems * sizeof(DevItem));
+  dfree(c, f.tiles, f.ntiles * sizeof(FusedTile));
+  dfree(c, f.deps, f.ndeps * sizeof(FusedDep));
+  dfree(c, f.counters, (c->plan.npairs + 1) * sizeof(int));
+  f = DevFused();
+}
+
+// Dataflow plan of one BSP apply: every tile of the forward steps, the
+// residual step and the backward steps in schedule order, each with the
+// per-block completion counts it waits for (all earlier tile-writes to the
+// blocks it reads or read-modify-writes; counts taken before its own step,
+// since the tiles of one step are independent).
+int build_fused(Ctx* c) {
+  free_fused(c);
+  DevFused& f = c->fused;
+  const Plan& P = c->plan;
+  const int n = c->n;
+  std::vector<DevItem> items;
+  std::vector<FusedTile> tiles;
+  std::vector<FusedDep> deps;
+  std::vector<int> written(P.npairs, 0);
+  auto add = [&](const DevStep& st, int phase) {
+    std::vector<int> inc;
+    for (const Item& it : st.host.items) {
+      const SubPlan& sp = P.subs[it.s];
+      DevItem d;
+      d.s = it.s; d.rlo = it.rlo; d.rhi = it.rhi; d.alt = it.alt;
+      for (int q = 0; q < 4; ++q) d.slot[q] = -1;
+      const int idx = (int)items.size();
+      items.push_back(d);
+      f.maxK = std::max(f.maxK, sp.k * n);
+      for (int tl = it.rlo / kRowTile; tl * kRowTile < it.rhi; ++tl) {
+        FusedTile ft;
+        ft.item = idx; ft.tile = tl; ft.phase = phase;
+        ft.dep0 = (int)deps.size(); ft.ndep = 0;
+        std::set<int> blocks;
+        for (int q = 0; q < sp.k; ++q) blocks.insert(sp.first_block + q);
+        const int r0 = std::max(it.rlo, tl * kRowTile), r1 = std::min(it.rhi, (tl + 1) * kRowTile);
+        for (int q = r0 / n; q * n < r1; ++q) {
+          blocks.insert(sp.tgt_block[q]);
+          inc.push_back(sp.tgt_block[q]);
+        }
+        for (int b : blocks)
+          if (written[b] > 0) {
+            deps.push_back({b, written[b]});
+            ft.ndep++;
+          }
+        tiles.push_back(ft);
+      }
+    }
+    for (int b : inc) written[b]++;
+    f.bytes += st.bytes_per_rhs_map + st.bytes_per_rhs_vec;
+  };
+  for (auto& st : c->fwd) add(st, 0);
+  add(c->full, 1);
+  for (auto& st : c->bwd) add(st, 2);
+  if (upload(c, &f.items, items) || upload(c, &f.tiles, tiles) || upload(c, &f.deps, deps)) return -1;
+  CK(dalloc(c, (void**)&f.counters, (P.npairs + 1) * sizeof(int)));
+  f.nitems = (int)items.size();
+  f.ntiles = (int)tiles.size();
+  f.ndeps = (int)deps.size();
+  f.built = true;
+  return 0;
+}
+
 int build_steps(Ctx* c) {
   if (!c->steps_dirty) return 0;
+  free_fused(c);
   for (auto& s : c->fwd) free_step(c, s);
   for (auto& s : c->bwd) free_step(c, s);
   for (auto& s : c->sp_fwd) free_step(c, s);
@@ -472,6 +540,26 @@ int do_precond(Ctx* c, int kind, const double2* r, double2* z, int R) {
   if (kind != HS_PC_BSP) return fail(c, 1, "unknown preconditioner kind");
   double2 *zl, *rp, *w;
   if (ws_get(c, "zL", LR, &zl) || ws_get(c, "rp", LR, &rp) || ws_get(c, "w", LR, &w)) return -1;
+  if (c->fused_mode && R == 1 && c->map_mode == 0 && c->plan.nranks == 1 && c->inter &&
+      c->seam == HS_SEAM_DEDUP && c->full.nitems > 0) {
+    // the whole apply as one dataflow launch (bitwise identical to the step sequence)
+    if (!c->fused.built && build_fused(c)) return -1;
+    CK(cudaMemcpyAsync(zl, r, LR * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->timing) {
+      e0 = ev_get(c);
+      e1 = ev_get(c);
+      cudaEventRecord(e0, c->stream);
+    }
+    CK(launch_bsp_fused(*c, c->fused, r, zl, rp, w, z));
+    if (e1) {
+      cudaEventRecord(e1, c->stream);
+      c->ev_pending.push_back({e0, e1});
+      c->ev_bytes.push_back(c->fused.bytes);
+      c->ev_flops.push_back(c->fused.bytes / 2.0);
+    }
+    return 0;
+  }
   if (do_half(c, 0, r, zl, R)) return -1;
   const double2* rsrc;
   if (c->inter) {
@@ -647,6 +735,7 @@ int hs_destroy(hs_ctx* c) {
     for (auto& s : c->sp_bwd) free_step(c, s);
     free_step(c, c->full);
     for (auto& oc : c->classes) cudaFree(oc.T4);
+    free_fused(c);
     cudaFree(c->T);
     cudaFree(c->Tcls);
     cudaFree(c->d_owned);
@@ -1297,6 +1386,12 @@ int hs_stream(hs_ctx* c, uint64_t* s) {
   if (!c) return 1;
   NEED_GPU(c);
   *s = (uint64_t)(uintptr_t)c->stream;
+  return 0;
+}
+
+int hs_set_fused(hs_ctx* c, int on) {
+  if (!c) return fail(nullptr, 1, "null context");
+  c->fused_mode = on ? 1 : 0;
   return 0;
 }
 

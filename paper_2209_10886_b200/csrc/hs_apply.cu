@@ -14,6 +14,8 @@
 // memory.  Map elements are read once with 128-bit streaming loads.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "hs_common.cuh"
 #include "hs_kernels.h"
 
@@ -69,6 +71,116 @@ __global__ void __launch_bounds__(NW * 32) k_step1(const DevTile* __restrict__ t
       else if (slot >= 0) e.send_up[(long long)slot * n + p] = y;
       else e.send_dn[(long long)(-slot - 2) * n + p] = y;
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// The whole BSP apply (forward half, intermediate residual, backward half) as
+// ONE persistent dataflow launch.  Tiles are claimed in schedule order from
+// an atomic ticket; a tile first waits until every block it reads (its
+// subdomain's incoming slab) or read-modify-writes (its output blocks) has
+// received all the tile-writes the schedule puts before it (per-block
+// completion counters), then runs exactly the k_step1 computation.  Step
+// t+1 of one window therefore streams while step t of another window drains,
+// and the 13-17 launches + ramps per apply disappear.  Deadlock-free: a
+// dependency always points to an earlier ticket, held by a running CTA.
+// Same arithmetic and summation order as k_step1 (bitwise identical result).
+struct FusedArgs {
+  const FusedTile* tiles;
+  const DevItem* items;
+  const FusedDep* deps;
+  const DevSub* subs;
+  const double2* T;
+  const double2* r;
+  double2* zL;
+  double2* rp;
+  double2* w;
+  double2* z;
+  int* done;
+  int* ticket;
+  int ntiles, n;
+};
+
+template <int NW>
+__global__ void __launch_bounds__(NW * 32) k_bsp_fused(FusedArgs a) {
+  extern __shared__ double2 sm[];
+  __shared__ int s_t;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int n = a.n;
+  for (;;) {
+    if (threadIdx.x == 0) s_t = atomicAdd(a.ticket, 1);
+    __syncthreads();
+    const int t = s_t;
+    if (t >= a.ntiles) return;
+    const FusedTile ft = a.tiles[t];
+    const DevItem it = a.items[ft.item];
+    const DevSub sb = a.subs[it.s];
+    for (int d = threadIdx.x; d < ft.ndep; d += blockDim.x) {
+      const FusedDep dp = a.deps[ft.dep0 + d];
+      const volatile int* p = a.done + dp.block;
+      while (*p < dp.count) __nanosleep(32);
+    }
+    __threadfence();
+    __syncthreads();
+    const int K = sb.k * n;
+    const double2* src;
+    if (ft.phase == 0) src = it.alt ? a.r : a.zL;
+    else if (ft.phase == 1) src = a.zL;
+    else src = it.alt ? a.rp : a.w;
+    src += sb.in_off;
+    double2* xs = sm;
+    double2* part = sm + K;
+    for (int i = threadIdx.x; i < K; i += NW * 32) xs[i] = __ldcg(src + i);
+    __syncthreads();
+    const double2* Tt = a.T + sb.T_off + (long long)ft.tile * K * kRowTile + lane;
+    const int per = (K + NW - 1) / NW;
+    const int c0 = warp * per;
+    const int c1 = min(K, c0 + per);
+    double2 a0 = make_double2(0, 0), a1 = make_double2(0, 0);
+    int c = c0;
+    for (; c + 8 <= c1; c += 8) {
+      double2 tv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) tv[u] = ld_stream(Tt + (long long)(c + u) * kRowTile);
+#pragma unroll
+      for (int u = 0; u < 8; u += 2) {
+        cfma(a0, tv[u], xs[c + u]);
+        cfma(a1, tv[u + 1], xs[c + u + 1]);
+      }
+    }
+    for (; c < c1; ++c) cfma(a0, ld_stream(Tt + (long long)c * kRowTile), xs[c]);
+    part[warp * 32 + lane] = cadd(a0, a1);
+    __syncthreads();
+    if (warp == 0) {
+      double2 y = part[lane];
+#pragma unroll
+      for (int ww = 1; ww < NW; ++ww) y = cadd(y, part[ww * 32 + lane]);
+      const int row = ft.tile * kRowTile + lane;
+      if (row >= it.rlo && row < it.rhi) {
+        const int q = row / n, p = row - q * n;
+        const long long off = (long long)sb.tgt[q] + p;
+        if (ft.phase == 0) {
+          a.zL[off] = cadd(__ldcg(a.zL + off), y);
+        } else if (ft.phase == 1) {
+          const double2 zl = __ldcg(a.zL + off);
+          const double2 v = csub(a.r[off], csub(zl, y));
+          a.rp[off] = v;
+          a.w[off] = v;
+          a.z[off] = cadd(zl, v);
+        } else {
+          a.w[off] = cadd(__ldcg(a.w + off), y);
+          a.z[off] = cadd(__ldcg(a.z + off), y);
+        }
+      }
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) {
+        // one completion per (tile, written block)
+        const int r0 = max(it.rlo, ft.tile * kRowTile), r1 = min(it.rhi, ft.tile * kRowTile + kRowTile);
+        for (int q = r0 / n; q * n < r1; ++q) atomicAdd(a.done + sb.tgt[q] / n, 1);
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -213,8 +325,33 @@ void launch_seam_add(Ctx& c, int dir, double2* z, const double2* r, int R) {
 }
 
 cudaError_t set_step_smem_limit() {
+  cudaFuncSetAttribute(k_bsp_fused<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   return cudaFuncSetAttribute(k_step1<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               200 * 1024);
+}
+
+cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double2* zL, double2* rp,
+                             double2* w, double2* z) {
+  constexpr int NW = 8;
+  const size_t smem = (size_t)(f.maxK + NW * 32) * sizeof(double2);
+  static int per_sm = 0;
+  static size_t per_sm_smem = 0;
+  if (per_sm == 0 || per_sm_smem != smem) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsp_fused<NW>, NW * 32, smem);
+    per_sm_smem = smem;
+    if (per_sm < 1) per_sm = 1;
+  }
+  cudaError_t e = cudaMemsetAsync(f.counters, 0, (c.plan.npairs + 1) * sizeof(int), c.stream);
+  if (e != cudaSuccess) return e;
+  FusedArgs a;
+  a.tiles = f.tiles; a.items = f.items; a.deps = f.deps; a.subs = c.dsubs; a.T = c.T;
+  a.r = r; a.zL = zL; a.rp = rp; a.w = w; a.z = z;
+  a.done = f.counters; a.ticket = f.counters + c.plan.npairs;
+  a.ntiles = f.ntiles; a.n = c.n;
+  const int grid = std::min(f.ntiles, per_sm * c.num_sms);
+  c.launches++;
+  k_bsp_fused<NW><<<grid > 0 ? grid : 1, NW * 32, smem, c.stream>>>(a);
+  return cudaGetLastError();
 }
 
 }  // namespace hs

@@ -98,6 +98,29 @@ struct DevStep {
   double bytes_per_rhs_map = 0, bytes_per_rhs_vec = 0;  // algorithmic bytes: map part, per-RHS vector part
 };
 
+// Fused BSP apply (one persistent dataflow launch): a tile of some step, with
+// the per-block completion counts it must wait for.
+struct FusedTile {
+  int item;        // index into the fused item list
+  int tile;        // 32-row strip
+  int phase;       // 0 forward (EPI_ACC on zL), 1 residual (EPI_RESID), 2 backward (EPI_ACC2)
+  int dep0, ndep;  // dependencies [dep0, dep0 + ndep) in the dep pool
+};
+
+struct FusedDep {
+  int block, count;  // wait until done[block] >= count
+};
+
+struct DevFused {
+  DevItem* items = nullptr;
+  FusedTile* tiles = nullptr;
+  FusedDep* deps = nullptr;
+  int nitems = 0, ntiles = 0, ndeps = 0, maxK = 0;
+  int* counters = nullptr;  // [npairs] block completion counters + [1] ticket
+  double bytes = 0;         // algorithmic bytes of one apply
+  bool built = false;
+};
+
 // One distinct subdomain operator (Dirichlet mask) and its factor.
 struct OpClass {
   std::vector<uint8_t> mask;          // n*n, 1 = Dirichlet cell
@@ -137,6 +160,8 @@ struct Ctx {
   bool steps_dirty = true;
   std::vector<DevStep> fwd, bwd, sp_fwd, sp_bwd;
   DevStep full;
+  DevFused fused;        // BSP apply as one dataflow launch (1 RHS, per-subdomain maps, 1 rank)
+  int fused_mode = 1;    // 1: use the fused kernel when applicable, 0: one launch per step
   std::vector<std::vector<int>> seam_blocks;  // [dir] blocks of seam groups (literal mode)
   int* d_seam[2] = {nullptr, nullptr};
   int n_seam[2] = {0, 0};
