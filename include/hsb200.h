@@ -139,10 +139,11 @@ int hs_half_apply(hs_ctx* ctx, int direction, const double* r, double* z, int nr
 int hs_gmres(hs_ctx* ctx, int pc_kind, const double* b, double* x, int nrhs, double tol,
              int maxit, int* iters, double* hist, int* converged, int mem);
 
-/* Arnoldi implementation: 0 = auto (one cooperative MGS kernel per iteration
- * on a single GPU; host-driven MGS with one ncclAllReduce per inner product
- * across row bands), 1 = force the host-driven MGS (single-GPU test of the
- * sharded algorithm). */
+/* Arnoldi implementation: 0 = auto (single GPU: one thread-block-cluster MGS
+ * + Givens kernel per iteration for vectors up to 196k elements, else one
+ * grid-wide cooperative MGS kernel; across row bands: host-driven MGS with one
+ * ncclAllReduce per inner product), 1 = force the host-driven MGS (single-GPU
+ * test of the sharded algorithm), 2 = force the grid-wide cooperative kernel. */
 int hs_set_gmres_mode(hs_ctx* ctx, int mode);
 
 /* 1 (default) = run a BSP apply with one RHS as a single persistent dataflow

@@ -736,6 +736,9 @@ int hs_destroy(hs_ctx* c) {
     free_step(c, c->full);
     for (auto& oc : c->classes) cudaFree(oc.T4);
     free_fused(c);
+    if (c->h_flags) cudaFreeHost(c->h_flags);
+    if (c->flag_ev[0]) cudaEventDestroy(c->flag_ev[0]);
+    if (c->flag_ev[1]) cudaEventDestroy(c->flag_ev[1]);
     cudaFree(c->T);
     cudaFree(c->Tcls);
     cudaFree(c->d_owned);
@@ -1168,8 +1171,22 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
   int nact = 0;
   CK(cudaMemcpyAsync(&nact, G.nactive, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
+  // Convergence flags come back through pinned memory.  When an iteration is
+  // short, iteration k+1 is enqueued before iteration k's flag is read (one
+  // iteration of lookahead hides the round trip; a speculative iteration after
+  // convergence is harmless: k_givens skips inactive right-hand sides and the
+  // solution uses the device-side iteration counts).
+  if (!c->h_flags) {
+    CK(cudaHostAlloc((void**)&c->h_flags, 4 * sizeof(int), cudaHostAllocDefault));
+    CK(cudaEventCreateWithFlags(&c->flag_ev[0], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->flag_ev[1], cudaEventDisableTiming));
+  }
+  const bool lookahead = c->map_mode == 1 || (double)c->T_elems * 16.0 < 2e9;
+  int cchunk = 0;
+  const int ccs = (dist || c->gmres_mode == 2) ? 0 : gmres_cluster_size(LR, R, &cchunk);
   int kdone = 0;
-  for (int k = 0; k < maxit && nact > 0; ++k) {
+  bool stop = nact == 0;
+  for (int k = 0; k < maxit && !stop; ++k) {
     double2* vk = V + (long long)k * LR;
     double2* w = V + (long long)(k + 1) * LR;
     const double2* zin = vk;
@@ -1178,12 +1195,23 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
       zin = Z;
     }
     if (do_apply(c, HS_APPLY_IMS, zin, w, R)) return -1;
-    if (dist) CK(gmres_arnoldi_dist(*c, G, k, c->d_owned, c->n_owned, part2, mgsout, c->nccl));
-    else CK(gmres_arnoldi(*c, G, k, grid, chunk));
-    CK(gmres_givens(*c, G, k));
-    CK(cudaMemcpyAsync(&nact, G.nactive, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-    CK(cudaStreamSynchronize(c->stream));
+    if (dist) {
+      CK(gmres_arnoldi_dist(*c, G, k, c->d_owned, c->n_owned, part2, mgsout, c->nccl));
+      CK(gmres_givens(*c, G, k));
+    } else if (ccs > 0) {
+      CK(gmres_arnoldi_cluster(*c, G, k, ccs, cchunk));  // includes the Givens update
+    } else {
+      CK(gmres_arnoldi(*c, G, k, grid, chunk));
+      CK(gmres_givens(*c, G, k));
+    }
+    CK(cudaMemcpyAsync(&c->h_flags[k & 1], G.nactive, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaEventRecord(c->flag_ev[k & 1], c->stream));
     kdone = k + 1;
+    const int chk = lookahead ? k - 1 : k;  // the iteration whose flag decides
+    if (chk >= 0) {
+      CK(cudaEventSynchronize(c->flag_ev[chk & 1]));
+      if (c->h_flags[chk & 1] == 0) stop = true;
+    }
   }
   if (kdone > 0) {
     double2* u;
@@ -1397,7 +1425,8 @@ int hs_set_fused(hs_ctx* c, int on) {
 
 int hs_set_gmres_mode(hs_ctx* c, int mode) {
   if (!c) return fail(nullptr, 1, "null context");
-  if (mode != 0 && mode != 1) return fail(c, 1, "gmres mode must be 0 (auto) or 1 (host-driven MGS)");
+  if (mode < 0 || mode > 2)
+    return fail(c, 1, "gmres mode must be 0 (auto), 1 (host-driven MGS) or 2 (grid-wide cooperative MGS)");
   c->gmres_mode = mode;
   return 0;
 }

@@ -173,6 +173,8 @@ struct Ctx {
   size_t xbuf_cap = 0;
   void* nccl = nullptr;  // ncclComm_t
   int gmres_mode = 0;    // 0 auto (cooperative MGS on one rank), 1 host-driven MGS over owned blocks
+  int* h_flags = nullptr;             // pinned: GMRES active counts (2 slots)
+  cudaEvent_t flag_ev[2] = {nullptr, nullptr};
   int* d_owned = nullptr;  // this rank's blocks (host-driven MGS)
   int n_owned = 0;
   // execution control / timing

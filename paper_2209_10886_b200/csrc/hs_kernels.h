@@ -79,6 +79,9 @@ cudaError_t gmres_arnoldi(Ctx& c, GmresDev& G, int k, int grid, int chunk);
 cudaError_t gmres_givens(Ctx& c, GmresDev& G, int k);
 cudaError_t gmres_finish(Ctx& c, GmresDev& G, int maxit, double2* u);
 int gmres_coop_grid(Ctx& c, long long LR, int R, int* chunk);
+// Arnoldi step + Givens on one thread-block cluster (small vectors)
+int gmres_cluster_size(long long LR, int R, int* chunk);
+cudaError_t gmres_arnoldi_cluster(Ctx& c, GmresDev& G, int k, int cs, int chunk);
 // host-driven MGS over owned blocks (+ one ncclAllReduce per inner product when comm != null)
 cudaError_t gmres_arnoldi_dist(Ctx& c, GmresDev& G, int k, const int* blocks, int nb, double2* part,
                                double2* out, void* nccl_comm);

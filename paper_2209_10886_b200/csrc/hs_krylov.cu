@@ -117,66 +117,155 @@ __global__ void k_mgs(GmresDev G, int k, int chunk) {
   }
 }
 
-// Givens update of column k for every active right-hand side.
-__global__ void k_givens(GmresDev G, int k) {
+// Givens update of column k of right-hand side r (if still active); returns
+// whether r stays active.
+__device__ bool givens_column(const GmresDev& G, int k, int r) {
   const int R = G.R;
   const double eps = 2.220446049250313e-16;
+  if (!G.active[r]) return false;
+  double2* Hk = G.H + hoff(k, R);
+  const double hn = Hk[(long long)(k + 1) * R + r].x;
+  for (int j = 0; j < k; ++j) {
+    const double c = G.cs[(long long)j * R + r];
+    const double2 s = G.sn[(long long)j * R + r];
+    const double2 a = Hk[(long long)j * R + r], b = Hk[(long long)(j + 1) * R + r];
+    // t = c a + s b ;  b' = -conj(s) a + c b
+    double2 t = cadd(make_double2(c * a.x, c * a.y), cmul(s, b));
+    double2 sc = make_double2(-s.x, s.y);  // -conj(s)
+    double2 b2 = cadd(cmul(sc, a), make_double2(c * b.x, c * b.y));
+    Hk[(long long)j * R + r] = t;
+    Hk[(long long)(j + 1) * R + r] = b2;
+  }
+  const double2 a = Hk[(long long)k * R + r];
+  const double bb = Hk[(long long)(k + 1) * R + r].x;
+  double c;
+  double2 s;
+  const double aa = hypot(a.x, a.y);
+  if (aa == 0.0) {
+    c = 0.0;
+    s = make_double2(1.0, 0.0);
+  } else {
+    const double rho = hypot(aa, fabs(bb));
+    c = aa / rho;
+    // s = (a/|a|) * conj(b) / rho, b real
+    s = make_double2(a.x / aa * bb / rho, a.y / aa * bb / rho);
+  }
+  G.cs[(long long)k * R + r] = c;
+  G.sn[(long long)k * R + r] = s;
+  Hk[(long long)k * R + r] = cadd(make_double2(c * a.x, c * a.y), make_double2(s.x * bb, s.y * bb));
+  Hk[(long long)(k + 1) * R + r] = make_double2(0, 0);
+  const double2 gk = G.g[(long long)k * R + r];
+  // g[k+1] = -conj(s) g[k];  g[k] = c g[k]
+  G.g[(long long)(k + 1) * R + r] = cmul(make_double2(-s.x, s.y), gk);
+  G.g[(long long)k * R + r] = make_double2(c * gk.x, c * gk.y);
+  const double2 gn = G.g[(long long)(k + 1) * R + r];
+  const double res = hypot(gn.x, gn.y) / G.beta[r];
+  G.hist[(long long)(k + 1) * R + r] = res;
+  G.iters[r] = k + 1;
+  if (res <= G.tol) {
+    G.conv[r] = 1;
+    G.active[r] = 0;
+    return false;
+  }
+  if (hn <= 16 * eps * G.wnorm0[r]) {
+    G.brk[r] = 1;
+    G.active[r] = 0;
+    return false;
+  }
+  return true;
+}
+
+// Givens update of column k for every active right-hand side.
+__global__ void k_givens(GmresDev G, int k) {
   __shared__ int cnt;
   if (threadIdx.x == 0) cnt = 0;
   __syncthreads();
-  for (int r = threadIdx.x; r < R; r += blockDim.x) {
-    if (!G.active[r]) continue;
-    double2* Hk = G.H + hoff(k, R);
-    const double hn = Hk[(long long)(k + 1) * R + r].x;
-    for (int j = 0; j < k; ++j) {
-      const double c = G.cs[(long long)j * R + r];
-      const double2 s = G.sn[(long long)j * R + r];
-      const double2 a = Hk[(long long)j * R + r], b = Hk[(long long)(j + 1) * R + r];
-      // t = c a + s b ;  b' = -conj(s) a + c b
-      double2 t = cadd(make_double2(c * a.x, c * a.y), cmul(s, b));
-      double2 sc = make_double2(-s.x, s.y);  // -conj(s)
-      double2 b2 = cadd(cmul(sc, a), make_double2(c * b.x, c * b.y));
-      Hk[(long long)j * R + r] = t;
-      Hk[(long long)(j + 1) * R + r] = b2;
-    }
-    const double2 a = Hk[(long long)k * R + r];
-    const double bb = Hk[(long long)(k + 1) * R + r].x;
-    double c;
-    double2 s;
-    const double aa = hypot(a.x, a.y);
-    if (aa == 0.0) {
-      c = 0.0;
-      s = make_double2(1.0, 0.0);
-    } else {
-      const double rho = hypot(aa, fabs(bb));
-      c = aa / rho;
-      // s = (a/|a|) * conj(b) / rho, b real
-      s = make_double2(a.x / aa * bb / rho, a.y / aa * bb / rho);
-    }
-    G.cs[(long long)k * R + r] = c;
-    G.sn[(long long)k * R + r] = s;
-    Hk[(long long)k * R + r] = cadd(make_double2(c * a.x, c * a.y), make_double2(s.x * bb, s.y * bb));
-    Hk[(long long)(k + 1) * R + r] = make_double2(0, 0);
-    const double2 gk = G.g[(long long)k * R + r];
-    // g[k+1] = -conj(s) g[k];  g[k] = c g[k]
-    G.g[(long long)(k + 1) * R + r] = cmul(make_double2(-s.x, s.y), gk);
-    G.g[(long long)k * R + r] = make_double2(c * gk.x, c * gk.y);
-    const double2 gn = G.g[(long long)(k + 1) * R + r];
-    const double res = hypot(gn.x, gn.y) / G.beta[r];
-    G.hist[(long long)(k + 1) * R + r] = res;
-    G.iters[r] = k + 1;
-    if (res <= G.tol) {
-      G.conv[r] = 1;
-      G.active[r] = 0;
-    } else if (hn <= 16 * eps * G.wnorm0[r]) {
-      G.brk[r] = 1;
-      G.active[r] = 0;
-    } else {
-      atomicAdd(&cnt, 1);
-    }
-  }
+  for (int r = threadIdx.x; r < G.R; r += blockDim.x)
+    if (givens_column(G, k, r)) atomicAdd(&cnt, 1);
   __syncthreads();
   if (threadIdx.x == 0) *G.nactive = cnt;
+}
+
+// Arnoldi step + Givens on one thread-block cluster (<= 16 CTAs): each CTA
+// keeps its slice of w in shared memory; the per-j partial sums are exchanged
+// through distributed shared memory and reduced in rank order by every CTA
+// (deterministic, identical on all CTAs), with one cluster barrier per j --
+// far cheaper than a grid-wide barrier for the small interface vectors of
+// configs 1-3.  CTA 0 then applies the Givens rotations of column k.
+__global__ void __launch_bounds__(1024) k_mgs_cluster(GmresDev G, int k, int chunk) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int CS = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+  extern __shared__ double2 sm[];
+  const int R = G.R;
+  double2* ws = sm;                       // chunk
+  double2* red = ws + chunk;              // blockDim
+  double2* pub = red + blockDim.x;        // 2 x R published partials (parity)
+  double2* hsh = pub + 2 * R;             // R
+  __shared__ int cnt;
+  const long long LR = G.LR;
+  const long long e0 = (long long)rank * chunk;
+  const int n_el = (int)max(0LL, min((long long)chunk, LR - e0));
+  const int tid = threadIdx.x;
+  double2* w = G.V + (long long)(k + 1) * LR;
+  int par = 0;
+  auto exchange = [&](double2 acc) {
+    // block reduce -> publish -> cluster barrier -> every CTA sums the ranks in order
+    red[tid] = acc;
+    block_colsum(red, R);
+    if (tid < R) pub[par * R + tid] = red[tid];
+    cl.sync();
+    for (int r = tid; r < R; r += blockDim.x) {
+      double2 s2 = make_double2(0, 0);
+      for (int q = 0; q < CS; ++q) s2 = cadd(s2, cl.map_shared_rank(pub, q)[par * R + r]);
+      hsh[r] = s2;
+    }
+    __syncthreads();
+    par ^= 1;
+  };
+  for (int i = tid; i < n_el; i += blockDim.x) ws[i] = w[e0 + i];
+  {
+    double2 acc = make_double2(0, 0);
+    for (int i = tid; i < n_el; i += blockDim.x) acc.x += ws[i].x * ws[i].x + ws[i].y * ws[i].y;
+    exchange(acc);
+    if (rank == 0 && tid < R) G.wnorm0[tid] = sqrt(hsh[tid].x);
+  }
+  double2* Hk = G.H + hoff(k, R);
+  for (int j = 0; j <= k; ++j) {
+    const double2* v = G.V + (long long)j * LR + e0;
+    double2 acc = make_double2(0, 0);
+    for (int i = tid; i < n_el; i += blockDim.x) cfma_conj(acc, v[i], ws[i]);
+    exchange(acc);
+    if (rank == 0 && tid < R) Hk[(long long)j * R + tid] = hsh[tid];
+    for (int i = tid; i < n_el; i += blockDim.x) {
+      const double2 h = hsh[(int)((e0 + i) % R)];
+      ws[i] = csub(ws[i], cmul(h, v[i]));
+    }
+    __syncthreads();
+  }
+  {
+    double2 acc = make_double2(0, 0);
+    for (int i = tid; i < n_el; i += blockDim.x) acc.x += ws[i].x * ws[i].x + ws[i].y * ws[i].y;
+    exchange(acc);
+  }
+  if (tid < R) {
+    const double hn = sqrt(hsh[tid].x);
+    hsh[tid].x = hn;
+    if (rank == 0) Hk[(long long)(k + 1) * R + tid] = make_double2(hn, 0);
+  }
+  __syncthreads();
+  for (int i = tid; i < n_el; i += blockDim.x) {
+    const double hn = hsh[(int)((e0 + i) % R)].x;
+    w[e0 + i] = hn > 0 ? make_double2(ws[i].x / hn, ws[i].y / hn) : make_double2(0, 0);
+  }
+  if (rank == 0) {
+    if (tid == 0) cnt = 0;
+    __syncthreads();
+    for (int r = tid; r < R; r += blockDim.x)
+      if (givens_column(G, k, r)) atomicAdd(&cnt, 1);
+    __syncthreads();
+    if (tid == 0) *G.nactive = cnt;
+  }
+  cl.sync();  // peers' shared memory must outlive the last remote read
 }
 
 // beta = ||b|| per column (two-pass deterministic), V0 = b / beta, state init.
@@ -306,6 +395,47 @@ cudaError_t gmres_init(Ctx& c, GmresDev& G, const double2* b) {
   int g2 = (int)std::min<long long>((G.LR + 255) / 256, (long long)c.num_sms * 8);
   k_scale_cols<<<g2 > 0 ? g2 : 1, 256, 0, c.stream>>>(G.V, b, G.beta, G.LR, R);
   return cudaGetLastError();
+}
+
+// Cluster size / slice for k_mgs_cluster: the smallest power of two such that
+// a CTA holds <= 12288 elements of w and has >= 2048 to stream; 0 when the
+// vector is too large for one 16-CTA cluster (then the grid-wide kernel runs).
+int gmres_cluster_size(long long LR, int R, int* chunk) {
+  // beyond ~32k elements the k basis vectors per iteration need the whole
+  // GPU's bandwidth more than cheap barriers (measured: cfg3 slower on 16 CTAs)
+  if (LR > 32768) return 0;
+  int cs = 1;
+  while (cs < 16 && ((LR + cs - 1) / cs > 12288 || (LR + cs - 1) / cs > 2048)) cs *= 2;
+  long long ch = (LR + cs - 1) / cs;
+  ch = ((ch + R - 1) / R) * R;
+  if (ch > 12288 + R) return 0;
+  *chunk = (int)ch;
+  return cs;
+}
+
+cudaError_t gmres_arnoldi_cluster(Ctx& c, GmresDev& G, int k, int cs, int chunk) {
+  const int bs = coop_block(G.R);
+  const size_t smem = (size_t)(chunk + bs + 3 * G.R) * sizeof(double2);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_mgs_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+    cudaFuncSetAttribute(k_mgs_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr = true;
+  }
+  c.launches++;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cs);
+  cfg.blockDim = dim3(bs);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c.stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_mgs_cluster, G, k, chunk);
 }
 
 cudaError_t gmres_arnoldi(Ctx& c, GmresDev& G, int k, int grid, int chunk) {

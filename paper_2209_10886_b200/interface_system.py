@@ -332,13 +332,15 @@ class GpuInterfaceSystem:
     # ---- SPEC.md:399-407 on the device
     def gmres(self, b, kind: str | None = None, tol: float = 1e-6, maxit: int = 200,
               arnoldi: str = "auto") -> GmresResult:
-        """arnoldi = "auto" (one cooperative MGS kernel per iteration; host-driven
-        MGS with an allreduce per inner product across row bands) or "hostloop"
-        (force the sharded algorithm on one GPU)."""
+        """arnoldi = "auto" (cluster MGS kernel for small vectors, grid-wide
+        cooperative kernel otherwise; host-driven MGS with an allreduce per inner
+        product across row bands), "hostloop" (force the sharded algorithm on
+        one GPU) or "grid" (force the grid-wide cooperative kernel)."""
         kind = self.sweep.kind if kind is None else kind
-        if arnoldi not in ("auto", "hostloop"):
-            raise ValueError(f"arnoldi must be 'auto' or 'hostloop', got {arnoldi!r}")
-        self.ctx.call("hs_set_gmres_mode", 1 if arnoldi == "hostloop" else 0)
+        modes = {"auto": 0, "hostloop": 1, "grid": 2}
+        if arnoldi not in modes:
+            raise ValueError(f"arnoldi must be one of {sorted(modes)}, got {arnoldi!r}")
+        self.ctx.call("hs_set_gmres_mode", modes[arnoldi])
         v = _Vec(self.layout.check(b), self.layout.size)
         out, optr = v.empty()
         R = v.R

@@ -101,10 +101,11 @@ def test_hostloop_mgs_equals_cooperative(k):
     s = system(k, "subdomain")
     b = s.rhs()
     a = s.gmres(b, "bsp", tol=1e-6, maxit=1000, arnoldi="auto")
-    h = s.gmres(b, "bsp", tol=1e-6, maxit=1000, arnoldi="hostloop")
-    assert h.iterations == a.iterations and h.converged
-    assert relerr(h.solution, a.solution) < 1e-12
-    np.testing.assert_allclose(h.history, a.history, rtol=1e-10)
+    for mode in ("hostloop", "grid"):
+        h = s.gmres(b, "bsp", tol=1e-6, maxit=1000, arnoldi=mode)
+        assert h.iterations == a.iterations and h.converged
+        assert relerr(h.solution, a.solution) < 1e-12
+        np.testing.assert_allclose(h.history, a.history, rtol=1e-10)
 
 
 def test_hostloop_mgs_batched_cfg4():
