@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cmath>
 #include <complex>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <tuple>
@@ -288,6 +289,15 @@ int build_fused(Ctx* c) {
   std::vector<FusedTile> tiles;
   std::vector<FusedDep> deps;
   std::vector<int> written(P.npairs, 0);
+  // tile shape: one 32-row strip, 16 warps splitting its columns (measured on
+  // B200: 16 warps beat 8 at cfg2/cfg5 -- twice the bytes in flight per tile
+  // shortens the dependency chain links; 2 strips per tile (80 registers,
+  // half the occupancy) was slower at cfg3).  HS_FUSED_RT / HS_FUSED_NW override.
+  f.rt = 1;
+  f.nw = 16;
+  if (const char* e = getenv("HS_FUSED_RT")) f.rt = std::max(1, std::min(2, atoi(e)));
+  if (const char* e = getenv("HS_FUSED_NW")) f.nw = atoi(e) == 8 ? 8 : 16;
+  const int TR = kRowTile * f.rt;
   auto add = [&](const DevStep& st, int phase) {
     std::vector<int> inc;
     for (const Item& it : st.host.items) {
@@ -298,13 +308,13 @@ int build_fused(Ctx* c) {
       const int idx = (int)items.size();
       items.push_back(d);
       f.maxK = std::max(f.maxK, sp.k * n);
-      for (int tl = it.rlo / kRowTile; tl * kRowTile < it.rhi; ++tl) {
+      for (int tl = it.rlo / TR; tl * TR < it.rhi; ++tl) {
         FusedTile ft;
         ft.item = idx; ft.tile = tl; ft.phase = phase;
         ft.dep0 = (int)deps.size(); ft.ndep = 0;
         std::set<int> blocks;
         for (int q = 0; q < sp.k; ++q) blocks.insert(sp.first_block + q);
-        const int r0 = std::max(it.rlo, tl * kRowTile), r1 = std::min(it.rhi, (tl + 1) * kRowTile);
+        const int r0 = std::max(it.rlo, tl * TR), r1 = std::min(it.rhi, (tl + 1) * TR);
         for (int q = r0 / n; q * n < r1; ++q) {
           blocks.insert(sp.tgt_block[q]);
           inc.push_back(sp.tgt_block[q]);

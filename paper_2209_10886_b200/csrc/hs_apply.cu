@@ -101,7 +101,9 @@ struct FusedArgs {
   int ntiles, n;
 };
 
-template <int NW>
+// RT = 32-row strips per tile (RT * K ~ 1024 columns-strips keeps the fixed
+// per-tile cost -- ticket, dependency check, slab load, epilogue -- amortised).
+template <int NW, int RT>
 __global__ void __launch_bounds__(NW * 32) k_bsp_fused(FusedArgs a) {
   extern __shared__ double2 sm[];
   __shared__ int s_t;
@@ -132,33 +134,49 @@ __global__ void __launch_bounds__(NW * 32) k_bsp_fused(FusedArgs a) {
     double2* part = sm + K;
     for (int i = threadIdx.x; i < K; i += NW * 32) xs[i] = __ldcg(src + i);
     __syncthreads();
-    const double2* Tt = a.T + sb.T_off + (long long)ft.tile * K * kRowTile + lane;
+    // strips beyond the map (RT > 1 at the last rows) are skipped
+    const int nstrip = (K + kRowTile - 1) / kRowTile;
+    const int s0 = ft.tile * RT;
+    const double2* Tt = a.T + sb.T_off + (long long)s0 * K * kRowTile + lane;
     const int per = (K + NW - 1) / NW;
     const int c0 = warp * per;
     const int c1 = min(K, c0 + per);
-    double2 a0 = make_double2(0, 0), a1 = make_double2(0, 0);
+    double2 acc[RT][2];
+#pragma unroll
+    for (int q = 0; q < RT; ++q) acc[q][0] = acc[q][1] = make_double2(0, 0);
     int c = c0;
     for (; c + 8 <= c1; c += 8) {
-      double2 tv[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) tv[u] = ld_stream(Tt + (long long)(c + u) * kRowTile);
+      for (int q = 0; q < RT; ++q) {
+        if (s0 + q >= nstrip) break;
+        const double2* Tq = Tt + (long long)q * K * kRowTile;
+        double2 tv[8];
 #pragma unroll
-      for (int u = 0; u < 8; u += 2) {
-        cfma(a0, tv[u], xs[c + u]);
-        cfma(a1, tv[u + 1], xs[c + u + 1]);
+        for (int u = 0; u < 8; ++u) tv[u] = ld_stream(Tq + (long long)(c + u) * kRowTile);
+#pragma unroll
+        for (int u = 0; u < 8; u += 2) {
+          cfma(acc[q][0], tv[u], xs[c + u]);
+          cfma(acc[q][1], tv[u + 1], xs[c + u + 1]);
+        }
       }
     }
-    for (; c < c1; ++c) cfma(a0, ld_stream(Tt + (long long)c * kRowTile), xs[c]);
-    part[warp * 32 + lane] = cadd(a0, a1);
-    __syncthreads();
-    if (warp == 0) {
-      double2 y = part[lane];
+    for (; c < c1; ++c)
 #pragma unroll
-      for (int ww = 1; ww < NW; ++ww) y = cadd(y, part[ww * 32 + lane]);
-      const int row = ft.tile * kRowTile + lane;
+      for (int q = 0; q < RT; ++q)
+        if (s0 + q < nstrip) cfma(acc[q][0], ld_stream(Tt + (long long)q * K * kRowTile + (long long)c * kRowTile), xs[c]);
+#pragma unroll
+    for (int q = 0; q < RT; ++q) part[(q * NW + warp) * 32 + lane] = cadd(acc[q][0], acc[q][1]);
+    __syncthreads();
+    if (warp < RT) {
+      // warp q finalises strip q: fixed-order sum over the warps' partials
+      const int q = warp;
+      double2 y = part[(q * NW) * 32 + lane];
+#pragma unroll
+      for (int ww = 1; ww < NW; ++ww) y = cadd(y, part[(q * NW + ww) * 32 + lane]);
+      const int row = (s0 + q) * kRowTile + lane;
       if (row >= it.rlo && row < it.rhi) {
-        const int q = row / n, p = row - q * n;
-        const long long off = (long long)sb.tgt[q] + p;
+        const int f = row / n, p = row - f * n;
+        const long long off = (long long)sb.tgt[f] + p;
         if (ft.phase == 0) {
           a.zL[off] = cadd(__ldcg(a.zL + off), y);
         } else if (ft.phase == 1) {
@@ -173,14 +191,13 @@ __global__ void __launch_bounds__(NW * 32) k_bsp_fused(FusedArgs a) {
         }
       }
       __threadfence();
-      __syncwarp();
-      if (lane == 0) {
-        // one completion per (tile, written block)
-        const int r0 = max(it.rlo, ft.tile * kRowTile), r1 = min(it.rhi, ft.tile * kRowTile + kRowTile);
-        for (int q = r0 / n; q * n < r1; ++q) atomicAdd(a.done + sb.tgt[q] / n, 1);
-      }
     }
     __syncthreads();
+    if (threadIdx.x == 0) {
+      // one completion per (tile, written block); all strips' stores are fenced above
+      const int r0 = max(it.rlo, s0 * kRowTile), r1 = min(it.rhi, (s0 + RT) * kRowTile);
+      for (int f = r0 / n; f * n < r1; ++f) atomicAdd(a.done + sb.tgt[f] / n, 1);
+    }
   }
 }
 
@@ -288,7 +305,7 @@ void launch_step(Ctx& c, const DevStep& st, const double2* srcA, const double2* 
                  const Epi& e, int R) {
   if (st.ntiles > 0) {
     if (R == 1) {
-      constexpr int NW = 8;
+      constexpr int NW = 16;  // same column split as the fused kernel (bitwise identical sums)
       size_t smem = (size_t)(st.maxK + NW * 32) * sizeof(double2);
       c.launches++;
       k_step1<NW><<<st.ntiles, NW * 32, smem, c.stream>>>(st.tiles, st.items, c.dsubs, c.T, srcA,
@@ -325,21 +342,27 @@ void launch_seam_add(Ctx& c, int dir, double2* z, const double2* r, int R) {
 }
 
 cudaError_t set_step_smem_limit() {
-  cudaFuncSetAttribute(k_bsp_fused<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  return cudaFuncSetAttribute(k_step1<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaFuncSetAttribute(k_bsp_fused<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_bsp_fused<16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_bsp_fused<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  return cudaFuncSetAttribute(k_step1<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               200 * 1024);
 }
 
 cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double2* zL, double2* rp,
                              double2* w, double2* z) {
-  constexpr int NW = 8;
-  const size_t smem = (size_t)(f.maxK + NW * 32) * sizeof(double2);
-  static int per_sm = 0;
-  static size_t per_sm_smem = 0;
-  if (per_sm == 0 || per_sm_smem != smem) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsp_fused<NW>, NW * 32, smem);
-    per_sm_smem = smem;
-    if (per_sm < 1) per_sm = 1;
+  // variant: 0 = 8 warps x 1 strip, 1 = 16 warps x 1 strip, 2 = 8 warps x 2 strips
+  const int var = f.rt == 2 ? 2 : (f.nw == 16 ? 1 : 0);
+  const int NWv = var == 1 ? 16 : 8;
+  const size_t smem = (size_t)(f.maxK + NWv * 32 * f.rt) * sizeof(double2);
+  static int per_sm[3] = {0, 0, 0};
+  static size_t per_sm_smem[3] = {0, 0, 0};
+  if (per_sm[var] == 0 || per_sm_smem[var] != smem) {
+    if (var == 2) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[var], k_bsp_fused<8, 2>, 256, smem);
+    else if (var == 1) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[var], k_bsp_fused<16, 1>, 512, smem);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[var], k_bsp_fused<8, 1>, 256, smem);
+    per_sm_smem[var] = smem;
+    if (per_sm[var] < 1) per_sm[var] = 1;
   }
   cudaError_t e = cudaMemsetAsync(f.counters, 0, (c.plan.npairs + 1) * sizeof(int), c.stream);
   if (e != cudaSuccess) return e;
@@ -348,9 +371,11 @@ cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double
   a.r = r; a.zL = zL; a.rp = rp; a.w = w; a.z = z;
   a.done = f.counters; a.ticket = f.counters + c.plan.npairs;
   a.ntiles = f.ntiles; a.n = c.n;
-  const int grid = std::min(f.ntiles, per_sm * c.num_sms);
+  const int grid = std::max(1, std::min(f.ntiles, per_sm[var] * c.num_sms));
   c.launches++;
-  k_bsp_fused<NW><<<grid > 0 ? grid : 1, NW * 32, smem, c.stream>>>(a);
+  if (var == 2) k_bsp_fused<8, 2><<<grid, 256, smem, c.stream>>>(a);
+  else if (var == 1) k_bsp_fused<16, 1><<<grid, 512, smem, c.stream>>>(a);
+  else k_bsp_fused<8, 1><<<grid, 256, smem, c.stream>>>(a);
   return cudaGetLastError();
 }
 

@@ -102,7 +102,7 @@ struct DevStep {
 // the per-block completion counts it must wait for.
 struct FusedTile {
   int item;        // index into the fused item list
-  int tile;        // 32-row strip
+  int tile;        // tile index in units of rt strips
   int phase;       // 0 forward (EPI_ACC on zL), 1 residual (EPI_RESID), 2 backward (EPI_ACC2)
   int dep0, ndep;  // dependencies [dep0, dep0 + ndep) in the dep pool
 };
@@ -116,6 +116,8 @@ struct DevFused {
   FusedTile* tiles = nullptr;
   FusedDep* deps = nullptr;
   int nitems = 0, ntiles = 0, ndeps = 0, maxK = 0;
+  int rt = 1;               // 32-row strips per tile
+  int nw = 8;               // warps per CTA
   int* counters = nullptr;  // [npairs] block completion counters + [1] ticket
   double bytes = 0;         // algorithmic bytes of one apply
   bool built = false;
