@@ -1,4 +1,4 @@
-# launch list + full capture of the dominant kernel (fused BSP apply) at cfg5
+# launch list + full capture of the dominant kernel (fused BSP apply) at cfg5 and cfg3
 B="python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-gmres --no-variants"
 $B > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_bsp_fused|k_step1|k_vec|k_mgs|k_givens" -c 40 --csv --log-file gpurun_out/launches_cfg5.csv $B > gpurun_out/ncu1.log 2>&1; echo "ncu1 rc=$?"

@@ -67,15 +67,20 @@ def main():
     ap.add_argument("--first-launch", type=int, default=20, help="index of the first captured k_step1 launch")
     ap.add_argument("--launches-csv", default=None)
     ap.add_argument("--out", required=True)
+    ap.add_argument("--fused", action="store_true", help="one launch = one whole BSP apply (k_bsp_fused)")
+    ap.add_argument("--kernel", default="k_step1<16>")
     a = ap.parse_args()
     per_step = step_bytes(a.config)
+    if a.fused:
+        per_step = [sum(per_step)]
     launches = []
     for i, r in enumerate(raw_rows(a.rep)):
         idx = a.first_launch + i
         alg = per_step[idx % len(per_step)]
         dram = float(r["dram__bytes_read.sum"][0]) * (1e6 if r["dram__bytes_read.sum"][1] == "Mbyte" else 1e9 if r["dram__bytes_read.sum"][1] == "Gbyte" else 1)
         dw = float(r["dram__bytes_write.sum"][0]) * (1e6 if r["dram__bytes_write.sum"][1] == "Mbyte" else 1e9 if r["dram__bytes_write.sum"][1] == "Gbyte" else 1)
-        dur_us = float(r["gpu__time_duration.sum"][0]) * (1e-3 if r["gpu__time_duration.sum"][1] == "ns" else 1.0)
+        du = r["gpu__time_duration.sum"][1]
+        dur_us = float(r["gpu__time_duration.sum"][0]) * {"ns": 1e-3, "nsecond": 1e-3, "ms": 1e3, "msecond": 1e3}.get(du, 1.0)
         launches.append({"launch_index": idx, "bsp_step": idx % len(per_step), "duration_us": dur_us,
                          "dram_read_bytes": dram, "dram_write_bytes": dw, "algorithmic_bytes": alg,
                          "traffic_over_algorithmic": (dram + dw) / alg,
@@ -83,7 +88,7 @@ def main():
                          "registers": int(float(r["launch__registers_per_thread"][0])),
                          "grid": int(float(r["launch__grid_size"][0])),
                          "warps_active_pct": float(r["sm__warps_active.avg.pct_of_peak_sustained_active"][0])})
-    summ = {"kernel": "k_step1<8>", "config": a.config, "source": os.path.basename(a.rep),
+    summ = {"kernel": a.kernel, "config": a.config, "source": os.path.basename(a.rep),
             "note": "ncu --set full --clock-control none, cold cache, serialised replays",
             "launches": launches,
             "dram_bytes_per_launch": sum(x["dram_read_bytes"] + x["dram_write_bytes"] for x in launches) / len(launches),
