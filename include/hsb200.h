@@ -143,7 +143,10 @@ int hs_gmres(hs_ctx* ctx, int pc_kind, const double* b, double* x, int nrhs, dou
  * + Givens kernel per iteration for vectors up to 196k elements, else one
  * grid-wide cooperative MGS kernel; across row bands: host-driven MGS with one
  * ncclAllReduce per inner product), 1 = force the host-driven MGS (single-GPU
- * test of the sharded algorithm), 2 = force the grid-wide cooperative kernel. */
+ * test of the sharded algorithm), 2 = force the grid-wide cooperative kernel,
+ * 3 = CGS2 (classical Gram-Schmidt + one reorthogonalisation; one RHS): two
+ * reductions per iteration instead of k+1 -- one allreduce each across row
+ * bands; same iteration counts as MGS within +-1. */
 int hs_set_gmres_mode(hs_ctx* ctx, int mode);
 
 /* 1 (default) = run a BSP apply with one RHS as a single persistent dataflow

@@ -1125,7 +1125,9 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
   if (R & (R - 1)) return fail(c, 1, "batched GMRES needs nrhs a power of two");
   // Arnoldi: one cooperative kernel per iteration on one GPU; across row bands
   // (or when forced) the host-driven MGS over owned blocks + allreduce per dot
-  const bool dist = c->plan.nranks > 1 || c->gmres_mode == 1;
+  const bool cgs2 = c->gmres_mode == 3;
+  if (cgs2 && R != 1) return fail(c, 1, "CGS2 Arnoldi supports one right-hand side");
+  const bool dist = c->plan.nranks > 1 || c->gmres_mode == 1 || cgs2;
   const long long LR = LRof(c, R);
   if (LR == 0) {  // empty interface system (1 x 1 lattice): 0 iterations
     for (int r = 0; r < R; ++r) {
@@ -1141,7 +1143,7 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
   int chunk = 0;
   int grid = dist ? 2 * c->num_sms : gmres_coop_grid(*c, LR, R, &chunk);
   if (grid <= 0) return fail(c, 3, "interface vector too large for the cooperative Arnoldi kernel");
-  double2 *part2 = nullptr, *mgsout = nullptr;
+  double2 *part2 = nullptr, *mgsout = nullptr, *part3 = nullptr, *hbuf = nullptr;
   if (dist) {
     if (!c->d_owned) {
       std::vector<int> owned;
@@ -1151,6 +1153,8 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
       c->n_owned = (int)owned.size();
     }
     if (ws_get(c, "part2", (size_t)grid * 2 * R, &part2) || ws_get(c, "mgsout", (size_t)2 * R, &mgsout)) return -1;
+    if (cgs2 && (ws_get(c, "part3", (size_t)grid * (maxit + 2), &part3) || ws_get(c, "hbuf", (size_t)maxit + 2, &hbuf)))
+      return -1;
   }
   GmresDev G;
   G.LR = LR; G.R = R; G.tol = tol;
@@ -1205,7 +1209,10 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
       zin = Z;
     }
     if (do_apply(c, HS_APPLY_IMS, zin, w, R)) return -1;
-    if (dist) {
+    if (cgs2) {
+      CK(gmres_arnoldi_cgs2(*c, G, k, c->d_owned, c->n_owned, part3, hbuf, c->nccl));
+      CK(gmres_givens(*c, G, k));
+    } else if (dist) {
       CK(gmres_arnoldi_dist(*c, G, k, c->d_owned, c->n_owned, part2, mgsout, c->nccl));
       CK(gmres_givens(*c, G, k));
     } else if (ccs > 0) {
@@ -1435,8 +1442,8 @@ int hs_set_fused(hs_ctx* c, int on) {
 
 int hs_set_gmres_mode(hs_ctx* c, int mode) {
   if (!c) return fail(nullptr, 1, "null context");
-  if (mode < 0 || mode > 2)
-    return fail(c, 1, "gmres mode must be 0 (auto), 1 (host-driven MGS) or 2 (grid-wide cooperative MGS)");
+  if (mode < 0 || mode > 3)
+    return fail(c, 1, "gmres mode must be 0 (auto), 1 (host-driven MGS), 2 (grid-wide MGS) or 3 (CGS2)");
   c->gmres_mode = mode;
   return 0;
 }

@@ -87,6 +87,9 @@ cudaError_t gmres_arnoldi_dist(Ctx& c, GmresDev& G, int k, const int* blocks, in
                                double2* out, void* nccl_comm);
 cudaError_t gmres_init_dist(Ctx& c, GmresDev& G, const double2* b, const int* blocks, int nb,
                             double2* part, double2* out, void* nccl_comm);
+// CGS2 Arnoldi (one RHS): two passes, one allreduce of k+1 values each across row bands
+cudaError_t gmres_arnoldi_cgs2(Ctx& c, GmresDev& G, int k, const int* blocks, int nb, double2* part,
+                               double2* hbuf, void* nccl_comm);
 // in-place sum over ranks (implemented next to the NCCL calls in hs_api.cu)
 cudaError_t allreduce_sum_doubles(Ctx& c, double* buf, size_t count, void* nccl_comm);
 

@@ -573,6 +573,112 @@ cudaError_t gmres_arnoldi_dist(Ctx& c, GmresDev& G, int k, const int* blocks, in
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// CGS2 Arnoldi (one RHS): classical Gram-Schmidt with one reorthogonalisation,
+// h = V^H w; w -= V h; h' = V^H w; w -= V h'; H[:,k] = h + h'.  All k+1 inner
+// products of a pass are formed in one kernel (one warp per basis vector, over
+// this CTA's slice of the owned blocks, shuffle-reduced: no block barriers),
+// reduced over CTAs in a fixed order, and -- across row bands -- summed with
+// ONE allreduce per pass instead of k+1.
+// part: [grid][kp1 + 1] (the extra slot: |w|^2 for the breakdown test).
+// inner products for j in [jbeg, jend); j == k+1 is |w|^2
+__global__ void k_cgs_dots(GmresDev G, const int* __restrict__ blocks, int nb, int n, int k, int jbeg, int jend,
+                           double2* part) {
+  const long long LR = G.LR;
+  const double2* w = G.V + (long long)(k + 1) * LR;
+  const long long total = (long long)nb * n;
+  const long long per = (total + gridDim.x - 1) / gridDim.x;
+  const long long i0 = blockIdx.x * per, i1 = min(total, i0 + per);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int kp1 = k + 1;
+  for (int j = jbeg + warp; j < jend; j += nw) {
+    double2 acc = make_double2(0, 0);
+    const double2* v = G.V + (long long)(j < kp1 ? j : 0) * LR;
+    for (long long i = i0 + lane; i < i1; i += 32) {
+      const long long e = (long long)blocks[i / n] * n + i % n;
+      const double2 x = w[e];
+      if (j < kp1) cfma_conj(acc, v[e], x);
+      else acc.x += x.x * x.x + x.y * x.y;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      acc.x += __shfl_down_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_down_sync(0xffffffffu, acc.y, o);
+    }
+    if (lane == 0) part[(long long)blockIdx.x * (kp1 + 1) + j] = acc;
+  }
+}
+
+// out[j] = sum over CTAs of part[g][j] (fixed order), j < cnt
+__global__ void k_cgs_reduce(const double2* part, int ngrid, int stride, int cnt, double2* out) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < cnt; j += gridDim.x * blockDim.x) {
+    double2 s = make_double2(0, 0);
+    for (int g = 0; g < ngrid; ++g) s = cadd(s, part[(long long)g * stride + j]);
+    out[j] = s;
+  }
+}
+
+// w -= sum_j h_j v_j over owned elements; pass 0 stores h, pass 1 adds h' into H[:,k]
+__global__ void k_cgs_update(GmresDev G, const int* __restrict__ blocks, int nb, int n, int k, const double2* h,
+                             int pass) {
+  const long long LR = G.LR;
+  double2* w = G.V + (long long)(k + 1) * LR;
+  const long long total = (long long)nb * n;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long e = (long long)blocks[i / n] * n + i % n;
+    double2 x = w[e];
+    for (int j = 0; j <= k; ++j) x = csub(x, cmul(h[j], G.V[(long long)j * LR + e]));
+    w[e] = x;
+  }
+  if (blockIdx.x == 0) {
+    double2* Hk = G.H + hoff(k, 1);
+    for (int j = threadIdx.x; j <= k; j += blockDim.x) Hk[j] = pass == 0 ? h[j] : cadd(Hk[j], h[j]);
+    if (pass == 0 && threadIdx.x == 0) G.wnorm0[0] = sqrt(h[k + 1].x);
+  }
+}
+
+__global__ void k_cgs_normalize(GmresDev G, const int* __restrict__ blocks, int nb, int n, int k,
+                                const double2* nrm2) {
+  const long long LR = G.LR;
+  double2* w = G.V + (long long)(k + 1) * LR;
+  const double hn = sqrt(nrm2[0].x);
+  const long long total = (long long)nb * n;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long e = (long long)blocks[i / n] * n + i % n;
+    const double2 x = w[e];
+    w[e] = hn > 0 ? make_double2(x.x / hn, x.y / hn) : make_double2(0, 0);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) G.H[hoff(k, 1) + k + 1] = make_double2(hn, 0);
+}
+
+cudaError_t gmres_arnoldi_cgs2(Ctx& c, GmresDev& G, int k, const int* blocks, int nb, double2* part,
+                               double2* hbuf, void* nccl_comm) {
+  const int grid = 2 * c.num_sms;
+  const int kp1 = k + 1;
+  auto allreduce = [&](int cnt) -> cudaError_t {
+    if (!nccl_comm) return cudaSuccess;
+    return allreduce_sum_doubles(c, (double*)hbuf, 2 * (size_t)cnt, nccl_comm);
+  };
+  const int ug = std::min(grid * 4, std::max(1, (int)(((long long)nb * c.n + 255) / 256)));
+  // pass 0 (+ |w|^2 before orthogonalisation), pass 1
+  for (int pass = 0; pass < 2; ++pass) {
+    const int cnt = kp1 + (pass == 0 ? 1 : 0);
+    c.launches += 3;
+    k_cgs_dots<<<grid, 256, 0, c.stream>>>(G, blocks, nb, c.n, k, 0, cnt, part);
+    k_cgs_reduce<<<(cnt + 127) / 128, 128, 0, c.stream>>>(part, grid, kp1 + 1, cnt, hbuf);
+    if (cudaError_t e = allreduce(cnt)) return e;
+    k_cgs_update<<<ug, 256, 0, c.stream>>>(G, blocks, nb, c.n, k, hbuf, pass);
+  }
+  // |w|^2 -> normalise
+  c.launches += 3;
+  k_cgs_dots<<<grid, 256, 0, c.stream>>>(G, blocks, nb, c.n, k, kp1, kp1 + 1, part);
+  k_cgs_reduce<<<1, 32, 0, c.stream>>>(part + kp1, grid, kp1 + 1, 1, hbuf);
+  if (cudaError_t e = allreduce(1)) return e;
+  k_cgs_normalize<<<ug, 256, 0, c.stream>>>(G, blocks, nb, c.n, k, hbuf);
+  return cudaGetLastError();
+}
+
 // beta over owned blocks (+ allreduce), then the usual init
 cudaError_t gmres_init_dist(Ctx& c, GmresDev& G, const double2* b, const int* blocks, int nb,
                             double2* part, double2* out, void* nccl_comm) {

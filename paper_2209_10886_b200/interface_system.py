@@ -335,9 +335,11 @@ class GpuInterfaceSystem:
         """arnoldi = "auto" (cluster MGS kernel for small vectors, grid-wide
         cooperative kernel otherwise; host-driven MGS with an allreduce per inner
         product across row bands), "hostloop" (force the sharded algorithm on
-        one GPU) or "grid" (force the grid-wide cooperative kernel)."""
+        one GPU), "grid" (force the grid-wide cooperative kernel) or "cgs2"
+        (classical Gram-Schmidt with one reorthogonalisation: 2 reductions per
+        iteration -- 2 allreduces across row bands -- instead of k+1)."""
         kind = self.sweep.kind if kind is None else kind
-        modes = {"auto": 0, "hostloop": 1, "grid": 2}
+        modes = {"auto": 0, "hostloop": 1, "grid": 2, "cgs2": 3}
         if arnoldi not in modes:
             raise ValueError(f"arnoldi must be one of {sorted(modes)}, got {arnoldi!r}")
         self.ctx.call("hs_set_gmres_mode", modes[arnoldi])

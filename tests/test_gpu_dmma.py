@@ -118,3 +118,17 @@ def test_hostloop_mgs_batched_cfg4():
     h = s.gmres(B, "bsp", tol=1e-6, maxit=1000, arnoldi="hostloop")
     assert h.iterations == a.iterations
     assert relerr(h.solution, a.solution) < 1e-12
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_cgs2_arnoldi(k):
+    """CGS2: iterations within +-1 of MGS, same solution to
+    the GMRES tolerance, and the reference's x within 1e-8 where a golden exists."""
+    s = system(k, "subdomain")
+    b = s.rhs()
+    a = s.gmres(b, "bsp", tol=1e-6, maxit=1000)
+    c2 = s.gmres(b, "bsp", tol=1e-6, maxit=1000, arnoldi="cgs2")
+    assert c2.converged and abs(c2.iterations - a.iterations) <= 1
+    assert relerr(c2.solution, a.solution) < 1e-9
+    assert relerr(s.apply_interface_operator(c2.solution), b) < 1e-6
+    np.testing.assert_allclose(c2.history[:a.iterations], a.history[:c2.iterations], rtol=1e-6)
