@@ -134,7 +134,12 @@ class Clocks:
 
 # ---------------------------------------------------------------- CPU baseline (oracle port)
 def _cpu_worker_init(cfgno):
-    global _W
+    """Factor one interior subdomain with the reference arithmetic; BLAS pinned
+    to one thread (SuperLU's supernodal updates call BLAS: one core per worker,
+    no oversubscription, and an honest core count)."""
+    global _W, _LIMIT
+    from threadpoolctl import threadpool_limits
+    _LIMIT = threadpool_limits(1)
     from paper_2209_10886_b200.configs import CONFIGS
     from oracle.fd import Problem, Subdomain
     from oracle.lattice import Lattice
