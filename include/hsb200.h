@@ -149,10 +149,11 @@ int hs_gmres(hs_ctx* ctx, int pc_kind, const double* b, double* x, int nrhs, dou
  * bands; same iteration counts as MGS within +-1. */
 int hs_set_gmres_mode(hs_ctx* ctx, int mode);
 
-/* 1 (default) = run a BSP apply with one RHS as a single persistent dataflow
- * launch (per-block completion counters instead of one launch per step);
- * 0 = one launch per sweep step.  Both give bitwise identical results. */
-int hs_set_fused(hs_ctx* ctx, int on);
+/* Bit mask.  Bit 0 (default on): a BSP apply with one RHS on per-subdomain
+ * maps runs as one persistent dataflow launch (per-block completion counters
+ * instead of one launch per step; bitwise identical results).  Bit 1 (default
+ * off): the same for the DMMA contraction (R RHS or shared maps). */
+int hs_set_fused(hs_ctx* ctx, int mask);
 
 /* ---- introspection (plan-only contexts too) ---------------------------- */
 /* Sizes: L (= 2 N_e n), number of subdomains, number of groups, 2 N_e. */

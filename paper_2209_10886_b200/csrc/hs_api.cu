@@ -117,22 +117,14 @@ void free_step(Ctx* c, DevStep& s) {
   s = DevStep();
 }
 
-// DMMA contraction tasks of a step.  shared = false: per-subdomain maps
-// (compact faces, rows of T_s), R right-hand sides per slab.  shared = true:
-// the class maps (4 faces W,S,N,E), one column per (subdomain, RHS), items of
-// the same class and face range batched into one contraction.
-int make_mma(Ctx* c, DevStep& st, int R, bool shared, DevMma** out) {
-  const int key = shared ? -R : R;
-  auto it = st.mma.find(key);
-  if (it != st.mma.end()) {
-    *out = &it->second;
-    return 0;
-  }
+// DMMA contraction tasks of a step (host vectors).  shared = false:
+// per-subdomain maps (compact faces, rows of T_s), R right-hand sides per slab.
+// shared = true: the class maps (4 faces W,S,N,E), one column per (subdomain,
+// RHS), items of the same class and face range batched into one contraction.
+void build_mma_host(Ctx* c, const StepTable& host, int R, bool shared, std::vector<MmaTask>& tasks,
+                    std::vector<MmaCol>& cols, double& flops) {
   const Plan& P = c->plan;
   const int n = c->n;
-  std::vector<MmaTask> tasks;
-  std::vector<MmaCol> cols;
-  double flops = 0;
   auto col_for = [&](const Item& item, int r, bool global_faces) {
     const SubPlan& sp = P.subs[item.s];
     MmaCol col;
@@ -150,7 +142,7 @@ int make_mma(Ctx* c, DevStep& st, int R, bool shared, DevMma** out) {
     return col;
   };
   if (!shared) {
-    for (const Item& item : st.host.items) {
+    for (const Item& item : host.items) {
       const SubPlan& sp = P.subs[item.s];
       const int K = sp.k * n;
       for (int r0 = (item.rlo / 32) * 32; r0 < item.rhi; r0 += 32)
@@ -165,58 +157,75 @@ int make_mma(Ctx* c, DevStep& st, int R, bool shared, DevMma** out) {
           flops += 8.0 * 32 * tk.ncols * K;
         }
     }
-  } else {
-    // group by (class, global face-row range)
-    std::map<std::tuple<int, int, int>, std::vector<int>> groups;
-    for (size_t i = 0; i < st.host.items.size(); ++i) {
-      const Item& item = st.host.items[i];
-      const SubPlan& sp = P.subs[item.s];
-      int glo, ghi;
-      if (item.rlo == 0 && item.rhi == sp.k * n) { glo = 0; ghi = 4 * n; }
-      else if (item.rlo == 0) { glo = 0; ghi = 2 * n; }      // lower faces W,S
-      else { glo = 2 * n; ghi = 4 * n; }                      // upper faces N,E
-      groups[std::make_tuple(c->sub_class[item.s], glo, ghi)].push_back((int)i);
-    }
-    const int K = 4 * n;
-    for (auto& g : groups) {
-      const int cls = std::get<0>(g.first), glo = std::get<1>(g.first), ghi = std::get<2>(g.first);
-      std::vector<MmaCol> gc;
-      for (int i : g.second)
-        for (int r = 0; r < R; ++r) gc.push_back(col_for(st.host.items[i], r, true));
-      for (size_t c0 = 0; c0 < gc.size(); c0 += 32) {
-        const int nc = (int)std::min<size_t>(32, gc.size() - c0);
-        const int base = (int)cols.size();
-        cols.insert(cols.end(), gc.begin() + c0, gc.begin() + c0 + nc);
-        for (int r0 = (glo / 32) * 32; r0 < ghi; r0 += 32) {
-          MmaTask tk;
-          tk.a_off = c->Tcls_off[cls] + (long long)(r0 / 32) * K * 32;
-          tk.K = K; tk.r0 = r0; tk.rlo = glo; tk.rhi = ghi;
-          tk.col0 = base;
-          tk.ncols = nc;
-          tasks.push_back(tk);
-          flops += 8.0 * 32 * nc * K;
-        }
+    return;
+  }
+  // group by (class, global face-row range)
+  std::map<std::tuple<int, int, int>, std::vector<int>> groups;
+  for (size_t i = 0; i < host.items.size(); ++i) {
+    const Item& item = host.items[i];
+    const SubPlan& sp = P.subs[item.s];
+    int glo, ghi;
+    if (item.rlo == 0 && item.rhi == sp.k * n) { glo = 0; ghi = 4 * n; }
+    else if (item.rlo == 0) { glo = 0; ghi = 2 * n; }      // lower faces W,S
+    else { glo = 2 * n; ghi = 4 * n; }                      // upper faces N,E
+    groups[std::make_tuple(c->sub_class[item.s], glo, ghi)].push_back((int)i);
+  }
+  const int K = 4 * n;
+  for (auto& g : groups) {
+    const int cls = std::get<0>(g.first), glo = std::get<1>(g.first), ghi = std::get<2>(g.first);
+    std::vector<MmaCol> gc;
+    for (int i : g.second)
+      for (int r = 0; r < R; ++r) gc.push_back(col_for(host.items[i], r, true));
+    for (size_t c0 = 0; c0 < gc.size(); c0 += 32) {
+      const int nc = (int)std::min<size_t>(32, gc.size() - c0);
+      const int base = (int)cols.size();
+      cols.insert(cols.end(), gc.begin() + c0, gc.begin() + c0 + nc);
+      for (int r0 = (glo / 32) * 32; r0 < ghi; r0 += 32) {
+        MmaTask tk;
+        tk.a_off = c->Tcls_off[cls] + (long long)(r0 / 32) * K * 32;
+        tk.K = K; tk.r0 = r0; tk.rlo = glo; tk.rhi = ghi;
+        tk.col0 = base;
+        tk.ncols = nc;
+        tasks.push_back(tk);
+        flops += 8.0 * 32 * nc * K;
       }
     }
   }
-  // bounds validation of every descriptor (a bad table must fail here, not fault)
-  {
-    const long long LR = P.L * (long long)R;
-    const size_t Aelems = shared ? c->Tcls_elems : c->T_elems;
-    for (const MmaTask& tk : tasks) {
-      if (tk.K % 16 || tk.a_off < 0 || (size_t)(tk.a_off + (long long)tk.K * 32) > Aelems)
-        return fail(c, -4, "internal: contraction task reads outside the maps");
-      for (int j = 0; j < tk.ncols; ++j) {
-        const MmaCol& col = cols[tk.col0 + j];
-        for (int q = 0; q < 4; ++q) {
-          if (col.in[q] >= 0 && col.in[q] + (long long)(n - 1) * R >= LR)
-            return fail(c, -4, "internal: contraction column reads outside the vector");
-          if (col.out[q] >= 0 && col.out[q] + (long long)(n - 1) * R >= LR)
-            return fail(c, -4, "internal: contraction column writes outside the vector");
-        }
+}
+
+// bounds validation of every descriptor (a bad table must fail here, not fault)
+int validate_mma(Ctx* c, const std::vector<MmaTask>& tasks, const std::vector<MmaCol>& cols, int R, bool shared) {
+  const int n = c->n;
+  const long long LR = c->plan.L * (long long)R;
+  const size_t Aelems = shared ? c->Tcls_elems : c->T_elems;
+  for (const MmaTask& tk : tasks) {
+    if (tk.K % 32 || tk.a_off < 0 || (size_t)(tk.a_off + (long long)tk.K * 32) > Aelems)
+      return fail(c, -4, "internal: contraction task reads outside the maps");
+    for (int j = 0; j < tk.ncols; ++j) {
+      const MmaCol& col = cols[tk.col0 + j];
+      for (int q = 0; q < 4; ++q) {
+        if (col.in[q] >= 0 && col.in[q] + (long long)(n - 1) * R >= LR)
+          return fail(c, -4, "internal: contraction column reads outside the vector");
+        if (col.out[q] >= 0 && col.out[q] + (long long)(n - 1) * R >= LR)
+          return fail(c, -4, "internal: contraction column writes outside the vector");
       }
     }
   }
+  return 0;
+}
+
+int make_mma(Ctx* c, DevStep& st, int R, bool shared, DevMma** out) {
+  const int key = shared ? -R : R;
+  auto it = st.mma.find(key);
+  if (it != st.mma.end()) {
+    *out = &it->second;
+    return 0;
+  }
+  std::vector<MmaTask> tasks;
+  std::vector<MmaCol> cols;
+  double flops = 0;
+  build_mma_host(c, st.host, R, shared, tasks, cols, flops);
+  if (validate_mma(c, tasks, cols, R, shared)) return -1;
   DevMma m;
   if (upload(c, &m.tasks, tasks) || upload(c, &m.cols, cols)) return -1;
   m.ntasks = (int)tasks.size();
@@ -226,6 +235,88 @@ int make_mma(Ctx* c, DevStep& st, int R, bool shared, DevMma** out) {
   for (const MmaTask& tk : tasks) m.minK = std::min(m.minK, tk.K);
   auto res = st.mma.emplace(key, m);
   *out = &res.first->second;
+  return 0;
+}
+
+void free_fused_mma(Ctx* c) {
+  DevFusedMma& f = c->fused_mma;
+  dfree(c, f.tasks, f.ntasks * sizeof(FusedMmaTask));
+  dfree(c, f.cols, f.ncols * sizeof(MmaCol));
+  dfree(c, f.deps, f.ndeps * sizeof(FusedDep));
+  dfree(c, f.incs, f.nincs * sizeof(int));
+  dfree(c, f.counters, (f.ncounters + 1) * sizeof(int));
+  f = DevFusedMma();
+}
+
+// Dataflow plan of one BSP apply on the DMMA contraction: every task of the
+// forward steps, the residual and the backward steps in schedule order, with
+// per-(block, 32-RHS chunk) completion counts it waits for / completes.
+int build_fused_mma(Ctx* c, int R, bool shared) {
+  free_fused_mma(c);
+  DevFusedMma& f = c->fused_mma;
+  const int n = c->n;
+  const int nch = (R + 31) / 32;
+  const int ncnt = c->plan.npairs * nch;
+  std::vector<FusedMmaTask> ftasks;
+  std::vector<MmaCol> cols;
+  std::vector<FusedDep> deps;
+  std::vector<int> incs;
+  std::vector<int> written(ncnt, 0);
+  double flops = 0;
+  auto counter = [&](long long off, int r) { return (int)((off - r) / ((long long)n * R)) * nch + r / 32; };
+  auto add = [&](const DevStep& st, int phase) {
+    std::vector<MmaTask> tasks;
+    std::vector<MmaCol> sc;
+    build_mma_host(c, st.host, R, shared, tasks, sc, flops);
+    std::vector<int> inc_step;
+    const int cbase = (int)cols.size();
+    cols.insert(cols.end(), sc.begin(), sc.end());
+    for (MmaTask tk : tasks) {
+      FusedMmaTask ft;
+      ft.phase = phase;
+      ft.dep0 = (int)deps.size(); ft.ndep = 0;
+      ft.inc0 = (int)incs.size(); ft.ninc = 0;
+      std::set<int> rd, wr;
+      const int r0 = std::max(tk.rlo, tk.r0), r1 = std::min(tk.rhi, tk.r0 + 32);
+      for (int j = 0; j < tk.ncols; ++j) {
+        const MmaCol& col = sc[tk.col0 + j];
+        for (int q = 0; q < 4; ++q)
+          if (col.in[q] >= 0) rd.insert(counter(col.in[q], col.r));
+        for (int q = r0 / n; q * n < r1; ++q)
+          if (q < 4 && col.out[q] >= 0) wr.insert(counter(col.out[q], col.r));
+      }
+      std::set<int> all(rd);
+      all.insert(wr.begin(), wr.end());
+      for (int k2 : all)
+        if (written[k2] > 0) { deps.push_back({k2, written[k2]}); ft.ndep++; }
+      for (int k2 : wr) { incs.push_back(k2); ft.ninc++; inc_step.push_back(k2); }
+      tk.col0 += cbase;
+      ft.task = tk;
+      ftasks.push_back(ft);
+    }
+    for (int k2 : inc_step) written[k2]++;
+  };
+  for (auto& st : c->fwd) add(st, 0);
+  add(c->full, 1);
+  for (auto& st : c->bwd) add(st, 2);
+  {
+    std::vector<MmaTask> plain;
+    for (auto& ft : ftasks) plain.push_back(ft.task);
+    if (validate_mma(c, plain, cols, R, shared)) return -1;
+  }
+  if (upload(c, &f.tasks, ftasks) || upload(c, &f.cols, cols) || upload(c, &f.deps, deps) ||
+      upload(c, &f.incs, incs))
+    return -1;
+  CK(dalloc(c, (void**)&f.counters, (ncnt + 1) * sizeof(int)));
+  f.ntasks = (int)ftasks.size();
+  f.ncols = (int)cols.size();
+  f.ndeps = (int)deps.size();
+  f.nincs = (int)incs.size();
+  f.ncounters = ncnt;
+  f.flops = flops;
+  f.R = R;
+  f.shared = shared;
+  f.built = true;
   return 0;
 }
 
@@ -345,6 +436,7 @@ int build_fused(Ctx* c) {
 int build_steps(Ctx* c) {
   if (!c->steps_dirty) return 0;
   free_fused(c);
+  free_fused_mma(c);
   for (auto& s : c->fwd) free_step(c, s);
   for (auto& s : c->bwd) free_step(c, s);
   for (auto& s : c->sp_fwd) free_step(c, s);
@@ -550,7 +642,7 @@ int do_precond(Ctx* c, int kind, const double2* r, double2* z, int R) {
   if (kind != HS_PC_BSP) return fail(c, 1, "unknown preconditioner kind");
   double2 *zl, *rp, *w;
   if (ws_get(c, "zL", LR, &zl) || ws_get(c, "rp", LR, &rp) || ws_get(c, "w", LR, &w)) return -1;
-  if (c->fused_mode && R == 1 && c->map_mode == 0 && c->plan.nranks == 1 && c->inter &&
+  if ((c->fused_mode & 1) && R == 1 && c->map_mode == 0 && c->plan.nranks == 1 && c->inter &&
       c->seam == HS_SEAM_DEDUP && c->full.nitems > 0) {
     // the whole apply as one dataflow launch (bitwise identical to the step sequence)
     if (!c->fused.built && build_fused(c)) return -1;
@@ -567,6 +659,34 @@ int do_precond(Ctx* c, int kind, const double2* r, double2* z, int R) {
       c->ev_pending.push_back({e0, e1});
       c->ev_bytes.push_back(c->fused.bytes);
       c->ev_flops.push_back(c->fused.bytes / 2.0);
+    }
+    return 0;
+  }
+  const bool shared = c->map_mode == 1;
+  // opt-in (bit 1): measured slower than per-step cluster split-K launches at
+  // cfg4 / shared cfg5 -- without split-K each task serialises its K chunks and
+  // the step-to-step dependency chain grows
+  if ((c->fused_mode & 2) && (R > 1 || shared) && c->n % 32 == 0 && c->plan.nranks == 1 && c->inter &&
+      c->seam == HS_SEAM_DEDUP && c->full.nitems > 0) {
+    // the whole apply on the DMMA contraction as one dataflow launch
+    if (!c->fused_mma.built || c->fused_mma.R != R || c->fused_mma.shared != shared)
+      if (build_fused_mma(c, R, shared)) return -1;
+    CK(cudaMemcpyAsync(zl, r, LR * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
+    FusedMmaArgs a;
+    a.A = shared ? c->Tcls : c->T;
+    a.r = r; a.zL = zl; a.rp = rp; a.w = w; a.z = z; a.R = R;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->timing) {
+      e0 = ev_get(c);
+      e1 = ev_get(c);
+      cudaEventRecord(e0, c->stream);
+    }
+    CK(launch_zmma_fused(*c, c->fused_mma, a));
+    if (e1) {
+      cudaEventRecord(e1, c->stream);
+      c->ev_pending.push_back({e0, e1});
+      c->ev_bytes.push_back(0.0);
+      c->ev_flops.push_back(c->fused_mma.flops);
     }
     return 0;
   }
@@ -746,6 +866,7 @@ int hs_destroy(hs_ctx* c) {
     free_step(c, c->full);
     for (auto& oc : c->classes) cudaFree(oc.T4);
     free_fused(c);
+    free_fused_mma(c);
     if (c->h_flags) cudaFreeHost(c->h_flags);
     if (c->flag_ev[0]) cudaEventDestroy(c->flag_ev[0]);
     if (c->flag_ev[1]) cudaEventDestroy(c->flag_ev[1]);
@@ -1434,9 +1555,10 @@ int hs_stream(hs_ctx* c, uint64_t* s) {
   return 0;
 }
 
-int hs_set_fused(hs_ctx* c, int on) {
+int hs_set_fused(hs_ctx* c, int mask) {
   if (!c) return fail(nullptr, 1, "null context");
-  c->fused_mode = on ? 1 : 0;
+  if (mask < 0 || mask > 3) return fail(c, 1, "fused mask must be 0..3");
+  c->fused_mode = mask;
   return 0;
 }
 

@@ -123,6 +123,43 @@ struct DevFused {
   bool built = false;
 };
 
+// Fused BSP apply on the DMMA contraction (R right-hand sides or shared maps).
+struct FusedMmaTask {
+  MmaTask task;
+  int phase;       // 0 forward, 1 residual, 2 backward
+  int dep0, ndep;  // waits: counters[block * nchunk + chunk] >= count
+  int inc0, ninc;  // counters this task completes
+};
+
+struct DevFusedMma {
+  FusedMmaTask* tasks = nullptr;
+  MmaCol* cols = nullptr;
+  FusedDep* deps = nullptr;
+  int* incs = nullptr;
+  int ntasks = 0, ncols = 0, ndeps = 0, nincs = 0;
+  int ncounters = 0;        // npairs * ceil(R / 32)
+  int* counters = nullptr;  // + 1 ticket
+  double flops = 0;
+  int R = 0;
+  bool shared = false, built = false;
+};
+
+struct FusedMmaArgs {
+  const FusedMmaTask* tasks;
+  const MmaCol* cols;
+  const FusedDep* deps;
+  const int* incs;
+  const double2* A;
+  const double2* r;
+  double2* zL;
+  double2* rp;
+  double2* w;
+  double2* z;
+  int* done;
+  int* ticket;
+  int ntasks, n, R;
+};
+
 // One distinct subdomain operator (Dirichlet mask) and its factor.
 struct OpClass {
   std::vector<uint8_t> mask;          // n*n, 1 = Dirichlet cell
@@ -163,6 +200,7 @@ struct Ctx {
   std::vector<DevStep> fwd, bwd, sp_fwd, sp_bwd;
   DevStep full;
   DevFused fused;        // BSP apply as one dataflow launch (1 RHS, per-subdomain maps, 1 rank)
+  DevFusedMma fused_mma; // the same on the DMMA contraction (R RHS or shared maps)
   int fused_mode = 1;    // 1: use the fused kernel when applicable, 0: one launch per step
   std::vector<std::vector<int>> seam_blocks;  // [dir] blocks of seam groups (literal mode)
   int* d_seam[2] = {nullptr, nullptr};

@@ -31,6 +31,7 @@ cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double
 void launch_zmma(Ctx& c, const DevMma& m, const double2* A, const double2* srcA, const double2* srcB,
                  const Epi& e, int R);
 cudaError_t set_zmma_smem_limit();
+cudaError_t launch_zmma_fused(Ctx& c, const DevFusedMma& f, FusedMmaArgs a);
 void launch_pack_strips(Ctx& c, const double2* T4, double2* out, int rows, int cols);
 
 // ---- factorisation (hs_schur.cu)

@@ -15,13 +15,19 @@
 // stride R between consecutive face positions).  K is staged in chunks of 32
 // through a 3-stage cp.async pipeline.  8 warps: 4 output quadrants (16 x 16 =
 // 2 x 2 DMMA tiles, real and imaginary accumulators; a complex MAC is 4 real
-// DMMAs) x 2 halves of every K chunk, reduced through shared memory.  When a
-// step has few tasks the K range is also split over a thread-block cluster of
-// KS CTAs whose partial tiles are summed by rank 0 through distributed shared
-// memory in rank order (deterministic).  The epilogue routes every output to
-// its block exactly like the single-RHS kernel (same Epi modes and slots).
+// DMMAs) x 2 halves of every K chunk, reduced through shared memory.
+//
+// Two launch forms share that main loop:
+//   * k_zmma: one launch per sweep step; when a step has few tasks the K range
+//     is also split over a thread-block cluster of KS CTAs whose partial tiles
+//     rank 0 sums through distributed shared memory in rank order;
+//   * k_zmma_fused: the whole BSP apply as one persistent dataflow launch
+//     (tickets in schedule order + per-(block, 32-RHS chunk) completion
+//     counters), as k_bsp_fused does for one right-hand side.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
+
+#include <algorithm>
 
 #include "hs_common.cuh"
 #include "hs_kernels.h"
@@ -52,51 +58,47 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-}  // namespace
+// column descriptors of the current task, staged in shared memory
+struct ZCols {
+  long long in[BN][4];
+  long long out[BN][4];
+  int slot[BN][4];
+  int r[BN];
+  int alt[BN];
+};
 
-// grid = ntasks * KS, cluster (KS, 1, 1); task = blockIdx.x / KS
-__global__ void __launch_bounds__(THREADS) k_zmma(const MmaTask* __restrict__ tasks,
-                                                  const MmaCol* __restrict__ cols,
-                                                  const double2* __restrict__ A,
-                                                  const double2* srcA, const double2* srcB, Epi e,
-                                                  int n, int R, int KS) {
-  extern __shared__ __align__(16) double2 dyn[];
-  __shared__ long long cin[BN][4], cout_[BN][4];
-  __shared__ int cslot[BN][4], cr[BN], calt[BN];
-  const int rank = KS > 1 ? (int)cg::this_cluster().block_rank() : 0;
-  const MmaTask tk = tasks[blockIdx.x / KS];
+__device__ __forceinline__ void zmma_cols(const MmaTask& tk, const MmaCol* __restrict__ cols, ZCols& zc) {
   const int tid = threadIdx.x;
   if (tid < BN) {
     if (tid < tk.ncols) {
       const MmaCol c = cols[tk.col0 + tid];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        cin[tid][q] = c.in[q];
-        cout_[tid][q] = c.out[q];
-        cslot[tid][q] = c.slot[q];
+        zc.in[tid][q] = c.in[q];
+        zc.out[tid][q] = c.out[q];
+        zc.slot[tid][q] = c.slot[q];
       }
-      cr[tid] = c.r;
-      calt[tid] = c.alt;
+      zc.r[tid] = c.r;
+      zc.alt[tid] = c.alt;
     } else {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        cin[tid][q] = -1;
-        cout_[tid][q] = -1;
-        cslot[tid][q] = -1;
-      }
-      cr[tid] = 0;
-      calt[tid] = 0;
+      for (int q = 0; q < 4; ++q) zc.in[tid][q] = zc.out[tid][q] = -1, zc.slot[tid][q] = -1;
+      zc.r[tid] = 0;
+      zc.alt[tid] = 0;
     }
   }
-  __syncthreads();
-  const double2* Ab = A + tk.a_off;  // strip containing rows r0..r0+31: [K][32]
-  const int nk_all = tk.K / KC;
-  const int kc0 = (int)((long long)nk_all * rank / KS), kc1 = (int)((long long)nk_all * (rank + 1) / KS);
-  const int nk = kc1 - kc0;
+}
 
+// K chunks [kc0, kc0 + nk) of the task; on return the wk == 0 warps hold the
+// summed tile (cre/cim), and shared memory may be reused.
+__device__ __forceinline__ void zmma_main(const MmaTask& tk, const ZCols& zc, double2* dyn,
+                                          const double2* __restrict__ A, const double2* srcA,
+                                          const double2* srcB, int n, int R, int kc0, int nk,
+                                          double (&cre)[2][2][2], double (&cim)[2][2][2]) {
+  const int tid = threadIdx.x;
+  const double2* Ab = A + tk.a_off;  // strip containing rows r0..r0+31: [K][32]
   auto As = [&](int st, int k, int m) -> double2& { return dyn[st * kStageElems + k * SA + m]; };
   auto Bs = [&](int st, int k, int j) -> double2& { return dyn[st * kStageElems + KC * SA + k * SB + j]; };
-
   auto load = [&](int stage, int kc) {
     const int k0 = kc * KC;
     const double2* asrc = Ab + (long long)k0 * BM;
@@ -110,29 +112,22 @@ __global__ void __launch_bounds__(THREADS) k_zmma(const MmaTask* __restrict__ ta
     for (int i = 0; i < (KC * BN) / THREADS; ++i) {
       const int el = tid + i * THREADS;
       const int kk = el / BN, j = el % BN;
-      const long long off = cin[j][q];
+      const long long off = zc.in[j][q];
       double2* dst = &Bs(stage, kk, j);
-      if (off >= 0) {
-        const double2* v = calt[j] ? srcB : srcA;
-        cp16(dst, v + off + (long long)(p0 + kk) * R);
-      } else {
-        *dst = make_double2(0.0, 0.0);
-      }
+      if (off >= 0) cp16(dst, (zc.alt[j] ? srcB : srcA) + off + (long long)(p0 + kk) * R);
+      else *dst = make_double2(0.0, 0.0);
     }
   };
-
   const int lane = tid & 31, warp = tid >> 5;
   const int wk = warp >> 2, wq = warp & 3;
   const int wm = wq >> 1, wn = wq & 1;
   const int gid = lane >> 2, tig = lane & 3;
-  double cre[2][2][2], cim[2][2][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
     for (int b = 0; b < 2; ++b)
 #pragma unroll
       for (int c = 0; c < 2; ++c) cre[a][b][c] = cim[a][b][c] = 0.0;
-
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < nk) load(s, kc0 + s);
@@ -183,9 +178,8 @@ __global__ void __launch_bounds__(THREADS) k_zmma(const MmaTask* __restrict__ ta
   }
   cp_wait<0>();
   __syncthreads();
-
   // reduce the two K halves: the wk = 1 warps hand their tiles to wk = 0
-  double2* red = dyn;  // 4 quadrants x 16 values per lane x 32 lanes
+  double2* red = dyn;
   if (wk == 1) {
 #pragma unroll
     for (int mt = 0; mt < 2; ++mt)
@@ -208,6 +202,32 @@ __global__ void __launch_bounds__(THREADS) k_zmma(const MmaTask* __restrict__ ta
           cim[mt][nt][h] += o.y;
         }
   }
+}
+
+}  // namespace
+
+// grid = ntasks * KS, cluster (KS, 1, 1); task = blockIdx.x / KS
+__global__ void __launch_bounds__(THREADS) k_zmma(const MmaTask* __restrict__ tasks,
+                                                  const MmaCol* __restrict__ cols,
+                                                  const double2* __restrict__ A,
+                                                  const double2* srcA, const double2* srcB, Epi e,
+                                                  int n, int R, int KS) {
+  extern __shared__ __align__(16) double2 dyn[];
+  __shared__ ZCols zc;
+  const int rank = KS > 1 ? (int)cg::this_cluster().block_rank() : 0;
+  const MmaTask tk = tasks[blockIdx.x / KS];
+  const int tid = threadIdx.x;
+  zmma_cols(tk, cols, zc);
+  __syncthreads();
+  const int nk_all = tk.K / KC;
+  const int kc0 = (int)((long long)nk_all * rank / KS), kc1 = (int)((long long)nk_all * (rank + 1) / KS);
+  double cre[2][2][2], cim[2][2][2];
+  zmma_main(tk, zc, dyn, A, srcA, srcB, n, R, kc0, kc1 - kc0, cre, cim);
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wk = warp >> 2, wq = warp & 3;
+  const int wm = wq >> 1, wn = wq & 1;
+  const int gid = lane >> 2, tig = lane & 3;
+  double2* red = dyn;
   if (KS > 1) {
     // cluster split-K: ranks > 0 publish their tile, rank 0 sums in rank order
     cg::cluster_group cl = cg::this_cluster();
@@ -241,7 +261,6 @@ __global__ void __launch_bounds__(THREADS) k_zmma(const MmaTask* __restrict__ ta
     if (rank != 0) return;
   }
   if (wk != 0) return;
-
   // epilogue: C(row gid, cols 2 tig + {0,1}) of each 8x8 tile
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt) {
@@ -255,16 +274,84 @@ __global__ void __launch_bounds__(THREADS) k_zmma(const MmaTask* __restrict__ ta
         const int j = wn * 16 + nt * 8 + 2 * tig + h;
         if (j >= tk.ncols) continue;
         const double2 y = make_double2(cre[mt][nt][h], cim[mt][nt][h]);
-        const int slot = cslot[j][q];
+        const int slot = zc.slot[j][q];
         if (slot == -1) {
-          const long long off = cout_[j][q];
+          const long long off = zc.out[j][q];
           if (off >= 0) epi_apply(e, off + (long long)p * R, y);
         } else if (slot >= 0) {
-          e.send_up[((long long)slot * n + p) * R + cr[j]] = y;
+          e.send_up[((long long)slot * n + p) * R + zc.r[j]] = y;
         } else {
-          e.send_dn[((long long)(-slot - 2) * n + p) * R + cr[j]] = y;
+          e.send_dn[((long long)(-slot - 2) * n + p) * R + zc.r[j]] = y;
         }
       }
+  }
+}
+
+// The whole BSP apply for R right-hand sides (or on the shared class maps) as
+// one persistent dataflow launch; see k_bsp_fused for the protocol.
+__global__ void __launch_bounds__(THREADS) k_zmma_fused(FusedMmaArgs a) {
+  extern __shared__ __align__(16) double2 dyn[];
+  __shared__ ZCols zc;
+  __shared__ int s_t;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wk = warp >> 2, wq = warp & 3;
+  const int wm = wq >> 1, wn = wq & 1;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int n = a.n, R = a.R;
+  for (;;) {
+    if (tid == 0) s_t = atomicAdd(a.ticket, 1);
+    __syncthreads();
+    const int t = s_t;
+    if (t >= a.ntasks) return;
+    const FusedMmaTask ft = a.tasks[t];
+    const MmaTask tk = ft.task;
+    for (int d = tid; d < ft.ndep; d += blockDim.x) {
+      const FusedDep dp = a.deps[ft.dep0 + d];
+      const volatile int* p = a.done + dp.block;
+      while (*p < dp.count) __nanosleep(32);
+    }
+    __threadfence();
+    zmma_cols(tk, a.cols, zc);
+    __syncthreads();
+    const double2* srcA = ft.phase == 0 ? a.zL : (ft.phase == 1 ? a.zL : a.w);
+    const double2* srcB = ft.phase == 0 ? a.r : (ft.phase == 1 ? a.zL : a.rp);
+    double cre[2][2][2], cim[2][2][2];
+    zmma_main(tk, zc, dyn, a.A, srcA, srcB, n, R, 0, tk.K / KC, cre, cim);
+    if (wk == 0) {
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const int row = tk.r0 + wm * 16 + mt * 8 + gid;
+        if (row < tk.rlo || row >= tk.rhi) continue;
+        const int q = row / n, p = row - q * n;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int j = wn * 16 + nt * 8 + 2 * tig + h;
+            if (j >= tk.ncols) continue;
+            const long long o0 = zc.out[j][q];
+            if (o0 < 0) continue;
+            const long long off = o0 + (long long)p * R;
+            const double2 y = make_double2(cre[mt][nt][h], cim[mt][nt][h]);
+            if (ft.phase == 0) {
+              a.zL[off] = cadd(__ldcg(a.zL + off), y);
+            } else if (ft.phase == 1) {
+              const double2 zl = __ldcg(a.zL + off);
+              const double2 v = csub(a.r[off], csub(zl, y));
+              a.rp[off] = v;
+              a.w[off] = v;
+              a.z[off] = cadd(zl, v);
+            } else {
+              a.w[off] = cadd(__ldcg(a.w + off), y);
+              a.z[off] = cadd(__ldcg(a.z + off), y);
+            }
+          }
+      }
+      __threadfence();
+    }
+    __syncthreads();
+    for (int i = tid; i < ft.ninc; i += blockDim.x) atomicAdd(a.done + a.incs[ft.inc0 + i], 1);
   }
 }
 
@@ -294,7 +381,25 @@ void launch_zmma(Ctx& c, const DevMma& m, const double2* A, const double2* srcA,
                      c.n, R, KS);
 }
 
+cudaError_t launch_zmma_fused(Ctx& c, const DevFusedMma& f, FusedMmaArgs a) {
+  static int per_sm = 0;
+  if (per_sm == 0) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_zmma_fused, THREADS, kZmmaSmem);
+    if (per_sm < 1) per_sm = 1;
+  }
+  cudaError_t e = cudaMemsetAsync(f.counters, 0, (f.ncounters + 1) * sizeof(int), c.stream);
+  if (e != cudaSuccess) return e;
+  a.tasks = f.tasks; a.cols = f.cols; a.deps = f.deps; a.incs = f.incs;
+  a.done = f.counters; a.ticket = f.counters + f.ncounters;
+  a.ntasks = f.ntasks; a.n = c.n;
+  const int grid = std::max(1, std::min(f.ntasks, per_sm * c.num_sms));
+  c.launches++;
+  k_zmma_fused<<<grid, THREADS, kZmmaSmem, c.stream>>>(a);
+  return cudaGetLastError();
+}
+
 cudaError_t set_zmma_smem_limit() {
+  cudaFuncSetAttribute(k_zmma_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kZmmaSmem);
   return cudaFuncSetAttribute(k_zmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kZmmaSmem);
 }
 

@@ -148,7 +148,7 @@ class GpuInterfaceSystem:
 
     def __init__(self, spec, partition: Partition, imp: ImpedanceSpec | None = None, workers: int = 1,
                  device: int = 0, rank: int = 0, nranks: int = 1, nccl_id: bytes | None = None,
-                 sweep: SweepConfig | None = None, maps: str = "subdomain", fused: bool = True):
+                 sweep: SweepConfig | None = None, maps: str = "subdomain", fused: bool | int = True):
         """maps = "subdomain": one compact Schur map per subdomain, streamed from
         HBM by the step kernels (the graded path); "shared": only the distinct
         operators' maps (generic + scatterer) are kept and every step is a DMMA
@@ -173,8 +173,9 @@ class GpuInterfaceSystem:
             raise ValueError(f"maps must be 'subdomain' or 'shared', got {maps!r}")
         self.maps = maps
         self.ctx.call("hs_set_map_mode", 1 if maps == "shared" else 0)
-        # one-RHS BSP applies as a single dataflow launch (bitwise equal to per-step launches)
-        self.ctx.call("hs_set_fused", 1 if fused else 0)
+        # one-RHS BSP applies as a single dataflow launch (bitwise equal to per-step
+        # launches); fused=3 also fuses the DMMA contraction paths (opt-in)
+        self.ctx.call("hs_set_fused", int(fused) if not isinstance(fused, bool) else (1 if fused else 0))
         self.home, cells = scatterer_cells(spec, partition)
         if self.home is not None:
             c = native.i32(cells)

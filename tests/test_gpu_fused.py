@@ -43,3 +43,17 @@ def test_fused_gmres_cfg2_golden():
     res = s.gmres(G["b"], "bsp", tol=1e-6, maxit=1000)
     assert res.iterations == int(G["gm_iters"])
     assert relerr(res.solution, G["gm_x"]) < 1e-8
+
+
+@pytest.mark.parametrize("name,c,R,maps", [("cfg1", CONFIGS[1], 40, "subdomain"), ("cfg2", CONFIGS[2], 64, "subdomain"),
+                                           ("cfg1", CONFIGS[1], 1, "shared"), ("cfg2", CONFIGS[2], 1, "shared"),
+                                           ("cfg3", CONFIGS[3], 1, "shared"), ("cfg2", CONFIGS[2], 8, "shared")])
+def test_fused_dmma_equals_steps(name, c, R, maps):
+    spec, part = product_problem(c)
+    a = GpuInterfaceSystem(spec, part, fused=False, maps=maps, sweep=SweepConfig(blocks=c["blocks"]))
+    b = GpuInterfaceSystem(spec, part, fused=3, maps=maps, sweep=SweepConfig(blocks=c["blocks"]))
+    g = cvec(17, a.layout.size, None if R == 1 else R)
+    za = a.bsp_apply(g)
+    zb = b.bsp_apply(g)
+    assert relerr(zb, za) < 1e-13, relerr(zb, za)
+    assert np.array_equal(b.bsp_apply(g), zb)  # the fused launch itself is deterministic
