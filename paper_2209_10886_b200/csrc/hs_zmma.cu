@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "hs_common.cuh"
 #include "hs_kernels.h"
@@ -363,7 +364,9 @@ void launch_zmma(Ctx& c, const DevMma& m, const double2* A, const double2* srcA,
   // split K over a cluster when the step has too few tasks to fill the GPU
   const int minK = m.minK;
   int KS = 1;
-  while (KS < 4 && (long long)m.ntasks * KS < 2LL * c.num_sms && minK / KC >= 2 * KS * 2) KS *= 2;
+  static int ks_max = getenv("HS_ZMMA_KS") ? atoi(getenv("HS_ZMMA_KS")) : 4;
+  static int min_chunks = getenv("HS_ZMMA_MINCH") ? atoi(getenv("HS_ZMMA_MINCH")) : 4;
+  while (KS < ks_max && (long long)m.ntasks * KS < 2LL * c.num_sms && minK / KC >= 2 * KS * min_chunks / 2) KS *= 2;
   c.launches++;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(m.ntasks * KS);
