@@ -65,18 +65,46 @@ int fail(Ctx* c, int code, const std::string& msg) {
     if ((c)->device < 0) return fail(c, 2, "plan-only context (device -1) cannot run kernels"); \
   } while (0)
 
+// Device allocations of a context are tracked by pointer so hs_memory is exact
+// whatever the caller passes as size to dfree.
 cudaError_t dalloc(Ctx* c, void** p, size_t bytes) {
   cudaError_t e = cudaMalloc(p, bytes > 0 ? bytes : 16);
-  if (e == cudaSuccess) c->dev_bytes += (int64_t)bytes;
+  if (e == cudaSuccess) {
+    c->alloc_sz[*p] = bytes;
+    c->dev_bytes += (int64_t)bytes;
+  }
   return e;
 }
 
-void dfree(Ctx* c, void* p, size_t bytes) {
-  if (p) {
-    cudaFree(p);
-    c->dev_bytes -= (int64_t)bytes;
+void dfree(Ctx* c, void* p, size_t /*bytes*/) {
+  if (!p) return;
+  auto it = c->alloc_sz.find(p);
+  if (it != c->alloc_sz.end()) {
+    c->dev_bytes -= (int64_t)it->second;
+    c->alloc_sz.erase(it);
   }
+  cudaFree(p);
 }
+
+// Temporaries of one call, freed when it returns (including error returns).
+struct TmpAllocs {
+  Ctx* c;
+  std::vector<void*> p;
+  explicit TmpAllocs(Ctx* ctx) : c(ctx) {}
+  ~TmpAllocs() {
+    for (void* q : p) dfree(c, q, 0);
+  }
+  template <class T>
+  cudaError_t alloc(T** out, size_t bytes) {
+    *out = nullptr;
+    cudaError_t e = dalloc(c, (void**)out, bytes);
+    if (e == cudaSuccess) p.push_back(*out);
+    return e;
+  }
+  void add(void* q) {
+    if (q) p.push_back(q);
+  }
+};
 
 // Named, grow-only device work buffers.
 int ws_get(Ctx* c, const std::string& name, size_t elems, double2** out) {
@@ -777,9 +805,11 @@ int upload_extras(Ctx* c, const std::map<std::tuple<int, int, int>, double2>& ex
     cols.push_back(std::get<2>(kv.first));
     vals.push_back(kv.second);
   }
-  if (upload(c, &e.d_x, xs) || upload(c, &e.d_col, cols) || upload(c, &e.d_val, vals)) return -1;
-  owned.push_back(e.d_x); owned.push_back(e.d_col); owned.push_back(e.d_val);
-  return 0;
+  e.d_x = nullptr; e.d_col = nullptr; e.d_val = nullptr;
+  const int up = upload(c, &e.d_x, xs) || upload(c, &e.d_col, cols) || upload(c, &e.d_val, vals);
+  for (void* q : {(void*)e.d_x, (void*)e.d_col, (void*)e.d_val})
+    if (q) owned.push_back(q);
+  return up ? -1 : 0;
 }
 
 }  // namespace
@@ -858,24 +888,19 @@ int hs_destroy(hs_ctx* c) {
   if (c->device >= 0) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
-    for (auto& kv : c->ws) cudaFree(kv.second.p);
     for (auto& s : c->fwd) free_step(c, s);
     for (auto& s : c->bwd) free_step(c, s);
     for (auto& s : c->sp_fwd) free_step(c, s);
     for (auto& s : c->sp_bwd) free_step(c, s);
     free_step(c, c->full);
-    for (auto& oc : c->classes) cudaFree(oc.T4);
     free_fused(c);
     free_fused_mma(c);
     if (c->h_flags) cudaFreeHost(c->h_flags);
     if (c->flag_ev[0]) cudaEventDestroy(c->flag_ev[0]);
     if (c->flag_ev[1]) cudaEventDestroy(c->flag_ev[1]);
-    cudaFree(c->T);
-    cudaFree(c->Tcls);
-    cudaFree(c->d_owned);
-    cudaFree(c->dsubs);
-    cudaFree(c->d_seam[0]);
-    cudaFree(c->d_seam[1]);
+    // everything else (maps, work buffers, factors, tables) is in the allocation map
+    for (auto& kv : c->alloc_sz) cudaFree(kv.first);
+    c->alloc_sz.clear();
     for (auto& p : c->ev_pending) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     if (c->nccl) ncclCommDestroy((ncclComm_t)c->nccl);
@@ -904,43 +929,52 @@ int hs_factor(hs_ctx* c) {
   NEED_GPU(c);
   CK(cudaSetDevice(c->device));
   const int n = c->n;
+  // a refactorisation replaces the previous class factors and maps
+  for (auto& oc : c->classes) {
+    dfree(c, oc.T4, 0);
+    oc.T4 = nullptr;
+  }
+  if (c->ws.count("__X")) {
+    dfree(c, c->ws["__X"].p, 0);
+    c->ws.erase("__X");
+  }
+  c->factored = false;
   build_classes(c);
   const int ncls = (int)c->classes.size();
   const long long nn = (long long)n * n;
+  TmpAllocs tmp(c);  // factorisation temporaries, released on every return path
   // masks
   std::vector<uint8_t> masks;
   for (auto& oc : c->classes) masks.insert(masks.end(), oc.mask.begin(), oc.mask.end());
   uint8_t* dmasks = nullptr;
   if (upload(c, &dmasks, masks)) return -1;
-  // X_k for all classes (kept: lifting solves reuse them)
-  if (c->ws.count("__X")) {
-    dfree(c, c->ws["__X"].p, c->ws["__X"].cap * sizeof(double2));
-    c->ws.erase("__X");
-  }
+  tmp.add(dmasks);
+  // X_k for all classes (kept: lifting solves reuse them; freed at destroy / refactor)
   double2* X;
   const long long xstride = nn * n;
   CK(dalloc(c, (void**)&X, (size_t)xstride * ncls * sizeof(double2)));
+  c->ws["__X"].p = X;
+  c->ws["__X"].cap = (size_t)xstride * ncls;
   double2 *Rp, *Cp;
   const long long pstride = 32LL * n;
-  CK(dalloc(c, (void**)&Rp, (size_t)pstride * ncls * sizeof(double2)));
-  CK(dalloc(c, (void**)&Cp, (size_t)pstride * ncls * sizeof(double2)));
+  CK(tmp.alloc(&Rp, (size_t)pstride * ncls * sizeof(double2)));
+  CK(tmp.alloc(&Cp, (size_t)pstride * ncls * sizeof(double2)));
   int* dbad;
-  CK(dalloc(c, (void**)&dbad, sizeof(int)));
+  CK(tmp.alloc(&dbad, sizeof(int)));
   CK(cudaMemsetAsync(dbad, 0, sizeof(int), c->stream));
   CK(factor_blocks(*c, X, xstride, dmasks, ncls, Rp, Cp, pstride, dbad));
   // boundary responses for the 4n unit columns
   const int R = 4 * n;
   double2 *Y, *Bk, *G;
   const long long ystride = nn * R, bstride = (long long)n * R, gstride = 4LL * n * R;
-  CK(dalloc(c, (void**)&Y, (size_t)ystride * ncls * sizeof(double2)));
-  CK(dalloc(c, (void**)&Bk, (size_t)bstride * ncls * sizeof(double2)));
-  CK(dalloc(c, (void**)&G, (size_t)gstride * ncls * sizeof(double2)));
+  CK(tmp.alloc(&Y, (size_t)ystride * ncls * sizeof(double2)));
+  CK(tmp.alloc(&Bk, (size_t)bstride * ncls * sizeof(double2)));
+  CK(tmp.alloc(&G, (size_t)gstride * ncls * sizeof(double2)));
   std::vector<ExtraRHS> extras(ncls);
-  std::vector<void*> owned;
   for (int k = 0; k < ncls; ++k) {
     std::map<std::tuple<int, int, int>, double2> ex;
     dirichlet_boundary_extras(c, c->classes[k], ex);
-    if (upload_extras(c, ex, extras[k], owned)) return -1;
+    if (upload_extras(c, ex, extras[k], tmp.p)) return -1;
   }
   CK(solve_boundary(*c, X, xstride, dmasks, ncls, R, R, extras.data(), Y, ystride, Bk, bstride, G, gstride));
   // T4 = -(s/d) I - (2 tau / (h^3 d^2)) G
@@ -950,7 +984,6 @@ int hs_factor(hs_ctx* c) {
   const std::complex<double> a = -(s / d), b = -(2.0 * tau) / (h * h * h * d * d);
   std::vector<double2*> T4s(ncls);
   for (int k = 0; k < ncls; ++k) {
-    dfree(c, c->classes[k].T4, 0);
     CK(dalloc(c, (void**)&c->classes[k].T4, (size_t)16 * nn * sizeof(double2)));
     launch_make_T4(*c, c->classes[k].T4, G + k * gstride, R, make_double2(a.real(), a.imag()),
                    make_double2(b.real(), b.imag()));
@@ -986,7 +1019,9 @@ int hs_factor(hs_ctx* c) {
       for (int q = 0; q < sp.k; ++q) faces[4 * s2 + q] = sp.face[q];
       cls[s2] = c->sub_class[s2];
     }
-    if (upload(c, &dtl, tl) || upload(c, &dfaces, faces) || upload(c, &dcls, cls) || upload(c, &dT4s, T4s)) return -1;
+    const int up = upload(c, &dtl, tl) || upload(c, &dfaces, faces) || upload(c, &dcls, cls) || upload(c, &dT4s, T4s);
+    tmp.add(dtl); tmp.add(dfaces); tmp.add(dcls); tmp.add(dT4s);
+    if (up) return -1;
     launch_scatter_T(*c, dtl, (int)tl.size(), dfaces, dcls, dT4s);
   } else if (n % 32 != 0) {
     return fail(c, 1, "shared-map mode needs cells_per_side divisible by 32");
@@ -1002,13 +1037,6 @@ int hs_factor(hs_ctx* c) {
     for (auto& v : h4)
       if (!std::isfinite(v.x) || !std::isfinite(v.y)) { bad = 2; break; }
   }
-  dfree(c, Y, 0); dfree(c, Bk, 0); dfree(c, G, 0); dfree(c, Rp, 0); dfree(c, Cp, 0); dfree(c, dbad, 0);
-  dfree(c, dtl, 0); dfree(c, dfaces, 0); dfree(c, dcls, 0); dfree(c, dT4s, 0); dfree(c, dmasks, 0);
-  for (void* p : owned) dfree(c, p, 0);
-  // keep masks of classes on host only; X stays for lifting solves
-  c->ws["__X"].p = X;  // freed at destroy / refactor
-  c->ws["__X"].cap = (size_t)xstride * ncls;
-  c->dev_bytes += 0;
   for (auto& oc : c->classes) oc.factored = true;
   if (bad) return fail(c, -3, "singular or non-finite subdomain factorisation");
   c->factored = true;
@@ -1055,26 +1083,26 @@ int hs_lifting_rhs(hs_ctx* c, const double* vals, int nrhs, double* bout, int me
     vpos += cells.size();
     if (sp.rank != c->plan.rank) continue;
     ExtraRHS er;
-    std::vector<void*> owned;
-    if (upload_extras(c, ex, er, owned)) return -1;
+    TmpAllocs tmp(c);
+    if (upload_extras(c, ex, er, tmp.p)) return -1;
     const long long nn = (long long)n * n;
     double2 *Y, *Bk, *G;
-    CK(dalloc(c, (void**)&Y, (size_t)nn * nrhs * sizeof(double2)));
-    CK(dalloc(c, (void**)&Bk, (size_t)n * nrhs * sizeof(double2)));
-    CK(dalloc(c, (void**)&G, (size_t)4 * n * nrhs * sizeof(double2)));
+    CK(tmp.alloc(&Y, (size_t)nn * nrhs * sizeof(double2)));
+    CK(tmp.alloc(&Bk, (size_t)n * nrhs * sizeof(double2)));
+    CK(tmp.alloc(&G, (size_t)4 * n * nrhs * sizeof(double2)));
     // single class: pass its X and mask
-    uint8_t* dm;
+    uint8_t* dm = nullptr;
     if (upload(c, &dm, oc.mask)) return -1;
+    tmp.add(dm);
     CK(solve_boundary(*c, oc.X, 0, dm, 1, nrhs, 0, &er, Y, 0, Bk, 0, G, 0));
     std::vector<int> ft(4, -1);
     for (int q = 0; q < sp.k; ++q) ft[sp.face[q]] = sp.tgt_block[q] * n;
-    int* dft;
+    int* dft = nullptr;
     if (upload(c, &dft, ft)) return -1;
+    tmp.add(dft);
     launch_lift_b(*c, b, G, nrhs, 0, nrhs, dft, make_double2(coef.real(), coef.imag()));
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(c->stream));
-    dfree(c, Y, 0); dfree(c, Bk, 0); dfree(c, G, 0); dfree(c, dm, 0); dfree(c, dft, 0);
-    for (void* p : owned) dfree(c, p, 0);
   }
   return finish_out(c, bout, b, LR, mem);
 }
@@ -1144,20 +1172,20 @@ int hs_reconstruct(hs_ctx* c, const double* g, const double* lift_vals, double* 
       }
     }
     ExtraRHS er;
-    std::vector<void*> owned;
-    if (upload_extras(c, ex, er, owned)) return -1;
-    int *dfo, *dab;
-    uint8_t* dm;
-    if (upload(c, &dfo, face_off) || upload(c, &dab, col_ab) || upload(c, &dm, oc.mask)) return -1;
+    TmpAllocs tmp(c);
+    if (upload_extras(c, ex, er, tmp.p)) return -1;
+    int *dfo = nullptr, *dab = nullptr;
+    uint8_t* dm = nullptr;
+    const int up = upload(c, &dfo, face_off) || upload(c, &dab, col_ab) || upload(c, &dm, oc.mask);
+    tmp.add(dfo); tmp.add(dab); tmp.add(dm);
+    if (up) return -1;
     double2 *Y, *Bk;
-    CK(dalloc(c, (void**)&Y, (size_t)n * n * R * sizeof(double2)));
-    CK(dalloc(c, (void**)&Bk, (size_t)n * R * sizeof(double2)));
+    CK(tmp.alloc(&Y, (size_t)n * n * R * sizeof(double2)));
+    CK(tmp.alloc(&Bk, (size_t)n * R * sizeof(double2)));
     CK(solve_fields(*c, oc.X, dm, R, dg, dfo, make_double2(rc.real(), rc.imag()), er, Y, Bk));
     launch_scatter_field(*c, df, c->n1 * n, Y, R, dab, 0);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(c->stream));
-    dfree(c, Y, 0); dfree(c, Bk, 0); dfree(c, dfo, 0); dfree(c, dab, 0); dfree(c, dm, 0);
-    for (void* p : owned) dfree(c, p, 0);
   }
   return finish_out(c, field, df, F, mem);
 }

@@ -227,6 +227,7 @@ struct Ctx {
   int64_t launches = 0;  // every kernel this context launched
   double k_ms = 0, k_bytes = 0, k_flops = 0;
   int64_t dev_bytes = 0;
+  std::map<void*, size_t> alloc_sz;  // live device allocations
   int num_sms = 148;
   int coop_ok = 0;
 };
