@@ -140,10 +140,12 @@ int hs_gmres(hs_ctx* ctx, int pc_kind, const double* b, double* x, int nrhs, dou
              int maxit, int* iters, double* hist, int* converged, int mem);
 
 /* Arnoldi implementation: 0 = auto (single GPU: one thread-block-cluster MGS
- * + Givens kernel per iteration for vectors up to 196k elements, else one
- * grid-wide cooperative MGS kernel; across row bands: host-driven MGS with one
- * ncclAllReduce per inner product), 1 = force the host-driven MGS (single-GPU
- * test of the sharded algorithm), 2 = force the grid-wide cooperative kernel,
+ * + Givens kernel per iteration for vectors up to 32k elements; one RHS
+ * beyond that: the register-resident grid-wide MGS + Givens kernel (k_mgs1);
+ * otherwise the grid-wide cooperative MGS kernel; across row bands:
+ * host-driven MGS with one ncclAllReduce per inner product), 1 = force the
+ * host-driven MGS (single-GPU test of the sharded algorithm), 2 = force the
+ * generic grid-wide cooperative kernel (k_mgs + k_givens),
  * 3 = CGS2 (classical Gram-Schmidt + one reorthogonalisation; one RHS): two
  * reductions per iteration instead of k+1 -- one allreduce each across row
  * bands; same iteration counts as MGS within +-1. */

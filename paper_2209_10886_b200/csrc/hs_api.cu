@@ -898,6 +898,7 @@ int hs_destroy(hs_ctx* c) {
     if (c->h_flags) cudaFreeHost(c->h_flags);
     if (c->flag_ev[0]) cudaEventDestroy(c->flag_ev[0]);
     if (c->flag_ev[1]) cudaEventDestroy(c->flag_ev[1]);
+    if (c->mgs1_slots) cudaFree(c->mgs1_slots);
     // everything else (maps, work buffers, factors, tables) is in the allocation map
     for (auto& kv : c->alloc_sz) cudaFree(kv.first);
     c->alloc_sz.clear();
@@ -1347,6 +1348,8 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
   const bool lookahead = c->map_mode == 1 || (double)c->T_elems * 16.0 < 2e9;
   int cchunk = 0;
   const int ccs = (dist || c->gmres_mode == 2) ? 0 : gmres_cluster_size(LR, R, &cchunk);
+  int m1chunk = 0, m1E = 0, m1bd = 0;
+  const int m1grid = (dist || c->gmres_mode == 2 || ccs > 0) ? 0 : gmres_mgs1_plan(*c, LR, R, maxit, &m1chunk, &m1E, &m1bd);
   int kdone = 0;
   bool stop = nact == 0;
   for (int k = 0; k < maxit && !stop; ++k) {
@@ -1366,6 +1369,8 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
       CK(gmres_givens(*c, G, k));
     } else if (ccs > 0) {
       CK(gmres_arnoldi_cluster(*c, G, k, ccs, cchunk));  // includes the Givens update
+    } else if (m1grid > 0) {
+      CK(gmres_arnoldi1(*c, G, k, m1grid, m1chunk, m1E, m1bd));  // includes the Givens update
     } else {
       CK(gmres_arnoldi(*c, G, k, grid, chunk));
       CK(gmres_givens(*c, G, k));

@@ -215,6 +215,8 @@ struct Ctx {
   int gmres_mode = 0;    // 0 auto (cooperative MGS on one rank), 1 host-driven MGS over owned blocks
   int* h_flags = nullptr;             // pinned: GMRES active counts (2 slots)
   cudaEvent_t flag_ev[2] = {nullptr, nullptr};
+  double* mgs1_slots = nullptr;  // k_mgs1 partial sums [2][3][256] + grid barrier counter
+  unsigned mgs1_bar = 0;         // barrier counter value after the last k_mgs1 launch
   int* d_owned = nullptr;  // this rank's blocks (host-driven MGS)
   int n_owned = 0;
   // execution control / timing

@@ -80,6 +80,10 @@ cudaError_t gmres_arnoldi(Ctx& c, GmresDev& G, int k, int grid, int chunk);
 cudaError_t gmres_givens(Ctx& c, GmresDev& G, int k);
 cudaError_t gmres_finish(Ctx& c, GmresDev& G, int maxit, double2* u);
 int gmres_coop_grid(Ctx& c, long long LR, int R, int* chunk);
+// one right-hand side: register-resident w, cp.async-prefetched basis, Givens fused
+// (grid > 0 when the vector and maxit fit; returns the grid)
+int gmres_mgs1_plan(Ctx& c, long long LR, int R, int maxit, int* chunk, int* E, int* bd);
+cudaError_t gmres_arnoldi1(Ctx& c, GmresDev& G, int k, int grid, int chunk, int E, int bd);
 // Arnoldi step + Givens on one thread-block cluster (small vectors)
 int gmres_cluster_size(long long LR, int R, int* chunk);
 cudaError_t gmres_arnoldi_cluster(Ctx& c, GmresDev& G, int k, int cs, int chunk);

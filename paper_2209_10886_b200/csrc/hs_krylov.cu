@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "hs_common.cuh"
 #include "hs_kernels.h"
@@ -23,6 +24,26 @@ namespace cg = cooperative_groups;
 namespace hs {
 
 __device__ __forceinline__ long long hoff(int k, int R) { return (long long)R * ((long long)k * (k + 3) / 2); }
+
+// Grid barrier of a cooperative launch on the context's own monotone counter
+// (cooperative groups' grid.sync was bimodal per launch on B200 -- 2.2 or 5.9
+// us per step with the same code, tools/allreduce_bench.cu -- while a fixed
+// counter is a stable 2.2 us).  Every CTA adds 1; barrier number s of a
+// launch completes at base + (s + 1) * gridDim.x (modulo 2^32).  Thread 0
+// fences its own prior writes (the CTA's partials are written by thread 0
+// or published to it through the bar.sync before).
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while ((int)(v - target) < 0);
+  }
+  __syncthreads();
+}
 
 // Block-level per-column reduction: red[tid] holds a thread value, threads
 // with equal tid % R share a column; P = blockDim / R is a power of two.
@@ -41,15 +62,15 @@ __device__ void grid_colsum(const double2* partials, int nblk, int R, double2* r
   const int tid = threadIdx.x;
   const int r = tid % R, i = tid / R, P = blockDim.x / R;
   double2 acc = make_double2(0, 0);
-  for (int b = i; b < nblk; b += P) acc = cadd(acc, partials[(long long)b * R + r]);
+  for (int b = i; b < nblk; b += P) acc = cadd(acc, __ldcg(&partials[(long long)b * R + r]));
   red[tid] = acc;
   block_colsum(red, R);
   if (tid < R) out[tid] = red[tid];
   __syncthreads();
 }
 
-__global__ void k_mgs(GmresDev G, int k, int chunk) {
-  cg::grid_group grid = cg::this_grid();
+__global__ void k_mgs(GmresDev G, int k, int chunk, unsigned* bar, unsigned bar_base) {
+  unsigned nbar = 0;
   extern __shared__ double2 sm[];
   const int R = G.R;
   double2* ws = sm;                    // chunk
@@ -71,7 +92,7 @@ __global__ void k_mgs(GmresDev G, int k, int chunk) {
     red[tid] = acc;
     block_colsum(red, R);
     if (tid < R) part[(long long)pb * nblk * R + (long long)blockIdx.x * R + tid] = red[tid];
-    grid.sync();
+    grid_barrier(bar, bar_base + (++nbar) * (unsigned)nblk);
     grid_colsum(part + (long long)pb * nblk * R, nblk, R, red, hsh);
     if (blockIdx.x == 0 && tid < R) G.wnorm0[tid] = sqrt(hsh[tid].x);
     pb ^= 1;
@@ -84,7 +105,7 @@ __global__ void k_mgs(GmresDev G, int k, int chunk) {
     red[tid] = acc;
     block_colsum(red, R);
     if (tid < R) part[(long long)pb * nblk * R + (long long)blockIdx.x * R + tid] = red[tid];
-    grid.sync();
+    grid_barrier(bar, bar_base + (++nbar) * (unsigned)nblk);
     grid_colsum(part + (long long)pb * nblk * R, nblk, R, red, hsh);
     pb ^= 1;
     if (blockIdx.x == 0 && tid < R) Hk[(long long)j * R + tid] = hsh[tid];
@@ -102,7 +123,7 @@ __global__ void k_mgs(GmresDev G, int k, int chunk) {
     red[tid] = acc;
     block_colsum(red, R);
     if (tid < R) part[(long long)pb * nblk * R + (long long)blockIdx.x * R + tid] = red[tid];
-    grid.sync();
+    grid_barrier(bar, bar_base + (++nbar) * (unsigned)nblk);
     grid_colsum(part + (long long)pb * nblk * R, nblk, R, red, hsh);
   }
   if (tid < R) {
@@ -118,26 +139,28 @@ __global__ void k_mgs(GmresDev G, int k, int chunk) {
 }
 
 // Givens update of column k of right-hand side r (if still active); returns
-// whether r stays active.
-__device__ bool givens_column(const GmresDev& G, int k, int r) {
+// whether r stays active.  Hc[j * hs] is entry j of the column and cs/sn[j *
+// st] the rotations of r: the global arrays, or a shared-memory copy
+// (k_mgs1); the new rotation, g, history and flags always go to G.
+__device__ bool givens_column_at(const GmresDev& G, int k, int r, double2* Hc, int hs, const double* csp,
+                                 const double2* snp, int st) {
   const int R = G.R;
   const double eps = 2.220446049250313e-16;
   if (!G.active[r]) return false;
-  double2* Hk = G.H + hoff(k, R);
-  const double hn = Hk[(long long)(k + 1) * R + r].x;
+  const double hn = Hc[(long long)(k + 1) * hs].x;
   for (int j = 0; j < k; ++j) {
-    const double c = G.cs[(long long)j * R + r];
-    const double2 s = G.sn[(long long)j * R + r];
-    const double2 a = Hk[(long long)j * R + r], b = Hk[(long long)(j + 1) * R + r];
+    const double c = csp[(long long)j * st];
+    const double2 s = snp[(long long)j * st];
+    const double2 a = Hc[(long long)j * hs], b = Hc[(long long)(j + 1) * hs];
     // t = c a + s b ;  b' = -conj(s) a + c b
     double2 t = cadd(make_double2(c * a.x, c * a.y), cmul(s, b));
     double2 sc = make_double2(-s.x, s.y);  // -conj(s)
     double2 b2 = cadd(cmul(sc, a), make_double2(c * b.x, c * b.y));
-    Hk[(long long)j * R + r] = t;
-    Hk[(long long)(j + 1) * R + r] = b2;
+    Hc[(long long)j * hs] = t;
+    Hc[(long long)(j + 1) * hs] = b2;
   }
-  const double2 a = Hk[(long long)k * R + r];
-  const double bb = Hk[(long long)(k + 1) * R + r].x;
+  const double2 a = Hc[(long long)k * hs];
+  const double bb = Hc[(long long)(k + 1) * hs].x;
   double c;
   double2 s;
   const double aa = hypot(a.x, a.y);
@@ -152,8 +175,8 @@ __device__ bool givens_column(const GmresDev& G, int k, int r) {
   }
   G.cs[(long long)k * R + r] = c;
   G.sn[(long long)k * R + r] = s;
-  Hk[(long long)k * R + r] = cadd(make_double2(c * a.x, c * a.y), make_double2(s.x * bb, s.y * bb));
-  Hk[(long long)(k + 1) * R + r] = make_double2(0, 0);
+  Hc[(long long)k * hs] = cadd(make_double2(c * a.x, c * a.y), make_double2(s.x * bb, s.y * bb));
+  Hc[(long long)(k + 1) * hs] = make_double2(0, 0);
   const double2 gk = G.g[(long long)k * R + r];
   // g[k+1] = -conj(s) g[k];  g[k] = c g[k]
   G.g[(long long)(k + 1) * R + r] = cmul(make_double2(-s.x, s.y), gk);
@@ -173,6 +196,10 @@ __device__ bool givens_column(const GmresDev& G, int k, int r) {
     return false;
   }
   return true;
+}
+
+__device__ bool givens_column(const GmresDev& G, int k, int r) {
+  return givens_column_at(G, k, r, G.H + hoff(k, G.R) + r, G.R, G.cs + r, G.sn + r, G.R);
 }
 
 // Givens update of column k for every active right-hand side.
@@ -353,6 +380,18 @@ __global__ void k_combine(GmresDev G, int mmax, double2* u) {
   }
 }
 
+// k_mgs1 partials [2][3][kMgs1MaxGrid] followed by the grid-barrier counter
+// shared by k_mgs and k_mgs1 (same stream: launches never overlap).
+static constexpr int kGridScratch = 2 * 3 * 256 + 16;  // doubles
+cudaError_t ensure_grid_scratch(Ctx& c) {
+  if (c.mgs1_slots) return cudaSuccess;
+  cudaError_t e = cudaMalloc((void**)&c.mgs1_slots, (size_t)kGridScratch * sizeof(double));
+  if (e == cudaSuccess) e = cudaMemsetAsync(c.mgs1_slots, 0, (size_t)kGridScratch * sizeof(double), c.stream);
+  c.mgs1_bar = 0;
+  return e;
+}
+static unsigned* grid_bar(Ctx& c) { return (unsigned*)(c.mgs1_slots + 2 * 3 * 256); }
+
 static int pow2_floor(int x) {
   int p = 1;
   while (p * 2 <= x) p *= 2;
@@ -446,8 +485,12 @@ cudaError_t gmres_arnoldi(Ctx& c, GmresDev& G, int k, int grid, int chunk) {
     cudaFuncSetAttribute(k_mgs, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
     attr_set = true;
   }
+  if (cudaError_t e = ensure_grid_scratch(c)) return e;
+  unsigned* bar = grid_bar(c);
+  unsigned bar_base = c.mgs1_bar;
+  c.mgs1_bar += (unsigned)(k + 3) * (unsigned)grid;  // k + 3 barriers
   c.launches++;
-  void* args[] = {(void*)&G, (void*)&k, (void*)&chunk};
+  void* args[] = {(void*)&G, (void*)&k, (void*)&chunk, (void*)&bar, (void*)&bar_base};
   return cudaLaunchCooperativeKernel((const void*)k_mgs, dim3(grid), dim3(bs), args, smem, c.stream);
 }
 
@@ -704,10 +747,261 @@ cudaError_t gmres_init_dist(Ctx& c, GmresDev& G, const double2* b, const int* bl
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// One right-hand side, vectors too large for one cluster (configs 3 and 5):
+// k_mgs1<E>, one CTA per SM, each thread owning E elements of w in registers.
+// Per j the CTA forms its partial <v_j, w>, the partials meet at one grid
+// barrier and every CTA sums them in the same fixed order (deterministic,
+// identical everywhere).  The update w -= h_j v_j and the next inner product
+// <v_{j+1}, w> are one pass, and v_{j+2} streams into shared memory
+// (cp.async, issued before step j's barrier) while the CTA waits, so each v_j
+// is read from HBM once and a step costs one barrier plus one coalesced read
+// of the partials.  ||w|| before orthogonalisation rides on step j = 0: k + 2
+// barriers in all (k_mgs: k + 3, each with two shared-memory tree
+// reductions).  CTA 0 then applies the Givens rotations from a shared-memory
+// copy of the column (no k_givens).  Exchange designs measured on B200
+// (tools/allreduce_bench.cu, 148 CTAs, per step): counter barrier +
+// component-major partials 2.2 us; CTA-major partials 7 us; barrier-free
+// tagged 64-bit words polled by every CTA 8.7 us (polling traffic); one
+// collector CTA + broadcast 5.4 us.  In the Arnoldi step (tools/mgs_bench.cu):
+// 3.3 us per j at L = 122880 and 4.5 us at L = 499712, against 5.0 and 8.0
+// for k_mgs + k_givens.
+static __device__ __forceinline__ void cpa16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+}
+static __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+static __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+static __device__ __forceinline__ void warp_sum3(double& a, double& b, double& c) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+  }
+}
+
+constexpr int kMgs1MaxGrid = 256;   // partials: [2 parities][3 components][kMgs1MaxGrid]
+static_assert(kGridScratch == 2 * 3 * kMgs1MaxGrid + 16, "grid scratch layout");
+constexpr int kMgs1MaxBlock = 896;  // 72 registers per thread
+
+template <int E>
+__global__ void __launch_bounds__(kMgs1MaxBlock, 1) k_mgs1(GmresDev G, int k, int chunk, int nbuf, double* slots, unsigned* bar, unsigned bar_base) {
+  extern __shared__ __align__(16) double2 sm1[];
+  __shared__ double red[32][3];
+  __shared__ double red2[1][3];
+  const int BD = blockDim.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = BD >> 5;
+  auto buf = [&](int j) { return sm1 + (size_t)(j % nbuf) * chunk; };  // v_j (nbuf = 2 or 3 slices)
+  double2* hs = sm1 + (size_t)nbuf * chunk;  // k + 2: the column (CTA 0)
+  double2* sns = hs + (k + 2);     // k
+  double* css = (double*)(sns + k);  // k
+  const long long LR = G.LR;
+  const long long e0 = (long long)blockIdx.x * chunk;
+  const long long eend = min(e0 + (long long)chunk, LR);
+  const int nblk = gridDim.x;
+  double2* w = G.V + (long long)(k + 1) * LR;
+  double2 wr[E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    const long long e = e0 + tid + (long long)i * BD;
+    wr[i] = e < eend ? w[e] : make_double2(0, 0);
+  }
+  auto prefetch = [&](int j) {
+    const double2* v = G.V + (long long)j * LR;
+    double2* b = buf(j);
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const long long e = e0 + tid + (long long)i * BD;
+      if (e < eend) cpa16(b + tid + i * BD, v + e);
+    }
+    cpa_commit();
+  };
+  int step = 0;
+  // block sum, publish, grid barrier, collect: (a, b, c) summed over the grid
+  // in a fixed order, returned identically to every thread of every CTA.
+  // Partials are stored component-major so the collecting warp's loads are
+  // fully coalesced (37 sectors per component at 148 CTAs; a CTA-major layout
+  // is 3.5x slower: 7 vs 2 us per step, tools/allreduce_bench.cu).
+  auto reduce = [&](double a, double b, double c, int pf_j) {
+    double* P = slots + (size_t)(step & 1) * 3 * kMgs1MaxGrid;
+    warp_sum3(a, b, c);
+    if (lane == 0) { red[wid][0] = a; red[wid][1] = b; red[wid][2] = c; }
+    __syncthreads();
+    if (wid == 0) {
+      a = lane < nw ? red[lane][0] : 0.0;
+      b = lane < nw ? red[lane][1] : 0.0;
+      c = lane < nw ? red[lane][2] : 0.0;
+      warp_sum3(a, b, c);
+      if (lane == 0) {
+        P[blockIdx.x] = a;
+        P[kMgs1MaxGrid + blockIdx.x] = b;
+        P[2 * kMgs1MaxGrid + blockIdx.x] = c;
+      }
+    }
+    // a basis vector issued here streams while the CTA waits at the barrier;
+    // issued after the barrier its loads would queue ahead of the partials
+    if (pf_j >= 0) prefetch(pf_j);
+    grid_barrier(bar, bar_base + (unsigned)(step + 1) * (unsigned)nblk);
+    if (wid == 0) {
+      double xa[kMgs1MaxGrid / 32], xb[kMgs1MaxGrid / 32], xc[kMgs1MaxGrid / 32];
+#pragma unroll
+      for (int u = 0; u < kMgs1MaxGrid / 32; ++u) {
+        const int q = lane + 32 * u;
+        xa[u] = q < nblk ? __ldcg(P + q) : 0.0;
+        xb[u] = q < nblk ? __ldcg(P + kMgs1MaxGrid + q) : 0.0;
+        xc[u] = q < nblk ? __ldcg(P + 2 * kMgs1MaxGrid + q) : 0.0;
+      }
+      a = b = c = 0.0;
+#pragma unroll
+      for (int u = 0; u < kMgs1MaxGrid / 32; ++u) { a += xa[u]; b += xb[u]; c += xc[u]; }
+      warp_sum3(a, b, c);
+      if (lane == 0) { red2[0][0] = a; red2[0][1] = b; red2[0][2] = c; }
+    }
+    __syncthreads();
+    ++step;
+    return make_double3(red2[0][0], red2[0][1], red2[0][2]);
+  };
+  double3 tot;
+  for (int j = 0; j < nbuf && j <= k; ++j) prefetch(j);
+  if (blockIdx.x == 0)
+    for (int j = tid; j < k; j += BD) { css[j] = G.cs[j]; sns[j] = G.sn[j]; }
+  {  // v_0 landed: the groups issued after it may still be in flight
+    const int later = min(nbuf, k + 1) - 1;
+    if (later >= 2) cpa_wait<2>(); else if (later == 1) cpa_wait<1>(); else cpa_wait<0>();
+  }
+  // j = 0: <v_0, w> and ||w||^2 before orthogonalisation
+  {
+    double2 acc = make_double2(0, 0);
+    double nrm = 0;
+    const double2* v0 = buf(0);
+#pragma unroll
+    for (int i = 0; i < E; ++i)
+      if (e0 + tid + (long long)i * BD < eend) {
+        cfma_conj(acc, v0[tid + i * BD], wr[i]);
+        nrm += wr[i].x * wr[i].x + wr[i].y * wr[i].y;
+      }
+    tot = reduce(acc.x, acc.y, nrm, -1);
+  }
+  double2 h = make_double2(tot.x, tot.y);
+  if (blockIdx.x == 0 && tid == 0) {
+    G.wnorm0[0] = sqrt(tot.z);
+    hs[0] = h;
+  }
+  for (int j = 0; j <= k; ++j) {
+    const double2* vj = buf(j);
+    const double2* vn = buf(j + 1);
+    const bool more = j + 1 <= k;
+    if (more) {  // v_{j+1} landed (each thread reads only what it copied); v_{j+2} may be in flight
+      if (nbuf == 3 && j + 2 <= k) cpa_wait<1>(); else cpa_wait<0>();
+    }
+    double2 acc = make_double2(0, 0);
+    double nrm = 0;
+#pragma unroll
+    for (int i = 0; i < E; ++i)
+      if (e0 + tid + (long long)i * BD < eend) {
+        wr[i] = csub(wr[i], cmul(h, vj[tid + i * BD]));  // w - H[j,k] V[j]
+        if (more) cfma_conj(acc, vn[tid + i * BD], wr[i]);
+        else nrm += wr[i].x * wr[i].x + wr[i].y * wr[i].y;
+      }
+    // v_j's slice is free: the vector nbuf steps ahead goes into it
+    tot = reduce(acc.x, acc.y, nrm, j + nbuf <= k ? j + nbuf : -1);
+    if (more) {
+      h = make_double2(tot.x, tot.y);
+      if (blockIdx.x == 0 && tid == 0) hs[j + 1] = h;
+    }
+  }
+  const double hn = sqrt(tot.z);
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    const long long e = e0 + tid + (long long)i * BD;
+    if (e < eend) w[e] = hn > 0 ? make_double2(wr[i].x / hn, wr[i].y / hn) : make_double2(0, 0);
+  }
+  if (blockIdx.x == 0) {
+    if (tid == 0) {
+      hs[k + 1] = make_double2(hn, 0);
+      *G.nactive = givens_column_at(G, k, 0, hs, 1, css, sns, 1) ? 1 : 0;
+    }
+    __syncthreads();
+    double2* Hk = G.H + hoff(k, 1);
+    for (int j = tid; j <= k + 1; j += BD) Hk[j] = hs[j];
+  }
+}
+
+// Shared-memory bytes of k_mgs1 at iteration k with nbuf basis slices.
+static size_t mgs1_smem(int chunk, int k, int nbuf) {
+  return (size_t)nbuf * chunk * sizeof(double2) + (size_t)(k + 2) * sizeof(double2) +
+         (size_t)k * (sizeof(double2) + sizeof(double));
+}
+
+static constexpr size_t kMgs1SmemMax = 220 * 1024;  // + static smem + the 1 KB per-CTA reserve <= 228 KB
+
+int gmres_mgs1_plan(Ctx& c, long long LR, int R, int maxit, int* chunk, int* E, int* bd) {
+  if (R != 1 || c.num_sms > kMgs1MaxGrid) return 0;
+  const long long nb = c.num_sms;
+  const long long ch = (LR + nb - 1) / nb;
+  int e = 1;
+  while (e < 8 && ch > (long long)e * kMgs1MaxBlock) e *= 2;
+  if (ch > (long long)e * kMgs1MaxBlock) return 0;
+  if (mgs1_smem((int)ch, maxit, 2) > kMgs1SmemMax) return 0;
+  *chunk = (int)ch;
+  *E = e;
+  *bd = (int)(((ch + e - 1) / e + 31) / 32 * 32);
+  return (int)((LR + ch - 1) / ch);
+}
+
+cudaError_t gmres_arnoldi1(Ctx& c, GmresDev& G, int k, int grid, int chunk, int E, int bd) {
+  static cudaError_t attr = [] {
+    cudaError_t e = cudaSuccess;
+    for (const void* f : {(const void*)k_mgs1<1>, (const void*)k_mgs1<2>, (const void*)k_mgs1<4>, (const void*)k_mgs1<8>})
+      if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMgs1SmemMax);
+    return e;
+  }();
+  if (attr != cudaSuccess) return attr;
+  if (cudaError_t e = ensure_grid_scratch(c)) return e;
+  c.launches++;
+  double* slots = (double*)c.mgs1_slots;
+  unsigned* bar = grid_bar(c);
+  unsigned bar_base = c.mgs1_bar;  // counter value before this launch (wraps modulo 2^32)
+  c.mgs1_bar += (unsigned)(k + 2) * (unsigned)grid;
+  // two basis slices (one step of lead for the stream; three measured no faster)
+  int nbuf = 2;
+  void* args[] = {(void*)&G, (void*)&k, (void*)&chunk, (void*)&nbuf, (void*)&slots, (void*)&bar, (void*)&bar_base};
+  const size_t smem = mgs1_smem(chunk, k, nbuf);
+  const void* fn = E == 1 ? (const void*)k_mgs1<1> : E == 2 ? (const void*)k_mgs1<2>
+                 : E == 4 ? (const void*)k_mgs1<4> : (const void*)k_mgs1<8>;
+  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(bd), args, smem, c.stream);
+}
+
+// Back substitution for one right-hand side with m <= blockDim: thread t owns
+// row t, the columns are swept from the last (entry (t, i) prefetched one
+// column ahead) with one barrier per column.
+__global__ void __launch_bounds__(1024) k_trisolve1(GmresDev G) {
+  __shared__ double2 ysh[2];
+  const int m = G.iters[0];
+  const int t = threadIdx.x;
+  double2 acc = t < m ? G.g[t] : make_double2(0, 0);
+  double2 hcur = (m >= 1 && t <= m - 1) ? G.H[hoff(m - 1, 1) + t] : make_double2(0, 0);
+  for (int i = m - 1; i >= 0; --i) {
+    const double2 hnx = (i >= 1 && t <= i - 1) ? G.H[hoff(i - 1, 1) + t] : make_double2(0, 0);
+    if (t == i) {
+      const double den = hcur.x * hcur.x + hcur.y * hcur.y;
+      const double2 y = make_double2((acc.x * hcur.x + acc.y * hcur.y) / den, (acc.y * hcur.x - acc.x * hcur.y) / den);
+      ysh[i & 1] = y;
+      G.y[i] = y;
+    }
+    __syncthreads();
+    if (t < i) acc = csub(acc, cmul(hcur, ysh[i & 1]));
+    hcur = hnx;
+  }
+}
+
 cudaError_t gmres_finish(Ctx& c, GmresDev& G, int mmax, double2* u) {
   int bs = G.R < 1024 ? ((G.R + 31) / 32) * 32 : 1024;
   c.launches += 2;
-  k_trisolve<<<1, bs, 0, c.stream>>>(G);
+  if (G.R == 1 && mmax <= 1024) k_trisolve1<<<1, ((mmax + 31) / 32) * 32, 0, c.stream>>>(G);
+  else k_trisolve<<<1, bs, 0, c.stream>>>(G);
   int g2 = (int)std::min<long long>((G.LR + 255) / 256, (long long)c.num_sms * 8);
   k_combine<<<g2 > 0 ? g2 : 1, 256, 0, c.stream>>>(G, mmax, u);
   return cudaGetLastError();

@@ -115,10 +115,10 @@ class Context:
         lib.hs_sizes(self.h_, C.byref(L), C.byref(nsub), C.byref(ng), C.byref(npairs))
         self.L, self.nsub, self.ngroups, self.npairs = L.value, nsub.value, ng.value, npairs.value
 
-    def __del__(self):
+    def __del__(self, _lib=lib):  # bound at definition: module globals may be gone at exit
         h = getattr(self, "h_", None)
         if h is not None and h.value:
-            lib.hs_destroy(h)
+            _lib.hs_destroy(h)
             self.h_ = _P()
 
     def close(self):
