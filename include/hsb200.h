@@ -139,10 +139,11 @@ int hs_half_apply(hs_ctx* ctx, int direction, const double* r, double* z, int nr
 int hs_gmres(hs_ctx* ctx, int pc_kind, const double* b, double* x, int nrhs, double tol,
              int maxit, int* iters, double* hist, int* converged, int mem);
 
-/* Arnoldi implementation: 0 = auto (single GPU: one thread-block-cluster MGS
- * + Givens kernel per iteration for vectors up to 32k elements; one RHS
- * beyond that: the register-resident grid-wide MGS + Givens kernel (k_mgs1);
- * otherwise the grid-wide cooperative MGS kernel; across row bands:
+/* Arnoldi implementation: 0 = auto (single GPU, one RHS: one MGS + Givens
+ * kernel per iteration with w register-resident -- on one thread-block
+ * cluster up to 32k elements (k_mgs1c), grid-wide beyond (k_mgs1); several
+ * RHS: the cluster kernel k_mgs_cluster up to 32k elements, else the
+ * grid-wide cooperative MGS kernel k_mgs + k_givens; across row bands:
  * host-driven MGS with one ncclAllReduce per inner product), 1 = force the
  * host-driven MGS (single-GPU test of the sharded algorithm), 2 = force the
  * generic grid-wide cooperative kernel (k_mgs + k_givens),

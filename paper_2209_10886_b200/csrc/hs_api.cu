@@ -1346,10 +1346,12 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
     CK(cudaEventCreateWithFlags(&c->flag_ev[1], cudaEventDisableTiming));
   }
   const bool lookahead = c->map_mode == 1 || (double)c->T_elems * 16.0 < 2e9;
+  int c1chunk = 0, c1E = 0, c1bd = 0;
+  const int c1cs = (dist || c->gmres_mode == 2) ? 0 : gmres_mgs1c_plan(LR, R, maxit, &c1chunk, &c1E, &c1bd);
   int cchunk = 0;
-  const int ccs = (dist || c->gmres_mode == 2) ? 0 : gmres_cluster_size(LR, R, &cchunk);
+  const int ccs = (dist || c->gmres_mode == 2 || c1cs > 0) ? 0 : gmres_cluster_size(LR, R, &cchunk);
   int m1chunk = 0, m1E = 0, m1bd = 0;
-  const int m1grid = (dist || c->gmres_mode == 2 || ccs > 0) ? 0 : gmres_mgs1_plan(*c, LR, R, maxit, &m1chunk, &m1E, &m1bd);
+  const int m1grid = (dist || c->gmres_mode == 2 || ccs > 0 || c1cs > 0) ? 0 : gmres_mgs1_plan(*c, LR, R, maxit, &m1chunk, &m1E, &m1bd);
   int kdone = 0;
   bool stop = nact == 0;
   for (int k = 0; k < maxit && !stop; ++k) {
@@ -1367,6 +1369,8 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
     } else if (dist) {
       CK(gmres_arnoldi_dist(*c, G, k, c->d_owned, c->n_owned, part2, mgsout, c->nccl));
       CK(gmres_givens(*c, G, k));
+    } else if (c1cs > 0) {
+      CK(gmres_arnoldi1c(*c, G, k, c1cs, c1chunk, c1E, c1bd));  // includes the Givens update
     } else if (ccs > 0) {
       CK(gmres_arnoldi_cluster(*c, G, k, ccs, cchunk));  // includes the Givens update
     } else if (m1grid > 0) {

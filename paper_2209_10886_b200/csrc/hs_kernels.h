@@ -84,6 +84,9 @@ int gmres_coop_grid(Ctx& c, long long LR, int R, int* chunk);
 // (grid > 0 when the vector and maxit fit; returns the grid)
 int gmres_mgs1_plan(Ctx& c, long long LR, int R, int maxit, int* chunk, int* E, int* bd);
 cudaError_t gmres_arnoldi1(Ctx& c, GmresDev& G, int k, int grid, int chunk, int E, int bd);
+// the same on one thread-block cluster (returns the cluster size; 0 = not applicable)
+int gmres_mgs1c_plan(long long LR, int R, int maxit, int* chunk, int* E, int* bd);
+cudaError_t gmres_arnoldi1c(Ctx& c, GmresDev& G, int k, int cs, int chunk, int E, int bd);
 // Arnoldi step + Givens on one thread-block cluster (small vectors)
 int gmres_cluster_size(long long LR, int R, int* chunk);
 cudaError_t gmres_arnoldi_cluster(Ctx& c, GmresDev& G, int k, int cs, int chunk);

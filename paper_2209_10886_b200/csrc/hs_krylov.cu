@@ -974,6 +974,192 @@ cudaError_t gmres_arnoldi1(Ctx& c, GmresDev& G, int k, int grid, int chunk, int 
   return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(bd), args, smem, c.stream);
 }
 
+// One right-hand side, small vectors (configs 1 and 2, L <= 32768): k_mgs1c<E>
+// runs the k_mgs1 algorithm on one thread-block cluster of CS <= 16 CTAs
+// (CS = 1: a single CTA, no cluster barrier).  The per-step partials are
+// exchanged through distributed shared memory -- each CTA publishes its
+// partial in its own shared memory, one cluster barrier, every CTA reads the
+// CS partials in rank order -- so a step costs a cluster barrier instead of a
+// grid barrier.  k_mgs_cluster (any R) needs ~5 us per step for the same work
+// (shared-memory tree reductions, unprefetched basis reads).
+template <int E>
+__global__ void __launch_bounds__(kMgs1MaxBlock, 1) k_mgs1c(GmresDev G, int k, int chunk) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int CS = (int)cl.num_blocks(), rank = (int)cl.block_rank();
+  extern __shared__ __align__(16) double2 sm1[];
+  __shared__ double red[32][3];
+  __shared__ double pub[2][3];  // this CTA's partial, by parity (read by the cluster)
+  __shared__ double tot3[3];
+  const int BD = blockDim.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = BD >> 5;
+  auto buf = [&](int j) { return sm1 + (size_t)(j & 1) * chunk; };  // v_j
+  double2* hs = sm1 + 2 * (size_t)chunk;  // k + 2: the column (rank 0)
+  double2* sns = hs + (k + 2);            // k
+  double* css = (double*)(sns + k);       // k
+  const long long LR = G.LR;
+  const long long e0 = (long long)rank * chunk;
+  const long long eend = min(e0 + (long long)chunk, LR);
+  double2* w = G.V + (long long)(k + 1) * LR;
+  double2 wr[E];
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    const long long e = e0 + tid + (long long)i * BD;
+    wr[i] = e < eend ? w[e] : make_double2(0, 0);
+  }
+  auto prefetch = [&](int j) {
+    const double2* v = G.V + (long long)j * LR;
+    double2* b = buf(j);
+#pragma unroll
+    for (int i = 0; i < E; ++i) {
+      const long long e = e0 + tid + (long long)i * BD;
+      if (e < eend) cpa16(b + tid + i * BD, v + e);
+    }
+    cpa_commit();
+  };
+  int step = 0;
+  auto reduce = [&](double a, double b, double c, int pf_j) {
+    const int par = step & 1;
+    warp_sum3(a, b, c);
+    if (lane == 0) { red[wid][0] = a; red[wid][1] = b; red[wid][2] = c; }
+    __syncthreads();
+    if (wid == 0) {
+      a = lane < nw ? red[lane][0] : 0.0;
+      b = lane < nw ? red[lane][1] : 0.0;
+      c = lane < nw ? red[lane][2] : 0.0;
+      warp_sum3(a, b, c);
+      if (lane == 0) {
+        if (CS > 1) { pub[par][0] = a; pub[par][1] = b; pub[par][2] = c; }
+        else { tot3[0] = a; tot3[1] = b; tot3[2] = c; }
+      }
+    }
+    if (pf_j >= 0) prefetch(pf_j);
+    if (CS == 1) {  // single CTA: the block sum is the total
+      __syncthreads();
+      ++step;
+      return make_double3(tot3[0], tot3[1], tot3[2]);
+    }
+    cl.sync();
+    if (wid == 0) {
+      // rank q's partial to lane q, summed in rank order by the butterfly
+      double x0 = 0.0, x1 = 0.0, x2 = 0.0;
+      if (lane < CS) {
+        const double* pq = cl.map_shared_rank(&pub[par][0], lane);
+        x0 = pq[0]; x1 = pq[1]; x2 = pq[2];
+      }
+      warp_sum3(x0, x1, x2);
+      if (lane == 0) { tot3[0] = x0; tot3[1] = x1; tot3[2] = x2; }
+    }
+    __syncthreads();
+    ++step;
+    return make_double3(tot3[0], tot3[1], tot3[2]);
+  };
+  double3 tot;
+  prefetch(0);
+  if (k >= 1) prefetch(1);
+  if (rank == 0)
+    for (int j = tid; j < k; j += BD) { css[j] = G.cs[j]; sns[j] = G.sn[j]; }
+  if (k >= 1) cpa_wait<1>(); else cpa_wait<0>();
+  {
+    double2 acc = make_double2(0, 0);
+    double nrm = 0;
+#pragma unroll
+    for (int i = 0; i < E; ++i)
+      if (e0 + tid + (long long)i * BD < eend) {
+        cfma_conj(acc, buf(0)[tid + i * BD], wr[i]);
+        nrm += wr[i].x * wr[i].x + wr[i].y * wr[i].y;
+      }
+    tot = reduce(acc.x, acc.y, nrm, -1);
+  }
+  double2 h = make_double2(tot.x, tot.y);
+  if (rank == 0 && tid == 0) {
+    G.wnorm0[0] = sqrt(tot.z);
+    hs[0] = h;
+  }
+  for (int j = 0; j <= k; ++j) {
+    const double2* vj = buf(j);
+    const double2* vn = buf(j + 1);
+    const bool more = j + 1 <= k;
+    if (more) cpa_wait<0>();
+    double2 acc = make_double2(0, 0);
+    double nrm = 0;
+#pragma unroll
+    for (int i = 0; i < E; ++i)
+      if (e0 + tid + (long long)i * BD < eend) {
+        wr[i] = csub(wr[i], cmul(h, vj[tid + i * BD]));  // w - H[j,k] V[j]
+        if (more) cfma_conj(acc, vn[tid + i * BD], wr[i]);
+        else nrm += wr[i].x * wr[i].x + wr[i].y * wr[i].y;
+      }
+    tot = reduce(acc.x, acc.y, nrm, j + 2 <= k ? j + 2 : -1);
+    if (more) {
+      h = make_double2(tot.x, tot.y);
+      if (rank == 0 && tid == 0) hs[j + 1] = h;
+    }
+  }
+  const double hn = sqrt(tot.z);
+#pragma unroll
+  for (int i = 0; i < E; ++i) {
+    const long long e = e0 + tid + (long long)i * BD;
+    if (e < eend) w[e] = hn > 0 ? make_double2(wr[i].x / hn, wr[i].y / hn) : make_double2(0, 0);
+  }
+  if (rank == 0) {
+    if (tid == 0) {
+      hs[k + 1] = make_double2(hn, 0);
+      *G.nactive = givens_column_at(G, k, 0, hs, 1, css, sns, 1) ? 1 : 0;
+    }
+    __syncthreads();
+    double2* Hk = G.H + hoff(k, 1);
+    for (int j = tid; j <= k + 1; j += BD) Hk[j] = hs[j];
+  }
+  if (CS > 1) cl.sync();  // peers' shared memory must outlive the last remote read
+}
+
+// Cluster size / slice for k_mgs1c: one CTA up to 2048 elements, else the
+// smallest power of two <= 16 with at most 1024 elements per CTA; 0 beyond
+// 32768 elements (k_mgs1 then).
+int gmres_mgs1c_plan(long long LR, int R, int maxit, int* chunk, int* E, int* bd) {
+  if (R != 1 || LR > 32768) return 0;
+  // measured (tools/mgs_bench.cu, us per step): L = 1536: 1 CTA 1.36, 2 CTAs
+  // 1.90; L = 14336: 16 CTAs 2.29, 8 CTAs 2.59, 4 CTAs 3.17
+  int cs = 1;
+  if (LR > 2048)
+    while (cs < 16 && (LR + cs - 1) / cs > 1024) cs *= 2;
+  const long long ch = (LR + cs - 1) / cs;
+  int e = 1;
+  while (e < 4 && ch > (long long)e * kMgs1MaxBlock) e *= 2;
+  if (ch > (long long)e * kMgs1MaxBlock || mgs1_smem((int)ch, maxit, 2) > kMgs1SmemMax) return 0;
+  *chunk = (int)ch;
+  *E = e;
+  *bd = (int)(((ch + e - 1) / e + 31) / 32 * 32);
+  return cs;
+}
+
+cudaError_t gmres_arnoldi1c(Ctx& c, GmresDev& G, int k, int cs, int chunk, int E, int bd) {
+  static cudaError_t attr = [] {
+    cudaError_t e = cudaSuccess;
+    for (const void* f : {(const void*)k_mgs1c<1>, (const void*)k_mgs1c<2>, (const void*)k_mgs1c<4>}) {
+      if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMgs1SmemMax);
+      if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    }
+    return e;
+  }();
+  if (attr != cudaSuccess) return attr;
+  c.launches++;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cs);
+  cfg.blockDim = dim3(bd);
+  cfg.dynamicSmemBytes = mgs1_smem(chunk, k, 2);
+  cfg.stream = c.stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cs;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (E == 1) return cudaLaunchKernelEx(&cfg, k_mgs1c<1>, G, k, chunk);
+  if (E == 2) return cudaLaunchKernelEx(&cfg, k_mgs1c<2>, G, k, chunk);
+  return cudaLaunchKernelEx(&cfg, k_mgs1c<4>, G, k, chunk);
+}
+
 // Back substitution for one right-hand side with m <= blockDim: thread t owns
 // row t, the columns are swept from the last (entry (t, i) prefetched one
 // column ahead) with one barrier per column.

@@ -58,17 +58,24 @@ int main(int argc, char** argv) {
   int chunk = 0, m1chunk = 0, E = 0, bd = 0;
   const int grid = gmres_coop_grid(c, L, 1, &chunk);
   const int m1grid = gmres_mgs1_plan(c, L, 1, maxit, &m1chunk, &E, &bd);
+  int ccchunk = 0, c1chunk = 0, c1E = 0, c1bd = 0;
+  const int ccs = gmres_cluster_size(L, 1, &ccchunk);
+  const int c1cs = gmres_mgs1c_plan(L, 1, maxit, &c1chunk, &c1E, &c1bd);
   std::vector<cudaEvent_t> ev(2 * (KMAX + 1));
   for (auto& e : ev) cudaEventCreate(&e);
   printf("{\"L\": %lld, \"grid\": %d, \"mgs1_grid\": %d, \"E\": %d, \"block\": %d}\n", L, grid, m1grid, E, bd);
-  for (int variant = 0; variant < 2; ++variant) {
+  const char* names[] = {"k_mgs+k_givens", "k_mgs1", "k_mgs_cluster", "k_mgs1c"};
+  for (int variant = 0; variant < 4; ++variant) {
+    if ((variant == 1 && m1grid <= 0) || (variant == 2 && ccs <= 0) || (variant == 3 && c1cs <= 0)) continue;
     // all launches back to back (the GPU stays busy, clocks stay up), events read at the end
     for (int k = 0; k <= KMAX; ++k) {
       cudaMemcpyAsync(G.V + (long long)(k + 1) * L, W, L * sizeof(double2), cudaMemcpyDeviceToDevice, c.stream);
       cudaEventRecord(ev[2 * k], c.stream);
       cudaError_t e;
       if (variant == 0) { e = gmres_arnoldi(c, G, k, grid, chunk); if (!e) e = gmres_givens(c, G, k); }
-      else e = gmres_arnoldi1(c, G, k, m1grid, m1chunk, E, bd);
+      else if (variant == 1) e = gmres_arnoldi1(c, G, k, m1grid, m1chunk, E, bd);
+      else if (variant == 2) e = gmres_arnoldi_cluster(c, G, k, ccs, ccchunk);
+      else e = gmres_arnoldi1c(c, G, k, c1cs, c1chunk, c1E, c1bd);
       cudaEventRecord(ev[2 * k + 1], c.stream);
       if (e) { printf("launch error %s\n", cudaGetErrorString(e)); return 1; }
     }
@@ -82,7 +89,7 @@ int main(int argc, char** argv) {
       if (k == 50) s50 = ms;
     }
     printf("{\"variant\": \"%s\", \"total_ms\": %.3f, \"k10_us\": %.1f, \"k50_us\": %.1f, \"per_j_us\": %.2f}\n",
-           variant == 0 ? "k_mgs+k_givens" : "k_mgs1", sum, s10 * 1e3, s50 * 1e3, (s50 - s10) * 1e3 / 40);
+           names[variant], sum, s10 * 1e3, s50 * 1e3, (s50 - s10) * 1e3 / 40);
   }
   {
     // the exchange micro-benchmark kernel (mode 1: grid.sync + component-major partials), same process/stream
