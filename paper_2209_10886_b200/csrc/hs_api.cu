@@ -408,14 +408,16 @@ int build_fused(Ctx* c) {
   std::vector<FusedTile> tiles;
   std::vector<FusedDep> deps;
   std::vector<int> written(P.npairs, 0);
-  // tile shape: one 32-row strip, 16 warps splitting its columns (measured on
-  // B200: 16 warps beat 8 at cfg2/cfg5 -- twice the bytes in flight per tile
-  // shortens the dependency chain links; 2 strips per tile (80 registers,
-  // half the occupancy) was slower at cfg3).  HS_FUSED_RT / HS_FUSED_NW override.
+  // tile shape: one 32-row strip, kSumWarps warps splitting its columns
+  // (2 strips per tile -- 80 registers, half the occupancy -- was slower at
+  // cfg3; HS_FUSED_RT=2 selects it).
   f.rt = 1;
-  f.nw = 16;
+  f.nw = kSumWarps;
   if (const char* e = getenv("HS_FUSED_RT")) f.rt = std::max(1, std::min(2, atoi(e)));
-  if (const char* e = getenv("HS_FUSED_NW")) f.nw = atoi(e) == 8 ? 8 : 16;
+  // TMA-staged maps (k_bsp_tma) up to 512 map columns, register streaming beyond
+  // (measured on B200, ms per apply, TMA vs streaming: cfg1 0.044/0.046, cfg2
+  // 0.091/0.094, cfg3 0.334/0.355, cfg5 2.37/2.25).  HS_FUSED_TMA=0/1 overrides.
+  f.tma = f.rt == 1;  // decided on maxK below
   const int TR = kRowTile * f.rt;
   auto add = [&](const DevStep& st, int phase) {
     std::vector<int> inc;
@@ -452,6 +454,8 @@ int build_fused(Ctx* c) {
   for (auto& st : c->fwd) add(st, 0);
   add(c->full, 1);
   for (auto& st : c->bwd) add(st, 2);
+  f.tma = f.tma && f.maxK <= 512;
+  if (const char* e = getenv("HS_FUSED_TMA")) f.tma = atoi(e) != 0 && f.rt == 1;
   if (upload(c, &f.items, items) || upload(c, &f.tiles, tiles) || upload(c, &f.deps, deps)) return -1;
   CK(dalloc(c, (void**)&f.counters, (P.npairs + 1) * sizeof(int)));
   f.nitems = (int)items.size();

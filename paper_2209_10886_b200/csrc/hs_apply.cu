@@ -14,6 +14,10 @@
 // memory.  Map elements are read once with 128-bit streaming loads.
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
 #include <algorithm>
 
 #include "hs_common.cuh"
@@ -40,23 +44,38 @@ __global__ void __launch_bounds__(NW * 32) k_step1(const DevTile* __restrict__ t
   for (int i = threadIdx.x; i < K; i += NW * 32) xs[i] = x[i];
   __syncthreads();
 
+  // column c belongs to warp (c % 32) / (32 / NW) and accumulator c & 1: the
+  // order of the TMA-staged fused kernel, which consumes 32-column chunks
   const double2* Tt = T + sb.T_off + (long long)tl.tile * K * kRowTile + lane;
-  const int per = (K + NW - 1) / NW;
-  const int c0 = warp * per;
-  const int c1 = min(K, c0 + per);
+  constexpr int CPW = 32 / NW;
   double2 a0 = make_double2(0, 0), a1 = make_double2(0, 0);
-  int c = c0;
-  for (; c + 8 <= c1; c += 8) {
-    double2 t[8];
+  constexpr int U = 8 / CPW;  // chunks per unrolled batch: 8 loads in flight
+  const int nch = (K + 31) / 32;
+  int ch = 0;
+  for (; ch + U <= nch && (ch + U) * 32 <= K; ch += U) {
+    double2 t[U][CPW];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) t[u] = ld_stream(Tt + (long long)(c + u) * kRowTile);
+    for (int v = 0; v < U; ++v)
 #pragma unroll
-    for (int u = 0; u < 8; u += 2) {
-      cfma(a0, t[u], xs[c + u]);
-      cfma(a1, t[u + 1], xs[c + u + 1]);
-    }
+      for (int u = 0; u < CPW; ++u) t[v][u] = ld_stream(Tt + (long long)((ch + v) * 32 + warp * CPW + u) * kRowTile);
+#pragma unroll
+    for (int v = 0; v < U; ++v)
+#pragma unroll
+      for (int u = 0; u < CPW; ++u) {
+        const int col = (ch + v) * 32 + warp * CPW + u;
+        if (col & 1) cfma(a1, t[v][u], xs[col]);
+        else cfma(a0, t[v][u], xs[col]);
+      }
   }
-  for (; c < c1; ++c) cfma(a0, ld_stream(Tt + (long long)c * kRowTile), xs[c]);
+  for (; ch < nch; ++ch)
+#pragma unroll
+    for (int u = 0; u < CPW; ++u) {
+      const int col = ch * 32 + warp * CPW + u;
+      if (col < K) {
+        if (col & 1) cfma(a1, ld_stream(Tt + (long long)col * kRowTile), xs[col]);
+        else cfma(a0, ld_stream(Tt + (long long)col * kRowTile), xs[col]);
+      }
+    }
   part[warp * 32 + lane] = cadd(a0, a1);
   __syncthreads();
   if (warp == 0) {
@@ -98,7 +117,7 @@ struct FusedArgs {
   double2* z;
   int* done;
   int* ticket;
-  int ntiles, n;
+  int ntiles, n, maxK;
 };
 
 // RT = 32-row strips per tile (RT * K ~ 1024 columns-strips keeps the fixed
@@ -138,32 +157,42 @@ __global__ void __launch_bounds__(NW * 32) k_bsp_fused(FusedArgs a) {
     const int nstrip = (K + kRowTile - 1) / kRowTile;
     const int s0 = ft.tile * RT;
     const double2* Tt = a.T + sb.T_off + (long long)s0 * K * kRowTile + lane;
-    const int per = (K + NW - 1) / NW;
-    const int c0 = warp * per;
-    const int c1 = min(K, c0 + per);
+    // column c belongs to warp (c % 32) / (32 / NW), accumulator c & 1 (k_step1's order)
+    constexpr int CPW = 32 / NW;
+    constexpr int U = 8 / CPW;  // chunks per unrolled batch: 8 loads in flight per strip
     double2 acc[RT][2];
 #pragma unroll
     for (int q = 0; q < RT; ++q) acc[q][0] = acc[q][1] = make_double2(0, 0);
-    int c = c0;
-    for (; c + 8 <= c1; c += 8) {
+    const int nch = (K + 31) / 32;
+    int ch = 0;
+    for (; ch + U <= nch && (ch + U) * 32 <= K; ch += U) {
 #pragma unroll
       for (int q = 0; q < RT; ++q) {
         if (s0 + q >= nstrip) break;
         const double2* Tq = Tt + (long long)q * K * kRowTile;
-        double2 tv[8];
+        double2 tv[U][CPW];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) tv[u] = ld_stream(Tq + (long long)(c + u) * kRowTile);
+        for (int v = 0; v < U; ++v)
 #pragma unroll
-        for (int u = 0; u < 8; u += 2) {
-          cfma(acc[q][0], tv[u], xs[c + u]);
-          cfma(acc[q][1], tv[u + 1], xs[c + u + 1]);
-        }
+          for (int u = 0; u < CPW; ++u) tv[v][u] = ld_stream(Tq + (long long)((ch + v) * 32 + warp * CPW + u) * kRowTile);
+#pragma unroll
+        for (int v = 0; v < U; ++v)
+#pragma unroll
+          for (int u = 0; u < CPW; ++u) {
+            const int col = (ch + v) * 32 + warp * CPW + u;
+            cfma(acc[q][col & 1], tv[v][u], xs[col]);
+          }
       }
     }
-    for (; c < c1; ++c)
+    for (; ch < nch; ++ch)
 #pragma unroll
-      for (int q = 0; q < RT; ++q)
-        if (s0 + q < nstrip) cfma(acc[q][0], ld_stream(Tt + (long long)q * K * kRowTile + (long long)c * kRowTile), xs[c]);
+      for (int u = 0; u < CPW; ++u) {
+        const int col = ch * 32 + warp * CPW + u;
+        if (col < K)
+#pragma unroll
+          for (int q = 0; q < RT; ++q)
+            if (s0 + q < nstrip) cfma(acc[q][col & 1], ld_stream(Tt + (long long)q * K * kRowTile + (long long)col * kRowTile), xs[col]);
+      }
 #pragma unroll
     for (int q = 0; q < RT; ++q) part[(q * NW + warp) * 32 + lane] = cadd(acc[q][0], acc[q][1]);
     __syncthreads();
@@ -197,6 +226,182 @@ __global__ void __launch_bounds__(NW * 32) k_bsp_fused(FusedArgs a) {
       // one completion per (tile, written block); all strips' stores are fenced above
       const int r0 = max(it.rlo, s0 * kRowTile), r1 = min(it.rhi, (s0 + RT) * kRowTile);
       for (int f = r0 / n; f * n < r1; ++f) atomicAdd(a.done + sb.tgt[f] / n, 1);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// The fused BSP apply with the maps staged by the Tensor Memory Accelerator:
+// a producer warp claims tiles (ticket order), and for each issues bulk
+// copies (cp.async.bulk, one elected thread) of the tile's 32-column chunks
+// -- 16 KB each, contiguous in the strip-major layout -- into a ring of S
+// shared-memory stages with mbarrier full/empty handshakes.  NW consumer warps
+// wait for the tile's dependencies, load its incoming slab and consume the
+// chunks as they land.  The map stream never waits on a dependency: while the
+// consumers wait (or run the epilogue) the producer keeps filling the ring
+// with this tile's and the next tile's chunks, so HBM stays busy (the
+// register-streaming kernel idles ~30 % of a tile's time at cfg3 on the
+// dependency wait, slab load and epilogue; profiles/r01/fused_trace_summary.txt).
+// Same arithmetic order as k_step1 (bitwise identical).
+struct TileDesc {
+  long long map_off;  // element offset of the tile's 32-row strip
+  int t, K, phase, alt, in_off, rlo, rhi, row0, dep0, ndep;
+  int tgt[4];
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  unsigned ok = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void consumers_sync(int nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+constexpr int kChunk = 32 * kRowTile;  // elements of one 32-column chunk of a strip
+
+template <int NW, int S>
+__global__ void __launch_bounds__((NW + 1) * 32, 1) k_bsp_tma(FusedArgs a) {
+  extern __shared__ __align__(128) double2 smt[];
+  double2* stage = smt;                // S x kChunk
+  double2* xs = stage + S * kChunk;    // maxK
+  double2* part = xs + a.maxK;         // NW x 32
+  __shared__ __align__(8) unsigned long long full[S], empty[S], dfull[2], dempty[2];
+  __shared__ TileDesc desc[2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NT = NW * 32;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], NW); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], NW); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == NW) {  // ---- producer
+    if (lane == 0) {
+      long long g = 0;
+      for (int q = 0;; ++q) {
+        const int d = q & 1;
+        mbar_wait(&dempty[d], ((q >> 1) & 1) ^ 1);
+        TileDesc td;
+        td.t = atomicAdd(a.ticket, 1);
+        if (td.t < a.ntiles) {
+          const FusedTile ft = a.tiles[td.t];
+          const DevItem it = a.items[ft.item];
+          const DevSub sb = a.subs[it.s];
+          td.K = sb.k * a.n;
+          td.row0 = ft.tile * kRowTile;
+          td.map_off = sb.T_off + (long long)ft.tile * td.K * kRowTile;
+          td.phase = ft.phase; td.alt = it.alt; td.in_off = sb.in_off;
+          td.rlo = it.rlo; td.rhi = it.rhi; td.dep0 = ft.dep0; td.ndep = ft.ndep;
+          for (int f = 0; f < 4; ++f) td.tgt[f] = sb.tgt[f];
+        }
+        desc[d] = td;
+        mbar_arrive(&dfull[d]);
+        if (td.t >= a.ntiles) break;
+        const int nch = (td.K + 31) / 32;
+        const double2* src = a.T + td.map_off;
+        for (int ch = 0; ch < nch; ++ch, ++g) {
+          const int st = (int)(g % S);
+          mbar_wait(&empty[st], (unsigned)((g / S) & 1) ^ 1);
+          const unsigned bytes = (unsigned)min(32, td.K - 32 * ch) * kRowTile * sizeof(double2);
+          mbar_expect_tx(&full[st], bytes);
+          bulk_g2s(stage + (size_t)st * kChunk, src + (long long)ch * kChunk, bytes, &full[st]);
+        }
+      }
+    }
+    return;
+  }
+  // ---- consumers
+  constexpr int CPW = 32 / NW;
+  const int n = a.n;
+  long long g = 0;
+  for (int q = 0;; ++q) {
+    const int d = q & 1;
+    mbar_wait(&dfull[d], (q >> 1) & 1);
+    const TileDesc td = desc[d];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&dempty[d]);
+    if (td.t >= a.ntiles) break;
+    for (int i = threadIdx.x; i < td.ndep; i += NT) {
+      const FusedDep dp = a.deps[td.dep0 + i];
+      const volatile int* p = a.done + dp.block;
+      while (*p < dp.count) __nanosleep(32);
+    }
+    __threadfence();
+    consumers_sync(NT);
+    const int K = td.K;
+    const double2* src;
+    if (td.phase == 0) src = td.alt ? a.r : a.zL;
+    else if (td.phase == 1) src = a.zL;
+    else src = td.alt ? a.rp : a.w;
+    src += td.in_off;
+    for (int i = threadIdx.x; i < K; i += NT) xs[i] = __ldcg(src + i);
+    consumers_sync(NT);
+    double2 a0 = make_double2(0, 0), a1 = make_double2(0, 0);
+    const int nch = (K + 31) / 32;
+    for (int ch = 0; ch < nch; ++ch, ++g) {
+      const int st = (int)(g % S);
+      mbar_wait(&full[st], (unsigned)((g / S) & 1));
+      const double2* Ts = stage + (size_t)st * kChunk;
+#pragma unroll
+      for (int u = 0; u < CPW; ++u) {
+        const int cc = warp * CPW + u, col = ch * 32 + cc;
+        if (col < K) {
+          if (col & 1) cfma(a1, Ts[cc * kRowTile + lane], xs[col]);
+          else cfma(a0, Ts[cc * kRowTile + lane], xs[col]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+    part[warp * 32 + lane] = cadd(a0, a1);
+    consumers_sync(NT);
+    if (warp == 0) {
+      double2 y = part[lane];
+#pragma unroll
+      for (int w = 1; w < NW; ++w) y = cadd(y, part[w * 32 + lane]);
+      const int row = td.row0 + lane;
+      if (row >= td.rlo && row < td.rhi) {
+        const int f = row / n, p = row - f * n;
+        const long long off = (long long)td.tgt[f] + p;
+        if (td.phase == 0) {
+          a.zL[off] = cadd(__ldcg(a.zL + off), y);
+        } else if (td.phase == 1) {
+          const double2 zl = __ldcg(a.zL + off);
+          const double2 v = csub(a.r[off], csub(zl, y));
+          a.rp[off] = v;
+          a.w[off] = v;
+          a.z[off] = cadd(zl, v);
+        } else {
+          a.w[off] = cadd(__ldcg(a.w + off), y);
+          a.z[off] = cadd(__ldcg(a.z + off), y);
+        }
+      }
+      __threadfence();
+    }
+    consumers_sync(NT);
+    if (threadIdx.x == 0) {
+      const int r0 = max(td.rlo, td.row0), r1 = min(td.rhi, td.row0 + kRowTile);
+      for (int f = r0 / n; f * n < r1; ++f) atomicAdd(a.done + td.tgt[f] / n, 1);
     }
   }
 }
@@ -305,7 +510,7 @@ void launch_step(Ctx& c, const DevStep& st, const double2* srcA, const double2* 
                  const Epi& e, int R) {
   if (st.ntiles > 0) {
     if (R == 1) {
-      constexpr int NW = 16;  // same column split as the fused kernel (bitwise identical sums)
+      constexpr int NW = kSumWarps;  // same column split as the fused kernels (bitwise identical sums)
       size_t smem = (size_t)(st.maxK + NW * 32) * sizeof(double2);
       c.launches++;
       k_step1<NW><<<st.ntiles, NW * 32, smem, c.stream>>>(st.tiles, st.items, c.dsubs, c.T, srcA,
@@ -343,23 +548,52 @@ void launch_seam_add(Ctx& c, int dir, double2* z, const double2* r, int R) {
 
 cudaError_t set_step_smem_limit() {
   cudaFuncSetAttribute(k_bsp_fused<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_bsp_fused<16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_bsp_fused<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  return cudaFuncSetAttribute(k_step1<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return cudaFuncSetAttribute(k_step1<kSumWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               200 * 1024);
 }
 
 cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double2* zL, double2* rp,
                              double2* w, double2* z) {
-  // variant: 0 = 8 warps x 1 strip, 1 = 16 warps x 1 strip, 2 = 8 warps x 2 strips
-  const int var = f.rt == 2 ? 2 : (f.nw == 16 ? 1 : 0);
-  const int NWv = var == 1 ? 16 : 8;
+  // TMA-staged (k_bsp_tma) or register streaming (k_bsp_fused: variant 0 = 1 strip
+  // per tile, 2 = 2 strips per tile)
+  if (f.tma) {
+    // 8 consumer warps, 5 x 16 KB stages: 2 CTAs per SM (measured on B200 against
+    // 16 warps, 3 or 10 stages; tools/run_bsp_variants.sh)
+    constexpr int NWt = kSumWarps, ST = 5;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_bsp_tma<NWt, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      attr = true;
+    }
+    const size_t smem = (size_t)(ST * kChunk + f.maxK + NWt * 32) * sizeof(double2);
+    static int per_sm = 0;
+    static size_t per_sm_smem = 0;
+    if (per_sm == 0 || per_sm_smem != smem) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsp_tma<NWt, ST>, (NWt + 1) * 32, smem);
+      per_sm = std::max(1, per_sm);
+      per_sm_smem = smem;
+    }
+    cudaError_t e = cudaMemsetAsync(f.counters, 0, (c.plan.npairs + 1) * sizeof(int), c.stream);
+    if (e != cudaSuccess) return e;
+    FusedArgs a;
+    a.tiles = f.tiles; a.items = f.items; a.deps = f.deps; a.subs = c.dsubs; a.T = c.T;
+    a.r = r; a.zL = zL; a.rp = rp; a.w = w; a.z = z;
+    a.done = f.counters; a.ticket = f.counters + c.plan.npairs;
+    a.ntiles = f.ntiles; a.n = c.n; a.maxK = f.maxK;
+    const int grid = std::max(1, std::min(f.ntiles, per_sm * c.num_sms));
+    c.launches++;
+    k_bsp_tma<NWt, ST><<<grid, (NWt + 1) * 32, smem, c.stream>>>(a);
+    return cudaGetLastError();
+  }
+  static_assert(kSumWarps == 8, "register-streaming fused kernels are instantiated for 8 warps");
+  const int var = f.rt == 2 ? 2 : 0;
+  const int NWv = 8;
   const size_t smem = (size_t)(f.maxK + NWv * 32 * f.rt) * sizeof(double2);
   static int per_sm[3] = {0, 0, 0};
   static size_t per_sm_smem[3] = {0, 0, 0};
   if (per_sm[var] == 0 || per_sm_smem[var] != smem) {
     if (var == 2) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[var], k_bsp_fused<8, 2>, 256, smem);
-    else if (var == 1) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[var], k_bsp_fused<16, 1>, 512, smem);
     else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[var], k_bsp_fused<8, 1>, 256, smem);
     per_sm_smem[var] = smem;
     if (per_sm[var] < 1) per_sm[var] = 1;
@@ -370,11 +604,10 @@ cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double
   a.tiles = f.tiles; a.items = f.items; a.deps = f.deps; a.subs = c.dsubs; a.T = c.T;
   a.r = r; a.zL = zL; a.rp = rp; a.w = w; a.z = z;
   a.done = f.counters; a.ticket = f.counters + c.plan.npairs;
-  a.ntiles = f.ntiles; a.n = c.n;
+  a.ntiles = f.ntiles; a.n = c.n; a.maxK = f.maxK;
   const int grid = std::max(1, std::min(f.ntiles, per_sm[var] * c.num_sms));
   c.launches++;
   if (var == 2) k_bsp_fused<8, 2><<<grid, 256, smem, c.stream>>>(a);
-  else if (var == 1) k_bsp_fused<16, 1><<<grid, 512, smem, c.stream>>>(a);
   else k_bsp_fused<8, 1><<<grid, 256, smem, c.stream>>>(a);
   return cudaGetLastError();
 }

@@ -13,6 +13,11 @@
 namespace hs {
 
 constexpr int kRowTile = 32;  // rows per tile of the tile-major map layout
+// Every 1-RHS step kernel (k_step1, k_bsp_fused, k_bsp_tma) splits a row's map
+// columns the same way -- column c into partial sum (c % 32) / (32 / kSumWarps),
+// accumulator c & 1, partials added in order -- so their results are bitwise
+// identical.
+constexpr int kSumWarps = 8;
 
 // Per-subdomain record on the device.  Maps are stored tile-major:
 // T_s[tile][col][lane] = T_s(tile*32 + lane, col), rows padded to a multiple of
@@ -117,7 +122,8 @@ struct DevFused {
   FusedDep* deps = nullptr;
   int nitems = 0, ntiles = 0, ndeps = 0, maxK = 0;
   int rt = 1;               // 32-row strips per tile
-  int nw = 8;               // warps per CTA
+  int nw = 8;               // warps per CTA (consumer warps for the TMA kernel)
+  bool tma = true;          // TMA-staged maps (k_bsp_tma), else register streaming (k_bsp_fused)
   int* counters = nullptr;  // [npairs] block completion counters + [1] ticket
   double bytes = 0;         // algorithmic bytes of one apply
   bool built = false;
