@@ -361,8 +361,10 @@ def main():
                            f"{pj['traffic_over_algorithmic']:.4f} over {len(pj['launches'])} captured launches")
         roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                 "frac": (ach / peak) if ach else None, "traffic": traffic, "traffic_source": traffic_src,
-                "kernel": "k_bsp_fused (whole BSP apply as one dataflow launch of the step-apply ZGEMV tiles, "
-                          "per-subdomain maps)" if m["kl"] <= args.steps else
+                "kernel": ("k_bsp_tma (whole BSP apply as one dataflow launch; maps staged by TMA bulk copies "
+                           "into an mbarrier ring, producer warp + 8 consumer warps)" if 4 * c["n"] <= 512 else
+                           "k_bsp_fused (whole BSP apply as one dataflow launch of the step-apply ZGEMV tiles, "
+                           "register streaming, per-subdomain maps)") if m["kl"] <= args.steps else
                           "k_step1 (batched step-apply ZGEMV, per-subdomain maps)",
                 "peak_source": peak_kind,
                 "peak_note": "measured peak = torch copy (half writes); this kernel's traffic is ~98% reads, so "
