@@ -386,22 +386,25 @@ int make_step(Ctx* c, const StepTable& t, DevStep& out) {
 }
 
 void free_fused(Ctx* c) {
-  DevFused& f = c->fused;
-  dfree(c, f.items, f.nitems * sizeof(DevItem));
-  dfree(c, f.tiles, f.ntiles * sizeof(FusedTile));
-  dfree(c, f.deps, f.ndeps * sizeof(FusedDep));
-  dfree(c, f.counters, (c->plan.npairs + 1) * sizeof(int));
-  f = DevFused();
+  for (DevFused* fp : {&c->fused, &c->fused_ims}) {
+    DevFused& f = *fp;
+    dfree(c, f.items, f.nitems * sizeof(DevItem));
+    dfree(c, f.tiles, f.ntiles * sizeof(FusedTile));
+    dfree(c, f.deps, f.ndeps * sizeof(FusedDep));
+    dfree(c, f.counters, (c->plan.npairs + 1) * sizeof(int));
+    f = DevFused();
+  }
 }
 
 // Dataflow plan of one BSP apply: every tile of the forward steps, the
 // residual step and the backward steps in schedule order, each with the
 // per-block completion counts it waits for (all earlier tile-writes to the
 // blocks it reads or read-modify-writes; counts taken before its own step,
-// since the tiles of one step are independent).
-int build_fused(Ctx* c) {
-  free_fused(c);
-  DevFused& f = c->fused;
+// since the tiles of one step are independent).  ims: append the (I - S) z
+// step as phase 3 (GMRES's A M v in one launch): its tiles wait for the final
+// z of the blocks they read and of their output rows, and signal nothing.
+int build_fused(Ctx* c, bool ims) {
+  DevFused& f = ims ? c->fused_ims : c->fused;
   const Plan& P = c->plan;
   const int n = c->n;
   std::vector<DevItem> items;
@@ -438,7 +441,7 @@ int build_fused(Ctx* c) {
         const int r0 = std::max(it.rlo, tl * TR), r1 = std::min(it.rhi, (tl + 1) * TR);
         for (int q = r0 / n; q * n < r1; ++q) {
           blocks.insert(sp.tgt_block[q]);
-          inc.push_back(sp.tgt_block[q]);
+          if (phase != 3) inc.push_back(sp.tgt_block[q]);
         }
         for (int b : blocks)
           if (written[b] > 0) {
@@ -454,6 +457,7 @@ int build_fused(Ctx* c) {
   for (auto& st : c->fwd) add(st, 0);
   add(c->full, 1);
   for (auto& st : c->bwd) add(st, 2);
+  if (ims) add(c->full, 3);
   f.tma = f.tma && f.maxK <= 512;
   if (const char* e = getenv("HS_FUSED_TMA")) f.tma = atoi(e) != 0 && f.rt == 1;
   if (upload(c, &f.items, items) || upload(c, &f.tiles, tiles) || upload(c, &f.deps, deps)) return -1;
@@ -654,6 +658,23 @@ int do_half(Ctx* c, int dir, const double2* r, double2* z, int R) {
   return 0;
 }
 
+bool fused_bsp_ok(const Ctx* c, int R) {
+  return (c->fused_mode & 1) && R == 1 && c->map_mode == 0 && c->plan.nranks == 1 && c->inter &&
+         c->seam == HS_SEAM_DEDUP && c->full.nitems > 0;
+}
+
+// GMRES's w = (I - S) M r with M = BSP as ONE dataflow launch (z = M r is
+// left in z).  Bitwise identical to do_precond + do_apply(HS_APPLY_IMS).
+int do_precond_ims(Ctx* c, const double2* r, double2* z, double2* wout) {
+  const long long L = c->plan.L;
+  double2 *zl, *rp, *w;
+  if (ws_get(c, "zL", L, &zl) || ws_get(c, "rp", L, &rp) || ws_get(c, "w", L, &w)) return -1;
+  if (!c->fused_ims.built && build_fused(c, true)) return -1;
+  CK(cudaMemcpyAsync(zl, r, L * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
+  CK(launch_bsp_fused(*c, c->fused_ims, r, zl, rp, w, z, wout));
+  return 0;
+}
+
 int do_precond(Ctx* c, int kind, const double2* r, double2* z, int R) {
   const long long LR = LRof(c, R);
   if (kind == HS_PC_NONE) {
@@ -674,10 +695,9 @@ int do_precond(Ctx* c, int kind, const double2* r, double2* z, int R) {
   if (kind != HS_PC_BSP) return fail(c, 1, "unknown preconditioner kind");
   double2 *zl, *rp, *w;
   if (ws_get(c, "zL", LR, &zl) || ws_get(c, "rp", LR, &rp) || ws_get(c, "w", LR, &w)) return -1;
-  if ((c->fused_mode & 1) && R == 1 && c->map_mode == 0 && c->plan.nranks == 1 && c->inter &&
-      c->seam == HS_SEAM_DEDUP && c->full.nitems > 0) {
+  if (fused_bsp_ok(c, R)) {
     // the whole apply as one dataflow launch (bitwise identical to the step sequence)
-    if (!c->fused.built && build_fused(c)) return -1;
+    if (!c->fused.built && build_fused(c, false)) return -1;
     CK(cudaMemcpyAsync(zl, r, LR * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->timing) {
@@ -1361,12 +1381,16 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
   for (int k = 0; k < maxit && !stop; ++k) {
     double2* vk = V + (long long)k * LR;
     double2* w = V + (long long)(k + 1) * LR;
-    const double2* zin = vk;
-    if (pc != HS_PC_NONE) {
-      if (do_precond(c, pc, vk, Z, R)) return -1;
-      zin = Z;
+    if (pc == HS_PC_BSP && fused_bsp_ok(c, R) && !c->timing) {
+      if (do_precond_ims(c, vk, Z, w)) return -1;  // A M v_k in one launch
+    } else {
+      const double2* zin = vk;
+      if (pc != HS_PC_NONE) {
+        if (do_precond(c, pc, vk, Z, R)) return -1;
+        zin = Z;
+      }
+      if (do_apply(c, HS_APPLY_IMS, zin, w, R)) return -1;
     }
-    if (do_apply(c, HS_APPLY_IMS, zin, w, R)) return -1;
     if (cgs2) {
       CK(gmres_arnoldi_cgs2(*c, G, k, c->d_owned, c->n_owned, part3, hbuf, c->nccl));
       CK(gmres_givens(*c, G, k));

@@ -115,6 +115,7 @@ struct FusedArgs {
   double2* rp;
   double2* w;
   double2* z;
+  double2* wout;  // phase 3 output (I - S) z (GMRES: the next basis vector), else null
   int* done;
   int* ticket;
   int ntiles, n, maxK;
@@ -147,7 +148,8 @@ __global__ void __launch_bounds__(NW * 32) k_bsp_fused(FusedArgs a) {
     const double2* src;
     if (ft.phase == 0) src = it.alt ? a.r : a.zL;
     else if (ft.phase == 1) src = a.zL;
-    else src = it.alt ? a.rp : a.w;
+    else if (ft.phase == 2) src = it.alt ? a.rp : a.w;
+    else src = a.z;  // phase 3: (I - S) z
     src += sb.in_off;
     double2* xs = sm;
     double2* part = sm + K;
@@ -214,15 +216,17 @@ __global__ void __launch_bounds__(NW * 32) k_bsp_fused(FusedArgs a) {
           a.rp[off] = v;
           a.w[off] = v;
           a.z[off] = cadd(zl, v);
-        } else {
+        } else if (ft.phase == 2) {
           a.w[off] = cadd(__ldcg(a.w + off), y);
           a.z[off] = cadd(__ldcg(a.z + off), y);
+        } else {
+          a.wout[off] = csub(__ldcg(a.z + off), y);  // EPI_IMS on the final z
         }
       }
       __threadfence();
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && ft.phase != 3) {
       // one completion per (tile, written block); all strips' stores are fenced above
       const int r0 = max(it.rlo, s0 * kRowTile), r1 = min(it.rhi, (s0 + RT) * kRowTile);
       for (int f = r0 / n; f * n < r1; ++f) atomicAdd(a.done + sb.tgt[f] / n, 1);
@@ -352,7 +356,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_bsp_tma(FusedArgs a) {
     const double2* src;
     if (td.phase == 0) src = td.alt ? a.r : a.zL;
     else if (td.phase == 1) src = a.zL;
-    else src = td.alt ? a.rp : a.w;
+    else if (td.phase == 2) src = td.alt ? a.rp : a.w;
+    else src = a.z;  // phase 3: (I - S) z
     src += td.in_off;
     for (int i = threadIdx.x; i < K; i += NT) xs[i] = __ldcg(src + i);
     consumers_sync(NT);
@@ -391,15 +396,17 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_bsp_tma(FusedArgs a) {
           a.rp[off] = v;
           a.w[off] = v;
           a.z[off] = cadd(zl, v);
-        } else {
+        } else if (td.phase == 2) {
           a.w[off] = cadd(__ldcg(a.w + off), y);
           a.z[off] = cadd(__ldcg(a.z + off), y);
+        } else {
+          a.wout[off] = csub(__ldcg(a.z + off), y);  // EPI_IMS on the final z
         }
       }
       __threadfence();
     }
     consumers_sync(NT);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && td.phase != 3) {  // nothing waits on the (I - S) z tiles
       const int r0 = max(td.rlo, td.row0), r1 = min(td.rhi, td.row0 + kRowTile);
       for (int f = r0 / n; f * n < r1; ++f) atomicAdd(a.done + td.tgt[f] / n, 1);
     }
@@ -554,7 +561,7 @@ cudaError_t set_step_smem_limit() {
 }
 
 cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double2* zL, double2* rp,
-                             double2* w, double2* z) {
+                             double2* w, double2* z, double2* wout) {
   // TMA-staged (k_bsp_tma) or register streaming (k_bsp_fused: variant 0 = 1 strip
   // per tile, 2 = 2 strips per tile)
   if (f.tma) {
@@ -578,7 +585,7 @@ cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double
     if (e != cudaSuccess) return e;
     FusedArgs a;
     a.tiles = f.tiles; a.items = f.items; a.deps = f.deps; a.subs = c.dsubs; a.T = c.T;
-    a.r = r; a.zL = zL; a.rp = rp; a.w = w; a.z = z;
+    a.r = r; a.zL = zL; a.rp = rp; a.w = w; a.z = z; a.wout = wout;
     a.done = f.counters; a.ticket = f.counters + c.plan.npairs;
     a.ntiles = f.ntiles; a.n = c.n; a.maxK = f.maxK;
     const int grid = std::max(1, std::min(f.ntiles, per_sm * c.num_sms));
@@ -602,7 +609,7 @@ cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double
   if (e != cudaSuccess) return e;
   FusedArgs a;
   a.tiles = f.tiles; a.items = f.items; a.deps = f.deps; a.subs = c.dsubs; a.T = c.T;
-  a.r = r; a.zL = zL; a.rp = rp; a.w = w; a.z = z;
+  a.r = r; a.zL = zL; a.rp = rp; a.w = w; a.z = z; a.wout = wout;
   a.done = f.counters; a.ticket = f.counters + c.plan.npairs;
   a.ntiles = f.ntiles; a.n = c.n; a.maxK = f.maxK;
   const int grid = std::max(1, std::min(f.ntiles, per_sm[var] * c.num_sms));

@@ -108,7 +108,7 @@ struct DevStep {
 struct FusedTile {
   int item;        // index into the fused item list
   int tile;        // tile index in units of rt strips
-  int phase;       // 0 forward (EPI_ACC on zL), 1 residual (EPI_RESID), 2 backward (EPI_ACC2)
+  int phase;       // 0 forward (EPI_ACC on zL), 1 residual (EPI_RESID), 2 backward (EPI_ACC2), 3 (I - S) z
   int dep0, ndep;  // dependencies [dep0, dep0 + ndep) in the dep pool
 };
 
@@ -206,6 +206,7 @@ struct Ctx {
   std::vector<DevStep> fwd, bwd, sp_fwd, sp_bwd;
   DevStep full;
   DevFused fused;        // BSP apply as one dataflow launch (1 RHS, per-subdomain maps, 1 rank)
+  DevFused fused_ims;    // the same followed by (I - S) z: GMRES's A M v in one launch
   DevFusedMma fused_mma; // the same on the DMMA contraction (R RHS or shared maps)
   int fused_mode = 1;    // 1: use the fused kernel when applicable, 0: one launch per step
   std::vector<std::vector<int>> seam_blocks;  // [dir] blocks of seam groups (literal mode)

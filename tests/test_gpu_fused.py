@@ -45,6 +45,22 @@ def test_fused_gmres_cfg2_golden():
     assert relerr(res.solution, G["gm_x"]) < 1e-8
 
 
+@pytest.mark.parametrize("name,c,blocks", [("small_3x3", small_case(3, 3, 8), 2), ("small_6x3", small_case(6, 3, 16), 5),
+                                           ("cfg1", CONFIGS[1], None), ("cfg2", CONFIGS[2], 4), ("cfg3", CONFIGS[3], 4)])
+def test_fused_gmres_bitwise_equals_steps(name, c, blocks):
+    """GMRES with A M v as ONE launch (BSP + (I - S) z, phase 3 of the fused
+    plan) runs bitwise the same iterations as the per-step kernels."""
+    spec, part = product_problem(c)
+    a = GpuInterfaceSystem(spec, part, fused=False, sweep=SweepConfig(blocks=blocks))
+    b = GpuInterfaceSystem(spec, part, fused=True, sweep=SweepConfig(blocks=blocks))
+    rhs = a.rhs() if c.get("center") is not None else cvec(5, a.layout.size)
+    ra = a.gmres(rhs, "bsp", tol=1e-8, maxit=300)
+    rb = b.gmres(rhs, "bsp", tol=1e-8, maxit=300)
+    assert ra.iterations == rb.iterations and ra.converged and rb.converged
+    assert np.array_equal(ra.solution, rb.solution), relerr(rb.solution, ra.solution)
+    assert np.array_equal(np.asarray(ra.history), np.asarray(rb.history))
+
+
 @pytest.mark.parametrize("name,c,R,maps", [("cfg1", CONFIGS[1], 40, "subdomain"), ("cfg2", CONFIGS[2], 64, "subdomain"),
                                            ("cfg1", CONFIGS[1], 1, "shared"), ("cfg2", CONFIGS[2], 1, "shared"),
                                            ("cfg3", CONFIGS[3], 1, "shared"), ("cfg2", CONFIGS[2], 8, "shared")])
