@@ -115,11 +115,14 @@ class Context:
         lib.hs_sizes(self.h_, C.byref(L), C.byref(nsub), C.byref(ng), C.byref(npairs))
         self.L, self.nsub, self.ngroups, self.npairs = L.value, nsub.value, ng.value, npairs.value
 
-    def __del__(self, _lib=lib):  # bound at definition: module globals may be gone at exit
+    def __del__(self, _destroy=lib.hs_destroy):  # bound at definition: module globals may be gone at exit
         h = getattr(self, "h_", None)
         if h is not None and h.value:
-            _lib.hs_destroy(h)
-            self.h_ = _P()
+            self.h_ = None
+            try:
+                _destroy(h)
+            except (TypeError, AttributeError):  # interpreter teardown: the process is exiting anyway
+                pass
 
     def close(self):
         self.__del__()
