@@ -410,7 +410,7 @@ int build_fused(Ctx* c, bool ims) {
   std::vector<DevItem> items;
   std::vector<FusedTile> tiles;
   std::vector<FusedDep> deps;
-  std::vector<int> written(P.npairs, 0);
+  std::vector<int> written(P.npairs, 0), zl_written(P.npairs, 0);
   // tile shape: one 32-row strip, kSumWarps warps splitting its columns
   // (2 strips per tile -- 80 registers, half the occupancy -- was slower at
   // cfg3; HS_FUSED_RT=2 selects it).
@@ -436,6 +436,14 @@ int build_fused(Ctx* c, bool ims) {
         FusedTile ft;
         ft.item = idx; ft.tile = tl; ft.phase = phase;
         ft.dep0 = (int)deps.size(); ft.ndep = 0;
+        ft.rmask = 0;
+        if (phase <= 1) {  // zL is never initialised: blocks without a forward write read r
+          if (phase == 1 || !it.alt)
+            for (int q = 0; q < sp.k; ++q)
+              if (zl_written[sp.first_block + q] == 0) ft.rmask |= 1 << q;
+          for (int q = 0; q < sp.k; ++q)
+            if (zl_written[sp.tgt_block[q]] == 0) ft.rmask |= 1 << (4 + q);
+        }
         std::set<int> blocks;
         for (int q = 0; q < sp.k; ++q) blocks.insert(sp.first_block + q);
         const int r0 = std::max(it.rlo, tl * TR), r1 = std::min(it.rhi, (tl + 1) * TR);
@@ -451,7 +459,10 @@ int build_fused(Ctx* c, bool ims) {
         tiles.push_back(ft);
       }
     }
-    for (int b : inc) written[b]++;
+    for (int b : inc) {
+      written[b]++;
+      if (phase == 0) zl_written[b]++;
+    }
     f.bytes += st.bytes_per_rhs_map + st.bytes_per_rhs_vec;
   };
   for (auto& st : c->fwd) add(st, 0);
@@ -670,7 +681,6 @@ int do_precond_ims(Ctx* c, const double2* r, double2* z, double2* wout) {
   double2 *zl, *rp, *w;
   if (ws_get(c, "zL", L, &zl) || ws_get(c, "rp", L, &rp) || ws_get(c, "w", L, &w)) return -1;
   if (!c->fused_ims.built && build_fused(c, true)) return -1;
-  CK(cudaMemcpyAsync(zl, r, L * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
   CK(launch_bsp_fused(*c, c->fused_ims, r, zl, rp, w, z, wout));
   return 0;
 }
@@ -698,7 +708,7 @@ int do_precond(Ctx* c, int kind, const double2* r, double2* z, int R) {
   if (fused_bsp_ok(c, R)) {
     // the whole apply as one dataflow launch (bitwise identical to the step sequence)
     if (!c->fused.built && build_fused(c, false)) return -1;
-    CK(cudaMemcpyAsync(zl, r, LR * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
+    // no zL = r copy: the plan's rmask makes tiles read r for blocks zL has not received yet
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->timing) {
       e0 = ev_get(c);

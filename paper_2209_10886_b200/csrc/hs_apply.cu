@@ -153,7 +153,9 @@ __global__ void __launch_bounds__(NW * 32) k_bsp_fused(FusedArgs a) {
     src += sb.in_off;
     double2* xs = sm;
     double2* part = sm + K;
-    for (int i = threadIdx.x; i < K; i += NW * 32) xs[i] = __ldcg(src + i);
+    // zL starts as r without a copy: faces of zL not yet written read r
+    for (int i = threadIdx.x; i < K; i += NW * 32)
+      xs[i] = __ldcg(((ft.rmask >> (i / n)) & 1 ? a.r + sb.in_off : src) + i);
     __syncthreads();
     // strips beyond the map (RT > 1 at the last rows) are skipped
     const int nstrip = (K + kRowTile - 1) / kRowTile;
@@ -208,10 +210,11 @@ __global__ void __launch_bounds__(NW * 32) k_bsp_fused(FusedArgs a) {
       if (row >= it.rlo && row < it.rhi) {
         const int f = row / n, p = row - f * n;
         const long long off = (long long)sb.tgt[f] + p;
+        const double2* zbase = (ft.rmask >> (4 + f)) & 1 ? a.r : a.zL;  // zL not yet written: r
         if (ft.phase == 0) {
-          a.zL[off] = cadd(__ldcg(a.zL + off), y);
+          a.zL[off] = cadd(__ldcg(zbase + off), y);
         } else if (ft.phase == 1) {
-          const double2 zl = __ldcg(a.zL + off);
+          const double2 zl = __ldcg(zbase + off);
           const double2 v = csub(a.r[off], csub(zl, y));
           a.rp[off] = v;
           a.w[off] = v;
@@ -249,7 +252,7 @@ __global__ void __launch_bounds__(NW * 32) k_bsp_fused(FusedArgs a) {
 // Same arithmetic order as k_step1 (bitwise identical).
 struct TileDesc {
   long long map_off;  // element offset of the tile's 32-row strip
-  int t, K, phase, alt, in_off, rlo, rhi, row0, dep0, ndep;
+  int t, K, phase, alt, in_off, rlo, rhi, row0, dep0, ndep, rmask;
   int tgt[4];
 };
 
@@ -315,7 +318,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_bsp_tma(FusedArgs a) {
           td.row0 = ft.tile * kRowTile;
           td.map_off = sb.T_off + (long long)ft.tile * td.K * kRowTile;
           td.phase = ft.phase; td.alt = it.alt; td.in_off = sb.in_off;
-          td.rlo = it.rlo; td.rhi = it.rhi; td.dep0 = ft.dep0; td.ndep = ft.ndep;
+          td.rlo = it.rlo; td.rhi = it.rhi; td.dep0 = ft.dep0; td.ndep = ft.ndep; td.rmask = ft.rmask;
           for (int f = 0; f < 4; ++f) td.tgt[f] = sb.tgt[f];
         }
         desc[d] = td;
@@ -359,7 +362,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_bsp_tma(FusedArgs a) {
     else if (td.phase == 2) src = td.alt ? a.rp : a.w;
     else src = a.z;  // phase 3: (I - S) z
     src += td.in_off;
-    for (int i = threadIdx.x; i < K; i += NT) xs[i] = __ldcg(src + i);
+    // zL starts as r without a copy: faces of zL not yet written read r
+    for (int i = threadIdx.x; i < K; i += NT) xs[i] = __ldcg(((td.rmask >> (i / n)) & 1 ? a.r + td.in_off : src) + i);
     consumers_sync(NT);
     double2 a0 = make_double2(0, 0), a1 = make_double2(0, 0);
     const int nch = (K + 31) / 32;
@@ -388,10 +392,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_bsp_tma(FusedArgs a) {
       if (row >= td.rlo && row < td.rhi) {
         const int f = row / n, p = row - f * n;
         const long long off = (long long)td.tgt[f] + p;
+        const double2* zbase = (td.rmask >> (4 + f)) & 1 ? a.r : a.zL;  // zL not yet written: r
         if (td.phase == 0) {
-          a.zL[off] = cadd(__ldcg(a.zL + off), y);
+          a.zL[off] = cadd(__ldcg(zbase + off), y);
         } else if (td.phase == 1) {
-          const double2 zl = __ldcg(a.zL + off);
+          const double2 zl = __ldcg(zbase + off);
           const double2 v = csub(a.r[off], csub(zl, y));
           a.rp[off] = v;
           a.w[off] = v;

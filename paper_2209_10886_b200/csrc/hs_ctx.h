@@ -110,6 +110,7 @@ struct FusedTile {
   int tile;        // tile index in units of rt strips
   int phase;       // 0 forward (EPI_ACC on zL), 1 residual (EPI_RESID), 2 backward (EPI_ACC2), 3 (I - S) z
   int dep0, ndep;  // dependencies [dep0, dep0 + ndep) in the dep pool
+  int rmask;       // bit q: slab face q of zL not yet written (read r); bit 4 + f: output face f likewise
 };
 
 struct FusedDep {

@@ -73,3 +73,19 @@ def test_fused_dmma_equals_steps(name, c, R, maps):
     zb = b.bsp_apply(g)
     assert relerr(zb, za) < 1e-13, relerr(zb, za)
     assert np.array_equal(b.bsp_apply(g), zb)  # the fused launch itself is deterministic
+
+
+@pytest.mark.parametrize("name,c,blocks", [("small_6x3", small_case(6, 3, 16), 5), ("cfg2", CONFIGS[2], 4),
+                                           ("cfg3", CONFIGS[3], 4)])
+def test_host_buffer_apply_bitwise(name, c, blocks):
+    """hs_precond on HOST buffers (pageable numpy, pinned torch) returns
+    bitwise the device-buffer result, call after call."""
+    spec, part = product_problem(c)
+    s = GpuInterfaceSystem(spec, part, sweep=SweepConfig(blocks=blocks))
+    g = cvec(23, s.layout.size)
+    zd = s.bsp_apply(torch.from_numpy(g).cuda()).cpu().numpy()
+    zh = s.bsp_apply(g)
+    assert np.array_equal(zd, zh), relerr(zh, zd)
+    gp = torch.from_numpy(g).pin_memory()
+    for _ in range(3):
+        assert np.array_equal(s.bsp_apply(gp).numpy(), zd)
