@@ -342,6 +342,8 @@ int build_fused_mma(Ctx* c, int R, bool shared) {
   f.nincs = (int)incs.size();
   f.ncounters = ncnt;
   f.flops = flops;
+  f.minK = 1 << 30;
+  for (const auto& ft : ftasks) f.minK = std::min(f.minK, ft.task.K);
   f.R = R;
   f.shared = shared;
   f.built = true;

@@ -146,6 +146,7 @@ struct DevFusedMma {
   int ntasks = 0, ncols = 0, ndeps = 0, nincs = 0;
   int ncounters = 0;        // npairs * ceil(R / 32)
   int* counters = nullptr;  // + 1 ticket
+  int minK = 0;             // smallest task K (split-K decision)
   double flops = 0;
   int R = 0;
   bool shared = false, built = false;

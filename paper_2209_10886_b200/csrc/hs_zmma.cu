@@ -356,6 +356,119 @@ __global__ void __launch_bounds__(THREADS) k_zmma_fused(FusedMmaArgs a) {
   }
 }
 
+// The fused apply with every task's K range split over a thread-block cluster
+// of KS CTAs: rank 0 claims the ticket and hands it to the cluster through
+// distributed shared memory, every rank waits for the task's dependencies and
+// contracts its share of the K chunks, ranks > 0 publish their partial tile
+// and rank 0 sums them in rank order (deterministic), runs the epilogue and
+// signals completion.  A subdomain step is then spread over KS x more SMs, so
+// the sweep's dependency chain (17 steps at cfg4) is paced by KS x shorter
+// tasks -- the per-step launches could split K the same way but pay a launch
+// and a ramp per step, and the unsplit fused kernel runs each task's whole K
+// on one SM.
+template <int KS>
+__global__ void __launch_bounds__(THREADS) k_zmma_fused_ks(FusedMmaArgs a) {
+  extern __shared__ __align__(16) double2 dyn[];
+  __shared__ ZCols zc;
+  __shared__ int s_t;
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank();
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wk = warp >> 2, wq = warp & 3;
+  const int wm = wq >> 1, wn = wq & 1;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int n = a.n, R = a.R;
+  for (;;) {
+    if (rank == 0 && tid == 0) {
+      // push the ticket into every rank's own shared memory before the barrier:
+      // no rank reads a peer's shared memory after it (a peer may have exited)
+      const int tt = atomicAdd(a.ticket, 1);
+      for (int q = 0; q < KS; ++q) *cl.map_shared_rank(&s_t, q) = tt;
+    }
+    cl.sync();
+    const int t = s_t;
+    if (t >= a.ntasks) return;  // the whole cluster leaves together
+    const FusedMmaTask ft = a.tasks[t];
+    const MmaTask tk = ft.task;
+    for (int d = tid; d < ft.ndep; d += blockDim.x) {
+      const FusedDep dp = a.deps[ft.dep0 + d];
+      const volatile int* p = a.done + dp.block;
+      while (*p < dp.count) __nanosleep(32);
+    }
+    __threadfence();
+    zmma_cols(tk, a.cols, zc);
+    __syncthreads();
+    const double2* srcA = ft.phase == 0 ? a.zL : (ft.phase == 1 ? a.zL : a.w);
+    const double2* srcB = ft.phase == 0 ? a.r : (ft.phase == 1 ? a.zL : a.rp);
+    const int nk_all = tk.K / KC;
+    const int kc0 = nk_all * rank / KS, kc1 = nk_all * (rank + 1) / KS;
+    double cre[2][2][2], cim[2][2][2];
+    zmma_main(tk, zc, dyn, a.A, srcA, srcB, n, R, kc0, kc1 - kc0, cre, cim);
+    double2* red = dyn;
+    __syncthreads();
+    if (wk == 0 && rank > 0) {
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            red[(wq * 8 + (mt * 4 + nt * 2 + h)) * 32 + lane] = make_double2(cre[mt][nt][h], cim[mt][nt][h]);
+    }
+    cl.sync();
+    if (rank == 0 && wk == 0) {
+      for (int src = 1; src < KS; ++src) {
+        const double2* rem = cl.map_shared_rank(red, src);
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const double2 o = rem[(wq * 8 + (mt * 4 + nt * 2 + h)) * 32 + lane];
+              cre[mt][nt][h] += o.x;
+              cim[mt][nt][h] += o.y;
+            }
+      }
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt) {
+        const int row = tk.r0 + wm * 16 + mt * 8 + gid;
+        if (row < tk.rlo || row >= tk.rhi) continue;
+        const int q = row / n, p = row - q * n;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int j = wn * 16 + nt * 8 + 2 * tig + h;
+            if (j >= tk.ncols) continue;
+            const long long o0 = zc.out[j][q];
+            if (o0 < 0) continue;
+            const long long off = o0 + (long long)p * R;
+            const double2 y = make_double2(cre[mt][nt][h], cim[mt][nt][h]);
+            if (ft.phase == 0) {
+              a.zL[off] = cadd(__ldcg(a.zL + off), y);
+            } else if (ft.phase == 1) {
+              const double2 zl = __ldcg(a.zL + off);
+              const double2 v = csub(a.r[off], csub(zl, y));
+              a.rp[off] = v;
+              a.w[off] = v;
+              a.z[off] = cadd(zl, v);
+            } else {
+              a.w[off] = cadd(__ldcg(a.w + off), y);
+              a.z[off] = cadd(__ldcg(a.z + off), y);
+            }
+          }
+      }
+      __threadfence();
+    }
+    cl.sync();  // remote partials read; s_t free for the next ticket
+    if (rank == 0) {
+      for (int i = tid; i < ft.ninc; i += blockDim.x) atomicAdd(a.done + a.incs[ft.inc0 + i], 1);
+    }
+  }
+}
+
 constexpr size_t kZmmaSmem = sizeof(double2) * STAGES * kStageElems;
 
 void launch_zmma(Ctx& c, const DevMma& m, const double2* A, const double2* srcA, const double2* srcB,
@@ -385,24 +498,55 @@ void launch_zmma(Ctx& c, const DevMma& m, const double2* A, const double2* srcA,
 }
 
 cudaError_t launch_zmma_fused(Ctx& c, const DevFusedMma& f, FusedMmaArgs a) {
-  static int per_sm = 0;
-  if (per_sm == 0) {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_zmma_fused, THREADS, kZmmaSmem);
-    if (per_sm < 1) per_sm = 1;
-  }
   cudaError_t e = cudaMemsetAsync(f.counters, 0, (f.ncounters + 1) * sizeof(int), c.stream);
   if (e != cudaSuccess) return e;
   a.tasks = f.tasks; a.cols = f.cols; a.deps = f.deps; a.incs = f.incs;
   a.done = f.counters; a.ticket = f.counters + f.ncounters;
   a.ntasks = f.ntasks; a.n = c.n;
-  const int grid = std::max(1, std::min(f.ntasks, per_sm * c.num_sms));
+  // K split over a cluster: KS ranks each keep >= 2 K chunks (HS_ZMMA_FUSED_KS overrides)
+  static const int ks_env = getenv("HS_ZMMA_FUSED_KS") ? atoi(getenv("HS_ZMMA_FUSED_KS")) : 0;
+  int KS = ks_env > 0 ? ks_env : 1;
+  if (ks_env <= 0)
+    while (KS < 4 && f.minK / KC >= 4 * KS) KS *= 2;
+  KS = KS >= 4 ? 4 : (KS >= 2 ? 2 : 1);
   c.launches++;
-  k_zmma_fused<<<grid, THREADS, kZmmaSmem, c.stream>>>(a);
-  return cudaGetLastError();
+  if (KS == 1) {
+    static int per_sm = 0;
+    if (per_sm == 0) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_zmma_fused, THREADS, kZmmaSmem);
+      if (per_sm < 1) per_sm = 1;
+    }
+    const int grid = std::max(1, std::min(f.ntasks, per_sm * c.num_sms));
+    k_zmma_fused<<<grid, THREADS, kZmmaSmem, c.stream>>>(a);
+    return cudaGetLastError();
+  }
+  const void* fn = KS == 2 ? (const void*)k_zmma_fused_ks<2> : (const void*)k_zmma_fused_ks<4>;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = kZmmaSmem;
+  cfg.stream = c.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = KS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  static int max_clusters[5] = {0, 0, 0, 0, 0};
+  if (max_clusters[KS] == 0) {
+    cfg.gridDim = dim3(KS * c.num_sms);
+    cudaOccupancyMaxActiveClusters(&max_clusters[KS], fn, &cfg);
+    if (max_clusters[KS] < 1) max_clusters[KS] = 1;
+  }
+  cfg.gridDim = dim3(KS * std::max(1, std::min(f.ntasks, max_clusters[KS])));
+  void* args[] = {(void*)&a};
+  return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
 cudaError_t set_zmma_smem_limit() {
   cudaFuncSetAttribute(k_zmma_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kZmmaSmem);
+  cudaFuncSetAttribute(k_zmma_fused_ks<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kZmmaSmem);
+  cudaFuncSetAttribute(k_zmma_fused_ks<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kZmmaSmem);
   return cudaFuncSetAttribute(k_zmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kZmmaSmem);
 }
 
