@@ -14,8 +14,8 @@
 // face from the vector (column descriptor: per-face element offset or -1,
 // stride R between consecutive face positions).  K is staged in chunks of 32
 // through a 3-stage cp.async pipeline.  8 warps: 4 output quadrants (16 x 16 =
-// 2 x 2 DMMA tiles, real and imaginary accumulators; a complex MAC is 4 real
-// DMMAs) x 2 halves of every K chunk, reduced through shared memory.
+// 2 x 2 DMMA tiles; a complex MAC is 3 real DMMAs by the 3M (Gauss) product)
+// x 2 halves of every K chunk, reduced through shared memory.
 //
 // Two launch forms share that main loop:
 //   * k_zmma: one launch per sweep step; when a step has few tasks the K range
@@ -123,12 +123,15 @@ __device__ __forceinline__ void zmma_main(const MmaTask& tk, const ZCols& zc, do
   const int wk = warp >> 2, wq = warp & 3;
   const int wm = wq >> 1, wn = wq & 1;
   const int gid = lane >> 2, tig = lane & 3;
+  // 3M (Gauss) complex product: s1 = sum ar br, s2 = sum ai bi, p3 = sum (ar + ai)(br + bi);
+  // re = s1 - s2, im = p3 - s1 - s2: 3 DMMAs per complex MAC instead of 4
+  double p3[2][2][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
     for (int b = 0; b < 2; ++b)
 #pragma unroll
-      for (int c = 0; c < 2; ++c) cre[a][b][c] = cim[a][b][c] = 0.0;
+      for (int c = 0; c < 2; ++c) cre[a][b][c] = cim[a][b][c] = p3[a][b][c] = 0.0;
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < nk) load(s, kc0 + s);
@@ -155,19 +158,18 @@ __device__ __forceinline__ void zmma_main(const MmaTask& tk, const ZCols& zc, do
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) bn[nt] = Bs(st, kb + k4 + 4 + tig, wn * 16 + nt * 8 + gid);
       }
+      double sb[2];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) sb[nt] = b[nt].x + b[nt].y;
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
-        const double nai = -a[mt].y;
+        const double sa = a[mt].x + a[mt].y;
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-          dmma(cre[mt][nt][0], cre[mt][nt][1], a[mt].x, b[nt].x);
-          dmma(cim[mt][nt][0], cim[mt][nt][1], a[mt].x, b[nt].y);
-        }
+        for (int nt = 0; nt < 2; ++nt) dmma(cre[mt][nt][0], cre[mt][nt][1], a[mt].x, b[nt].x);  // s1
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-          dmma(cre[mt][nt][0], cre[mt][nt][1], nai, b[nt].y);
-          dmma(cim[mt][nt][0], cim[mt][nt][1], a[mt].y, b[nt].x);
-        }
+        for (int nt = 0; nt < 2; ++nt) dmma(cim[mt][nt][0], cim[mt][nt][1], a[mt].y, b[nt].y);  // s2
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) dmma(p3[mt][nt][0], p3[mt][nt][1], sa, sb[nt]);
       }
       if (k4 + 4 < KC / 2) {
 #pragma unroll
@@ -178,6 +180,16 @@ __device__ __forceinline__ void zmma_main(const MmaTask& tk, const ZCols& zc, do
     }
   }
   cp_wait<0>();
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const double s1 = cre[a][b][c], s2 = cim[a][b][c];
+        cre[a][b][c] = s1 - s2;
+        cim[a][b][c] = p3[a][b][c] - s1 - s2;
+      }
   __syncthreads();
   // reduce the two K halves: the wk = 1 warps hand their tiles to wk = 0
   double2* red = dyn;
