@@ -226,11 +226,13 @@ __global__ void __launch_bounds__(NW * 32) k_bsp_fused(FusedArgs a) {
           a.wout[off] = csub(__ldcg(a.z + off), y);  // EPI_IMS on the final z
         }
       }
-      __threadfence();
     }
     __syncthreads();
     if (threadIdx.x == 0 && ft.phase != 3) {
-      // one completion per (tile, written block); all strips' stores are fenced above
+      // one completion per (tile, written block).  One gpu-scope fence by the
+      // signalling thread publishes the epilogue stores the barrier ordered
+      // before it (cumulativity), instead of a fence per storing lane.
+      __threadfence();
       const int r0 = max(it.rlo, s0 * kRowTile), r1 = min(it.rhi, (s0 + RT) * kRowTile);
       for (int f = r0 / n; f * n < r1; ++f) atomicAdd(a.done + sb.tgt[f] / n, 1);
     }
@@ -355,6 +357,20 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_bsp_tma(FusedArgs a) {
     }
     __threadfence();
     consumers_sync(NT);
+    // warp 0 (lane = output row) fetches its epilogue operands now, in the
+    // shadow of the slab load and the contraction, not after them
+    const int erow = td.row0 + lane;
+    const bool erow_ok = warp == 0 && erow >= td.rlo && erow < td.rhi;
+    const int ef = erow / n;
+    const long long eoff = erow_ok ? (long long)td.tgt[ef] + (erow - ef * n) : 0;
+    double2 e1 = make_double2(0, 0), e2 = make_double2(0, 0);
+    if (erow_ok) {
+      const double2* zbase = (td.rmask >> (4 + ef)) & 1 ? a.r : a.zL;  // zL not yet written: r
+      if (td.phase == 0) e1 = __ldcg(zbase + eoff);
+      else if (td.phase == 1) { e1 = __ldcg(zbase + eoff); e2 = a.r[eoff]; }
+      else if (td.phase == 2) { e1 = __ldcg(a.w + eoff); e2 = __ldcg(a.z + eoff); }
+      else e1 = __ldcg(a.z + eoff);
+    }
     const int K = td.K;
     const double2* src;
     if (td.phase == 0) src = td.alt ? a.r : a.zL;
@@ -388,30 +404,26 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_bsp_tma(FusedArgs a) {
       double2 y = part[lane];
 #pragma unroll
       for (int w = 1; w < NW; ++w) y = cadd(y, part[w * 32 + lane]);
-      const int row = td.row0 + lane;
-      if (row >= td.rlo && row < td.rhi) {
-        const int f = row / n, p = row - f * n;
-        const long long off = (long long)td.tgt[f] + p;
-        const double2* zbase = (td.rmask >> (4 + f)) & 1 ? a.r : a.zL;  // zL not yet written: r
+      if (erow_ok) {
+        const long long off = eoff;
         if (td.phase == 0) {
-          a.zL[off] = cadd(__ldcg(zbase + off), y);
+          a.zL[off] = cadd(e1, y);
         } else if (td.phase == 1) {
-          const double2 zl = __ldcg(zbase + off);
-          const double2 v = csub(a.r[off], csub(zl, y));
+          const double2 v = csub(e2, csub(e1, y));  // r - (zL - S zL)
           a.rp[off] = v;
           a.w[off] = v;
-          a.z[off] = cadd(zl, v);
+          a.z[off] = cadd(e1, v);
         } else if (td.phase == 2) {
-          a.w[off] = cadd(__ldcg(a.w + off), y);
-          a.z[off] = cadd(__ldcg(a.z + off), y);
+          a.w[off] = cadd(e1, y);
+          a.z[off] = cadd(e2, y);
         } else {
-          a.wout[off] = csub(__ldcg(a.z + off), y);  // EPI_IMS on the final z
+          a.wout[off] = csub(e1, y);  // EPI_IMS on the final z
         }
       }
-      __threadfence();
     }
     consumers_sync(NT);
     if (threadIdx.x == 0 && td.phase != 3) {  // nothing waits on the (I - S) z tiles
+      __threadfence();  // publishes the epilogue stores ordered before it by the barrier
       const int r0 = max(td.rlo, td.row0), r1 = min(td.rhi, td.row0 + kRowTile);
       for (int f = r0 / n; f * n < r1; ++f) atomicAdd(a.done + td.tgt[f] / n, 1);
     }
