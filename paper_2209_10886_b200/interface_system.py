@@ -187,6 +187,18 @@ class GpuInterfaceSystem:
         self.sweep = SweepConfig()
         self.configure(sweep or SweepConfig())
 
+    # ---- resources
+    def close(self):
+        """Release the device memory of this system now (maps, factors, work buffers)."""
+        self.ctx.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+        return False
+
     # ---- reference attributes
     @property
     def operators(self):

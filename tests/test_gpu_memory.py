@@ -54,7 +54,9 @@ def test_memory_stable_and_released():
     # the accounting matches what the device lost (within allocator granularity)
     used = free0 - _free()
     assert used >= 0.9 * sys_.ctx.memory() - (64 << 20)
-    sys_.ctx.close()
+    sys_.close()
+    with pytest.raises(ValueError):  # a closed system refuses calls
+        sys_.apply_interface_operator(cvec(3, L))
     del sys_
     gc.collect()
     assert free0 - _free() <= (64 << 20)
