@@ -89,3 +89,33 @@ def test_host_buffer_apply_bitwise(name, c, blocks):
     gp = torch.from_numpy(g).pin_memory()
     for _ in range(3):
         assert np.array_equal(s.bsp_apply(gp).numpy(), zd)
+
+
+_VARIANT_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, 'tests')
+from conftest import cvec, product_problem
+from paper_2209_10886_b200.configs import CONFIGS, small_case
+from paper_2209_10886_b200.interface_system import GpuInterfaceSystem, SweepConfig
+for c, blocks in ((small_case(6, 3, 16), 5), (CONFIGS[2], 4), (CONFIGS[3], 4)):
+    spec, part = product_problem(c)
+    a = GpuInterfaceSystem(spec, part, fused=False, sweep=SweepConfig(blocks=blocks))
+    b = GpuInterfaceSystem(spec, part, fused=True, sweep=SweepConfig(blocks=blocks))
+    g = cvec(29, a.layout.size)
+    assert np.array_equal(a.bsp_apply(g), b.bsp_apply(g)), c["name"]
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("env", [{"HS_FUSED_TMA": "0"}, {"HS_FUSED_TMA": "1"}, {"HS_FUSED_RT": "2"}])
+def test_fused_variants_bitwise(env):
+    """Every fused-kernel variant (TMA-staged, register streaming, two strips
+    per tile) is bitwise the per-step result; the knobs are read once per
+    process, so each runs in its own interpreter."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT], cwd=root, env=dict(os.environ, **env),
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
