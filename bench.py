@@ -165,6 +165,21 @@ def _cpu_worker_solves(nsolves):
     return nsolves, time.perf_counter() - t0
 
 
+def host_info():
+    """CPU model and logical core count of the host (SURVEY.md §8d reporting)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "cpu_count": os.cpu_count(),
+            "note": "the reference's thread pool gives no speed-up (SURVEY.md §2a): parallel runs use processes"}
+
+
 def cpu_baseline(cfgno, n_solves_apply, budget_s=20.0):
     """Single-core sample of the reference arithmetic (SuperLU solve + outgoing
     traces of one interior subdomain), projected to one BSP apply."""
@@ -180,7 +195,7 @@ def cpu_baseline(cfgno, n_solves_apply, budget_s=20.0):
             "sample": f"{n2} SuperLU solves + outgoing traces of one interior subdomain "
                       f"({t_solve * 1e3:.2f} ms each; factor {t_fac:.2f} s), projected to one BSP apply = "
                       f"{n_solves_apply} subdomain solves",
-            "t_solve_s": t_solve}
+            "t_solve_s": t_solve, "host": host_info()}
 
 
 def run_reference(args):
@@ -220,7 +235,8 @@ def run_reference(args):
             "cpu_baseline": {"value": value, "unit": "applies/s", "cores": procs, "kind": "port",
                              "sample": f"each step: {procs} processes x {per} SuperLU solves + outgoing traces of "
                                        f"an interior {c['n']}x{c['n']} subdomain; applies/s = solves/s / {nsol} "
-                                       f"solves per BSP apply"},
+                                       f"solves per BSP apply",
+                             "host": host_info()},
             "e2e": {"value": value, "unit": "applies/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -448,6 +464,8 @@ def main():
                 "config": config_json(c, world), "roofline": roof,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": m["launches"], "clocks": m["clk"],
                 "gmres": gm, "setup_s": setup_s, "setup_warm_s": setup_warm_s, "variants": variants}
+        if R > 1:  # one apply covers all R right-hand sides (RHS-applies/s for cfg 4)
+            line["rhs_applies_per_s"] = value * R
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
