@@ -46,12 +46,16 @@ def test_seam_modes_differ_from_iteration_1(tmp_path):
 
 
 def test_rerun_byte_identical(tmp_path):
-    a, b = tmp_path / "r1", tmp_path / "r2"
-    base = ["--n1", "4", "--n2", "3", "--precond", "bsp"]
-    assert cli.main(base + ["--out", str(a)]) == 0
-    assert cli.main(base + ["--out", str(b), "--workers", "4"]) == 0
+    """SPEC acceptance 8: report, residuals and field byte-identical for
+    workers in {1, 2, 4} on a 3x3 run."""
+    base = ["--n1", "3", "--n2", "3", "--precond", "bsp"]
+    outs = []
+    for w in (1, 2, 4):
+        d = tmp_path / f"w{w}"
+        assert cli.main(base + ["--out", str(d), "--workers", str(w)]) == 0
+        outs.append(d)
     for name in ("residuals.csv", "schedule.txt", "field.csv", "report.txt"):
-        assert _read(a, name) == _read(b, name), name
+        assert _read(outs[0], name) == _read(outs[1], name) == _read(outs[2], name), name
 
 
 def test_not_converged_exit_2(tmp_path):

@@ -88,3 +88,27 @@ def test_reconstruction_vs_oracle_local_solves():
     rng = np.random.default_rng(5)
     g = rng.standard_normal(itf.size) + 1j * rng.standard_normal(itf.size)
     assert relerr(s.reconstruct_solution(g), reconstruct(itf, g, itf.liftings())) < 1e-11
+
+
+def test_convergence_trend_acceptance_6():
+    """SPEC acceptance 6 on the GPU path: kappa = 2 pi, n = 25, N1 = 5,
+    N2 in {5, 10}: SP and BSP converge to 1e-6, BSP needs at least SP's
+    iterations, and fewer total sequential steps at N2 = 10; the iteration
+    counts equal the CPU oracle's."""
+    from oracle.pipeline import solve_problem as oracle_solve
+    out = {}
+    for n2 in (5, 10):
+        c = small_case(5, n2, 25)
+        spec, part = product_problem(c)
+        prob, lat = oracle_problem(c)
+        for kind in ("sp", "bsp"):
+            rep = solve_problem(spec, part, SweepConfig(kind=kind), GmresOptions(tol=1e-6, maxit=500),
+                                reconstruct=False)
+            assert rep.converged
+            ref = oracle_solve(prob, lat, kind=kind, tol=1e-6, maxit=500)
+            assert abs(rep.iterations - ref.iterations) <= 1, (n2, kind, rep.iterations, ref.iterations)
+            out[(n2, kind)] = (rep.iterations, rep.steps_per_iteration)
+    for n2 in (5, 10):
+        assert out[(n2, "bsp")][0] >= out[(n2, "sp")][0]
+    sp, bsp = out[(10, "sp")], out[(10, "bsp")]
+    assert bsp[0] * bsp[1] <= sp[0] * sp[1]
