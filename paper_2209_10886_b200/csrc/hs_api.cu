@@ -993,7 +993,7 @@ int hs_factor(hs_ctx* c) {
   c->ws["__X"].p = X;
   c->ws["__X"].cap = (size_t)xstride * ncls;
   double2 *Rp, *Cp;
-  const long long pstride = 32LL * n;
+  const long long pstride = 32LL * n + 32 * 32;  // row/column panel + the panel inverse
   CK(tmp.alloc(&Rp, (size_t)pstride * ncls * sizeof(double2)));
   CK(tmp.alloc(&Cp, (size_t)pstride * ncls * sizeof(double2)));
   int* dbad;

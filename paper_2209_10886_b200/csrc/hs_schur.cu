@@ -80,127 +80,151 @@ __global__ void k_formS(double2* X, long long xstride, const uint8_t* masks, OpP
 }
 
 // Panel step of blocked Gauss-Jordan on A = X_k (n x n, in place), panel
-// columns J = [j0, j0+nb).  Each CTA inverts P = A[J,J] in shared memory
-// (GJ with partial pivoting), then writes row panel Rp[:, cols] = P^{-1} A[J, cols]
-// (cols outside J) or P^{-1}[:, cols-j0] (cols inside J) for its column tile,
-// and copies part of the column panel Cp = A[:, J].
-// grid (ceil(n/64), ncls), block 256
-__global__ void __launch_bounds__(256) k_gj_panel(const double2* X, long long xstride, int k, int n,
-                                                  int j0, int nb, double2* Rp, double2* Cp,
-                                                  long long pstride, int* bad) {
-  __shared__ double2 Aug[32][65];   // [P | I]
-  __shared__ double2 fcol[32];
-  __shared__ int piv;
+// columns J = [j0, j0+nb), in two kernels:
+//   k_gj_inv:    CTA 0: P^{-1} of P = A[J,J] by Gauss-Jordan with partial
+//                pivoting (max |re| + |im|, ties to the lower row) -> Pinv;
+//                the other CTAs copy the panels A[J, :] and A[:, J];
+//   k_gj_update: each 32 x 32 tile forms its row-panel tile P^{-1} A[J, cols]
+//                and applies the trailing update.
+// k_gj_inv keeps [P | I] in registers: warp w owns columns [8w, 8w + 8),
+// lane = row.  Per pivot step the warp owning column p finds the pivot and
+// publishes the column and the pivot's inverse (double-buffered by step
+// parity), one barrier, then every warp swaps rows p and pr, scales the pivot
+// row and eliminates its columns with warp shuffles: one barrier per step
+// (the shared-memory form had five and took 57 us per panel).
+// grid (ncls), block 256
+__global__ void __launch_bounds__(256) k_gj_inv(const double2* X, long long xstride, int k, int n, int j0,
+                                                int nb, double2* Pinv, double2* Bp, double2* Cp,
+                                                long long pstride, int* bad) {
+  __shared__ double2 gj_f[2][32];
+  __shared__ double2 gj_inv[2];
+  __shared__ int gj_piv[2];
   const int c = blockIdx.y;
   const double2* A = X + c * xstride + (long long)k * n * n;
-  double2* R = Rp + c * pstride;
-  double2* Cpp = Cp + c * pstride;
-  const int tid = threadIdx.x;
-  for (int i = tid; i < 32 * 64; i += 256) {
-    int r = i / 64, q = i % 64;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (blockIdx.x > 0) {
+    // the other CTAs copy the row panel Bp = A[J, :] and the column panel
+    // Cp = A[:, J] before the update overwrites A
+    const int nc = gridDim.x - 1, b = blockIdx.x - 1;
+    double2* B = Bp + c * pstride;
+    double2* Cpp = Cp + c * pstride;
+    for (int i = b * 256 + tid; i < nb * n; i += nc * 256) {
+      const int t = i / n, col = i % n;
+      B[(long long)t * n + col] = A[(long long)(j0 + t) * n + col];
+    }
+    for (int i = b * 256 + tid; i < n * nb; i += nc * 256) {
+      const int r = i / nb, t = i % nb;
+      Cpp[(long long)r * 32 + t] = A[(long long)r * n + j0 + t];
+    }
+    return;
+  }
+  double2 a[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int q = warp * 8 + u;
     double2 v = make_double2(0, 0);
-    if (r < nb) {
-      if (q < nb) v = A[(long long)(j0 + r) * n + j0 + q];
-      else if (q - 32 == r) v = make_double2(1, 0);
-    } else if (q == r || q - 32 == r) {
-      v = make_double2(q == r ? 1 : 0, 0);  // pad rows: identity, never pivoted into
+    if (lane < nb) {
+      if (q < nb) v = A[(long long)(j0 + lane) * n + j0 + q];
+      else if (q - 32 == lane) v = make_double2(1, 0);
+    } else if (q == lane || q - 32 == lane) {
+      v = make_double2(q == lane ? 1 : 0, 0);  // pad rows: identity, never pivoted into
     }
-    Aug[r][q] = v;
+    a[u] = v;
   }
-  __syncthreads();
-  for (int p = 0; p < nb; ++p) {
-    if (tid < 32) {
-      double best = -1.0;
-      int bi = p;
-      if (tid >= p && tid < nb) {
-        best = fabs(Aug[tid][p].x) + fabs(Aug[tid][p].y);
-        bi = tid;
-      }
-      for (int o = 16; o > 0; o >>= 1) {
-        double ob = __shfl_xor_sync(0xffffffffu, best, o);
-        int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
-      }
-      if (tid == 0) {
-        piv = bi;
-        if (!(best > 0.0) && bad) atomicExch(bad, 1);
-      }
-    }
-    __syncthreads();
-    const int pr = piv;
-    if (pr != p) {
-      for (int q = tid; q < 64; q += 256) {
-        double2 t = Aug[p][q];
-        Aug[p][q] = Aug[pr][q];
-        Aug[pr][q] = t;
-      }
-      __syncthreads();
-    }
-    double2 d = Aug[p][p];
-    double den = d.x * d.x + d.y * d.y;
-    double2 inv = make_double2(d.x / den, -d.y / den);
-    __syncthreads();
-    for (int q = tid; q < 64; q += 256) Aug[p][q] = cmul(Aug[p][q], inv);
-    if (tid < 32) fcol[tid] = Aug[tid][p];
-    __syncthreads();
-    for (int i = tid; i < 32 * 64; i += 256) {
-      int r = i / 64, q = i % 64;
-      if (r == p || r >= nb) continue;
-      double2 f = fcol[r];
-      if (f.x == 0.0 && f.y == 0.0) continue;
-      double2 pv = Aug[p][q];
-      Aug[r][q] = csub(Aug[r][q], cmul(f, pv));
-    }
-    __syncthreads();
-  }
-  // Aug[:, 32:32+nb] = P^{-1}.  Thread owns column q of the 64-column tile and
-  // rows r = (tid >> 6) + 4 i; the original A[J, col] column is read once.
-  const int col0 = blockIdx.x * 64;
-  {
-    const int q = tid & 63, col = col0 + q;
-    if (col < n) {
-      const bool inJ = col >= j0 && col < j0 + nb;
-      double2 bcol[32];
-      if (!inJ) {
+  // p = 8 pb + pu with pu unrolled: the pivot column is a static register
+#pragma unroll 1
+  for (int pb = 0; pb * 8 < nb; ++pb)
 #pragma unroll
-        for (int t = 0; t < 32; ++t) bcol[t] = t < nb ? A[(long long)(j0 + t) * n + col] : make_double2(0, 0);
+  for (int pu = 0; pu < 8; ++pu) {
+    const int p = pb * 8 + pu;
+    if (p >= nb) break;
+    const int par = p & 1;
+    if (warp == pb) {
+      const double2 v = a[pu];
+      // pivot = max |re| + |im| in one warp reduction: the magnitude rounded to
+      // float (non-negative floats order like their bit patterns) with the low
+      // 5 bits replaced by 31 - row, so ties go to the lower row
+      unsigned key = 0;
+      if (lane >= p && lane < nb) {
+        const float m = (float)(fabs(v.x) + fabs(v.y));
+        key = (__float_as_uint(m) & ~31u) | (31u - lane);
       }
-      for (int r = tid >> 6; r < nb; r += 4) {
-        double2 v;
-        if (inJ) {
-          v = Aug[r][32 + col - j0];
-        } else {
-          v = make_double2(0, 0);
-#pragma unroll
-          for (int t = 0; t < 32; ++t) cfma(v, Aug[r][32 + t], bcol[t]);
-        }
-        R[(long long)r * n + col] = v;
+      const unsigned best = __reduce_max_sync(0xffffffffu, key);
+      const int bi = 31 - (int)(best & 31u);
+      gj_f[par][lane] = v;
+      if (lane == 0) {
+        gj_piv[par] = bi;
+        if ((best & ~31u) == 0u && bad) atomicExch(bad, 1);  // zero pivot column
+      }
+      if (lane == bi) {
+        const double rden = 1.0 / (v.x * v.x + v.y * v.y);
+        gj_inv[par] = make_double2(v.x * rden, -v.y * rden);
       }
     }
+    __syncthreads();
+    const int pr = gj_piv[par];
+    const double2 inv = gj_inv[par];
+    const int src = lane == p ? pr : (lane == pr ? p : lane);  // row of the swapped matrix
+    const double2 f = gj_f[par][src];
+    const bool fz = f.x == 0.0 && f.y == 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      double2 pv, pp;  // rows pr and p of this column before the swap
+      pv.x = __shfl_sync(0xffffffffu, a[u].x, pr);
+      pv.y = __shfl_sync(0xffffffffu, a[u].y, pr);
+      pp.x = __shfl_sync(0xffffffffu, a[u].x, p);
+      pp.y = __shfl_sync(0xffffffffu, a[u].y, p);
+      const double2 np = cmul(pv, inv);  // scaled pivot row
+      const double2 arq = lane == pr ? pp : a[u];
+      if (lane == p) a[u] = np;
+      else if (lane < nb) a[u] = fz ? arq : csub(arq, cmul(f, np));
+    }
   }
-  // column panel copy: rows split across CTAs
-  for (int i = blockIdx.x * 256 + tid; i < n * nb; i += gridDim.x * 256) {
-    int r = i / nb, t = i % nb;
-    Cpp[(long long)r * 32 + t] = A[(long long)r * n + j0 + t];
+  if (warp >= 4) {  // columns 32..63 hold P^{-1}
+    double2* Pi = Pinv + c * pstride;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) Pi[lane * 32 + (warp - 4) * 8 + u] = a[u];
   }
 }
 
+constexpr size_t kGjUpdSmem = 4 * 32 * 33 * sizeof(double2);
+
 // Trailing update of the GJ panel step.  grid (ceil(n/32), ceil(n/32), ncls), block 256
 __global__ void __launch_bounds__(256) k_gj_update(double2* X, long long xstride, int k, int n,
-                                                   int j0, int nb, const double2* Rp,
+                                                   int j0, int nb, const double2* Pinv, const double2* Bp,
                                                    const double2* Cp, long long pstride) {
-  __shared__ double2 Cs[32][33];
-  __shared__ double2 Rs[32][33];
+  extern __shared__ double2 upd_sm[];  // Cs, Rs, Ps, Bs: 4 x [32][33]
+  auto Cs = reinterpret_cast<double2 (*)[33]>(upd_sm);
+  auto Rs = reinterpret_cast<double2 (*)[33]>(upd_sm + 32 * 33);
+  auto Ps = reinterpret_cast<double2 (*)[33]>(upd_sm + 2 * 32 * 33);
+  auto Bs = reinterpret_cast<double2 (*)[33]>(upd_sm + 3 * 32 * 33);
   const int c = blockIdx.z;
   double2* A = X + c * xstride + (long long)k * n * n;
-  const double2* R = Rp + c * pstride;
+  const double2* B = Bp + c * pstride;
   const double2* C = Cp + c * pstride;
+  const double2* Pi = Pinv + c * pstride;
   const int r0 = blockIdx.y * 32, q0 = blockIdx.x * 32;
   const int tid = threadIdx.x;
   for (int i = tid; i < 32 * 32; i += 256) {
     int a = i / 32, b = i % 32;
     Cs[a][b] = (r0 + a < n && b < nb) ? C[(long long)(r0 + a) * 32 + b] : make_double2(0, 0);
-    Rs[a][b] = (a < nb && q0 + b < n) ? R[(long long)a * n + q0 + b] : make_double2(0, 0);
+    Ps[a][b] = Pi[i];
+    Bs[a][b] = (a < nb && q0 + b < n) ? B[(long long)a * n + q0 + b] : make_double2(0, 0);
+  }
+  __syncthreads();
+  // row panel tile R = P^{-1} A[J, cols] (cols outside J) or P^{-1}[:, cols - j0]
+  for (int i = tid; i < 32 * 32; i += 256) {
+    const int t = i / 32, b = i % 32, col = q0 + b;
+    double2 v = make_double2(0, 0);
+    if (t < nb && col < n) {
+      if (col >= j0 && col < j0 + nb) {
+        v = Ps[t][col - j0];
+      } else {
+#pragma unroll
+        for (int u = 0; u < 32; ++u) cfma(v, Ps[t][u], Bs[u][b]);
+      }
+    }
+    Rs[t][b] = v;
   }
   __syncthreads();
   const int ql = tid & 31;
@@ -474,16 +498,20 @@ static OpParams op_params(const Ctx& c) {
 // X_k = S_k^{-1} for all rows and all classes (batched over the classes).
 cudaError_t factor_blocks(Ctx& c, double2* X, long long xstride, const uint8_t* dmasks, int ncls,
                           double2* Rp, double2* Cp, long long pstride, int* dbad) {
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(k_gj_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGjUpdSmem);
+  if (attr != cudaSuccess) return attr;
   const int n = c.n;
   OpParams P = op_params(c);
   for (int k = 0; k < n; ++k) {
     k_formS<<<dim3(n, ncls), 128, 0, c.stream>>>(X, xstride, dmasks, P, k);
     for (int j0 = 0; j0 < n; j0 += 32) {
       int nb = n - j0 < 32 ? n - j0 : 32;
-      k_gj_panel<<<dim3((n + 63) / 64, ncls), 256, 0, c.stream>>>(X, xstride, k, n, j0, nb, Rp, Cp,
-                                                                  pstride, dbad);
-      k_gj_update<<<dim3((n + 31) / 32, (n + 31) / 32, ncls), 256, 0, c.stream>>>(
-          X, xstride, k, n, j0, nb, Rp, Cp, pstride);
+      // Rp slice of a class: the row panel A[J, :] (32 x n), then P^{-1} (32 x 32)
+      k_gj_inv<<<dim3(1 + 8, ncls), 256, 0, c.stream>>>(X, xstride, k, n, j0, nb, Rp + 32LL * n, Rp, Cp,
+                                                          pstride, dbad);
+      k_gj_update<<<dim3((n + 31) / 32, (n + 31) / 32, ncls), 256, kGjUpdSmem, c.stream>>>(
+          X, xstride, k, n, j0, nb, Rp + 32LL * n, Rp, Cp, pstride);
     }
   }
   return cudaGetLastError();
