@@ -42,6 +42,10 @@ cudaError_t solve_boundary(Ctx& c, const double2* X, long long xstride, const ui
                            int ncls, int R, int nunit, const ExtraRHS* extras, double2* Y,
                            long long ystride, double2* Bk, long long bstride, double2* G,
                            long long gstride);
+// DMMA path of zgemm (M, N, K multiples of 32); false when not applicable
+bool zgemm_dmma(cudaStream_t st, int M, int N, int K, double2 alpha, const double2* A, int lda, long long sa,
+                const double2* B, int ldb, long long sb, double2 beta, double2* C, int ldc, long long sc,
+                int batch);
 void zgemm(cudaStream_t st, int M, int N, int K, double2 alpha, const double2* A, int lda,
            long long sa, const double2* B, int ldb, long long sb, double2 beta, double2* C, int ldc,
            long long sc, int batch);

@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 
 #include "hs_common.cuh"
 #include "hs_kernels.h"
@@ -520,6 +521,8 @@ cudaError_t factor_blocks(Ctx& c, double2* X, long long xstride, const uint8_t* 
 void zgemm(cudaStream_t st, int M, int N, int K, double2 alpha, const double2* A, int lda,
            long long sa, const double2* B, int ldb, long long sb, double2 beta, double2* C, int ldc,
            long long sc, int batch) {
+  static const bool use_dmma = !(getenv("HS_ZGEMM_FMA") && atoi(getenv("HS_ZGEMM_FMA")) != 0);
+  if (use_dmma && zgemm_dmma(st, M, N, K, alpha, A, lda, sa, B, ldb, sb, beta, C, ldc, sc, batch)) return;
   dim3 grid((N + 63) / 64, (M + 63) / 64, batch);
   k_zgemm<<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, sa, B, ldb, sb, beta, C, ldc, sc);
 }

@@ -92,14 +92,26 @@ __device__ __forceinline__ void zmma_cols(const MmaTask& tk, const MmaCol* __res
 
 // K chunks [kc0, kc0 + nk) of the task; on return the wk == 0 warps hold the
 // summed tile (cre/cim), and shared memory may be reused.
+__device__ __forceinline__ double2& zAs(double2* dyn, int st, int k, int m) { return dyn[st * kStageElems + k * SA + m]; }
+__device__ __forceinline__ double2& zBs(double2* dyn, int st, int k, int j) {
+  return dyn[st * kStageElems + KC * SA + k * SB + j];
+}
+
+// The pipelined contraction of K chunks [kc0, kc0 + nk): load(stage, kc) stages
+// chunk kc's A tile ([k][m], 32 x 32) and B tile ([k][j], 32 x 32) with
+// cp.async; on return the wk == 0 warps hold the summed 32 x 32 tile.
+template <class Load>
+__device__ __forceinline__ void zmma_core(double2* dyn, Load load, int kc0, int nk, double (&cre)[2][2][2],
+                                          double (&cim)[2][2][2]);
+
 __device__ __forceinline__ void zmma_main(const MmaTask& tk, const ZCols& zc, double2* dyn,
                                           const double2* __restrict__ A, const double2* srcA,
                                           const double2* srcB, int n, int R, int kc0, int nk,
                                           double (&cre)[2][2][2], double (&cim)[2][2][2]) {
   const int tid = threadIdx.x;
   const double2* Ab = A + tk.a_off;  // strip containing rows r0..r0+31: [K][32]
-  auto As = [&](int st, int k, int m) -> double2& { return dyn[st * kStageElems + k * SA + m]; };
-  auto Bs = [&](int st, int k, int j) -> double2& { return dyn[st * kStageElems + KC * SA + k * SB + j]; };
+  auto As = [&](int st, int k, int m) -> double2& { return zAs(dyn, st, k, m); };
+  auto Bs = [&](int st, int k, int j) -> double2& { return zBs(dyn, st, k, j); };
   auto load = [&](int stage, int kc) {
     const int k0 = kc * KC;
     const double2* asrc = Ab + (long long)k0 * BM;
@@ -119,6 +131,15 @@ __device__ __forceinline__ void zmma_main(const MmaTask& tk, const ZCols& zc, do
       else *dst = make_double2(0.0, 0.0);
     }
   };
+  zmma_core(dyn, load, kc0, nk, cre, cim);
+}
+
+template <class Load>
+__device__ __forceinline__ void zmma_core(double2* dyn, Load load, int kc0, int nk, double (&cre)[2][2][2],
+                                          double (&cim)[2][2][2]) {
+  const int tid = threadIdx.x;
+  auto As = [&](int st, int k, int m) -> double2& { return zAs(dyn, st, k, m); };
+  auto Bs = [&](int st, int k, int j) -> double2& { return zBs(dyn, st, k, j); };
   const int lane = tid & 31, warp = tid >> 5;
   const int wk = warp >> 2, wq = warp & 3;
   const int wm = wq >> 1, wn = wq & 1;
@@ -479,6 +500,69 @@ __global__ void __launch_bounds__(THREADS) k_zmma_fused_ks(FusedMmaArgs a) {
       for (int i = tid; i < ft.ninc; i += blockDim.x) atomicAdd(a.done + a.incs[ft.inc0 + i], 1);
     }
   }
+}
+
+// Batched complex GEMM on the DMMA pipe for the factorisation's solves
+// (C = alpha A B + beta C, row-major, M, N, K multiples of 32): the
+// contraction core above with tiles loaded straight from the matrices.
+// grid (N / 32, M / 32, batch), 256 threads
+__global__ void __launch_bounds__(THREADS) k_zgemm_dmma(int K, double2 alpha, const double2* __restrict__ A,
+                                                        int lda, long long sa, const double2* __restrict__ B,
+                                                        int ldb, long long sb, double2 beta, double2* C, int ldc,
+                                                        long long sc) {
+  extern __shared__ __align__(16) double2 dyn[];
+  const int z = blockIdx.z;
+  const double2* Ab = A + z * sa + (long long)blockIdx.y * 32 * lda;
+  const double2* Bb = B + z * sb + (long long)blockIdx.x * 32;
+  const int tid = threadIdx.x;
+  auto load = [&](int stage, int kc) {
+    const int k0 = kc * KC;
+#pragma unroll
+    for (int i = 0; i < (KC * BM) / THREADS; ++i) {  // A[m][k0 + kk] -> As[kk][m]
+      const int el = tid + i * THREADS, m = el / KC, kk = el % KC;
+      cp16(&zAs(dyn, stage, kk, m), Ab + (long long)m * lda + k0 + kk);
+    }
+#pragma unroll
+    for (int i = 0; i < (KC * BN) / THREADS; ++i) {  // B[k0 + kk][j] -> Bs[kk][j]
+      const int el = tid + i * THREADS, kk = el / BN, j = el % BN;
+      cp16(&zBs(dyn, stage, kk, j), Bb + (long long)(k0 + kk) * ldb + j);
+    }
+  };
+  double cre[2][2][2], cim[2][2][2];
+  zmma_core(dyn, load, 0, K / KC, cre, cim);
+  const int lane = tid & 31, warp = tid >> 5;
+  const int wk = warp >> 2, wq = warp & 3;
+  const int wm = wq >> 1, wn = wq & 1;
+  const int gid = lane >> 2, tig = lane & 3;
+  if (wk != 0) return;
+  double2* Cb = C + z * sc + (long long)blockIdx.y * 32 * ldc + blockIdx.x * 32;
+  const bool b0 = beta.x == 0.0 && beta.y == 0.0;
+#pragma unroll
+  for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int row = wm * 16 + mt * 8 + gid, col = wn * 16 + nt * 8 + 2 * tig + h;
+        double2* cp = Cb + (long long)row * ldc + col;
+        const double2 acc = make_double2(cre[mt][nt][h], cim[mt][nt][h]);
+        double2 v = cmul(alpha, acc);
+        if (!b0) v = cadd(v, cmul(beta, *cp));
+        *cp = v;
+      }
+}
+
+bool zgemm_dmma(cudaStream_t st, int M, int N, int K, double2 alpha, const double2* A, int lda, long long sa,
+                const double2* B, int ldb, long long sb, double2 beta, double2* C, int ldc, long long sc,
+                int batch) {
+  if (M % 32 || N % 32 || K % 32 || M == 0 || N == 0 || K == 0) return false;
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(k_zgemm_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(sizeof(double2) * STAGES * kStageElems));
+  if (attr != cudaSuccess) return false;
+  k_zgemm_dmma<<<dim3(N / 32, M / 32, batch), THREADS, sizeof(double2) * STAGES * kStageElems, st>>>(
+      K, alpha, A, lda, sa, B, ldb, sb, beta, C, ldc, sc);
+  return true;
 }
 
 constexpr size_t kZmmaSmem = sizeof(double2) * STAGES * kStageElems;
