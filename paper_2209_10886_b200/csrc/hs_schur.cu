@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(256) k_gj_inv(const double2* X, long long xstr
                                                 long long pstride, int* bad) {
   __shared__ double2 gj_f[2][32];
   __shared__ double2 gj_inv[2];
-  __shared__ int gj_piv[2];
+  __shared__ int gj_piv[2], gj_pos[2];
   const int c = blockIdx.y;
   const double2* A = X + c * xstride + (long long)k * n * n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -132,6 +132,10 @@ __global__ void __launch_bounds__(256) k_gj_inv(const double2* X, long long xstr
     }
     a[u] = v;
   }
+  // Rows are not moved: each lane keeps its row's logical position (the
+  // position row swaps would give it) and the pivot row is only broadcast.
+  int mypos = lane;
+  bool used = false;
   // p = 8 pb + pu with pu unrolled: the pivot column is a static register
 #pragma unroll 1
   for (int pb = 0; pb * 8 < nb; ++pb)
@@ -142,49 +146,53 @@ __global__ void __launch_bounds__(256) k_gj_inv(const double2* X, long long xstr
     const int par = p & 1;
     if (warp == pb) {
       const double2 v = a[pu];
-      // pivot = max |re| + |im| in one warp reduction: the magnitude rounded to
-      // float (non-negative floats order like their bit patterns) with the low
-      // 5 bits replaced by 31 - row, so ties go to the lower row
+      // pivot = max |re| + |im| over the rows not yet pivoted, in one warp
+      // reduction: the magnitude rounded to float (non-negative floats order
+      // like their bit patterns) with the low 5 bits replaced by 31 - position,
+      // so ties go to the lower (swapped) row
       unsigned key = 0;
-      if (lane >= p && lane < nb) {
+      if (!used && lane < nb) {
         const float m = (float)(fabs(v.x) + fabs(v.y));
-        key = (__float_as_uint(m) & ~31u) | (31u - lane);
+        key = (__float_as_uint(m) & ~31u) | (31u - (unsigned)mypos);
       }
       const unsigned best = __reduce_max_sync(0xffffffffu, key);
-      const int bi = 31 - (int)(best & 31u);
+      const int pl = __ffs(__ballot_sync(0xffffffffu, key == best)) - 1;
       gj_f[par][lane] = v;
       if (lane == 0) {
-        gj_piv[par] = bi;
+        gj_piv[par] = pl;
+        gj_pos[par] = 31 - (int)(best & 31u);
         if ((best & ~31u) == 0u && bad) atomicExch(bad, 1);  // zero pivot column
       }
-      if (lane == bi) {
+      if (lane == pl) {
         const double rden = 1.0 / (v.x * v.x + v.y * v.y);
         gj_inv[par] = make_double2(v.x * rden, -v.y * rden);
       }
     }
     __syncthreads();
-    const int pr = gj_piv[par];
+    const int pl = gj_piv[par], q = gj_pos[par];
     const double2 inv = gj_inv[par];
-    const int src = lane == p ? pr : (lane == pr ? p : lane);  // row of the swapped matrix
-    const double2 f = gj_f[par][src];
+    const double2 f = gj_f[par][lane];
     const bool fz = f.x == 0.0 && f.y == 0.0;
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      double2 pv, pp;  // rows pr and p of this column before the swap
-      pv.x = __shfl_sync(0xffffffffu, a[u].x, pr);
-      pv.y = __shfl_sync(0xffffffffu, a[u].y, pr);
-      pp.x = __shfl_sync(0xffffffffu, a[u].x, p);
-      pp.y = __shfl_sync(0xffffffffu, a[u].y, p);
+      double2 pv;  // the pivot row of this column
+      pv.x = __shfl_sync(0xffffffffu, a[u].x, pl);
+      pv.y = __shfl_sync(0xffffffffu, a[u].y, pl);
       const double2 np = cmul(pv, inv);  // scaled pivot row
-      const double2 arq = lane == pr ? pp : a[u];
-      if (lane == p) a[u] = np;
-      else if (lane < nb) a[u] = fz ? arq : csub(arq, cmul(f, np));
+      if (lane == pl) a[u] = np;
+      else if (lane < nb && !fz) a[u] = csub(a[u], cmul(f, np));
+    }
+    if (lane == pl) {
+      mypos = p;
+      used = true;
+    } else if (mypos == p) {
+      mypos = q;  // the row at position p moves to the pivot's position
     }
   }
-  if (warp >= 4) {  // columns 32..63 hold P^{-1}
+  if (warp >= 4) {  // columns 32..63 hold P^{-1}, row = the lane's position
     double2* Pi = Pinv + c * pstride;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) Pi[lane * 32 + (warp - 4) * 8 + u] = a[u];
+    for (int u = 0; u < 8; ++u) Pi[mypos * 32 + (warp - 4) * 8 + u] = a[u];
   }
 }
 
