@@ -655,7 +655,7 @@ int check_ready(Ctx* c, int R) {
   NEED_GPU(c);
   if (!c->factored) return fail(c, 1, "hs_factor has not been called");
   if (R < 1 || R > 1024) return fail(c, 1, "nrhs must be in 1..1024");
-  if (build_steps(c)) return -1;
+  if (int e_ = build_steps(c)) return e_;
   if (ensure_xbuf(c, R)) return -1;
   return 0;
 }
@@ -666,7 +666,7 @@ int do_half(Ctx* c, int dir, const double2* r, double2* z, int R) {
   CK(cudaMemcpyAsync(z, r, LR * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
   auto& steps = dir == 0 ? c->fwd : c->bwd;
   for (auto& st : steps)
-    if (run_step(c, st, z, r, epi(EPI_ACC, z), R)) return -1;
+    if (int e_ = run_step(c, st, z, r, epi(EPI_ACC, z), R)) return e_;
   if (c->seam == HS_SEAM_LITERAL) launch_seam_add(*c, dir, z, r, R);
   return 0;
 }
@@ -698,10 +698,10 @@ int do_precond(Ctx* c, int kind, const double2* r, double2* z, int R) {
     if (ws_get(c, "zL", LR, &zl)) return -1;
     CK(cudaMemcpyAsync(zl, r, LR * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
     for (auto& st : c->sp_fwd)
-      if (run_step(c, st, zl, r, epi(EPI_ACC, zl), R)) return -1;
+      if (int e_ = run_step(c, st, zl, r, epi(EPI_ACC, zl), R)) return e_;
     CK(cudaMemcpyAsync(z, zl, LR * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
     for (auto& st : c->sp_bwd)
-      if (run_step(c, st, z, zl, epi(EPI_ACC, z), R)) return -1;
+      if (int e_ = run_step(c, st, z, zl, epi(EPI_ACC, z), R)) return e_;
     return 0;
   }
   if (kind != HS_PC_BSP) return fail(c, 1, "unknown preconditioner kind");
@@ -734,7 +734,7 @@ int do_precond(Ctx* c, int kind, const double2* r, double2* z, int R) {
       c->seam == HS_SEAM_DEDUP && c->full.nitems > 0) {
     // the whole apply on the DMMA contraction as one dataflow launch
     if (!c->fused_mma.built || c->fused_mma.R != R || c->fused_mma.shared != shared)
-      if (build_fused_mma(c, R, shared)) return -1;
+      if (int e_ = build_fused_mma(c, R, shared)) return e_;
     CK(cudaMemcpyAsync(zl, r, LR * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
     FusedMmaArgs a;
     a.A = shared ? c->Tcls : c->T;
@@ -754,17 +754,17 @@ int do_precond(Ctx* c, int kind, const double2* r, double2* z, int R) {
     }
     return 0;
   }
-  if (do_half(c, 0, r, zl, R)) return -1;
+  if (int e_ = do_half(c, 0, r, zl, R)) return e_;
   const double2* rsrc;
   if (c->inter) {
-    if (run_step(c, c->full, zl, zl, epi(EPI_RESID, rp, w, z, r, zl), R)) return -1;
+    if (int e_ = run_step(c, c->full, zl, zl, epi(EPI_RESID, rp, w, z, r, zl), R)) return e_;
     rsrc = rp;
   } else {
     launch_vec(*c, VEC_INIT_BWD, LR, w, z, r, zl);
     rsrc = r;
   }
   for (auto& st : c->bwd)
-    if (run_step(c, st, w, rsrc, epi(EPI_ACC2, w, z), R)) return -1;
+    if (int e_ = run_step(c, st, w, rsrc, epi(EPI_ACC2, w, z), R)) return e_;
   if (c->seam == HS_SEAM_LITERAL) launch_seam_add(*c, 1, z, rsrc, R);
   return 0;
 }
@@ -1088,7 +1088,7 @@ int hs_lifting_rhs(hs_ctx* c, const double* vals, int nrhs, double* bout, int me
   const int n = c->n;
   const long long LR = LRof(c, nrhs);
   double2* b;
-  if (dev_out(c, bout, LR, mem, "out", &b)) return -1;
+  if (int e = dev_out(c, bout, LR, mem, "out", &b)) return e;
   CK(cudaMemsetAsync(b, 0, LR * sizeof(double2), c->stream));
   const double ih2 = 1.0 / (c->h * c->h);
   const std::complex<double> tau(c->tau_re, c->tau_im);
@@ -1152,7 +1152,8 @@ int hs_reconstruct(hs_ctx* c, const double* g, const double* lift_vals, double* 
   const long long F = (long long)c->n1 * c->n2 * n * n;
   const double2* dg;
   double2* df;
-  if (dev_in(c, g, L, mem, "rin", &dg) || dev_out(c, field, F, mem, "rout", &df)) return -1;
+  if (int e = dev_in(c, g, L, mem, "rin", &dg)) return e;
+  if (int e = dev_out(c, field, F, mem, "rout", &df)) return e;
   CK(cudaMemsetAsync(df, 0, F * sizeof(double2), c->stream));
   const double ih2 = 1.0 / (c->h * c->h);
   const std::complex<double> tau(c->tau_re, c->tau_im);
@@ -1233,8 +1234,9 @@ int hs_apply(hs_ctx* c, int mode, const double* g, double* out, int nrhs, int me
   const long long LR = LRof(c, nrhs);
   const double2* dg;
   double2* dout;
-  if (dev_in(c, g, LR, mem, "in", &dg) || dev_out(c, out, LR, mem, "out", &dout)) return -1;
-  if (do_apply(c, mode, dg, dout, nrhs)) return -1;
+  if (int e = dev_in(c, g, LR, mem, "in", &dg)) return e;
+  if (int e = dev_out(c, out, LR, mem, "out", &dout)) return e;
+  if (int e_ = do_apply(c, mode, dg, dout, nrhs)) return e_;
   return finish_out(c, out, dout, LR, mem);
 }
 
@@ -1245,7 +1247,8 @@ int hs_restricted_apply(hs_ctx* c, const double* g, double* out, int nrhs, const
   const long long LR = LRof(c, nrhs);
   const double2* dg;
   double2* dout;
-  if (dev_in(c, g, LR, mem, "in", &dg) || dev_out(c, out, LR, mem, "out", &dout)) return -1;
+  if (int e = dev_in(c, g, LR, mem, "in", &dg)) return e;
+  if (int e = dev_out(c, out, LR, mem, "out", &dout)) return e;
   std::vector<int> S(src, src + std::max(nsrc, 0)), Tg(tgt, tgt + std::max(ntgt, 0));
   DevStep st;
   if (make_step(c, c->plan.restricted_step(S, Tg), st)) return -1;
@@ -1285,8 +1288,9 @@ int hs_precond(hs_ctx* c, int kind, const double* r, double* z, int nrhs, int me
   const long long LR = LRof(c, nrhs);
   const double2* dr;
   double2* dz;
-  if (dev_in(c, r, LR, mem, "in", &dr) || dev_out(c, z, LR, mem, "out", &dz)) return -1;
-  if (do_precond(c, kind, dr, dz, nrhs)) return -1;
+  if (int e = dev_in(c, r, LR, mem, "in", &dr)) return e;
+  if (int e = dev_out(c, z, LR, mem, "out", &dz)) return e;
+  if (int e_ = do_precond(c, kind, dr, dz, nrhs)) return e_;
   return finish_out(c, z, dz, LR, mem);
 }
 
@@ -1297,8 +1301,9 @@ int hs_half_apply(hs_ctx* c, int direction, const double* r, double* z, int nrhs
   const long long LR = LRof(c, nrhs);
   const double2* dr;
   double2* dz;
-  if (dev_in(c, r, LR, mem, "in", &dr) || dev_out(c, z, LR, mem, "out", &dz)) return -1;
-  if (do_half(c, direction, dr, dz, nrhs)) return -1;
+  if (int e = dev_in(c, r, LR, mem, "in", &dr)) return e;
+  if (int e = dev_out(c, z, LR, mem, "out", &dz)) return e;
+  if (int e_ = do_half(c, direction, dr, dz, nrhs)) return e_;
   return finish_out(c, z, dz, LR, mem);
 }
 
@@ -1325,7 +1330,8 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
   }
   const double2* db;
   double2* dx;
-  if (dev_in(c, b, LR, mem, "gin", &db) || dev_out(c, x, LR, mem, "gout", &dx)) return -1;
+  if (int e = dev_in(c, b, LR, mem, "gin", &db)) return e;
+  if (int e = dev_out(c, x, LR, mem, "gout", &dx)) return e;
   int chunk = 0;
   int grid = dist ? 2 * c->num_sms : gmres_coop_grid(*c, LR, R, &chunk);
   if (grid <= 0) return fail(c, 3, "interface vector too large for the cooperative Arnoldi kernel");
@@ -1394,14 +1400,14 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
     double2* vk = V + (long long)k * LR;
     double2* w = V + (long long)(k + 1) * LR;
     if (pc == HS_PC_BSP && fused_bsp_ok(c, R) && !c->timing) {
-      if (do_precond_ims(c, vk, Z, w)) return -1;  // A M v_k in one launch
+      if (int e_ = do_precond_ims(c, vk, Z, w)) return e_;  // A M v_k in one launch
     } else {
       const double2* zin = vk;
       if (pc != HS_PC_NONE) {
-        if (do_precond(c, pc, vk, Z, R)) return -1;
+        if (int e_ = do_precond(c, pc, vk, Z, R)) return e_;
         zin = Z;
       }
-      if (do_apply(c, HS_APPLY_IMS, zin, w, R)) return -1;
+      if (int e_ = do_apply(c, HS_APPLY_IMS, zin, w, R)) return e_;
     }
     if (cgs2) {
       CK(gmres_arnoldi_cgs2(*c, G, k, c->d_owned, c->n_owned, part3, hbuf, c->nccl));
@@ -1433,7 +1439,7 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
     if (ws_get(c, "U", LR, &u)) return -1;
     CK(gmres_finish(*c, G, kdone, u));
     if (pc != HS_PC_NONE) {
-      if (do_precond(c, pc, u, dx, R)) return -1;
+      if (int e_ = do_precond(c, pc, u, dx, R)) return e_;
     } else {
       CK(cudaMemcpyAsync(dx, u, LR * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
     }
