@@ -152,6 +152,14 @@ int hs_gmres(hs_ctx* ctx, int pc_kind, const double* b, double* x, int nrhs, dou
  * bands; same iteration counts as MGS within +-1. */
 int hs_set_gmres_mode(hs_ctx* ctx, int mode);
 
+/* Test hook for the multi-GPU path: run the fused 1-RHS BSP
+ * apply of hs_precond as `ranks` row-band ranks emulated on this GPU -- every
+ * rank with its own vectors, counters and tile list, reaching the other
+ * ranks' blocks through their buffers (the peer-memory protocol of the
+ * multi-GPU kernel) -- in one launch.  1 = off.  Results are bitwise those of
+ * the single-rank apply. */
+int hs_set_emulated_ranks(hs_ctx* ctx, int ranks);
+
 /* Bit mask.  Bit 0 (default on): a BSP apply with one RHS on per-subdomain
  * maps runs as one persistent dataflow launch (per-block completion counters
  * instead of one launch per step; bitwise identical results).  Bit 1 (default

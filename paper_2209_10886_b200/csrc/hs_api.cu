@@ -482,9 +482,12 @@ int build_fused(Ctx* c, bool ims) {
   return 0;
 }
 
+void free_emu(Ctx* c);
+
 int build_steps(Ctx* c) {
   if (!c->steps_dirty) return 0;
   free_fused(c);
+  free_emu(c);
   free_fused_mma(c);
   for (auto& s : c->fwd) free_step(c, s);
   for (auto& s : c->bwd) free_step(c, s);
@@ -671,6 +674,79 @@ int do_half(Ctx* c, int dir, const double2* r, double2* z, int R) {
   return 0;
 }
 
+void free_emu(Ctx* c) {
+  EmuRanks& e = c->emu;
+  dfree(c, e.blk_rank, 0);
+  for (int g = 0; g < kMaxRanks; ++g) dfree(c, e.tiles[g], 0);
+  dfree(c, e.buf, 0);
+  dfree(c, e.counters, 0);
+  const int G = e.G;
+  e = EmuRanks();
+  e.G = G;
+}
+
+// Per-rank tile lists, owners and buffers of the emulated row bands (the
+// row-band partition of Plan::build with G ranks).
+int build_emu(Ctx* c) {
+  EmuRanks& e = c->emu;
+  free_emu(c);
+  const Plan& P = c->plan;
+  const DevFused& f = c->fused;
+  Plan pg;
+  std::string err = pg.build(P.n1, P.n2, P.n, 0, e.G);
+  if (!err.empty()) return fail(c, 1, "emulated ranks: " + err);
+  e.sub_rank.assign(P.nsub, 0);
+  for (int s = 0; s < P.nsub; ++s) e.sub_rank[s] = pg.subs[s].rank;
+  std::vector<int> br(P.npairs);
+  for (int b = 0; b < P.npairs; ++b) br[b] = e.sub_rank[P.block_sub[b]];
+  if (upload(c, &e.blk_rank, br)) return -1;
+  std::vector<FusedTile> tiles(f.ntiles);
+  std::vector<DevItem> items(f.nitems);
+  CK(cudaMemcpy(tiles.data(), f.tiles, tiles.size() * sizeof(FusedTile), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(items.data(), f.items, items.size() * sizeof(DevItem), cudaMemcpyDeviceToHost));
+  std::vector<std::vector<FusedTile>> per(e.G);
+  for (const FusedTile& t : tiles) per[e.sub_rank[items[t.item].s]].push_back(t);
+  for (int g = 0; g < e.G; ++g) {
+    e.ntiles[g] = (int)per[g].size();
+    if (upload(c, &e.tiles[g], per[g])) return -1;
+  }
+  CK(dalloc(c, (void**)&e.buf, (size_t)e.G * 5 * P.L * sizeof(double2)));
+  CK(dalloc(c, (void**)&e.counters, (size_t)e.G * (P.npairs + 1) * sizeof(int)));
+  e.built = true;
+  return 0;
+}
+
+// The fused BSP apply over G emulated row-band ranks on this GPU: every rank
+// has its own copy of r, zL, rp, w, z and of the completion counters, uses
+// only the blocks it owns, and reaches other ranks' blocks through their
+// buffers -- the multi-GPU peer-memory protocol in one launch.
+int do_precond_emulated(Ctx* c, const double2* r, double2* z) {
+  EmuRanks& e = c->emu;
+  if (!e.built && build_emu(c)) return -1;
+  const Plan& P = c->plan;
+  const long long L = P.L;
+  MultiRankArgs mr;
+  mr.G = e.G;
+  mr.self = -1;
+  mr.blk_rank = e.blk_rank;
+  const double2* zsrc[kMaxRanks];
+  CK(cudaMemsetAsync(e.counters, 0, (size_t)e.G * (P.npairs + 1) * sizeof(int), c->stream));
+  for (int g = 0; g < e.G; ++g) {
+    double2* base = e.buf + (size_t)g * 5 * L;
+    CK(cudaMemcpyAsync(base, r, L * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
+    for (int k = 0; k < 5; ++k) mr.v[k][g] = base + (size_t)k * L;  // r, zL, rp, w, z
+    mr.v[FV_WOUT][g] = nullptr;
+    mr.done[g] = e.counters + (size_t)g * (P.npairs + 1);
+    mr.ticket[g] = mr.done[g] + P.npairs;
+    mr.tiles[g] = e.tiles[g];
+    mr.ntiles[g] = e.ntiles[g];
+    zsrc[g] = mr.v[FV_Z][g];
+  }
+  CK(launch_bsp_fused_ranks(*c, c->fused, mr));
+  launch_gather_blocks(*c, z, zsrc, e.G, e.blk_rank, L);
+  return cudaGetLastError() == cudaSuccess ? 0 : fail(c, -1, "emulated ranks: launch failed");
+}
+
 bool fused_bsp_ok(const Ctx* c, int R) {
   return (c->fused_mode & 1) && R == 1 && c->map_mode == 0 && c->plan.nranks == 1 && c->inter &&
          c->seam == HS_SEAM_DEDUP && c->full.nitems > 0;
@@ -710,6 +786,7 @@ int do_precond(Ctx* c, int kind, const double2* r, double2* z, int R) {
   if (fused_bsp_ok(c, R)) {
     // the whole apply as one dataflow launch (bitwise identical to the step sequence)
     if (!c->fused.built && build_fused(c, false)) return -1;
+    if (c->emu.G > 1) return do_precond_emulated(c, r, z);
     // no zL = r copy: the plan's rmask makes tiles read r for blocks zL has not received yet
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->timing) {
@@ -1642,6 +1719,16 @@ int hs_set_fused(hs_ctx* c, int mask) {
   if (!c) return fail(nullptr, 1, "null context");
   if (mask < 0 || mask > 3) return fail(c, 1, "fused mask must be 0..3");
   c->fused_mode = mask;
+  return 0;
+}
+
+int hs_set_emulated_ranks(hs_ctx* c, int ranks) {
+  if (!c) return fail(nullptr, 1, "null context");
+  if (ranks < 1 || ranks > kMaxRanks || ranks > c->n2)
+    return fail(c, 1, "emulated ranks must be in 1..min(8, N2)");
+  if (c->plan.nranks != 1) return fail(c, 1, "emulated ranks need a single-rank context");
+  free_emu(c);
+  c->emu.G = ranks;
   return 0;
 }
 

@@ -104,6 +104,12 @@ __global__ void __launch_bounds__(NW * 32) k_step1(const DevTile* __restrict__ t
 // and the 13-17 launches + ramps per apply disappear.  Deadlock-free: a
 // dependency always points to an earlier ticket, held by a running CTA.
 // Same arithmetic and summation order as k_step1 (bitwise identical result).
+// Row-band ranks (multi-rank instantiations, MR): every block lives -- all its
+// vectors and its completion counter -- on its owner rank; a tile reads its
+// subdomain's slab on its own rank and writes its output blocks, and signals
+// their counters, on the owners' ranks (peer memory across GPUs).  self >= 0:
+// all CTAs are that rank (one GPU per rank); self < 0: CTA c emulates rank
+// c % G on one GPU (one launch over all ranks' data).
 struct FusedArgs {
   const FusedTile* tiles;
   const DevItem* items;
@@ -119,43 +125,83 @@ struct FusedArgs {
   int* done;
   int* ticket;
   int ntiles, n, maxK;
+  MultiRankArgs mr;
+};
+
+// Rank view of a CTA: its tile list and the owner-rank addressing of blocks.
+template <bool MR>
+struct RankView {
+  const FusedArgs& a;
+  int cr;
+  __device__ explicit RankView(const FusedArgs& args)
+      : a(args), cr(MR ? (args.mr.self >= 0 ? args.mr.self : (int)(blockIdx.x % args.mr.G)) : 0) {}
+  __device__ const FusedTile* tiles() const { return MR ? a.mr.tiles[cr] : a.tiles; }
+  __device__ int* ticket() const { return MR ? a.mr.ticket[cr] : a.ticket; }
+  __device__ int ntiles() const { return MR ? a.mr.ntiles[cr] : a.ntiles; }
+  __device__ int owner(int block) const { return MR ? a.mr.blk_rank[block] : 0; }
+  __device__ int* done(int block) const { return (MR ? a.mr.done[owner(block)] : a.done) + block; }
+  __device__ double2* vec(int k, int rk) const {
+    if (MR) return a.mr.v[k][rk];
+    switch (k) {
+      case FV_R: return const_cast<double2*>(a.r);
+      case FV_ZL: return a.zL;
+      case FV_RP: return a.rp;
+      case FV_W: return a.w;
+      case FV_Z: return a.z;
+      default: return a.wout;
+    }
+  }
+  // publishing a tile's stores before its signals: to the whole system when
+  // the owners are other GPUs
+  __device__ void fence() const {
+    if (MR && a.mr.self >= 0) __threadfence_system();
+    else __threadfence();
+  }
 };
 
 // RT = 32-row strips per tile (RT * K ~ 1024 columns-strips keeps the fixed
 // per-tile cost -- ticket, dependency check, slab load, epilogue -- amortised).
-template <int NW, int RT>
-__global__ void __launch_bounds__(NW * 32) k_bsp_fused(FusedArgs a) {
+// 6 CTAs of 8 warps per SM (40 registers) for the one-strip form: the map
+// stream needs the bytes in flight (5 CTAs per SM measured ~10 % slower at cfg5)
+template <int NW, int RT, bool MR>
+__global__ void __launch_bounds__(NW * 32, RT == 1 ? 6 : 1) k_bsp_fused(FusedArgs a) {
   extern __shared__ double2 sm[];
   __shared__ int s_t;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int n = a.n;
+  const RankView<MR> rv(a);
+  const int cr = rv.cr;
+  const FusedTile* tiles = rv.tiles();
+  const int ntiles = rv.ntiles();
   for (;;) {
-    if (threadIdx.x == 0) s_t = atomicAdd(a.ticket, 1);
+    if (threadIdx.x == 0) s_t = atomicAdd(rv.ticket(), 1);
     __syncthreads();
     const int t = s_t;
-    if (t >= a.ntiles) return;
-    const FusedTile ft = a.tiles[t];
+    if (t >= ntiles) return;
+    const FusedTile ft = tiles[t];
     const DevItem it = a.items[ft.item];
     const DevSub sb = a.subs[it.s];
     for (int d = threadIdx.x; d < ft.ndep; d += blockDim.x) {
       const FusedDep dp = a.deps[ft.dep0 + d];
-      const volatile int* p = a.done + dp.block;
+      const volatile int* p = rv.done(dp.block);
       while (*p < dp.count) __nanosleep(32);
     }
     __threadfence();
     __syncthreads();
     const int K = sb.k * n;
+    // the slab (this subdomain's incoming blocks) lives on this CTA's rank
     const double2* src;
-    if (ft.phase == 0) src = it.alt ? a.r : a.zL;
-    else if (ft.phase == 1) src = a.zL;
-    else if (ft.phase == 2) src = it.alt ? a.rp : a.w;
-    else src = a.z;  // phase 3: (I - S) z
+    if (ft.phase == 0) src = rv.vec(it.alt ? FV_R : FV_ZL, cr);
+    else if (ft.phase == 1) src = rv.vec(FV_ZL, cr);
+    else if (ft.phase == 2) src = rv.vec(it.alt ? FV_RP : FV_W, cr);
+    else src = rv.vec(FV_Z, cr);  // phase 3: (I - S) z
     src += sb.in_off;
+    const double2* rsrc = rv.vec(FV_R, cr) + sb.in_off;
     double2* xs = sm;
     double2* part = sm + K;
     // zL starts as r without a copy: faces of zL not yet written read r
     for (int i = threadIdx.x; i < K; i += NW * 32)
-      xs[i] = __ldcg(((ft.rmask >> (i / n)) & 1 ? a.r + sb.in_off : src) + i);
+      xs[i] = __ldcg(((ft.rmask >> (i / n)) & 1 ? rsrc : src) + i);
     __syncthreads();
     // strips beyond the map (RT > 1 at the last rows) are skipped
     const int nstrip = (K + kRowTile - 1) / kRowTile;
@@ -210,31 +256,36 @@ __global__ void __launch_bounds__(NW * 32) k_bsp_fused(FusedArgs a) {
       if (row >= it.rlo && row < it.rhi) {
         const int f = row / n, p = row - f * n;
         const long long off = (long long)sb.tgt[f] + p;
-        const double2* zbase = (ft.rmask >> (4 + f)) & 1 ? a.r : a.zL;  // zL not yet written: r
+        const int o = rv.owner(sb.tgt[f] / n);  // the output block's rank
+        const double2* r_o = rv.vec(FV_R, o);
+        double2* zL_o = rv.vec(FV_ZL, o);
+        const double2* zbase = (ft.rmask >> (4 + f)) & 1 ? r_o : zL_o;  // zL not yet written: r
         if (ft.phase == 0) {
-          a.zL[off] = cadd(__ldcg(zbase + off), y);
+          zL_o[off] = cadd(__ldcg(zbase + off), y);
         } else if (ft.phase == 1) {
           const double2 zl = __ldcg(zbase + off);
-          const double2 v = csub(a.r[off], csub(zl, y));
-          a.rp[off] = v;
-          a.w[off] = v;
-          a.z[off] = cadd(zl, v);
+          const double2 v = csub(r_o[off], csub(zl, y));
+          rv.vec(FV_RP, o)[off] = v;
+          rv.vec(FV_W, o)[off] = v;
+          rv.vec(FV_Z, o)[off] = cadd(zl, v);
         } else if (ft.phase == 2) {
-          a.w[off] = cadd(__ldcg(a.w + off), y);
-          a.z[off] = cadd(__ldcg(a.z + off), y);
+          double2* w_o = rv.vec(FV_W, o);
+          double2* z_o = rv.vec(FV_Z, o);
+          w_o[off] = cadd(__ldcg(w_o + off), y);
+          z_o[off] = cadd(__ldcg(z_o + off), y);
         } else {
-          a.wout[off] = csub(__ldcg(a.z + off), y);  // EPI_IMS on the final z
+          rv.vec(FV_WOUT, o)[off] = csub(__ldcg(rv.vec(FV_Z, o) + off), y);  // EPI_IMS on the final z
         }
       }
     }
     __syncthreads();
     if (threadIdx.x == 0 && ft.phase != 3) {
-      // one completion per (tile, written block).  One gpu-scope fence by the
-      // signalling thread publishes the epilogue stores the barrier ordered
-      // before it (cumulativity), instead of a fence per storing lane.
-      __threadfence();
+      // one completion per (tile, written block).  One fence by the signalling
+      // thread publishes the epilogue stores the barrier ordered before it
+      // (cumulativity), instead of a fence per storing lane.
+      rv.fence();
       const int r0 = max(it.rlo, s0 * kRowTile), r1 = min(it.rhi, (s0 + RT) * kRowTile);
-      for (int f = r0 / n; f * n < r1; ++f) atomicAdd(a.done + sb.tgt[f] / n, 1);
+      for (int f = r0 / n; f * n < r1; ++f) atomicAdd(rv.done(sb.tgt[f] / n), 1);
     }
   }
 }
@@ -288,8 +339,10 @@ __device__ __forceinline__ void consumers_sync(int nthreads) {
 
 constexpr int kChunk = 32 * kRowTile;  // elements of one 32-column chunk of a strip
 
-template <int NW, int S>
+template <int NW, int S, bool MR>
 __global__ void __launch_bounds__((NW + 1) * 32, 1) k_bsp_tma(FusedArgs a) {
+  const RankView<MR> rv(a);
+  const int cr = rv.cr;
   extern __shared__ __align__(128) double2 smt[];
   double2* stage = smt;                // S x kChunk
   double2* xs = stage + S * kChunk;    // maxK
@@ -311,9 +364,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_bsp_tma(FusedArgs a) {
         const int d = q & 1;
         mbar_wait(&dempty[d], ((q >> 1) & 1) ^ 1);
         TileDesc td;
-        td.t = atomicAdd(a.ticket, 1);
-        if (td.t < a.ntiles) {
-          const FusedTile ft = a.tiles[td.t];
+        td.t = atomicAdd(rv.ticket(), 1);
+        if (td.t < rv.ntiles()) {
+          const FusedTile ft = rv.tiles()[td.t];
           const DevItem it = a.items[ft.item];
           const DevSub sb = a.subs[it.s];
           td.K = sb.k * a.n;
@@ -325,7 +378,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_bsp_tma(FusedArgs a) {
         }
         desc[d] = td;
         mbar_arrive(&dfull[d]);
-        if (td.t >= a.ntiles) break;
+        if (td.t >= rv.ntiles()) break;
         const int nch = (td.K + 31) / 32;
         const double2* src = a.T + td.map_off;
         for (int ch = 0; ch < nch; ++ch, ++g) {
@@ -349,10 +402,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_bsp_tma(FusedArgs a) {
     const TileDesc td = desc[d];
     __syncwarp();
     if (lane == 0) mbar_arrive(&dempty[d]);
-    if (td.t >= a.ntiles) break;
+    if (td.t >= rv.ntiles()) break;
     for (int i = threadIdx.x; i < td.ndep; i += NT) {
       const FusedDep dp = a.deps[td.dep0 + i];
-      const volatile int* p = a.done + dp.block;
+      const volatile int* p = rv.done(dp.block);
       while (*p < dp.count) __nanosleep(32);
     }
     __threadfence();
@@ -363,23 +416,27 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_bsp_tma(FusedArgs a) {
     const bool erow_ok = warp == 0 && erow >= td.rlo && erow < td.rhi;
     const int ef = erow / n;
     const long long eoff = erow_ok ? (long long)td.tgt[ef] + (erow - ef * n) : 0;
+    const int eo = erow_ok ? rv.owner(td.tgt[ef] / n) : cr;  // the output block's rank
     double2 e1 = make_double2(0, 0), e2 = make_double2(0, 0);
     if (erow_ok) {
-      const double2* zbase = (td.rmask >> (4 + ef)) & 1 ? a.r : a.zL;  // zL not yet written: r
+      const double2* r_o = rv.vec(FV_R, eo);
+      const double2* zbase = (td.rmask >> (4 + ef)) & 1 ? r_o : rv.vec(FV_ZL, eo);  // zL not yet written: r
       if (td.phase == 0) e1 = __ldcg(zbase + eoff);
-      else if (td.phase == 1) { e1 = __ldcg(zbase + eoff); e2 = a.r[eoff]; }
-      else if (td.phase == 2) { e1 = __ldcg(a.w + eoff); e2 = __ldcg(a.z + eoff); }
-      else e1 = __ldcg(a.z + eoff);
+      else if (td.phase == 1) { e1 = __ldcg(zbase + eoff); e2 = r_o[eoff]; }
+      else if (td.phase == 2) { e1 = __ldcg(rv.vec(FV_W, eo) + eoff); e2 = __ldcg(rv.vec(FV_Z, eo) + eoff); }
+      else e1 = __ldcg(rv.vec(FV_Z, eo) + eoff);
     }
     const int K = td.K;
+    // the slab (this subdomain's incoming blocks) lives on this CTA's rank
     const double2* src;
-    if (td.phase == 0) src = td.alt ? a.r : a.zL;
-    else if (td.phase == 1) src = a.zL;
-    else if (td.phase == 2) src = td.alt ? a.rp : a.w;
-    else src = a.z;  // phase 3: (I - S) z
+    if (td.phase == 0) src = rv.vec(td.alt ? FV_R : FV_ZL, cr);
+    else if (td.phase == 1) src = rv.vec(FV_ZL, cr);
+    else if (td.phase == 2) src = rv.vec(td.alt ? FV_RP : FV_W, cr);
+    else src = rv.vec(FV_Z, cr);  // phase 3: (I - S) z
     src += td.in_off;
+    const double2* rsrc = rv.vec(FV_R, cr) + td.in_off;
     // zL starts as r without a copy: faces of zL not yet written read r
-    for (int i = threadIdx.x; i < K; i += NT) xs[i] = __ldcg(((td.rmask >> (i / n)) & 1 ? a.r + td.in_off : src) + i);
+    for (int i = threadIdx.x; i < K; i += NT) xs[i] = __ldcg(((td.rmask >> (i / n)) & 1 ? rsrc : src) + i);
     consumers_sync(NT);
     double2 a0 = make_double2(0, 0), a1 = make_double2(0, 0);
     const int nch = (K + 31) / 32;
@@ -407,25 +464,25 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_bsp_tma(FusedArgs a) {
       if (erow_ok) {
         const long long off = eoff;
         if (td.phase == 0) {
-          a.zL[off] = cadd(e1, y);
+          rv.vec(FV_ZL, eo)[off] = cadd(e1, y);
         } else if (td.phase == 1) {
           const double2 v = csub(e2, csub(e1, y));  // r - (zL - S zL)
-          a.rp[off] = v;
-          a.w[off] = v;
-          a.z[off] = cadd(e1, v);
+          rv.vec(FV_RP, eo)[off] = v;
+          rv.vec(FV_W, eo)[off] = v;
+          rv.vec(FV_Z, eo)[off] = cadd(e1, v);
         } else if (td.phase == 2) {
-          a.w[off] = cadd(e1, y);
-          a.z[off] = cadd(e2, y);
+          rv.vec(FV_W, eo)[off] = cadd(e1, y);
+          rv.vec(FV_Z, eo)[off] = cadd(e2, y);
         } else {
-          a.wout[off] = csub(e1, y);  // EPI_IMS on the final z
+          rv.vec(FV_WOUT, eo)[off] = csub(e1, y);  // EPI_IMS on the final z
         }
       }
     }
     consumers_sync(NT);
     if (threadIdx.x == 0 && td.phase != 3) {  // nothing waits on the (I - S) z tiles
-      __threadfence();  // publishes the epilogue stores ordered before it by the barrier
+      rv.fence();  // publishes the epilogue stores ordered before it by the barrier
       const int r0 = max(td.rlo, td.row0), r1 = min(td.rhi, td.row0 + kRowTile);
-      for (int f = r0 / n; f * n < r1; ++f) atomicAdd(a.done + td.tgt[f] / n, 1);
+      for (int f = r0 / n; f * n < r1; ++f) atomicAdd(rv.done(td.tgt[f] / n), 1);
     }
   }
 }
@@ -571,8 +628,8 @@ void launch_seam_add(Ctx& c, int dir, double2* z, const double2* r, int R) {
 }
 
 cudaError_t set_step_smem_limit() {
-  cudaFuncSetAttribute(k_bsp_fused<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  cudaFuncSetAttribute(k_bsp_fused<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_bsp_fused<8, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_bsp_fused<8, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   return cudaFuncSetAttribute(k_step1<kSumWarps>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               200 * 1024);
 }
@@ -587,14 +644,14 @@ cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double
     constexpr int NWt = kSumWarps, ST = 5;
     static bool attr = false;
     if (!attr) {
-      cudaFuncSetAttribute(k_bsp_tma<NWt, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      cudaFuncSetAttribute(k_bsp_tma<NWt, ST, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
       attr = true;
     }
     const size_t smem = (size_t)(ST * kChunk + f.maxK + NWt * 32) * sizeof(double2);
     static int per_sm = 0;
     static size_t per_sm_smem = 0;
     if (per_sm == 0 || per_sm_smem != smem) {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsp_tma<NWt, ST>, (NWt + 1) * 32, smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsp_tma<NWt, ST, false>, (NWt + 1) * 32, smem);
       per_sm = std::max(1, per_sm);
       per_sm_smem = smem;
     }
@@ -607,7 +664,7 @@ cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double
     a.ntiles = f.ntiles; a.n = c.n; a.maxK = f.maxK;
     const int grid = std::max(1, std::min(f.ntiles, per_sm * c.num_sms));
     c.launches++;
-    k_bsp_tma<NWt, ST><<<grid, (NWt + 1) * 32, smem, c.stream>>>(a);
+    k_bsp_tma<NWt, ST, false><<<grid, (NWt + 1) * 32, smem, c.stream>>>(a);
     return cudaGetLastError();
   }
   static_assert(kSumWarps == 8, "register-streaming fused kernels are instantiated for 8 warps");
@@ -617,8 +674,8 @@ cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double
   static int per_sm[3] = {0, 0, 0};
   static size_t per_sm_smem[3] = {0, 0, 0};
   if (per_sm[var] == 0 || per_sm_smem[var] != smem) {
-    if (var == 2) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[var], k_bsp_fused<8, 2>, 256, smem);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[var], k_bsp_fused<8, 1>, 256, smem);
+    if (var == 2) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[var], k_bsp_fused<8, 2, false>, 256, smem);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[var], k_bsp_fused<8, 1, false>, 256, smem);
     per_sm_smem[var] = smem;
     if (per_sm[var] < 1) per_sm[var] = 1;
   }
@@ -631,8 +688,63 @@ cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double
   a.ntiles = f.ntiles; a.n = c.n; a.maxK = f.maxK;
   const int grid = std::max(1, std::min(f.ntiles, per_sm[var] * c.num_sms));
   c.launches++;
-  if (var == 2) k_bsp_fused<8, 2><<<grid, 256, smem, c.stream>>>(a);
-  else k_bsp_fused<8, 1><<<grid, 256, smem, c.stream>>>(a);
+  if (var == 2) k_bsp_fused<8, 2, false><<<grid, 256, smem, c.stream>>>(a);
+  else k_bsp_fused<8, 1, false><<<grid, 256, smem, c.stream>>>(a);
+  return cudaGetLastError();
+}
+
+// out[block b] = the copy of block b held by its owner rank (emulated ranks).
+struct RankBases {
+  const double2* p[kMaxRanks];
+};
+__global__ void k_gather_blocks(double2* out, RankBases src, const int* __restrict__ blk_rank, int n, long long L) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < L; i += (long long)gridDim.x * blockDim.x)
+    out[i] = src.p[blk_rank[i / n]][i];
+}
+
+void launch_gather_blocks(Ctx& c, double2* out, const double2* const* src, int G, const int* blk_rank, long long L) {
+  RankBases b;
+  for (int g = 0; g < kMaxRanks; ++g) b.p[g] = g < G ? src[g] : nullptr;
+  c.launches++;
+  k_gather_blocks<<<grid_for(L, c.num_sms), 256, 0, c.stream>>>(out, b, blk_rank, c.n, L);
+}
+
+// The fused apply over row-band ranks: `mr` carries every rank's vectors,
+// counters and tile list.  Emulation (mr.self < 0): one launch, CTA c works
+// for rank c % G.  (The caller zeroes the counters.)
+cudaError_t launch_bsp_fused_ranks(Ctx& c, const DevFused& f, const MultiRankArgs& mr) {
+  FusedArgs a;
+  a.tiles = nullptr; a.items = f.items; a.deps = f.deps; a.subs = c.dsubs; a.T = c.T;
+  a.r = nullptr; a.zL = a.rp = a.w = a.z = a.wout = nullptr;
+  a.done = nullptr; a.ticket = nullptr;
+  a.ntiles = 0; a.n = c.n; a.maxK = f.maxK;
+  a.mr = mr;
+  c.launches++;
+  const int G = mr.self < 0 ? mr.G : 1;
+  if (f.tma) {
+    constexpr int NWt = kSumWarps, ST = 5;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_bsp_tma<NWt, ST, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      attr = true;
+    }
+    const size_t smem = (size_t)(ST * kChunk + f.maxK + NWt * 32) * sizeof(double2);
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsp_tma<NWt, ST, true>, (NWt + 1) * 32, smem);
+    const int grid = std::max(G, (std::max(1, per_sm) * c.num_sms / G) * G);
+    k_bsp_tma<NWt, ST, true><<<grid, (NWt + 1) * 32, smem, c.stream>>>(a);
+    return cudaGetLastError();
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_bsp_fused<8, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  const size_t smem = (size_t)(f.maxK + 8 * 32) * sizeof(double2);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsp_fused<8, 1, true>, 256, smem);
+  const int grid = std::max(G, (std::max(1, per_sm) * c.num_sms / G) * G);
+  k_bsp_fused<8, 1, true><<<grid, 256, smem, c.stream>>>(a);
   return cudaGetLastError();
 }
 

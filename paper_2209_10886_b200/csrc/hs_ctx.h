@@ -168,6 +168,34 @@ struct FusedMmaArgs {
   int ntasks, n, R;
 };
 
+// Row-band ranks of the fused apply (multi-rank kernel instantiations): every
+// block -- its vectors and its completion counter -- lives on its owner rank.
+constexpr int kMaxRanks = 8;
+enum FusedVec { FV_R = 0, FV_ZL, FV_RP, FV_W, FV_Z, FV_WOUT, FV_N };
+struct MultiRankArgs {
+  int G = 1, self = 0;                 // ranks; self >= 0: this GPU's rank, < 0: CTA c emulates rank c % G
+  const int* blk_rank = nullptr;       // block -> owner rank
+  double2* v[FV_N][kMaxRanks] = {};    // per rank: r, zL, rp, w, z, wout
+  int* done[kMaxRanks] = {};
+  int* ticket[kMaxRanks] = {};
+  const FusedTile* tiles[kMaxRanks] = {};
+  int ntiles[kMaxRanks] = {};
+};
+
+// Emulated row bands on one GPU (hs_set_emulated_ranks): per-rank vectors,
+// counters and tile lists of the fused plan, for testing the multi-rank
+// kernels against the single-rank result.
+struct EmuRanks {
+  int G = 1;
+  bool built = false;
+  std::vector<int> sub_rank;             // subdomain -> rank
+  int* blk_rank = nullptr;               // device: block -> rank
+  FusedTile* tiles[kMaxRanks] = {};      // device: per-rank tile lists (plan order)
+  int ntiles[kMaxRanks] = {};
+  double2* buf = nullptr;                // device: G x (r, zL, rp, w, z) full-length vectors
+  int* counters = nullptr;               // device: G x (npairs done + 1 ticket)
+};
+
 // One distinct subdomain operator (Dirichlet mask) and its factor.
 struct OpClass {
   std::vector<uint8_t> mask;          // n*n, 1 = Dirichlet cell
@@ -209,6 +237,7 @@ struct Ctx {
   DevStep full;
   DevFused fused;        // BSP apply as one dataflow launch (1 RHS, per-subdomain maps, 1 rank)
   DevFused fused_ims;    // the same followed by (I - S) z: GMRES's A M v in one launch
+  EmuRanks emu;          // emulated row-band ranks for the fused apply (tests)
   DevFusedMma fused_mma; // the same on the DMMA contraction (R RHS or shared maps)
   int fused_mode = 1;    // 1: use the fused kernel when applicable, 0: one launch per step
   std::vector<std::vector<int>> seam_blocks;  // [dir] blocks of seam groups (literal mode)

@@ -26,6 +26,8 @@ void launch_vec(Ctx& c, int op, long long len, double2* o1, double2* o2, const d
                 const double2* b);
 void launch_seam_add(Ctx& c, int dir, double2* z, const double2* r, int R);
 cudaError_t set_step_smem_limit();
+cudaError_t launch_bsp_fused_ranks(Ctx& c, const DevFused& f, const MultiRankArgs& mr);
+void launch_gather_blocks(Ctx& c, double2* out, const double2* const* src, int G, const int* blk_rank, long long L);
 // wout != null: the plan's phase-3 tiles write (I - S) z there (GMRES A M v in one launch)
 cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double2* zL, double2* rp,
                              double2* w, double2* z, double2* wout = nullptr);

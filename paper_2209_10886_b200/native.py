@@ -64,6 +64,7 @@ _SIGS = {
     "hs_kernel_stats": (_I, [_P, C.POINTER(C.c_int64), C.POINTER(_D), C.POINTER(_D), C.POINTER(_D), _I]),
     "hs_set_map_mode": (_I, [_P, _I]),
     "hs_set_gmres_mode": (_I, [_P, _I]),
+    "hs_set_emulated_ranks": (_I, [_P, _I]),
     "hs_set_fused": (_I, [_P, _I]),
     "hs_memory": (_I, [_P, C.POINTER(C.c_int64)]),
     "hs_launch_count": (_I, [_P, C.POINTER(C.c_int64)]),

@@ -119,3 +119,25 @@ def test_fused_variants_bitwise(env):
     out = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT], cwd=root, env=dict(os.environ, **env),
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
+
+
+@pytest.mark.parametrize("name,c,blocks,ranks", [("small_6x3", small_case(6, 3, 16), 5, (2, 3)),
+                                                 ("small_4x4_n160", small_case(4, 4, 160), None, (2, 4)),
+                                                 ("cfg2", CONFIGS[2], 4, (2, 4, 8)), ("cfg3", CONFIGS[3], 4, (2, 8))])
+def test_emulated_row_band_ranks_bitwise(name, c, blocks, ranks):
+    """The multi-rank fused kernels (every block on its owner rank, output
+    blocks and their counters reached in the owner's buffers -- the
+    peer-memory protocol of the multi-GPU path) emulated on one GPU: bitwise
+    the single-rank apply, for TMA-staged (maps <= 512 columns) and
+    register-streaming (n = 160: 640 columns) kernels."""
+    spec, part = product_problem(c)
+    s = GpuInterfaceSystem(spec, part, sweep=SweepConfig(blocks=blocks))
+    g = cvec(31, s.layout.size)
+    ref = s.bsp_apply(g)
+    for G in ranks:
+        s.ctx.call("hs_set_emulated_ranks", G)
+        for _ in range(2):
+            z = s.bsp_apply(g)
+            assert np.array_equal(z, ref), (name, G, relerr(z, ref))
+    s.ctx.call("hs_set_emulated_ranks", 1)
+    assert np.array_equal(s.bsp_apply(g), ref)
