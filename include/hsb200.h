@@ -162,8 +162,13 @@ int hs_set_emulated_ranks(hs_ctx* ctx, int ranks);
 
 /* Bit mask.  Bit 0 (default on): a BSP apply with one RHS on per-subdomain
  * maps runs as one persistent dataflow launch (per-block completion counters
- * instead of one launch per step; bitwise identical results).  Bit 1 (default
- * off): the same for the DMMA contraction (R RHS or shared maps). */
+ * instead of one launch per step).  Bit 2 (default off) selects the per-step
+ * plan for it -- the step sequence's arithmetic, bitwise identical to bit 0
+ * clear; otherwise the map-once plan computes the same z with every map row
+ * read about once per apply (the intermediate residual vanishes inside the
+ * forward windows and shares the backward steps' map reads),
+ * equal to the step sequence to rounding.  Bit 1 (default off): the fused
+ * launch for the DMMA contraction (R RHS or shared maps). */
 int hs_set_fused(hs_ctx* ctx, int mask);
 
 /* ---- introspection (plan-only contexts too) ---------------------------- */

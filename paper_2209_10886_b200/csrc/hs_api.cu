@@ -403,8 +403,25 @@ void free_fused(Ctx* c) {
 // per-block completion counts it waits for (all earlier tile-writes to the
 // blocks it reads or read-modify-writes; counts taken before its own step,
 // since the tiles of one step are independent).  ims: append the (I - S) z
-// step as phase 3 (GMRES's A M v in one launch): its tiles wait for the final
-// z of the blocks they read and of their output rows, and signal nothing.
+// step (GMRES's A M v in one launch): its tiles wait for the final z of the
+// blocks they read and of their output rows, and signal nothing.
+//
+// Two plans (FusedTile phases, hs_ctx.h):
+//  * per-step (c->fused_mode & 4): forward, full residual, backward, full
+//    (I - S) z -- the k_step1 arithmetic in the same order, bitwise equal.
+//  * map-once (default): the same z (and (I - S) z) with each map row read
+//    about once.  Within a forward window the substitution is exact, so
+//    r' = r - (I - S) zL vanishes on every W/S block whose writer read the
+//    final zL of its slab (every forward writer but the window starts at
+//    seams, whose residual rows are recomputed: phase 1 "a").  On N/E blocks
+//    r' = T_low zL, which shares the map rows of the backward step: both
+//    products come from one read (phase 4), except for writers whose output
+//    feeds a backward window start (phase 1 "b" early + phase 2 late).  With
+//    (I - S) z = (r - r') + (I - S) w and w the backward state, (I - S) z is
+//    r on N/E blocks whose writer read its final w, and r - T_up w on W/S
+//    blocks: phase 4 / 2 tiles read the whole map (upper rows on the final w)
+//    when their slab is final; the backward window starts (slab read from
+//    rp, final w later) and subdomains without lower faces get phase 5.
 int build_fused(Ctx* c, bool ims) {
   DevFused& f = ims ? c->fused_ims : c->fused;
   const Plan& P = c->plan;
@@ -413,34 +430,49 @@ int build_fused(Ctx* c, bool ims) {
   std::vector<FusedTile> tiles;
   std::vector<FusedDep> deps;
   std::vector<int> written(P.npairs, 0), zl_written(P.npairs, 0);
+  f.map_once = !(c->fused_mode & 4);
   // tile shape: one 32-row strip, kSumWarps warps splitting its columns
   // (2 strips per tile -- 80 registers, half the occupancy -- was slower at
-  // cfg3; HS_FUSED_RT=2 selects it).
+  // cfg3; HS_FUSED_RT=2 selects it, per-step plan only).
   f.rt = 1;
   f.nw = kSumWarps;
+  f.nv = 1;
   if (const char* e = getenv("HS_FUSED_RT")) f.rt = std::max(1, std::min(2, atoi(e)));
+  if (f.map_once) f.rt = 1;
   // TMA-staged maps (k_bsp_tma) up to 512 map columns, register streaming beyond
   // (measured on B200, ms per apply, TMA vs streaming: cfg1 0.044/0.046, cfg2
   // 0.091/0.094, cfg3 0.334/0.355, cfg5 2.37/2.25).  HS_FUSED_TMA=0/1 overrides.
   f.tma = f.rt == 1;  // decided on maxK below
+  f.bytes = 0;
   const int TR = kRowTile * f.rt;
-  auto add = [&](const DevStep& st, int phase) {
+  struct VItem {
+    Item it;
+    int phase, flags;
+  };
+  // one virtual step: tiles of independent items (counts taken before the step)
+  auto add = [&](const std::vector<VItem>& step) {
     std::vector<int> inc;
-    for (const Item& it : st.host.items) {
+    for (const VItem& v : step) {
+      const Item& it = v.it;
+      const int phase = v.phase;
       const SubPlan& sp = P.subs[it.s];
       DevItem d;
       d.s = it.s; d.rlo = it.rlo; d.rhi = it.rhi; d.alt = it.alt;
       for (int q = 0; q < 4; ++q) d.slot[q] = -1;
       const int idx = (int)items.size();
       items.push_back(d);
-      f.maxK = std::max(f.maxK, sp.k * n);
+      const int K = sp.k * n;
+      f.maxK = std::max(f.maxK, K);
+      const int nv = phase == 4 ? 2 : 1;
+      f.nv = std::max(f.nv, nv);
+      f.bytes += 16.0 * ((double)(it.rhi - it.rlo) * K + nv * K + 2.0 * (it.rhi - it.rlo));
       for (int tl = it.rlo / TR; tl * TR < it.rhi; ++tl) {
         FusedTile ft;
-        ft.item = idx; ft.tile = tl; ft.phase = phase;
+        ft.item = idx; ft.tile = tl; ft.phase = phase; ft.flags = v.flags;
         ft.dep0 = (int)deps.size(); ft.ndep = 0;
         ft.rmask = 0;
-        if (phase <= 1) {  // zL is never initialised: blocks without a forward write read r
-          if (phase == 1 || !it.alt)
+        if (phase <= 1 || phase == 4) {  // zL is never initialised: blocks without a forward write read r
+          if (phase != 0 || !it.alt)
             for (int q = 0; q < sp.k; ++q)
               if (zl_written[sp.first_block + q] == 0) ft.rmask |= 1 << q;
           for (int q = 0; q < sp.k; ++q)
@@ -451,7 +483,9 @@ int build_fused(Ctx* c, bool ims) {
         const int r0 = std::max(it.rlo, tl * TR), r1 = std::min(it.rhi, (tl + 1) * TR);
         for (int q = r0 / n; q * n < r1; ++q) {
           blocks.insert(sp.tgt_block[q]);
-          if (phase != 3) inc.push_back(sp.tgt_block[q]);
+          // phases 2 and 4 complete their lower-face blocks only (upper rows write wout)
+          const bool signals = phase <= 1 || ((phase == 2 || phase == 4) && q < sp.nlower);
+          if (signals) inc.push_back(sp.tgt_block[q]);
         }
         for (int b : blocks)
           if (written[b] > 0) {
@@ -461,16 +495,82 @@ int build_fused(Ctx* c, bool ims) {
         tiles.push_back(ft);
       }
     }
-    for (int b : inc) {
-      written[b]++;
-      if (phase == 0) zl_written[b]++;
-    }
-    f.bytes += st.bytes_per_rhs_map + st.bytes_per_rhs_vec;
+    for (int b : inc) written[b]++;
+    return inc;
   };
-  for (auto& st : c->fwd) add(st, 0);
-  add(c->full, 1);
-  for (auto& st : c->bwd) add(st, 2);
-  if (ims) add(c->full, 3);
+  auto vstep = [](const DevStep& st, int phase, int flags) {
+    std::vector<VItem> v;
+    for (const Item& it : st.host.items) v.push_back({it, phase, flags});
+    return v;
+  };
+  auto mark_zl = [&](const std::vector<int>& inc) {
+    for (int b : inc) zl_written[b]++;
+  };
+  if (!f.map_once) {
+    for (auto& st : c->fwd) mark_zl(add(vstep(st, 0, 0)));
+    add(vstep(c->full, 1, 0));
+    for (auto& st : c->bwd) add(vstep(st, 2, 0));
+    if (ims) add(vstep(c->full, 3, 0));
+  } else {
+    // backward window starts below the top group (their slab is read from rp)
+    std::set<int> bstart;
+    for (auto& w : P.win_upper)
+      if (w.second < P.ng + 1) bstart.insert(w.second);
+    std::vector<VItem> resid;
+    for (auto& st : c->fwd) {
+      std::vector<VItem> step;
+      for (const Item& it : st.host.items) {
+        const bool seam = it.alt && P.subs[it.s].nlower > 0;  // slab zL != r: residual rows recomputed
+        step.push_back({it, 0, seam ? 0 : FT_ZERO});
+        if (seam) {
+          Item r = it;
+          r.alt = 0;
+          resid.push_back({r, 1, 0});
+        }
+      }
+      mark_zl(add(step));
+    }
+    std::vector<bool> has_bwd(P.nsub, false), late(P.nsub, false);
+    std::vector<std::vector<VItem>> bsteps;
+    for (auto& st : c->bwd) {
+      std::vector<VItem> step;
+      for (const Item& it : st.host.items) {
+        const SubPlan& sp = P.subs[it.s];
+        has_bwd[it.s] = true;
+        const bool final_slab = !it.alt || sp.k == sp.nlower;  // reads its final w
+        if (!final_slab) late[it.s] = true;
+        Item b = it;
+        int flags = 0;
+        if (ims && final_slab) {
+          flags = FT_WOUT;
+          b.rhi = sp.k * n;  // upper rows too: wout = r - T_up w
+        }
+        if (bstart.count(sp.group - 1)) {  // feeds a backward window start: residual early
+          Item r = it;
+          r.alt = 0;
+          resid.push_back({r, 1, 0});
+          step.push_back({b, 2, flags});
+        } else {
+          step.push_back({b, 4, flags});
+        }
+      }
+      bsteps.push_back(step);
+    }
+    add(resid);
+    for (auto& st : bsteps) add(st);
+    if (ims) {
+      std::vector<VItem> lt;
+      for (int s = 0; s < P.nsub; ++s) {
+        const SubPlan& sp = P.subs[s];
+        if (late[s] || (!has_bwd[s] && sp.k > sp.nlower)) {
+          Item it;
+          it.s = s; it.rlo = 0; it.rhi = sp.k * n; it.alt = 0;
+          lt.push_back({it, 5, 0});
+        }
+      }
+      add(lt);
+    }
+  }
   f.tma = f.tma && f.maxK <= 512;
   if (const char* e = getenv("HS_FUSED_TMA")) f.tma = atoi(e) != 0 && f.rt == 1;
   if (upload(c, &f.items, items) || upload(c, &f.tiles, tiles) || upload(c, &f.deps, deps)) return -1;
@@ -971,6 +1071,7 @@ int hs_create(hs_ctx** out, int device, int n1, int n2, int n, double h, double 
       const SubPlan& sp = x->plan.subs[s];
       DevSub d;
       d.k = sp.k;
+      d.nlow = sp.nlower;
       d.in_off = sp.first_block * n;
       for (int q = 0; q < 4; ++q) d.tgt[q] = q < sp.k ? sp.tgt_block[q] * n : -1;
       const long long K = (long long)sp.k * n;
@@ -1717,7 +1818,11 @@ int hs_stream(hs_ctx* c, uint64_t* s) {
 
 int hs_set_fused(hs_ctx* c, int mask) {
   if (!c) return fail(nullptr, 1, "null context");
-  if (mask < 0 || mask > 3) return fail(c, 1, "fused mask must be 0..3");
+  if (mask < 0 || mask > 7) return fail(c, 1, "fused mask must be 0..7");
+  if ((mask ^ c->fused_mode) & 4) {  // plan kind changed: rebuild the fused plans
+    free_fused(c);
+    free_emu(c);
+  }
   c->fused_mode = mask;
   return 0;
 }

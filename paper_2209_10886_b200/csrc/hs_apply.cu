@@ -125,6 +125,7 @@ struct FusedArgs {
   int* done;
   int* ticket;
   int ntiles, n, maxK;
+  int nv;  // slab vectors per tile at most (shared-memory layout)
   MultiRankArgs mr;
 };
 
@@ -159,10 +160,162 @@ struct RankView {
   }
 };
 
+// Epilogue operands of one output row (phase table in hs_ctx.h), fetched
+// before the tile's products are needed: o = the output block's rank, off =
+// element offset, low = the row feeds a lower neighbour (W/S face), zr = zL
+// of the output face not yet written (read r).
+template <bool MR>
+__device__ __forceinline__ void epi_fetch(const RankView<MR>& rv, int phase, int flags, bool low, bool zr, int o,
+                                          long long off, double2& e1, double2& e2, double2& e3) {
+  const double2* r_o = rv.vec(FV_R, o);
+  const double2* zb = zr ? r_o : rv.vec(FV_ZL, o);
+  switch (phase) {
+    case 0: e1 = __ldcg(zb + off); break;
+    case 1: e1 = __ldcg(zb + off); e2 = r_o[off]; break;
+    case 2:
+      if (low) { e1 = __ldcg(rv.vec(FV_W, o) + off); e2 = __ldcg(rv.vec(FV_Z, o) + off); }
+      if (flags & FT_WOUT) e3 = r_o[off];
+      break;
+    case 3: e1 = __ldcg(rv.vec(FV_Z, o) + off); break;
+    case 4:
+      if (low) e1 = __ldcg(zb + off);
+      e2 = r_o[off];
+      break;
+    default:
+      e1 = r_o[off];
+      if (low) { e2 = __ldcg(rv.vec(FV_RP, o) + off); e3 = __ldcg(rv.vec(FV_W, o) + off); }
+  }
+}
+
+template <bool MR>
+__device__ __forceinline__ void epi_store(const RankView<MR>& rv, int phase, int flags, bool low, int o, long long off,
+                                          double2 y1, double2 y2, double2 e1, double2 e2, double2 e3) {
+  const double2 zero = make_double2(0, 0);
+  switch (phase) {
+    case 0: {
+      const double2 zn = cadd(e1, y1);
+      rv.vec(FV_ZL, o)[off] = zn;
+      if (flags & FT_ZERO) {  // r' = 0 exactly: the window's substitution was exact here
+        rv.vec(FV_RP, o)[off] = zero;
+        rv.vec(FV_W, o)[off] = zero;
+        rv.vec(FV_Z, o)[off] = zn;
+      }
+      break;
+    }
+    case 1: {
+      const double2 v = csub(e2, csub(e1, y1));  // r - (zL - S zL)
+      rv.vec(FV_RP, o)[off] = v;
+      rv.vec(FV_W, o)[off] = v;
+      rv.vec(FV_Z, o)[off] = cadd(e1, v);
+      break;
+    }
+    case 2:
+      if (low) {
+        rv.vec(FV_W, o)[off] = cadd(e1, y1);
+        rv.vec(FV_Z, o)[off] = cadd(e2, y1);
+        if (flags & FT_WOUT) rv.vec(FV_WOUT, o)[off] = e3;
+      } else {
+        rv.vec(FV_WOUT, o)[off] = csub(e3, y1);
+      }
+      break;
+    case 3: rv.vec(FV_WOUT, o)[off] = csub(e1, y1); break;  // EPI_IMS on the final z
+    case 4:
+      if (low) {
+        const double2 v = csub(e2, csub(e1, y1));
+        rv.vec(FV_RP, o)[off] = v;
+        rv.vec(FV_W, o)[off] = cadd(v, y2);
+        rv.vec(FV_Z, o)[off] = cadd(cadd(e1, v), y2);
+        if (flags & FT_WOUT) rv.vec(FV_WOUT, o)[off] = e2;
+      } else {
+        rv.vec(FV_WOUT, o)[off] = csub(e2, y2);
+      }
+      break;
+    default:
+      rv.vec(FV_WOUT, o)[off] = low ? cadd(csub(e1, e2), csub(e3, y1)) : csub(e1, y1);
+  }
+}
+
+// Slab sources of a tile: X1 (and X2 for phase 4) on this CTA's rank.
+template <bool MR>
+__device__ __forceinline__ void slab_srcs(const RankView<MR>& rv, int phase, int alt, int cr, const double2*& x1,
+                                          const double2*& x2) {
+  x2 = nullptr;
+  switch (phase) {
+    case 0: x1 = rv.vec(alt ? FV_R : FV_ZL, cr); break;
+    case 1: x1 = rv.vec(FV_ZL, cr); break;
+    case 2: x1 = rv.vec(alt ? FV_RP : FV_W, cr); break;
+    case 3: x1 = rv.vec(FV_Z, cr); break;
+    case 4: x1 = rv.vec(FV_ZL, cr); x2 = rv.vec(alt ? FV_RP : FV_W, cr); break;
+    default: x1 = rv.vec(FV_W, cr);
+  }
+}
+
+// Signal the blocks a tile completed (phases 0-2 and 4; lower faces only for
+// phases 2 and 4, whose upper rows write wout).  One fence by the signalling
+// thread publishes the epilogue stores the barrier ordered before it
+// (cumulativity), instead of a fence per storing lane.
+template <bool MR>
+__device__ __forceinline__ void tile_signal(const RankView<MR>& rv, int phase, int r0, int r1, int n, int nlow,
+                                            const int* tgt) {
+  if (phase == 3 || phase == 5) return;
+  rv.fence();
+  for (int f = r0 / n; f * n < r1; ++f)
+    if (phase <= 1 || f < nlow) atomicAdd(rv.done(tgt[f] / n), 1);
+}
+
+// Register-streaming contraction of RT strips with NV slab vectors (xs,
+// xs + K); column c into warp (c % 32) / (32 / NW), accumulator c & 1.
+template <int NW, int RT, int NV>
+__device__ __forceinline__ void contract_regs(const double2* __restrict__ Tt, const double2* xs, int K, int nstrip,
+                                              int s0, int warp, double2 (&acc)[RT][NV][2]) {
+  constexpr int CPW = 32 / NW;
+  constexpr int U = 8 / CPW;  // chunks per unrolled batch: 8 loads in flight per strip
+#pragma unroll
+  for (int q = 0; q < RT; ++q)
+#pragma unroll
+    for (int v = 0; v < NV; ++v) acc[q][v][0] = acc[q][v][1] = make_double2(0, 0);
+  const int nch = (K + 31) / 32;
+  int ch = 0;
+  for (; ch + U <= nch && (ch + U) * 32 <= K; ch += U) {
+#pragma unroll
+    for (int q = 0; q < RT; ++q) {
+      if (s0 + q >= nstrip) break;
+      const double2* Tq = Tt + (long long)q * K * kRowTile;
+      double2 tv[U][CPW];
+#pragma unroll
+      for (int v = 0; v < U; ++v)
+#pragma unroll
+        for (int u = 0; u < CPW; ++u) tv[v][u] = ld_stream(Tq + (long long)((ch + v) * 32 + warp * CPW + u) * kRowTile);
+#pragma unroll
+      for (int v = 0; v < U; ++v)
+#pragma unroll
+        for (int u = 0; u < CPW; ++u) {
+          const int col = (ch + v) * 32 + warp * CPW + u;
+#pragma unroll
+          for (int x = 0; x < NV; ++x) cfma(acc[q][x][col & 1], tv[v][u], xs[x * K + col]);
+        }
+    }
+  }
+  for (; ch < nch; ++ch)
+#pragma unroll
+    for (int u = 0; u < CPW; ++u) {
+      const int col = ch * 32 + warp * CPW + u;
+      if (col < K)
+#pragma unroll
+        for (int q = 0; q < RT; ++q)
+          if (s0 + q < nstrip) {
+            const double2 t = ld_stream(Tt + (long long)q * K * kRowTile + (long long)col * kRowTile);
+#pragma unroll
+            for (int x = 0; x < NV; ++x) cfma(acc[q][x][col & 1], t, xs[x * K + col]);
+          }
+    }
+}
+
 // RT = 32-row strips per tile (RT * K ~ 1024 columns-strips keeps the fixed
 // per-tile cost -- ticket, dependency check, slab load, epilogue -- amortised).
-// 6 CTAs of 8 warps per SM (40 registers) for the one-strip form: the map
-// stream needs the bytes in flight (5 CTAs per SM measured ~10 % slower at cfg5)
+// 6 CTAs of 8 warps per SM for the one-strip form: the map stream needs the
+// bytes in flight (5 CTAs per SM measured ~10 % slower at cfg5).  Phase-4
+// tiles (map-once plan, RT = 1) multiply two slab vectors per map read.
 template <int NW, int RT, bool MR>
 __global__ void __launch_bounds__(NW * 32, RT == 1 ? 6 : 1) k_bsp_fused(FusedArgs a) {
   extern __shared__ double2 sm[];
@@ -189,104 +342,61 @@ __global__ void __launch_bounds__(NW * 32, RT == 1 ? 6 : 1) k_bsp_fused(FusedArg
     __threadfence();
     __syncthreads();
     const int K = sb.k * n;
+    const int nv = (RT == 1 && ft.phase == 4) ? 2 : 1;
     // the slab (this subdomain's incoming blocks) lives on this CTA's rank
-    const double2* src;
-    if (ft.phase == 0) src = rv.vec(it.alt ? FV_R : FV_ZL, cr);
-    else if (ft.phase == 1) src = rv.vec(FV_ZL, cr);
-    else if (ft.phase == 2) src = rv.vec(it.alt ? FV_RP : FV_W, cr);
-    else src = rv.vec(FV_Z, cr);  // phase 3: (I - S) z
-    src += sb.in_off;
+    const double2 *x1, *x2;
+    slab_srcs(rv, ft.phase, it.alt, cr, x1, x2);
+    x1 += sb.in_off;
     const double2* rsrc = rv.vec(FV_R, cr) + sb.in_off;
     double2* xs = sm;
-    double2* part = sm + K;
+    double2* part = sm + nv * K;
     // zL starts as r without a copy: faces of zL not yet written read r
     for (int i = threadIdx.x; i < K; i += NW * 32)
-      xs[i] = __ldcg(((ft.rmask >> (i / n)) & 1 ? rsrc : src) + i);
+      xs[i] = __ldcg(((ft.rmask >> (i / n)) & 1 ? rsrc : x1) + i);
+    if (nv == 2)
+      for (int i = threadIdx.x; i < K; i += NW * 32) xs[K + i] = __ldcg(x2 + sb.in_off + i);
     __syncthreads();
     // strips beyond the map (RT > 1 at the last rows) are skipped
     const int nstrip = (K + kRowTile - 1) / kRowTile;
     const int s0 = ft.tile * RT;
     const double2* Tt = a.T + sb.T_off + (long long)s0 * K * kRowTile + lane;
-    // column c belongs to warp (c % 32) / (32 / NW), accumulator c & 1 (k_step1's order)
-    constexpr int CPW = 32 / NW;
-    constexpr int U = 8 / CPW;  // chunks per unrolled batch: 8 loads in flight per strip
-    double2 acc[RT][2];
+    if (RT == 1 && nv == 2) {
+      double2 acc[1][2][2];
+      contract_regs<NW, 1, 2>(Tt, xs, K, nstrip, s0, warp, acc);
 #pragma unroll
-    for (int q = 0; q < RT; ++q) acc[q][0] = acc[q][1] = make_double2(0, 0);
-    const int nch = (K + 31) / 32;
-    int ch = 0;
-    for (; ch + U <= nch && (ch + U) * 32 <= K; ch += U) {
+      for (int x = 0; x < 2; ++x) part[(x * NW + warp) * 32 + lane] = cadd(acc[0][x][0], acc[0][x][1]);
+    } else {
+      double2 acc[RT][1][2];
+      contract_regs<NW, RT, 1>(Tt, xs, K, nstrip, s0, warp, acc);
 #pragma unroll
-      for (int q = 0; q < RT; ++q) {
-        if (s0 + q >= nstrip) break;
-        const double2* Tq = Tt + (long long)q * K * kRowTile;
-        double2 tv[U][CPW];
-#pragma unroll
-        for (int v = 0; v < U; ++v)
-#pragma unroll
-          for (int u = 0; u < CPW; ++u) tv[v][u] = ld_stream(Tq + (long long)((ch + v) * 32 + warp * CPW + u) * kRowTile);
-#pragma unroll
-        for (int v = 0; v < U; ++v)
-#pragma unroll
-          for (int u = 0; u < CPW; ++u) {
-            const int col = (ch + v) * 32 + warp * CPW + u;
-            cfma(acc[q][col & 1], tv[v][u], xs[col]);
-          }
-      }
+      for (int q = 0; q < RT; ++q) part[(q * NW + warp) * 32 + lane] = cadd(acc[q][0][0], acc[q][0][1]);
     }
-    for (; ch < nch; ++ch)
-#pragma unroll
-      for (int u = 0; u < CPW; ++u) {
-        const int col = ch * 32 + warp * CPW + u;
-        if (col < K)
-#pragma unroll
-          for (int q = 0; q < RT; ++q)
-            if (s0 + q < nstrip) cfma(acc[q][col & 1], ld_stream(Tt + (long long)q * K * kRowTile + (long long)col * kRowTile), xs[col]);
-      }
-#pragma unroll
-    for (int q = 0; q < RT; ++q) part[(q * NW + warp) * 32 + lane] = cadd(acc[q][0], acc[q][1]);
     __syncthreads();
     if (warp < RT) {
       // warp q finalises strip q: fixed-order sum over the warps' partials
       const int q = warp;
-      double2 y = part[(q * NW) * 32 + lane];
+      double2 y1 = part[(q * NW) * 32 + lane], y2 = make_double2(0, 0);
 #pragma unroll
-      for (int ww = 1; ww < NW; ++ww) y = cadd(y, part[(q * NW + ww) * 32 + lane]);
+      for (int ww = 1; ww < NW; ++ww) y1 = cadd(y1, part[(q * NW + ww) * 32 + lane]);
+      if (nv == 2) {
+        y2 = part[NW * 32 + lane];
+#pragma unroll
+        for (int ww = 1; ww < NW; ++ww) y2 = cadd(y2, part[(NW + ww) * 32 + lane]);
+      }
       const int row = (s0 + q) * kRowTile + lane;
       if (row >= it.rlo && row < it.rhi) {
         const int f = row / n, p = row - f * n;
         const long long off = (long long)sb.tgt[f] + p;
         const int o = rv.owner(sb.tgt[f] / n);  // the output block's rank
-        const double2* r_o = rv.vec(FV_R, o);
-        double2* zL_o = rv.vec(FV_ZL, o);
-        const double2* zbase = (ft.rmask >> (4 + f)) & 1 ? r_o : zL_o;  // zL not yet written: r
-        if (ft.phase == 0) {
-          zL_o[off] = cadd(__ldcg(zbase + off), y);
-        } else if (ft.phase == 1) {
-          const double2 zl = __ldcg(zbase + off);
-          const double2 v = csub(r_o[off], csub(zl, y));
-          rv.vec(FV_RP, o)[off] = v;
-          rv.vec(FV_W, o)[off] = v;
-          rv.vec(FV_Z, o)[off] = cadd(zl, v);
-        } else if (ft.phase == 2) {
-          double2* w_o = rv.vec(FV_W, o);
-          double2* z_o = rv.vec(FV_Z, o);
-          w_o[off] = cadd(__ldcg(w_o + off), y);
-          z_o[off] = cadd(__ldcg(z_o + off), y);
-        } else {
-          rv.vec(FV_WOUT, o)[off] = csub(__ldcg(rv.vec(FV_Z, o) + off), y);  // EPI_IMS on the final z
-        }
+        const bool low = f < sb.nlow, zr = (ft.rmask >> (4 + f)) & 1;
+        double2 e1 = make_double2(0, 0), e2 = e1, e3 = e1;
+        epi_fetch(rv, ft.phase, ft.flags, low, zr, o, off, e1, e2, e3);
+        epi_store(rv, ft.phase, ft.flags, low, o, off, y1, y2, e1, e2, e3);
       }
     }
     __syncthreads();
-    if (threadIdx.x == 0 && ft.phase != 3) {
-      // one completion per (tile, written block).  One fence by the signalling
-      // thread publishes the epilogue stores the barrier ordered before it
-      // (cumulativity), instead of a fence per storing lane.
-      rv.fence();
-      const int r0 = max(it.rlo, s0 * kRowTile), r1 = min(it.rhi, (s0 + RT) * kRowTile);
-      for (int f = r0 / n; f * n < r1; ++f) atomicAdd(rv.done(sb.tgt[f] / n), 1);
-    }
+    if (threadIdx.x == 0)
+      tile_signal(rv, ft.phase, max(it.rlo, s0 * kRowTile), min(it.rhi, (s0 + RT) * kRowTile), n, sb.nlow, sb.tgt);
   }
 }
 
@@ -305,7 +415,7 @@ __global__ void __launch_bounds__(NW * 32, RT == 1 ? 6 : 1) k_bsp_fused(FusedArg
 // Same arithmetic order as k_step1 (bitwise identical).
 struct TileDesc {
   long long map_off;  // element offset of the tile's 32-row strip
-  int t, K, phase, alt, in_off, rlo, rhi, row0, dep0, ndep, rmask;
+  int t, K, phase, flags, alt, in_off, rlo, rhi, row0, dep0, ndep, rmask, nlow;
   int tgt[4];
 };
 
@@ -346,7 +456,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_bsp_tma(FusedArgs a) {
   extern __shared__ __align__(128) double2 smt[];
   double2* stage = smt;                // S x kChunk
   double2* xs = stage + S * kChunk;    // maxK
-  double2* part = xs + a.maxK;         // NW x 32
+  double2* part = xs + a.nv * a.maxK;  // nv x NW x 32
   __shared__ __align__(8) unsigned long long full[S], empty[S], dfull[2], dempty[2];
   __shared__ TileDesc desc[2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -372,7 +482,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_bsp_tma(FusedArgs a) {
           td.K = sb.k * a.n;
           td.row0 = ft.tile * kRowTile;
           td.map_off = sb.T_off + (long long)ft.tile * td.K * kRowTile;
-          td.phase = ft.phase; td.alt = it.alt; td.in_off = sb.in_off;
+          td.phase = ft.phase; td.flags = ft.flags; td.alt = it.alt; td.in_off = sb.in_off; td.nlow = sb.nlow;
           td.rlo = it.rlo; td.rhi = it.rhi; td.dep0 = ft.dep0; td.ndep = ft.ndep; td.rmask = ft.rmask;
           for (int f = 0; f < 4; ++f) td.tgt[f] = sb.tgt[f];
         }
@@ -417,73 +527,74 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_bsp_tma(FusedArgs a) {
     const int ef = erow / n;
     const long long eoff = erow_ok ? (long long)td.tgt[ef] + (erow - ef * n) : 0;
     const int eo = erow_ok ? rv.owner(td.tgt[ef] / n) : cr;  // the output block's rank
-    double2 e1 = make_double2(0, 0), e2 = make_double2(0, 0);
-    if (erow_ok) {
-      const double2* r_o = rv.vec(FV_R, eo);
-      const double2* zbase = (td.rmask >> (4 + ef)) & 1 ? r_o : rv.vec(FV_ZL, eo);  // zL not yet written: r
-      if (td.phase == 0) e1 = __ldcg(zbase + eoff);
-      else if (td.phase == 1) { e1 = __ldcg(zbase + eoff); e2 = r_o[eoff]; }
-      else if (td.phase == 2) { e1 = __ldcg(rv.vec(FV_W, eo) + eoff); e2 = __ldcg(rv.vec(FV_Z, eo) + eoff); }
-      else e1 = __ldcg(rv.vec(FV_Z, eo) + eoff);
-    }
+    const bool elow = ef < td.nlow;
+    double2 e1 = make_double2(0, 0), e2 = e1, e3 = e1;
+    if (erow_ok) epi_fetch(rv, td.phase, td.flags, elow, (td.rmask >> (4 + ef)) & 1, eo, eoff, e1, e2, e3);
     const int K = td.K;
+    const int nv = td.phase == 4 ? 2 : 1;
     // the slab (this subdomain's incoming blocks) lives on this CTA's rank
-    const double2* src;
-    if (td.phase == 0) src = rv.vec(td.alt ? FV_R : FV_ZL, cr);
-    else if (td.phase == 1) src = rv.vec(FV_ZL, cr);
-    else if (td.phase == 2) src = rv.vec(td.alt ? FV_RP : FV_W, cr);
-    else src = rv.vec(FV_Z, cr);  // phase 3: (I - S) z
-    src += td.in_off;
+    const double2 *x1, *x2;
+    slab_srcs(rv, td.phase, td.alt, cr, x1, x2);
+    x1 += td.in_off;
     const double2* rsrc = rv.vec(FV_R, cr) + td.in_off;
     // zL starts as r without a copy: faces of zL not yet written read r
-    for (int i = threadIdx.x; i < K; i += NT) xs[i] = __ldcg(((td.rmask >> (i / n)) & 1 ? rsrc : src) + i);
+    for (int i = threadIdx.x; i < K; i += NT) xs[i] = __ldcg(((td.rmask >> (i / n)) & 1 ? rsrc : x1) + i);
+    if (nv == 2)
+      for (int i = threadIdx.x; i < K; i += NT) xs[K + i] = __ldcg(x2 + td.in_off + i);
     consumers_sync(NT);
-    double2 a0 = make_double2(0, 0), a1 = make_double2(0, 0);
+    double2 a0 = make_double2(0, 0), a1 = a0, b0 = a0, b1 = a0;
     const int nch = (K + 31) / 32;
-    for (int ch = 0; ch < nch; ++ch, ++g) {
-      const int st = (int)(g % S);
-      mbar_wait(&full[st], (unsigned)((g / S) & 1));
-      const double2* Ts = stage + (size_t)st * kChunk;
+    if (nv == 2) {
+      for (int ch = 0; ch < nch; ++ch, ++g) {
+        const int st = (int)(g % S);
+        mbar_wait(&full[st], (unsigned)((g / S) & 1));
+        const double2* Ts = stage + (size_t)st * kChunk;
 #pragma unroll
-      for (int u = 0; u < CPW; ++u) {
-        const int cc = warp * CPW + u, col = ch * 32 + cc;
-        if (col < K) {
-          if (col & 1) cfma(a1, Ts[cc * kRowTile + lane], xs[col]);
-          else cfma(a0, Ts[cc * kRowTile + lane], xs[col]);
+        for (int u = 0; u < CPW; ++u) {
+          const int cc = warp * CPW + u, col = ch * 32 + cc;
+          if (col < K) {
+            const double2 tv = Ts[cc * kRowTile + lane];
+            if (col & 1) { cfma(a1, tv, xs[col]); cfma(b1, tv, xs[K + col]); }
+            else { cfma(a0, tv, xs[col]); cfma(b0, tv, xs[K + col]); }
+          }
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
+    } else {
+      for (int ch = 0; ch < nch; ++ch, ++g) {
+        const int st = (int)(g % S);
+        mbar_wait(&full[st], (unsigned)((g / S) & 1));
+        const double2* Ts = stage + (size_t)st * kChunk;
+#pragma unroll
+        for (int u = 0; u < CPW; ++u) {
+          const int cc = warp * CPW + u, col = ch * 32 + cc;
+          if (col < K) {
+            if (col & 1) cfma(a1, Ts[cc * kRowTile + lane], xs[col]);
+            else cfma(a0, Ts[cc * kRowTile + lane], xs[col]);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+      }
     }
     part[warp * 32 + lane] = cadd(a0, a1);
+    if (nv == 2) part[(NW + warp) * 32 + lane] = cadd(b0, b1);
     consumers_sync(NT);
     if (warp == 0) {
-      double2 y = part[lane];
+      double2 y1 = part[lane], y2 = make_double2(0, 0);
 #pragma unroll
-      for (int w = 1; w < NW; ++w) y = cadd(y, part[w * 32 + lane]);
-      if (erow_ok) {
-        const long long off = eoff;
-        if (td.phase == 0) {
-          rv.vec(FV_ZL, eo)[off] = cadd(e1, y);
-        } else if (td.phase == 1) {
-          const double2 v = csub(e2, csub(e1, y));  // r - (zL - S zL)
-          rv.vec(FV_RP, eo)[off] = v;
-          rv.vec(FV_W, eo)[off] = v;
-          rv.vec(FV_Z, eo)[off] = cadd(e1, v);
-        } else if (td.phase == 2) {
-          rv.vec(FV_W, eo)[off] = cadd(e1, y);
-          rv.vec(FV_Z, eo)[off] = cadd(e2, y);
-        } else {
-          rv.vec(FV_WOUT, eo)[off] = csub(e1, y);  // EPI_IMS on the final z
-        }
+      for (int w = 1; w < NW; ++w) y1 = cadd(y1, part[w * 32 + lane]);
+      if (nv == 2) {
+        y2 = part[NW * 32 + lane];
+#pragma unroll
+        for (int w = 1; w < NW; ++w) y2 = cadd(y2, part[(NW + w) * 32 + lane]);
       }
+      if (erow_ok) epi_store(rv, td.phase, td.flags, elow, eo, eoff, y1, y2, e1, e2, e3);
     }
     consumers_sync(NT);
-    if (threadIdx.x == 0 && td.phase != 3) {  // nothing waits on the (I - S) z tiles
-      rv.fence();  // publishes the epilogue stores ordered before it by the barrier
-      const int r0 = max(td.rlo, td.row0), r1 = min(td.rhi, td.row0 + kRowTile);
-      for (int f = r0 / n; f * n < r1; ++f) atomicAdd(rv.done(td.tgt[f] / n), 1);
-    }
+    if (threadIdx.x == 0)  // nothing waits on the (I - S) z tiles
+      tile_signal(rv, td.phase, max(td.rlo, td.row0), min(td.rhi, td.row0 + kRowTile), n, td.nlow, td.tgt);
   }
 }
 
@@ -647,7 +758,7 @@ cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double
       cudaFuncSetAttribute(k_bsp_tma<NWt, ST, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
       attr = true;
     }
-    const size_t smem = (size_t)(ST * kChunk + f.maxK + NWt * 32) * sizeof(double2);
+    const size_t smem = (size_t)(ST * kChunk + f.nv * (f.maxK + NWt * 32)) * sizeof(double2);
     static int per_sm = 0;
     static size_t per_sm_smem = 0;
     if (per_sm == 0 || per_sm_smem != smem) {
@@ -661,7 +772,7 @@ cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double
     a.tiles = f.tiles; a.items = f.items; a.deps = f.deps; a.subs = c.dsubs; a.T = c.T;
     a.r = r; a.zL = zL; a.rp = rp; a.w = w; a.z = z; a.wout = wout;
     a.done = f.counters; a.ticket = f.counters + c.plan.npairs;
-    a.ntiles = f.ntiles; a.n = c.n; a.maxK = f.maxK;
+    a.ntiles = f.ntiles; a.n = c.n; a.maxK = f.maxK; a.nv = f.nv;
     const int grid = std::max(1, std::min(f.ntiles, per_sm * c.num_sms));
     c.launches++;
     k_bsp_tma<NWt, ST, false><<<grid, (NWt + 1) * 32, smem, c.stream>>>(a);
@@ -670,7 +781,7 @@ cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double
   static_assert(kSumWarps == 8, "register-streaming fused kernels are instantiated for 8 warps");
   const int var = f.rt == 2 ? 2 : 0;
   const int NWv = 8;
-  const size_t smem = (size_t)(f.maxK + NWv * 32 * f.rt) * sizeof(double2);
+  const size_t smem = (size_t)(f.nv * f.maxK + NWv * 32 * std::max(f.rt, f.nv)) * sizeof(double2);
   static int per_sm[3] = {0, 0, 0};
   static size_t per_sm_smem[3] = {0, 0, 0};
   if (per_sm[var] == 0 || per_sm_smem[var] != smem) {
@@ -685,7 +796,7 @@ cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double
   a.tiles = f.tiles; a.items = f.items; a.deps = f.deps; a.subs = c.dsubs; a.T = c.T;
   a.r = r; a.zL = zL; a.rp = rp; a.w = w; a.z = z; a.wout = wout;
   a.done = f.counters; a.ticket = f.counters + c.plan.npairs;
-  a.ntiles = f.ntiles; a.n = c.n; a.maxK = f.maxK;
+  a.ntiles = f.ntiles; a.n = c.n; a.maxK = f.maxK; a.nv = f.nv;
   const int grid = std::max(1, std::min(f.ntiles, per_sm[var] * c.num_sms));
   c.launches++;
   if (var == 2) k_bsp_fused<8, 2, false><<<grid, 256, smem, c.stream>>>(a);
@@ -717,7 +828,7 @@ cudaError_t launch_bsp_fused_ranks(Ctx& c, const DevFused& f, const MultiRankArg
   a.tiles = nullptr; a.items = f.items; a.deps = f.deps; a.subs = c.dsubs; a.T = c.T;
   a.r = nullptr; a.zL = a.rp = a.w = a.z = a.wout = nullptr;
   a.done = nullptr; a.ticket = nullptr;
-  a.ntiles = 0; a.n = c.n; a.maxK = f.maxK;
+  a.ntiles = 0; a.n = c.n; a.maxK = f.maxK; a.nv = f.nv;
   a.mr = mr;
   c.launches++;
   const int G = mr.self < 0 ? mr.G : 1;
@@ -728,7 +839,7 @@ cudaError_t launch_bsp_fused_ranks(Ctx& c, const DevFused& f, const MultiRankArg
       cudaFuncSetAttribute(k_bsp_tma<NWt, ST, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
       attr = true;
     }
-    const size_t smem = (size_t)(ST * kChunk + f.maxK + NWt * 32) * sizeof(double2);
+    const size_t smem = (size_t)(ST * kChunk + f.nv * (f.maxK + NWt * 32)) * sizeof(double2);
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsp_tma<NWt, ST, true>, (NWt + 1) * 32, smem);
     const int grid = std::max(G, (std::max(1, per_sm) * c.num_sms / G) * G);
@@ -740,7 +851,7 @@ cudaError_t launch_bsp_fused_ranks(Ctx& c, const DevFused& f, const MultiRankArg
     cudaFuncSetAttribute(k_bsp_fused<8, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  const size_t smem = (size_t)(f.maxK + 8 * 32) * sizeof(double2);
+  const size_t smem = (size_t)(f.nv * (f.maxK + 8 * 32)) * sizeof(double2);
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsp_fused<8, 1, true>, 256, smem);
   const int grid = std::max(G, (std::max(1, per_sm) * c.num_sms / G) * G);

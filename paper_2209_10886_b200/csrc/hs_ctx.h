@@ -26,6 +26,7 @@ struct DevSub {
   long long T_off;  // element offset of the map
   int in_off;       // element offset of the incoming slab m(s, .) (block * n)
   int k;            // interface faces; K = k * n columns
+  int nlow;         // leading W/S faces (map rows [0, nlow * n) feed the lower neighbours)
   int tgt[4];       // element offset (block * n) of the block written by each face
 };
 
@@ -105,10 +106,22 @@ struct DevStep {
 
 // Fused BSP apply (one persistent dataflow launch): a tile of some step, with
 // the per-block completion counts it must wait for.
+// Phases (what a tile multiplies and how its rows are finished; FT_* flags):
+//   0 forward         y1 = T (r | zL):   zL += y1            [FT_ZERO: rp = w = 0, z = zL]
+//   1 residual        y1 = T zL:         v = r - (zL - y1); rp = w = v; z = zL + v
+//   2 backward        y1 = T (rp | w):   w += y1, z += y1    [FT_WOUT: wout = r; upper rows wout = r - y1]
+//   3 (I - S) z       y1 = T z:          wout = z - y1
+//   4 residual+bwd    y1 = T zL, y2 = T (rp | w): v = r - (zL - y1); rp = v; w = v + y2; z = (zL + v) + y2
+//                                        [FT_WOUT: wout = r; upper rows wout = r - y2]
+//   5 (I - S) late    y1 = T w (final):  lower rows wout = (r - rp) + (w - y1); upper rows wout = r - y1
+// Phases 0-3 in step order are the per-step arithmetic (bitwise); 0-2 + 4 + 5
+// are the map-once plan of build_fused (each map row read ~once per apply).
+enum FusedFlags { FT_ZERO = 1, FT_WOUT = 2 };
 struct FusedTile {
   int item;        // index into the fused item list
   int tile;        // tile index in units of rt strips
-  int phase;       // 0 forward (EPI_ACC on zL), 1 residual (EPI_RESID), 2 backward (EPI_ACC2), 3 (I - S) z
+  int phase;       // see above
+  int flags;       // FT_*
   int dep0, ndep;  // dependencies [dep0, dep0 + ndep) in the dep pool
   int rmask;       // bit q: slab face q of zL not yet written (read r); bit 4 + f: output face f likewise
 };
@@ -122,6 +135,8 @@ struct DevFused {
   FusedTile* tiles = nullptr;
   FusedDep* deps = nullptr;
   int nitems = 0, ntiles = 0, ndeps = 0, maxK = 0;
+  int nv = 1;               // vectors per tile (2: the map-once plan's phase-4 tiles)
+  bool map_once = false;    // map-once plan (else per-step order, bitwise = k_step1)
   int rt = 1;               // 32-row strips per tile
   int nw = 8;               // warps per CTA (consumer warps for the TMA kernel)
   bool tma = true;          // TMA-staged maps (k_bsp_tma), else register streaming (k_bsp_fused)

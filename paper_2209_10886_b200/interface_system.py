@@ -148,7 +148,7 @@ class GpuInterfaceSystem:
 
     def __init__(self, spec, partition: Partition, imp: ImpedanceSpec | None = None, workers: int = 1,
                  device: int = 0, rank: int = 0, nranks: int = 1, nccl_id: bytes | None = None,
-                 sweep: SweepConfig | None = None, maps: str = "subdomain", fused: bool | int = True):
+                 sweep: SweepConfig | None = None, maps: str = "subdomain", fused: bool | int | str = True):
         """maps = "subdomain": one compact Schur map per subdomain, streamed from
         HBM by the step kernels (the graded path); "shared": only the distinct
         operators' maps (generic + scatterer) are kept and every step is a DMMA
@@ -173,9 +173,20 @@ class GpuInterfaceSystem:
             raise ValueError(f"maps must be 'subdomain' or 'shared', got {maps!r}")
         self.maps = maps
         self.ctx.call("hs_set_map_mode", 1 if maps == "shared" else 0)
-        # one-RHS BSP applies as a single dataflow launch (bitwise equal to per-step
-        # launches); fused=3 also fuses the DMMA contraction paths (opt-in)
-        self.ctx.call("hs_set_fused", int(fused) if not isinstance(fused, bool) else (1 if fused else 0))
+        # one-RHS BSP applies as a single dataflow launch: fused=True runs the
+        # map-once plan (each map row read ~once per apply; equal to the step
+        # sequence to rounding), fused="steps" the per-step plan (bitwise equal
+        # to per-step launches, fused=False); fused=3 also fuses the DMMA
+        # contraction paths (opt-in); an int is the raw hs_set_fused mask
+        if isinstance(fused, str):
+            if fused != "steps":
+                raise ValueError(f"fused must be a bool, an int mask or 'steps', got {fused!r}")
+            mask = 5
+        elif isinstance(fused, bool):
+            mask = 1 if fused else 0
+        else:
+            mask = int(fused)
+        self.ctx.call("hs_set_fused", mask)
         self.home, cells = scatterer_cells(spec, partition)
         if self.home is not None:
             c = native.i32(cells)

@@ -1,7 +1,8 @@
 """GPU: the fused dataflow BSP apply (one persistent launch, per-block
-completion counters) is bitwise identical to the one-launch-per-step sequence,
-including 1-step windows (seams written and read in the same step) and the
-reference-window / block-count variants."""
+completion counters).  Its per-step plan (fused="steps") is bitwise identical
+to the one-launch-per-step sequence, including 1-step windows (seams written
+and read in the same step) and the reference-window / block-count variants;
+the map-once plan (the default) equals it to rounding and matches the oracle."""
 
 import numpy as np
 import pytest
@@ -25,7 +26,7 @@ CASES = [("small_1x4", small_case(1, 4, 8), [None, 1]), ("small_3x3", small_case
 def test_fused_bitwise_equals_steps(name, c, blocks):
     spec, part = product_problem(c)
     a = GpuInterfaceSystem(spec, part, fused=False)
-    b = GpuInterfaceSystem(spec, part, fused=True)
+    b = GpuInterfaceSystem(spec, part, fused="steps")
     g = cvec(13, a.layout.size)
     for p in blocks:
         a.configure(SweepConfig(blocks=p))
@@ -49,10 +50,10 @@ def test_fused_gmres_cfg2_golden():
                                            ("cfg1", CONFIGS[1], None), ("cfg2", CONFIGS[2], 4), ("cfg3", CONFIGS[3], 4)])
 def test_fused_gmres_bitwise_equals_steps(name, c, blocks):
     """GMRES with A M v as ONE launch (BSP + (I - S) z, phase 3 of the fused
-    plan) runs bitwise the same iterations as the per-step kernels."""
+    per-step plan) runs bitwise the same iterations as the per-step kernels."""
     spec, part = product_problem(c)
     a = GpuInterfaceSystem(spec, part, fused=False, sweep=SweepConfig(blocks=blocks))
-    b = GpuInterfaceSystem(spec, part, fused=True, sweep=SweepConfig(blocks=blocks))
+    b = GpuInterfaceSystem(spec, part, fused="steps", sweep=SweepConfig(blocks=blocks))
     rhs = a.rhs() if c.get("center") is not None else cvec(5, a.layout.size)
     ra = a.gmres(rhs, "bsp", tol=1e-8, maxit=300)
     rb = b.gmres(rhs, "bsp", tol=1e-8, maxit=300)
@@ -92,7 +93,7 @@ def test_host_buffer_apply_bitwise(name, c, blocks):
 
 
 _VARIANT_SCRIPT = r"""
-import sys, numpy as np
+import hashlib, sys, numpy as np
 sys.path.insert(0, 'tests')
 from conftest import cvec, product_problem
 from paper_2209_10886_b200.configs import CONFIGS, small_case
@@ -100,18 +101,16 @@ from paper_2209_10886_b200.interface_system import GpuInterfaceSystem, SweepConf
 for c, blocks in ((small_case(6, 3, 16), 5), (CONFIGS[2], 4), (CONFIGS[3], 4)):
     spec, part = product_problem(c)
     a = GpuInterfaceSystem(spec, part, fused=False, sweep=SweepConfig(blocks=blocks))
-    b = GpuInterfaceSystem(spec, part, fused=True, sweep=SweepConfig(blocks=blocks))
+    b = GpuInterfaceSystem(spec, part, fused="steps", sweep=SweepConfig(blocks=blocks))
     g = cvec(29, a.layout.size)
     assert np.array_equal(a.bsp_apply(g), b.bsp_apply(g)), c["name"]
+    m = GpuInterfaceSystem(spec, part, fused=True, sweep=SweepConfig(blocks=blocks))
+    print(c["name"], hashlib.sha1(m.bsp_apply(g).tobytes()).hexdigest())
 print("ok")
 """
 
 
-@pytest.mark.parametrize("env", [{"HS_FUSED_TMA": "0"}, {"HS_FUSED_TMA": "1"}, {"HS_FUSED_RT": "2"}])
-def test_fused_variants_bitwise(env):
-    """Every fused-kernel variant (TMA-staged, register streaming, two strips
-    per tile) is bitwise the per-step result; the knobs are read once per
-    process, so each runs in its own interpreter."""
+def _run_variant(env):
     import os
     import subprocess
     import sys
@@ -119,19 +118,33 @@ def test_fused_variants_bitwise(env):
     out = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT], cwd=root, env=dict(os.environ, **env),
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
+    return [ln for ln in out.stdout.splitlines() if ln != "ok"]
+
+
+def test_fused_variants_bitwise():
+    """Every fused-kernel variant (TMA-staged, register streaming, two strips
+    per tile) of the per-step plan is bitwise the per-step result, and the
+    map-once plan gives bitwise the same z on the TMA-staged and the register-
+    streaming kernel (one column split); the knobs are read once per process,
+    so each runs in its own interpreter."""
+    tma = _run_variant({"HS_FUSED_TMA": "1"})
+    regs = _run_variant({"HS_FUSED_TMA": "0"})
+    _run_variant({"HS_FUSED_RT": "2"})
+    assert tma == regs, (tma, regs)
 
 
 @pytest.mark.parametrize("name,c,blocks,ranks", [("small_6x3", small_case(6, 3, 16), 5, (2, 3)),
                                                  ("small_4x4_n160", small_case(4, 4, 160), None, (2, 4)),
                                                  ("cfg2", CONFIGS[2], 4, (2, 4, 8)), ("cfg3", CONFIGS[3], 4, (2, 8))])
-def test_emulated_row_band_ranks_bitwise(name, c, blocks, ranks):
+@pytest.mark.parametrize("plan", [True, "steps"])
+def test_emulated_row_band_ranks_bitwise(name, c, blocks, ranks, plan):
     """The multi-rank fused kernels (every block on its owner rank, output
     blocks and their counters reached in the owner's buffers -- the
     peer-memory protocol of the multi-GPU path) emulated on one GPU: bitwise
     the single-rank apply, for TMA-staged (maps <= 512 columns) and
     register-streaming (n = 160: 640 columns) kernels."""
     spec, part = product_problem(c)
-    s = GpuInterfaceSystem(spec, part, sweep=SweepConfig(blocks=blocks))
+    s = GpuInterfaceSystem(spec, part, sweep=SweepConfig(blocks=blocks), fused=plan)
     g = cvec(31, s.layout.size)
     ref = s.bsp_apply(g)
     for G in ranks:
@@ -141,3 +154,46 @@ def test_emulated_row_band_ranks_bitwise(name, c, blocks, ranks):
             assert np.array_equal(z, ref), (name, G, relerr(z, ref))
     s.ctx.call("hs_set_emulated_ranks", 1)
     assert np.array_equal(s.bsp_apply(g), ref)
+
+
+MAP_ONCE_CASES = [("small_1x4", small_case(1, 4, 8), [None, 1]), ("small_3x3", small_case(3, 3, 8), [None, 1, 2]),
+                  ("small_6x3", small_case(6, 3, 16), [None, 2, 5]), ("small_4x4_n160", small_case(4, 4, 160), [None, 3]),
+                  ("cfg1", CONFIGS[1], [None, 1, 3]), ("cfg2", CONFIGS[2], [None, 1, 2, 4, 8]), ("cfg3", CONFIGS[3], [4])]
+
+
+@pytest.mark.parametrize("name,c,blocks", MAP_ONCE_CASES)
+def test_map_once_equals_steps(name, c, blocks):
+    """The map-once plan (residual elided inside forward windows, residual and
+    backward products sharing one map read) gives the step sequence's z to
+    rounding, for every block count incl. 1-step windows; repeated launches are
+    bitwise reproducible."""
+    spec, part = product_problem(c)
+    a = GpuInterfaceSystem(spec, part, fused=False)
+    b = GpuInterfaceSystem(spec, part, fused=True)
+    g = cvec(13, a.layout.size)
+    for p in blocks:
+        a.configure(SweepConfig(blocks=p))
+        b.configure(SweepConfig(blocks=p))
+        za, zb = a.bsp_apply(g), b.bsp_apply(g)
+        assert relerr(zb, za) < 1e-13, (name, p, relerr(zb, za))
+        for _ in range(2):
+            assert np.array_equal(b.bsp_apply(g), zb)
+
+
+@pytest.mark.parametrize("name,c,blocks", [("small_1x4", small_case(1, 4, 8), 1), ("small_3x3", small_case(3, 3, 8), 2),
+                                           ("small_6x3", small_case(6, 3, 16), 5), ("cfg1", CONFIGS[1], None),
+                                           ("cfg2", CONFIGS[2], 8), ("cfg3", CONFIGS[3], 4)])
+def test_map_once_gmres_equals_steps(name, c, blocks):
+    """GMRES with A M v as one map-once launch (BSP + (I - S) z reading each
+    map row ~1.5 times instead of 3): the per-step iterations, history to
+    1e-10 and solution to 1e-10."""
+    spec, part = product_problem(c)
+    a = GpuInterfaceSystem(spec, part, fused=False, sweep=SweepConfig(blocks=blocks))
+    b = GpuInterfaceSystem(spec, part, fused=True, sweep=SweepConfig(blocks=blocks))
+    rhs = a.rhs() if c.get("center") is not None else cvec(5, a.layout.size)
+    ra = a.gmres(rhs, "bsp", tol=1e-8, maxit=300)
+    rb = b.gmres(rhs, "bsp", tol=1e-8, maxit=300)
+    assert ra.converged and rb.converged and ra.iterations == rb.iterations
+    assert relerr(rb.solution, ra.solution) < 1e-10, relerr(rb.solution, ra.solution)
+    ha, hb = np.asarray(ra.history), np.asarray(rb.history)
+    assert np.max(np.abs(hb - ha) / ha) < 1e-8
