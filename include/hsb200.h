@@ -171,6 +171,14 @@ int hs_set_emulated_ranks(hs_ctx* ctx, int ranks);
  * launch for the DMMA contraction (R RHS or shared maps). */
 int hs_set_fused(hs_ctx* ctx, int mask);
 
+/* Diagnostics: record a per-tile timeline of the fused 1-RHS apply (on = 1).
+ * hs_get_trace copies the last traced launch: rows of 6 words per ticket --
+ * claimed, work started, inputs ready, map streamed, completion signalled
+ * (globaltimer ns), (SM id << 32) | (CTA << 8) | phase.  out = NULL returns
+ * the row count only. */
+int hs_set_trace(hs_ctx* ctx, int on);
+int hs_get_trace(hs_ctx* ctx, uint64_t* out, int cap, int* rows);
+
 /* ---- introspection (plan-only contexts too) ---------------------------- */
 /* Sizes: L (= 2 N_e n), number of subdomains, number of groups, 2 N_e. */
 int hs_sizes(const hs_ctx* ctx, int64_t* L, int* nsub, int* ngroups, int* npairs);

@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <queue>
 #include <tuple>
 #include <set>
 #include <string>
@@ -398,6 +399,79 @@ void free_fused(Ctx* c) {
   }
 }
 
+// Ticket order of a fused plan.  CTAs claim tiles in ticket order and wait
+// for their dependencies, so a ticket claimed long before its inputs exist
+// idles a CTA that could stream another tile's map.  List-schedule the tiles
+// on `workers` simulated CTAs (duration = fixed cost + streamed bytes at the
+// per-CTA share of HBM bandwidth): whenever a CTA frees up, it takes, among
+// the tiles whose inputs are complete by then, the one with the longest path
+// to the end of the apply (else the one that becomes ready first).  The
+// result is a topological order of the dependency graph (a tile's
+// predecessors are the first `count` writers of each block it waits on), so
+// any such order keeps the plan deadlock-free and the arithmetic unchanged.
+std::vector<FusedTile> schedule_tickets(const std::vector<FusedTile>& tiles, const std::vector<FusedDep>& deps,
+                                        const std::vector<std::vector<int>>& tile_inc,
+                                        const std::vector<double>& cost, int nblocks, int workers) {
+  const int T = (int)tiles.size();
+  std::vector<std::vector<int>> writers(nblocks);
+  for (int t = 0; t < T; ++t)
+    for (int b : tile_inc[t]) writers[b].push_back(t);
+  std::vector<std::vector<int>> succ(T);
+  std::vector<int> npred(T, 0);
+  for (int t = 0; t < T; ++t) {
+    std::vector<int> pre;
+    for (int d = 0; d < tiles[t].ndep; ++d) {
+      const FusedDep& dp = deps[tiles[t].dep0 + d];
+      for (int i = 0; i < dp.count; ++i) pre.push_back(writers[dp.block][i]);
+    }
+    std::sort(pre.begin(), pre.end());
+    pre.erase(std::unique(pre.begin(), pre.end()), pre.end());
+    npred[t] = (int)pre.size();
+    for (int p : pre) succ[p].push_back(t);
+  }
+  const double bw = 6.5e12 / std::max(1, workers);  // bytes/s per CTA
+  const double fixed = 3e-6;                         // ticket, waits, slab, epilogue
+  std::vector<double> dur(T), bl(T, 0.0), ready(T, 0.0);
+  for (int t = 0; t < T; ++t) dur[t] = fixed + cost[t] / bw;
+  for (int t = T - 1; t >= 0; --t) {  // successors come later in plan order
+    double m = 0;
+    for (int s : succ[t]) m = std::max(m, bl[s]);
+    bl[t] = dur[t] + m;
+  }
+  using Q = std::pair<double, int>;
+  std::priority_queue<Q, std::vector<Q>, std::greater<Q>> waiting, freew;  // by ready time / free time
+  std::priority_queue<Q> avail;                                             // by bottom level
+  for (int w = 0; w < workers; ++w) freew.push({0.0, w});
+  for (int t = 0; t < T; ++t)
+    if (npred[t] == 0) waiting.push({0.0, t});
+  std::vector<FusedTile> out;
+  out.reserve(T);
+  while ((int)out.size() < T) {
+    const double tau = freew.top().first;
+    freew.pop();
+    while (!waiting.empty() && waiting.top().first <= tau) {
+      avail.push({bl[waiting.top().second], waiting.top().second});
+      waiting.pop();
+    }
+    int t;
+    if (!avail.empty()) {
+      t = avail.top().second;
+      avail.pop();
+    } else {
+      t = waiting.top().second;
+      waiting.pop();
+    }
+    const double fin = std::max(tau, ready[t]) + dur[t];
+    out.push_back(tiles[t]);
+    freew.push({fin, 0});
+    for (int s : succ[t]) {
+      ready[s] = std::max(ready[s], fin);
+      if (--npred[s] == 0) waiting.push({ready[s], s});
+    }
+  }
+  return out;
+}
+
 // Dataflow plan of one BSP apply: every tile of the forward steps, the
 // residual step and the backward steps in schedule order, each with the
 // per-block completion counts it waits for (all earlier tile-writes to the
@@ -450,8 +524,11 @@ int build_fused(Ctx* c, bool ims) {
     int phase, flags;
   };
   // one virtual step: tiles of independent items (counts taken before the step)
+  std::vector<std::vector<int>> tile_inc;  // blocks each tile completes
+  std::vector<double> tile_cost;           // bytes each tile streams
   auto add = [&](const std::vector<VItem>& step) {
     std::vector<int> inc;
+    size_t inc0 = 0;
     for (const VItem& v : step) {
       const Item& it = v.it;
       const int phase = v.phase;
@@ -493,6 +570,9 @@ int build_fused(Ctx* c, bool ims) {
             ft.ndep++;
           }
         tiles.push_back(ft);
+        tile_inc.push_back(std::vector<int>(inc.begin() + inc0, inc.end()));
+        tile_cost.push_back(16.0 * ((double)(r1 - r0) * K + nv * K));
+        inc0 = inc.size();
       }
     }
     for (int b : inc) written[b]++;
@@ -571,8 +651,16 @@ int build_fused(Ctx* c, bool ims) {
       add(lt);
     }
   }
-  f.tma = f.tma && f.maxK <= 512;
+  // per-step plan: TMA up to 512 map columns; map-once plan: TMA at every
+  // width (cfg5, 1024 columns, ms per apply TMA / register streaming: 1.43 / 1.50)
+  f.tma = f.tma && (f.map_once || f.maxK <= 512);
   if (const char* e = getenv("HS_FUSED_TMA")) f.tma = atoi(e) != 0 && f.rt == 1;
+  bool reorder = true;
+  if (const char* e = getenv("HS_FUSED_ORDER")) reorder = atoi(e) != 0;
+  if (reorder) {
+    const int workers = (f.tma ? 2 : (f.rt == 1 ? 6 : 1)) * c->num_sms;
+    tiles = schedule_tickets(tiles, deps, tile_inc, tile_cost, P.npairs, workers);
+  }
   if (upload(c, &f.items, items) || upload(c, &f.tiles, tiles) || upload(c, &f.deps, deps)) return -1;
   CK(dalloc(c, (void**)&f.counters, (P.npairs + 1) * sizeof(int)));
   f.nitems = (int)items.size();
@@ -1824,6 +1912,30 @@ int hs_set_fused(hs_ctx* c, int mask) {
     free_emu(c);
   }
   c->fused_mode = mask;
+  return 0;
+}
+
+int hs_set_trace(hs_ctx* c, int on) {
+  if (!c) return fail(nullptr, 1, "null context");
+  if (c->device < 0) return fail(c, 1, "plan-only context");
+  c->trace_on = on != 0;
+  if (c->trace_on && !c->trace) {
+    size_t rows = 0;  // every strip of every map, up to 4 times (phases of one apply)
+    for (const SubPlan& sp : c->plan.subs) rows += 4 * (size_t)((sp.k * c->n + kRowTile - 1) / kRowTile);
+    CK(dalloc(c, (void**)&c->trace, rows * 6 * sizeof(unsigned long long)));
+    c->trace_cap = rows;
+  }
+  c->trace_rows = 0;
+  return 0;
+}
+
+int hs_get_trace(hs_ctx* c, uint64_t* out, int cap, int* rows) {
+  if (!c || !rows) return fail(c, 1, "null argument");
+  *rows = c->trace_rows;
+  if (!out || c->trace_rows == 0) return 0;
+  if (cap < c->trace_rows) return fail(c, 1, "trace buffer too small");
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaMemcpy(out, c->trace, (size_t)c->trace_rows * 6 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
   return 0;
 }
 

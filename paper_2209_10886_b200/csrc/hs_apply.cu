@@ -126,8 +126,20 @@ struct FusedArgs {
   int* ticket;
   int ntiles, n, maxK;
   int nv;  // slab vectors per tile at most (shared-memory layout)
+  unsigned long long* trace;  // per ticket: claim, inputs ready, map streamed, signalled (globaltimer ns), sm<<32|tile
   MultiRankArgs mr;
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %smid;" : "=r"(r));
+  return r;
+}
 
 // Rank view of a CTA: its tile list and the owner-rank addressing of blocks.
 template <bool MR>
@@ -331,6 +343,8 @@ __global__ void __launch_bounds__(NW * 32, RT == 1 ? 6 : 1) k_bsp_fused(FusedArg
     __syncthreads();
     const int t = s_t;
     if (t >= ntiles) return;
+    unsigned long long* tr = (a.trace && !MR) ? a.trace + 6ll * t : nullptr;
+    if (tr && threadIdx.x == 0) tr[0] = tr[1] = gtimer();
     const FusedTile ft = tiles[t];
     const DevItem it = a.items[ft.item];
     const DevSub sb = a.subs[it.s];
@@ -341,6 +355,7 @@ __global__ void __launch_bounds__(NW * 32, RT == 1 ? 6 : 1) k_bsp_fused(FusedArg
     }
     __threadfence();
     __syncthreads();
+    if (tr && threadIdx.x == 0) tr[2] = gtimer();
     const int K = sb.k * n;
     const int nv = (RT == 1 && ft.phase == 4) ? 2 : 1;
     // the slab (this subdomain's incoming blocks) lives on this CTA's rank
@@ -349,7 +364,9 @@ __global__ void __launch_bounds__(NW * 32, RT == 1 ? 6 : 1) k_bsp_fused(FusedArg
     x1 += sb.in_off;
     const double2* rsrc = rv.vec(FV_R, cr) + sb.in_off;
     double2* xs = sm;
-    double2* part = sm + nv * K;
+    // the partial sums reuse the slab's shared memory once every warp is done
+    // with it (one barrier): 6 CTAs per SM fit with two 1024-column slabs
+    double2* part = sm;
     // zL starts as r without a copy: faces of zL not yet written read r
     for (int i = threadIdx.x; i < K; i += NW * 32)
       xs[i] = __ldcg(((ft.rmask >> (i / n)) & 1 ? rsrc : x1) + i);
@@ -363,15 +380,18 @@ __global__ void __launch_bounds__(NW * 32, RT == 1 ? 6 : 1) k_bsp_fused(FusedArg
     if (RT == 1 && nv == 2) {
       double2 acc[1][2][2];
       contract_regs<NW, 1, 2>(Tt, xs, K, nstrip, s0, warp, acc);
+      __syncthreads();
 #pragma unroll
       for (int x = 0; x < 2; ++x) part[(x * NW + warp) * 32 + lane] = cadd(acc[0][x][0], acc[0][x][1]);
     } else {
       double2 acc[RT][1][2];
       contract_regs<NW, RT, 1>(Tt, xs, K, nstrip, s0, warp, acc);
+      __syncthreads();
 #pragma unroll
       for (int q = 0; q < RT; ++q) part[(q * NW + warp) * 32 + lane] = cadd(acc[q][0][0], acc[q][0][1]);
     }
     __syncthreads();
+    if (tr && threadIdx.x == 0) tr[3] = gtimer();
     if (warp < RT) {
       // warp q finalises strip q: fixed-order sum over the warps' partials
       const int q = warp;
@@ -395,8 +415,13 @@ __global__ void __launch_bounds__(NW * 32, RT == 1 ? 6 : 1) k_bsp_fused(FusedArg
       }
     }
     __syncthreads();
-    if (threadIdx.x == 0)
+    if (threadIdx.x == 0) {
       tile_signal(rv, ft.phase, max(it.rlo, s0 * kRowTile), min(it.rhi, (s0 + RT) * kRowTile), n, sb.nlow, sb.tgt);
+      if (tr) {
+        tr[4] = gtimer();
+        tr[5] = ((unsigned long long)smid() << 32) | ((unsigned)blockIdx.x << 8) | (unsigned)ft.phase;
+      }
+    }
   }
 }
 
@@ -417,6 +442,7 @@ struct TileDesc {
   long long map_off;  // element offset of the tile's 32-row strip
   int t, K, phase, flags, alt, in_off, rlo, rhi, row0, dep0, ndep, rmask, nlow;
   int tgt[4];
+  unsigned long long claimed;  // globaltimer at the producer's claim (trace only)
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -450,13 +476,13 @@ __device__ __forceinline__ void consumers_sync(int nthreads) {
 constexpr int kChunk = 32 * kRowTile;  // elements of one 32-column chunk of a strip
 
 template <int NW, int S, bool MR>
-__global__ void __launch_bounds__((NW + 1) * 32, 1) k_bsp_tma(FusedArgs a) {
+__global__ void __maxnreg__(96) k_bsp_tma(FusedArgs a) {  // 96: two 9-warp CTAs per SM (per-SMSP register file)
   const RankView<MR> rv(a);
   const int cr = rv.cr;
   extern __shared__ __align__(128) double2 smt[];
   double2* stage = smt;                // S x kChunk
   double2* xs = stage + S * kChunk;    // maxK
-  double2* part = xs + a.nv * a.maxK;  // nv x NW x 32
+  double2* part = xs;                  // nv x NW x 32 partial sums, reusing the slab once consumed
   __shared__ __align__(8) unsigned long long full[S], empty[S], dfull[2], dempty[2];
   __shared__ TileDesc desc[2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -475,6 +501,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_bsp_tma(FusedArgs a) {
         mbar_wait(&dempty[d], ((q >> 1) & 1) ^ 1);
         TileDesc td;
         td.t = atomicAdd(rv.ticket(), 1);
+        if (a.trace) td.claimed = gtimer();
         if (td.t < rv.ntiles()) {
           const FusedTile ft = rv.tiles()[td.t];
           const DevItem it = a.items[ft.item];
@@ -513,6 +540,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_bsp_tma(FusedArgs a) {
     __syncwarp();
     if (lane == 0) mbar_arrive(&dempty[d]);
     if (td.t >= rv.ntiles()) break;
+    unsigned long long* tr = (a.trace && !MR) ? a.trace + 6ll * td.t : nullptr;
+    if (tr && threadIdx.x == 0) {
+      tr[0] = td.claimed;
+      tr[1] = gtimer();
+    }
     for (int i = threadIdx.x; i < td.ndep; i += NT) {
       const FusedDep dp = a.deps[td.dep0 + i];
       const volatile int* p = rv.done(dp.block);
@@ -520,6 +552,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_bsp_tma(FusedArgs a) {
     }
     __threadfence();
     consumers_sync(NT);
+    if (tr && threadIdx.x == 0) tr[2] = gtimer();
     // warp 0 (lane = output row) fetches its epilogue operands now, in the
     // shadow of the slab load and the contraction, not after them
     const int erow = td.row0 + lane;
@@ -578,9 +611,11 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_bsp_tma(FusedArgs a) {
         if (lane == 0) mbar_arrive(&empty[st]);
       }
     }
+    consumers_sync(NT);  // every consumer is done with the slab
     part[warp * 32 + lane] = cadd(a0, a1);
     if (nv == 2) part[(NW + warp) * 32 + lane] = cadd(b0, b1);
     consumers_sync(NT);
+    if (tr && threadIdx.x == 0) tr[3] = gtimer();
     if (warp == 0) {
       double2 y1 = part[lane], y2 = make_double2(0, 0);
 #pragma unroll
@@ -593,8 +628,13 @@ __global__ void __launch_bounds__((NW + 1) * 32, 1) k_bsp_tma(FusedArgs a) {
       if (erow_ok) epi_store(rv, td.phase, td.flags, elow, eo, eoff, y1, y2, e1, e2, e3);
     }
     consumers_sync(NT);
-    if (threadIdx.x == 0)  // nothing waits on the (I - S) z tiles
+    if (threadIdx.x == 0) {  // nothing waits on the (I - S) z tiles
       tile_signal(rv, td.phase, max(td.rlo, td.row0), min(td.rhi, td.row0 + kRowTile), n, td.nlow, td.tgt);
+      if (tr) {
+        tr[4] = gtimer();
+        tr[5] = ((unsigned long long)smid() << 32) | ((unsigned)blockIdx.x << 8) | (unsigned)td.phase;
+      }
+    }
   }
 }
 
@@ -756,13 +796,15 @@ cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(k_bsp_tma<NWt, ST, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      cudaFuncSetAttribute(k_bsp_tma<NWt, ST, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       attr = true;
     }
-    const size_t smem = (size_t)(ST * kChunk + f.nv * (f.maxK + NWt * 32)) * sizeof(double2);
+    const size_t smem = (size_t)(ST * kChunk + f.nv * std::max(f.maxK, NWt * 32)) * sizeof(double2);
     static int per_sm = 0;
     static size_t per_sm_smem = 0;
     if (per_sm == 0 || per_sm_smem != smem) {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsp_tma<NWt, ST, false>, (NWt + 1) * 32, smem);
+      cudaError_t oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsp_tma<NWt, ST, false>, (NWt + 1) * 32, smem);
+      if (getenv("HS_DEBUG")) fprintf(stderr, "k_bsp_tma: smem %zu per_sm %d (%s)\n", smem, per_sm, cudaGetErrorString(oe));
       per_sm = std::max(1, per_sm);
       per_sm_smem = smem;
     }
@@ -773,6 +815,8 @@ cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double
     a.r = r; a.zL = zL; a.rp = rp; a.w = w; a.z = z; a.wout = wout;
     a.done = f.counters; a.ticket = f.counters + c.plan.npairs;
     a.ntiles = f.ntiles; a.n = c.n; a.maxK = f.maxK; a.nv = f.nv;
+    a.trace = (c.trace_on && c.trace && c.trace_cap >= (size_t)f.ntiles) ? c.trace : nullptr;
+    if (a.trace) c.trace_rows = f.ntiles;
     const int grid = std::max(1, std::min(f.ntiles, per_sm * c.num_sms));
     c.launches++;
     k_bsp_tma<NWt, ST, false><<<grid, (NWt + 1) * 32, smem, c.stream>>>(a);
@@ -781,7 +825,7 @@ cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double
   static_assert(kSumWarps == 8, "register-streaming fused kernels are instantiated for 8 warps");
   const int var = f.rt == 2 ? 2 : 0;
   const int NWv = 8;
-  const size_t smem = (size_t)(f.nv * f.maxK + NWv * 32 * std::max(f.rt, f.nv)) * sizeof(double2);
+  const size_t smem = (size_t)std::max(f.nv * f.maxK, NWv * 32 * std::max(f.rt, f.nv)) * sizeof(double2);
   static int per_sm[3] = {0, 0, 0};
   static size_t per_sm_smem[3] = {0, 0, 0};
   if (per_sm[var] == 0 || per_sm_smem[var] != smem) {
@@ -797,6 +841,8 @@ cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double
   a.r = r; a.zL = zL; a.rp = rp; a.w = w; a.z = z; a.wout = wout;
   a.done = f.counters; a.ticket = f.counters + c.plan.npairs;
   a.ntiles = f.ntiles; a.n = c.n; a.maxK = f.maxK; a.nv = f.nv;
+    a.trace = (c.trace_on && c.trace && c.trace_cap >= (size_t)f.ntiles) ? c.trace : nullptr;
+    if (a.trace) c.trace_rows = f.ntiles;
   const int grid = std::max(1, std::min(f.ntiles, per_sm[var] * c.num_sms));
   c.launches++;
   if (var == 2) k_bsp_fused<8, 2, false><<<grid, 256, smem, c.stream>>>(a);
@@ -828,7 +874,7 @@ cudaError_t launch_bsp_fused_ranks(Ctx& c, const DevFused& f, const MultiRankArg
   a.tiles = nullptr; a.items = f.items; a.deps = f.deps; a.subs = c.dsubs; a.T = c.T;
   a.r = nullptr; a.zL = a.rp = a.w = a.z = a.wout = nullptr;
   a.done = nullptr; a.ticket = nullptr;
-  a.ntiles = 0; a.n = c.n; a.maxK = f.maxK; a.nv = f.nv;
+  a.ntiles = 0; a.n = c.n; a.maxK = f.maxK; a.nv = f.nv; a.trace = nullptr;
   a.mr = mr;
   c.launches++;
   const int G = mr.self < 0 ? mr.G : 1;
@@ -837,9 +883,10 @@ cudaError_t launch_bsp_fused_ranks(Ctx& c, const DevFused& f, const MultiRankArg
     static bool attr = false;
     if (!attr) {
       cudaFuncSetAttribute(k_bsp_tma<NWt, ST, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      cudaFuncSetAttribute(k_bsp_tma<NWt, ST, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
       attr = true;
     }
-    const size_t smem = (size_t)(ST * kChunk + f.nv * (f.maxK + NWt * 32)) * sizeof(double2);
+    const size_t smem = (size_t)(ST * kChunk + f.nv * std::max(f.maxK, NWt * 32)) * sizeof(double2);
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsp_tma<NWt, ST, true>, (NWt + 1) * 32, smem);
     const int grid = std::max(G, (std::max(1, per_sm) * c.num_sms / G) * G);
@@ -851,7 +898,7 @@ cudaError_t launch_bsp_fused_ranks(Ctx& c, const DevFused& f, const MultiRankArg
     cudaFuncSetAttribute(k_bsp_fused<8, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  const size_t smem = (size_t)(f.nv * (f.maxK + 8 * 32)) * sizeof(double2);
+  const size_t smem = (size_t)std::max(f.nv * f.maxK, 8 * 32 * f.nv) * sizeof(double2);
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsp_fused<8, 1, true>, 256, smem);
   const int grid = std::max(G, (std::max(1, per_sm) * c.num_sms / G) * G);

@@ -275,6 +275,11 @@ struct Ctx {
   // execution control / timing
   int async_mode = 0;
   bool timing = false;
+  // per-ticket timeline of the fused 1-RHS apply (hs_set_trace; diagnostics)
+  bool trace_on = false;
+  unsigned long long* trace = nullptr;
+  size_t trace_cap = 0;   // rows of 5 words
+  int trace_rows = 0;     // rows of the last traced launch
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pending;
   std::vector<double> ev_bytes, ev_flops;
   std::vector<cudaEvent_t> ev_pool;

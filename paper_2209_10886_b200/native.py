@@ -65,6 +65,8 @@ _SIGS = {
     "hs_set_map_mode": (_I, [_P, _I]),
     "hs_set_gmres_mode": (_I, [_P, _I]),
     "hs_set_emulated_ranks": (_I, [_P, _I]),
+    "hs_set_trace": (_I, [_P, _I]),
+    "hs_get_trace": (_I, [_P, C.POINTER(C.c_uint64), _I, C.POINTER(_I)]),
     "hs_set_fused": (_I, [_P, _I]),
     "hs_memory": (_I, [_P, C.POINTER(C.c_int64)]),
     "hs_launch_count": (_I, [_P, C.POINTER(C.c_int64)]),

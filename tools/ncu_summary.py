@@ -69,10 +69,19 @@ def main():
     ap.add_argument("--out", required=True)
     ap.add_argument("--fused", action="store_true", help="one launch = one whole BSP apply (k_bsp_fused)")
     ap.add_argument("--kernel", default="k_step1<16>")
+    ap.add_argument("--alg-bytes", type=float, default=None,
+                    help="algorithmic bytes of one captured launch (the map-once plan's, from the bench line's "
+                         "roofline.algorithmic_bytes_per_apply); default: the per-step formula of SURVEY.md 8d")
+    ap.add_argument("--bench-json", default=None, help="read --alg-bytes from this bench line")
     a = ap.parse_args()
     per_step = step_bytes(a.config)
     if a.fused:
         per_step = [sum(per_step)]
+    if a.bench_json:
+        with open(a.bench_json) as f:
+            a.alg_bytes = json.loads(f.read().strip().splitlines()[-1])["roofline"]["algorithmic_bytes_per_apply"]
+    if a.alg_bytes:
+        per_step = [a.alg_bytes]
     launches = []
     for i, r in enumerate(raw_rows(a.rep)):
         idx = a.first_launch + i
