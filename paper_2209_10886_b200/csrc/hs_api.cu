@@ -362,6 +362,7 @@ int make_step(Ctx* c, const StepTable& t, DevStep& out) {
     DevItem d;
     d.s = it.s; d.rlo = it.rlo; d.rhi = it.rhi; d.alt = it.alt;
     for (int q = 0; q < 4; ++q) d.slot[q] = it.slot[q];
+    d.c0 = 0; d.c1 = c->plan.subs[it.s].k * c->n;
     items.push_back(d);
     const int K = c->plan.subs[it.s].k * c->n;
     maxK = std::max(maxK, K);
@@ -522,6 +523,7 @@ int build_fused(Ctx* c, bool ims) {
   struct VItem {
     Item it;
     int phase, flags;
+    int c0 = 0, c1 = -1;  // column range (-1: all K columns)
   };
   // one virtual step: tiles of independent items (counts taken before the step)
   std::vector<std::vector<int>> tile_inc;  // blocks each tile completes
@@ -533,16 +535,18 @@ int build_fused(Ctx* c, bool ims) {
       const Item& it = v.it;
       const int phase = v.phase;
       const SubPlan& sp = P.subs[it.s];
+      const int K = sp.k * n;
       DevItem d;
       d.s = it.s; d.rlo = it.rlo; d.rhi = it.rhi; d.alt = it.alt;
       for (int q = 0; q < 4; ++q) d.slot[q] = -1;
+      d.c0 = v.c0; d.c1 = v.c1 < 0 ? K : v.c1;
       const int idx = (int)items.size();
       items.push_back(d);
-      const int K = sp.k * n;
+      const int KC = d.c1 - d.c0;  // columns streamed
       f.maxK = std::max(f.maxK, K);
       const int nv = phase == 4 ? 2 : 1;
       f.nv = std::max(f.nv, nv);
-      f.bytes += 16.0 * ((double)(it.rhi - it.rlo) * K + nv * K + 2.0 * (it.rhi - it.rlo));
+      f.bytes += 16.0 * ((double)(it.rhi - it.rlo) * KC + nv * KC + 2.0 * (it.rhi - it.rlo));
       for (int tl = it.rlo / TR; tl * TR < it.rhi; ++tl) {
         FusedTile ft;
         ft.item = idx; ft.tile = tl; ft.phase = phase; ft.flags = v.flags;
@@ -571,7 +575,7 @@ int build_fused(Ctx* c, bool ims) {
           }
         tiles.push_back(ft);
         tile_inc.push_back(std::vector<int>(inc.begin() + inc0, inc.end()));
-        tile_cost.push_back(16.0 * ((double)(r1 - r0) * K + nv * K));
+        tile_cost.push_back(16.0 * ((double)(r1 - r0) * KC + nv * KC));
         inc0 = inc.size();
       }
     }
@@ -602,10 +606,10 @@ int build_fused(Ctx* c, bool ims) {
       for (const Item& it : st.host.items) {
         const bool seam = it.alt && P.subs[it.s].nlower > 0;  // slab zL != r: residual rows recomputed
         step.push_back({it, 0, seam ? 0 : FT_ZERO});
-        if (seam) {
+        if (seam) {  // r' = T_up (zL - r): zL differs from r on the W/S slab faces only
           Item r = it;
           r.alt = 0;
-          resid.push_back({r, 1, 0});
+          resid.push_back({r, 1, FT_DIFF, 0, P.subs[it.s].nlower * n});
         }
       }
       mark_zl(add(step));
@@ -644,8 +648,13 @@ int build_fused(Ctx* c, bool ims) {
         const SubPlan& sp = P.subs[s];
         if (late[s] || (!has_bwd[s] && sp.k > sp.nlower)) {
           Item it;
-          it.s = s; it.rlo = 0; it.rhi = sp.k * n; it.alt = 0;
-          lt.push_back({it, 5, 0});
+          it.s = s; it.alt = 0;
+          it.rlo = sp.nlower * n; it.rhi = sp.k * n;  // upper rows: wout = r - T_up w
+          if (it.rhi > it.rlo) lt.push_back({it, 5, 0});
+          if (late[s]) {  // lower rows: wout = r - T_low (w - rp), nonzero on the N/E slab faces only
+            it.rlo = 0; it.rhi = sp.nlower * n;
+            lt.push_back({it, 5, FT_DIFF, sp.nlower * n, sp.k * n});
+          }
         }
       }
       add(lt);
@@ -1163,8 +1172,9 @@ int hs_create(hs_ctx** out, int device, int n1, int n2, int n, double h, double 
       d.in_off = sp.first_block * n;
       for (int q = 0; q < 4; ++q) d.tgt[q] = q < sp.k ? sp.tgt_block[q] * n : -1;
       const long long K = (long long)sp.k * n;
-      d.T_off = off;
-      off += ((K + kRowTile - 1) / kRowTile) * kRowTile * K;
+      // row bands: a rank stores the maps of its own subdomains only
+      d.T_off = sp.rank == x->plan.rank ? off : -1;
+      if (sp.rank == x->plan.rank) off += ((K + kRowTile - 1) / kRowTile) * kRowTile * K;
       x->plan.subs[s].T_off = d.T_off;
       subs[s] = d;
     }
@@ -1318,7 +1328,8 @@ int hs_factor(hs_ctx* c) {
     for (int s2 = 0; s2 < c->plan.nsub; ++s2) {
       const SubPlan& sp = c->plan.subs[s2];
       const int K = sp.k * n;
-      for (int t = 0; t * kRowTile < K; ++t) tl.push_back(make_int2(s2, t));
+      if (sp.rank == c->plan.rank)  // own maps only (row bands)
+        for (int t = 0; t * kRowTile < K; ++t) tl.push_back(make_int2(s2, t));
       for (int q = 0; q < sp.k; ++q) faces[4 * s2 + q] = sp.face[q];
       cls[s2] = c->sub_class[s2];
     }
@@ -1840,7 +1851,7 @@ int hs_get_schur(hs_ctx* c, int i1, int i2, double* T) {
   const long long K = (long long)sp.k * c->n;
   const long long nt = (K + kRowTile - 1) / kRowTile;
   CK(cudaStreamSynchronize(c->stream));
-  if (!c->T) {  // shared-map mode: compact sub-block of the class map
+  if (!c->T || sp.T_off < 0) {  // shared-map mode or another band's subdomain: compact sub-block of the class map
     const int n = c->n, n4 = 4 * n;
     std::vector<double2> t4((size_t)n4 * n4);
     CK(cudaMemcpy(t4.data(), c->classes[c->sub_class[s]].T4, t4.size() * sizeof(double2),
@@ -1870,6 +1881,7 @@ int hs_set_schur(hs_ctx* c, int i1, int i2, const double* T) {
   if (i1 < 1 || i1 > c->n1 || i2 < 1 || i2 > c->n2) return fail(c, 1, "subdomain out of range");
   if (!c->T) CK(dalloc(c, (void**)&c->T, c->T_elems * sizeof(double2)));
   const SubPlan& sp = c->plan.subs[c->plan.ordinal(i1, i2)];
+  if (sp.T_off < 0) return fail(c, 1, "subdomain not in this rank's row band");
   const long long K = (long long)sp.k * c->n;
   const long long nt = (K + kRowTile - 1) / kRowTile;
   std::vector<double2> tm((size_t)nt * kRowTile * K, make_double2(0, 0));

@@ -195,7 +195,7 @@ __device__ __forceinline__ void epi_fetch(const RankView<MR>& rv, int phase, int
       break;
     default:
       e1 = r_o[off];
-      if (low) { e2 = __ldcg(rv.vec(FV_RP, o) + off); e3 = __ldcg(rv.vec(FV_W, o) + off); }
+      if (low && !(flags & FT_DIFF)) { e2 = __ldcg(rv.vec(FV_RP, o) + off); e3 = __ldcg(rv.vec(FV_W, o) + off); }
   }
 }
 
@@ -215,7 +215,7 @@ __device__ __forceinline__ void epi_store(const RankView<MR>& rv, int phase, int
       break;
     }
     case 1: {
-      const double2 v = csub(e2, csub(e1, y1));  // r - (zL - S zL)
+      const double2 v = (flags & FT_DIFF) ? y1 : csub(e2, csub(e1, y1));  // T_up (zL - r), or r - (zL - S zL)
       rv.vec(FV_RP, o)[off] = v;
       rv.vec(FV_W, o)[off] = v;
       rv.vec(FV_Z, o)[off] = cadd(e1, v);
@@ -243,8 +243,21 @@ __device__ __forceinline__ void epi_store(const RankView<MR>& rv, int phase, int
       }
       break;
     default:
-      rv.vec(FV_WOUT, o)[off] = low ? cadd(csub(e1, e2), csub(e3, y1)) : csub(e1, y1);
+      rv.vec(FV_WOUT, o)[off] = (low && !(flags & FT_DIFF)) ? cadd(csub(e1, e2), csub(e3, y1)) : csub(e1, y1);
   }
+}
+
+// Slab value i of a tile: X1 (r where zL is not written yet, bit q of rmask),
+// zero outside the item's column range; FT_DIFF subtracts r (phase 1) or rp
+// (phase 5).
+template <bool MR>
+__device__ __forceinline__ double2 slab_value(const RankView<MR>& rv, int cr, const double2* x1, const double2* rsrc,
+                                              int i, int n, int rmask, int c0, int c1, int phase, int flags,
+                                              int in_off) {
+  if (i < c0 || i >= c1) return make_double2(0, 0);
+  double2 v = __ldcg(((rmask >> (i / n)) & 1 ? rsrc : x1) + i);
+  if (flags & FT_DIFF) v = csub(v, __ldcg((phase == 1 ? rsrc : rv.vec(FV_RP, cr) + in_off) + i));
+  return v;
 }
 
 // Slab sources of a tile: X1 (and X2 for phase 4) on this CTA's rank.
@@ -279,15 +292,14 @@ __device__ __forceinline__ void tile_signal(const RankView<MR>& rv, int phase, i
 // xs + K); column c into warp (c % 32) / (32 / NW), accumulator c & 1.
 template <int NW, int RT, int NV>
 __device__ __forceinline__ void contract_regs(const double2* __restrict__ Tt, const double2* xs, int K, int nstrip,
-                                              int s0, int warp, double2 (&acc)[RT][NV][2]) {
+                                              int s0, int warp, int ch0, int nch, double2 (&acc)[RT][NV][2]) {
   constexpr int CPW = 32 / NW;
   constexpr int U = 8 / CPW;  // chunks per unrolled batch: 8 loads in flight per strip
 #pragma unroll
   for (int q = 0; q < RT; ++q)
 #pragma unroll
     for (int v = 0; v < NV; ++v) acc[q][v][0] = acc[q][v][1] = make_double2(0, 0);
-  const int nch = (K + 31) / 32;
-  int ch = 0;
+  int ch = ch0;
   for (; ch + U <= nch && (ch + U) * 32 <= K; ch += U) {
 #pragma unroll
     for (int q = 0; q < RT; ++q) {
@@ -369,23 +381,24 @@ __global__ void __launch_bounds__(NW * 32, RT == 1 ? 6 : 1) k_bsp_fused(FusedArg
     double2* part = sm;
     // zL starts as r without a copy: faces of zL not yet written read r
     for (int i = threadIdx.x; i < K; i += NW * 32)
-      xs[i] = __ldcg(((ft.rmask >> (i / n)) & 1 ? rsrc : x1) + i);
+      xs[i] = slab_value(rv, cr, x1, rsrc, i, n, ft.rmask, it.c0, it.c1, ft.phase, ft.flags, sb.in_off);
     if (nv == 2)
       for (int i = threadIdx.x; i < K; i += NW * 32) xs[K + i] = __ldcg(x2 + sb.in_off + i);
     __syncthreads();
+    const int ch0 = it.c0 / 32, nch = (it.c1 + 31) / 32;
     // strips beyond the map (RT > 1 at the last rows) are skipped
     const int nstrip = (K + kRowTile - 1) / kRowTile;
     const int s0 = ft.tile * RT;
     const double2* Tt = a.T + sb.T_off + (long long)s0 * K * kRowTile + lane;
     if (RT == 1 && nv == 2) {
       double2 acc[1][2][2];
-      contract_regs<NW, 1, 2>(Tt, xs, K, nstrip, s0, warp, acc);
+      contract_regs<NW, 1, 2>(Tt, xs, K, nstrip, s0, warp, ch0, nch, acc);
       __syncthreads();
 #pragma unroll
       for (int x = 0; x < 2; ++x) part[(x * NW + warp) * 32 + lane] = cadd(acc[0][x][0], acc[0][x][1]);
     } else {
       double2 acc[RT][1][2];
-      contract_regs<NW, RT, 1>(Tt, xs, K, nstrip, s0, warp, acc);
+      contract_regs<NW, RT, 1>(Tt, xs, K, nstrip, s0, warp, ch0, nch, acc);
       __syncthreads();
 #pragma unroll
       for (int q = 0; q < RT; ++q) part[(q * NW + warp) * 32 + lane] = cadd(acc[q][0][0], acc[q][0][1]);
@@ -440,7 +453,7 @@ __global__ void __launch_bounds__(NW * 32, RT == 1 ? 6 : 1) k_bsp_fused(FusedArg
 // Same arithmetic order as k_step1 (bitwise identical).
 struct TileDesc {
   long long map_off;  // element offset of the tile's 32-row strip
-  int t, K, phase, flags, alt, in_off, rlo, rhi, row0, dep0, ndep, rmask, nlow;
+  int t, K, phase, flags, alt, in_off, rlo, rhi, row0, dep0, ndep, rmask, nlow, c0, c1;
   int tgt[4];
   unsigned long long claimed;  // globaltimer at the producer's claim (trace only)
 };
@@ -463,11 +476,20 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
         : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
   } while (!ok);
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
+// Map chunks are read exactly once per apply: evict them from L2 first, so the
+// interface vectors (a few x 8 MB, re-read by every tile) stay L2-resident.
+__device__ __forceinline__ unsigned long long l2_evict_first_policy() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
+                                         unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
 }
 __device__ __forceinline__ void consumers_sync(int nthreads) {
   asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
@@ -495,6 +517,7 @@ __global__ void __maxnreg__(96) k_bsp_tma(FusedArgs a) {  // 96: two 9-warp CTAs
   __syncthreads();
   if (warp == NW) {  // ---- producer
     if (lane == 0) {
+      const unsigned long long pol = l2_evict_first_policy();
       long long g = 0;
       for (int q = 0;; ++q) {
         const int d = q & 1;
@@ -510,20 +533,21 @@ __global__ void __maxnreg__(96) k_bsp_tma(FusedArgs a) {  // 96: two 9-warp CTAs
           td.row0 = ft.tile * kRowTile;
           td.map_off = sb.T_off + (long long)ft.tile * td.K * kRowTile;
           td.phase = ft.phase; td.flags = ft.flags; td.alt = it.alt; td.in_off = sb.in_off; td.nlow = sb.nlow;
+          td.c0 = it.c0; td.c1 = it.c1;
           td.rlo = it.rlo; td.rhi = it.rhi; td.dep0 = ft.dep0; td.ndep = ft.ndep; td.rmask = ft.rmask;
           for (int f = 0; f < 4; ++f) td.tgt[f] = sb.tgt[f];
         }
         desc[d] = td;
         mbar_arrive(&dfull[d]);
         if (td.t >= rv.ntiles()) break;
-        const int nch = (td.K + 31) / 32;
+        const int nch = (td.c1 + 31) / 32;
         const double2* src = a.T + td.map_off;
-        for (int ch = 0; ch < nch; ++ch, ++g) {
+        for (int ch = td.c0 / 32; ch < nch; ++ch, ++g) {
           const int st = (int)(g % S);
           mbar_wait(&empty[st], (unsigned)((g / S) & 1) ^ 1);
           const unsigned bytes = (unsigned)min(32, td.K - 32 * ch) * kRowTile * sizeof(double2);
           mbar_expect_tx(&full[st], bytes);
-          bulk_g2s(stage + (size_t)st * kChunk, src + (long long)ch * kChunk, bytes, &full[st]);
+          bulk_g2s(stage + (size_t)st * kChunk, src + (long long)ch * kChunk, bytes, &full[st], pol);
         }
       }
     }
@@ -571,14 +595,15 @@ __global__ void __maxnreg__(96) k_bsp_tma(FusedArgs a) {  // 96: two 9-warp CTAs
     x1 += td.in_off;
     const double2* rsrc = rv.vec(FV_R, cr) + td.in_off;
     // zL starts as r without a copy: faces of zL not yet written read r
-    for (int i = threadIdx.x; i < K; i += NT) xs[i] = __ldcg(((td.rmask >> (i / n)) & 1 ? rsrc : x1) + i);
+    for (int i = threadIdx.x; i < K; i += NT)
+      xs[i] = slab_value(rv, cr, x1, rsrc, i, n, td.rmask, td.c0, td.c1, td.phase, td.flags, td.in_off);
     if (nv == 2)
       for (int i = threadIdx.x; i < K; i += NT) xs[K + i] = __ldcg(x2 + td.in_off + i);
     consumers_sync(NT);
     double2 a0 = make_double2(0, 0), a1 = a0, b0 = a0, b1 = a0;
-    const int nch = (K + 31) / 32;
+    const int ch0 = td.c0 / 32, nch = (td.c1 + 31) / 32;
     if (nv == 2) {
-      for (int ch = 0; ch < nch; ++ch, ++g) {
+      for (int ch = ch0; ch < nch; ++ch, ++g) {
         const int st = (int)(g % S);
         mbar_wait(&full[st], (unsigned)((g / S) & 1));
         const double2* Ts = stage + (size_t)st * kChunk;
@@ -595,7 +620,7 @@ __global__ void __maxnreg__(96) k_bsp_tma(FusedArgs a) {  // 96: two 9-warp CTAs
         if (lane == 0) mbar_arrive(&empty[st]);
       }
     } else {
-      for (int ch = 0; ch < nch; ++ch, ++g) {
+      for (int ch = ch0; ch < nch; ++ch, ++g) {
         const int st = (int)(g % S);
         mbar_wait(&full[st], (unsigned)((g / S) & 1));
         const double2* Ts = stage + (size_t)st * kChunk;

@@ -33,6 +33,7 @@ struct DevSub {
 struct DevItem {
   int s, rlo, rhi, alt;
   int slot[4];
+  int c0, c1;  // map columns used by the fused kernels (the rest of the slab reads as zero)
 };
 
 struct DevTile {
@@ -114,9 +115,12 @@ struct DevStep {
 //   4 residual+bwd    y1 = T zL, y2 = T (rp | w): v = r - (zL - y1); rp = v; w = v + y2; z = (zL + v) + y2
 //                                        [FT_WOUT: wout = r; upper rows wout = r - y2]
 //   5 (I - S) late    y1 = T w (final):  lower rows wout = (r - rp) + (w - y1); upper rows wout = r - y1
+// FT_DIFF (map-once, on a column range of the item): phase 1 multiplies
+// zL - r and finishes with v = y1; phase 5 multiplies w - rp and finishes
+// with wout = r - y1.
 // Phases 0-3 in step order are the per-step arithmetic (bitwise); 0-2 + 4 + 5
 // are the map-once plan of build_fused (each map row read ~once per apply).
-enum FusedFlags { FT_ZERO = 1, FT_WOUT = 2 };
+enum FusedFlags { FT_ZERO = 1, FT_WOUT = 2, FT_DIFF = 4 };
 struct FusedTile {
   int item;        // index into the fused item list
   int tile;        // tile index in units of rt strips
