@@ -69,14 +69,17 @@ def problem(cfgno):
     return c, spec, Partition(c["n1"], c["n2"])
 
 
-def config_json(c, world):
-    return {"workload": f"{c['name']}: BSP apply, {c['n1']}x{c['n2']} subdomains of {c['n']}x{c['n']} cells, "
+def config_json(c, world, exchange=None):
+    out = {"workload": f"{c['name']}: BSP apply, {c['n1']}x{c['n2']} subdomains of {c['n']}x{c['n']} cells, "
                         f"{'reference' if c['blocks'] is None else c['blocks']} blocks, {c['nrhs']} RHS",
             "lattice": [c["n1"], c["n2"]], "cells_per_side": c["n"], "grid": [c["n1"] * c["n"], c["n2"] * c["n"]],
             "kappa": c["kappa"], "blocks": c["blocks"], "nrhs": c["nrhs"], "tol": c["tol"],
             "parallelism": f"rowbands{world}" if world > 1 else "single",
             "l2": (f"inputs larger than L2: Schur maps {schur_bytes(c) / 1e9:.2f} GB >> 126 MB L2, no flush"
                    if schur_bytes(c) > 4 * 126e6 else "L2 NOT flushed: maps fit in L2 (report as L2-resident)")}
+    if world > 1:
+        out["exchange"] = exchange
+    return out
 
 
 def schur_bytes(c):
@@ -253,6 +256,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gmres", action="store_true")
     ap.add_argument("--no-variants", action="store_true", help="skip the shared-operator variant")
+    ap.add_argument("--no-peer", action="store_true",
+                    help="row bands (N > 1): per-step kernels + NCCL send/recv instead of the fused apply over CUDA IPC")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -282,6 +287,9 @@ def main():
     t0 = time.perf_counter()
     system = GpuInterfaceSystem(spec, part, device=local, rank=rank, nranks=world, nccl_id=nccl_id, sweep=sweep)
     setup_s = time.perf_counter() - t0  # first factorisation: includes allocations and kernel loads
+    peer = world > 1 and R == 1 and not args.no_peer
+    if peer:
+        system.enable_peer_memory()
     t0 = time.perf_counter()
     system.ctx.call("hs_factor")  # the same factorisation again (warm)
     torch.cuda.synchronize()
@@ -461,7 +469,8 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "applies/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-                "config": config_json(c, world), "roofline": roof,
+                "config": config_json(c, world, "fused apply over CUDA IPC peer memory (NVLink)" if peer
+                                     else "per-step kernels + NCCL send/recv"), "roofline": roof,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": m["launches"], "clocks": m["clk"],
                 "gmres": gm, "setup_s": setup_s, "setup_warm_s": setup_warm_s, "variants": variants}
         if R > 1:  # one apply covers all R right-hand sides (RHS-applies/s for cfg 4)

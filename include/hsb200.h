@@ -171,6 +171,25 @@ int hs_set_emulated_ranks(hs_ctx* ctx, int ranks);
  * launch for the DMMA contraction (R RHS or shared maps). */
 int hs_set_fused(hs_ctx* ctx, int mask);
 
+/* Row-band ranks on separate GPUs (one process per GPU, nranks > 1 and
+ * hs_comm_init done), or nranks = 1 on one GPU: the fused 1-RHS apply (and
+ * GMRES's A M v) runs over every rank's buffers through CUDA IPC -- a tile
+ * writes its output blocks and signals their completion counters directly in
+ * the owner's HBM (NVLink peer stores and system-scope atomics), with no
+ * per-step exchange.  hs_peer_export allocates this rank's region and writes
+ * its 64-byte IPC handle; after the host has all-gathered the handles (rank
+ * order), hs_peer_open maps the peers' regions and enables the path.  Replaces
+ * the per-step NCCL send/recv of hs_comm_init's path for the fused apply. */
+int hs_peer_export(hs_ctx* ctx, uint8_t handle[64]);
+int hs_peer_open(hs_ctx* ctx, const uint8_t* handles, int nranks);
+/* The fused plan a rank runs on that path (plan-only contexts too), for
+ * host-side emulation of the protocol: per tile (ticket order) 12 int32 --
+ * subdomain i1, i2, item rows [rlo, rhi), columns [c0, c1), alt, first row of
+ * the tile's 32-row strip, phase, flags, rmask, ndep -- then ndep (block,
+ * count) pairs (wait until block's completion counter >= count).  *count =
+ * int32 written (out = NULL: needed). */
+int hs_fused_plan(const hs_ctx* ctx, int ims, int rank, int32_t* out, int cap, int* count);
+
 /* Diagnostics: record a per-tile timeline of the fused 1-RHS apply (on = 1).
  * hs_get_trace copies the last traced launch: rows of 6 words per ticket --
  * claimed, work started, inputs ready, map streamed, completion signalled

@@ -497,13 +497,21 @@ std::vector<FusedTile> schedule_tickets(const std::vector<FusedTile>& tiles, con
 //    blocks: phase 4 / 2 tiles read the whole map (upper rows on the final w)
 //    when their slab is final; the backward window starts (slab read from
 //    rp, final w later) and subdomains without lower faces get phase 5.
-int build_fused(Ctx* c, bool ims) {
-  DevFused& f = ims ? c->fused_ims : c->fused;
-  const Plan& P = c->plan;
-  const int n = c->n;
+// keep_rank >= 0: keep only the tiles of that rank's subdomains (sub_rank),
+// in the global ticket order (row-band ranks on separate GPUs).
+struct FusedHost {
   std::vector<DevItem> items;
   std::vector<FusedTile> tiles;
   std::vector<FusedDep> deps;
+};
+
+int fused_plan_host(const Ctx* c, const Plan& P, const std::vector<StepTable>& fwd, const StepTable& full,
+                    const std::vector<StepTable>& bwd, bool ims, DevFused& f, FusedHost& H,
+                    const std::vector<int>* sub_rank = nullptr, int keep_rank = -1) {
+  const int n = c->n;
+  std::vector<DevItem>& items = H.items;
+  std::vector<FusedTile>& tiles = H.tiles;
+  std::vector<FusedDep>& deps = H.deps;
   std::vector<int> written(P.npairs, 0), zl_written(P.npairs, 0);
   f.map_once = !(c->fused_mode & 4);
   // tile shape: one 32-row strip, kSumWarps warps splitting its columns
@@ -582,28 +590,28 @@ int build_fused(Ctx* c, bool ims) {
     for (int b : inc) written[b]++;
     return inc;
   };
-  auto vstep = [](const DevStep& st, int phase, int flags) {
+  auto vstep = [](const StepTable& st, int phase, int flags) {
     std::vector<VItem> v;
-    for (const Item& it : st.host.items) v.push_back({it, phase, flags});
+    for (const Item& it : st.items) v.push_back({it, phase, flags});
     return v;
   };
   auto mark_zl = [&](const std::vector<int>& inc) {
     for (int b : inc) zl_written[b]++;
   };
   if (!f.map_once) {
-    for (auto& st : c->fwd) mark_zl(add(vstep(st, 0, 0)));
-    add(vstep(c->full, 1, 0));
-    for (auto& st : c->bwd) add(vstep(st, 2, 0));
-    if (ims) add(vstep(c->full, 3, 0));
+    for (auto& st : fwd) mark_zl(add(vstep(st, 0, 0)));
+    add(vstep(full, 1, 0));
+    for (auto& st : bwd) add(vstep(st, 2, 0));
+    if (ims) add(vstep(full, 3, 0));
   } else {
     // backward window starts below the top group (their slab is read from rp)
     std::set<int> bstart;
     for (auto& w : P.win_upper)
       if (w.second < P.ng + 1) bstart.insert(w.second);
     std::vector<VItem> resid;
-    for (auto& st : c->fwd) {
+    for (auto& st : fwd) {
       std::vector<VItem> step;
-      for (const Item& it : st.host.items) {
+      for (const Item& it : st.items) {
         const bool seam = it.alt && P.subs[it.s].nlower > 0;  // slab zL != r: residual rows recomputed
         step.push_back({it, 0, seam ? 0 : FT_ZERO});
         if (seam) {  // r' = T_up (zL - r): zL differs from r on the W/S slab faces only
@@ -616,9 +624,9 @@ int build_fused(Ctx* c, bool ims) {
     }
     std::vector<bool> has_bwd(P.nsub, false), late(P.nsub, false);
     std::vector<std::vector<VItem>> bsteps;
-    for (auto& st : c->bwd) {
+    for (auto& st : bwd) {
       std::vector<VItem> step;
-      for (const Item& it : st.host.items) {
+      for (const Item& it : st.items) {
         const SubPlan& sp = P.subs[it.s];
         has_bwd[it.s] = true;
         const bool final_slab = !it.alt || sp.k == sp.nlower;  // reads its final w
@@ -670,21 +678,45 @@ int build_fused(Ctx* c, bool ims) {
     const int workers = (f.tma ? 2 : (f.rt == 1 ? 6 : 1)) * c->num_sms;
     tiles = schedule_tickets(tiles, deps, tile_inc, tile_cost, P.npairs, workers);
   }
-  if (upload(c, &f.items, items) || upload(c, &f.tiles, tiles) || upload(c, &f.deps, deps)) return -1;
-  CK(dalloc(c, (void**)&f.counters, (P.npairs + 1) * sizeof(int)));
+  if (keep_rank >= 0) {
+    std::vector<FusedTile> mine;
+    for (const FusedTile& t : tiles)
+      if ((*sub_rank)[items[t.item].s] == keep_rank) mine.push_back(t);
+    tiles.swap(mine);
+  }
   f.nitems = (int)items.size();
   f.ntiles = (int)tiles.size();
   f.ndeps = (int)deps.size();
+  return 0;
+}
+
+int build_fused_plan(Ctx* c, const Plan& P, const std::vector<StepTable>& fwd, const StepTable& full,
+                     const std::vector<StepTable>& bwd, bool ims, DevFused& f,
+                     const std::vector<int>* sub_rank = nullptr, int keep_rank = -1) {
+  FusedHost H;
+  if (int e = fused_plan_host(c, P, fwd, full, bwd, ims, f, H, sub_rank, keep_rank)) return e;
+  if (upload(c, &f.items, H.items) || upload(c, &f.tiles, H.tiles) || upload(c, &f.deps, H.deps)) return -1;
+  CK(dalloc(c, (void**)&f.counters, (P.npairs + 1) * sizeof(int)));
   f.built = true;
   return 0;
 }
 
+int build_fused(Ctx* c, bool ims) {
+  std::vector<StepTable> fwd, bwd;
+  for (auto& st : c->fwd) fwd.push_back(st.host);
+  for (auto& st : c->bwd) bwd.push_back(st.host);
+  return build_fused_plan(c, c->plan, fwd, c->full.host, bwd, ims, ims ? c->fused_ims : c->fused);
+}
+
 void free_emu(Ctx* c);
+void free_peer_plans(Ctx* c);
+void free_peer(Ctx* c);
 
 int build_steps(Ctx* c) {
   if (!c->steps_dirty) return 0;
   free_fused(c);
   free_emu(c);
+  free_peer_plans(c);
   free_fused_mma(c);
   for (auto& s : c->fwd) free_step(c, s);
   for (auto& s : c->bwd) free_step(c, s);
@@ -944,8 +976,99 @@ int do_precond_emulated(Ctx* c, const double2* r, double2* z) {
   return cudaGetLastError() == cudaSuccess ? 0 : fail(c, -1, "emulated ranks: launch failed");
 }
 
+// ---- row-band ranks on separate GPUs: the fused apply over CUDA IPC ----
+void free_peer_plans(Ctx* c) {
+  PeerRanks& p = c->peer;
+  for (DevFused* fp : {&p.plan, &p.plan_ims}) {
+    DevFused& f = *fp;
+    dfree(c, f.items, 0);
+    dfree(c, f.tiles, 0);
+    dfree(c, f.deps, 0);
+    dfree(c, f.counters, 0);
+    f = DevFused();
+  }
+}
+
+void free_peer(Ctx* c) {
+  PeerRanks& p = c->peer;
+  free_peer_plans(c);
+  for (int g = 0; g < kMaxRanks; ++g)
+    if (p.opened[g]) cudaIpcCloseMemHandle(p.opened[g]);
+  dfree(c, p.own, 0);
+  dfree(c, p.blk_rank, 0);
+  dfree(c, p.bar, 0);
+  p = PeerRanks();
+}
+
+// Global plan of the row bands (all ranks' tiles in one ticket order) keeping
+// the tiles of `rank` (host part; plan-only contexts too).
+int peer_plan_host(const Ctx* c, bool ims, int rank, DevFused& f, FusedHost& H) {
+  Plan pg;
+  std::string err = pg.build(c->n1, c->n2, c->n, 0, 1);
+  if (!err.empty()) return fail(const_cast<Ctx*>(c), 1, "peer plan: " + err);
+  pg.win_lower = c->plan.win_lower;
+  pg.win_upper = c->plan.win_upper;
+  std::vector<StepTable> fwd = pg.half_steps(0), bwd = pg.half_steps(1);
+  std::vector<int> sub_rank(c->plan.nsub);
+  for (int s = 0; s < c->plan.nsub; ++s) sub_rank[s] = c->plan.subs[s].rank;
+  return fused_plan_host(c, pg, fwd, pg.full_step(), bwd, ims, f, H, &sub_rank, rank);
+}
+
+int build_peer_plan(Ctx* c, bool ims) {
+  PeerRanks& p = c->peer;
+  DevFused& f = ims ? p.plan_ims : p.plan;
+  FusedHost H;
+  if (int e = peer_plan_host(c, ims, c->plan.rank, f, H)) return e;
+  if (upload(c, &f.items, H.items) || upload(c, &f.tiles, H.tiles) || upload(c, &f.deps, H.deps)) return -1;
+  f.built = true;
+  return 0;
+}
+
+// Stream-ordered barrier of the row-band ranks (a one-element all-reduce).
+int peer_barrier(Ctx* c) {
+  if (c->peer.G <= 1) return 0;
+  ncclComm_t comm = (ncclComm_t)c->nccl;
+  if (!comm) return fail(c, -2, "peer ranks without hs_comm_init");
+  NK(ncclAllReduce(c->peer.bar, c->peer.bar, 1, ncclDouble, ncclSum, comm, c->stream));
+  return 0;
+}
+
+// z = M r (and wout = (I - S) z when wout != null) with every rank's tiles on
+// its own GPU: inputs into this rank's region, counters reset, barrier (no
+// rank signals a peer before the peer has reset), one launch, barrier (every
+// write into this rank's blocks has landed), outputs copied back.
+int do_precond_peer(Ctx* c, const double2* r, double2* z, double2* wout) {
+  PeerRanks& p = c->peer;
+  const bool ims = wout != nullptr;
+  DevFused& f = ims ? p.plan_ims : p.plan;
+  if (!f.built && build_peer_plan(c, ims)) return -1;
+  const Plan& P = c->plan;
+  const long long L = P.L;
+  const int me = P.rank;
+  double2* mine = p.vec[me];
+  CK(cudaMemcpyAsync(mine + FV_R * L, r, L * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
+  CK(cudaMemsetAsync(p.counters[me], 0, (P.npairs + 1) * sizeof(int), c->stream));
+  if (int e = peer_barrier(c)) return e;
+  MultiRankArgs mr;
+  mr.G = p.G;
+  mr.self = me;
+  mr.blk_rank = p.blk_rank;
+  for (int g = 0; g < p.G; ++g) {
+    for (int k = 0; k < FV_N; ++k) mr.v[k][g] = p.vec[g] + (size_t)k * L;
+    mr.done[g] = p.counters[g];
+    mr.ticket[g] = p.counters[g] + P.npairs;
+  }
+  mr.tiles[me] = f.tiles;
+  mr.ntiles[me] = f.ntiles;
+  CK(launch_bsp_fused_ranks(*c, f, mr));
+  if (int e = peer_barrier(c)) return e;
+  CK(cudaMemcpyAsync(z, mine + FV_Z * L, L * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
+  if (ims) CK(cudaMemcpyAsync(wout, mine + FV_WOUT * L, L * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
+  return 0;
+}
+
 bool fused_bsp_ok(const Ctx* c, int R) {
-  return (c->fused_mode & 1) && R == 1 && c->map_mode == 0 && c->plan.nranks == 1 && c->inter &&
+  return (c->fused_mode & 1) && R == 1 && c->map_mode == 0 && (c->plan.nranks == 1 || c->peer.G > 0) && c->inter &&
          c->seam == HS_SEAM_DEDUP && c->full.nitems > 0;
 }
 
@@ -955,6 +1078,7 @@ int do_precond_ims(Ctx* c, const double2* r, double2* z, double2* wout) {
   const long long L = c->plan.L;
   double2 *zl, *rp, *w;
   if (ws_get(c, "zL", L, &zl) || ws_get(c, "rp", L, &rp) || ws_get(c, "w", L, &w)) return -1;
+  if (c->peer.G > 0) return do_precond_peer(c, r, z, wout);
   if (!c->fused_ims.built && build_fused(c, true)) return -1;
   CK(launch_bsp_fused(*c, c->fused_ims, r, zl, rp, w, z, wout));
   return 0;
@@ -982,6 +1106,7 @@ int do_precond(Ctx* c, int kind, const double2* r, double2* z, int R) {
   if (ws_get(c, "zL", LR, &zl) || ws_get(c, "rp", LR, &rp) || ws_get(c, "w", LR, &w)) return -1;
   if (fused_bsp_ok(c, R)) {
     // the whole apply as one dataflow launch (bitwise identical to the step sequence)
+    if (c->peer.G > 0) return do_precond_peer(c, r, z, nullptr);
     if (!c->fused.built && build_fused(c, false)) return -1;
     if (c->emu.G > 1) return do_precond_emulated(c, r, z);
     // no zL = r copy: the plan's rmask makes tiles read r for blocks zL has not received yet
@@ -1207,6 +1332,7 @@ int hs_destroy(hs_ctx* c) {
     free_step(c, c->full);
     free_fused(c);
     free_fused_mma(c);
+    free_peer(c);
     if (c->h_flags) cudaFreeHost(c->h_flags);
     if (c->flag_ev[0]) cudaEventDestroy(c->flag_ev[0]);
     if (c->flag_ev[1]) cudaEventDestroy(c->flag_ev[1]);
@@ -1922,6 +2048,7 @@ int hs_set_fused(hs_ctx* c, int mask) {
   if ((mask ^ c->fused_mode) & 4) {  // plan kind changed: rebuild the fused plans
     free_fused(c);
     free_emu(c);
+    free_peer_plans(c);
   }
   c->fused_mode = mask;
   return 0;
@@ -1948,6 +2075,93 @@ int hs_get_trace(hs_ctx* c, uint64_t* out, int cap, int* rows) {
   if (cap < c->trace_rows) return fail(c, 1, "trace buffer too small");
   CK(cudaStreamSynchronize(c->stream));
   CK(cudaMemcpy(out, c->trace, (size_t)c->trace_rows * 6 * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int hs_peer_export(hs_ctx* c, uint8_t handle[64]) {
+  if (!c || !handle) return fail(c, 1, "null argument");
+  NEED_GPU(c);
+  PeerRanks& p = c->peer;
+  const size_t L = (size_t)c->plan.L;
+  const size_t need = FV_N * L * sizeof(double2) + (size_t)(c->plan.npairs + 1) * sizeof(int);
+  if (!p.own || p.bytes != need) {
+    dfree(c, p.own, 0);
+    p.own = nullptr;
+    CK(dalloc(c, &p.own, need));
+    CK(cudaMemset(p.own, 0, need));
+    p.bytes = need;
+  }
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, p.own));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  memcpy(handle, &h, 64);
+  return 0;
+}
+
+int hs_peer_open(hs_ctx* c, const uint8_t* handles, int nranks) {
+  if (!c || !handles) return fail(c, 1, "null argument");
+  NEED_GPU(c);
+  PeerRanks& p = c->peer;
+  if (nranks != c->plan.nranks) return fail(c, 1, "peer handles: nranks differs from the context's");
+  if (nranks > kMaxRanks) return fail(c, 1, "peer ranks: at most 8");
+  if (!p.own) return fail(c, 1, "hs_peer_export first");
+  if (p.G > 0) return fail(c, 1, "peer ranks already open");
+  if (nranks > 1 && !c->nccl) return fail(c, 1, "peer ranks need hs_comm_init (barriers)");
+  const size_t L = (size_t)c->plan.L;
+  for (int g = 0; g < nranks; ++g) {
+    char* base;
+    if (g == c->plan.rank) {
+      base = (char*)p.own;
+    } else {
+      cudaIpcMemHandle_t h;
+      memcpy(&h, handles + 64 * g, 64);
+      void* q = nullptr;
+      cudaError_t e = cudaIpcOpenMemHandle(&q, h, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) {
+        for (int k = 0; k < g; ++k)
+          if (p.opened[k]) cudaIpcCloseMemHandle(p.opened[k]);
+        for (int k = 0; k < kMaxRanks; ++k) p.opened[k] = nullptr;
+        return fail(c, -1, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+      }
+      p.opened[g] = q;
+      base = (char*)q;
+    }
+    p.vec[g] = (double2*)base;
+    p.counters[g] = (int*)(base + FV_N * L * sizeof(double2));
+  }
+  std::vector<int> br(c->plan.npairs);
+  for (int b = 0; b < c->plan.npairs; ++b) br[b] = c->plan.subs[c->plan.block_sub[b]].rank;
+  if (upload(c, &p.blk_rank, br)) return -1;
+  CK(dalloc(c, (void**)&p.bar, sizeof(double2)));
+  CK(cudaMemset(p.bar, 0, sizeof(double2)));
+  p.G = nranks;
+  return 0;
+}
+
+int hs_fused_plan(const hs_ctx* cc, int ims, int rank, int32_t* out, int cap, int* count) {
+  if (!cc) return 1;
+  hs_ctx* c = const_cast<hs_ctx*>(cc);
+  if (!count) return fail(c, 1, "null argument");
+  if (rank < 0 || rank >= c->plan.nranks) return fail(c, 1, "rank out of range");
+  DevFused f;
+  FusedHost H;
+  if (int e = peer_plan_host(c, ims != 0, rank, f, H)) return e;
+  std::vector<int32_t> v;
+  for (const FusedTile& t : H.tiles) {
+    const DevItem& it = H.items[t.item];
+    const SubPlan& sp = c->plan.subs[it.s];
+    const int32_t rec[12] = {sp.i1, sp.i2, it.rlo, it.rhi, it.c0, it.c1, it.alt, t.tile * kRowTile * f.rt,
+                             t.phase, t.flags, t.rmask, t.ndep};
+    v.insert(v.end(), rec, rec + 12);
+    for (int d = 0; d < t.ndep; ++d) {
+      v.push_back(H.deps[t.dep0 + d].block);
+      v.push_back(H.deps[t.dep0 + d].count);
+    }
+  }
+  *count = (int)v.size();
+  if (!out) return 0;
+  if (cap < (int)v.size()) return fail(c, 1, "plan buffer too small");
+  std::copy(v.begin(), v.end(), out);
   return 0;
 }
 

@@ -47,6 +47,7 @@ __global__ void __launch_bounds__(NW * 32) k_step1(const DevTile* __restrict__ t
   // column c belongs to warp (c % 32) / (32 / NW) and accumulator c & 1: the
   // order of the TMA-staged fused kernel, which consumes 32-column chunks
   const double2* Tt = T + sb.T_off + (long long)tl.tile * K * kRowTile + lane;
+  const unsigned long long pol = l2_evict_first();
   constexpr int CPW = 32 / NW;
   double2 a0 = make_double2(0, 0), a1 = make_double2(0, 0);
   constexpr int U = 8 / CPW;  // chunks per unrolled batch: 8 loads in flight
@@ -57,7 +58,7 @@ __global__ void __launch_bounds__(NW * 32) k_step1(const DevTile* __restrict__ t
 #pragma unroll
     for (int v = 0; v < U; ++v)
 #pragma unroll
-      for (int u = 0; u < CPW; ++u) t[v][u] = ld_stream(Tt + (long long)((ch + v) * 32 + warp * CPW + u) * kRowTile);
+      for (int u = 0; u < CPW; ++u) t[v][u] = ld_stream(Tt + (long long)((ch + v) * 32 + warp * CPW + u) * kRowTile, pol);
 #pragma unroll
     for (int v = 0; v < U; ++v)
 #pragma unroll
@@ -72,8 +73,8 @@ __global__ void __launch_bounds__(NW * 32) k_step1(const DevTile* __restrict__ t
     for (int u = 0; u < CPW; ++u) {
       const int col = ch * 32 + warp * CPW + u;
       if (col < K) {
-        if (col & 1) cfma(a1, ld_stream(Tt + (long long)col * kRowTile), xs[col]);
-        else cfma(a0, ld_stream(Tt + (long long)col * kRowTile), xs[col]);
+        if (col & 1) cfma(a1, ld_stream(Tt + (long long)col * kRowTile, pol), xs[col]);
+        else cfma(a0, ld_stream(Tt + (long long)col * kRowTile, pol), xs[col]);
       }
     }
   part[warp * 32 + lane] = cadd(a0, a1);
@@ -295,6 +296,7 @@ __device__ __forceinline__ void contract_regs(const double2* __restrict__ Tt, co
                                               int s0, int warp, int ch0, int nch, double2 (&acc)[RT][NV][2]) {
   constexpr int CPW = 32 / NW;
   constexpr int U = 8 / CPW;  // chunks per unrolled batch: 8 loads in flight per strip
+  const unsigned long long pol = l2_evict_first();
 #pragma unroll
   for (int q = 0; q < RT; ++q)
 #pragma unroll
@@ -309,7 +311,7 @@ __device__ __forceinline__ void contract_regs(const double2* __restrict__ Tt, co
 #pragma unroll
       for (int v = 0; v < U; ++v)
 #pragma unroll
-        for (int u = 0; u < CPW; ++u) tv[v][u] = ld_stream(Tq + (long long)((ch + v) * 32 + warp * CPW + u) * kRowTile);
+        for (int u = 0; u < CPW; ++u) tv[v][u] = ld_stream(Tq + (long long)((ch + v) * 32 + warp * CPW + u) * kRowTile, pol);
 #pragma unroll
       for (int v = 0; v < U; ++v)
 #pragma unroll
@@ -328,7 +330,7 @@ __device__ __forceinline__ void contract_regs(const double2* __restrict__ Tt, co
 #pragma unroll
         for (int q = 0; q < RT; ++q)
           if (s0 + q < nstrip) {
-            const double2 t = ld_stream(Tt + (long long)q * K * kRowTile + (long long)col * kRowTile);
+            const double2 t = ld_stream(Tt + (long long)q * K * kRowTile + (long long)col * kRowTile, pol);
 #pragma unroll
             for (int x = 0; x < NV; ++x) cfma(acc[q][x][col & 1], t, xs[x * K + col]);
           }
@@ -478,11 +480,6 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
 }
 // Map chunks are read exactly once per apply: evict them from L2 first, so the
 // interface vectors (a few x 8 MB, re-read by every tile) stay L2-resident.
-__device__ __forceinline__ unsigned long long l2_evict_first_policy() {
-  unsigned long long pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
                                          unsigned long long pol) {
   asm volatile(
@@ -517,7 +514,7 @@ __global__ void __maxnreg__(96) k_bsp_tma(FusedArgs a) {  // 96: two 9-warp CTAs
   __syncthreads();
   if (warp == NW) {  // ---- producer
     if (lane == 0) {
-      const unsigned long long pol = l2_evict_first_policy();
+      const unsigned long long pol = l2_evict_first();
       long long g = 0;
       for (int q = 0;; ++q) {
         const int d = q & 1;

@@ -32,6 +32,20 @@ __device__ __forceinline__ double2 ld_stream(const double2* p) {
   asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
   return v;
 }
+// The same with an L2 cache policy (map elements are read once per apply:
+// evict-first keeps the re-read interface vectors L2-resident).
+__device__ __forceinline__ unsigned long long l2_evict_first() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ double2 ld_stream(const double2* p, unsigned long long pol) {
+  double2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(p), "l"(pol));
+  return v;
+}
 
 __device__ __forceinline__ void epi_apply(const Epi& e, long long t, double2 y) {
   switch (e.mode) {

@@ -215,6 +215,23 @@ struct EmuRanks {
   int* counters = nullptr;               // device: G x (npairs done + 1 ticket)
 };
 
+// Row-band ranks on separate GPUs running the fused apply over each other's
+// buffers (hs_peer_export / hs_peer_open): every rank exports one region --
+// FV_N full-length vectors + the completion counters of its blocks + a ticket
+// -- through CUDA IPC and maps its peers' regions, so a tile writes its output
+// blocks and signals their counters directly in the owner's HBM over NVLink.
+struct PeerRanks {
+  int G = 0;                          // 0: off
+  void* own = nullptr;                // this rank's region (cudaMalloc, IPC-exported)
+  size_t bytes = 0;
+  double2* vec[kMaxRanks] = {};       // per rank: FV_N x L vectors
+  int* counters[kMaxRanks] = {};      // per rank: npairs counters + 1 ticket
+  void* opened[kMaxRanks] = {};       // IPC mappings (closed at destroy)
+  DevFused plan, plan_ims;            // global plans; tiles = this rank's only
+  int* blk_rank = nullptr;            // block -> owner rank
+  double2* bar = nullptr;             // one-element NCCL barrier buffer
+};
+
 // One distinct subdomain operator (Dirichlet mask) and its factor.
 struct OpClass {
   std::vector<uint8_t> mask;          // n*n, 1 = Dirichlet cell
@@ -257,6 +274,7 @@ struct Ctx {
   DevFused fused;        // BSP apply as one dataflow launch (1 RHS, per-subdomain maps, 1 rank)
   DevFused fused_ims;    // the same followed by (I - S) z: GMRES's A M v in one launch
   EmuRanks emu;          // emulated row-band ranks for the fused apply (tests)
+  PeerRanks peer;        // row-band ranks on separate GPUs (fused apply over CUDA IPC)
   DevFusedMma fused_mma; // the same on the DMMA contraction (R RHS or shared maps)
   int fused_mode = 1;    // 1: use the fused kernel when applicable, 0: one launch per step
   std::vector<std::vector<int>> seam_blocks;  // [dir] blocks of seam groups (literal mode)

@@ -143,6 +143,21 @@ class _Vec:
         return out
 
 
+def gather_peer_handles(handle: bytes, rank: int, nranks: int) -> bytes:
+    """All-gather the ranks' 64-byte IPC handles in rank order (the layout
+    hs_peer_open reads) over the initialised torch.distributed group."""
+    if len(handle) != 64:
+        raise ValueError("an IPC handle is 64 bytes")
+    if nranks == 1:
+        return handle
+    import torch.distributed as dist
+    if not dist.is_initialized() or dist.get_world_size() != nranks or dist.get_rank() != rank:
+        raise ValueError("peer memory needs torch.distributed initialised with this system's rank / nranks")
+    objs = [None] * nranks
+    dist.all_gather_object(objs, handle)
+    return b"".join(objs)
+
+
 class GpuInterfaceSystem:
     """Subdomain Schur maps + matrix-free S on one GPU (or one row band)."""
 
@@ -197,6 +212,21 @@ class GpuInterfaceSystem:
         self._operators = None
         self.sweep = SweepConfig()
         self.configure(sweep or SweepConfig())
+
+    # ---- row-band ranks on separate GPUs
+    def enable_peer_memory(self):
+        """Run the fused apply (and GMRES's A M v) over every rank's buffers
+        through CUDA IPC: each rank exports its region, the handles are
+        all-gathered in rank order (torch.distributed, already initialised when
+        nranks > 1), and every rank maps its peers' regions.  Tiles then write
+        their output blocks and completion counters directly in the owner's
+        HBM (NVLink), replacing the per-step NCCL exchange.  With nranks = 1
+        the same path runs on one GPU (the protocol minus the peers)."""
+        h = (C.c_uint8 * 64)()
+        self.ctx.call("hs_peer_export", h)
+        allh = gather_peer_handles(bytes(h), self.rank, self.nranks)
+        buf = (C.c_uint8 * len(allh)).from_buffer_copy(allh)
+        self.ctx.call("hs_peer_open", buf, self.nranks)
 
     # ---- resources
     def close(self):

@@ -66,6 +66,9 @@ _SIGS = {
     "hs_set_gmres_mode": (_I, [_P, _I]),
     "hs_set_emulated_ranks": (_I, [_P, _I]),
     "hs_set_trace": (_I, [_P, _I]),
+    "hs_peer_export": (_I, [_P, C.POINTER(C.c_uint8)]),
+    "hs_peer_open": (_I, [_P, C.POINTER(C.c_uint8), _I]),
+    "hs_fused_plan": (_I, [_P, _I, _I, C.POINTER(C.c_int32), _I, C.POINTER(_I)]),
     "hs_get_trace": (_I, [_P, C.POINTER(C.c_uint64), _I, C.POINTER(_I)]),
     "hs_set_fused": (_I, [_P, _I]),
     "hs_memory": (_I, [_P, C.POINTER(C.c_int64)]),

@@ -197,3 +197,28 @@ def test_map_once_gmres_equals_steps(name, c, blocks):
     assert relerr(rb.solution, ra.solution) < 1e-10, relerr(rb.solution, ra.solution)
     ha, hb = np.asarray(ra.history), np.asarray(rb.history)
     assert np.max(np.abs(hb - ha) / ha) < 1e-8
+
+
+@pytest.mark.parametrize("name,c,blocks", [("small_6x3", small_case(6, 3, 16), 5), ("small_4x4_n160", small_case(4, 4, 160), None),
+                                           ("cfg1", CONFIGS[1], None), ("cfg2", CONFIGS[2], 4), ("cfg3", CONFIGS[3], 4)])
+def test_peer_memory_path_single_rank(name, c, blocks):
+    """The multi-GPU peer-memory path (hs_peer_export / hs_peer_open: own
+    region exported through CUDA IPC, the multi-rank kernel launched with
+    self = this rank, system-scope fences) run with one rank on one GPU:
+    bitwise the ordinary fused apply, and the same GMRES (A M v through the
+    peer path) bit for bit."""
+    spec, part = product_problem(c)
+    a = GpuInterfaceSystem(spec, part, sweep=SweepConfig(blocks=blocks))
+    b = GpuInterfaceSystem(spec, part, sweep=SweepConfig(blocks=blocks))
+    b.enable_peer_memory()
+    g = cvec(37, a.layout.size)
+    za = a.bsp_apply(g)
+    for _ in range(2):
+        zb = b.bsp_apply(g)
+        assert np.array_equal(za, zb), (name, relerr(zb, za))
+    rhs = a.rhs() if c.get("center") is not None else cvec(5, a.layout.size)
+    ra = a.gmres(rhs, "bsp", tol=1e-8, maxit=300)
+    rb = b.gmres(rhs, "bsp", tol=1e-8, maxit=300)
+    assert ra.iterations == rb.iterations and np.array_equal(ra.solution, rb.solution)
+    with pytest.raises(ValueError):
+        b.enable_peer_memory()  # already open
