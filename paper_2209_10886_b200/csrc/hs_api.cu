@@ -672,10 +672,17 @@ int fused_plan_host(const Ctx* c, const Plan& P, const std::vector<StepTable>& f
   // width (cfg5, 1024 columns, ms per apply TMA / register streaming: 1.43 / 1.50)
   f.tma = f.tma && (f.map_once || f.maxK <= 512);
   if (const char* e = getenv("HS_FUSED_TMA")) f.tma = atoi(e) != 0 && f.rt == 1;
+  // TMA ring: 5 stages / 2 CTAs per SM, or 12 stages / 1 CTA per SM for small
+  // plans (< 2 tiles per 5-stage CTA), where a tile's map is prefetched while it
+  // waits (ms per apply, 5 / 12 stages: cfg2 0.100 / 0.087, cfg3 0.205 / 0.249,
+  // cfg5 1.32 / 1.63)
+  f.stages = (int)tiles.size() < 4 * c->num_sms ? 12 : 5;
+  if (const char* e = getenv("HS_TMA_STAGES")) f.stages = atoi(e) == 12 ? 12 : 5;
+  if (f.stages == 12 && (12 * 1024 + f.nv * std::max(f.maxK, 256)) * 16 > 225 * 1024) f.stages = 5;  // must fit one CTA
   bool reorder = true;
   if (const char* e = getenv("HS_FUSED_ORDER")) reorder = atoi(e) != 0;
   if (reorder) {
-    const int workers = (f.tma ? 2 : (f.rt == 1 ? 6 : 1)) * c->num_sms;
+    const int workers = (f.tma ? (f.stages == 12 ? 1 : 2) : (f.rt == 1 ? 6 : 1)) * c->num_sms;
     tiles = schedule_tickets(tiles, deps, tile_inc, tile_cost, P.npairs, workers);
   }
   if (keep_rank >= 0) {

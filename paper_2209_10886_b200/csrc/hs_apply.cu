@@ -807,6 +807,32 @@ cudaError_t set_step_smem_limit() {
                               200 * 1024);
 }
 
+// TMA-staged fused kernel with an ST-stage ring: the grid is every CTA that
+// fits (ST = 5: two CTAs per SM, the map stream's bytes in flight; ST = 12:
+// one CTA per SM holding up to 192 KB of a tile's map while it waits for its
+// inputs -- for critical-path-bound plans).  G > 1: emulated ranks, grid a
+// multiple of G.
+template <int ST, bool MR>
+cudaError_t launch_tma(Ctx& c, const DevFused& f, const FusedArgs& a, int G) {
+  constexpr int NWt = kSumWarps;
+  const size_t smem = (size_t)(ST * kChunk + f.nv * std::max(f.maxK, NWt * 32)) * sizeof(double2);
+  static int per_sm = 0;
+  static size_t per_sm_smem = 0;
+  if (per_sm == 0 || per_sm_smem != smem) {
+    cudaError_t ae = cudaFuncSetAttribute(k_bsp_tma<NWt, ST, MR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (ae != cudaSuccess) return ae;  // does not fit one CTA per SM
+    cudaFuncSetAttribute(k_bsp_tma<NWt, ST, MR>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaError_t oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsp_tma<NWt, ST, MR>, (NWt + 1) * 32, smem);
+    if (getenv("HS_DEBUG")) fprintf(stderr, "k_bsp_tma<%d>: smem %zu per_sm %d (%s)\n", ST, smem, per_sm, cudaGetErrorString(oe));
+    per_sm = std::max(1, per_sm);
+    per_sm_smem = smem;
+  }
+  const int grid = G > 1 ? std::max(G, (per_sm * c.num_sms / G) * G) : std::max(1, std::min(std::max(1, f.ntiles), per_sm * c.num_sms));
+  c.launches++;
+  k_bsp_tma<NWt, ST, MR><<<grid, (NWt + 1) * 32, smem, c.stream>>>(a);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double2* zL, double2* rp,
                              double2* w, double2* z, double2* wout) {
   // TMA-staged (k_bsp_tma) or register streaming (k_bsp_fused: variant 0 = 1 strip
@@ -814,22 +840,6 @@ cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double
   if (f.tma) {
     // 8 consumer warps, 5 x 16 KB stages: 2 CTAs per SM (measured on B200 against
     // 16 warps, 3 or 10 stages; tools/run_bsp_variants.sh)
-    constexpr int NWt = kSumWarps, ST = 5;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_bsp_tma<NWt, ST, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-      cudaFuncSetAttribute(k_bsp_tma<NWt, ST, false>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      attr = true;
-    }
-    const size_t smem = (size_t)(ST * kChunk + f.nv * std::max(f.maxK, NWt * 32)) * sizeof(double2);
-    static int per_sm = 0;
-    static size_t per_sm_smem = 0;
-    if (per_sm == 0 || per_sm_smem != smem) {
-      cudaError_t oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsp_tma<NWt, ST, false>, (NWt + 1) * 32, smem);
-      if (getenv("HS_DEBUG")) fprintf(stderr, "k_bsp_tma: smem %zu per_sm %d (%s)\n", smem, per_sm, cudaGetErrorString(oe));
-      per_sm = std::max(1, per_sm);
-      per_sm_smem = smem;
-    }
     cudaError_t e = cudaMemsetAsync(f.counters, 0, (c.plan.npairs + 1) * sizeof(int), c.stream);
     if (e != cudaSuccess) return e;
     FusedArgs a;
@@ -839,10 +849,7 @@ cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double
     a.ntiles = f.ntiles; a.n = c.n; a.maxK = f.maxK; a.nv = f.nv;
     a.trace = (c.trace_on && c.trace && c.trace_cap >= (size_t)f.ntiles) ? c.trace : nullptr;
     if (a.trace) c.trace_rows = f.ntiles;
-    const int grid = std::max(1, std::min(f.ntiles, per_sm * c.num_sms));
-    c.launches++;
-    k_bsp_tma<NWt, ST, false><<<grid, (NWt + 1) * 32, smem, c.stream>>>(a);
-    return cudaGetLastError();
+    return f.stages == 12 ? launch_tma<12, false>(c, f, a, 1) : launch_tma<5, false>(c, f, a, 1);
   }
   static_assert(kSumWarps == 8, "register-streaming fused kernels are instantiated for 8 warps");
   const int var = f.rt == 2 ? 2 : 0;
@@ -898,23 +905,11 @@ cudaError_t launch_bsp_fused_ranks(Ctx& c, const DevFused& f, const MultiRankArg
   a.done = nullptr; a.ticket = nullptr;
   a.ntiles = 0; a.n = c.n; a.maxK = f.maxK; a.nv = f.nv; a.trace = nullptr;
   a.mr = mr;
-  c.launches++;
   const int G = mr.self < 0 ? mr.G : 1;
   if (f.tma) {
-    constexpr int NWt = kSumWarps, ST = 5;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_bsp_tma<NWt, ST, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-      cudaFuncSetAttribute(k_bsp_tma<NWt, ST, true>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      attr = true;
-    }
-    const size_t smem = (size_t)(ST * kChunk + f.nv * std::max(f.maxK, NWt * 32)) * sizeof(double2);
-    int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsp_tma<NWt, ST, true>, (NWt + 1) * 32, smem);
-    const int grid = std::max(G, (std::max(1, per_sm) * c.num_sms / G) * G);
-    k_bsp_tma<NWt, ST, true><<<grid, (NWt + 1) * 32, smem, c.stream>>>(a);
-    return cudaGetLastError();
+    return f.stages == 12 ? launch_tma<12, true>(c, f, a, G) : launch_tma<5, true>(c, f, a, G);
   }
+  c.launches++;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_bsp_fused<8, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);

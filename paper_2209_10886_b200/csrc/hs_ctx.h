@@ -144,6 +144,7 @@ struct DevFused {
   int rt = 1;               // 32-row strips per tile
   int nw = 8;               // warps per CTA (consumer warps for the TMA kernel)
   bool tma = true;          // TMA-staged maps (k_bsp_tma), else register streaming (k_bsp_fused)
+  int stages = 5;           // TMA ring depth: 5 (two CTAs per SM) or 12 (one CTA per SM)
   int* counters = nullptr;  // [npairs] block completion counters + [1] ticket
   double bytes = 0;         // algorithmic bytes of one apply
   bool built = false;
