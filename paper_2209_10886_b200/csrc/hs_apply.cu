@@ -165,11 +165,12 @@ struct RankView {
       default: return a.wout;
     }
   }
-  // publishing a tile's stores before its signals: to the whole system when
-  // the owners are other GPUs
+  // release (a tile's stores before its signals) / acquire (the producers'
+  // stores before a tile's reads) -- acq_rel, not the sequentially consistent
+  // __threadfence(); system scope when the owners are other GPUs
   __device__ void fence() const {
-    if (MR && a.mr.self >= 0) __threadfence_system();
-    else __threadfence();
+    if (MR && a.mr.self >= 0) asm volatile("fence.acq_rel.sys;" ::: "memory");
+    else asm volatile("fence.acq_rel.gpu;" ::: "memory");
   }
 };
 
@@ -367,7 +368,7 @@ __global__ void __launch_bounds__(NW * 32, RT == 1 ? 6 : 1) k_bsp_fused(FusedArg
       const volatile int* p = rv.done(dp.block);
       while (*p < dp.count) __nanosleep(32);
     }
-    __threadfence();
+    rv.fence();  // acquire: the producers' stores before this CTA's reads
     __syncthreads();
     if (tr && threadIdx.x == 0) tr[2] = gtimer();
     const int K = sb.k * n;
@@ -453,6 +454,12 @@ __global__ void __launch_bounds__(NW * 32, RT == 1 ? 6 : 1) k_bsp_fused(FusedArg
 // register-streaming kernel idles ~30 % of a tile's time at cfg3 on the
 // dependency wait, slab load and epilogue; profiles/r01/fused_trace_summary.txt).
 // Same arithmetic order as k_step1 (bitwise identical).
+struct SigRec {  // a tile's completions, handed from the consumers to the signaller warp
+  int phase, nlow, r0, r1;
+  int tgt[4];
+  unsigned long long* tr;
+};
+
 struct TileDesc {
   long long map_off;  // element offset of the tile's 32-row strip
   int t, K, phase, flags, alt, in_off, rlo, rhi, row0, dep0, ndep, rmask, nlow, c0, c1;
@@ -495,23 +502,41 @@ __device__ __forceinline__ void consumers_sync(int nthreads) {
 constexpr int kChunk = 32 * kRowTile;  // elements of one 32-column chunk of a strip
 
 template <int NW, int S, bool MR>
-__global__ void __maxnreg__(96) k_bsp_tma(FusedArgs a) {  // 96: two 9-warp CTAs per SM (per-SMSP register file)
+__global__ void __maxnreg__(96) k_bsp_tma(FusedArgs a) {  // 96: two 10-warp CTAs per SM (per-SMSP register file)
   const RankView<MR> rv(a);
   const int cr = rv.cr;
   extern __shared__ __align__(128) double2 smt[];
   double2* stage = smt;                // S x kChunk
   double2* xs = stage + S * kChunk;    // maxK
   double2* part = xs;                  // nv x NW x 32 partial sums, reusing the slab once consumed
-  __shared__ __align__(8) unsigned long long full[S], empty[S], dfull[2], dempty[2];
+  __shared__ __align__(8) unsigned long long full[S], empty[S], dfull[2], dempty[2], sfull[2], sempty[2];
   __shared__ TileDesc desc[2];
+  __shared__ SigRec sig[2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int NT = NW * 32;
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], NW); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&dfull[i], 1); mbar_init(&dempty[i], NW); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&dfull[i], 1); mbar_init(&dempty[i], NW);
+      mbar_init(&sfull[i], 1); mbar_init(&sempty[i], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  if (warp == NW + 1) {  // ---- signaller: publishes each tile's completions off the consumers' path
+    if (lane == 0) {
+      for (int q = 0;; ++q) {
+        const int d = q & 1;
+        mbar_wait(&sfull[d], (q >> 1) & 1);  // acquire: warp 0's epilogue stores
+        const SigRec r = sig[d];
+        mbar_arrive(&sempty[d]);
+        if (r.phase < 0) break;
+        tile_signal(rv, r.phase, r.r0, r.r1, a.n, r.nlow, r.tgt);
+        if (r.tr) r.tr[4] = gtimer();
+      }
+    }
+    return;
+  }
   if (warp == NW) {  // ---- producer
     if (lane == 0) {
       const unsigned long long pol = l2_evict_first();
@@ -560,7 +585,14 @@ __global__ void __maxnreg__(96) k_bsp_tma(FusedArgs a) {  // 96: two 9-warp CTAs
     const TileDesc td = desc[d];
     __syncwarp();
     if (lane == 0) mbar_arrive(&dempty[d]);
-    if (td.t >= rv.ntiles()) break;
+    if (td.t >= rv.ntiles()) {
+      if (threadIdx.x == 0) {  // tell the signaller to stop
+        mbar_wait(&sempty[q & 1], ((q >> 1) & 1) ^ 1);
+        sig[q & 1].phase = -1;
+        mbar_arrive(&sfull[q & 1]);
+      }
+      break;
+    }
     unsigned long long* tr = (a.trace && !MR) ? a.trace + 6ll * td.t : nullptr;
     if (tr && threadIdx.x == 0) {
       tr[0] = td.claimed;
@@ -571,7 +603,7 @@ __global__ void __maxnreg__(96) k_bsp_tma(FusedArgs a) {  // 96: two 9-warp CTAs
       const volatile int* p = rv.done(dp.block);
       while (*p < dp.count) __nanosleep(32);
     }
-    __threadfence();
+    rv.fence();  // acquire: the producers' stores before this CTA's reads
     consumers_sync(NT);
     if (tr && threadIdx.x == 0) tr[2] = gtimer();
     // warp 0 (lane = output row) fetches its epilogue operands now, in the
@@ -648,15 +680,20 @@ __global__ void __maxnreg__(96) k_bsp_tma(FusedArgs a) {  // 96: two 9-warp CTAs
         for (int w = 1; w < NW; ++w) y2 = cadd(y2, part[(NW + w) * 32 + lane]);
       }
       if (erow_ok) epi_store(rv, td.phase, td.flags, elow, eo, eoff, y1, y2, e1, e2, e3);
-    }
-    consumers_sync(NT);
-    if (threadIdx.x == 0) {  // nothing waits on the (I - S) z tiles
-      tile_signal(rv, td.phase, max(td.rlo, td.row0), min(td.rhi, td.row0 + kRowTile), n, td.nlow, td.tgt);
-      if (tr) {
-        tr[4] = gtimer();
-        tr[5] = ((unsigned long long)smid() << 32) | ((unsigned)blockIdx.x << 8) | (unsigned)td.phase;
+      __syncwarp();
+      if (lane == 0) {  // hand the completion signals to the signaller warp
+        mbar_wait(&sempty[q & 1], ((q >> 1) & 1) ^ 1);
+        SigRec& r = sig[q & 1];
+        r.phase = td.phase; r.nlow = td.nlow;
+        r.r0 = max(td.rlo, td.row0); r.r1 = min(td.rhi, td.row0 + kRowTile);
+        for (int f = 0; f < 4; ++f) r.tgt[f] = td.tgt[f];
+        r.tr = tr;
+        if (tr) tr[5] = ((unsigned long long)smid() << 32) | ((unsigned)blockIdx.x << 8) | (unsigned)td.phase;
+        mbar_arrive(&sfull[q & 1]);  // release: this warp's epilogue stores
       }
     }
+    // no CTA barrier here: the next tile's slab overwrites the partial sums only
+    // after the next consumers_sync, which warp 0 joins after its epilogue
   }
 }
 
@@ -822,14 +859,14 @@ cudaError_t launch_tma(Ctx& c, const DevFused& f, const FusedArgs& a, int G) {
     cudaError_t ae = cudaFuncSetAttribute(k_bsp_tma<NWt, ST, MR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (ae != cudaSuccess) return ae;  // does not fit one CTA per SM
     cudaFuncSetAttribute(k_bsp_tma<NWt, ST, MR>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaError_t oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsp_tma<NWt, ST, MR>, (NWt + 1) * 32, smem);
+    cudaError_t oe = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bsp_tma<NWt, ST, MR>, (NWt + 2) * 32, smem);
     if (getenv("HS_DEBUG")) fprintf(stderr, "k_bsp_tma<%d>: smem %zu per_sm %d (%s)\n", ST, smem, per_sm, cudaGetErrorString(oe));
     per_sm = std::max(1, per_sm);
     per_sm_smem = smem;
   }
   const int grid = G > 1 ? std::max(G, (per_sm * c.num_sms / G) * G) : std::max(1, std::min(std::max(1, f.ntiles), per_sm * c.num_sms));
   c.launches++;
-  k_bsp_tma<NWt, ST, MR><<<grid, (NWt + 1) * 32, smem, c.stream>>>(a);
+  k_bsp_tma<NWt, ST, MR><<<grid, (NWt + 2) * 32, smem, c.stream>>>(a);
   return cudaGetLastError();
 }
 
