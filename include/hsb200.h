@@ -128,6 +128,12 @@ int hs_set_precond_options(hs_ctx* ctx, int seam_mode, int intermediate_residual
 
 /* z = M r for M in {identity, SP = S_U^-1 S_L^-1, BSP}. */
 int hs_precond(hs_ctx* ctx, int kind, const double* r, double* z, int nrhs, int mem);
+/* hs_precond on a batch of nvec independent HOST vectors (r[i] -> z[i], each
+ * L x nrhs; pinned memory for full speed), pipelined: vector i+1 is copied in
+ * and vector i-1 copied out on two copy streams while vector i is applied
+ * (double-buffered device slots).  Returns when every z[i] is on the host.
+ * The serving form of the SPEC.md:340-348 apply. */
+int hs_precond_batch(hs_ctx* ctx, int kind, const double* const* r, double* const* z, int nvec, int nrhs);
 
 /* One block-Jacobi half (bj_half_apply) with the configured
  * windows; with one window per direction it is forward_sweep / backward_sweep. */

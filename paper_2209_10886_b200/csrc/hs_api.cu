@@ -1350,6 +1350,10 @@ int hs_destroy(hs_ctx* c) {
     for (auto& p : c->ev_pending) { cudaEventDestroy(p.first); cudaEventDestroy(p.second); }
     for (auto e : c->ev_pool) cudaEventDestroy(e);
     if (c->nccl) ncclCommDestroy((ncclComm_t)c->nccl);
+    for (auto e : c->bev)
+      if (e) cudaEventDestroy(e);
+    if (c->copy_in) cudaStreamDestroy(c->copy_in);
+    if (c->copy_out) cudaStreamDestroy(c->copy_out);
     cudaStreamDestroy(c->stream);
   }
   delete c;
@@ -1702,6 +1706,48 @@ int hs_precond(hs_ctx* c, int kind, const double* r, double* z, int nrhs, int me
   if (int e = dev_out(c, z, LR, mem, "out", &dz)) return e;
   if (int e_ = do_precond(c, kind, dr, dz, nrhs)) return e_;
   return finish_out(c, z, dz, LR, mem);
+}
+
+// A batch of independent host vectors through the preconditioner, pipelined
+// over two copy streams and two device slots: vector i+1 lands (H2D) and
+// vector i-1 drains (D2H) while vector i is applied, so each vector's copies
+// hide behind a neighbour's apply.  Every vector still makes the full round
+// trip host -> HBM -> host.
+int hs_precond_batch(hs_ctx* c, int kind, const double* const* r, double* const* z, int nvec, int nrhs) {
+  if (!c) return fail(nullptr, 1, "null context");
+  if (nvec < 0 || (nvec > 0 && (!r || !z))) return fail(c, 1, "bad batch");
+  if (int e = check_ready(c, nrhs)) return e;
+  if (nvec == 0) return 0;
+  const long long LR = LRof(c, nrhs);
+  const size_t bytes = LR * sizeof(double2);
+  if (!c->copy_in) {
+    CK(cudaStreamCreateWithFlags(&c->copy_in, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->copy_out, cudaStreamNonBlocking));
+    for (auto& e : c->bev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  double2 *din[2], *dout[2];
+  if (ws_get(c, "bin0", LR, &din[0]) || ws_get(c, "bin1", LR, &din[1]) || ws_get(c, "bout0", LR, &dout[0]) ||
+      ws_get(c, "bout1", LR, &dout[1]))
+    return -1;
+  cudaEvent_t* landed = c->bev;       // [2] input slot filled
+  cudaEvent_t* applied = c->bev + 2;  // [2] apply done: input slot free, output ready
+  cudaEvent_t* drained = c->bev + 4;  // [2] output copied out: output slot free
+  for (int i = 0; i < nvec; ++i) {
+    const int s = i & 1;
+    if (i >= 2) CK(cudaStreamWaitEvent(c->copy_in, applied[s], 0));
+    CK(cudaMemcpyAsync(din[s], r[i], bytes, cudaMemcpyHostToDevice, c->copy_in));
+    CK(cudaEventRecord(landed[s], c->copy_in));
+    CK(cudaStreamWaitEvent(c->stream, landed[s], 0));
+    if (i >= 2) CK(cudaStreamWaitEvent(c->stream, drained[s], 0));
+    if (int e_ = do_precond(c, kind, din[s], dout[s], nrhs)) return e_;
+    CK(cudaEventRecord(applied[s], c->stream));
+    CK(cudaStreamWaitEvent(c->copy_out, applied[s], 0));
+    CK(cudaMemcpyAsync(z[i], dout[s], bytes, cudaMemcpyDeviceToHost, c->copy_out));
+    CK(cudaEventRecord(drained[s], c->copy_out));
+  }
+  CK(cudaStreamSynchronize(c->copy_out));
+  CK(cudaStreamSynchronize(c->stream));
+  return 0;
 }
 
 int hs_half_apply(hs_ctx* c, int direction, const double* r, double* z, int nrhs, int mem) {

@@ -264,6 +264,8 @@ struct Ctx {
   size_t Tcls_elems = 0;
   // device state
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_in = nullptr, copy_out = nullptr;  // host-batch pipeline (hs_precond_batch)
+  cudaEvent_t bev[6] = {};                              // per slot: input landed, applied, output drained
   double2* T = nullptr;
   size_t T_elems = 0;
   DevSub* dsubs = nullptr;

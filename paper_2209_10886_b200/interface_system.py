@@ -287,6 +287,33 @@ class GpuInterfaceSystem:
                           native.HS_MEM_HOST)
         return out[:, 0] if directions is None else out
 
+    def precondition_batch(self, rs, kind: str = "bsp", out=None):
+        """Apply the preconditioner to a batch of independent HOST vectors
+        (numpy arrays or CPU torch tensors, all the same shape; pinned torch
+        tensors copy at full PCIe rate), pipelined so that each vector's
+        host<->device copies overlap a neighbour's apply (hs_precond_batch).
+        `out`: optional list of preallocated outputs of the inputs' kind."""
+        if kind not in _PC:
+            raise ValueError(f"unknown preconditioner {kind!r}")
+        vs = [_Vec(self.layout.check(r), self.layout.size) for r in rs]
+        if any(not v.cpu for v in vs):
+            raise ValueError("precondition_batch takes host vectors (use bsp_apply for device tensors)")
+        if len({v.shape for v in vs}) > 1:
+            raise ValueError("precondition_batch: all vectors must have the same shape")
+        if out is None:
+            outs = [v.empty()[0] for v in vs]
+        else:
+            outs = list(out)
+            if len(outs) != len(vs):
+                raise ValueError("precondition_batch: one output per input")
+        optrs = [(o.data_ptr() if hasattr(o, "data_ptr") else o.ctypes.data) for o in outs]
+        n = len(vs)
+        rp = (C.c_void_p * max(n, 1))(*[v.ptr for v in vs])
+        zp = (C.c_void_p * max(n, 1))(*optrs)
+        if n:
+            self.ctx.call("hs_precond_batch", _PC[kind], rp, zp, n, vs[0].R)
+        return outs if out is not None else [v.wrap(o) for v, o in zip(vs, outs)]
+
     def apply_scattering(self, g):
         return self._call_io("hs_apply", g, pre=(native.HS_APPLY_S,))
 

@@ -222,3 +222,27 @@ def test_peer_memory_path_single_rank(name, c, blocks):
     assert ra.iterations == rb.iterations and np.array_equal(ra.solution, rb.solution)
     with pytest.raises(ValueError):
         b.enable_peer_memory()  # already open
+
+
+@pytest.mark.parametrize("name,c,blocks", [("small_6x3", small_case(6, 3, 16), 5), ("cfg2", CONFIGS[2], 4)])
+def test_precondition_batch_pipelined(name, c, blocks):
+    """hs_precond_batch (host vectors copied in / out on two copy streams
+    while the neighbouring vector is applied) returns bitwise the one-call
+    result for every vector, numpy and pinned torch alike, for odd and even
+    batch sizes and for SP as well as BSP."""
+    spec, part = product_problem(c)
+    s = GpuInterfaceSystem(spec, part, sweep=SweepConfig(blocks=blocks))
+    gs = [cvec(41 + i, s.layout.size) for i in range(5)]
+    for kind in ("bsp", "sp"):
+        ref = [s.precondition(g, kind) for g in gs]
+        for nb in (1, 2, 5):
+            out = s.precondition_batch(gs[:nb], kind)
+            for a, b in zip(out, ref):
+                assert np.array_equal(a, b), (name, kind, nb)
+    pin = [torch.from_numpy(g).pin_memory() for g in gs[:3]]
+    zs = [torch.empty_like(p).pin_memory() for p in pin]
+    s.precondition_batch(pin, out=zs)
+    for i in range(3):
+        assert np.array_equal(zs[i].numpy(), s.precondition(gs[i], "bsp"))
+    with pytest.raises(ValueError):
+        s.precondition_batch([torch.from_numpy(gs[0]).cuda()])
