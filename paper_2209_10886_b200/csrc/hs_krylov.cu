@@ -380,9 +380,9 @@ __global__ void k_combine(GmresDev G, int mmax, double2* u) {
   }
 }
 
-// k_mgs1 partials [2][3][kMgs1MaxGrid] followed by the grid-barrier counter
+// k_mgs1 partials [2][6][kMgs1MaxGrid] followed by the grid-barrier counter
 // shared by k_mgs and k_mgs1 (same stream: launches never overlap).
-static constexpr int kGridScratch = 2 * 3 * 256 + 16;  // doubles
+static constexpr int kGridScratch = 2 * 6 * 256 + 16;  // doubles
 cudaError_t ensure_grid_scratch(Ctx& c) {
   if (c.mgs1_slots) return cudaSuccess;
   cudaError_t e = cudaMalloc((void**)&c.mgs1_slots, (size_t)kGridScratch * sizeof(double));
@@ -390,7 +390,7 @@ cudaError_t ensure_grid_scratch(Ctx& c) {
   c.mgs1_bar = 0;
   return e;
 }
-static unsigned* grid_bar(Ctx& c) { return (unsigned*)(c.mgs1_slots + 2 * 3 * 256); }
+static unsigned* grid_bar(Ctx& c) { return (unsigned*)(c.mgs1_slots + 2 * 6 * 256); }
 
 static int pow2_floor(int x) {
   int p = 1;
@@ -783,17 +783,18 @@ static __device__ __forceinline__ void warp_sum3(double& a, double& b, double& c
   }
 }
 
-constexpr int kMgs1MaxGrid = 256;   // partials: [2 parities][3 components][kMgs1MaxGrid]
-static_assert(kGridScratch == 2 * 3 * kMgs1MaxGrid + 16, "grid scratch layout");
+constexpr int kMgs1MaxGrid = 256;   // partials: [2 parities][6 components][kMgs1MaxGrid]
+constexpr int kMgs1Comp = 6;
+static_assert(kGridScratch == 2 * kMgs1Comp * kMgs1MaxGrid + 16, "grid scratch layout");
 constexpr int kMgs1MaxBlock = 896;  // 72 registers per thread
 
 template <int E>
 __global__ void __launch_bounds__(kMgs1MaxBlock, 1) k_mgs1(GmresDev G, int k, int chunk, int nbuf, double* slots, unsigned* bar, unsigned bar_base) {
   extern __shared__ __align__(16) double2 sm1[];
-  __shared__ double red[32][3];
-  __shared__ double red2[1][3];
+  __shared__ double red[32][kMgs1Comp];
+  __shared__ double red2[kMgs1Comp];
   const int BD = blockDim.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = BD >> 5;
-  auto buf = [&](int j) { return sm1 + (size_t)(j % nbuf) * chunk; };  // v_j (nbuf = 2 or 3 slices)
+  auto buf = [&](int j) { return sm1 + (size_t)(j % nbuf) * chunk; };  // v_j (nbuf = 2, 3 or 4 slices)
   double2* hs = sm1 + (size_t)nbuf * chunk;  // k + 2: the column (CTA 0)
   double2* sns = hs + (k + 2);     // k
   double* css = (double*)(sns + k);  // k
@@ -801,6 +802,7 @@ __global__ void __launch_bounds__(kMgs1MaxBlock, 1) k_mgs1(GmresDev G, int k, in
   const long long e0 = (long long)blockIdx.x * chunk;
   const long long eend = min(e0 + (long long)chunk, LR);
   const int nblk = gridDim.x;
+  const bool pairs = nbuf == 4;  // two MGS steps per grid barrier
   double2* w = G.V + (long long)(k + 1) * LR;
   double2 wr[E];
 #pragma unroll
@@ -819,56 +821,71 @@ __global__ void __launch_bounds__(kMgs1MaxBlock, 1) k_mgs1(GmresDev G, int k, in
     cpa_commit();
   };
   int step = 0;
-  // block sum, publish, grid barrier, collect: (a, b, c) summed over the grid
-  // in a fixed order, returned identically to every thread of every CTA.
+  // block sum, publish, grid barrier, collect: x[0..5] summed over the grid in
+  // a fixed order, returned identically to every thread of every CTA.
   // Partials are stored component-major so the collecting warp's loads are
-  // fully coalesced (37 sectors per component at 148 CTAs; a CTA-major layout
-  // is 3.5x slower: 7 vs 2 us per step, tools/allreduce_bench.cu).
-  auto reduce = [&](double a, double b, double c, int pf_j) {
-    double* P = slots + (size_t)(step & 1) * 3 * kMgs1MaxGrid;
-    warp_sum3(a, b, c);
-    if (lane == 0) { red[wid][0] = a; red[wid][1] = b; red[wid][2] = c; }
+  // fully coalesced (a CTA-major layout is 3.5x slower: 7 vs 2 us per step,
+  // tools/allreduce_bench.cu).  pf0 / pf1 >= 0: basis vectors to prefetch.
+  auto reduce = [&](double (&x)[kMgs1Comp], int pf0, int pf1) {
+    double* P = slots + (size_t)(step & 1) * kMgs1Comp * kMgs1MaxGrid;
+    warp_sum3(x[0], x[1], x[2]);
+    warp_sum3(x[3], x[4], x[5]);
+    if (lane == 0)
+#pragma unroll
+      for (int q = 0; q < kMgs1Comp; ++q) red[wid][q] = x[q];
     __syncthreads();
     if (wid == 0) {
-      a = lane < nw ? red[lane][0] : 0.0;
-      b = lane < nw ? red[lane][1] : 0.0;
-      c = lane < nw ? red[lane][2] : 0.0;
-      warp_sum3(a, b, c);
-      if (lane == 0) {
-        P[blockIdx.x] = a;
-        P[kMgs1MaxGrid + blockIdx.x] = b;
-        P[2 * kMgs1MaxGrid + blockIdx.x] = c;
-      }
+#pragma unroll
+      for (int q = 0; q < kMgs1Comp; ++q) x[q] = lane < nw ? red[lane][q] : 0.0;
+      warp_sum3(x[0], x[1], x[2]);
+      warp_sum3(x[3], x[4], x[5]);
+      if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < kMgs1Comp; ++q) P[q * kMgs1MaxGrid + blockIdx.x] = x[q];
     }
     // a basis vector issued here streams while the CTA waits at the barrier;
     // issued after the barrier its loads would queue ahead of the partials
-    if (pf_j >= 0) prefetch(pf_j);
+    if (pf0 >= 0) prefetch(pf0);
+    if (pf1 >= 0) prefetch(pf1);
     grid_barrier(bar, bar_base + (unsigned)(step + 1) * (unsigned)nblk);
     if (wid == 0) {
-      double xa[kMgs1MaxGrid / 32], xb[kMgs1MaxGrid / 32], xc[kMgs1MaxGrid / 32];
+      const int nc = pairs ? kMgs1Comp : 3;  // one step per barrier publishes 3 components
 #pragma unroll
-      for (int u = 0; u < kMgs1MaxGrid / 32; ++u) {
-        const int q = lane + 32 * u;
-        xa[u] = q < nblk ? __ldcg(P + q) : 0.0;
-        xb[u] = q < nblk ? __ldcg(P + kMgs1MaxGrid + q) : 0.0;
-        xc[u] = q < nblk ? __ldcg(P + 2 * kMgs1MaxGrid + q) : 0.0;
+      for (int q = 0; q < kMgs1Comp; ++q) {
+        if (q >= nc) {
+          x[q] = 0.0;
+          continue;
+        }
+        double xs[kMgs1MaxGrid / 32];
+#pragma unroll
+        for (int u = 0; u < kMgs1MaxGrid / 32; ++u) {
+          const int t = lane + 32 * u;
+          xs[u] = t < nblk ? __ldcg(P + q * kMgs1MaxGrid + t) : 0.0;
+        }
+        double a = 0.0;
+#pragma unroll
+        for (int u = 0; u < kMgs1MaxGrid / 32; ++u) a += xs[u];
+        x[q] = a;
       }
-      a = b = c = 0.0;
+      warp_sum3(x[0], x[1], x[2]);
+      warp_sum3(x[3], x[4], x[5]);
+      if (lane == 0)
 #pragma unroll
-      for (int u = 0; u < kMgs1MaxGrid / 32; ++u) { a += xa[u]; b += xb[u]; c += xc[u]; }
-      warp_sum3(a, b, c);
-      if (lane == 0) { red2[0][0] = a; red2[0][1] = b; red2[0][2] = c; }
+        for (int q = 0; q < kMgs1Comp; ++q) red2[q] = x[q];
     }
     __syncthreads();
     ++step;
-    return make_double3(red2[0][0], red2[0][1], red2[0][2]);
+#pragma unroll
+    for (int q = 0; q < kMgs1Comp; ++q) x[q] = red2[q];
   };
-  double3 tot;
-  for (int j = 0; j < nbuf && j <= k; ++j) prefetch(j);
+  double x[kMgs1Comp];
+  // initial lead: v_0..v_{nbuf-1} (pairs: v_0..v_2, each pass then fetches the pair after next)
+  const int lead = pairs ? 3 : nbuf;
+  for (int j = 0; j < lead && j <= k; ++j) prefetch(j);
   if (blockIdx.x == 0)
     for (int j = tid; j < k; j += BD) { css[j] = G.cs[j]; sns[j] = G.sn[j]; }
   {  // v_0 landed: the groups issued after it may still be in flight
-    const int later = min(nbuf, k + 1) - 1;
+    const int later = min(lead, k + 1) - 1;
     if (later >= 2) cpa_wait<2>(); else if (later == 1) cpa_wait<1>(); else cpa_wait<0>();
   }
   // j = 0: <v_0, w> and ||w||^2 before orthogonalisation
@@ -882,37 +899,96 @@ __global__ void __launch_bounds__(kMgs1MaxBlock, 1) k_mgs1(GmresDev G, int k, in
         cfma_conj(acc, v0[tid + i * BD], wr[i]);
         nrm += wr[i].x * wr[i].x + wr[i].y * wr[i].y;
       }
-    tot = reduce(acc.x, acc.y, nrm, -1);
+    x[0] = acc.x; x[1] = acc.y; x[2] = nrm; x[3] = x[4] = x[5] = 0.0;
+    reduce(x, -1, -1);
   }
-  double2 h = make_double2(tot.x, tot.y);
+  double2 h = make_double2(x[0], x[1]);
   if (blockIdx.x == 0 && tid == 0) {
-    G.wnorm0[0] = sqrt(tot.z);
+    G.wnorm0[0] = sqrt(x[2]);
     hs[0] = h;
   }
-  for (int j = 0; j <= k; ++j) {
-    const double2* vj = buf(j);
-    const double2* vn = buf(j + 1);
-    const bool more = j + 1 <= k;
-    if (more) {  // v_{j+1} landed (each thread reads only what it copied); v_{j+2} may be in flight
-      if (nbuf == 3 && j + 2 <= k) cpa_wait<1>(); else cpa_wait<0>();
-    }
-    double2 acc = make_double2(0, 0);
-    double nrm = 0;
+  double hn2 = 0;
+  if (pairs) {
+    // Two MGS steps per barrier.  With the pending update w -= h_p v_p (p =
+    // the previous pair) applied, one pass forms alpha = <v_a, w>, beta =
+    // <v_b, w> and gamma = <v_b, v_a> for the next pair (a, b = a + 1); then
+    // h_a = alpha and h_b = <v_b, w - h_a v_a> = beta - h_a gamma, exactly
+    // the MGS coefficients (rounding differs only at the 1e-16 level).
+    int p0 = 0, p1 = -1;
+    double2 hp0 = h, hp1 = make_double2(0, 0);
+    for (int a = 1;; a += 2) {
+      const int bb = a + 1;
+      const bool ha = a <= k, hb = bb <= k;
+      cpa_wait<0>();  // v_a, v_b (issued before the previous barrier)
+      const double2* vp0 = buf(p0);
+      const double2* vp1 = p1 >= 0 ? buf(p1) : vp0;
+      const double2* va = buf(a);
+      const double2* vb = buf(bb);
+      double2 al = make_double2(0, 0), be = al, ga = al;
+      double nrm = 0;
 #pragma unroll
-    for (int i = 0; i < E; ++i)
-      if (e0 + tid + (long long)i * BD < eend) {
-        wr[i] = csub(wr[i], cmul(h, vj[tid + i * BD]));  // w - H[j,k] V[j]
-        if (more) cfma_conj(acc, vn[tid + i * BD], wr[i]);
-        else nrm += wr[i].x * wr[i].x + wr[i].y * wr[i].y;
+      for (int i = 0; i < E; ++i)
+        if (e0 + tid + (long long)i * BD < eend) {
+          const int o = tid + i * BD;
+          wr[i] = csub(wr[i], cmul(hp0, vp0[o]));
+          if (p1 >= 0) wr[i] = csub(wr[i], cmul(hp1, vp1[o]));
+          if (ha) {
+            const double2 xa = va[o];
+            cfma_conj(al, xa, wr[i]);
+            if (hb) {
+              const double2 xb = vb[o];
+              cfma_conj(be, xb, wr[i]);
+              cfma_conj(ga, xb, xa);
+            }
+          } else {
+            nrm += wr[i].x * wr[i].x + wr[i].y * wr[i].y;
+          }
+        }
+      x[0] = al.x; x[1] = al.y; x[2] = ha ? be.x : nrm; x[3] = be.y; x[4] = ga.x; x[5] = ga.y;
+      // the pending pair's slices are free: the pair after (a, b) goes into them
+      reduce(x, bb + 1 <= k ? bb + 1 : -1, bb + 2 <= k ? bb + 2 : -1);
+      if (!ha) {
+        hn2 = x[2];
+        break;
       }
-    // v_j's slice is free: the vector nbuf steps ahead goes into it
-    tot = reduce(acc.x, acc.y, nrm, j + nbuf <= k ? j + nbuf : -1);
-    if (more) {
-      h = make_double2(tot.x, tot.y);
-      if (blockIdx.x == 0 && tid == 0) hs[j + 1] = h;
+      const double2 h_a = make_double2(x[0], x[1]);
+      const double2 h_b = csub(make_double2(x[2], x[3]), cmul(h_a, make_double2(x[4], x[5])));
+      if (blockIdx.x == 0 && tid == 0) {
+        hs[a] = h_a;
+        if (hb) hs[bb] = h_b;
+      }
+      p0 = a; hp0 = h_a;
+      p1 = hb ? bb : -1; hp1 = h_b;
+    }
+  } else {
+    for (int j = 0; j <= k; ++j) {
+      const double2* vj = buf(j);
+      const double2* vn = buf(j + 1);
+      const bool more = j + 1 <= k;
+      if (more) {  // v_{j+1} landed (each thread reads only what it copied); v_{j+2} may be in flight
+        if (nbuf == 3 && j + 2 <= k) cpa_wait<1>(); else cpa_wait<0>();
+      }
+      double2 acc = make_double2(0, 0);
+      double nrm = 0;
+#pragma unroll
+      for (int i = 0; i < E; ++i)
+        if (e0 + tid + (long long)i * BD < eend) {
+          wr[i] = csub(wr[i], cmul(h, vj[tid + i * BD]));  // w - H[j,k] V[j]
+          if (more) cfma_conj(acc, vn[tid + i * BD], wr[i]);
+          else nrm += wr[i].x * wr[i].x + wr[i].y * wr[i].y;
+        }
+      // v_j's slice is free: the vector nbuf steps ahead goes into it
+      x[0] = acc.x; x[1] = acc.y; x[2] = nrm; x[3] = x[4] = x[5] = 0.0;
+      reduce(x, j + nbuf <= k ? j + nbuf : -1, -1);
+      if (more) {
+        h = make_double2(x[0], x[1]);
+        if (blockIdx.x == 0 && tid == 0) hs[j + 1] = h;
+      } else {
+        hn2 = x[2];
+      }
     }
   }
-  const double hn = sqrt(tot.z);
+  const double hn = sqrt(hn2);
 #pragma unroll
   for (int i = 0; i < E; ++i) {
     const long long e = e0 + tid + (long long)i * BD;
@@ -964,9 +1040,15 @@ cudaError_t gmres_arnoldi1(Ctx& c, GmresDev& G, int k, int grid, int chunk, int 
   double* slots = (double*)c.mgs1_slots;
   unsigned* bar = grid_bar(c);
   unsigned bar_base = c.mgs1_bar;  // counter value before this launch (wraps modulo 2^32)
-  c.mgs1_bar += (unsigned)(k + 2) * (unsigned)grid;
-  // two basis slices (one step of lead for the stream; three measured no faster)
-  int nbuf = 2;
+  // four basis slices: two MGS steps per grid barrier (the pending pair and the
+  // next one); else two slices, one step per barrier (three measured no faster)
+  static const bool pairs_ok = [] {
+    const char* e = getenv("HS_MGS1_PAIRS");
+    return !e || atoi(e) != 0;
+  }();
+  int nbuf = pairs_ok && mgs1_smem(chunk, k, 4) <= kMgs1SmemMax ? 4 : 2;
+  const unsigned nbar = nbuf == 4 ? (unsigned)((k + 1) / 2 + 2) : (unsigned)(k + 2);
+  c.mgs1_bar += nbar * (unsigned)grid;
   void* args[] = {(void*)&G, (void*)&k, (void*)&chunk, (void*)&nbuf, (void*)&slots, (void*)&bar, (void*)&bar_base};
   const size_t smem = mgs1_smem(chunk, k, nbuf);
   const void* fn = E == 1 ? (const void*)k_mgs1<1> : E == 2 ? (const void*)k_mgs1<2>
