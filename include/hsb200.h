@@ -184,8 +184,11 @@ int hs_set_fused(hs_ctx* ctx, int mask);
  * the owner's HBM (NVLink peer stores and system-scope atomics), with no
  * per-step exchange.  hs_peer_export allocates this rank's region and writes
  * its 64-byte IPC handle; after the host has all-gathered the handles (rank
- * order), hs_peer_open maps the peers' regions and enables the path.  Replaces
- * the per-step NCCL send/recv of hs_comm_init's path for the fused apply. */
+ * order), hs_peer_open maps the peers' regions and enables the path.  Between
+ * applies there is no barrier: counters carry epochs, each rank posts its
+ * inputs' epoch and the kernel drains its own blocks (HS_PEER_BARRIERS=1: reset
+ * + two NCCL barriers per apply instead).  Replaces the per-step NCCL
+ * send/recv of hs_comm_init's path for the fused apply. */
 int hs_peer_export(hs_ctx* ctx, uint8_t handle[64]);
 int hs_peer_open(hs_ctx* ctx, const uint8_t* handles, int nranks);
 /* The fused plan a rank runs on that path (plan-only contexts too), for

@@ -694,6 +694,7 @@ int fused_plan_host(const Ctx* c, const Plan& P, const std::vector<StepTable>& f
   f.nitems = (int)items.size();
   f.ntiles = (int)tiles.size();
   f.ndeps = (int)deps.size();
+  f.wtot = written;  // signals per block per apply (every rank's tiles)
   return 0;
 }
 
@@ -994,6 +995,26 @@ void free_peer_plans(Ctx* c) {
     dfree(c, f.counters, 0);
     f = DevFused();
   }
+  dfree(c, p.wtot, 0);
+  p.wtot = nullptr;
+}
+
+int peer_barrier(Ctx* c);
+
+// New plans (other windows / plan kind): the epoch counters restart from zero.
+// Every rank rebuilds at the same point of its call sequence; one barrier so no
+// peer still signals the old epochs, the reset, one barrier so no peer signals
+// the new ones before it.
+int peer_restart_epochs(Ctx* c) {
+  PeerRanks& p = c->peer;
+  if (p.epoch == 0) return 0;
+  CK(cudaStreamSynchronize(c->stream));
+  if (int e = peer_barrier(c)) return e;
+  CK(cudaMemsetAsync(p.counters[c->plan.rank], 0, (c->plan.npairs + 2) * sizeof(int), c->stream));
+  if (int e = peer_barrier(c)) return e;
+  p.epoch = 0;
+  p.epochs = !(getenv("HS_PEER_BARRIERS") && atoi(getenv("HS_PEER_BARRIERS")) != 0);
+  return 0;
 }
 
 void free_peer(Ctx* c) {
@@ -1003,6 +1024,8 @@ void free_peer(Ctx* c) {
     if (p.opened[g]) cudaIpcCloseMemHandle(p.opened[g]);
   dfree(c, p.own, 0);
   dfree(c, p.blk_rank, 0);
+  dfree(c, p.own_blocks, 0);
+  dfree(c, p.wtot, 0);
   dfree(c, p.bar, 0);
   p = PeerRanks();
 }
@@ -1024,11 +1047,23 @@ int peer_plan_host(const Ctx* c, bool ims, int rank, DevFused& f, FusedHost& H) 
 int build_peer_plan(Ctx* c, bool ims) {
   PeerRanks& p = c->peer;
   DevFused& f = ims ? p.plan_ims : p.plan;
+  if (!p.plan.built && !p.plan_ims.built)
+    if (int e = peer_restart_epochs(c)) return e;
   FusedHost H;
   if (int e = peer_plan_host(c, ims, c->plan.rank, f, H)) return e;
   if (upload(c, &f.items, H.items) || upload(c, &f.tiles, H.tiles) || upload(c, &f.deps, H.deps)) return -1;
+  // the epoch protocol needs the same signals per block from every plan
+  // (the BSP and the A M v plans signal the same blocks the same number of times)
+  const DevFused& other = ims ? p.plan : p.plan_ims;
+  if (other.built && other.wtot != f.wtot) p.epochs = false;
+  if (!p.wtot && upload(c, &p.wtot, f.wtot)) return -1;
   f.built = true;
   return 0;
+}
+
+__global__ void k_post_epoch(int* flag, int e) {
+  asm volatile("fence.acq_rel.sys;" ::: "memory");  // this rank's inputs (copied before, stream order) first
+  *(volatile int*)flag = e;
 }
 
 // Stream-ordered barrier of the row-band ranks (a one-element all-reduce).
@@ -1053,10 +1088,24 @@ int do_precond_peer(Ctx* c, const double2* r, double2* z, double2* wout) {
   const long long L = P.L;
   const int me = P.rank;
   double2* mine = p.vec[me];
-  CK(cudaMemcpyAsync(mine + FV_R * L, r, L * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
-  CK(cudaMemsetAsync(p.counters[me], 0, (P.npairs + 1) * sizeof(int), c->stream));
-  if (int e = peer_barrier(c)) return e;
   MultiRankArgs mr;
+  CK(cudaMemcpyAsync(mine + FV_R * L, r, L * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
+  if (p.epochs) {
+    // no barrier: post this rank's inputs for the epoch; the kernel's CTAs wait
+    // for every rank's post, dependencies count from the epoch's base, and the
+    // kernel drains this rank's blocks before it ends
+    mr.epoch = ++p.epoch;
+    mr.wtot = p.wtot;
+    mr.own_blocks = p.own_blocks;
+    mr.n_own = p.n_own;
+    for (int g = 0; g < p.G; ++g) mr.inflag[g] = p.inflag[g];
+    CK(cudaMemsetAsync(p.counters[me] + P.npairs, 0, sizeof(int), c->stream));  // own ticket only
+    c->launches++;
+    k_post_epoch<<<1, 1, 0, c->stream>>>(p.inflag[me], (int)mr.epoch);
+  } else {
+    CK(cudaMemsetAsync(p.counters[me], 0, (P.npairs + 1) * sizeof(int), c->stream));
+    if (int e = peer_barrier(c)) return e;
+  }
   mr.G = p.G;
   mr.self = me;
   mr.blk_rank = p.blk_rank;
@@ -1068,7 +1117,8 @@ int do_precond_peer(Ctx* c, const double2* r, double2* z, double2* wout) {
   mr.tiles[me] = f.tiles;
   mr.ntiles[me] = f.ntiles;
   CK(launch_bsp_fused_ranks(*c, f, mr));
-  if (int e = peer_barrier(c)) return e;
+  if (!p.epochs)
+    if (int e = peer_barrier(c)) return e;
   CK(cudaMemcpyAsync(z, mine + FV_Z * L, L * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
   if (ims) CK(cudaMemcpyAsync(wout, mine + FV_WOUT * L, L * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
   return 0;
@@ -2136,7 +2186,8 @@ int hs_peer_export(hs_ctx* c, uint8_t handle[64]) {
   NEED_GPU(c);
   PeerRanks& p = c->peer;
   const size_t L = (size_t)c->plan.L;
-  const size_t need = FV_N * L * sizeof(double2) + (size_t)(c->plan.npairs + 1) * sizeof(int);
+  // FV_N vectors, npairs completion counters, the ticket, the inputs-posted epoch flag
+  const size_t need = FV_N * L * sizeof(double2) + (size_t)(c->plan.npairs + 2) * sizeof(int);
   if (!p.own || p.bytes != need) {
     dfree(c, p.own, 0);
     p.own = nullptr;
@@ -2181,10 +2232,18 @@ int hs_peer_open(hs_ctx* c, const uint8_t* handles, int nranks) {
     }
     p.vec[g] = (double2*)base;
     p.counters[g] = (int*)(base + FV_N * L * sizeof(double2));
+    p.inflag[g] = p.counters[g] + c->plan.npairs + 1;
   }
-  std::vector<int> br(c->plan.npairs);
-  for (int b = 0; b < c->plan.npairs; ++b) br[b] = c->plan.subs[c->plan.block_sub[b]].rank;
+  std::vector<int> br(c->plan.npairs), own;
+  for (int b = 0; b < c->plan.npairs; ++b) {
+    br[b] = c->plan.subs[c->plan.block_sub[b]].rank;
+    if (br[b] == c->plan.rank) own.push_back(b);
+  }
   if (upload(c, &p.blk_rank, br)) return -1;
+  if (upload(c, &p.own_blocks, own)) return -1;
+  p.n_own = (int)own.size();
+  p.epoch = 0;
+  p.epochs = !(getenv("HS_PEER_BARRIERS") && atoi(getenv("HS_PEER_BARRIERS")) != 0);
   CK(dalloc(c, (void**)&p.bar, sizeof(double2)));
   CK(cudaMemset(p.bar, 0, sizeof(double2)));
   p.G = nranks;

@@ -154,6 +154,31 @@ struct RankView {
   __device__ int ntiles() const { return MR ? a.mr.ntiles[cr] : a.ntiles; }
   __device__ int owner(int block) const { return MR ? a.mr.blk_rank[block] : 0; }
   __device__ int* done(int block) const { return (MR ? a.mr.done[owner(block)] : a.done) + block; }
+  // completion count a dependency waits for (epoch protocol: counters accumulate)
+  __device__ int target(const FusedDep& dp) const {
+    return MR && a.mr.epoch ? dp.count + (int)(a.mr.epoch - 1) * a.mr.wtot[dp.block] : dp.count;
+  }
+  // epoch protocol: wait until every rank has posted this apply's inputs
+  __device__ void wait_inputs() const {
+    if (!MR || !a.mr.epoch) return;
+    for (int g = 0; g < a.mr.G; ++g) {
+      const volatile int* f = a.mr.inflag[g];
+      while (*f < (int)a.mr.epoch) __nanosleep(64);
+    }
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+  }
+  // epoch protocol: this rank's blocks have received every write of this apply
+  // (some come from other ranks' tiles); threads [i0, +stride) share the list
+  __device__ void drain(int i0, int stride) const {
+    if (!MR || !a.mr.epoch) return;
+    for (int i = i0; i < a.mr.n_own; i += stride) {
+      const int b = a.mr.own_blocks[i];
+      const volatile int* p = a.mr.done[cr] + b;
+      const int want = (int)a.mr.epoch * a.mr.wtot[b];
+      while (*p < want) __nanosleep(64);
+    }
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
+  }
   __device__ double2* vec(int k, int rk) const {
     if (MR) return a.mr.v[k][rk];
     switch (k) {
@@ -353,11 +378,16 @@ __global__ void __launch_bounds__(NW * 32, RT == 1 ? 6 : 1) k_bsp_fused(FusedArg
   const int cr = rv.cr;
   const FusedTile* tiles = rv.tiles();
   const int ntiles = rv.ntiles();
+  if (threadIdx.x == 0) rv.wait_inputs();
+  __syncthreads();
   for (;;) {
     if (threadIdx.x == 0) s_t = atomicAdd(rv.ticket(), 1);
     __syncthreads();
     const int t = s_t;
-    if (t >= ntiles) return;
+    if (t >= ntiles) {
+      rv.drain(blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+      return;
+    }
     unsigned long long* tr = (a.trace && !MR) ? a.trace + 6ll * t : nullptr;
     if (tr && threadIdx.x == 0) tr[0] = tr[1] = gtimer();
     const FusedTile ft = tiles[t];
@@ -366,7 +396,7 @@ __global__ void __launch_bounds__(NW * 32, RT == 1 ? 6 : 1) k_bsp_fused(FusedArg
     for (int d = threadIdx.x; d < ft.ndep; d += blockDim.x) {
       const FusedDep dp = a.deps[ft.dep0 + d];
       const volatile int* p = rv.done(dp.block);
-      while (*p < dp.count) __nanosleep(32);
+      while (*p < rv.target(dp)) __nanosleep(32);
     }
     rv.fence();  // acquire: the producers' stores before this CTA's reads
     __syncthreads();
@@ -579,6 +609,8 @@ __global__ void __maxnreg__(96) k_bsp_tma(FusedArgs a) {  // 96: two 10-warp CTA
   constexpr int CPW = 32 / NW;
   const int n = a.n;
   long long g = 0;
+  if (threadIdx.x == 0) rv.wait_inputs();
+  consumers_sync(NT);
   for (int q = 0;; ++q) {
     const int d = q & 1;
     mbar_wait(&dfull[d], (q >> 1) & 1);
@@ -591,6 +623,7 @@ __global__ void __maxnreg__(96) k_bsp_tma(FusedArgs a) {  // 96: two 10-warp CTA
         sig[q & 1].phase = -1;
         mbar_arrive(&sfull[q & 1]);
       }
+      rv.drain(blockIdx.x * NT + threadIdx.x, gridDim.x * NT);
       break;
     }
     unsigned long long* tr = (a.trace && !MR) ? a.trace + 6ll * td.t : nullptr;
@@ -601,7 +634,7 @@ __global__ void __maxnreg__(96) k_bsp_tma(FusedArgs a) {  // 96: two 10-warp CTA
     for (int i = threadIdx.x; i < td.ndep; i += NT) {
       const FusedDep dp = a.deps[td.dep0 + i];
       const volatile int* p = rv.done(dp.block);
-      while (*p < dp.count) __nanosleep(32);
+      while (*p < rv.target(dp)) __nanosleep(32);
     }
     rv.fence();  // acquire: the producers' stores before this CTA's reads
     consumers_sync(NT);

@@ -139,6 +139,7 @@ struct DevFused {
   FusedTile* tiles = nullptr;
   FusedDep* deps = nullptr;
   int nitems = 0, ntiles = 0, ndeps = 0, maxK = 0;
+  std::vector<int> wtot;    // block -> completion signals per apply (all ranks' tiles)
   int nv = 1;               // vectors per tile (2: the map-once plan's phase-4 tiles)
   bool map_once = false;    // map-once plan (else per-step order, bitwise = k_step1)
   int rt = 1;               // 32-row strips per tile
@@ -200,6 +201,17 @@ struct MultiRankArgs {
   int* ticket[kMaxRanks] = {};
   const FusedTile* tiles[kMaxRanks] = {};
   int ntiles[kMaxRanks] = {};
+  // Epoch protocol (separate GPUs, epoch > 0): counters are never reset -- a
+  // dependency (block, count) of apply `epoch` waits for count + (epoch - 1) *
+  // wtot[block]; the consumers first wait until every rank has posted its
+  // inputs for this epoch (inflag[g] >= epoch: its previous apply is over and
+  // its r is in place), and before exiting drain this rank's own blocks
+  // (counter == epoch * wtot): no barrier of any kind between applies.
+  unsigned epoch = 0;
+  const int* wtot = nullptr;           // block -> completion signals per apply
+  const int* inflag[kMaxRanks] = {};   // per rank: last epoch whose inputs are posted
+  const int* own_blocks = nullptr;     // this rank's blocks (drain)
+  int n_own = 0;
 };
 
 // Emulated row bands on one GPU (hs_set_emulated_ranks): per-rank vectors,
@@ -228,8 +240,14 @@ struct PeerRanks {
   double2* vec[kMaxRanks] = {};       // per rank: FV_N x L vectors
   int* counters[kMaxRanks] = {};      // per rank: npairs counters + 1 ticket
   void* opened[kMaxRanks] = {};       // IPC mappings (closed at destroy)
+  int* inflag[kMaxRanks] = {};        // per rank: epoch whose inputs are posted (region tail)
   DevFused plan, plan_ims;            // global plans; tiles = this rank's only
   int* blk_rank = nullptr;            // block -> owner rank
+  int* wtot = nullptr;                // block -> completion signals per apply (same for both plans)
+  int* own_blocks = nullptr;          // this rank's blocks
+  int n_own = 0;
+  unsigned epoch = 0;                 // applies run so far (epoch protocol)
+  bool epochs = true;                 // false: two NCCL barriers per apply (HS_PEER_BARRIERS=1)
   double2* bar = nullptr;             // one-element NCCL barrier buffer
 };
 

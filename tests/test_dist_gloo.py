@@ -299,7 +299,21 @@ def _parse_plan(v):
     return out
 
 
-def _run_peer_tiles(band, plan, V, CNT):
+def _tile_signals(band, rec):
+    """Blocks a tile completes (the kernel's tile_signal rule)."""
+    i1, i2, rlo, rhi, c0, c1, alt, row0, phase, flags, rmask, _ = rec
+    s, n = (i1, i2), band.n
+    if phase in (3, 5):
+        return []
+    nlow = sum(1 for f, _ in band.lat.faces[s] if f in (0, 1))
+    r0, r1 = max(rlo, row0), min(rhi, row0 + 32)
+    return [band.lat.m_index(band.lat.faces[s][f][1], s) - 1 for f in range(r0 // n, (r1 - 1) // n + 1)
+            if phase <= 1 or f < nlow]
+
+
+def _run_peer_tiles(band, plan, V, CNT, base=None):
+    """base: per-block completion count at the start of this apply (epoch
+    protocol: counters are never reset), else zero."""
     import time
     n = band.n
     for rec, deps in plan:
@@ -307,7 +321,8 @@ def _run_peer_tiles(band, plan, V, CNT):
         s = (i1, i2)
         for b, cnt in deps:
             o = band.owner[b]
-            while CNT[o, b] < cnt:
+            want = cnt + (0 if base is None else base[b])
+            while CNT[o, b] < want:
                 time.sleep(0)
         me = band.rank
         k = len(band.lat.faces[s])
@@ -371,13 +386,69 @@ def _run_peer_tiles(band, plan, V, CNT):
                     Vo[FV_WOUT, t] = (Vo[FV_R, t] - Vo[FV_RP, t]) + (Vo[FV_W, t] - a)
                 else:
                     Vo[FV_WOUT, t] = Vo[FV_R, t] - a
-        if phase in (3, 5):
-            continue
-        for f in range(r0 // n, (r1 - 1) // n + 1):
-            if phase <= 1 or f < nlow:
-                _, j = band.lat.faces[s][f]
-                blk = band.lat.m_index(j, s) - 1
-                CNT[band.owner[blk], blk] += 1
+        for blk in _tile_signals(band, rec):
+            CNT[band.owner[blk], blk] += 1
+
+
+def _plan_of(band, ims, rank):
+    import ctypes as C
+    cnt = C.c_int(0)
+    band.ctx.call("hs_fused_plan", int(ims), rank, None, 0, C.byref(cnt))
+    buf = (C.c_int32 * cnt.value)()
+    band.ctx.call("hs_fused_plan", int(ims), rank, buf, cnt.value, C.byref(cnt))
+    return _parse_plan(np.frombuffer(buf, dtype=np.int32))
+
+
+def _peer_epoch_worker(rank, world, port, case, blocks, vbuf, cbuf, fbuf, napply, q):
+    """The barrier-free epoch protocol of the GPU path: for apply e every rank
+    copies in its r, posts e, waits for every rank's post, runs its tiles with
+    dependency counts offset by the blocks' totals of the previous applies,
+    drains its own blocks (counter = e * total) and reads its z -- no barrier
+    between applies; BSP and A M v applies alternate."""
+    import time
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        band = Band(case, rank, world, blocks)
+        plans = {ims: _plan_of(band, ims, rank) for ims in (False, True)}
+        wt = {}
+        for ims in (False, True):  # signals per block per apply: every rank's tiles
+            w = np.zeros(len(band.owner), dtype=np.int64)
+            for r in range(world):
+                for rec, _ in _plan_of(band, ims, r):
+                    for b in _tile_signals(band, rec):
+                        w[b] += 1
+            wt[ims] = w
+        assert np.array_equal(wt[False], wt[True])  # one total per block for both plans
+        W = wt[False]
+        V = vbuf.numpy().view(complex)[..., 0]
+        CNT, FLAG = cbuf.numpy(), fbuf.numpy()
+        own = np.where(band.owner == rank)[0]
+        m = band.owned_mask()
+        from oracle import Preconditioner
+        pc = Preconditioner(band.itf, "bsp", blocks=blocks)
+        dist.barrier()  # buffers zeroed by the parent, every process started
+        errs = []
+        for e in range(1, napply + 1):
+            ims = e % 2 == 0
+            rng = np.random.default_rng(100 + e)
+            r = rng.standard_normal(V.shape[2]) + 1j * rng.standard_normal(V.shape[2])
+            V[rank, FV_R] = r
+            FLAG[rank] = e  # post this epoch's inputs
+            for g in range(world):
+                while FLAG[g] < e:
+                    time.sleep(0)
+            _run_peer_tiles(band, plans[ims], V, CNT, base=(e - 1) * W)
+            for b in own:  # drain: every write into this rank's blocks has landed
+                while CNT[rank, b] < e * W[b]:
+                    time.sleep(0)
+            ref = pc.bsp_apply(r)
+            got = V[rank, FV_WOUT if ims else FV_Z].copy()
+            want = band.itf.apply_A(ref) if ims else ref
+            errs.append(float(np.abs(got[m] - want[m]).max() / np.abs(want).max()))
+        q.put((rank, errs))
+    finally:
+        dist.destroy_process_group()
 
 
 def _peer_worker(rank, world, port, case, blocks, vbuf, cbuf, ims, q):
@@ -439,3 +510,29 @@ def test_peer_memory_protocol_matches_oracle(case, world, blocks, ims):
     for rank, ntiles, ez, ew in res:
         assert ez < 1e-12, (rank, ez)
         assert ew < 1e-12, (rank, ew)
+
+
+@pytest.mark.parametrize("case,world,blocks", [(CASE, 2, None), (CASE5, 3, 4)])
+def test_peer_memory_epoch_protocol(case, world, blocks):
+    """Four back-to-back applies (BSP, A M v, BSP, A M v) over the peer
+    buffers with the epoch protocol and no barrier between them: every rank's
+    blocks equal the oracle each time."""
+    from oracle.lattice import Lattice
+    lat = Lattice(case["n1"], case["n2"])
+    L = lat.n_pairs * case["n"]
+    vbuf = torch.zeros(world, 6, L, 2, dtype=torch.float64).share_memory_()
+    cbuf = torch.zeros(world, lat.n_pairs, dtype=torch.int64).share_memory_()
+    fbuf = torch.zeros(world, dtype=torch.int64).share_memory_()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_epoch_worker, args=(r, world, port, case, blocks, vbuf, cbuf, fbuf, 4, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, errs in res:
+        assert len(errs) == 4 and max(errs) < 1e-12, (rank, errs)

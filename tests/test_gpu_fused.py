@@ -220,6 +220,11 @@ def test_peer_memory_path_single_rank(name, c, blocks):
     ra = a.gmres(rhs, "bsp", tol=1e-8, maxit=300)
     rb = b.gmres(rhs, "bsp", tol=1e-8, maxit=300)
     assert ra.iterations == rb.iterations and np.array_equal(ra.solution, rb.solution)
+    # new windows: the peer plans are rebuilt and the epoch counters restart
+    for p in (2, None):
+        a.configure(SweepConfig(blocks=p))
+        b.configure(SweepConfig(blocks=p))
+        assert np.array_equal(a.bsp_apply(g), b.bsp_apply(g)), (name, p)
     with pytest.raises(ValueError):
         b.enable_peer_memory()  # already open
 
