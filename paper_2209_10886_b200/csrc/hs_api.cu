@@ -678,6 +678,11 @@ int fused_plan_host(const Ctx* c, const Plan& P, const std::vector<StepTable>& f
   // cfg5 1.32 / 1.63)
   f.stages = (int)tiles.size() < 4 * c->num_sms ? 12 : 5;
   if (const char* e = getenv("HS_TMA_STAGES")) f.stages = atoi(e) == 12 ? 12 : 5;
+  // the signaller warp takes the fence + atomics off the consumers' path; on
+  // smaller (critical-path-bound) plans its extra hop sits on the chain (ms per
+  // apply, signaller / direct: cfg5 1.311 / 1.335, cfg3 0.208 / 0.205)
+  f.direct_signal = (int)tiles.size() < 32 * c->num_sms ? 1 : 0;
+  if (const char* e = getenv("HS_DIRECT_SIGNAL")) f.direct_signal = atoi(e) != 0;
   if (f.stages == 12 && (12 * 1024 + f.nv * std::max(f.maxK, 256)) * 16 > 225 * 1024) f.stages = 5;  // must fit one CTA
   bool reorder = true;
   if (const char* e = getenv("HS_FUSED_ORDER")) reorder = atoi(e) != 0;

@@ -128,6 +128,7 @@ struct FusedArgs {
   int ntiles, n, maxK;
   int nv;  // slab vectors per tile at most (shared-memory layout)
   unsigned long long* trace;  // per ticket: claim, inputs ready, map streamed, signalled (globaltimer ns), sm<<32|tile
+  int direct_signal;          // TMA kernel: warp 0 signals itself (latency-bound plans), else the signaller warp
   MultiRankArgs mr;
 };
 
@@ -554,7 +555,7 @@ __global__ void __maxnreg__(96) k_bsp_tma(FusedArgs a) {  // 96: two 10-warp CTA
   }
   __syncthreads();
   if (warp == NW + 1) {  // ---- signaller: publishes each tile's completions off the consumers' path
-    if (lane == 0) {
+    if (lane == 0 && !a.direct_signal) {
       for (int q = 0;; ++q) {
         const int d = q & 1;
         mbar_wait(&sfull[d], (q >> 1) & 1);  // acquire: warp 0's epilogue stores
@@ -618,7 +619,7 @@ __global__ void __maxnreg__(96) k_bsp_tma(FusedArgs a) {  // 96: two 10-warp CTA
     __syncwarp();
     if (lane == 0) mbar_arrive(&dempty[d]);
     if (td.t >= rv.ntiles()) {
-      if (threadIdx.x == 0) {  // tell the signaller to stop
+      if (threadIdx.x == 0 && !a.direct_signal) {  // tell the signaller to stop
         mbar_wait(&sempty[q & 1], ((q >> 1) & 1) ^ 1);
         sig[q & 1].phase = -1;
         mbar_arrive(&sfull[q & 1]);
@@ -714,7 +715,13 @@ __global__ void __maxnreg__(96) k_bsp_tma(FusedArgs a) {  // 96: two 10-warp CTA
       }
       if (erow_ok) epi_store(rv, td.phase, td.flags, elow, eo, eoff, y1, y2, e1, e2, e3);
       __syncwarp();
-      if (lane == 0) {  // hand the completion signals to the signaller warp
+      if (lane == 0 && a.direct_signal) {  // latency-bound plans: no hand-off hop
+        tile_signal(rv, td.phase, max(td.rlo, td.row0), min(td.rhi, td.row0 + kRowTile), n, td.nlow, td.tgt);
+        if (tr) {
+          tr[4] = gtimer();
+          tr[5] = ((unsigned long long)smid() << 32) | ((unsigned)blockIdx.x << 8) | (unsigned)td.phase;
+        }
+      } else if (lane == 0) {  // hand the completion signals to the signaller warp
         mbar_wait(&sempty[q & 1], ((q >> 1) & 1) ^ 1);
         SigRec& r = sig[q & 1];
         r.phase = td.phase; r.nlow = td.nlow;
@@ -917,6 +924,7 @@ cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double
     a.r = r; a.zL = zL; a.rp = rp; a.w = w; a.z = z; a.wout = wout;
     a.done = f.counters; a.ticket = f.counters + c.plan.npairs;
     a.ntiles = f.ntiles; a.n = c.n; a.maxK = f.maxK; a.nv = f.nv;
+    a.direct_signal = f.direct_signal;
     a.trace = (c.trace_on && c.trace && c.trace_cap >= (size_t)f.ntiles) ? c.trace : nullptr;
     if (a.trace) c.trace_rows = f.ntiles;
     return f.stages == 12 ? launch_tma<12, false>(c, f, a, 1) : launch_tma<5, false>(c, f, a, 1);
@@ -974,6 +982,7 @@ cudaError_t launch_bsp_fused_ranks(Ctx& c, const DevFused& f, const MultiRankArg
   a.r = nullptr; a.zL = a.rp = a.w = a.z = a.wout = nullptr;
   a.done = nullptr; a.ticket = nullptr;
   a.ntiles = 0; a.n = c.n; a.maxK = f.maxK; a.nv = f.nv; a.trace = nullptr;
+  a.direct_signal = f.direct_signal;
   a.mr = mr;
   const int G = mr.self < 0 ? mr.G : 1;
   if (f.tma) {

@@ -146,6 +146,7 @@ struct DevFused {
   int nw = 8;               // warps per CTA (consumer warps for the TMA kernel)
   bool tma = true;          // TMA-staged maps (k_bsp_tma), else register streaming (k_bsp_fused)
   int stages = 5;           // TMA ring depth: 5 (two CTAs per SM) or 12 (one CTA per SM)
+  int direct_signal = 0;    // TMA kernel: consumers signal completions themselves (no signaller hop)
   int* counters = nullptr;  // [npairs] block completion counters + [1] ticket
   double bytes = 0;         // algorithmic bytes of one apply
   bool built = false;
