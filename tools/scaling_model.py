@@ -64,7 +64,45 @@ def lattice_maps(c):
     return Lattice(c["n1"], c["n2"])
 
 
-def simulate(cfg, G, ctas=296, rate=31.6e9, fixed=3.0e-6, lat=3.0e-6, hbm=6.9e12, rate_max=None, split=False):
+def tile_key(rec):
+    return tuple(rec[:10])
+
+
+def critical_tiles(cfg, frac, rate=31.6e9, fixed=3.0e-6):
+    """Tiles whose longest path to the end of the apply is >= frac of the
+    longest (the global plan, unlimited CTAs)."""
+    pl, owner, c = plans(cfg, 1)
+    lat_ = lattice_maps(c)
+    n = c["n"]
+    tl = pl[0]
+    writers = {}
+    dur = []
+    for i, (rec, deps) in enumerate(tl):
+        i1, i2, rlo, rhi, c0, c1, alt, row0, phase, flags, rmask, _ = rec
+        rows = min(rhi, row0 + 32) - max(rlo, row0)
+        dur.append(fixed + 16.0 * rows * (c1 - c0) / rate)
+    succ = [[] for _ in tl]
+    for i, (rec, deps) in enumerate(tl):
+        for b, cnt in deps:
+            for w in writers.get(b, [])[:cnt]:
+                succ[w].append(i)
+        i1, i2, rlo, rhi, c0, c1, alt, row0, phase, flags, rmask, _ = rec
+        s = (i1, i2)
+        if phase not in (3, 5):
+            nlow = sum(1 for f, _ in lat_.faces[s] if f in (0, 1))
+            r0, r1 = max(rlo, row0), min(rhi, row0 + 32)
+            for f in range(r0 // n, (r1 - 1) // n + 1):
+                if phase <= 1 or f < nlow:
+                    writers.setdefault(lat_.m_index(lat_.faces[s][f][1], s) - 1, []).append(i)
+    bl = [0.0] * len(tl)
+    for i in range(len(tl) - 1, -1, -1):
+        bl[i] = dur[i] + max((bl[j] for j in succ[i]), default=0.0)
+    top = max(bl)
+    return {tile_key(tl[i][0]) for i in range(len(tl)) if bl[i] >= frac * top}
+
+
+def simulate(cfg, G, ctas=296, rate=31.6e9, fixed=3.0e-6, lat=3.0e-6, hbm=6.9e12, rate_max=None, split=False,
+             split_set=None):
     """rate: per-CTA stream rate under full load (calibrated); rate_max: the
     ring-latency limit of one CTA (5 x 16 KB in flight) when fewer CTAs share
     the HBM -- the rate of a tile is then min(rate_max, hbm / CTAs streaming at
@@ -123,7 +161,7 @@ def simulate(cfg, G, ctas=296, rate=31.6e9, fixed=3.0e-6, lat=3.0e-6, hbm=6.9e12
                     while act and act[0] <= start:
                         heapq.heappop(act)
                     r = min(rate_max, hbm / (len(act) + 1))
-                if split and c1 - c0 >= 256:
+                if (split or (split_set is not None and tile_key(rec) in split_set)) and c1 - c0 >= 256:
                     # split-K: a second CTA streams the other column half; the
                     # later one adds the halves (fixed order) and finishes the rows
                     claim2 = heapq.heappop(free[g])
@@ -160,6 +198,9 @@ def main():
         calib = dict(calib, rate_max=75e9)
     if "--split" in sys.argv:
         calib = dict(calib, split=True)
+    for a in sys.argv:
+        if a.startswith("--split-critical="):
+            calib = dict(calib, split_set=critical_tiles(cfg, float(a.split("=")[1])))
     rows = []
     t1 = None
     for G in Gs:
