@@ -736,6 +736,11 @@ int build_steps(Ctx* c) {
   for (auto& s : c->sp_fwd) free_step(c, s);
   for (auto& s : c->sp_bwd) free_step(c, s);
   free_step(c, c->full);
+  free_step(c, c->mo_resid);
+  free_step(c, c->mo_ims_up);
+  free_step(c, c->mo_ims_late);
+  dfree(c, c->mo_zero_blocks, 0); c->mo_zero_blocks = nullptr; c->n_mo_zero = 0;
+  dfree(c, c->mo_r_blocks, 0); c->mo_r_blocks = nullptr; c->n_mo_r = 0;
   Plan& P = c->plan;
   auto f = P.half_steps(0), b = P.half_steps(1);
   c->fwd.assign(f.size(), DevStep());
@@ -756,6 +761,40 @@ int build_steps(Ctx* c) {
   for (size_t i = 0; i < sf.size(); ++i) if (make_step(c, sf[i], c->sp_fwd[i])) return -1;
   for (size_t i = 0; i < sb.size(); ++i) if (make_step(c, sb[i], c->sp_bwd[i])) return -1;
   if (make_step(c, P.full_step(), c->full)) return -1;
+  // map-once per-step tables (see do_precond / do_ims_mo)
+  {
+    std::set<int> fseam, bstart;  // forward window starts past group 2; backward starts below the top
+    for (auto& w : P.win_lower)
+      if (w.first > 2) fseam.insert(w.first);
+    for (auto& w : P.win_upper)
+      if (w.second < P.ng + 1) bstart.insert(w.second);
+    StepTable rs, up, late;
+    std::vector<int> zero, rfill;
+    for (int s2 = 0; s2 < P.nsub; ++s2) {
+      const SubPlan& sp = P.subs[s2];
+      const int nl = sp.nlower, K = sp.k * c->n;
+      const bool seam = fseam.count(sp.group) && nl > 0 && sp.k > nl;        // slab z_L != r at its forward read
+      const bool late_b = bstart.count(sp.group) && nl > 0 && sp.k > nl;     // slab rp != final w at its backward read
+      Item it;
+      it.s = s2;
+      if (nl > 0) { it.rlo = 0; it.rhi = nl * c->n; rs.items.push_back(it); }
+      if (seam) { it.rlo = nl * c->n; it.rhi = K; rs.items.push_back(it); }
+      if (sp.k > nl) { it.rlo = nl * c->n; it.rhi = K; up.items.push_back(it); }
+      if (late_b) { it.rlo = 0; it.rhi = nl * c->n; late.items.push_back(it); }
+      for (int q = 0; q < sp.k; ++q) {
+        const int tb = sp.tgt_block[q];
+        if (P.subs[P.block_sub[tb]].rank != P.rank) continue;  // own blocks only
+        if (q >= nl && !seam) zero.push_back(tb);   // W/S block of an exact forward writer: r' = 0
+        if (q < nl && !late_b) rfill.push_back(tb);  // N/E block of a final backward writer: (I - S) z = r
+      }
+    }
+    if (make_step(c, P.localize(rs), c->mo_resid) || make_step(c, P.localize(up), c->mo_ims_up) ||
+        make_step(c, P.localize(late), c->mo_ims_late))
+      return -1;
+    if (upload(c, &c->mo_zero_blocks, zero) || upload(c, &c->mo_r_blocks, rfill)) return -1;
+    c->n_mo_zero = (int)zero.size();
+    c->n_mo_r = (int)rfill.size();
+  }
   // seam blocks (literal mode): groups shared by consecutive windows
   for (int dir = 0; dir < 2; ++dir) {
     const auto& W = dir == 0 ? P.win_lower : P.win_upper;
@@ -778,6 +817,7 @@ int build_steps(Ctx* c) {
     for (auto& s : v) need = std::max(need, (size_t)std::max(std::max(s.nsend_up, s.nsend_dn), std::max(s.nrecv_up, s.nrecv_dn)));
   };
   upd(c->fwd); upd(c->bwd); upd(c->sp_fwd); upd(c->sp_bwd);
+  upd({c->mo_resid, c->mo_ims_up, c->mo_ims_late});
   need = std::max(need, (size_t)std::max(std::max(c->full.nsend_up, c->full.nsend_dn), std::max(c->full.nrecv_up, c->full.nrecv_dn)));
   c->xbuf_cap = need * c->n;  // per RHS; grown with R in ensure_xbuf
   c->steps_dirty = false;
@@ -854,9 +894,9 @@ int run_step(Ctx* c, DevStep& st, const double2* srcA, const double2* srcB, Epi 
 }
 
 Epi epi(int mode, double2* o1, double2* o2 = nullptr, double2* o3 = nullptr,
-        const double2* a = nullptr, const double2* b = nullptr) {
+        const double2* a = nullptr, const double2* b = nullptr, const double2* cc = nullptr) {
   Epi e;
-  e.mode = mode; e.o1 = o1; e.o2 = o2; e.o3 = o3; e.a = a; e.b = b;
+  e.mode = mode; e.o1 = o1; e.o2 = o2; e.o3 = o3; e.a = a; e.b = b; e.c = cc;
   e.send_up = e.send_dn = nullptr;
   return e;
 }
@@ -1146,6 +1186,31 @@ int do_precond_ims(Ctx* c, const double2* r, double2* z, double2* wout) {
   return 0;
 }
 
+// The per-step BSP in map-once form (dedup seams, intermediate residual, not
+// the literal-arithmetic mask bit 2).
+bool mma_fused_path(const Ctx* c, int R) {
+  return (c->fused_mode & 2) && (R > 1 || c->map_mode == 1) && c->n % 32 == 0 && c->plan.nranks == 1 && c->inter &&
+         c->seam == HS_SEAM_DEDUP && c->full.nitems > 0;
+}
+
+bool map_once_steps(const Ctx* c) {
+  return c->inter && c->seam == HS_SEAM_DEDUP && !(c->fused_mode & 4) && c->mo_resid.host.items.size() > 0;
+}
+
+// wout = (I - S) z right after the per-step map-once BSP apply of r (whose
+// zL, rp and w are still in the workspace): r on the N/E blocks of final
+// backward writers, r - T_up w on every W/S block, (r - rp) + (w - T_low w) on
+// the lower rows of the backward window starts -- about half the map reads of
+// a full (I - S) step.
+int do_ims_mo(Ctx* c, const double2* r, double2* wout, int R) {
+  const long long LR = LRof(c, R);
+  double2 *zl, *rp, *w;
+  if (ws_get(c, "zL", LR, &zl) || ws_get(c, "rp", LR, &rp) || ws_get(c, "w", LR, &w)) return -1;
+  launch_block_fill(*c, c->mo_r_blocks, c->n_mo_r, 1, wout, nullptr, nullptr, r, R);
+  if (int e_ = run_step(c, c->mo_ims_up, w, w, epi(EPI_IMS, wout, nullptr, nullptr, r), R)) return e_;
+  return run_step(c, c->mo_ims_late, w, w, epi(EPI_LATE, wout, nullptr, nullptr, r, rp, w), R);
+}
+
 int do_precond(Ctx* c, int kind, const double2* r, double2* z, int R) {
   const long long LR = LRof(c, R);
   if (kind == HS_PC_NONE) {
@@ -1191,8 +1256,7 @@ int do_precond(Ctx* c, int kind, const double2* r, double2* z, int R) {
   // opt-in (bit 1): measured slower than per-step cluster split-K launches at
   // cfg4 / shared cfg5 -- without split-K each task serialises its K chunks and
   // the step-to-step dependency chain grows
-  if ((c->fused_mode & 2) && (R > 1 || shared) && c->n % 32 == 0 && c->plan.nranks == 1 && c->inter &&
-      c->seam == HS_SEAM_DEDUP && c->full.nitems > 0) {
+  if (mma_fused_path(c, R)) {
     // the whole apply on the DMMA contraction as one dataflow launch
     if (!c->fused_mma.built || c->fused_mma.R != R || c->fused_mma.shared != shared)
       if (int e_ = build_fused_mma(c, R, shared)) return e_;
@@ -1217,7 +1281,13 @@ int do_precond(Ctx* c, int kind, const double2* r, double2* z, int R) {
   }
   if (int e_ = do_half(c, 0, r, zl, R)) return e_;
   const double2* rsrc;
-  if (c->inter) {
+  if (map_once_steps(c)) {
+    // map-once: r' = 0 on the W/S blocks of exact forward writers (no map read);
+    // the residual step covers only the rows where r' can be nonzero
+    launch_block_fill(*c, c->mo_zero_blocks, c->n_mo_zero, 0, rp, w, z, zl, R);
+    if (int e_ = run_step(c, c->mo_resid, zl, zl, epi(EPI_RESID, rp, w, z, r, zl), R)) return e_;
+    rsrc = rp;
+  } else if (c->inter) {
     if (int e_ = run_step(c, c->full, zl, zl, epi(EPI_RESID, rp, w, z, r, zl), R)) return e_;
     rsrc = rp;
   } else {
@@ -1918,7 +1988,11 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
         if (int e_ = do_precond(c, pc, vk, Z, R)) return e_;
         zin = Z;
       }
-      if (int e_ = do_apply(c, HS_APPLY_IMS, zin, w, R)) return e_;
+      if (pc == HS_PC_BSP && map_once_steps(c) && !fused_bsp_ok(c, R) && !mma_fused_path(c, R)) {
+        if (int e_ = do_ims_mo(c, vk, w, R)) return e_;  // (I - S) M v_k from the apply's own state
+      } else {
+        if (int e_ = do_apply(c, HS_APPLY_IMS, zin, w, R)) return e_;
+      }
     }
     if (cgs2) {
       CK(gmres_arnoldi_cgs2(*c, G, k, c->d_owned, c->n_owned, part3, hbuf, c->nccl));

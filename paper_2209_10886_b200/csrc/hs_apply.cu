@@ -831,6 +831,25 @@ __global__ void k_seam_add(const int* __restrict__ blocks, int nb, double2* z, c
   }
 }
 
+// Blocks finished without a map read (map-once per-step plan): mode 0:
+// o1 = o2 = 0, o3 = a (rp = w = 0, z = zL); mode 1: o1 = a ((I - S) z = r).
+__global__ void k_block_fill(const int* __restrict__ blocks, int nb, int mode, double2* o1, double2* o2, double2* o3,
+                             const double2* a, int n, int R) {
+  const long long per = (long long)n * R;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < per * nb;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(i / per);
+    const long long t = (long long)blocks[j] * per + (i - j * per);
+    if (mode == 0) {
+      o1[t] = make_double2(0, 0);
+      o2[t] = make_double2(0, 0);
+      o3[t] = a[t];
+    } else {
+      o1[t] = a[t];
+    }
+  }
+}
+
 static int grid_for(long long len, int sms) {
   long long g = (len + 255) / 256;
   long long cap = (long long)sms * 8;
@@ -867,6 +886,14 @@ void launch_vec(Ctx& c, int op, long long len, double2* o1, double2* o2, const d
   if (len <= 0) return;
   c.launches++;
   k_vec<<<grid_for(len, c.num_sms), 256, 0, c.stream>>>(op, len, o1, o2, a, b);
+}
+
+void launch_block_fill(Ctx& c, const int* blocks, int nb, int mode, double2* o1, double2* o2, double2* o3,
+                       const double2* a, int R) {
+  if (nb == 0) return;
+  long long len = (long long)nb * c.n * R;
+  c.launches++;
+  k_block_fill<<<grid_for(len, c.num_sms), 256, 0, c.stream>>>(blocks, nb, mode, o1, o2, o3, a, c.n, R);
 }
 
 void launch_seam_add(Ctx& c, int dir, double2* z, const double2* r, int R) {

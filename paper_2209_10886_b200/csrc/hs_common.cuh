@@ -60,6 +60,7 @@ __device__ __forceinline__ void epi_apply(const Epi& e, long long t, double2 y) 
       e.o2[t] = v;
       e.o3[t] = cadd(zl, v);
     } break;
+    case EPI_LATE: e.o1[t] = cadd(csub(e.a[t], e.b[t]), csub(e.c[t], y)); break;
     case EPI_ACC2:
       e.o1[t] = cadd(e.o1[t], y);
       e.o2[t] = cadd(e.o2[t], y);

@@ -52,6 +52,7 @@ enum EpiMode {
   EPI_IMS = 2,    // o1[t] = a[t] - y                 ((I - S) g)
   EPI_RESID = 3,  // v = a[t] - b[t] + y; o1 = v; o2 = v; o3 = b[t] + v   (BSP residual)
   EPI_ACC2 = 4,   // o1[t] += y; o2[t] += y           (BSP backward step)
+  EPI_LATE = 5,   // o1[t] = (a[t] - b[t]) + (c[t] - y)  ((I - S) z on a backward window start's rows)
 };
 
 struct Epi {
@@ -61,6 +62,7 @@ struct Epi {
   double2* o3;
   const double2* a;
   const double2* b;
+  const double2* c;
   double2* send_up;
   double2* send_dn;
 };
@@ -293,6 +295,13 @@ struct Ctx {
   bool steps_dirty = true;
   std::vector<DevStep> fwd, bwd, sp_fwd, sp_bwd;
   DevStep full;
+  // map-once form of the per-step BSP (and of GMRES's A M v): the residual
+  // step on the rows where r' can be nonzero, the upper rows of (I - S) z on
+  // the final backward state, the window starts' late rows, and the blocks
+  // filled without a map read (device lists of own blocks)
+  DevStep mo_resid, mo_ims_up, mo_ims_late;
+  int* mo_zero_blocks = nullptr;  int n_mo_zero = 0;   // rp = w = 0, z = zL
+  int* mo_r_blocks = nullptr;     int n_mo_r = 0;      // (I - S) z = r
   DevFused fused;        // BSP apply as one dataflow launch (1 RHS, per-subdomain maps, 1 rank)
   DevFused fused_ims;    // the same followed by (I - S) z: GMRES's A M v in one launch
   EmuRanks emu;          // emulated row-band ranks for the fused apply (tests)

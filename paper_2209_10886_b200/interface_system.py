@@ -190,13 +190,15 @@ class GpuInterfaceSystem:
         self.ctx.call("hs_set_map_mode", 1 if maps == "shared" else 0)
         # one-RHS BSP applies as a single dataflow launch: fused=True runs the
         # map-once plan (each map row read ~once per apply; equal to the step
-        # sequence to rounding), fused="steps" the per-step plan (bitwise equal
-        # to per-step launches, fused=False); fused=3 also fuses the DMMA
-        # contraction paths (opt-in); an int is the raw hs_set_fused mask
+        # sequence to rounding); fused=False one launch per step, also in
+        # map-once form; fused="steps" / "literal" the literal SPEC arithmetic
+        # as one launch / per step (bitwise equal to each other); fused=3 also
+        # fuses the DMMA contraction paths (opt-in); an int is the raw
+        # hs_set_fused mask
         if isinstance(fused, str):
-            if fused != "steps":
-                raise ValueError(f"fused must be a bool, an int mask or 'steps', got {fused!r}")
-            mask = 5
+            if fused not in ("steps", "literal"):
+                raise ValueError(f"fused must be a bool, an int mask, 'steps' or 'literal', got {fused!r}")
+            mask = 5 if fused == "steps" else 4
         elif isinstance(fused, bool):
             mask = 1 if fused else 0
         else:

@@ -25,7 +25,7 @@ CASES = [("small_1x4", small_case(1, 4, 8), [None, 1]), ("small_3x3", small_case
 @pytest.mark.parametrize("name,c,blocks", CASES)
 def test_fused_bitwise_equals_steps(name, c, blocks):
     spec, part = product_problem(c)
-    a = GpuInterfaceSystem(spec, part, fused=False)
+    a = GpuInterfaceSystem(spec, part, fused="literal")
     b = GpuInterfaceSystem(spec, part, fused="steps")
     g = cvec(13, a.layout.size)
     for p in blocks:
@@ -52,7 +52,7 @@ def test_fused_gmres_bitwise_equals_steps(name, c, blocks):
     """GMRES with A M v as ONE launch (BSP + (I - S) z, phase 3 of the fused
     per-step plan) runs bitwise the same iterations as the per-step kernels."""
     spec, part = product_problem(c)
-    a = GpuInterfaceSystem(spec, part, fused=False, sweep=SweepConfig(blocks=blocks))
+    a = GpuInterfaceSystem(spec, part, fused="literal", sweep=SweepConfig(blocks=blocks))
     b = GpuInterfaceSystem(spec, part, fused="steps", sweep=SweepConfig(blocks=blocks))
     rhs = a.rhs() if c.get("center") is not None else cvec(5, a.layout.size)
     ra = a.gmres(rhs, "bsp", tol=1e-8, maxit=300)
@@ -100,7 +100,7 @@ from paper_2209_10886_b200.configs import CONFIGS, small_case
 from paper_2209_10886_b200.interface_system import GpuInterfaceSystem, SweepConfig
 for c, blocks in ((small_case(6, 3, 16), 5), (CONFIGS[2], 4), (CONFIGS[3], 4)):
     spec, part = product_problem(c)
-    a = GpuInterfaceSystem(spec, part, fused=False, sweep=SweepConfig(blocks=blocks))
+    a = GpuInterfaceSystem(spec, part, fused="literal", sweep=SweepConfig(blocks=blocks))
     b = GpuInterfaceSystem(spec, part, fused="steps", sweep=SweepConfig(blocks=blocks))
     g = cvec(29, a.layout.size)
     assert np.array_equal(a.bsp_apply(g), b.bsp_apply(g)), c["name"]
@@ -168,14 +168,16 @@ def test_map_once_equals_steps(name, c, blocks):
     rounding, for every block count incl. 1-step windows; repeated launches are
     bitwise reproducible."""
     spec, part = product_problem(c)
-    a = GpuInterfaceSystem(spec, part, fused=False)
+    a = GpuInterfaceSystem(spec, part, fused="literal")
     b = GpuInterfaceSystem(spec, part, fused=True)
+    d = GpuInterfaceSystem(spec, part, fused=False)  # per-step launches, map-once form
     g = cvec(13, a.layout.size)
     for p in blocks:
-        a.configure(SweepConfig(blocks=p))
-        b.configure(SweepConfig(blocks=p))
-        za, zb = a.bsp_apply(g), b.bsp_apply(g)
+        for x in (a, b, d):
+            x.configure(SweepConfig(blocks=p))
+        za, zb, zd = a.bsp_apply(g), b.bsp_apply(g), d.bsp_apply(g)
         assert relerr(zb, za) < 1e-13, (name, p, relerr(zb, za))
+        assert relerr(zd, za) < 1e-13, (name, p, relerr(zd, za))
         for _ in range(2):
             assert np.array_equal(b.bsp_apply(g), zb)
 
@@ -184,19 +186,22 @@ def test_map_once_equals_steps(name, c, blocks):
                                            ("small_6x3", small_case(6, 3, 16), 5), ("cfg1", CONFIGS[1], None),
                                            ("cfg2", CONFIGS[2], 8), ("cfg3", CONFIGS[3], 4)])
 def test_map_once_gmres_equals_steps(name, c, blocks):
-    """GMRES with A M v as one map-once launch (BSP + (I - S) z reading each
-    map row ~1.5 times instead of 3): the per-step iterations, history to
-    1e-10 and solution to 1e-10."""
+    """GMRES with A M v in map-once form -- one launch (BSP + (I - S) z reading
+    each map row ~1.7 times instead of 3), and per-step launches (restricted
+    residual step, (I - S) z on the upper rows + window starts): the literal
+    iterations, history to 1e-8 and solution to 1e-10."""
     spec, part = product_problem(c)
-    a = GpuInterfaceSystem(spec, part, fused=False, sweep=SweepConfig(blocks=blocks))
-    b = GpuInterfaceSystem(spec, part, fused=True, sweep=SweepConfig(blocks=blocks))
+    a = GpuInterfaceSystem(spec, part, fused="literal", sweep=SweepConfig(blocks=blocks))
     rhs = a.rhs() if c.get("center") is not None else cvec(5, a.layout.size)
     ra = a.gmres(rhs, "bsp", tol=1e-8, maxit=300)
-    rb = b.gmres(rhs, "bsp", tol=1e-8, maxit=300)
-    assert ra.converged and rb.converged and ra.iterations == rb.iterations
-    assert relerr(rb.solution, ra.solution) < 1e-10, relerr(rb.solution, ra.solution)
-    ha, hb = np.asarray(ra.history), np.asarray(rb.history)
-    assert np.max(np.abs(hb - ha) / ha) < 1e-8
+    ha = np.asarray(ra.history)
+    for fused in (True, False):  # one launch per A M v / per-step map-once (residual + (I - S) z rows)
+        b = GpuInterfaceSystem(spec, part, fused=fused, sweep=SweepConfig(blocks=blocks))
+        rb = b.gmres(rhs, "bsp", tol=1e-8, maxit=300)
+        assert ra.converged and rb.converged and ra.iterations == rb.iterations, fused
+        assert relerr(rb.solution, ra.solution) < 1e-10, (fused, relerr(rb.solution, ra.solution))
+        hb = np.asarray(rb.history)
+        assert np.max(np.abs(hb - ha) / ha) < 1e-8, fused
 
 
 @pytest.mark.parametrize("name,c,blocks", [("small_6x3", small_case(6, 3, 16), 5), ("small_4x4_n160", small_case(4, 4, 160), None),
@@ -251,3 +256,23 @@ def test_precondition_batch_pipelined(name, c, blocks):
         assert np.array_equal(zs[i].numpy(), s.precondition(gs[i], "bsp"))
     with pytest.raises(ValueError):
         s.precondition_batch([torch.from_numpy(gs[0]).cuda()])
+
+
+@pytest.mark.parametrize("name,c,R,maps", [("small_6x3", small_case(6, 3, 16), 1, "subdomain"),
+                                           ("cfg2", CONFIGS[2], 8, "subdomain"), ("cfg2", CONFIGS[2], 1, "shared"),
+                                           ("cfg1", CONFIGS[1], 4, "shared")])
+def test_map_once_steps_dmma_and_multi_rhs(name, c, R, maps):
+    """The per-step map-once form on the DMMA contraction (R right-hand
+    sides, shared class maps) and on k_step1: BSP equal to the literal step
+    sequence to rounding, and batched GMRES (A M v with the (I - S) z rows of
+    the map-once form) in the literal iterations."""
+    spec, part = product_problem(c)
+    blocks = c.get("blocks")
+    a = GpuInterfaceSystem(spec, part, fused="literal", maps=maps, sweep=SweepConfig(blocks=blocks))
+    d = GpuInterfaceSystem(spec, part, fused=False, maps=maps, sweep=SweepConfig(blocks=blocks))
+    g = cvec(19, a.layout.size, None if R == 1 else R)
+    assert relerr(d.bsp_apply(g), a.bsp_apply(g)) < 1e-13
+    ra = a.gmres(g, "bsp", tol=1e-8, maxit=300)
+    rd = d.gmres(g, "bsp", tol=1e-8, maxit=300)
+    assert ra.iterations == rd.iterations
+    assert relerr(rd.solution, ra.solution) < 1e-9
