@@ -392,6 +392,8 @@ int make_step(Ctx* c, const StepTable& t, DevStep& out) {
 void free_fused(Ctx* c) {
   for (DevFused* fp : {&c->fused, &c->fused_ims}) {
     DevFused& f = *fp;
+    dfree(c, f.split_buf, 0);
+    dfree(c, f.split_cnt, 0);
     dfree(c, f.items, f.nitems * sizeof(DevItem));
     dfree(c, f.tiles, f.ntiles * sizeof(FusedTile));
     dfree(c, f.deps, f.ndeps * sizeof(FusedDep));
@@ -425,6 +427,8 @@ std::vector<FusedTile> schedule_tickets(const std::vector<FusedTile>& tiles, con
       const FusedDep& dp = deps[tiles[t].dep0 + d];
       for (int i = 0; i < dp.count; ++i) pre.push_back(writers[dp.block][i]);
     }
+    // split-K: half 1 (the pair's writer in `writers`) finishes after half 0
+    if (tiles[t].ks == 1 && t > 0 && tiles[t - 1].pair == tiles[t].pair) pre.push_back(t - 1);
     std::sort(pre.begin(), pre.end());
     pre.erase(std::unique(pre.begin(), pre.end()), pre.end());
     npred[t] = (int)pre.size();
@@ -499,6 +503,16 @@ std::vector<FusedTile> schedule_tickets(const std::vector<FusedTile>& tiles, con
 //    rp, final w later) and subdomains without lower faces get phase 5.
 // keep_rank >= 0: keep only the tiles of that rank's subdomains (sub_rank),
 // in the global ticket order (row-band ranks on separate GPUs).
+// Partial-sum slots and arrival counters of the split-K pairs (zeroed once:
+// arrivals are counted modulo 2, so they are never reset).
+int alloc_split(Ctx* c, DevFused& f) {
+  if (f.npairs_split == 0) return 0;
+  CK(dalloc(c, (void**)&f.split_buf, (size_t)f.npairs_split * 2 * 32 * 2 * sizeof(double2)));
+  CK(dalloc(c, (void**)&f.split_cnt, (size_t)f.npairs_split * sizeof(int)));
+  CK(cudaMemsetAsync(f.split_cnt, 0, (size_t)f.npairs_split * sizeof(int), c->stream));
+  return 0;
+}
+
 struct FusedHost {
   std::vector<DevItem> items;
   std::vector<FusedTile> tiles;
@@ -558,6 +572,7 @@ int fused_plan_host(const Ctx* c, const Plan& P, const std::vector<StepTable>& f
       for (int tl = it.rlo / TR; tl * TR < it.rhi; ++tl) {
         FusedTile ft;
         ft.item = idx; ft.tile = tl; ft.phase = phase; ft.flags = v.flags;
+        ft.c0 = d.c0; ft.c1 = d.c1; ft.ks = -1; ft.pair = -1;
         ft.dep0 = (int)deps.size(); ft.ndep = 0;
         ft.rmask = 0;
         if (phase <= 1 || phase == 4) {  // zL is never initialised: blocks without a forward write read r
@@ -684,6 +699,41 @@ int fused_plan_host(const Ctx* c, const Plan& P, const std::vector<StepTable>& f
   f.direct_signal = (int)tiles.size() < 32 * c->num_sms ? 1 : 0;
   if (const char* e = getenv("HS_DIRECT_SIGNAL")) f.direct_signal = atoi(e) != 0;
   if (f.stages == 12 && (12 * 1024 + f.nv * std::max(f.maxK, 256)) * 16 > 225 * 1024) f.stages = 5;  // must fit one CTA
+  // split-K (opt-in, HS_SPLITK=1): each strip of >= 8 chunks is streamed by
+  // two CTAs, the later one adding the two halves in a fixed order.  Meant for
+  // plans near their critical path (row bands on many GPUs: the conservative
+  // model, tools/scaling_model.py --split, gives cfg5 on 8 GPUs 0.26 -> 0.21
+  // ms), but the doubled per-tile cost measured on one GPU (cfg5 1.30 -> 1.50
+  // ms, cfg3 0.207 -> 0.274 ms) is far above the model's, so it stays off until
+  // it can be measured on real row bands.
+  {
+    bool split = false;
+    if (const char* e = getenv("HS_SPLITK")) split = f.tma && atoi(e) != 0;
+    f.npairs_split = 0;
+    if (split) {
+      std::vector<FusedTile> t2;
+      std::vector<std::vector<int>> inc2;
+      std::vector<double> cost2;
+      for (size_t i = 0; i < tiles.size(); ++i) {
+        const FusedTile& t = tiles[i];
+        const int nch = (t.c1 + 31) / 32 - t.c0 / 32;
+        if (nch < 8) {
+          t2.push_back(t); inc2.push_back(tile_inc[i]); cost2.push_back(tile_cost[i]);
+          continue;
+        }
+        const int mid = (t.c0 / 32 + nch / 2) * 32;
+        FusedTile a = t, b = t;
+        a.c1 = mid; b.c0 = mid;
+        a.ks = 0; b.ks = 1;
+        a.pair = b.pair = f.npairs_split++;
+        t2.push_back(a); inc2.push_back({}); cost2.push_back(tile_cost[i] * (mid - t.c0) / (t.c1 - t.c0));
+        t2.push_back(b); inc2.push_back(tile_inc[i]); cost2.push_back(tile_cost[i] * (t.c1 - mid) / (t.c1 - t.c0));
+      }
+      tiles.swap(t2);
+      tile_inc.swap(inc2);
+      tile_cost.swap(cost2);
+    }
+  }
   bool reorder = true;
   if (const char* e = getenv("HS_FUSED_ORDER")) reorder = atoi(e) != 0;
   if (reorder) {
@@ -710,6 +760,7 @@ int build_fused_plan(Ctx* c, const Plan& P, const std::vector<StepTable>& fwd, c
   if (int e = fused_plan_host(c, P, fwd, full, bwd, ims, f, H, sub_rank, keep_rank)) return e;
   if (upload(c, &f.items, H.items) || upload(c, &f.tiles, H.tiles) || upload(c, &f.deps, H.deps)) return -1;
   CK(dalloc(c, (void**)&f.counters, (P.npairs + 1) * sizeof(int)));
+  if (int e = alloc_split(c, f)) return e;
   f.built = true;
   return 0;
 }
@@ -1034,6 +1085,8 @@ void free_peer_plans(Ctx* c) {
   PeerRanks& p = c->peer;
   for (DevFused* fp : {&p.plan, &p.plan_ims}) {
     DevFused& f = *fp;
+    dfree(c, f.split_buf, 0);
+    dfree(c, f.split_cnt, 0);
     dfree(c, f.items, 0);
     dfree(c, f.tiles, 0);
     dfree(c, f.deps, 0);
@@ -1097,6 +1150,7 @@ int build_peer_plan(Ctx* c, bool ims) {
   FusedHost H;
   if (int e = peer_plan_host(c, ims, c->plan.rank, f, H)) return e;
   if (upload(c, &f.items, H.items) || upload(c, &f.tiles, H.tiles) || upload(c, &f.deps, H.deps)) return -1;
+  if (int e = alloc_split(c, f)) return e;
   // the epoch protocol needs the same signals per block from every plan
   // (the BSP and the A M v plans signal the same blocks the same number of times)
   const DevFused& other = ims ? p.plan : p.plan_ims;

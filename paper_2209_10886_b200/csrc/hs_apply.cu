@@ -129,6 +129,8 @@ struct FusedArgs {
   int nv;  // slab vectors per tile at most (shared-memory layout)
   unsigned long long* trace;  // per ticket: claim, inputs ready, map streamed, signalled (globaltimer ns), sm<<32|tile
   int direct_signal;          // TMA kernel: warp 0 signals itself (latency-bound plans), else the signaller warp
+  double2* split_buf;         // split-K partial sums [pair][half][32 rows][2]
+  int* split_cnt;             // split-K arrivals per pair (odd arrival combines)
   MultiRankArgs mr;
 };
 
@@ -415,11 +417,11 @@ __global__ void __launch_bounds__(NW * 32, RT == 1 ? 6 : 1) k_bsp_fused(FusedArg
     double2* part = sm;
     // zL starts as r without a copy: faces of zL not yet written read r
     for (int i = threadIdx.x; i < K; i += NW * 32)
-      xs[i] = slab_value(rv, cr, x1, rsrc, i, n, ft.rmask, it.c0, it.c1, ft.phase, ft.flags, sb.in_off);
+      xs[i] = slab_value(rv, cr, x1, rsrc, i, n, ft.rmask, ft.c0, ft.c1, ft.phase, ft.flags, sb.in_off);
     if (nv == 2)
       for (int i = threadIdx.x; i < K; i += NW * 32) xs[K + i] = __ldcg(x2 + sb.in_off + i);
     __syncthreads();
-    const int ch0 = it.c0 / 32, nch = (it.c1 + 31) / 32;
+    const int ch0 = ft.c0 / 32, nch = (ft.c1 + 31) / 32;
     // strips beyond the map (RT > 1 at the last rows) are skipped
     const int nstrip = (K + kRowTile - 1) / kRowTile;
     const int s0 = ft.tile * RT;
@@ -493,7 +495,7 @@ struct SigRec {  // a tile's completions, handed from the consumers to the signa
 
 struct TileDesc {
   long long map_off;  // element offset of the tile's 32-row strip
-  int t, K, phase, flags, alt, in_off, rlo, rhi, row0, dep0, ndep, rmask, nlow, c0, c1;
+  int t, K, phase, flags, alt, in_off, rlo, rhi, row0, dep0, ndep, rmask, nlow, c0, c1, ks, pair;
   int tgt[4];
   unsigned long long claimed;  // globaltimer at the producer's claim (trace only)
 };
@@ -586,7 +588,7 @@ __global__ void __maxnreg__(96) k_bsp_tma(FusedArgs a) {  // 96: two 10-warp CTA
           td.row0 = ft.tile * kRowTile;
           td.map_off = sb.T_off + (long long)ft.tile * td.K * kRowTile;
           td.phase = ft.phase; td.flags = ft.flags; td.alt = it.alt; td.in_off = sb.in_off; td.nlow = sb.nlow;
-          td.c0 = it.c0; td.c1 = it.c1;
+          td.c0 = ft.c0; td.c1 = ft.c1; td.ks = ft.ks; td.pair = ft.pair;
           td.rlo = it.rlo; td.rhi = it.rhi; td.dep0 = ft.dep0; td.ndep = ft.ndep; td.rmask = ft.rmask;
           for (int f = 0; f < 4; ++f) td.tgt[f] = sb.tgt[f];
         }
@@ -713,10 +715,34 @@ __global__ void __maxnreg__(96) k_bsp_tma(FusedArgs a) {  // 96: two 10-warp CTA
 #pragma unroll
         for (int w = 1; w < NW; ++w) y2 = cadd(y2, part[(NW + w) * 32 + lane]);
       }
-      if (erow_ok) epi_store(rv, td.phase, td.flags, elow, eo, eoff, y1, y2, e1, e2, e3);
+      bool finish = true;
+      if (td.ks >= 0) {
+        // split-K: publish this half's partial sums; the second of the pair to
+        // arrive adds them in half order (deterministic) and finishes the rows
+        double2* mine = a.split_buf + ((size_t)td.pair * 2 + td.ks) * 64;
+        mine[lane] = y1;
+        mine[32 + lane] = y2;
+        __syncwarp();
+        int old = 0;
+        if (lane == 0) {
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          old = atomicAdd(a.split_cnt + td.pair, 1);
+        }
+        old = __shfl_sync(0xffffffffu, old, 0);
+        finish = old & 1;
+        if (finish) {
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          const double2* other = a.split_buf + ((size_t)td.pair * 2 + (1 - td.ks)) * 64;
+          const double2 o1 = __ldcg(other + lane), o2 = __ldcg(other + 32 + lane);
+          y1 = td.ks == 0 ? cadd(y1, o1) : cadd(o1, y1);
+          y2 = td.ks == 0 ? cadd(y2, o2) : cadd(o2, y2);
+        }
+      }
+      if (finish && erow_ok) epi_store(rv, td.phase, td.flags, elow, eo, eoff, y1, y2, e1, e2, e3);
+      const int sphase = finish ? td.phase : 3;  // the first half of a pair signals nothing
       __syncwarp();
       if (lane == 0 && a.direct_signal) {  // latency-bound plans: no hand-off hop
-        tile_signal(rv, td.phase, max(td.rlo, td.row0), min(td.rhi, td.row0 + kRowTile), n, td.nlow, td.tgt);
+        tile_signal(rv, sphase, max(td.rlo, td.row0), min(td.rhi, td.row0 + kRowTile), n, td.nlow, td.tgt);
         if (tr) {
           tr[4] = gtimer();
           tr[5] = ((unsigned long long)smid() << 32) | ((unsigned)blockIdx.x << 8) | (unsigned)td.phase;
@@ -724,7 +750,7 @@ __global__ void __maxnreg__(96) k_bsp_tma(FusedArgs a) {  // 96: two 10-warp CTA
       } else if (lane == 0) {  // hand the completion signals to the signaller warp
         mbar_wait(&sempty[q & 1], ((q >> 1) & 1) ^ 1);
         SigRec& r = sig[q & 1];
-        r.phase = td.phase; r.nlow = td.nlow;
+        r.phase = sphase; r.nlow = td.nlow;
         r.r0 = max(td.rlo, td.row0); r.r1 = min(td.rhi, td.row0 + kRowTile);
         for (int f = 0; f < 4; ++f) r.tgt[f] = td.tgt[f];
         r.tr = tr;
@@ -952,6 +978,7 @@ cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double
     a.done = f.counters; a.ticket = f.counters + c.plan.npairs;
     a.ntiles = f.ntiles; a.n = c.n; a.maxK = f.maxK; a.nv = f.nv;
     a.direct_signal = f.direct_signal;
+    a.split_buf = f.split_buf; a.split_cnt = f.split_cnt;
     a.trace = (c.trace_on && c.trace && c.trace_cap >= (size_t)f.ntiles) ? c.trace : nullptr;
     if (a.trace) c.trace_rows = f.ntiles;
     return f.stages == 12 ? launch_tma<12, false>(c, f, a, 1) : launch_tma<5, false>(c, f, a, 1);
@@ -1010,6 +1037,7 @@ cudaError_t launch_bsp_fused_ranks(Ctx& c, const DevFused& f, const MultiRankArg
   a.done = nullptr; a.ticket = nullptr;
   a.ntiles = 0; a.n = c.n; a.maxK = f.maxK; a.nv = f.nv; a.trace = nullptr;
   a.direct_signal = f.direct_signal;
+  a.split_buf = f.split_buf; a.split_cnt = f.split_cnt;
   a.mr = mr;
   const int G = mr.self < 0 ? mr.G : 1;
   if (f.tma) {

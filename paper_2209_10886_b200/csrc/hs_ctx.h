@@ -130,6 +130,8 @@ struct FusedTile {
   int flags;       // FT_*
   int dep0, ndep;  // dependencies [dep0, dep0 + ndep) in the dep pool
   int rmask;       // bit q: slab face q of zL not yet written (read r); bit 4 + f: output face f likewise
+  int c0, c1;      // map columns this tile streams (the item's range, or one half of it when split)
+  int ks, pair;    // split-K: half 0 / 1 of pair `pair` (ks = -1: not split)
 };
 
 struct FusedDep {
@@ -149,6 +151,9 @@ struct DevFused {
   bool tma = true;          // TMA-staged maps (k_bsp_tma), else register streaming (k_bsp_fused)
   int stages = 5;           // TMA ring depth: 5 (two CTAs per SM) or 12 (one CTA per SM)
   int direct_signal = 0;    // TMA kernel: consumers signal completions themselves (no signaller hop)
+  int npairs_split = 0;     // split-K tile pairs (their partial sums meet in `split_buf`)
+  double2* split_buf = nullptr;  // [pair][half][32 rows][2 vectors]
+  int* split_cnt = nullptr;      // [pair] arrivals (never reset: the odd arrival combines)
   int* counters = nullptr;  // [npairs] block completion counters + [1] ticket
   double bytes = 0;         // algorithmic bytes of one apply
   bool built = false;

@@ -276,3 +276,52 @@ def test_map_once_steps_dmma_and_multi_rhs(name, c, R, maps):
     rd = d.gmres(g, "bsp", tol=1e-8, maxit=300)
     assert ra.iterations == rd.iterations
     assert relerr(rd.solution, ra.solution) < 1e-9
+
+
+_SPLIT_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, 'tests')
+from conftest import cvec, product_problem, relerr
+from paper_2209_10886_b200.configs import CONFIGS, small_case
+from paper_2209_10886_b200.interface_system import GpuInterfaceSystem, SweepConfig
+for c, blocks in ((small_case(4, 4, 160), None), (CONFIGS[2], 4), (CONFIGS[3], 4)):
+    spec, part = product_problem(c)
+    a = GpuInterfaceSystem(spec, part, fused="literal", sweep=SweepConfig(blocks=blocks))
+    b = GpuInterfaceSystem(spec, part, sweep=SweepConfig(blocks=blocks))  # map-once, split-K forced
+    g = cvec(43, a.layout.size)
+    za, zb = a.bsp_apply(g), b.bsp_apply(g)
+    assert relerr(zb, za) < 1e-13, (c["name"], relerr(zb, za))
+    for _ in range(3):  # deterministic: the pair's halves are added in half order
+        assert np.array_equal(b.bsp_apply(g), zb)
+    b.ctx.call("hs_set_emulated_ranks", 2)
+    assert np.array_equal(b.bsp_apply(g), zb)
+    b.ctx.call("hs_set_emulated_ranks", 1)
+    rhs = a.rhs()
+    ra, rb = a.gmres(rhs, "bsp", tol=1e-8, maxit=300), b.gmres(rhs, "bsp", tol=1e-8, maxit=300)
+    assert ra.iterations == rb.iterations and relerr(rb.solution, ra.solution) < 1e-10
+    p = GpuInterfaceSystem(spec, part, sweep=SweepConfig(blocks=blocks))
+    p.enable_peer_memory()
+    assert np.array_equal(p.bsp_apply(g), zb)
+print("ok")
+"""
+
+
+def test_split_k_pairs():
+    """Split-K tiles (each strip streamed by two CTAs, the second arrival adds
+    the halves in half order and finishes the rows -- the large-GPU-count
+    mode, forced here with HS_SPLITK=1): the literal result to rounding,
+    bitwise reproducible, identical under emulated row bands and on the peer
+    path, and the literal GMRES iterations."""
+    out = _run_variant_script(_SPLIT_SCRIPT, {"HS_SPLITK": "1"})
+    assert out.endswith("ok")
+
+
+def _run_variant_script(script, env):
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", script], cwd=root, env=dict(os.environ, **env),
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    return out.stdout.strip()
