@@ -172,3 +172,19 @@ def test_no_scatterer_zero_rhs():
     assert np.all(b == 0)
     res = s.gmres(b, "bsp")
     assert res.iterations == 0 and np.all(res.solution == 0)
+
+
+@pytest.mark.parametrize("fused", [True, False, "literal"])
+def test_gmres_not_converged_is_data(fused):
+    """maxit below the iteration count: converged False, exactly maxit
+    iterations, the history and the iterate of the golden run's first maxit
+    steps (non-convergence is data, not an error), on the fused
+    map-once, per-step map-once and literal paths."""
+    G = golden("cfg1")
+    c = CASES["cfg1"]
+    spec, part = product_problem(c)
+    s = GpuInterfaceSystem(spec, part, fused=fused, sweep=SweepConfig(blocks=c.get("blocks")))
+    res = s.gmres(G["b"], "bsp", tol=1e-6, maxit=7)
+    assert not res.converged and res.iterations == 7
+    np.testing.assert_allclose(res.history[:8], G["gm_hist"][:8], rtol=1e-8, atol=1e-14)
+    assert relerr(s.apply_interface_operator(res.solution), G["b"]) == pytest.approx(res.history[-1], rel=1e-6)
