@@ -1951,7 +1951,11 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
   if (R & (R - 1)) return fail(c, 1, "batched GMRES needs nrhs a power of two");
   // Arnoldi: one cooperative kernel per iteration on one GPU; across row bands
   // (or when forced) the host-driven MGS over owned blocks + allreduce per dot
-  const bool cgs2 = c->gmres_mode == 3;
+  // Row bands, one RHS, auto mode: CGS2 -- two all-reduces per iteration
+  // instead of one per inner product (k + 1), which would dominate the sharded
+  // iteration (54 small all-reduces per iteration on average at cfg5);
+  // iterations within +-1 of MGS (tests).
+  const bool cgs2 = c->gmres_mode == 3 || (c->gmres_mode == 0 && c->plan.nranks > 1 && R == 1);
   if (cgs2 && R != 1) return fail(c, 1, "CGS2 Arnoldi supports one right-hand side");
   const bool dist = c->plan.nranks > 1 || c->gmres_mode == 1 || cgs2;
   const long long LR = LRof(c, R);

@@ -416,11 +416,13 @@ class GpuInterfaceSystem:
     def gmres(self, b, kind: str | None = None, tol: float = 1e-6, maxit: int = 200,
               arnoldi: str = "auto") -> GmresResult:
         """arnoldi = "auto" (cluster MGS kernel for small vectors, grid-wide
-        cooperative kernel otherwise; host-driven MGS with an allreduce per inner
-        product across row bands), "hostloop" (force the sharded algorithm on
-        one GPU), "grid" (force the grid-wide cooperative kernel) or "cgs2"
-        (classical Gram-Schmidt with one reorthogonalisation: 2 reductions per
-        iteration -- 2 allreduces across row bands -- instead of k+1)."""
+        cooperative kernel otherwise; across row bands CGS2 for one right-hand
+        side -- two allreduces per iteration instead of one per inner product --
+        and host-driven MGS with an allreduce per inner product for several),
+        "hostloop" (force the sharded MGS on one GPU or across bands), "grid"
+        (force the grid-wide cooperative kernel) or "cgs2" (classical
+        Gram-Schmidt with one reorthogonalisation, iterations within +-1 of
+        MGS)."""
         kind = self.sweep.kind if kind is None else kind
         modes = {"auto": 0, "hostloop": 1, "grid": 2, "cgs2": 3}
         if arnoldi not in modes:
