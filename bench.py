@@ -394,11 +394,13 @@ def main():
                            f"{pj['traffic_over_algorithmic']:.4f} over {len(pj['launches'])} captured launches")
         roof = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                 "frac": (ach / peak) if ach else None, "traffic": traffic, "traffic_source": traffic_src,
-                "kernel": ("k_bsp_tma (whole BSP apply as one dataflow launch; maps staged by TMA bulk copies "
-                           "into an mbarrier ring, producer warp + 8 consumer warps)" if 4 * c["n"] <= 512 else
-                           "k_bsp_fused (whole BSP apply as one dataflow launch of the step-apply ZGEMV tiles, "
-                           "register streaming, per-subdomain maps)") if m["kl"] <= args.steps else
+                "kernel": ("k_bsp_tma, map-once plan (the whole BSP apply as one dataflow launch; maps staged "
+                           "by TMA bulk copies with an L2 evict-first policy into an mbarrier ring; producer warp "
+                           "+ 8 consumer warps + signaller warp; per-subdomain maps)") if m["kl"] <= args.steps else
                           "k_step1 (batched step-apply ZGEMV, per-subdomain maps)",
+                "algorithmic_bytes_note": "bytes the map-once plan must move: 16 (rows cols + nv cols + 2 rows) per "
+                                          "item (DESIGN.md 3a); SURVEY 8d's literal two-pass B_BSP is larger "
+                                          "(15.84 GB at cfg5)",
                 "peak_source": peak_kind,
                 "peak_note": "measured peak = torch copy (half writes); this kernel's traffic is ~98% reads, so "
                              "frac can exceed 1 slightly; vs the 8 TB/s nominal HBM3e see achieved/8000",
