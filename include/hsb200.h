@@ -198,6 +198,12 @@ int hs_peer_open(hs_ctx* ctx, const uint8_t* handles, int nranks);
  * count) pairs (wait until block's completion counter >= count).  *count =
  * int32 written (out = NULL: needed). */
 int hs_fused_plan(const hs_ctx* ctx, int ims, int rank, int32_t* out, int cap, int* count);
+/* The map-once per-step form's tables (plan-only contexts too): which = 0
+ * residual rows, 1 (I - S) z upper rows, 2 the window starts' late rows -- 4
+ * int32 per item (subdomain i1, i2, rows [rlo, rhi)), every rank's items; 3 /
+ * 4: this rank's blocks filled without a map read (rp = w = 0, z = z_L /
+ * (I - S) z = r).  hs_exchange_plan kinds 3..5 are the same three steps. */
+int hs_map_once_plan(const hs_ctx* ctx, int which, int32_t* out, int cap, int* count);
 
 /* Diagnostics: record a per-tile timeline of the fused 1-RHS apply (on = 1).
  * hs_get_trace copies the last traced launch: rows of 6 words per ticket --
@@ -221,7 +227,9 @@ int hs_schedule(const hs_ctx* ctx, int kind, int32_t* rec, int cap, int* count);
 /* Trace-exchange plan of a step kind across row bands, for this rank: recv = 0
  * lists what it sends to `peer`, recv = 1 what it receives from `peer`, as
  * triples (step index, 0-based block m, buffer slot) in slot order, for the
- * steps of kind 0 (forward half), 1 (backward half) or 2 (full apply). */
+ * steps of kind 0 (forward half), 1 (backward half), 2 (full apply) or the
+ * map-once per-step form's 3 (residual rows), 4 ((I - S) z upper rows), 5
+ * (window starts' late rows). */
 int hs_exchange_plan(const hs_ctx* ctx, int kind, int peer, int recv, int32_t* triples, int cap,
                      int* count);
 

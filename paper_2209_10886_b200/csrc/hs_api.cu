@@ -772,6 +772,41 @@ int build_fused(Ctx* c, bool ims) {
   return build_fused_plan(c, c->plan, fwd, c->full.host, bwd, ims, ims ? c->fused_ims : c->fused);
 }
 
+// Global (not yet localized) tables of the map-once per-step form and this
+// rank's blocks filled without a map read:
+//   rs   -- residual rows: every lower face, plus the upper faces of the forward
+//           window starts past group 2 (their slab z_L != r at the forward read)
+//   up   -- (I - S) z: every subdomain's upper rows on the final w
+//   late -- (I - S) z: lower rows of the backward window starts below the top
+//   zero -- W/S blocks of exact forward writers (r' = 0: rp = w = 0, z = z_L)
+//   rfill-- N/E blocks of final backward writers ((I - S) z = r)
+void map_once_tables(const Plan& P, int n, StepTable& rs, StepTable& up, StepTable& late, std::vector<int>& zero,
+                     std::vector<int>& rfill) {
+  std::set<int> fseam, bstart;  // forward window starts past group 2; backward starts below the top
+  for (auto& w : P.win_lower)
+    if (w.first > 2) fseam.insert(w.first);
+  for (auto& w : P.win_upper)
+    if (w.second < P.ng + 1) bstart.insert(w.second);
+  for (int s2 = 0; s2 < P.nsub; ++s2) {
+    const SubPlan& sp = P.subs[s2];
+    const int nl = sp.nlower, K = sp.k * n;
+    const bool seam = fseam.count(sp.group) && nl > 0 && sp.k > nl;
+    const bool late_b = bstart.count(sp.group) && nl > 0 && sp.k > nl;
+    Item it;
+    it.s = s2;
+    if (nl > 0) { it.rlo = 0; it.rhi = nl * n; rs.items.push_back(it); }
+    if (seam) { it.rlo = nl * n; it.rhi = K; rs.items.push_back(it); }
+    if (sp.k > nl) { it.rlo = nl * n; it.rhi = K; up.items.push_back(it); }
+    if (late_b) { it.rlo = 0; it.rhi = nl * n; late.items.push_back(it); }
+    for (int q = 0; q < sp.k; ++q) {
+      const int tb = sp.tgt_block[q];
+      if (P.subs[P.block_sub[tb]].rank != P.rank) continue;  // own blocks only
+      if (q >= nl && !seam) zero.push_back(tb);
+      if (q < nl && !late_b) rfill.push_back(tb);
+    }
+  }
+}
+
 void free_emu(Ctx* c);
 void free_peer_plans(Ctx* c);
 void free_peer(Ctx* c);
@@ -814,31 +849,9 @@ int build_steps(Ctx* c) {
   if (make_step(c, P.full_step(), c->full)) return -1;
   // map-once per-step tables (see do_precond / do_ims_mo)
   {
-    std::set<int> fseam, bstart;  // forward window starts past group 2; backward starts below the top
-    for (auto& w : P.win_lower)
-      if (w.first > 2) fseam.insert(w.first);
-    for (auto& w : P.win_upper)
-      if (w.second < P.ng + 1) bstart.insert(w.second);
     StepTable rs, up, late;
     std::vector<int> zero, rfill;
-    for (int s2 = 0; s2 < P.nsub; ++s2) {
-      const SubPlan& sp = P.subs[s2];
-      const int nl = sp.nlower, K = sp.k * c->n;
-      const bool seam = fseam.count(sp.group) && nl > 0 && sp.k > nl;        // slab z_L != r at its forward read
-      const bool late_b = bstart.count(sp.group) && nl > 0 && sp.k > nl;     // slab rp != final w at its backward read
-      Item it;
-      it.s = s2;
-      if (nl > 0) { it.rlo = 0; it.rhi = nl * c->n; rs.items.push_back(it); }
-      if (seam) { it.rlo = nl * c->n; it.rhi = K; rs.items.push_back(it); }
-      if (sp.k > nl) { it.rlo = nl * c->n; it.rhi = K; up.items.push_back(it); }
-      if (late_b) { it.rlo = 0; it.rhi = nl * c->n; late.items.push_back(it); }
-      for (int q = 0; q < sp.k; ++q) {
-        const int tb = sp.tgt_block[q];
-        if (P.subs[P.block_sub[tb]].rank != P.rank) continue;  // own blocks only
-        if (q >= nl && !seam) zero.push_back(tb);   // W/S block of an exact forward writer: r' = 0
-        if (q < nl && !late_b) rfill.push_back(tb);  // N/E block of a final backward writer: (I - S) z = r
-      }
-    }
+    map_once_tables(P, c->n, rs, up, late, zero, rfill);
     if (make_step(c, P.localize(rs), c->mo_resid) || make_step(c, P.localize(up), c->mo_ims_up) ||
         make_step(c, P.localize(late), c->mo_ims_late))
       return -1;
@@ -2173,7 +2186,12 @@ int hs_exchange_plan(const hs_ctx* cc, int kind, int peer, int recv, int32_t* bl
   if (kind == 0) steps = P.half_steps(0);
   else if (kind == 1) steps = P.half_steps(1);
   else if (kind == 2) steps.push_back(P.full_step());
-  else return fail(c, 1, "kind must be 0, 1 or 2");
+  else if (kind >= 3 && kind <= 5) {  // map-once per-step tables: residual rows, (I - S) upper, late
+    StepTable rs, up, late;
+    std::vector<int> zero, rfill;
+    map_once_tables(P, c->n, rs, up, late, zero, rfill);
+    steps.push_back(P.localize(kind == 3 ? rs : kind == 4 ? up : late));
+  } else return fail(c, 1, "kind must be 0..5");
   std::vector<int32_t> out;
   for (size_t t = 0; t < steps.size(); ++t) {
     if (recv) {
@@ -2384,6 +2402,30 @@ int hs_peer_open(hs_ctx* c, const uint8_t* handles, int nranks) {
   CK(dalloc(c, (void**)&p.bar, sizeof(double2)));
   CK(cudaMemset(p.bar, 0, sizeof(double2)));
   p.G = nranks;
+  return 0;
+}
+
+int hs_map_once_plan(const hs_ctx* cc, int which, int32_t* out, int cap, int* count) {
+  if (!cc) return 1;
+  hs_ctx* c = const_cast<hs_ctx*>(cc);
+  if (!count) return fail(c, 1, "null argument");
+  if (which < 0 || which > 4) return fail(c, 1, "which must be 0..4");
+  StepTable rs, up, late;
+  std::vector<int> zero, rfill;
+  map_once_tables(c->plan, c->n, rs, up, late, zero, rfill);
+  std::vector<int32_t> v;
+  if (which <= 2) {
+    for (const Item& it : (which == 0 ? rs : which == 1 ? up : late).items) {
+      const SubPlan& sp = c->plan.subs[it.s];
+      v.insert(v.end(), {sp.i1, sp.i2, it.rlo, it.rhi});
+    }
+  } else {
+    v.assign((which == 3 ? zero : rfill).begin(), (which == 3 ? zero : rfill).end());
+  }
+  *count = (int)v.size();
+  if (!out) return 0;
+  if (cap < (int)v.size()) return fail(c, 1, "buffer too small");
+  std::copy(v.begin(), v.end(), out);
   return 0;
 }
 

@@ -69,6 +69,7 @@ _SIGS = {
     "hs_peer_export": (_I, [_P, C.POINTER(C.c_uint8)]),
     "hs_peer_open": (_I, [_P, C.POINTER(C.c_uint8), _I]),
     "hs_fused_plan": (_I, [_P, _I, _I, C.POINTER(C.c_int32), _I, C.POINTER(_I)]),
+    "hs_map_once_plan": (_I, [_P, _I, C.POINTER(C.c_int32), _I, C.POINTER(_I)]),
     "hs_precond_batch": (_I, [_P, _I, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), _I, _I]),
     "hs_get_trace": (_I, [_P, C.POINTER(C.c_uint64), _I, C.POINTER(_I)]),
     "hs_set_fused": (_I, [_P, _I]),

@@ -143,6 +143,67 @@ class Band:
             self.run_step(1, t - 1, self.half_items(1, t, w, rp), acc2)
         return z
 
+    def map_once(self, which):
+        import ctypes as C
+        cnt = C.c_int(0)
+        self.ctx.call("hs_map_once_plan", which, None, 0, C.byref(cnt))
+        buf = (C.c_int32 * max(cnt.value, 1))()
+        self.ctx.call("hs_map_once_plan", which, buf, cnt.value, C.byref(cnt))
+        return np.frombuffer(buf, dtype=np.int32)[:cnt.value]
+
+    def mo_items(self, which, src):
+        v = self.map_once(which).reshape(-1, 4)
+        return [((int(i1), int(i2)), src, range(int(lo) // self.n, int(hi) // self.n)) for i1, i2, lo, hi in v]
+
+    def bsp_map_once(self, b):
+        """The per-step map-once BSP of the library's row-band path: forward
+        half, W/S blocks of exact forward writers filled (r' = 0), the residual
+        step on the map-once rows (kind 3), backward half."""
+        zl = b.copy()
+        depth = max(hi - lo for lo, hi in self.lower)
+        for t in range(1, depth + 1):
+            def acc(blk, y):
+                zl[self.blk(blk)] += y
+            self.run_step(0, t - 1, self.half_items(0, t, zl, b), acc)
+        rp, w, z = np.zeros_like(b), np.zeros_like(b), np.zeros_like(b)
+        for blk in self.map_once(3):
+            sl = self.blk(int(blk))
+            rp[sl] = w[sl] = 0
+            z[sl] = zl[sl]
+
+        def resid(blk, y):
+            sl = self.blk(blk)
+            v = b[sl] - (zl[sl] - y)
+            rp[sl], w[sl], z[sl] = v, v, zl[sl] + v
+        self.run_step(3, 0, self.mo_items(0, zl), resid)
+        depth = max(hi - lo for lo, hi in self.upper)
+        for t in range(1, depth + 1):
+            def acc2(blk, y):
+                w[self.blk(blk)] += y
+                z[self.blk(blk)] += y
+            self.run_step(1, t - 1, self.half_items(1, t, w, rp), acc2)
+        return z, rp, w
+
+    def ims_map_once(self, r, rp, w):
+        """(I - S) z right after bsp_map_once(r): r on the N/E blocks of final
+        backward writers, r - T_up w (kind 4), (r - rp) + (w - T_low w) on the
+        window starts' lower rows (kind 5)."""
+        out = np.zeros_like(r)
+        for blk in self.map_once(4):
+            sl = self.blk(int(blk))
+            out[sl] = r[sl]
+
+        def ims(blk, y):
+            sl = self.blk(blk)
+            out[sl] = r[sl] - y
+
+        def late(blk, y):
+            sl = self.blk(blk)
+            out[sl] = (r[sl] - rp[sl]) + (w[sl] - y)
+        self.run_step(4, 0, self.mo_items(1, w), ims)
+        self.run_step(5, 0, self.mo_items(2, w), late)
+        return out
+
     def apply_A(self, g):
         out = np.zeros_like(g)
 
@@ -536,3 +597,43 @@ def test_peer_memory_epoch_protocol(case, world, blocks):
         assert p.exitcode == 0
     for rank, errs in res:
         assert len(errs) == 4 and max(errs) < 1e-12, (rank, errs)
+
+
+def _mo_worker(rank, world, port, case, blocks, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        band = Band(case, rank, world, blocks)
+        from oracle import Preconditioner
+        rng = np.random.default_rng(11)
+        r = rng.standard_normal(band.itf.size) + 1j * rng.standard_normal(band.itf.size)
+        ref = Preconditioner(band.itf, "bsp", blocks=blocks).bsp_apply(r)
+        z, rp, w = band.bsp_map_once(r)
+        out = band.ims_map_once(r, rp, w)
+        m = band.owned_mask()
+        refw = band.itf.apply_A(ref)
+        q.put((rank, float(np.abs(z[m] - ref[m]).max() / np.abs(ref).max()),
+               float(np.abs(out[m] - refw[m]).max() / np.abs(refw).max())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case,world,blocks", [(CASE, 2, None), (CASE, 3, 2), (CASE5, 2, 4), (CASE5, 3, None)])
+def test_sharded_map_once_per_step(case, world, blocks):
+    """The row-band per-step path in map-once form (the NCCL-exchange fallback
+    for R right-hand sides / no peer memory): the library's map-once tables
+    and fill lists (hs_map_once_plan) and their band-crossing exchange plans
+    (hs_exchange_plan kinds 3-5) give the oracle's BSP z and (I - S) z on
+    every rank's blocks."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_mo_worker, args=(r, world, port, case, blocks, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for rank, ez, ew in res:
+        assert ez < 1e-13 and ew < 1e-13, (rank, ez, ew)
