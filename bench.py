@@ -479,6 +479,23 @@ def main():
                          "frac": fl / fp64_peak() if fl else None},
             "setup_s": sh_setup, "gmres": None if args.no_gmres else gmres_tts(sh),
             "map_bytes": sh.ctx.memory()}
+        del sh
+        torch.cuda.empty_cache()
+        if R == 1:
+            # one compact map per (operator class, face set), aliased by every subdomain of that
+            # kind: the same fused map-once kernel and bitwise the same result, the stream from L2
+            t0 = time.perf_counter()
+            kd = GpuInterfaceSystem(spec, part, device=local, sweep=sweep, maps="kinds")
+            kd_setup = time.perf_counter() - t0
+            ms_kd = measure(kd, max(10, args.steps), args.warmup, False)
+            variants["kind_maps"] = {
+                "what": "maps='kinds': one compact map per (operator class, face set), every subdomain's record "
+                        "aliasing its kind's; the per-subdomain path's kernels and bitwise its result, the map "
+                        "stream served from L2 (evict-last policy)",
+                "applies_per_s": 1e3 / ms_kd["ms_per"], "ms_per_apply": ms_kd["ms_per"],
+                "l2_stream_gbs": (ms_kd["kbytes"] / (ms_kd["kms"] * 1e-3)) / 1e9 if ms_kd["kms"] > 0 else None,
+                "setup_s": kd_setup, "gmres": None if args.no_gmres else gmres_tts(kd),
+                "device_bytes": kd.ctx.memory()}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

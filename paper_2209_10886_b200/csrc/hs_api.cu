@@ -1237,7 +1237,7 @@ int do_precond_peer(Ctx* c, const double2* r, double2* z, double2* wout) {
 }
 
 bool fused_bsp_ok(const Ctx* c, int R) {
-  return (c->fused_mode & 1) && R == 1 && c->map_mode == 0 && (c->plan.nranks == 1 || c->peer.G > 0) && c->inter &&
+  return (c->fused_mode & 1) && R == 1 && c->map_mode != 1 && (c->plan.nranks == 1 || c->peer.G > 0) && c->inter &&
          c->seam == HS_SEAM_DEDUP && c->full.nitems > 0;
 }
 
@@ -1566,6 +1566,54 @@ int hs_set_dirichlet(hs_ctx* c, int i1, int i2, const int32_t* cells, int ncells
   return 0;
 }
 
+// Map storage offsets for map modes 0 (every own subdomain its own map) and 2
+// (one map per distinct (class, face set); aliases share it).  Rewrites the
+// device subdomain records and reallocates the map storage when its size
+// changes; `rep` = the subdomains whose maps are materialised.
+int assign_map_offsets(Ctx* c, std::vector<int>& rep) {
+  Plan& P = c->plan;
+  const int n = c->n;
+  std::map<std::pair<int, int>, long long> kind_off;  // (class, face mask) -> offset
+  std::vector<DevSub> subs(P.nsub);
+  CK(cudaMemcpy(subs.data(), c->dsubs, subs.size() * sizeof(DevSub), cudaMemcpyDeviceToHost));
+  long long off = 0;
+  rep.clear();
+  for (int s = 0; s < P.nsub; ++s) {
+    SubPlan& sp = P.subs[s];
+    const long long K = (long long)sp.k * n;
+    const long long sz = ((K + kRowTile - 1) / kRowTile) * kRowTile * K;
+    long long o = -1;
+    if (sp.rank == P.rank) {
+      if (c->map_mode == 2) {
+        int mask = 0;
+        for (int q = 0; q < sp.k; ++q) mask |= 1 << sp.face[q];
+        auto key = std::make_pair(c->sub_class[s], mask);
+        auto it = kind_off.find(key);
+        if (it == kind_off.end()) {
+          kind_off[key] = o = off;
+          off += sz;
+          rep.push_back(s);
+        } else {
+          o = it->second;
+        }
+      } else {
+        o = off;
+        off += sz;
+        rep.push_back(s);
+      }
+    }
+    sp.T_off = o;
+    subs[s].T_off = o;
+  }
+  if ((size_t)off != c->T_elems) {
+    dfree(c, c->T, 0);
+    c->T = nullptr;
+    c->T_elems = (size_t)off;
+  }
+  CK(cudaMemcpy(c->dsubs, subs.data(), subs.size() * sizeof(DevSub), cudaMemcpyHostToDevice));
+  return 0;
+}
+
 int hs_factor(hs_ctx* c) {
   if (!c) return fail(nullptr, 1, "null context");
   NEED_GPU(c);
@@ -1646,19 +1694,22 @@ int hs_factor(hs_ctx* c) {
       launch_pack_strips(*c, c->classes[k].T4, c->Tcls + per * k, 4 * n, 4 * n);
     }
   }
-  // per-subdomain maps, tile-major (the HBM-streamed path)
+  // per-subdomain maps, tile-major (the HBM-streamed path); map mode 2: one
+  // compact map per distinct (operator class, face set), every subdomain's
+  // record pointing at its own kind's
   int2* dtl = nullptr;
   int *dfaces = nullptr, *dcls = nullptr;
   double2** dT4s = nullptr;
-  if (c->map_mode == 0) {
+  if (c->map_mode == 0 || c->map_mode == 2) {
+    std::vector<int> rep;  // subdomains whose maps are materialised
+    if (int e = assign_map_offsets(c, rep)) return e;
     if (!c->T) CK(dalloc(c, (void**)&c->T, c->T_elems * sizeof(double2)));
     std::vector<int2> tl;
     std::vector<int> faces(4 * c->plan.nsub, 0), cls(c->plan.nsub, 0);
+    for (int s2 : rep)
+      for (int t = 0; t * kRowTile < c->plan.subs[s2].k * n; ++t) tl.push_back(make_int2(s2, t));
     for (int s2 = 0; s2 < c->plan.nsub; ++s2) {
       const SubPlan& sp = c->plan.subs[s2];
-      const int K = sp.k * n;
-      if (sp.rank == c->plan.rank)  // own maps only (row bands)
-        for (int t = 0; t * kRowTile < K; ++t) tl.push_back(make_int2(s2, t));
       for (int q = 0; q < sp.k; ++q) faces[4 * s2 + q] = sp.face[q];
       cls[s2] = c->sub_class[s2];
     }
@@ -2476,7 +2527,8 @@ int hs_set_gmres_mode(hs_ctx* c, int mode) {
 
 int hs_set_map_mode(hs_ctx* c, int mode) {
   if (!c) return fail(nullptr, 1, "null context");
-  if (mode != 0 && mode != 1) return fail(c, 1, "map mode must be 0 (per subdomain) or 1 (shared)");
+  if (mode < 0 || mode > 2)
+    return fail(c, 1, "map mode must be 0 (per subdomain), 1 (shared class maps, DMMA) or 2 (per kind, aliased)");
   if (mode != c->map_mode) {
     c->map_mode = mode;
     c->factored = false;  // maps must be (re)built in the new layout

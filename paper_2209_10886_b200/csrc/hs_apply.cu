@@ -129,6 +129,7 @@ struct FusedArgs {
   int nv;  // slab vectors per tile at most (shared-memory layout)
   unsigned long long* trace;  // per ticket: claim, inputs ready, map streamed, signalled (globaltimer ns), sm<<32|tile
   int direct_signal;          // TMA kernel: warp 0 signals itself (latency-bound plans), else the signaller warp
+  int map_keep;               // maps re-read by many tiles (aliased per-kind maps): keep them in L2
   double2* split_buf;         // split-K partial sums [pair][half][32 rows][2]
   int* split_cnt;             // split-K arrivals per pair (odd arrival combines)
   MultiRankArgs mr;
@@ -572,7 +573,7 @@ __global__ void __maxnreg__(96) k_bsp_tma(FusedArgs a) {  // 96: two 10-warp CTA
   }
   if (warp == NW) {  // ---- producer
     if (lane == 0) {
-      const unsigned long long pol = l2_evict_first();
+      const unsigned long long pol = a.map_keep ? l2_evict_last() : l2_evict_first();
       long long g = 0;
       for (int q = 0;; ++q) {
         const int d = q & 1;
@@ -979,6 +980,7 @@ cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double
     a.ntiles = f.ntiles; a.n = c.n; a.maxK = f.maxK; a.nv = f.nv;
     a.direct_signal = f.direct_signal;
     a.split_buf = f.split_buf; a.split_cnt = f.split_cnt;
+    a.map_keep = c.map_mode == 2;
     a.trace = (c.trace_on && c.trace && c.trace_cap >= (size_t)f.ntiles) ? c.trace : nullptr;
     if (a.trace) c.trace_rows = f.ntiles;
     return f.stages == 12 ? launch_tma<12, false>(c, f, a, 1) : launch_tma<5, false>(c, f, a, 1);
@@ -1038,6 +1040,7 @@ cudaError_t launch_bsp_fused_ranks(Ctx& c, const DevFused& f, const MultiRankArg
   a.ntiles = 0; a.n = c.n; a.maxK = f.maxK; a.nv = f.nv; a.trace = nullptr;
   a.direct_signal = f.direct_signal;
   a.split_buf = f.split_buf; a.split_cnt = f.split_cnt;
+  a.map_keep = c.map_mode == 2;
   a.mr = mr;
   const int G = mr.self < 0 ? mr.G : 1;
   if (f.tma) {

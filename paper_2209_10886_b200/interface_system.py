@@ -167,7 +167,11 @@ class GpuInterfaceSystem:
         """maps = "subdomain": one compact Schur map per subdomain, streamed from
         HBM by the step kernels (the graded path); "shared": only the distinct
         operators' maps (generic + scatterer) are kept and every step is a DMMA
-        contraction with the map L2-resident (discretization.py:224-229)."""
+        contraction with the map L2-resident (discretization.py:224-229);
+        "kinds": one compact map per distinct (operator, face set) -- the same
+        bytes as "subdomain" for every subdomain, read by the same fused
+        kernels, but ~18 maps instead of one per subdomain, so the stream is
+        served from L2 (kept there with an evict-last policy)."""
         if workers < 1:
             raise ValueError(f"workers must be >= 1, got {workers}")
         self.spec = spec
@@ -184,10 +188,11 @@ class GpuInterfaceSystem:
                 raise ValueError("a sharded system needs the NCCL unique id of rank 0")
             buf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
             self.ctx.call("hs_comm_init", buf)
-        if maps not in ("subdomain", "shared"):
-            raise ValueError(f"maps must be 'subdomain' or 'shared', got {maps!r}")
+        modes = {"subdomain": 0, "shared": 1, "kinds": 2}
+        if maps not in modes:
+            raise ValueError(f"maps must be 'subdomain', 'shared' or 'kinds', got {maps!r}")
         self.maps = maps
-        self.ctx.call("hs_set_map_mode", 1 if maps == "shared" else 0)
+        self.ctx.call("hs_set_map_mode", modes[maps])
         # one-RHS BSP applies as a single dataflow launch: fused=True runs the
         # map-once plan (each map row read ~once per apply; equal to the step
         # sequence to rounding); fused=False one launch per step, also in

@@ -325,3 +325,24 @@ def _run_variant_script(script, env):
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-3000:]
     return out.stdout.strip()
+
+
+@pytest.mark.parametrize("name,c,blocks", [("small_6x3", small_case(6, 3, 16), 5), ("cfg1", CONFIGS[1], None),
+                                           ("cfg2", CONFIGS[2], 4), ("cfg3", CONFIGS[3], 4)])
+def test_kind_maps_bitwise(name, c, blocks):
+    """maps="kinds" (one compact map per (operator class, face set), every
+    subdomain record aliasing its kind's): bitwise the per-subdomain maps, for
+    the fused apply, GMRES, the per-step path and the (I - S) apply."""
+    spec, part = product_problem(c)
+    a = GpuInterfaceSystem(spec, part, sweep=SweepConfig(blocks=blocks))
+    b = GpuInterfaceSystem(spec, part, maps="kinds", sweep=SweepConfig(blocks=blocks))
+    assert b.ctx.memory() < a.ctx.memory() or c["n1"] * c["n2"] <= 9
+    g = cvec(47, a.layout.size)
+    assert np.array_equal(a.bsp_apply(g), b.bsp_apply(g))
+    assert np.array_equal(a.apply_interface_operator(g), b.apply_interface_operator(g))
+    rhs = a.rhs() if c.get("center") is not None else cvec(5, a.layout.size)
+    ra, rb = a.gmres(rhs, "bsp", tol=1e-8, maxit=300), b.gmres(rhs, "bsp", tol=1e-8, maxit=300)
+    assert ra.iterations == rb.iterations and np.array_equal(ra.solution, rb.solution)
+    d = GpuInterfaceSystem(spec, part, maps="kinds", fused=False, sweep=SweepConfig(blocks=blocks))
+    e = GpuInterfaceSystem(spec, part, fused=False, sweep=SweepConfig(blocks=blocks))
+    assert np.array_equal(d.bsp_apply(g), e.bsp_apply(g))
