@@ -740,6 +740,17 @@ int fused_plan_host(const Ctx* c, const Plan& P, const std::vector<StepTable>& f
     const int workers = (f.tma ? (f.stages == 12 ? 1 : 2) : (f.rt == 1 ? 6 : 1)) * c->num_sms;
     tiles = schedule_tickets(tiles, deps, tile_inc, tile_cost, P.npairs, workers);
   }
+  // wout writes per block per apply (tile faces of phases 3 / 5 and FT_WOUT 2 / 4)
+  f.wwtot.assign(P.npairs, 0);
+  for (const FusedTile& t : tiles) {
+    if (t.ks == 0) continue;  // a split-K pair writes once (its second arrival)
+    const bool wo = t.phase == 3 || t.phase == 5 || ((t.phase == 2 || t.phase == 4) && (t.flags & FT_WOUT));
+    if (!wo) continue;
+    const DevItem& it = items[t.item];
+    const SubPlan& sp = P.subs[it.s];
+    const int r0 = std::max(it.rlo, t.tile * kRowTile * f.rt), r1 = std::min(it.rhi, (t.tile + 1) * kRowTile * f.rt);
+    for (int q = r0 / n; q * n < r1; ++q) f.wwtot[sp.tgt_block[q]]++;
+  }
   if (keep_rank >= 0) {
     std::vector<FusedTile> mine;
     for (const FusedTile& t : tiles)
@@ -750,6 +761,7 @@ int fused_plan_host(const Ctx* c, const Plan& P, const std::vector<StepTable>& f
   f.ntiles = (int)tiles.size();
   f.ndeps = (int)deps.size();
   f.wtot = written;  // signals per block per apply (every rank's tiles)
+
   return 0;
 }
 
@@ -1108,6 +1120,8 @@ void free_peer_plans(Ctx* c) {
   }
   dfree(c, p.wtot, 0);
   p.wtot = nullptr;
+  dfree(c, p.wwtot, 0);
+  p.wwtot = nullptr;
 }
 
 int peer_barrier(Ctx* c);
@@ -1121,9 +1135,10 @@ int peer_restart_epochs(Ctx* c) {
   if (p.epoch == 0) return 0;
   CK(cudaStreamSynchronize(c->stream));
   if (int e = peer_barrier(c)) return e;
-  CK(cudaMemsetAsync(p.counters[c->plan.rank], 0, (c->plan.npairs + 2) * sizeof(int), c->stream));
+  CK(cudaMemsetAsync(p.counters[c->plan.rank], 0, (2 * c->plan.npairs + 2) * sizeof(int), c->stream));
   if (int e = peer_barrier(c)) return e;
   p.epoch = 0;
+  p.ims_epoch = 0;
   p.epochs = !(getenv("HS_PEER_BARRIERS") && atoi(getenv("HS_PEER_BARRIERS")) != 0);
   return 0;
 }
@@ -1169,6 +1184,7 @@ int build_peer_plan(Ctx* c, bool ims) {
   const DevFused& other = ims ? p.plan : p.plan_ims;
   if (other.built && other.wtot != f.wtot) p.epochs = false;
   if (!p.wtot && upload(c, &p.wtot, f.wtot)) return -1;
+  if (ims && !p.wwtot && upload(c, &p.wwtot, f.wwtot)) return -1;
   f.built = true;
   return 0;
 }
@@ -1210,7 +1226,14 @@ int do_precond_peer(Ctx* c, const double2* r, double2* z, double2* wout) {
     mr.wtot = p.wtot;
     mr.own_blocks = p.own_blocks;
     mr.n_own = p.n_own;
-    for (int g = 0; g < p.G; ++g) mr.inflag[g] = p.inflag[g];
+    for (int g = 0; g < p.G; ++g) {
+      mr.inflag[g] = p.inflag[g];
+      mr.wdone[g] = p.wdone[g];
+    }
+    if (ims) {  // the A M v apply also drains the wout rows other ranks write
+      mr.ims_epoch = ++p.ims_epoch;
+      mr.wwtot = p.wwtot;
+    }
     CK(cudaMemsetAsync(p.counters[me] + P.npairs, 0, sizeof(int), c->stream));  // own ticket only
     c->launches++;
     k_post_epoch<<<1, 1, 0, c->stream>>>(p.inflag[me], (int)mr.epoch);
@@ -2392,8 +2415,9 @@ int hs_peer_export(hs_ctx* c, uint8_t handle[64]) {
   NEED_GPU(c);
   PeerRanks& p = c->peer;
   const size_t L = (size_t)c->plan.L;
-  // FV_N vectors, npairs completion counters, the ticket, the inputs-posted epoch flag
-  const size_t need = FV_N * L * sizeof(double2) + (size_t)(c->plan.npairs + 2) * sizeof(int);
+  // FV_N vectors, npairs completion counters, the ticket, the inputs-posted
+  // epoch flag, npairs wout-write counters
+  const size_t need = FV_N * L * sizeof(double2) + (size_t)(2 * c->plan.npairs + 2) * sizeof(int);
   if (!p.own || p.bytes != need) {
     dfree(c, p.own, 0);
     p.own = nullptr;
@@ -2439,6 +2463,7 @@ int hs_peer_open(hs_ctx* c, const uint8_t* handles, int nranks) {
     p.vec[g] = (double2*)base;
     p.counters[g] = (int*)(base + FV_N * L * sizeof(double2));
     p.inflag[g] = p.counters[g] + c->plan.npairs + 1;
+    p.wdone[g] = p.inflag[g] + 1;
   }
   std::vector<int> br(c->plan.npairs), own;
   for (int b = 0; b < c->plan.npairs; ++b) {

@@ -158,6 +158,7 @@ struct RankView {
   __device__ int ntiles() const { return MR ? a.mr.ntiles[cr] : a.ntiles; }
   __device__ int owner(int block) const { return MR ? a.mr.blk_rank[block] : 0; }
   __device__ int* done(int block) const { return (MR ? a.mr.done[owner(block)] : a.done) + block; }
+  __device__ int* wdone(int block) const { return a.mr.wdone[owner(block)] + block; }
   // completion count a dependency waits for (epoch protocol: counters accumulate)
   __device__ int target(const FusedDep& dp) const {
     return MR && a.mr.epoch ? dp.count + (int)(a.mr.epoch - 1) * a.mr.wtot[dp.block] : dp.count;
@@ -180,6 +181,11 @@ struct RankView {
       const volatile int* p = a.mr.done[cr] + b;
       const int want = (int)a.mr.epoch * a.mr.wtot[b];
       while (*p < want) __nanosleep(64);
+      if (a.mr.ims_epoch && a.mr.wwtot) {  // A M v: the wout rows other ranks write
+        const volatile int* q = a.mr.wdone[cr] + b;
+        const int wq = (int)a.mr.ims_epoch * a.mr.wwtot[b];
+        while (*q < wq) __nanosleep(64);
+      }
     }
     asm volatile("fence.acq_rel.sys;" ::: "memory");
   }
@@ -310,13 +316,21 @@ __device__ __forceinline__ void slab_srcs(const RankView<MR>& rv, int phase, int
 // phases 2 and 4, whose upper rows write wout).  One fence by the signalling
 // thread publishes the epilogue stores the barrier ordered before it
 // (cumulativity), instead of a fence per storing lane.
+// Row bands with the epoch protocol also count the wout writes (phases 3 and
+// 5, phases 2 / 4 with FT_WOUT) per block, so the owner can drain them.
+// phase < 0: nothing (the first half of a split-K pair).
 template <bool MR>
-__device__ __forceinline__ void tile_signal(const RankView<MR>& rv, int phase, int r0, int r1, int n, int nlow,
-                                            const int* tgt) {
-  if (phase == 3 || phase == 5) return;
+__device__ __forceinline__ void tile_signal(const RankView<MR>& rv, int phase, int flags, int r0, int r1, int n,
+                                            int nlow, const int* tgt) {
+  if (phase < 0) return;
+  const bool wout = phase == 3 || phase == 5 || ((phase == 2 || phase == 4) && (flags & FT_WOUT));
+  const bool counts = MR && wout && rv.a.mr.wdone[0] != nullptr;
+  if ((phase == 3 || phase == 5) && !counts) return;
   rv.fence();
-  for (int f = r0 / n; f * n < r1; ++f)
-    if (phase <= 1 || f < nlow) atomicAdd(rv.done(tgt[f] / n), 1);
+  for (int f = r0 / n; f * n < r1; ++f) {
+    if (phase <= 1 || ((phase == 2 || phase == 4) && f < nlow)) atomicAdd(rv.done(tgt[f] / n), 1);
+    if (counts) atomicAdd(rv.wdone(tgt[f] / n), 1);
+  }
 }
 
 // Register-streaming contraction of RT strips with NV slab vectors (xs,
@@ -466,7 +480,8 @@ __global__ void __launch_bounds__(NW * 32, RT == 1 ? 6 : 1) k_bsp_fused(FusedArg
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      tile_signal(rv, ft.phase, max(it.rlo, s0 * kRowTile), min(it.rhi, (s0 + RT) * kRowTile), n, sb.nlow, sb.tgt);
+      tile_signal(rv, ft.phase, ft.flags, max(it.rlo, s0 * kRowTile), min(it.rhi, (s0 + RT) * kRowTile), n, sb.nlow,
+                  sb.tgt);
       if (tr) {
         tr[4] = gtimer();
         tr[5] = ((unsigned long long)smid() << 32) | ((unsigned)blockIdx.x << 8) | (unsigned)ft.phase;
@@ -488,8 +503,9 @@ __global__ void __launch_bounds__(NW * 32, RT == 1 ? 6 : 1) k_bsp_fused(FusedArg
 // register-streaming kernel idles ~30 % of a tile's time at cfg3 on the
 // dependency wait, slab load and epilogue; profiles/r01/fused_trace_summary.txt).
 // Same arithmetic order as k_step1 (bitwise identical).
+constexpr int kSigStop = -99;  // SigRec.phase: the consumers are done (phase -1: a record with nothing to signal)
 struct SigRec {  // a tile's completions, handed from the consumers to the signaller warp
-  int phase, nlow, r0, r1;
+  int phase, flags, nlow, r0, r1;
   int tgt[4];
   unsigned long long* tr;
 };
@@ -564,8 +580,8 @@ __global__ void __maxnreg__(96) k_bsp_tma(FusedArgs a) {  // 96: two 10-warp CTA
         mbar_wait(&sfull[d], (q >> 1) & 1);  // acquire: warp 0's epilogue stores
         const SigRec r = sig[d];
         mbar_arrive(&sempty[d]);
-        if (r.phase < 0) break;
-        tile_signal(rv, r.phase, r.r0, r.r1, a.n, r.nlow, r.tgt);
+        if (r.phase == kSigStop) break;
+        tile_signal(rv, r.phase, r.flags, r.r0, r.r1, a.n, r.nlow, r.tgt);
         if (r.tr) r.tr[4] = gtimer();
       }
     }
@@ -624,7 +640,7 @@ __global__ void __maxnreg__(96) k_bsp_tma(FusedArgs a) {  // 96: two 10-warp CTA
     if (td.t >= rv.ntiles()) {
       if (threadIdx.x == 0 && !a.direct_signal) {  // tell the signaller to stop
         mbar_wait(&sempty[q & 1], ((q >> 1) & 1) ^ 1);
-        sig[q & 1].phase = -1;
+        sig[q & 1].phase = kSigStop;
         mbar_arrive(&sfull[q & 1]);
       }
       rv.drain(blockIdx.x * NT + threadIdx.x, gridDim.x * NT);
@@ -740,10 +756,10 @@ __global__ void __maxnreg__(96) k_bsp_tma(FusedArgs a) {  // 96: two 10-warp CTA
         }
       }
       if (finish && erow_ok) epi_store(rv, td.phase, td.flags, elow, eo, eoff, y1, y2, e1, e2, e3);
-      const int sphase = finish ? td.phase : 3;  // the first half of a pair signals nothing
+      const int sphase = finish ? td.phase : -1;  // the first half of a pair signals nothing
       __syncwarp();
       if (lane == 0 && a.direct_signal) {  // latency-bound plans: no hand-off hop
-        tile_signal(rv, sphase, max(td.rlo, td.row0), min(td.rhi, td.row0 + kRowTile), n, td.nlow, td.tgt);
+        tile_signal(rv, sphase, td.flags, max(td.rlo, td.row0), min(td.rhi, td.row0 + kRowTile), n, td.nlow, td.tgt);
         if (tr) {
           tr[4] = gtimer();
           tr[5] = ((unsigned long long)smid() << 32) | ((unsigned)blockIdx.x << 8) | (unsigned)td.phase;
@@ -751,7 +767,7 @@ __global__ void __maxnreg__(96) k_bsp_tma(FusedArgs a) {  // 96: two 10-warp CTA
       } else if (lane == 0) {  // hand the completion signals to the signaller warp
         mbar_wait(&sempty[q & 1], ((q >> 1) & 1) ^ 1);
         SigRec& r = sig[q & 1];
-        r.phase = sphase; r.nlow = td.nlow;
+        r.phase = sphase; r.flags = td.flags; r.nlow = td.nlow;
         r.r0 = max(td.rlo, td.row0); r.r1 = min(td.rhi, td.row0 + kRowTile);
         for (int f = 0; f < 4; ++f) r.tgt[f] = td.tgt[f];
         r.tr = tr;

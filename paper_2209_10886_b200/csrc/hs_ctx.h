@@ -144,6 +144,7 @@ struct DevFused {
   FusedDep* deps = nullptr;
   int nitems = 0, ntiles = 0, ndeps = 0, maxK = 0;
   std::vector<int> wtot;    // block -> completion signals per apply (all ranks' tiles)
+  std::vector<int> wwtot;   // block -> wout-writing tile faces per apply (all ranks' tiles)
   int nv = 1;               // vectors per tile (2: the map-once plan's phase-4 tiles)
   bool map_once = false;    // map-once plan (else per-step order, bitwise = k_step1)
   int rt = 1;               // 32-row strips per tile
@@ -220,6 +221,11 @@ struct MultiRankArgs {
   const int* inflag[kMaxRanks] = {};   // per rank: last epoch whose inputs are posted
   const int* own_blocks = nullptr;     // this rank's blocks (drain)
   int n_own = 0;
+  // wout (GMRES's (I - S) z) is written by tiles that signal nothing on done:
+  // they count in wdone, drained to ims_epoch * wwtot for the A M v applies
+  int* wdone[kMaxRanks] = {};
+  const int* wwtot = nullptr;
+  unsigned ims_epoch = 0;
 };
 
 // Emulated row bands on one GPU (hs_set_emulated_ranks): per-rank vectors,
@@ -249,6 +255,9 @@ struct PeerRanks {
   int* counters[kMaxRanks] = {};      // per rank: npairs counters + 1 ticket
   void* opened[kMaxRanks] = {};       // IPC mappings (closed at destroy)
   int* inflag[kMaxRanks] = {};        // per rank: epoch whose inputs are posted (region tail)
+  int* wdone[kMaxRanks] = {};         // per rank: wout-write counters of its blocks (region tail)
+  int* wwtot = nullptr;               // block -> wout writes per A M v apply
+  unsigned ims_epoch = 0;             // A M v applies run so far
   DevFused plan, plan_ims;            // global plans; tiles = this rank's only
   int* blk_rank = nullptr;            // block -> owner rank
   int* wtot = nullptr;                // block -> completion signals per apply (same for both plans)

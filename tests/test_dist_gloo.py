@@ -372,7 +372,17 @@ def _tile_signals(band, rec):
             if phase <= 1 or f < nlow]
 
 
-def _run_peer_tiles(band, plan, V, CNT, base=None):
+def _tile_wout(band, rec):
+    """Blocks whose wout rows a tile writes (counted for the owner's drain)."""
+    i1, i2, rlo, rhi, c0, c1, alt, row0, phase, flags, rmask, _ = rec
+    if not (phase in (3, 5) or (phase in (2, 4) and flags & 2)):
+        return []
+    s, n = (i1, i2), band.n
+    r0, r1 = max(rlo, row0), min(rhi, row0 + 32)
+    return [band.lat.m_index(band.lat.faces[s][f][1], s) - 1 for f in range(r0 // n, (r1 - 1) // n + 1)]
+
+
+def _run_peer_tiles(band, plan, V, CNT, base=None, WCNT=None):
     """base: per-block completion count at the start of this apply (epoch
     protocol: counters are never reset), else zero."""
     import time
@@ -449,6 +459,9 @@ def _run_peer_tiles(band, plan, V, CNT, base=None):
                     Vo[FV_WOUT, t] = Vo[FV_R, t] - a
         for blk in _tile_signals(band, rec):
             CNT[band.owner[blk], blk] += 1
+        if WCNT is not None:
+            for blk in _tile_wout(band, rec):
+                WCNT[band.owner[blk], blk] += 1
 
 
 def _plan_of(band, ims, rank):
@@ -460,7 +473,7 @@ def _plan_of(band, ims, rank):
     return _parse_plan(np.frombuffer(buf, dtype=np.int32))
 
 
-def _peer_epoch_worker(rank, world, port, case, blocks, vbuf, cbuf, fbuf, napply, q):
+def _peer_epoch_worker(rank, world, port, case, blocks, vbuf, cbuf, fbuf, napply, q, wbuf=None):
     """The barrier-free epoch protocol of the GPU path: for apply e every rank
     copies in its r, posts e, waits for every rank's post, runs its tiles with
     dependency counts offset by the blocks' totals of the previous applies,
@@ -482,8 +495,15 @@ def _peer_epoch_worker(rank, world, port, case, blocks, vbuf, cbuf, fbuf, napply
             wt[ims] = w
         assert np.array_equal(wt[False], wt[True])  # one total per block for both plans
         W = wt[False]
+        WW = np.zeros(len(band.owner), dtype=np.int64)  # wout writes per block per A M v apply
+        for r in range(world):
+            for rec, _ in _plan_of(band, True, r):
+                for b in _tile_wout(band, rec):
+                    WW[b] += 1
         V = vbuf.numpy().view(complex)[..., 0]
         CNT, FLAG = cbuf.numpy(), fbuf.numpy()
+        WCNT = wbuf.numpy()
+        n_ims = 0
         own = np.where(band.owner == rank)[0]
         m = band.owned_mask()
         from oracle import Preconditioner
@@ -499,9 +519,12 @@ def _peer_epoch_worker(rank, world, port, case, blocks, vbuf, cbuf, fbuf, napply
             for g in range(world):
                 while FLAG[g] < e:
                     time.sleep(0)
-            _run_peer_tiles(band, plans[ims], V, CNT, base=(e - 1) * W)
+            n_ims += int(ims)
+            _run_peer_tiles(band, plans[ims], V, CNT, base=(e - 1) * W, WCNT=WCNT)
             for b in own:  # drain: every write into this rank's blocks has landed
                 while CNT[rank, b] < e * W[b]:
+                    time.sleep(0)
+                while ims and WCNT[rank, b] < n_ims * WW[b]:  # and the wout rows (A M v)
                     time.sleep(0)
             ref = pc.bsp_apply(r)
             got = V[rank, FV_WOUT if ims else FV_Z].copy()
@@ -577,17 +600,21 @@ def test_peer_memory_protocol_matches_oracle(case, world, blocks, ims):
 def test_peer_memory_epoch_protocol(case, world, blocks):
     """Four back-to-back applies (BSP, A M v, BSP, A M v) over the peer
     buffers with the epoch protocol and no barrier between them: every rank's
-    blocks equal the oracle each time."""
+    blocks equal the oracle each time.  (The wout rows of the A M v plan are
+    written by tiles that signal no completion; without their own counters
+    and drain a rank read its (I - S) z before a peer's late tile had written
+    it -- this test caught that race intermittently.)"""
     from oracle.lattice import Lattice
     lat = Lattice(case["n1"], case["n2"])
     L = lat.n_pairs * case["n"]
     vbuf = torch.zeros(world, 6, L, 2, dtype=torch.float64).share_memory_()
     cbuf = torch.zeros(world, lat.n_pairs, dtype=torch.int64).share_memory_()
     fbuf = torch.zeros(world, dtype=torch.int64).share_memory_()
+    wbuf = torch.zeros(world, lat.n_pairs, dtype=torch.int64).share_memory_()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_peer_epoch_worker, args=(r, world, port, case, blocks, vbuf, cbuf, fbuf, 4, q))
+    procs = [ctx.Process(target=_peer_epoch_worker, args=(r, world, port, case, blocks, vbuf, cbuf, fbuf, 4, q, wbuf))
              for r in range(world)]
     for p in procs:
         p.start()
