@@ -1675,8 +1675,8 @@ int hs_factor(hs_ctx* c) {
   int* dbad;
   CK(tmp.alloc(&dbad, sizeof(int)));
   CK(cudaMemsetAsync(dbad, 0, sizeof(int), c->stream));
-  CK(factor_blocks(*c, X, xstride, dmasks, ncls, Rp, Cp, pstride, dbad));
-  // boundary responses for the 4n unit columns
+  // boundary responses for the 4n unit columns, the forward sweep overlapped
+  // with the factorisation (factor_and_solve_boundary)
   const int R = 4 * n;
   double2 *Y, *Bk, *G;
   const long long ystride = nn * R, bstride = (long long)n * R, gstride = 4LL * n * R;
@@ -1689,7 +1689,8 @@ int hs_factor(hs_ctx* c) {
     dirichlet_boundary_extras(c, c->classes[k], ex);
     if (upload_extras(c, ex, extras[k], tmp.p)) return -1;
   }
-  CK(solve_boundary(*c, X, xstride, dmasks, ncls, R, R, extras.data(), Y, ystride, Bk, bstride, G, gstride));
+  CK(factor_and_solve_boundary(*c, X, xstride, dmasks, ncls, Rp, Cp, pstride, dbad, R, R, extras.data(), Y, ystride,
+                               Bk, bstride, G, gstride));
   // T4 = -(s/d) I - (2 tau / (h^3 d^2)) G
   const std::complex<double> tau(c->tau_re, c->tau_im);
   const double h = c->h;

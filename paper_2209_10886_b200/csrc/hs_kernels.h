@@ -42,6 +42,10 @@ void launch_pack_strips(Ctx& c, const double2* T4, double2* out, int rows, int c
 // ---- factorisation (hs_schur.cu)
 cudaError_t factor_blocks(Ctx& c, double2* X, long long xstride, const uint8_t* dmasks, int ncls,
                           double2* Rp, double2* Cp, long long pstride, int* dbad);
+cudaError_t factor_and_solve_boundary(Ctx& c, double2* X, long long xstride, const uint8_t* dmasks, int ncls,
+                                      double2* Rp, double2* Cp, long long pstride, int* dbad, int R, int nunit,
+                                      const ExtraRHS* extras, double2* Y, long long ystride, double2* Bk,
+                                      long long bstride, double2* G, long long gstride);
 cudaError_t solve_boundary(Ctx& c, const double2* X, long long xstride, const uint8_t* dmasks,
                            int ncls, int R, int nunit, const ExtraRHS* extras, double2* Y,
                            long long ystride, double2* Bk, long long bstride, double2* G,

@@ -535,6 +535,73 @@ void zgemm(cudaStream_t st, int M, int N, int K, double2 alpha, const double2* A
   k_zgemm<<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, sa, B, ldb, sb, beta, C, ldc, sc);
 }
 
+// Factorisation interleaved with the forward sweep of the boundary solves:
+// row k's forward step only needs X_k, so it runs on a side stream while the
+// main stream factors rows k+1.. (the panel chain is latency-bound and leaves
+// the GPU mostly idle); the backward sweep and the extraction follow.
+// Same kernels and arithmetic as factor_blocks + solve_boundary.
+cudaError_t factor_and_solve_boundary(Ctx& c, double2* X, long long xstride, const uint8_t* dmasks, int ncls,
+                                      double2* Rp, double2* Cp, long long pstride, int* dbad, int R, int nunit,
+                                      const ExtraRHS* extras, double2* Y, long long ystride, double2* Bk,
+                                      long long bstride, double2* G, long long gstride) {
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(k_gj_update, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGjUpdSmem);
+  if (attr != cudaSuccess) return attr;
+  const int n = c.n;
+  const double ih2 = 1.0 / (c.h * c.h);
+  const long long nn = (long long)n * n;
+  const int rthreads = R < 256 ? ((R + 31) / 32) * 32 : 256;
+  OpParams P = op_params(c);
+  cudaStream_t side;
+  cudaError_t e = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
+  if (e != cudaSuccess) return e;
+  std::vector<cudaEvent_t> ev(n);
+  for (auto& x : ev) cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+  cudaEvent_t start, done;
+  cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+  cudaEventRecord(start, c.stream);  // the side stream starts after everything queued before
+  cudaStreamWaitEvent(side, start, 0);
+  for (int k = 0; k < n; ++k) {
+    k_formS<<<dim3(n, ncls), 128, 0, c.stream>>>(X, xstride, dmasks, P, k);
+    for (int j0 = 0; j0 < n; j0 += 32) {
+      int nb = n - j0 < 32 ? n - j0 : 32;
+      k_gj_inv<<<dim3(1 + 8, ncls), 256, 0, c.stream>>>(X, xstride, k, n, j0, nb, Rp + 32LL * n, Rp, Cp,
+                                                          pstride, dbad);
+      k_gj_update<<<dim3((n + 31) / 32, (n + 31) / 32, ncls), 256, kGjUpdSmem, c.stream>>>(
+          X, xstride, k, n, j0, nb, Rp + 32LL * n, Rp, Cp, pstride);
+    }
+    cudaEventRecord(ev[k], c.stream);  // X_k complete
+    cudaStreamWaitEvent(side, ev[k], 0);
+    k_rhs_fwd<<<dim3(n, ncls), rthreads, 0, side>>>(Bk, bstride, Y, ystride, dmasks, n, R, nunit, ih2, k);
+    for (int cl = 0; cl < ncls; ++cl) {
+      const ExtraRHS& ex = extras[cl];
+      if (ex.row_ptr.empty()) continue;
+      int b0 = ex.row_ptr[k], b1 = ex.row_ptr[k + 1];
+      if (b1 > b0)
+        k_rhs_extra<<<(b1 - b0 + 255) / 256, 256, 0, side>>>(Bk, bstride, R, ex.d_x + b0, ex.d_col + b0,
+                                                              ex.d_val + b0, b1 - b0, cl);
+    }
+    zgemm(side, n, R, n, make_double2(1, 0), X + k * nn, n, xstride, Bk, R, bstride, make_double2(0, 0),
+          Y + (long long)k * n * R, R, ystride, ncls);
+  }
+  cudaEventRecord(done, side);
+  cudaStreamWaitEvent(c.stream, done, 0);
+  for (int k = n - 2; k >= 0; --k) {
+    k_rhs_bwd<<<dim3(n, ncls), rthreads, 0, c.stream>>>(Bk, bstride, Y, ystride, dmasks, n, R, ih2, k);
+    zgemm(c.stream, n, R, n, make_double2(-1, 0), X + k * nn, n, xstride, Bk, R, bstride,
+          make_double2(1, 0), Y + (long long)k * n * R, R, ystride, ncls);
+  }
+  k_extract<<<dim3(4 * n, ncls), rthreads, 0, c.stream>>>(G, gstride, Y, ystride, n, R);
+  e = cudaGetLastError();
+  cudaStreamSynchronize(side);  // before the side stream and its events go away
+  for (auto& x : ev) cudaEventDestroy(x);
+  cudaEventDestroy(start);
+  cudaEventDestroy(done);
+  cudaStreamDestroy(side);
+  return e;
+}
+
 // Solve the factored block-tridiagonal systems for R right-hand sides and
 // extract the boundary values G (4n x R) per class.
 cudaError_t solve_boundary(Ctx& c, const double2* X, long long xstride, const uint8_t* dmasks,

@@ -9,5 +9,5 @@ torch.zeros(1, device="cuda"); torch.cuda.synchronize()
 t0 = time.perf_counter()
 s = GpuInterfaceSystem(spec, part, sweep=SweepConfig(blocks=c["blocks"]))
 torch.cuda.synchronize(); print("create+factor", time.perf_counter() - t0, "setup_time", s.setup_time)
-for i in range(3):
+for i in range(8):
     t0 = time.perf_counter(); s.ctx.call("hs_factor"); torch.cuda.synchronize(); print("refactor", i, time.perf_counter() - t0)
