@@ -753,8 +753,18 @@ int fused_plan_host(const Ctx* c, const Plan& P, const std::vector<StepTable>& f
   }
   if (keep_rank >= 0) {
     std::vector<FusedTile> mine;
-    for (const FusedTile& t : tiles)
-      if ((*sub_rank)[items[t.item].s] == keep_rank) mine.push_back(t);
+    double own_bytes = 0, all_bytes = 0;
+    for (const FusedTile& t : tiles) {  // streamed bytes of a tile (map rows x its columns + slabs)
+      const DevItem& it = items[t.item];
+      const int r0 = std::max(it.rlo, t.tile * kRowTile * f.rt), r1 = std::min(it.rhi, (t.tile + 1) * kRowTile * f.rt);
+      const double b = 16.0 * ((double)(r1 - r0) * (t.c1 - t.c0) + (t.phase == 4 ? 2 : 1) * (t.c1 - t.c0));
+      all_bytes += b;
+      if ((*sub_rank)[it.s] == keep_rank) {
+        mine.push_back(t);
+        own_bytes += b;
+      }
+    }
+    if (all_bytes > 0) f.bytes *= own_bytes / all_bytes;  // this rank's share of the apply's bytes
     tiles.swap(mine);
   }
   f.nitems = (int)items.size();
@@ -1251,7 +1261,19 @@ int do_precond_peer(Ctx* c, const double2* r, double2* z, double2* wout) {
   }
   mr.tiles[me] = f.tiles;
   mr.ntiles[me] = f.ntiles;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (c->timing) {
+    e0 = ev_get(c);
+    e1 = ev_get(c);
+    cudaEventRecord(e0, c->stream);
+  }
   CK(launch_bsp_fused_ranks(*c, f, mr));
+  if (e1) {  // this rank's kernel and its share of the algorithmic bytes
+    cudaEventRecord(e1, c->stream);
+    c->ev_pending.push_back({e0, e1});
+    c->ev_bytes.push_back(f.bytes);
+    c->ev_flops.push_back(f.bytes / 2.0);
+  }
   if (!p.epochs)
     if (int e = peer_barrier(c)) return e;
   CK(cudaMemcpyAsync(z, mine + FV_Z * L, L * sizeof(double2), cudaMemcpyDeviceToDevice, c->stream));
