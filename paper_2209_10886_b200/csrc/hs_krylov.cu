@@ -1065,18 +1065,19 @@ cudaError_t gmres_arnoldi1(Ctx& c, GmresDev& G, int k, int grid, int chunk, int 
 // grid barrier.  k_mgs_cluster (any R) needs ~5 us per step for the same work
 // (shared-memory tree reductions, unprefetched basis reads).
 template <int E>
-__global__ void __launch_bounds__(kMgs1MaxBlock, 1) k_mgs1c(GmresDev G, int k, int chunk) {
+__global__ void __launch_bounds__(kMgs1MaxBlock, 1) k_mgs1c(GmresDev G, int k, int chunk, int nbuf) {
   cg::cluster_group cl = cg::this_cluster();
   const int CS = (int)cl.num_blocks(), rank = (int)cl.block_rank();
   extern __shared__ __align__(16) double2 sm1[];
-  __shared__ double red[32][3];
-  __shared__ double pub[2][3];  // this CTA's partial, by parity (read by the cluster)
-  __shared__ double tot3[3];
+  __shared__ double red[32][kMgs1Comp];
+  __shared__ double pub[2][kMgs1Comp];  // this CTA's partial, by parity (read by the cluster)
+  __shared__ double tot6[kMgs1Comp];
   const int BD = blockDim.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = BD >> 5;
-  auto buf = [&](int j) { return sm1 + (size_t)(j & 1) * chunk; };  // v_j
-  double2* hs = sm1 + 2 * (size_t)chunk;  // k + 2: the column (rank 0)
-  double2* sns = hs + (k + 2);            // k
-  double* css = (double*)(sns + k);       // k
+  const bool pairs = nbuf == 4;  // two MGS steps per cluster barrier (see k_mgs1)
+  auto buf = [&](int j) { return sm1 + (size_t)(j % nbuf) * chunk; };  // v_j
+  double2* hs = sm1 + (size_t)nbuf * chunk;  // k + 2: the column (rank 0)
+  double2* sns = hs + (k + 2);               // k
+  double* css = (double*)(sns + k);          // k
   const long long LR = G.LR;
   const long long e0 = (long long)rank * chunk;
   const long long eend = min(e0 + (long long)chunk, LR);
@@ -1098,48 +1099,54 @@ __global__ void __launch_bounds__(kMgs1MaxBlock, 1) k_mgs1c(GmresDev G, int k, i
     cpa_commit();
   };
   int step = 0;
-  auto reduce = [&](double a, double b, double c, int pf_j) {
+  const int nc = pairs ? kMgs1Comp : 3;
+  auto reduce = [&](double (&x)[kMgs1Comp], int pf0, int pf1) {
     const int par = step & 1;
-    warp_sum3(a, b, c);
-    if (lane == 0) { red[wid][0] = a; red[wid][1] = b; red[wid][2] = c; }
+    warp_sum3(x[0], x[1], x[2]);
+    if (pairs) warp_sum3(x[3], x[4], x[5]);
+    if (lane == 0)
+      for (int q = 0; q < nc; ++q) red[wid][q] = x[q];
     __syncthreads();
     if (wid == 0) {
-      a = lane < nw ? red[lane][0] : 0.0;
-      b = lane < nw ? red[lane][1] : 0.0;
-      c = lane < nw ? red[lane][2] : 0.0;
-      warp_sum3(a, b, c);
-      if (lane == 0) {
-        if (CS > 1) { pub[par][0] = a; pub[par][1] = b; pub[par][2] = c; }
-        else { tot3[0] = a; tot3[1] = b; tot3[2] = c; }
-      }
+      for (int q = 0; q < nc; ++q) x[q] = lane < nw ? red[lane][q] : 0.0;
+      warp_sum3(x[0], x[1], x[2]);
+      if (pairs) warp_sum3(x[3], x[4], x[5]);
+      if (lane == 0)
+        for (int q = 0; q < nc; ++q) {
+          if (CS > 1) pub[par][q] = x[q];
+          else tot6[q] = x[q];
+        }
     }
-    if (pf_j >= 0) prefetch(pf_j);
-    if (CS == 1) {  // single CTA: the block sum is the total
-      __syncthreads();
-      ++step;
-      return make_double3(tot3[0], tot3[1], tot3[2]);
-    }
-    cl.sync();
-    if (wid == 0) {
-      // rank q's partial to lane q, summed in rank order by the butterfly
-      double x0 = 0.0, x1 = 0.0, x2 = 0.0;
-      if (lane < CS) {
-        const double* pq = cl.map_shared_rank(&pub[par][0], lane);
-        x0 = pq[0]; x1 = pq[1]; x2 = pq[2];
+    if (pf0 >= 0) prefetch(pf0);
+    if (pf1 >= 0) prefetch(pf1);
+    if (CS > 1) {
+      cl.sync();
+      if (wid == 0) {
+        // rank q's partial to lane q, summed in rank order by the butterfly
+        double y[kMgs1Comp] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        if (lane < CS) {
+          const double* pq = cl.map_shared_rank(&pub[par][0], lane);
+          for (int q = 0; q < nc; ++q) y[q] = pq[q];
+        }
+        warp_sum3(y[0], y[1], y[2]);
+        if (pairs) warp_sum3(y[3], y[4], y[5]);
+        if (lane == 0)
+          for (int q = 0; q < nc; ++q) tot6[q] = y[q];
       }
-      warp_sum3(x0, x1, x2);
-      if (lane == 0) { tot3[0] = x0; tot3[1] = x1; tot3[2] = x2; }
     }
     __syncthreads();
     ++step;
-    return make_double3(tot3[0], tot3[1], tot3[2]);
+    for (int q = 0; q < kMgs1Comp; ++q) x[q] = q < nc ? tot6[q] : 0.0;
   };
-  double3 tot;
-  prefetch(0);
-  if (k >= 1) prefetch(1);
+  double x[kMgs1Comp];
+  const int lead = pairs ? 3 : 2;
+  for (int j = 0; j < lead && j <= k; ++j) prefetch(j);
   if (rank == 0)
     for (int j = tid; j < k; j += BD) { css[j] = G.cs[j]; sns[j] = G.sn[j]; }
-  if (k >= 1) cpa_wait<1>(); else cpa_wait<0>();
+  {
+    const int later = min(lead, k + 1) - 1;
+    if (later >= 2) cpa_wait<2>(); else if (later == 1) cpa_wait<1>(); else cpa_wait<0>();
+  }
   {
     double2 acc = make_double2(0, 0);
     double nrm = 0;
@@ -1149,34 +1156,87 @@ __global__ void __launch_bounds__(kMgs1MaxBlock, 1) k_mgs1c(GmresDev G, int k, i
         cfma_conj(acc, buf(0)[tid + i * BD], wr[i]);
         nrm += wr[i].x * wr[i].x + wr[i].y * wr[i].y;
       }
-    tot = reduce(acc.x, acc.y, nrm, -1);
+    x[0] = acc.x; x[1] = acc.y; x[2] = nrm; x[3] = x[4] = x[5] = 0.0;
+    reduce(x, -1, -1);
   }
-  double2 h = make_double2(tot.x, tot.y);
+  double2 h = make_double2(x[0], x[1]);
   if (rank == 0 && tid == 0) {
-    G.wnorm0[0] = sqrt(tot.z);
+    G.wnorm0[0] = sqrt(x[2]);
     hs[0] = h;
   }
-  for (int j = 0; j <= k; ++j) {
-    const double2* vj = buf(j);
-    const double2* vn = buf(j + 1);
-    const bool more = j + 1 <= k;
-    if (more) cpa_wait<0>();
-    double2 acc = make_double2(0, 0);
-    double nrm = 0;
+  double hn2 = 0;
+  if (pairs) {
+    int p0 = 0, p1 = -1;
+    double2 hp0 = h, hp1 = make_double2(0, 0);
+    for (int a = 1;; a += 2) {
+      const int bb = a + 1;
+      const bool ha = a <= k, hb = bb <= k;
+      cpa_wait<0>();
+      const double2* vp0 = buf(p0);
+      const double2* vp1 = p1 >= 0 ? buf(p1) : vp0;
+      const double2* va = buf(a);
+      const double2* vb = buf(bb);
+      double2 al = make_double2(0, 0), be = al, ga = al;
+      double nrm = 0;
 #pragma unroll
-    for (int i = 0; i < E; ++i)
-      if (e0 + tid + (long long)i * BD < eend) {
-        wr[i] = csub(wr[i], cmul(h, vj[tid + i * BD]));  // w - H[j,k] V[j]
-        if (more) cfma_conj(acc, vn[tid + i * BD], wr[i]);
-        else nrm += wr[i].x * wr[i].x + wr[i].y * wr[i].y;
+      for (int i = 0; i < E; ++i)
+        if (e0 + tid + (long long)i * BD < eend) {
+          const int o = tid + i * BD;
+          wr[i] = csub(wr[i], cmul(hp0, vp0[o]));
+          if (p1 >= 0) wr[i] = csub(wr[i], cmul(hp1, vp1[o]));
+          if (ha) {
+            const double2 xa = va[o];
+            cfma_conj(al, xa, wr[i]);
+            if (hb) {
+              const double2 xb = vb[o];
+              cfma_conj(be, xb, wr[i]);
+              cfma_conj(ga, xb, xa);
+            }
+          } else {
+            nrm += wr[i].x * wr[i].x + wr[i].y * wr[i].y;
+          }
+        }
+      x[0] = al.x; x[1] = al.y; x[2] = ha ? be.x : nrm; x[3] = be.y; x[4] = ga.x; x[5] = ga.y;
+      reduce(x, bb + 1 <= k ? bb + 1 : -1, bb + 2 <= k ? bb + 2 : -1);
+      if (!ha) {
+        hn2 = x[2];
+        break;
       }
-    tot = reduce(acc.x, acc.y, nrm, j + 2 <= k ? j + 2 : -1);
-    if (more) {
-      h = make_double2(tot.x, tot.y);
-      if (rank == 0 && tid == 0) hs[j + 1] = h;
+      const double2 h_a = make_double2(x[0], x[1]);
+      const double2 h_b = csub(make_double2(x[2], x[3]), cmul(h_a, make_double2(x[4], x[5])));
+      if (rank == 0 && tid == 0) {
+        hs[a] = h_a;
+        if (hb) hs[bb] = h_b;
+      }
+      p0 = a; hp0 = h_a;
+      p1 = hb ? bb : -1; hp1 = h_b;
+    }
+  } else {
+    for (int j = 0; j <= k; ++j) {
+      const double2* vj = buf(j);
+      const double2* vn = buf(j + 1);
+      const bool more = j + 1 <= k;
+      if (more) cpa_wait<0>();
+      double2 acc = make_double2(0, 0);
+      double nrm = 0;
+#pragma unroll
+      for (int i = 0; i < E; ++i)
+        if (e0 + tid + (long long)i * BD < eend) {
+          wr[i] = csub(wr[i], cmul(h, vj[tid + i * BD]));  // w - H[j,k] V[j]
+          if (more) cfma_conj(acc, vn[tid + i * BD], wr[i]);
+          else nrm += wr[i].x * wr[i].x + wr[i].y * wr[i].y;
+        }
+      x[0] = acc.x; x[1] = acc.y; x[2] = nrm; x[3] = x[4] = x[5] = 0.0;
+      reduce(x, j + 2 <= k ? j + 2 : -1, -1);
+      if (more) {
+        h = make_double2(x[0], x[1]);
+        if (rank == 0 && tid == 0) hs[j + 1] = h;
+      } else {
+        hn2 = x[2];
+      }
     }
   }
-  const double hn = sqrt(tot.z);
+  const double hn = sqrt(hn2);
 #pragma unroll
   for (int i = 0; i < E; ++i) {
     const long long e = e0 + tid + (long long)i * BD;
@@ -1225,10 +1285,15 @@ cudaError_t gmres_arnoldi1c(Ctx& c, GmresDev& G, int k, int cs, int chunk, int E
   }();
   if (attr != cudaSuccess) return attr;
   c.launches++;
+  static const bool pairs_ok = [] {
+    const char* e = getenv("HS_MGS1_PAIRS");
+    return !e || atoi(e) != 0;
+  }();
+  int nbuf = pairs_ok && mgs1_smem(chunk, k, 4) <= kMgs1SmemMax ? 4 : 2;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cs);
   cfg.blockDim = dim3(bd);
-  cfg.dynamicSmemBytes = mgs1_smem(chunk, k, 2);
+  cfg.dynamicSmemBytes = mgs1_smem(chunk, k, nbuf);
   cfg.stream = c.stream;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -1237,9 +1302,9 @@ cudaError_t gmres_arnoldi1c(Ctx& c, GmresDev& G, int k, int cs, int chunk, int E
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  if (E == 1) return cudaLaunchKernelEx(&cfg, k_mgs1c<1>, G, k, chunk);
-  if (E == 2) return cudaLaunchKernelEx(&cfg, k_mgs1c<2>, G, k, chunk);
-  return cudaLaunchKernelEx(&cfg, k_mgs1c<4>, G, k, chunk);
+  if (E == 1) return cudaLaunchKernelEx(&cfg, k_mgs1c<1>, G, k, chunk, nbuf);
+  if (E == 2) return cudaLaunchKernelEx(&cfg, k_mgs1c<2>, G, k, chunk, nbuf);
+  return cudaLaunchKernelEx(&cfg, k_mgs1c<4>, G, k, chunk, nbuf);
 }
 
 // Back substitution for one right-hand side with m <= blockDim: thread t owns
