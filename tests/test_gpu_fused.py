@@ -156,7 +156,8 @@ def test_emulated_row_band_ranks_bitwise(name, c, blocks, ranks, plan):
     assert np.array_equal(s.bsp_apply(g), ref)
 
 
-MAP_ONCE_CASES = [("small_1x4", small_case(1, 4, 8), [None, 1]), ("small_3x3", small_case(3, 3, 8), [None, 1, 2]),
+MAP_ONCE_CASES = [("small_1x4", small_case(1, 4, 8), [None, 1]), ("small_5x1", small_case(5, 1, 8), [None, 1, 2]),
+                  ("small_2x7_n20", small_case(2, 7, 20), [None, 1, 3]), ("small_3x3", small_case(3, 3, 8), [None, 1, 2]),
                   ("small_6x3", small_case(6, 3, 16), [None, 2, 5]), ("small_4x4_n160", small_case(4, 4, 160), [None, 3]),
                   ("cfg1", CONFIGS[1], [None, 1, 3]), ("cfg2", CONFIGS[2], [None, 1, 2, 4, 8]), ("cfg3", CONFIGS[3], [4])]
 
