@@ -2136,7 +2136,8 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
     CK(cudaEventCreateWithFlags(&c->flag_ev[0], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->flag_ev[1], cudaEventDisableTiming));
   }
-  const bool lookahead = c->map_mode == 1 || (double)c->T_elems * 16.0 < 2e9;
+  bool lookahead = c->map_mode == 1 || (double)c->T_elems * 16.0 < 2e9;
+  if (const char* e = getenv("HS_GMRES_LOOKAHEAD")) lookahead = atoi(e) != 0;
   int c1chunk = 0, c1E = 0, c1bd = 0;
   const int c1cs = (dist || c->gmres_mode == 2) ? 0 : gmres_mgs1c_plan(LR, R, maxit, &c1chunk, &c1E, &c1bd);
   int cchunk = 0;
