@@ -502,7 +502,13 @@ __global__ void __launch_bounds__(NW * 32, RT == 1 ? 6 : 1) k_bsp_fused(FusedArg
 // with this tile's and the next tile's chunks, so HBM stays busy (the
 // register-streaming kernel idles ~30 % of a tile's time at cfg3 on the
 // dependency wait, slab load and epilogue; profiles/r01/fused_trace_summary.txt).
-// Same arithmetic order as k_step1 (bitwise identical).
+// Warps: producer (NW), signaller (NW + 1: takes each tile's release fence and
+// completion atomics off the consumers' path, or idle when the plan has the
+// consumers signal directly), consumers 0..NW-1 (warp 0 finishes the rows).
+// Map chunks carry an L2 evict-first policy (evict-last for aliased per-kind
+// maps).  Phase-4 tiles multiply two slabs per map read; split-K pairs (opt-in)
+// meet in `split_buf`.  Per-step plan: the k_step1 arithmetic order (bitwise
+// identical); map-once plan: the same column split, other phases (hs_ctx.h).
 constexpr int kSigStop = -99;  // SigRec.phase: the consumers are done (phase -1: a record with nothing to signal)
 struct SigRec {  // a tile's completions, handed from the consumers to the signaller warp
   int phase, flags, nlow, r0, r1;
