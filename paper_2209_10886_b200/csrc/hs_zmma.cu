@@ -248,10 +248,16 @@ __global__ void __launch_bounds__(THREADS) k_zmma(const MmaTask* __restrict__ ta
                                                   int n, int R, int KS) {
   extern __shared__ __align__(16) double2 dyn[];
   __shared__ ZCols zc;
+  // programmatic dependent launch: the next step's grid may launch now and
+  // run up to its own wait (task and column descriptors) while this one works
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int rank = KS > 1 ? (int)cg::this_cluster().block_rank() : 0;
   const MmaTask tk = tasks[blockIdx.x / KS];
   const int tid = threadIdx.x;
   zmma_cols(tk, cols, zc);
+  // the previous step's outputs (this step's inputs and epilogue operands) are
+  // complete and visible past this point
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   __syncthreads();
   const int nk_all = tk.K / KC;
   const int kc0 = (int)((long long)nk_all * rank / KS), kc1 = (int)((long long)nk_all * (rank + 1) / KS);
@@ -582,13 +588,16 @@ void launch_zmma(Ctx& c, const DevMma& m, const double2* A, const double2* srcA,
   cfg.blockDim = dim3(THREADS);
   cfg.dynamicSmemBytes = kZmmaSmem;
   cfg.stream = c.stream;
-  cudaLaunchAttribute attr[1];
+  static const bool pdl = !(getenv("HS_ZMMA_PDL") && atoi(getenv("HS_ZMMA_PDL")) == 0);
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = KS;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap with the previous step's tail
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 2 : 1;
   cudaLaunchKernelEx(&cfg, k_zmma, (const MmaTask*)m.tasks, (const MmaCol*)m.cols, A, srcA, srcB, e,
                      c.n, R, KS);
 }
