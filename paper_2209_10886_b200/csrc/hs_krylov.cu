@@ -61,8 +61,18 @@ __device__ void block_colsum(double2* red, int R) {
 __device__ void grid_colsum(const double2* partials, int nblk, int R, double2* red, double2* out) {
   const int tid = threadIdx.x;
   const int r = tid % R, i = tid / R, P = blockDim.x / R;
-  double2 acc = make_double2(0, 0);
-  for (int b = i; b < nblk; b += P) acc = cadd(acc, __ldcg(&partials[(long long)b * R + r]));
+  // four independent accumulators keep four L2 loads in flight per thread
+  // (the partials are read by every CTA at every step); fixed order
+  double2 a0 = make_double2(0, 0), a1 = a0, a2 = a0, a3 = a0;
+  int b = i;
+  for (; b + 3 * P < nblk; b += 4 * P) {
+    a0 = cadd(a0, __ldcg(&partials[(long long)b * R + r]));
+    a1 = cadd(a1, __ldcg(&partials[(long long)(b + P) * R + r]));
+    a2 = cadd(a2, __ldcg(&partials[(long long)(b + 2 * P) * R + r]));
+    a3 = cadd(a3, __ldcg(&partials[(long long)(b + 3 * P) * R + r]));
+  }
+  for (; b < nblk; b += P) a0 = cadd(a0, __ldcg(&partials[(long long)b * R + r]));
+  const double2 acc = cadd(cadd(a0, a1), cadd(a2, a3));
   red[tid] = acc;
   block_colsum(red, R);
   if (tid < R) out[tid] = red[tid];
