@@ -664,3 +664,40 @@ def test_sharded_map_once_per_step(case, world, blocks):
         assert p.exitcode == 0
     for rank, ez, ew in res:
         assert ez < 1e-13 and ew < 1e-13, (rank, ez, ew)
+
+
+def _handles_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2209_10886_b200.interface_system import gather_peer_handles
+        mine = bytes([rank + 1]) * 64
+        allh = gather_peer_handles(mine, rank, world)
+        try:
+            gather_peer_handles(mine, rank, world + 1)
+            bad = False
+        except ValueError:
+            bad = True
+        q.put((rank, allh, bad))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_handle_exchange(world):
+    """The host side of hs_peer_open: the ranks' 64-byte IPC handles are
+    all-gathered in rank order (the layout hs_peer_open reads), and a rank /
+    world mismatch with the process group is refused."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_handles_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = b"".join(bytes([r + 1]) * 64 for r in range(world))
+    for rank, allh, bad in res:
+        assert allh == want and bad, rank
