@@ -1396,8 +1396,18 @@ int do_precond(Ctx* c, int kind, const double2* r, double2* z, int R) {
   if (map_once_steps(c)) {
     // map-once: r' = 0 on the W/S blocks of exact forward writers (no map read);
     // the residual step covers only the rows where r' can be nonzero
-    launch_block_fill(*c, c->mo_zero_blocks, c->n_mo_zero, 0, rp, w, z, zl, R);
+    // (the fill touches other blocks than the residual step: it runs beside it)
+    if (!c->aux) {
+      CK(cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking));
+      CK(cudaEventCreateWithFlags(&c->aux_fork, cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->aux_join, cudaEventDisableTiming));
+    }
+    CK(cudaEventRecord(c->aux_fork, c->stream));
+    CK(cudaStreamWaitEvent(c->aux, c->aux_fork, 0));
+    launch_block_fill(*c, c->mo_zero_blocks, c->n_mo_zero, 0, rp, w, z, zl, R, c->aux);
+    CK(cudaEventRecord(c->aux_join, c->aux));
     if (int e_ = run_step(c, c->mo_resid, zl, zl, epi(EPI_RESID, rp, w, z, r, zl), R)) return e_;
+    CK(cudaStreamWaitEvent(c->stream, c->aux_join, 0));
     rsrc = rp;
   } else if (c->inter) {
     if (int e_ = run_step(c, c->full, zl, zl, epi(EPI_RESID, rp, w, z, r, zl), R)) return e_;
@@ -1589,6 +1599,9 @@ int hs_destroy(hs_ctx* c) {
     if (c->nccl) ncclCommDestroy((ncclComm_t)c->nccl);
     for (auto e : c->bev)
       if (e) cudaEventDestroy(e);
+    if (c->aux_fork) cudaEventDestroy(c->aux_fork);
+    if (c->aux_join) cudaEventDestroy(c->aux_join);
+    if (c->aux) cudaStreamDestroy(c->aux);
     if (c->copy_in) cudaStreamDestroy(c->copy_in);
     if (c->copy_out) cudaStreamDestroy(c->copy_out);
     cudaStreamDestroy(c->stream);

@@ -938,11 +938,11 @@ void launch_vec(Ctx& c, int op, long long len, double2* o1, double2* o2, const d
 }
 
 void launch_block_fill(Ctx& c, const int* blocks, int nb, int mode, double2* o1, double2* o2, double2* o3,
-                       const double2* a, int R) {
+                       const double2* a, int R, cudaStream_t st) {
   if (nb == 0) return;
   long long len = (long long)nb * c.n * R;
   c.launches++;
-  k_block_fill<<<grid_for(len, c.num_sms), 256, 0, c.stream>>>(blocks, nb, mode, o1, o2, o3, a, c.n, R);
+  k_block_fill<<<grid_for(len, c.num_sms), 256, 0, st ? st : c.stream>>>(blocks, nb, mode, o1, o2, o3, a, c.n, R);
 }
 
 void launch_seam_add(Ctx& c, int dir, double2* z, const double2* r, int R) {

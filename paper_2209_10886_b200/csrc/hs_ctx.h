@@ -300,6 +300,8 @@ struct Ctx {
   // device state
   cudaStream_t stream = nullptr;
   cudaStream_t copy_in = nullptr, copy_out = nullptr;  // host-batch pipeline (hs_precond_batch)
+  cudaStream_t aux = nullptr;                           // side work overlapping a step (map-once fills)
+  cudaEvent_t aux_fork = nullptr, aux_join = nullptr;
   cudaEvent_t bev[6] = {};                              // per slot: input landed, applied, output drained
   double2* T = nullptr;
   size_t T_elems = 0;

@@ -26,7 +26,7 @@ void launch_vec(Ctx& c, int op, long long len, double2* o1, double2* o2, const d
                 const double2* b);
 void launch_seam_add(Ctx& c, int dir, double2* z, const double2* r, int R);
 void launch_block_fill(Ctx& c, const int* blocks, int nb, int mode, double2* o1, double2* o2, double2* o3,
-                       const double2* a, int R);
+                       const double2* a, int R, cudaStream_t st = nullptr);
 cudaError_t set_step_smem_limit();
 cudaError_t launch_bsp_fused_ranks(Ctx& c, const DevFused& f, const MultiRankArgs& mr);
 void launch_gather_blocks(Ctx& c, double2* out, const double2* const* src, int G, const int* blk_rank, long long L);
