@@ -218,7 +218,10 @@ def run_reference(args):
         pool.map(_cpu_worker_solves, [1] * procs)
         t0 = time.perf_counter()
         pool.map(_cpu_worker_solves, [1] * procs)
-        per = max(1, int(1.5 / max((time.perf_counter() - t0), 1e-3)))
+        # each step a bounded sample: ~1.5 s, less when many steps are asked for,
+        # so that the whole --steps K --warmup W run stays near two minutes
+        target = max(0.05, min(1.5, 120.0 / max(1, args.steps + args.warmup)))
+        per = max(1, int(target / max((time.perf_counter() - t0), 1e-3)))
         for _ in range(args.warmup):
             pool.map(_cpu_worker_solves, [per] * procs)
         times = []
