@@ -22,6 +22,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import hashlib
+
 import numpy as np
 import scipy.sparse as sp
 from scipy.sparse.linalg import splu
@@ -138,6 +140,17 @@ class Subdomain:
         self.dcells = prob.dirichlet_cells(lat, sub) if dcells is None else np.asarray(dcells, dtype=np.intp)
         self.matrix = helmholtz_matrix(n, n, h, prob.kappa, s / d, self.dcells)
         self.lu = splu(self.matrix.tocsc()) if factor else None
+
+    def factorise(self):
+        self.lu = splu(self.matrix.tocsc())
+
+    def matrix_key(self) -> str:
+        """Digest of the exact CSC arrays handed to splu (shared-factor cache key)."""
+        A = self.matrix.tocsc()
+        h = hashlib.sha256()
+        for arr in (A.data, A.indices, A.indptr, np.asarray(A.shape)):
+            h.update(np.ascontiguousarray(arr).tobytes())
+        return h.hexdigest()
 
     def solve(self, traces=None, source=None):
         """solve_local (discretization.py:264-293); traces: {face index: trace}."""

@@ -27,16 +27,37 @@ DENSE_GUARD = 6000
 
 
 class Interface:
-    def __init__(self, prob: Problem, lat: Lattice, backend: str = "superlu", subs=None):
+    def __init__(self, prob: Problem, lat: Lattice, backend: str = "superlu", subs=None,
+                 share_factors: bool = False):
         """`subs` optionally restricts which subdomains are factorised (spot checks
-        at configs too large to factor every subdomain)."""
+        at configs too large to factor every subdomain).  `share_factors` gives
+        every subdomain whose matrix is bitwise identical to an earlier one that
+        one's SuperLU object: `_assemble_grid` uses one ghost ratio on all four
+        faces (discretization.py:224-229), so only the generic and the scatterer
+        operator exist, and each solve is bit-for-bit the unshared one (SuperLU
+        is deterministic; solves are read-only on the factor,
+        discretization.py:119-123).  cfg5 then holds 2 factors instead of 512."""
         self.prob, self.lat, self.n = prob, lat, prob.n
         self.size = lat.n_pairs * prob.n
         self.backend = backend
         todo = lat.subs if subs is None else [tuple(s) for s in subs]
         self.home = prob.home(lat)
         if backend == "superlu":
-            self.ops = {s: Subdomain(prob, lat, s) for s in todo}
+            if share_factors:
+                cache = {}
+                self.ops = {}
+                for s in todo:
+                    op = Subdomain(prob, lat, s, factor=False)
+                    key = op.matrix_key()
+                    if key not in cache:
+                        op.factorise()
+                        cache[key] = op.lu
+                    op.lu = cache[key]
+                    self.ops[s] = op
+                self.n_factors = len(cache)
+            else:
+                self.ops = {s: Subdomain(prob, lat, s) for s in todo}
+                self.n_factors = len(self.ops)
         elif backend == "schur":
             from .schur import schur_maps_for
             self.T = schur_maps_for(prob, lat, todo)

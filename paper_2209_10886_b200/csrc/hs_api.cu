@@ -66,6 +66,24 @@ int fail(Ctx* c, int code, const std::string& msg) {
     if ((c)->device < 0) return fail(c, 2, "plan-only context (device -1) cannot run kernels"); \
   } while (0)
 
+// Every entry point that can touch the GPU runs on the context's device and
+// restores the caller's current device on return: two contexts on two GPUs in
+// one process, or a torch.cuda.set_device between calls, must not launch into
+// another device's streams or allocate the workspace on the wrong GPU.
+struct DeviceScope {
+  int prev = -1;
+  bool restore = false;
+  explicit DeviceScope(const Ctx* c) {
+    if (!c || c->device < 0) return;
+    if (cudaGetDevice(&prev) == cudaSuccess && prev != c->device)
+      restore = cudaSetDevice(c->device) == cudaSuccess;
+  }
+  ~DeviceScope() {
+    if (restore) cudaSetDevice(prev);
+  }
+};
+#define DEV_SCOPE(c) DeviceScope dev_scope_(c)
+
 // Device allocations of a context are tracked by pointer so hs_memory is exact
 // whatever the caller passes as size to dfree.
 cudaError_t dalloc(Ctx* c, void** p, size_t bytes) {
@@ -1406,8 +1424,11 @@ int do_precond(Ctx* c, int kind, const double2* r, double2* z, int R) {
     CK(cudaStreamWaitEvent(c->aux, c->aux_fork, 0));
     launch_block_fill(*c, c->mo_zero_blocks, c->n_mo_zero, 0, rp, w, z, zl, R, c->aux);
     CK(cudaEventRecord(c->aux_join, c->aux));
-    if (int e_ = run_step(c, c->mo_resid, zl, zl, epi(EPI_RESID, rp, w, z, r, zl), R)) return e_;
+    const int e_res = run_step(c, c->mo_resid, zl, zl, epi(EPI_RESID, rp, w, z, r, zl), R);
+    // join the side stream on every path: the fill may still be writing rp/w/z
+    // when a failed residual step returns, and the caller may then reuse them
     CK(cudaStreamWaitEvent(c->stream, c->aux_join, 0));
+    if (e_res) return e_res;
     rsrc = rp;
   } else if (c->inter) {
     if (int e_ = run_step(c, c->full, zl, zl, epi(EPI_RESID, rp, w, z, r, zl), R)) return e_;
@@ -1527,6 +1548,14 @@ int hs_create(hs_ctx** out, int device, int n1, int n2, int n, double h, double 
   x->device = device;
   x->n1 = n1; x->n2 = n2; x->n = n;
   x->h = h; x->kappa = kappa; x->tau_re = tau_re; x->tau_im = tau_im;
+  int prev_dev = -1;
+  if (device >= 0 && cudaGetDevice(&prev_dev) != cudaSuccess) prev_dev = -1;
+  struct Restore {  // the caller's current device is left as it was
+    int d;
+    ~Restore() {
+      if (d >= 0) cudaSetDevice(d);
+    }
+  } restore_dev{prev_dev};
   if (device >= 0) {
     c = x;
     cudaError_t ce = cudaSetDevice(device);
@@ -1576,6 +1605,7 @@ int hs_create(hs_ctx** out, int device, int n1, int n2, int n, double h, double 
 
 int hs_destroy(hs_ctx* c) {
   if (!c) return 0;
+  DEV_SCOPE(c);
   if (c->device >= 0) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
@@ -1674,6 +1704,7 @@ int assign_map_offsets(Ctx* c, std::vector<int>& rep) {
 
 int hs_factor(hs_ctx* c) {
   if (!c) return fail(nullptr, 1, "null context");
+  DEV_SCOPE(c);
   NEED_GPU(c);
   CK(cudaSetDevice(c->device));
   const int n = c->n;
@@ -1799,6 +1830,7 @@ int hs_factor(hs_ctx* c) {
 
 int hs_lifting_rhs(hs_ctx* c, const double* vals, int nrhs, double* bout, int mem) {
   if (!c) return fail(nullptr, 1, "null context");
+  DEV_SCOPE(c);
   if (int e = check_ready(c, nrhs)) return e;
   CK(cudaSetDevice(c->device));
   const int n = c->n;
@@ -1862,6 +1894,7 @@ int hs_lifting_rhs(hs_ctx* c, const double* vals, int nrhs, double* bout, int me
 
 int hs_reconstruct(hs_ctx* c, const double* g, const double* lift_vals, double* field, int mem) {
   if (!c) return fail(nullptr, 1, "null context");
+  DEV_SCOPE(c);
   if (int e = check_ready(c, 1)) return e;
   const int n = c->n;
   const long long L = c->plan.L;
@@ -1946,6 +1979,7 @@ int hs_reconstruct(hs_ctx* c, const double* g, const double* lift_vals, double* 
 
 int hs_apply(hs_ctx* c, int mode, const double* g, double* out, int nrhs, int mem) {
   if (!c) return fail(nullptr, 1, "null context");
+  DEV_SCOPE(c);
   if (int e = check_ready(c, nrhs)) return e;
   const long long LR = LRof(c, nrhs);
   const double2* dg;
@@ -1959,6 +1993,7 @@ int hs_apply(hs_ctx* c, int mode, const double* g, double* out, int nrhs, int me
 int hs_restricted_apply(hs_ctx* c, const double* g, double* out, int nrhs, const int32_t* src,
                         int nsrc, const int32_t* tgt, int ntgt, int mem) {
   if (!c) return fail(nullptr, 1, "null context");
+  DEV_SCOPE(c);
   if (int e = check_ready(c, nrhs)) return e;
   const long long LR = LRof(c, nrhs);
   const double2* dg;
@@ -1978,6 +2013,7 @@ int hs_restricted_apply(hs_ctx* c, const double* g, double* out, int nrhs, const
 
 int hs_set_windows(hs_ctx* c, int kind, const int32_t* lo, const int32_t* hi, int nwin) {
   if (!c) return fail(nullptr, 1, "null context");
+  DEV_SCOPE(c);
   if (kind != 0 && kind != 1) return fail(c, 1, "window kind must be 0 (lower) or 1 (upper)");
   std::vector<std::pair<int, int>> w;
   const int ng = c->plan.ng;
@@ -1992,6 +2028,7 @@ int hs_set_windows(hs_ctx* c, int kind, const int32_t* lo, const int32_t* hi, in
 
 int hs_set_precond_options(hs_ctx* c, int seam_mode, int inter) {
   if (!c) return fail(nullptr, 1, "null context");
+  DEV_SCOPE(c);
   if (seam_mode != HS_SEAM_DEDUP && seam_mode != HS_SEAM_LITERAL) return fail(c, 1, "bad seam mode");
   c->seam = seam_mode;
   c->inter = inter ? 1 : 0;
@@ -2000,6 +2037,7 @@ int hs_set_precond_options(hs_ctx* c, int seam_mode, int inter) {
 
 int hs_precond(hs_ctx* c, int kind, const double* r, double* z, int nrhs, int mem) {
   if (!c) return fail(nullptr, 1, "null context");
+  DEV_SCOPE(c);
   if (int e = check_ready(c, nrhs)) return e;
   const long long LR = LRof(c, nrhs);
   const double2* dr;
@@ -2017,6 +2055,7 @@ int hs_precond(hs_ctx* c, int kind, const double* r, double* z, int nrhs, int me
 // trip host -> HBM -> host.
 int hs_precond_batch(hs_ctx* c, int kind, const double* const* r, double* const* z, int nvec, int nrhs) {
   if (!c) return fail(nullptr, 1, "null context");
+  DEV_SCOPE(c);
   if (nvec < 0 || (nvec > 0 && (!r || !z))) return fail(c, 1, "bad batch");
   if (int e = check_ready(c, nrhs)) return e;
   if (nvec == 0) return 0;
@@ -2041,7 +2080,13 @@ int hs_precond_batch(hs_ctx* c, int kind, const double* const* r, double* const*
     CK(cudaEventRecord(landed[s], c->copy_in));
     CK(cudaStreamWaitEvent(c->stream, landed[s], 0));
     if (i >= 2) CK(cudaStreamWaitEvent(c->stream, drained[s], 0));
-    if (int e_ = do_precond(c, kind, din[s], dout[s], nrhs)) return e_;
+    if (int e_ = do_precond(c, kind, din[s], dout[s], nrhs)) {
+      // no copy may still be in flight into the caller's buffers or the slots
+      cudaStreamSynchronize(c->copy_in);
+      cudaStreamSynchronize(c->copy_out);
+      cudaStreamSynchronize(c->stream);
+      return e_;
+    }
     CK(cudaEventRecord(applied[s], c->stream));
     CK(cudaStreamWaitEvent(c->copy_out, applied[s], 0));
     CK(cudaMemcpyAsync(z[i], dout[s], bytes, cudaMemcpyDeviceToHost, c->copy_out));
@@ -2054,6 +2099,7 @@ int hs_precond_batch(hs_ctx* c, int kind, const double* const* r, double* const*
 
 int hs_half_apply(hs_ctx* c, int direction, const double* r, double* z, int nrhs, int mem) {
   if (!c) return fail(nullptr, 1, "null context");
+  DEV_SCOPE(c);
   if (direction != 0 && direction != 1) return fail(c, 1, "direction must be 0 or 1");
   if (int e = check_ready(c, nrhs)) return e;
   const long long LR = LRof(c, nrhs);
@@ -2068,10 +2114,10 @@ int hs_half_apply(hs_ctx* c, int direction, const double* r, double* z, int nrhs
 int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, int maxit,
              int* iters, double* hist, int* converged, int mem) {
   if (!c) return fail(nullptr, 1, "null context");
+  DEV_SCOPE(c);
   if (int e = check_ready(c, R)) return e;
   if (!(tol > 0) || maxit < 1) return fail(c, 1, "tol must be > 0 and maxit >= 1");
   if (pc < HS_PC_NONE || pc > HS_PC_BSP) return fail(c, 1, "unknown preconditioner kind");
-  if (R & (R - 1)) return fail(c, 1, "batched GMRES needs nrhs a power of two");
   // Arnoldi: one cooperative kernel per iteration on one GPU; across row bands
   // (or when forced) the host-driven MGS over owned blocks + allreduce per dot
   // Row bands, one RHS, auto mode: CGS2 -- two all-reduces per iteration
@@ -2338,6 +2384,7 @@ int hs_exchange_plan(const hs_ctx* cc, int kind, int peer, int recv, int32_t* bl
 
 int hs_get_schur(hs_ctx* c, int i1, int i2, double* T) {
   if (!c) return fail(nullptr, 1, "null context");
+  DEV_SCOPE(c);
   NEED_GPU(c);
   if (!c->factored || (!c->T && !c->Tcls)) return fail(c, 1, "no maps (call hs_factor)");
   if (i1 < 1 || i1 > c->n1 || i2 < 1 || i2 > c->n2) return fail(c, 1, "subdomain out of range");
@@ -2372,6 +2419,7 @@ int hs_get_schur(hs_ctx* c, int i1, int i2, double* T) {
 
 int hs_set_schur(hs_ctx* c, int i1, int i2, const double* T) {
   if (!c) return fail(nullptr, 1, "null context");
+  DEV_SCOPE(c);
   NEED_GPU(c);
   if (i1 < 1 || i1 > c->n1 || i2 < 1 || i2 > c->n2) return fail(c, 1, "subdomain out of range");
   if (!c->T) CK(dalloc(c, (void**)&c->T, c->T_elems * sizeof(double2)));
@@ -2393,12 +2441,14 @@ int hs_set_schur(hs_ctx* c, int i1, int i2, const double* T) {
 
 int hs_set_async(hs_ctx* c, int a) {
   if (!c) return 1;
+  DEV_SCOPE(c);
   c->async_mode = a ? 1 : 0;
   return 0;
 }
 
 int hs_sync(hs_ctx* c) {
   if (!c) return 1;
+  DEV_SCOPE(c);
   NEED_GPU(c);
   CK(cudaStreamSynchronize(c->stream));
   return 0;
@@ -2413,6 +2463,7 @@ int hs_stream(hs_ctx* c, uint64_t* s) {
 
 int hs_set_fused(hs_ctx* c, int mask) {
   if (!c) return fail(nullptr, 1, "null context");
+  DEV_SCOPE(c);
   if (mask < 0 || mask > 7) return fail(c, 1, "fused mask must be 0..7");
   if ((mask ^ c->fused_mode) & 4) {  // plan kind changed: rebuild the fused plans
     free_fused(c);
@@ -2425,6 +2476,7 @@ int hs_set_fused(hs_ctx* c, int mask) {
 
 int hs_set_trace(hs_ctx* c, int on) {
   if (!c) return fail(nullptr, 1, "null context");
+  DEV_SCOPE(c);
   if (c->device < 0) return fail(c, 1, "plan-only context");
   c->trace_on = on != 0;
   if (c->trace_on && !c->trace) {
@@ -2439,6 +2491,7 @@ int hs_set_trace(hs_ctx* c, int on) {
 
 int hs_get_trace(hs_ctx* c, uint64_t* out, int cap, int* rows) {
   if (!c || !rows) return fail(c, 1, "null argument");
+  DEV_SCOPE(c);
   *rows = c->trace_rows;
   if (!out || c->trace_rows == 0) return 0;
   if (cap < c->trace_rows) return fail(c, 1, "trace buffer too small");
@@ -2449,6 +2502,7 @@ int hs_get_trace(hs_ctx* c, uint64_t* out, int cap, int* rows) {
 
 int hs_peer_export(hs_ctx* c, uint8_t handle[64]) {
   if (!c || !handle) return fail(c, 1, "null argument");
+  DEV_SCOPE(c);
   NEED_GPU(c);
   PeerRanks& p = c->peer;
   const size_t L = (size_t)c->plan.L;
@@ -2471,6 +2525,7 @@ int hs_peer_export(hs_ctx* c, uint8_t handle[64]) {
 
 int hs_peer_open(hs_ctx* c, const uint8_t* handles, int nranks) {
   if (!c || !handles) return fail(c, 1, "null argument");
+  DEV_SCOPE(c);
   NEED_GPU(c);
   PeerRanks& p = c->peer;
   if (nranks != c->plan.nranks) return fail(c, 1, "peer handles: nranks differs from the context's");
@@ -2571,6 +2626,7 @@ int hs_fused_plan(const hs_ctx* cc, int ims, int rank, int32_t* out, int cap, in
 
 int hs_set_emulated_ranks(hs_ctx* c, int ranks) {
   if (!c) return fail(nullptr, 1, "null context");
+  DEV_SCOPE(c);
   if (ranks < 1 || ranks > kMaxRanks || ranks > c->n2)
     return fail(c, 1, "emulated ranks must be in 1..min(8, N2)");
   if (c->plan.nranks != 1) return fail(c, 1, "emulated ranks need a single-rank context");
@@ -2581,6 +2637,7 @@ int hs_set_emulated_ranks(hs_ctx* c, int ranks) {
 
 int hs_set_gmres_mode(hs_ctx* c, int mode) {
   if (!c) return fail(nullptr, 1, "null context");
+  DEV_SCOPE(c);
   if (mode < 0 || mode > 3)
     return fail(c, 1, "gmres mode must be 0 (auto), 1 (host-driven MGS), 2 (grid-wide MGS) or 3 (CGS2)");
   c->gmres_mode = mode;
@@ -2589,6 +2646,7 @@ int hs_set_gmres_mode(hs_ctx* c, int mode) {
 
 int hs_set_map_mode(hs_ctx* c, int mode) {
   if (!c) return fail(nullptr, 1, "null context");
+  DEV_SCOPE(c);
   if (mode < 0 || mode > 2)
     return fail(c, 1, "map mode must be 0 (per subdomain), 1 (shared class maps, DMMA) or 2 (per kind, aliased)");
   if (mode != c->map_mode) {
@@ -2601,12 +2659,14 @@ int hs_set_map_mode(hs_ctx* c, int mode) {
 
 int hs_set_kernel_timing(hs_ctx* c, int on) {
   if (!c) return 1;
+  DEV_SCOPE(c);
   c->timing = on != 0;
   return 0;
 }
 
 int hs_kernel_stats(hs_ctx* c, int64_t* launches, double* ms, double* bytes, double* flops, int reset) {
   if (!c) return 1;
+  DEV_SCOPE(c);
   NEED_GPU(c);
   CK(cudaStreamSynchronize(c->stream));
   for (size_t i = 0; i < c->ev_pending.size(); ++i) {
@@ -2653,6 +2713,7 @@ int hs_nccl_unique_id(uint8_t id[128]) {
 
 int hs_comm_init(hs_ctx* c, const uint8_t id[128]) {
   if (!c) return fail(nullptr, 1, "null context");
+  DEV_SCOPE(c);
   NEED_GPU(c);
   CK(cudaSetDevice(c->device));
   ncclUniqueId u;

@@ -16,6 +16,7 @@ right-hand sides; results come back as the same kind.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import time
 from dataclasses import dataclass, field
@@ -267,6 +268,19 @@ class GpuInterfaceSystem:
             raise ValueError(f"bsp_seam must be 'dedup' or 'literal', got {sweep.bsp_seam!r}")
         self.ctx.call("hs_set_precond_options", seam, int(bool(sweep.bsp_intermediate_residual)))
         self.sweep = sweep
+
+    @contextlib.contextmanager
+    def using(self, sweep: SweepConfig):
+        """Run a block under another SweepConfig and restore the previous one."""
+        prev = self.sweep
+        if sweep == prev:
+            yield self
+            return
+        self.configure(sweep)
+        try:
+            yield self
+        finally:
+            self.configure(prev)
 
     def _call_io(self, fn, g, pre=(), post=()):
         v = _Vec(self.layout.check(g), self.layout.size)

@@ -43,4 +43,8 @@ def gmres(apply_A, apply_M, b, opts: GmresOptions | None = None) -> GmresResult:
     kind = _kind_of(apply_M, system)
     if kind is None:
         raise TypeError("gmres: apply_M must be None or a preconditioner of the same GpuInterfaceSystem")
-    return system.gmres(b, kind=kind, tol=opts.tol, maxit=opts.maxit)
+    sweep = getattr(apply_M, "sweep", None) if getattr(apply_M, "owner", None) is system else None
+    if sweep is None:
+        return system.gmres(b, kind=kind, tol=opts.tol, maxit=opts.maxit)
+    with system.using(sweep):  # the preconditioner's own windows / seams
+        return system.gmres(b, kind=kind, tol=opts.tol, maxit=opts.maxit)

@@ -27,10 +27,12 @@ def bsp_apply(system: GpuInterfaceSystem, b):
 
 
 def step_schedule(config: SweepConfig, system: GpuInterfaceSystem):
+    """Schedule of `config`; the system's own configuration
+    is restored afterwards."""
     if config.kind == "none":
         return []
-    system.configure(config)
-    return system.step_schedule(config.kind)
+    with system.using(config):
+        return system.step_schedule(config.kind)
 
 
 def steps_per_apply(config: SweepConfig, system: GpuInterfaceSystem) -> int:
@@ -44,14 +46,19 @@ def format_trace(records) -> str:
 
 
 def make_preconditioner(system: GpuInterfaceSystem, config: SweepConfig):
-    """apply_M for krylov.gmres; carries its system and kind for the device fast path."""
-    system.configure(config)
+    """apply_M for krylov.gmres; carries its system, kind and configuration
+    for the device fast path.  Each call runs under the preconditioner's own
+    configuration (the system's current one is restored afterwards), so
+    preconditioners built for different configurations coexist."""
+    config = SweepConfig(**vars(config))  # a snapshot: later edits of the caller's object do not leak in
 
     class _M:
         kind = config.kind
         owner = system
+        sweep = config
 
         def __call__(self, r):
-            return system.precondition(r, config.kind)
+            with system.using(config):
+                return system.precondition(r, config.kind)
 
     return _M()

@@ -1,6 +1,9 @@
 """Generate golden fixtures from the REAL reference package (build container only).
 
     PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py [--cfg3]
+    python tests/golden/make_golden.py --check-cfg3   # shared-factor harness == cfg3 golden, bitwise
+    python tests/golden/make_golden.py --cfg2-sweep   # cfg2 block counts p = 1, 2, 4, 8
+    python tests/golden/make_golden.py --cfg5         # headline config, ~1 h on 8 cores
 
 Writes tests/golden/*.npz.  What is pinned:
   * lattice.npz   : m-order pair tables and reference windows for several lattices
@@ -14,6 +17,9 @@ Writes tests/golden/*.npz.  What is pinned:
                     application is the reference's InterfaceSystem.restricted_apply
                     / apply_interface_operator (SPEC.md:306-424);
   * mono_*.npz    : mono_solve fields (discretization.py:335-370).
+  * cfg5.npz / cfg2 sweep / cfg3 check: the same reference arithmetic run by
+    `refpar` (shared bitwise-identical SuperLU factors + forked workers calling
+    the reference's own `_scatter_one`); see tests/golden/refpar.py.
 The reference package is never imported by the product, the GPU tests or bench.
 """
 
@@ -148,11 +154,137 @@ def apply_fixture(name, c, dense=False, mono=False, gm=True, seeds=(1, 2)):
     print(f"{name}: L={L} done in {time.time() - t0:.1f}s")
 
 
+def par_system(c, workers):
+    """Reference system with shared factors, driven by forked workers (refpar)."""
+    from refpar import ParAdapter, shared_splu
+    t0 = time.time()
+    with shared_splu(ref_disc) as st:
+        spec, part, sysr = ref_system(c)
+    print(f"{c['name']}: reference system built in {time.time() - t0:.1f}s "
+          f"({st['factor']} SuperLU factorisations, {st['reuse']} reused)", flush=True)
+    return spec, part, sysr, ParAdapter(sysr, Lattice(c["n1"], c["n2"]), workers)
+
+
+def _gmres_record(adap, b, blocks, tol, out, suffix=""):
+    pc = Preconditioner(adap, "bsp", blocks=blocks)
+    t1 = time.time()
+    res = gmres(adap.apply_A, pc, b, tol=tol, maxit=1000)
+    out[f"gm_x{suffix}"] = res.x
+    out[f"gm_iters{suffix}"] = res.iterations
+    out[f"gm_hist{suffix}"] = np.array(res.history)
+    out[f"gm_time{suffix}"] = time.time() - t1
+    print(f"  gmres{suffix}: {res.iterations} it, converged {res.converged}, {time.time() - t1:.1f}s", flush=True)
+    return res
+
+
+def check_cfg3(workers):
+    """The shared-factor, process-parallel harness reproduces the committed cfg3
+    golden (one SuperLU factor per subdomain, serial reference loop) bit for bit."""
+    import json
+    G = np.load(os.path.join(HERE, "cfg3.npz"))
+    c = CONFIGS[3]
+    spec, part, sysr, adap = par_system(c, workers)
+    L = sysr.layout.size
+    out = {}
+    out["b"] = sysr.assemble_rhs(sysr.compute_liftings())
+    out["Ag"] = adap.apply_A(rng_vec(int(G["seed_g"]), L))
+    out["M_bsp4"] = Preconditioner(adap, "bsp", blocks=4)(rng_vec(int(G["seed_r"]), L))
+    _gmres_record(adap, out["b"], 4, 1e-6, out)
+    adap.close()
+    rep = {}
+    for k in ("b", "Ag", "M_bsp4", "gm_x", "gm_hist"):
+        a, g = np.asarray(out[k]), np.asarray(G[k])
+        rep[k] = {"bitwise_equal": bool(a.shape == g.shape and np.array_equal(a, g)),
+                  "max_abs_diff": float(np.abs(a - g).max()) if a.shape == g.shape else None}
+    rep["gm_iters"] = {"golden": int(G["gm_iters"]), "shared": int(out["gm_iters"])}
+    rep["workers"] = adap.workers
+    rep["gmres_s"] = float(out["gm_time"])
+    print(json.dumps(rep, indent=1))
+    with open(os.path.join(HERE, "cfg3_shared_check.json"), "w") as f:
+        json.dump(rep, f, indent=1)
+        f.write("\n")
+    assert all(v["bitwise_equal"] for k, v in rep.items() if isinstance(v, dict) and "bitwise_equal" in v)
+    assert rep["gm_iters"]["golden"] == rep["gm_iters"]["shared"]
+
+
+def cfg2_sweep(workers):
+    """cfg2 block counts p = 1, 2, 4, 8 through the reference's restricted_apply
+    (windows: SURVEY.md §8d rules (i)-(iii)); keys added to cfg2.npz."""
+    G = dict(np.load(os.path.join(HERE, "cfg2.npz")))
+    c = CONFIGS[2]
+    spec, part, sysr, adap = par_system(c, workers)
+    r = G["r"]
+    b = G["b"]
+    for p in (1, 2, 4, 8):
+        z = Preconditioner(adap, "bsp", blocks=p)(r)
+        G[f"M_bsp_p{p}"] = z
+        out = {}
+        _gmres_record(adap, b, p, 1e-6, out, suffix=f"_p{p}")
+        G.update(out)
+    adap.close()
+    assert np.array_equal(G["M_bsp_p1"], G["M_bsp1"]) and np.array_equal(G["M_bsp_p2"], G["M_bsp"])
+    np.savez_compressed(os.path.join(HERE, "cfg2.npz"), **G)
+
+
+def cfg5_fixture(workers):
+    """Headline config: b, seeded (I-S) g and BSP z, and the full GMRES run in
+    the reference arithmetic; plus the accurate (Dirichlet-eliminated Schur map)
+    oracle's solution, stored as its complex64 difference from the reference x."""
+    from oracle import Interface
+    c = CONFIGS[5]
+    t0 = time.time()
+    spec, part, sysr, adap = par_system(c, workers)
+    L = sysr.layout.size
+    out = {"L": L, "seed_g": 1, "seed_r": 2}
+    out["b"] = sysr.assemble_rhs(sysr.compute_liftings())
+    t1 = time.time()
+    out["Ag"] = adap.apply_A(rng_vec(1, L))
+    out["t_Ag"] = time.time() - t1
+    t1 = time.time()
+    out["M_bsp8"] = Preconditioner(adap, "bsp", blocks=8)(rng_vec(2, L))
+    out["t_bsp"] = time.time() - t1
+    print(f"cfg5: applies done ({out['t_Ag']:.1f}s, {out['t_bsp']:.1f}s)", flush=True)
+    np.savez(os.path.join(HERE, "cfg5_partial.npz"), **out)
+    _gmres_record(adap, out["b"], 8, 1e-6, out)
+    adap.close()
+    prob, lat = oracle_from(c)
+    itf = Interface(prob, lat, backend="schur")
+    acc = gmres(itf.apply_A, Preconditioner(itf, "bsp", blocks=8), out["b"], tol=1e-6, maxit=1000)
+    out["acc_iters"] = acc.iterations
+    out["acc_dx"] = (acc.x - out["gm_x"]).astype(np.complex64)
+    out["workers"] = adap.workers
+    np.savez_compressed(os.path.join(HERE, "cfg5.npz"), **out)
+    os.remove(os.path.join(HERE, "cfg5_partial.npz"))
+    print(f"cfg5: done in {time.time() - t0:.1f}s; accurate oracle {acc.iterations} it", flush=True)
+
+
+def oracle_from(c):
+    from oracle import Problem
+    ang = c["angle"] if c["angle"] is not None else 0.0
+    prob = Problem(kappa=c["kappa"], n=c["n"], side=c["side"],
+                   center=None if c["center"] is None else tuple(c["center"]), radius=c["radius"],
+                   direction=(float(np.cos(ang)), float(np.sin(ang))))
+    return prob, Lattice(c["n1"], c["n2"])
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg3", action="store_true", help="also run config 3 (about 8 minutes)")
+    ap.add_argument("--check-cfg3", action="store_true")
+    ap.add_argument("--cfg2-sweep", action="store_true")
+    ap.add_argument("--cfg5", action="store_true")
+    ap.add_argument("--workers", type=int, default=None)
     ap.add_argument("--only", default=None)
     a = ap.parse_args()
+    if a.check_cfg3 or a.cfg2_sweep or a.cfg5:
+        sys.path.insert(0, HERE)
+        if a.check_cfg3:
+            check_cfg3(a.workers)
+        if a.cfg2_sweep:
+            cfg2_sweep(a.workers)
+        if a.cfg5:
+            cfg5_fixture(a.workers)
+        return
     if a.only in (None, "lattice"):
         lattice_fixture()
     jobs = [

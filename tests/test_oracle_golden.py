@@ -149,3 +149,35 @@ def test_subdomain_matrix_is_reference_matrix():
     D[op.dcells] = True
     S = A - A.T
     assert np.abs(S[~D][:, ~D]).max() == 0.0
+
+
+def test_shared_factor_parallel_oracle_bitwise_cfg2_sweep():
+    """The CPU baseline's machinery (oracle.parallel over Interface(share_factors=
+    True): 2 SuperLU factors, forked workers) reproduces the reference's cfg2
+    block-sweep goldens bit for bit (make_golden.py --cfg2-sweep)."""
+    from oracle.parallel import ParInterface
+    G = golden("cfg2")
+    if "M_bsp_p8" not in G.files:
+        pytest.skip("cfg2 golden without the block sweep")
+    prob, lat = oracle_problem(CONFIGS[2])
+    I = Interface(prob, lat, share_factors=True)
+    assert I.n_factors == 2
+    with ParInterface(I, 2) as P:
+        for p in (4, 8):
+            assert np.array_equal(Preconditioner(P, "bsp", blocks=p)(G["r"]), G[f"M_bsp_p{p}"]), p
+        assert np.array_equal(P.apply_A(G["g"]), G["Ag"])
+        assert np.array_equal(P.restricted(G["g"], {5}, {6}), G["R_5_6"])
+
+
+def test_cfg3_shared_factor_record():
+    """Record of make_golden.py --check-cfg3: the shared-factor, process-parallel
+    reference harness reproduced the cfg3 golden (one factor per subdomain,
+    serial loop) bit for bit -- the premise of the cfg5 golden."""
+    import json
+    import os
+    from conftest import GOLDEN
+    with open(os.path.join(GOLDEN, "cfg3_shared_check.json")) as f:
+        rep = json.load(f)
+    for k in ("b", "Ag", "M_bsp4", "gm_x", "gm_hist"):
+        assert rep[k]["bitwise_equal"] and rep[k]["max_abs_diff"] == 0.0, k
+    assert rep["gm_iters"]["golden"] == rep["gm_iters"]["shared"] == 67
