@@ -16,9 +16,12 @@ step-apply, timed per launch with CUDA events), GMRES time-to-solution, the
 CPU baseline (the oracle port of the reference path on the host cores) and
 the SM clocks seen during the timed region.
 
-`--impl reference` times the reference algorithm on the host cores instead
-(oracle port: SciPy SuperLU subdomain solves, all cores via a process pool),
-as a bounded sample per step projected to applies/s.
+`--impl reference` times the reference algorithm on the host cores instead:
+real BSP applies through the reference loop (oracle restatement, bitwise the
+reference; SuperLU solves with the 2 distinct factors shared, every S
+application's subdomain solves on all host cores via forked processes), each
+step a bounded sample, plus the projected GMRES time-to-solution.  That arm
+imports no product code.
 Under torchrun with N > 1 the subdomain rows are sharded over the ranks
 (strong scaling: the apply is split; traces cross band edges over NCCL).
 """
@@ -135,37 +138,17 @@ class Clocks:
                 "samples": len(sm)}
 
 
-# ---------------------------------------------------------------- CPU baseline (oracle port)
-def _cpu_worker_init(cfgno):
-    """Factor one interior subdomain with the reference arithmetic; BLAS pinned
-    to one thread (SuperLU's supernodal updates call BLAS: one core per worker,
-    no oversubscription, and an honest core count)."""
-    global _W, _LIMIT
-    from threadpoolctl import threadpool_limits
-    _LIMIT = threadpool_limits(1)
-    from paper_2209_10886_b200.configs import CONFIGS
-    from oracle.fd import Problem, Subdomain
-    from oracle.lattice import Lattice
-    c = CONFIGS[cfgno]
-    prob = Problem(kappa=c["kappa"], n=c["n"], side=c["side"], center=tuple(c["center"]), radius=c["radius"])
-    lat = Lattice(c["n1"], c["n2"])
-    home = prob.home(lat)
-    interior = [s for s in lat.subs if len(lat.faces[s]) == 4 and s != home]
-    sub = interior[len(interior) // 2] if interior else next(s for s in lat.subs if s != home)
-    op = Subdomain(prob, lat, sub)
-    rng = np.random.default_rng(0)
-    tr = {f: rng.standard_normal(c["n"]) + 1j * rng.standard_normal(c["n"]) for f in op.iface}
-    _W = (op, tr)
-
-
-def _cpu_worker_solves(nsolves):
-    op, tr = _W
-    t0 = time.perf_counter()
-    for _ in range(nsolves):
-        u = op.solve(tr)
-        for f in op.iface:
-            op.outgoing(u, tr[f], f)
-    return nsolves, time.perf_counter() - t0
+# ---------------------------------------------------------------- CPU baseline / reference arm
+def load_configs():
+    """The BASELINE config table, loaded from its file WITHOUT importing the
+    product package (configs.py is plain data; importing
+    paper_2209_10886_b200.indexing would map libhsb200.so into the reference
+    arm's process)."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_hs_configs", os.path.join(ROOT, "paper_2209_10886_b200", "configs.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
 
 
 def host_info():
@@ -180,70 +163,153 @@ def host_info():
     except OSError:
         pass
     return {"cpu_model": model, "cpu_count": os.cpu_count(),
-            "note": "the reference's thread pool gives no speed-up (SURVEY.md §2a): parallel runs use processes"}
+            "note": "the reference's thread pool gives no speed-up (SURVEY.md §2a): the subdomain solves of "
+                    "each S application run in forked processes, one BLAS thread each"}
 
 
-def cpu_baseline(cfgno, n_solves_apply, budget_s=20.0):
-    """Single-core sample of the reference arithmetic (SuperLU solve + outgoing
-    traces of one interior subdomain), projected to one BSP apply."""
-    t0 = time.perf_counter()
-    _cpu_worker_init(cfgno)
-    t_fac = time.perf_counter() - t0
-    n, dt = _cpu_worker_solves(1)
-    k = max(1, int(budget_s / max(dt, 1e-4)) - 1)
-    k = min(k, 400)
-    n2, dt2 = _cpu_worker_solves(k)
-    t_solve = dt2 / n2
-    return {"value": 1.0 / (n_solves_apply * t_solve), "unit": "applies/s", "cores": 1, "kind": "port",
-            "sample": f"{n2} SuperLU solves + outgoing traces of one interior subdomain "
-                      f"({t_solve * 1e3:.2f} ms each; factor {t_fac:.2f} s), projected to one BSP apply = "
-                      f"{n_solves_apply} subdomain solves",
-            "t_solve_s": t_solve, "host": host_info()}
+def reference_iterations(cfgno):
+    """GMRES iterations of the reference arithmetic on this config, from its golden
+    run (tests/golden/cfg*.npz; config 4 = config 2's geometry, per angle)."""
+    name = {4: "cfg2"}.get(cfgno, f"cfg{cfgno}")
+    p = os.path.join(ROOT, "tests", "golden", f"{name}.npz")
+    if not os.path.exists(p):
+        return None, None
+    with np.load(p) as G:
+        if "gm_iters" not in G.files:
+            return None, None
+        return int(G["gm_iters"]), (float(G["gm_time"]) if "gm_time" in G.files else None)
+
+
+class ReferenceCPU:
+    """The reference's arithmetic on the host cores: the oracle's SuperLU back
+    end (bitwise the reference's _scatter_one, tests/test_oracle_golden.py) with
+    its 2 distinct factors shared (discretization.py:224-229), the BSP apply of
+    the SPEC restatement (oracle/sweeps.py) over the reference loop
+    restricted_apply / apply_interface_operator (interface_system.py:135-162:
+    gather, zero-skip, solve, outgoing traces, scatter), every subdomain solve
+    of an S application spread over `workers` forked processes
+    (oracle/parallel.py).  No product code is imported."""
+
+    def __init__(self, cfgno, workers=None):
+        from oracle import Interface, Lattice, Preconditioner, Problem
+        from oracle.parallel import ParInterface
+        c = load_configs().CONFIGS[cfgno]
+        self.c = c
+        ang = c["angle"] if c["angle"] is not None else 0.0
+        prob = Problem(kappa=c["kappa"], n=c["n"], side=c["side"], center=tuple(c["center"]), radius=c["radius"],
+                       direction=(float(np.cos(ang)), float(np.sin(ang))))
+        t0 = time.perf_counter()
+        self.itf = Interface(prob, Lattice(c["n1"], c["n2"]), share_factors=True)
+        self.setup_s = time.perf_counter() - t0
+        self.P = ParInterface(self.itf, workers)
+        self.workers = self.P.workers
+        self.pc = Preconditioner(self.P, "bsp", blocks=c["blocks"])
+        rng = np.random.default_rng(1234)
+        self.r = rng.standard_normal(self.itf.size) + 1j * rng.standard_normal(self.itf.size)
+        self.R = int(c["nrhs"])  # the reference has one right-hand side: R applies per multi-RHS apply
+        self._stages = None
+        self.solves_per_apply = None
+        self.P.apply_A(self.r)  # warm: every worker has touched its share of the operators and factors
+
+    def close(self):
+        self.P.close()
+
+    def time_apply(self):
+        """One full BSP apply: (seconds, subdomain solves)."""
+        s0, t0 = self.P.solves, time.perf_counter()
+        self.pc.bsp_apply(self.r)
+        dt, ns = time.perf_counter() - t0, self.P.solves - s0
+        self.solves_per_apply = ns
+        return dt, ns
+
+    def time_ims(self):
+        t0 = time.perf_counter()
+        self.P.apply_A(self.r)
+        return time.perf_counter() - t0
+
+    def run_solves(self, quota):
+        """Run BSP apply stages (one S application each, in apply order, a new
+        apply starting when one completes) until >= quota solves: (solves, s)."""
+        s0, t0 = self.P.solves, time.perf_counter()
+        while self.P.solves - s0 < quota:
+            if self._stages is None:
+                self._stages = self.pc.bsp_apply_iter(self.r)
+            try:
+                next(self._stages)
+            except StopIteration:
+                self._stages = None
+        return self.P.solves - s0, time.perf_counter() - t0
+
+
+def cpu_baseline(cfgno):
+    """The reference arithmetic on all host cores, bounded sample: one full BSP
+    apply and one (I-S) apply after the shared-factor setup (~10-30 s at cfg5)."""
+    ref = ReferenceCPU(cfgno)
+    try:
+        t_bsp, ns = ref.time_apply()
+        t_ims = ref.time_ims()
+    finally:
+        ref.close()
+    its, _ = reference_iterations(cfgno)
+    per = t_bsp * ref.R
+    out = {"value": 1.0 / per, "unit": "applies/s", "cores": ref.workers, "kind": "port",
+           "sample": f"one full BSP apply ({ns} subdomain SuperLU solves + outgoing traces through the reference "
+                     f"loop; x{ref.R} right-hand sides, the reference has one) and one (I-S) apply on "
+                     f"{ref.workers} processes",
+           "t_bsp_apply_s": t_bsp, "t_ims_apply_s": t_ims, "setup_s": ref.setup_s, "host": host_info()}
+    if its:
+        out["gmres_projected_s"] = ref.R * (its * (t_bsp + t_ims) + t_bsp)
+        out["gmres_projection"] = (f"{its} reference iterations x (BSP + (I-S) apply) + the final x = M(V y) apply"
+                                   + (f", x {ref.R} right-hand sides" if ref.R > 1 else ""))
+    return out
 
 
 def run_reference(args):
-    """--impl reference: the reference path (oracle port) on all host cores."""
+    """--impl reference: the reference path on the host cores (ReferenceCPU)."""
     rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)
     if rank != 0:
         return 0
-    import multiprocessing as mp
-    from paper_2209_10886_b200.configs import CONFIGS
-    c = CONFIGS[args.config]
-    # the reference solves every subdomain of a step that has an output face
-    # (interface_system.py:122-124), once per right-hand side
-    nsol = solves_per_apply_cfg(c) * int(c["nrhs"])
-    procs = os.cpu_count() or 1
-    ctx = mp.get_context("fork")
-    with ctx.Pool(procs, initializer=_cpu_worker_init, initargs=(args.config,)) as pool:
-        pool.map(_cpu_worker_solves, [1] * procs)
-        t0 = time.perf_counter()
-        pool.map(_cpu_worker_solves, [1] * procs)
-        # each step a bounded sample: ~1.5 s, less when many steps are asked for,
-        # so that the whole --steps K --warmup W run stays near two minutes
-        target = max(0.05, min(1.5, 120.0 / max(1, args.steps + args.warmup)))
-        per = max(1, int(target / max((time.perf_counter() - t0), 1e-3)))
-        for _ in range(args.warmup):
-            pool.map(_cpu_worker_solves, [per] * procs)
-        times = []
-        total = 0
+    ref = ReferenceCPU(args.config)
+    try:
+        t_apply, ns = ref.time_apply()  # the first (warm-up) apply also sizes the samples
+        t_ims = ref.time_ims()
+        for _ in range(max(0, args.warmup - 1)):
+            if t_apply * args.warmup > 60.0:
+                break
+            t_apply, ns = ref.time_apply()
+        # each timed step is a bounded sample: a whole apply when the run fits in
+        # ~2 minutes, otherwise the next S applications of the apply sequence up
+        # to a solve quota (stage granularity; applies continue across steps)
+        frac = min(1.0, 120.0 / max(1e-9, args.steps * t_apply))
+        quota = max(1, int(round(frac * ns)))
+        done, times = 0, []
         for _ in range(args.steps):
-            t0 = time.perf_counter()
-            res = pool.map(_cpu_worker_solves, [per] * procs)
-            times.append(time.perf_counter() - t0)
-            total += sum(r[0] for r in res)
+            k, dt = ref.run_solves(quota)
+            done += k
+            times.append(dt)
+    finally:
+        ref.close()
     wall = sum(times)
-    solves_s = total / wall
-    value = solves_s / nsol
+    value = (done / (ns * ref.R)) / wall
+    its, t_golden = reference_iterations(args.config)
+    c = ref.c
+    cpu = {"value": value, "unit": "applies/s", "cores": ref.workers, "kind": "port",
+           "sample": (f"each step: {'one full BSP apply' if frac >= 1.0 else f'{quota} of the {ns} subdomain solves of a BSP apply'}"
+                      f" through the reference loop (S applications in apply order, gather / zero-skip / SuperLU "
+                      f"solve / outgoing traces / scatter), every S application's solves on {ref.workers} forked "
+                      f"processes" + (f"; x{ref.R} single-RHS applies per multi-RHS apply" if ref.R > 1 else "")),
+           "setup_s": ref.setup_s, "t_bsp_apply_s": t_apply, "t_ims_apply_s": t_ims, "host": host_info()}
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "applies/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / len(times),
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / max(1, len(times)),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128",
-            "data": "synthetic", "config": config_json(c, 1),
-            "cpu_baseline": {"value": value, "unit": "applies/s", "cores": procs, "kind": "port",
-                             "sample": f"each step: {procs} processes x {per} SuperLU solves + outgoing traces of "
-                                       f"an interior {c['n']}x{c['n']} subdomain; applies/s = solves/s / {nsol} "
-                                       f"solves per BSP apply",
-                             "host": host_info()},
+            "data": "synthetic", "config": config_json(c, 1), "cpu_baseline": cpu,
             "e2e": {"value": value, "unit": "applies/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if its:
+        line["gmres"] = {"time_to_solution_s": ref.R * (its * (t_apply + t_ims) + t_apply), "projected": True,
+                         "iterations": its,
+                         "projection": "reference iterations x (BSP apply + (I-S) apply) + the final M apply, each "
+                                       "timed above on this host" + (f", x {ref.R} right-hand sides" if ref.R > 1 else ""),
+                         "build_container_measured_s": t_golden}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -519,7 +585,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_baseline(args.config, solves_per_apply_cfg(c) * R)
+            cpu = cpu_baseline(args.config)
         except Exception as e:  # report, do not fail the bench
             cpu = {"value": None, "unit": "applies/s", "cores": 1, "kind": "port", "sample": f"failed: {e}"}
 
@@ -544,24 +610,6 @@ def fp64_peak():
     p = os.path.join(ROOT, "profiles", "fp64_peak_b200.json")
     with open(p) as f:
         return float(json.load(f)["dmma_m8n8k4_tflops"])
-
-
-def solves_per_apply_cfg(c):
-    """Subdomain solves of one BSP apply in the reference path: one per
-    subdomain of every forward / backward step (windows) plus N_dom for the
-    intermediate residual."""
-    from oracle.lattice import Lattice
-    from paper_2209_10886_b200.indexing import window_ranges
-    lat = Lattice(c["n1"], c["n2"])
-
-    def nl(s):
-        return sum(1 for f, _ in lat.faces[s] if f in (0, 1))
-
-    nfw = sum(1 for lo, hi in window_ranges(c["n1"], c["n2"], "lower", c["blocks"]) for t in range(1, hi - lo + 1)
-              for s in lat.groups.get(lo + t - 1, []) if len(lat.faces[s]) > nl(s))
-    nbw = sum(1 for lo, hi in window_ranges(c["n1"], c["n2"], "upper", c["blocks"]) for t in range(1, hi - lo + 1)
-              for s in lat.groups.get(hi - t + 1, []) if nl(s) > 0)
-    return nfw + nbw + len(lat.subs)
 
 
 if __name__ == "__main__":

@@ -53,6 +53,7 @@ class Interface:
                         op.factorise()
                         cache[key] = op.lu
                     op.lu = cache[key]
+                    op.matrix = None  # the shared factor is all a solve needs (512 x 7 MB at cfg5)
                     self.ops[s] = op
                 self.n_factors = len(cache)
             else:

@@ -39,10 +39,13 @@ def _work(args):
     subs, targets = args
     g = np.ndarray((_L, 1), dtype=complex, buffer=_SHM.buf)
     out = []
+    solves = 0
     for s in subs:
-        for sl, r, tr in _ITF.scatter_one(s, g, targets):
+        writes = _ITF.scatter_one(s, g, targets)
+        solves += bool(writes)  # scatter_one returns no writes exactly when it skips the solve
+        for sl, r, tr in writes:
             out.append((sl.start, sl.stop, np.asarray(tr).reshape(-1)))
-    return out
+    return solves, out
 
 
 class ParInterface:
@@ -59,6 +62,7 @@ class ParInterface:
         self.g = np.ndarray((itf.size,), dtype=complex, buffer=_SHM.buf)
         self.workers = max(1, int(workers or os.cpu_count() or 1))
         self.pool = mp.get_context("fork").Pool(self.workers, initializer=_init)
+        self.solves = 0  # subdomain solves performed so far (the reference's unit of work)
 
     def close(self):
         self.pool.close()
@@ -80,7 +84,8 @@ class ParInterface:
         out = np.zeros(self.size, dtype=complex)
         # round robin: every subdomain solve costs the same (one SuperLU solve of an n^2 system)
         chunks = [solves[w::self.workers] for w in range(self.workers)]
-        for writes in self.pool.map(_work, [(c, targets) for c in chunks if c]):
+        for ns, writes in self.pool.map(_work, [(c, targets) for c in chunks if c]):
+            self.solves += ns
             for a, b, tr in writes:
                 out[a:b] = tr
         return out

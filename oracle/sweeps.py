@@ -18,6 +18,15 @@ from .interface import Interface
 from .lattice import windows as make_windows
 
 
+def _run(gen):
+    """Drive a stage generator to completion and return its value."""
+    while True:
+        try:
+            next(gen)
+        except StopIteration as stop:
+            return stop.value
+
+
 def _mask(itf: Interface, groups):
     """Boolean mask over vector entries owned by the given groups
     (TraceLayout.group_indices, interface_system.py:48-56)."""
@@ -58,36 +67,57 @@ class Preconditioner:
         return self.backward_sweep(self.forward_sweep(r))
 
     # ---- BSP
-    def _window_solve(self, r, lo, hi, direction):
+    # The *_iter forms yield after every S application (one restricted_apply or
+    # apply_interface_operator call of the reference) so that a caller can run
+    # an apply stage by stage (bench.py's bounded CPU-baseline samples); the
+    # plain forms run them to completion -- one implementation of the arithmetic.
+    def _window_solve_iter(self, r, lo, hi, direction):
         zw = np.where(_mask(self.itf, range(lo, hi + 1)).reshape((-1,) + (1,) * (np.ndim(r) - 1)), r, 0)
         zw = zw.astype(complex)
         if direction == "forward":
             for gam in range(lo + 1, hi + 1):
                 zw += self.itf.restricted(zw, {gam - 1}, {gam})
+                yield
         else:
             for gam in range(hi - 1, lo - 1, -1):
                 zw += self.itf.restricted(zw, {gam + 1}, {gam})
+                yield
         return zw
 
-    def bj_half_apply(self, r, direction):
+    def bj_half_apply_iter(self, r, direction):
         r = np.asarray(r, dtype=complex)
         wins = self.lower if direction == "forward" else self.upper
         if self.seam == "dedup":
             z = r.copy()
             for lo, hi in wins:
                 m = _mask(self.itf, range(lo, hi + 1)).reshape((-1,) + (1,) * (r.ndim - 1))
-                z += self._window_solve(r, lo, hi, direction) - np.where(m, r, 0)
+                zw = yield from self._window_solve_iter(r, lo, hi, direction)
+                z += zw - np.where(m, r, 0)
             return z
         z = np.zeros_like(r)
         for lo, hi in wins:
-            z += self._window_solve(r, lo, hi, direction)
+            z += yield from self._window_solve_iter(r, lo, hi, direction)
         return z
 
-    def bsp_apply(self, b):
+    def bsp_apply_iter(self, b):
         b = np.asarray(b, dtype=complex)
-        zL = self.bj_half_apply(b, "forward")
-        rp = b - self.itf.apply_A(zL) if self.inter else b
-        return zL + self.bj_half_apply(rp, "backward")
+        zL = yield from self.bj_half_apply_iter(b, "forward")
+        if self.inter:
+            rp = b - self.itf.apply_A(zL)
+            yield
+        else:
+            rp = b
+        zU = yield from self.bj_half_apply_iter(rp, "backward")
+        return zL + zU
+
+    def _window_solve(self, r, lo, hi, direction):
+        return _run(self._window_solve_iter(r, lo, hi, direction))
+
+    def bj_half_apply(self, r, direction):
+        return _run(self.bj_half_apply_iter(r, direction))
+
+    def bsp_apply(self, b):
+        return _run(self.bsp_apply_iter(b))
 
     def __call__(self, r):
         if self.kind == "none":

@@ -869,6 +869,11 @@ int build_steps(Ctx* c) {
   dfree(c, c->mo_r_blocks, 0); c->mo_r_blocks = nullptr; c->n_mo_r = 0;
   Plan& P = c->plan;
   auto f = P.half_steps(0), b = P.half_steps(1);
+  for (auto* v : {&f, &b})
+    for (const auto& st : *v) {
+      const std::string bad = P.check_step(st, true);
+      if (!bad.empty()) return fail(c, 1, "windows give an unsafe sweep: " + bad);
+    }
   c->fwd.assign(f.size(), DevStep());
   c->bwd.assign(b.size(), DevStep());
   for (size_t i = 0; i < f.size(); ++i) if (make_step(c, f[i], c->fwd[i])) return -1;
@@ -2306,9 +2311,11 @@ int hs_schedule(const hs_ctx* cc, int kind, int32_t* rec, int cap, int* count) {
   P.nranks = 1; P.rank = 0;
   for (auto& s : P.subs) s.rank = 0;
   std::vector<int32_t> out;
+  std::string bad;
   auto emit = [&](const std::vector<StepTable>& steps, int phase, int& step) {
     for (auto& st : steps) {
       ++step;
+      if (bad.empty()) bad = P.check_step(st, true);
       std::set<int> seen;
       for (auto& it : st.items)
         if (seen.insert(it.s).second) { out.push_back(step); out.push_back(phase); out.push_back(it.s); }
@@ -2326,6 +2333,7 @@ int hs_schedule(const hs_ctx* cc, int kind, int32_t* rec, int cap, int* count) {
   } else if (kind != HS_PC_NONE) {
     return fail(c, 1, "unknown preconditioner kind");
   }
+  if (!bad.empty()) return fail(c, 1, "windows give an unsafe sweep: " + bad);
   *count = (int)(out.size() / 3);
   if (rec) {
     if (cap < *count) return fail(c, 1, "schedule buffer too small");

@@ -134,6 +134,27 @@ std::vector<StepTable> Plan::half_steps(int dir) const {
   return out;
 }
 
+std::string Plan::check_step(const StepTable& st, bool in_place) const {
+  std::set<int> reads, writes;
+  for (const Item& it : st.items) {
+    if (it.alt) continue;  // a window start reads the half's input r, not the z being written
+    const SubPlan& sp = subs[it.s];
+    for (int q = 0; q < sp.k; ++q) reads.insert(sp.first_block + q);  // its incoming slab m(s, .)
+  }
+  for (const Item& it : st.items) {
+    const SubPlan& sp = subs[it.s];
+    for (int q = it.rlo / n; q < (it.rhi + n - 1) / n; ++q) {
+      const int b = sp.tgt_block[q];  // m(nbr, s): the block subdomain s writes toward face q
+      if (!writes.insert(b).second)
+        return "step record writes block " + std::to_string(b + 1) + " twice";
+      if (in_place && reads.count(b))
+        return "step record reads and writes block " + std::to_string(b + 1) + " (subdomain (" +
+               std::to_string(sp.i1) + "," + std::to_string(sp.i2) + ") writes into a slab solved in the same step)";
+    }
+  }
+  return "";
+}
+
 StepTable Plan::full_step() const {
   StepTable st;
   for (int s = 0; s < nsub; ++s) {

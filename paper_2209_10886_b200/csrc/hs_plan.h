@@ -66,6 +66,12 @@ struct Plan {
 
   // Step tables of the sweeps.  dir 0 = forward over win_lower, 1 = backward over win_upper.
   std::vector<StepTable> half_steps(int dir) const;
+  // within a sweep step record the blocks the solves write are
+  // pairwise distinct and disjoint from the blocks they read in z (the sweeps
+  // update z in place, so an overlap would make the result depend on the order
+  // of the step's solves; a window start reads the half's input r instead, the
+  // dedup rule of SURVEY.md §8a11).  Empty string = OK, else the violation.
+  std::string check_step(const StepTable& st, bool in_place) const;
   StepTable full_step() const;
   StepTable restricted_step(const std::vector<int>& src, const std::vector<int>& tgt) const;
   // Keep this rank's items; fill send slots / receive lists (row-band exchange).

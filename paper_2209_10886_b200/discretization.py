@@ -54,8 +54,7 @@ class ProblemSpec:
         return (-self.subdomain_side / 2.0, -self.subdomain_side / 2.0)
 
     def incident_wave(self, x, y, direction=None):
-        dx, dy = self.incident_direction if direction is None else direction
-        return np.exp(1j * self.kappa * (dx * x + dy * y) / np.hypot(dx, dy))
+        return plane_wave(self.kappa, self.incident_direction if direction is None else direction, x, y)
 
 
 @dataclass(frozen=True)
@@ -119,8 +118,16 @@ def lifting_data(spec, partition, directions=None) -> tuple[MultiIndex | None, n
         return None, np.zeros((0, 1), dtype=complex)
     X, Y = cell_centres(spec, home)
     x, y = X.ravel()[cells], Y.ravel()[cells]
-    dirs = [spec.incident_direction] if directions is None else list(directions)
-    return home, np.stack([-spec.incident_wave(x, y, d) for d in dirs], axis=1)
+    if directions is None:
+        # the spec's own incident_wave (discretization.py:79-83): also a reference ProblemSpec's
+        return home, -np.asarray(spec.incident_wave(x, y))[:, None]
+    return home, np.stack([-plane_wave(spec.kappa, d, x, y) for d in directions], axis=1)
+
+
+def plane_wave(kappa, direction, x, y):
+    """exp(i kappa d.x / |d|) (discretization.py:79-83) for any direction d."""
+    dx, dy = direction
+    return np.exp(1j * kappa * (dx * x + dy * y) / np.hypot(dx, dy))
 
 
 def face_cells(n: int) -> dict[str, np.ndarray]:

@@ -215,7 +215,11 @@ class GpuInterfaceSystem:
             c = native.i32(cells)
             self.ctx.call("hs_set_dirichlet", self.home.i1, self.home.i2, native.iptr(c), len(c))
         t0 = time.perf_counter()
-        self.ctx.call("hs_factor")
+        if device >= 0:
+            self.ctx.call("hs_factor")
+        # device = -1: a plan-only system (lattice tables, windows, schedules,
+        # exchange plans; no factorisation, every apply raises) -- the host side
+        # of the boundary, usable without a GPU
         self.setup_time = time.perf_counter() - t0
         self._operators = None
         self.sweep = SweepConfig()

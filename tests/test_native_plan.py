@@ -121,3 +121,28 @@ def test_row_band_exchange_plan(n1, n2, G):
                     if 0 <= peer < G:
                         moved |= {int(b) for _, b, _ in ctxs[r].exchange_plan(2, peer)}
             assert moved == crossing
+
+
+def test_step_records_read_write_disjoint():
+    """every sweep step record's written blocks are distinct and
+    disjoint from the blocks it reads in z -- checked by the native plan for
+    every lattice / block count the schedules are built for (hs_schedule fails
+    on a violation), and a violation is caught: overlapping windows make a
+    subdomain write into a slab another solve of the same step reads."""
+    import ctypes as C
+    from paper_2209_10886_b200 import native
+    from paper_2209_10886_b200.indexing import window_ranges
+    for n1, n2 in [(4, 4), (8, 8), (5, 10), (6, 3), (16, 16), (32, 16), (1, 5), (7, 2)]:
+        for p in (None, 1, 2, 3, 4, 8):
+            ctx = native.Context(-1, n1, n2, 8, 0.1, 2.0, 2.0j, 0, 1)
+            for k, kind in ((0, "lower"), (1, "upper")):
+                w = window_ranges(n1, n2, kind, p)
+                lo, hi = native.i32([a for a, _ in w]), native.i32([b for _, b in w])
+                ctx.call("hs_set_windows", k, native.iptr(lo), native.iptr(hi), len(w))
+            ctx.schedule(native.HS_PC_BSP)
+            ctx.schedule(native.HS_PC_SP)
+    ctx = native.Context(-1, 5, 5, 8, 0.1, 2.0, 2.0j, 0, 1)
+    lo, hi = native.i32([2, 3]), native.i32([5, 6])
+    ctx.call("hs_set_windows", 0, native.iptr(lo), native.iptr(hi), 2)
+    with pytest.raises(ValueError, match="unsafe sweep"):
+        ctx.schedule(native.HS_PC_BSP)
