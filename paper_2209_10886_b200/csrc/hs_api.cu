@@ -169,7 +169,7 @@ void free_step(Ctx* c, DevStep& s) {
 // shared = true: the class maps (4 faces W,S,N,E), one column per (subdomain,
 // RHS), items of the same class and face range batched into one contraction.
 void build_mma_host(Ctx* c, const StepTable& host, int R, bool shared, std::vector<MmaTask>& tasks,
-                    std::vector<MmaCol>& cols, double& flops) {
+                    std::vector<MmaCol>& cols, double& flops, int bn = 32) {
   const Plan& P = c->plan;
   const int n = c->n;
   auto col_for = [&](const Item& item, int r, bool global_faces) {
@@ -193,12 +193,12 @@ void build_mma_host(Ctx* c, const StepTable& host, int R, bool shared, std::vect
       const SubPlan& sp = P.subs[item.s];
       const int K = sp.k * n;
       for (int r0 = (item.rlo / 32) * 32; r0 < item.rhi; r0 += 32)
-        for (int c0 = 0; c0 < R; c0 += 32) {
+        for (int c0 = 0; c0 < R; c0 += bn) {
           MmaTask tk;
           tk.a_off = sp.T_off + (long long)(r0 / 32) * K * 32;
           tk.K = K; tk.r0 = r0; tk.rlo = item.rlo; tk.rhi = item.rhi;
           tk.col0 = (int)cols.size();
-          tk.ncols = std::min(32, R - c0);
+          tk.ncols = std::min(bn, R - c0);
           for (int r = c0; r < c0 + tk.ncols; ++r) cols.push_back(col_for(item, r, false));
           tasks.push_back(tk);
           flops += 8.0 * 32 * tk.ncols * K;
@@ -223,8 +223,8 @@ void build_mma_host(Ctx* c, const StepTable& host, int R, bool shared, std::vect
     std::vector<MmaCol> gc;
     for (int i : g.second)
       for (int r = 0; r < R; ++r) gc.push_back(col_for(host.items[i], r, true));
-    for (size_t c0 = 0; c0 < gc.size(); c0 += 32) {
-      const int nc = (int)std::min<size_t>(32, gc.size() - c0);
+    for (size_t c0 = 0; c0 < gc.size(); c0 += bn) {
+      const int nc = (int)std::min<size_t>(bn, gc.size() - c0);
       const int base = (int)cols.size();
       cols.insert(cols.end(), gc.begin() + c0, gc.begin() + c0 + nc);
       for (int r0 = (glo / 32) * 32; r0 < ghi; r0 += 32) {
@@ -261,6 +261,23 @@ int validate_mma(Ctx* c, const std::vector<MmaTask>& tasks, const std::vector<Mm
   return 0;
 }
 
+// k_zmma2's k-major operand form needs every task's columns to be consecutive
+// right-hand sides of one slab read from one source: B row k is then one
+// contiguous run at in[0] + k R.
+bool slab_rows(const std::vector<MmaTask>& tasks, const std::vector<MmaCol>& cols) {
+  for (const MmaTask& tk : tasks) {
+    const MmaCol& c0 = cols[tk.col0];
+    if (c0.in[0] < 0) return false;
+    for (int j = 1; j < tk.ncols; ++j) {
+      const MmaCol& cj = cols[tk.col0 + j];
+      if (cj.alt != c0.alt) return false;
+      for (int q = 0; q < 4; ++q)
+        if ((c0.in[q] < 0) != (cj.in[q] < 0) || (c0.in[q] >= 0 && cj.in[q] != c0.in[q] + j)) return false;
+    }
+  }
+  return true;
+}
+
 int make_mma(Ctx* c, DevStep& st, int R, bool shared, DevMma** out) {
   const int key = shared ? -R : R;
   auto it = st.mma.find(key);
@@ -271,9 +288,29 @@ int make_mma(Ctx* c, DevStep& st, int R, bool shared, DevMma** out) {
   std::vector<MmaTask> tasks;
   std::vector<MmaCol> cols;
   double flops = 0;
-  build_mma_host(c, st.host, R, shared, tasks, cols, flops);
+  // k_zmma2 (bulk-copy staged): slabs of R RHS (64-column tasks when R > 32) or
+  // shared maps with one RHS (64 subdomain columns); k_zmma otherwise.
+  // HS_ZMMA2=0 keeps k_zmma everywhere.
+  static const bool z2 = !(getenv("HS_ZMMA2") && atoi(getenv("HS_ZMMA2")) == 0);
+  int kind = 0, bn = 32;
+  if (z2 && !shared) kind = 1, bn = R > 32 ? 64 : 32;
+  else if (z2 && shared && R == 1) kind = 2, bn = 64;
+  build_mma_host(c, st.host, R, shared, tasks, cols, flops, bn);
+  static const int bn_env = getenv("HS_ZMMA2_BN") ? atoi(getenv("HS_ZMMA2_BN")) : 0;  // 32 / 64: fixed
+  if (bn == 64 && (bn_env == 32 || (bn_env != 64 && (int)tasks.size() < c->num_sms))) {
+    // a step with fewer 64-column tasks than SMs: 32-column tasks, twice the CTAs
+    tasks.clear(); cols.clear(); flops = 0; bn = 32;
+    build_mma_host(c, st.host, R, shared, tasks, cols, flops, bn);
+  }
   if (validate_mma(c, tasks, cols, R, shared)) return -1;
+  if (kind == 1 && !slab_rows(tasks, cols)) return fail(c, -4, "internal: contraction task columns are not one slab");
+  if (kind != 0 && !c->zeros) {
+    CK(dalloc(c, (void**)&c->zeros, 64 * sizeof(double2)));
+    CK(cudaMemsetAsync(c->zeros, 0, 64 * sizeof(double2), c->stream));
+  }
   DevMma m;
+  m.kind = kind;
+  m.bn = bn;
   if (upload(c, &m.tasks, tasks) || upload(c, &m.cols, cols)) return -1;
   m.ntasks = (int)tasks.size();
   m.ncols = (int)cols.size();
@@ -976,7 +1013,7 @@ int run_step(Ctx* c, DevStep& st, const double2* srcA, const double2* srcB, Epi 
     e1 = ev_get(c);
     cudaEventRecord(e0, c->stream);
   }
-  if (mm) launch_zmma(*c, *mm, shared ? c->Tcls : c->T, srcA, srcB, e, R);
+  if (mm) launch_zmma(*c, *mm, shared ? c->Tcls : c->T, srcA, srcB, c->zeros, e, R);
   else launch_step(*c, st, srcA, srcB, e, R);
   if (e1) {
     cudaEventRecord(e1, c->stream);
@@ -2488,8 +2525,8 @@ int hs_set_trace(hs_ctx* c, int on) {
   if (c->device < 0) return fail(c, 1, "plan-only context");
   c->trace_on = on != 0;
   if (c->trace_on && !c->trace) {
-    size_t rows = 0;  // every strip of every map, up to 4 times (phases of one apply)
-    for (const SubPlan& sp : c->plan.subs) rows += 4 * (size_t)((sp.k * c->n + kRowTile - 1) / kRowTile);
+    size_t rows = 0;  // every strip of every map, up to 16 times (phases / RHS chunks / split-K ranks)
+    for (const SubPlan& sp : c->plan.subs) rows += 16 * (size_t)((sp.k * c->n + kRowTile - 1) / kRowTile);
     CK(dalloc(c, (void**)&c->trace, rows * 6 * sizeof(unsigned long long)));
     c->trace_cap = rows;
   }

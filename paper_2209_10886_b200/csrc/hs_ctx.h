@@ -92,6 +92,8 @@ struct DevMma {
   int ntasks = 0, ncols = 0;
   int minK = 0;  // smallest K of the tasks (split-K decision)
   double flops = 0;
+  int bn = 32;      // columns per task
+  int kind = 0;     // 0: k_zmma (cp.async); 1: k_zmma2 k-major slab rows; 2: k_zmma2 n-major columns
 };
 
 // A step uploaded to the device: items + tiles + receive list.
@@ -359,6 +361,7 @@ struct Ctx {
   std::map<void*, size_t> alloc_sz;  // live device allocations
   int num_sms = 148;
   int coop_ok = 0;
+  double2* zeros = nullptr;  // 64 zero elements: the source of absent faces in bulk-copied operands
 };
 
 }  // namespace hs

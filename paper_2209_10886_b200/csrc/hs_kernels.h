@@ -34,7 +34,7 @@ void launch_gather_blocks(Ctx& c, double2* out, const double2* const* src, int G
 cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double2* zL, double2* rp,
                              double2* w, double2* z, double2* wout = nullptr);
 void launch_zmma(Ctx& c, const DevMma& m, const double2* A, const double2* srcA, const double2* srcB,
-                 const Epi& e, int R);
+                 const double2* zeros, const Epi& e, int R);
 cudaError_t set_zmma_smem_limit();
 cudaError_t launch_zmma_fused(Ctx& c, const DevFusedMma& f, FusedMmaArgs a);
 void launch_pack_strips(Ctx& c, const double2* T4, double2* out, int rows, int cols);

@@ -327,6 +327,468 @@ __global__ void __launch_bounds__(THREADS) k_zmma(const MmaTask* __restrict__ ta
   }
 }
 
+// ---------------------------------------------------------------------------
+// k_zmma2: the per-step contraction with bulk-copy (TMA) staging.
+//
+// One CTA = one task of 32 map rows x BN columns (64: all 64 right-hand sides
+// of a subdomain's slab, or 64 subdomain columns of a shared-map step), or a
+// 1/KS slice of its K range when the step has too few tasks to fill the GPU
+// (cluster split-K, partial tiles summed by rank 0 through DSMEM in rank
+// order -- deterministic).  A producer warp streams K in chunks of 32 through
+// an S-stage ring with cp.async.bulk copies (mbarrier complete_tx):
+//   A [k][m]  one 16 KB copy per chunk (unpadded, see Z2::SA);
+//   B rows padded so the 128-bit fragment loads are conflict-free:
+//   B k-major [k][j] (R RHS of one slab: one contiguous row per position)
+//             stride BN + 2, the same argument;
+//   B n-major [j][k] (shared maps, one column per subdomain: its 32 positions
+//             of the chunk's face are one contiguous 512-byte run) stride 36:
+//             units 4 gid + tig (mod 8), distinct.
+// Absent faces read a zero buffer.  NWC consumer warps each own TM x TN 8x8
+// DMMA tiles of the output over the whole chunk (no intra-CTA K split), 3M
+// complex product.  The map chunks do not depend on the previous step, so the
+// producer issues the first S stages' map rows before griddepcontrol.wait
+// (programmatic dependent launch) and only the vector rows after it.
+// tools/zcore_bench.cu: this core sustains 0.80-0.86 of the DMMA peak on
+// L2-resident operands (the cp.async core with 4 warps x 2 K halves: ~0.4).
+constexpr int Z2KC = 32;
+
+template <int BN, int TM, int TN, bool NMAJ, int S, bool PERS, int KG = 1>
+struct Z2 {
+  // KG warp groups split every chunk's k range (each group owns the whole tile;
+  // group 1's partial is added to group 0's through shared memory): a 32 x 32
+  // tile then keeps 8 warps x 12 accumulator chains in flight, which the DMMA
+  // pipe needs to stay busy (tools/zcore_bench.cu: 4 warps x 12 reach ~0.4)
+  static constexpr int WM = 32 / (8 * TM), WN = BN / (8 * TN), NWQ = WM * WN, NWC = NWQ * KG,
+                       THREADS = (NWC + 1) * 32;
+  static_assert(KG == 1 || !PERS, "the persistent form keeps one warp group");
+  // A: the chunk's 32 k rows x 32 map rows are one contiguous 16 KB run of the
+  // strip-major layout -> ONE bulk copy, unpadded (a small copy costs the TMA
+  // unit ~60 cycles whatever its size, so 32 padded row copies made the
+  // n-major contraction copy-bound; the 4-way bank conflicts of the unpadded
+  // fragment loads are hidden behind the DMMAs, tools/zcore_bench.cu)
+  static constexpr int SA = 32;
+  static constexpr int SB = NMAJ ? Z2KC + 4 : BN + 2;
+  static constexpr int BROWS = NMAJ ? BN : Z2KC;
+  static constexpr int STAGE = Z2KC * SA + BROWS * SB;
+  static constexpr int YS = BN + 1;  // output tile row stride (conflict-free fragment writes and row/column reads)
+  static constexpr int RING = S * STAGE;
+  // persistent: a separate output tile (the ring already holds the next task's
+  // chunks); one task per CTA: the drained ring holds it
+  static constexpr size_t SMEM = sizeof(double2) * (RING + (PERS ? 32 * YS : 0));
+  static constexpr int ND = PERS ? 2 : 1;  // task descriptor buffers
+  static constexpr int EPT = 32 * BN / (NWC * 32);  // epilogue elements per consumer thread
+  static_assert(WM * TM * 8 == 32 && WN * TN * 8 == BN, "tile split");
+  static_assert(PERS || RING >= 32 * YS, "output tile must fit in the ring");
+};
+
+template <int BN>
+struct ZCols2 {
+  MmaTask tk;
+  long long in[BN][4];
+  long long out[BN][4];
+  int slot[BN][4];
+  int r[BN];
+  int alt[BN];
+};
+
+template <int N>
+__device__ __forceinline__ void consumers_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ unsigned long long z2_gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned z2_smem(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void z2_bar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(z2_smem(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void z2_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(z2_smem(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void z2_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(z2_smem(b)) : "memory");
+}
+__device__ __forceinline__ void z2_wait(unsigned long long* b, unsigned parity) {
+  unsigned ok = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(z2_smem(b)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void z2_copy(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   z2_smem(dst)),
+               "l"(src), "r"(bytes), "r"(z2_smem(bar))
+               : "memory");
+}
+
+// Epilogue operands of one output element, loaded before any store so a lane's
+// up to 2 TM TN loads are in flight together (the epilogue is on every sweep
+// step's critical path).
+struct EpiIn {
+  double2 u, v;
+};
+__device__ __forceinline__ EpiIn epi_load(const Epi& e, long long t) {
+  EpiIn x;
+  switch (e.mode) {
+    case EPI_ACC: x.u = e.o1[t]; break;
+    case EPI_IMS: x.u = e.a[t]; break;
+    case EPI_RESID: x.u = e.a[t]; x.v = e.b[t]; break;
+    case EPI_LATE: x.u = csub(e.a[t], e.b[t]); x.v = e.c[t]; break;
+    case EPI_ACC2: x.u = e.o1[t]; x.v = e.o2[t]; break;
+    default: break;
+  }
+  return x;
+}
+// the arithmetic of epi_apply (hs_common.cuh), same operation order
+__device__ __forceinline__ void epi_store(const Epi& e, long long t, double2 y, const EpiIn& x) {
+  switch (e.mode) {
+    case EPI_SET: e.o1[t] = y; break;
+    case EPI_ACC: e.o1[t] = cadd(x.u, y); break;
+    case EPI_IMS: e.o1[t] = csub(x.u, y); break;
+    case EPI_RESID: {
+      const double2 v = csub(x.u, csub(x.v, y));
+      e.o1[t] = v;
+      e.o2[t] = v;
+      e.o3[t] = cadd(x.v, v);
+    } break;
+    case EPI_LATE: e.o1[t] = cadd(x.u, csub(x.v, y)); break;
+    case EPI_ACC2:
+      e.o1[t] = cadd(x.u, y);
+      e.o2[t] = cadd(x.v, y);
+      break;
+  }
+}
+
+// The kernel.  PERS = false: one task (or one split-K slice of it) per CTA,
+// grid = ntasks x KS.  PERS = true (steps with at least one task per SM):
+// grid <= #SMs, CTA b runs tasks b, b + grid, ... with the producer streaming
+// the next task's chunks while the consumers finish the current one (task
+// descriptors double-buffered, mbarrier dfull / dempty).  Epilogue: the tile
+// goes through shared memory and is finished by all consumer threads with
+// coalesced accesses (k-major: consecutive right-hand sides of a row are
+// consecutive elements; n-major: consecutive rows of a column are).
+template <int BN, int TM, int TN, bool NMAJ, int S, bool PERS, int KG>
+__global__ void __launch_bounds__(Z2<BN, TM, TN, NMAJ, S, PERS, KG>::THREADS, 1)
+    k_zmma2(const MmaTask* __restrict__ tasks, int ntasks, const MmaCol* __restrict__ cols,
+            const double2* __restrict__ A, const double2* srcA, const double2* srcB,
+            const double2* __restrict__ zeros, Epi e, int n, int R, int KS, unsigned long long* tr, int seq) {
+  using F = Z2<BN, TM, TN, NMAJ, S, PERS, KG>;
+  extern __shared__ __align__(128) double2 sm[];
+  __shared__ __align__(8) unsigned long long full[S], empty[S], dfull[2], dempty[2];
+  __shared__ ZCols2<BN> zcs[F::ND];
+  double2* ys = PERS ? sm + F::RING : sm;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int rank = (!PERS && KS > 1) ? (int)cg::this_cluster().block_rank() : 0;
+  const int t0 = PERS ? (int)blockIdx.x : (int)blockIdx.x / KS;
+  const int tstep = PERS ? (int)gridDim.x : ntasks;
+  // trace row (hs_set_trace): start, setup done, first chunk landed, contraction
+  // done, end, (seq << 40 | smid << 32 | block)
+  unsigned long long* trow = tr ? tr + 6ull * blockIdx.x : nullptr;
+  if (trow && tid == 0) trow[0] = z2_gtimer();
+  auto kslice = [&](const MmaTask& tk, int& kc0, int& nk) {
+    const int nk_all = tk.K / Z2KC;
+    kc0 = (int)((long long)nk_all * rank / KS);
+    nk = (int)((long long)nk_all * (rank + 1) / KS) - kc0;
+  };
+  auto stage_cols = [&](ZCols2<BN>& zc, const MmaTask& tk, int j0, int jstep) {
+    for (int j = j0; j < BN; j += jstep) {
+      if (j < tk.ncols) {
+        const MmaCol c = cols[tk.col0 + j];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) zc.in[j][q] = c.in[q], zc.out[j][q] = c.out[q], zc.slot[j][q] = c.slot[q];
+        zc.r[j] = c.r;
+        zc.alt[j] = c.alt;
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) zc.in[j][q] = zc.out[j][q] = -1, zc.slot[j][q] = -1;
+        zc.r[j] = 0;
+        zc.alt[j] = 0;
+      }
+    }
+  };
+  if (warp == F::NWC && lane == 0) {
+    for (int i = 0; i < S; ++i) z2_bar_init(&full[i], 1), z2_bar_init(&empty[i], F::NWC);
+    for (int i = 0; i < 2; ++i) z2_bar_init(&dfull[i], 1), z2_bar_init(&dempty[i], F::NWC);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (!PERS) {
+    // one task: the consumers stage its column table while the producer starts
+    // the map stream (the maps depend neither on it nor on the previous step)
+    if (warp < F::NWC) {
+      if (tid == 0) zcs[0].tk = tasks[t0];
+      stage_cols(zcs[0], tasks[t0], tid, F::NWC * 32);
+    }
+  }
+  __syncthreads();
+  if (trow && tid == 0) trow[1] = z2_gtimer();
+  if (warp == F::NWC) {  // ---------------- producer
+    long long g = 0;
+    for (int t = t0, it = 0; t < ntasks; t += tstep, ++it) {
+      const int d = PERS ? (it & 1) : 0;
+      ZCols2<BN>& zc = zcs[d];
+      const MmaTask tk = tasks[t];
+      if (PERS) {
+        z2_wait(&dempty[d], (unsigned)((it >> 1) & 1) ^ 1);
+        if (lane == 0) zc.tk = tk;
+        stage_cols(zc, tk, lane, 32);
+        __syncwarp();
+        if (lane == 0) z2_arrive(&dfull[d]);  // release: the table is visible to the consumers
+      }
+      int kc0, nk;
+      kslice(tk, kc0, nk);
+      const unsigned bytesB =
+          NMAJ ? (unsigned)(BN * 32 * sizeof(double2)) : (unsigned)(Z2KC * tk.ncols * sizeof(double2));
+      const unsigned bytes = (unsigned)(Z2KC * 32 * sizeof(double2)) + bytesB;
+      const double2* Ab = A + tk.a_off;
+      auto issueA = [&](int st, int kc) {
+        if (lane == 0)
+          z2_copy(sm + (size_t)st * F::STAGE, Ab + (long long)kc * Z2KC * 32, Z2KC * 32 * sizeof(double2), &full[st]);
+      };
+      auto issueB = [&](int st, int kc) {
+        double2* sb = sm + (size_t)st * F::STAGE + Z2KC * F::SA;
+        const int k0 = kc * Z2KC, q = k0 / n, p0 = k0 - q * n;
+        if (NMAJ) {
+          for (int j = lane; j < BN; j += 32) {
+            const long long off = zc.in[j][q];
+            const double2* src = off >= 0 ? (zc.alt[j] ? srcB : srcA) + off + (long long)p0 * R : zeros;
+            z2_copy(sb + j * F::SB, src, 32 * sizeof(double2), &full[st]);
+          }
+        } else {
+          // one slab: positions k0.. of the compact faces are consecutive rows of R
+          const double2* base = (zc.alt[0] ? srcB : srcA) + zc.in[0][0] + (long long)k0 * R;
+          for (int r = lane; r < Z2KC; r += 32)
+            z2_copy(sb + r * F::SB, base + (long long)r * R, tk.ncols * sizeof(double2), &full[st]);
+        }
+      };
+      int i = 0;
+      if (it == 0) {
+        // first task: its first stages' map rows before the dependency wait
+        const int pre = nk < S ? nk : S;
+        for (int k = 0; k < pre; ++k) {
+          if (lane == 0) z2_expect_tx(&full[k], bytes);
+          __syncwarp();
+          issueA(k, kc0 + k);
+        }
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        for (int k = 0; k < pre; ++k) issueB(k, kc0 + k);
+        i = pre;
+        g = pre;
+      }
+      for (; i < nk; ++i, ++g) {
+        const int st = (int)(g % S);
+        if (g >= S) z2_wait(&empty[st], (unsigned)((g / S) & 1) ^ 1);
+        if (lane == 0) z2_expect_tx(&full[st], bytes);
+        __syncwarp();
+        issueA(st, kc0 + i);
+        issueB(st, kc0 + i);
+      }
+    }
+  } else {  // ---------------- consumers
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // epilogue operands: the previous step's outputs
+    const int kg = warp / F::NWQ, wq = warp % F::NWQ;
+    const int wm = wq / F::WN, wn = wq % F::WN;
+    const int gid = lane >> 2, tig = lane & 3;
+    const int ctid = tid;  // consumers are warps 0 .. NWC - 1
+    constexpr int KH = Z2KC / KG;  // k rows of a chunk per warp group
+    long long g = 0;
+    for (int t = t0, it = 0; t < ntasks; t += tstep, ++it) {
+      const int d = PERS ? (it & 1) : 0;
+      if (PERS) z2_wait(&dfull[d], (unsigned)((it >> 1) & 1));
+      const ZCols2<BN>& zc = zcs[d];
+      const MmaTask tk = zc.tk;
+      int kc0, nk;
+      kslice(tk, kc0, nk);
+      double cr[TM][TN][2], ci[TM][TN][2], p3[TM][TN][2];
+#pragma unroll
+      for (int a = 0; a < TM; ++a)
+#pragma unroll
+        for (int b = 0; b < TN; ++b)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) cr[a][b][c] = ci[a][b][c] = p3[a][b][c] = 0.0;
+      for (int i = 0; i < nk; ++i, ++g) {
+        const int st = (int)(g % S);
+        z2_wait(&full[st], (unsigned)((g / S) & 1));
+        if (trow && tid == 0 && g == 0) trow[2] = z2_gtimer();
+        const double2* sa = sm + (size_t)st * F::STAGE;
+        const double2* sb = sa + Z2KC * F::SA;
+#pragma unroll
+        for (int kk = 0; kk < KH; kk += 4) {
+          const int k4 = kg * KH + kk;
+          double2 a[TM], b[TN];
+#pragma unroll
+          for (int mt = 0; mt < TM; ++mt) a[mt] = sa[(k4 + tig) * F::SA + (wm * TM + mt) * 8 + gid];
+#pragma unroll
+          for (int nt = 0; nt < TN; ++nt)
+            b[nt] = NMAJ ? sb[((wn * TN + nt) * 8 + gid) * F::SB + k4 + tig]
+                         : sb[(k4 + tig) * F::SB + (wn * TN + nt) * 8 + gid];
+          double s_b[TN];
+#pragma unroll
+          for (int nt = 0; nt < TN; ++nt) s_b[nt] = b[nt].x + b[nt].y;
+#pragma unroll
+          for (int mt = 0; mt < TM; ++mt) {
+            const double s_a = a[mt].x + a[mt].y;
+#pragma unroll
+            for (int nt = 0; nt < TN; ++nt) dmma(cr[mt][nt][0], cr[mt][nt][1], a[mt].x, b[nt].x);
+#pragma unroll
+            for (int nt = 0; nt < TN; ++nt) dmma(ci[mt][nt][0], ci[mt][nt][1], a[mt].y, b[nt].y);
+#pragma unroll
+            for (int nt = 0; nt < TN; ++nt) dmma(p3[mt][nt][0], p3[mt][nt][1], s_a, s_b[nt]);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) z2_arrive(&empty[st]);
+      }
+#pragma unroll
+      for (int a = 0; a < TM; ++a)
+#pragma unroll
+        for (int b = 0; b < TN; ++b)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const double s1 = cr[a][b][c], s2 = ci[a][b][c];
+            cr[a][b][c] = s1 - s2;
+            ci[a][b][c] = p3[a][b][c] - s1 - s2;
+          }
+      if (trow && tid == 0 && it == 0) trow[3] = z2_gtimer();
+      constexpr int NT = TM * TN * 2;  // accumulator pairs per lane
+      if (KG > 1) {
+        // group g > 0 hands its partial tile to group 0 (the drained ring holds it)
+        consumers_bar<F::NWC * 32>();
+        if (kg > 0) {
+#pragma unroll
+          for (int a = 0; a < TM; ++a)
+#pragma unroll
+            for (int b = 0; b < TN; ++b)
+#pragma unroll
+              for (int c = 0; c < 2; ++c)
+                sm[((warp - F::NWQ) * NT + (a * TN + b) * 2 + c) * 32 + lane] = make_double2(cr[a][b][c], ci[a][b][c]);
+        }
+        consumers_bar<F::NWC * 32>();
+        if (kg == 0) {
+#pragma unroll
+          for (int a = 0; a < TM; ++a)
+#pragma unroll
+            for (int b = 0; b < TN; ++b)
+#pragma unroll
+              for (int c = 0; c < 2; ++c) {
+                const double2 o = sm[(warp * NT + (a * TN + b) * 2 + c) * 32 + lane];
+                cr[a][b][c] += o.x;
+                ci[a][b][c] += o.y;
+              }
+        }
+      }
+      if (!PERS && KS > 1) {
+        // cluster split-K: ranks > 0 publish their tile (in their drained
+        // ring, past the group-reduction area), rank 0 sums in rank order.
+        // Consumers only: the producer has left its loop and issues nothing more.
+        cg::cluster_group cl = cg::this_cluster();
+        double2* red = sm + F::NWQ * NT * 32;
+        if (rank > 0 && kg == 0) {
+#pragma unroll
+          for (int a = 0; a < TM; ++a)
+#pragma unroll
+            for (int b = 0; b < TN; ++b)
+#pragma unroll
+              for (int c = 0; c < 2; ++c)
+                red[(warp * NT + (a * TN + b) * 2 + c) * 32 + lane] = make_double2(cr[a][b][c], ci[a][b][c]);
+        }
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        if (rank == 0 && kg == 0) {
+          for (int src = 1; src < KS; ++src) {
+            const double2* rem = cl.map_shared_rank(red, src);
+            double2 o[NT];
+#pragma unroll
+            for (int i = 0; i < NT; ++i) o[i] = rem[(warp * NT + i) * 32 + lane];
+#pragma unroll
+            for (int a = 0; a < TM; ++a)
+#pragma unroll
+              for (int b = 0; b < TN; ++b)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                  cr[a][b][c] += o[(a * TN + b) * 2 + c].x;
+                  ci[a][b][c] += o[(a * TN + b) * 2 + c].y;
+                }
+          }
+        }
+        // keep remote shared memory alive until rank 0 has read it
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        if (rank != 0) break;
+      }
+      // ---- epilogue through the output tile
+      consumers_bar<F::NWC * 32>();  // the previous task's tile readers (and group partials) are done
+      if (kg == 0) {
+#pragma unroll
+        for (int mt = 0; mt < TM; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < TN; ++nt)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              ys[((wm * TM + mt) * 8 + gid) * F::YS + (wn * TN + nt) * 8 + 2 * tig + h] =
+                  make_double2(cr[mt][nt][h], ci[mt][nt][h]);
+      }
+      consumers_bar<F::NWC * 32>();
+      long long toff[F::EPT];
+      EpiIn xin[F::EPT];
+#pragma unroll
+      for (int u = 0; u < F::EPT; ++u) {
+        const int el = u * F::NWC * 32 + ctid;
+        const int rr = NMAJ ? el % 32 : el / BN, j = NMAJ ? el / 32 : el % BN;
+        const int row = tk.r0 + rr;
+        long long t = -1;
+        if (row >= tk.rlo && row < tk.rhi && j < tk.ncols) {
+          const int q = row / n, p = row - q * n;
+          const int slot = zc.slot[j][q];
+          if (slot == -1) {
+            const long long off = zc.out[j][q];
+            if (off >= 0) t = off + (long long)p * R;
+          } else {
+            // row-band exchange buffers: encoded as -2 - (2 index + (down ? 1 : 0))
+            t = slot >= 0 ? -2 - 2 * (((long long)slot * n + p) * R + zc.r[j])
+                          : -3 - 2 * (((long long)(-slot - 2) * n + p) * R + zc.r[j]);
+          }
+        }
+        toff[u] = t;
+        if (t >= 0) xin[u] = epi_load(e, t);
+      }
+#pragma unroll
+      for (int u = 0; u < F::EPT; ++u) {
+        const int el = u * F::NWC * 32 + ctid;
+        const int rr = NMAJ ? el % 32 : el / BN, j = NMAJ ? el / 32 : el % BN;
+        const long long t = toff[u];
+        const double2 y = ys[rr * F::YS + j];
+        if (t >= 0) {
+          epi_store(e, t, y, xin[u]);
+        } else if (t <= -2) {
+          const long long v = -2 - t;
+          if (v & 1) e.send_dn[v >> 1] = y;
+          else e.send_up[v >> 1] = y;
+        }
+      }
+      if (PERS) {
+        __syncwarp();
+        if (lane == 0) z2_arrive(&dempty[d]);  // this warp is done with the task's table
+      }
+    }
+  }
+  if (!PERS && KS > 1 && warp == F::NWC) {
+    // the producer warp takes part in both cluster barriers
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  }
+  if (trow && tid == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    trow[4] = z2_gtimer();
+    trow[5] = ((unsigned long long)seq << 40) | ((unsigned long long)smid << 32) | blockIdx.x;
+  }
+}
+
 // The whole BSP apply for R right-hand sides (or on the shared class maps) as
 // one persistent dataflow launch; see k_bsp_fused for the protocol.
 __global__ void __launch_bounds__(THREADS) k_zmma_fused(FusedMmaArgs a) {
@@ -573,31 +1035,76 @@ bool zgemm_dmma(cudaStream_t st, int M, int N, int K, double2 alpha, const doubl
 
 constexpr size_t kZmmaSmem = sizeof(double2) * STAGES * kStageElems;
 
+// k_zmma2 instantiations: (BN, TM, TN, n-major B, stages, persistent).
+// 64-column tasks (steps with >= 1 task per SM): persistent, one CTA per SM;
+// 32-column tasks (smaller steps): one task per CTA (one per SM: 4-stage ring,
+// two warp groups splitting each chunk's k range), cluster split-K.
+using Z2Slab64 = Z2<64, 2, 2, false, 3, true>;
+using Z2Slab32 = Z2<32, 2, 2, false, 4, false, 2>;
+using Z2Cols64 = Z2<64, 2, 2, true, 3, true>;
+using Z2Cols32 = Z2<32, 2, 2, true, 4, false, 2>;
+#define Z2K_SLAB64 k_zmma2<64, 2, 2, false, 3, true, 1>
+#define Z2K_SLAB32 k_zmma2<32, 2, 2, false, 4, false, 2>
+#define Z2K_COLS64 k_zmma2<64, 2, 2, true, 3, true, 1>
+#define Z2K_COLS32 k_zmma2<32, 2, 2, true, 4, false, 2>
+
 void launch_zmma(Ctx& c, const DevMma& m, const double2* A, const double2* srcA, const double2* srcB,
-                 const Epi& e, int R) {
+                 const double2* zeros, const Epi& e, int R) {
   if (m.ntasks == 0) return;
-  // split K over a cluster when the step has too few tasks to fill the GPU
-  const int minK = m.minK;
-  int KS = 1;
-  static int ks_max = getenv("HS_ZMMA_KS") ? atoi(getenv("HS_ZMMA_KS")) : 4;
-  static int min_chunks = getenv("HS_ZMMA_MINCH") ? atoi(getenv("HS_ZMMA_MINCH")) : 4;
-  while (KS < ks_max && (long long)m.ntasks * KS < 2LL * c.num_sms && minK / KC >= 2 * KS * min_chunks / 2) KS *= 2;
-  c.launches++;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(m.ntasks * KS);
-  cfg.blockDim = dim3(THREADS);
-  cfg.dynamicSmemBytes = kZmmaSmem;
-  cfg.stream = c.stream;
   static const bool pdl = !(getenv("HS_ZMMA_PDL") && atoi(getenv("HS_ZMMA_PDL")) == 0);
+  cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = KS;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap with the previous step's tail
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 2 : 1;
+  cfg.stream = c.stream;
+  c.launches++;
+  if (m.kind != 0) {
+    int KS = 1;
+    if (m.bn == 64) {
+      cfg.gridDim = dim3(std::min(m.ntasks, c.num_sms));
+    } else {
+      // split K over a cluster while the step's tasks leave SMs idle and every
+      // rank keeps >= 2 chunks (HS_ZMMA2_KS caps the cluster size)
+      static const int ks_cap = getenv("HS_ZMMA2_KS") ? atoi(getenv("HS_ZMMA2_KS")) : 8;
+      while (KS < ks_cap && (long long)m.ntasks * KS * 2 <= c.num_sms && m.minK / Z2KC >= 4 * KS) KS *= 2;
+      cfg.gridDim = dim3(m.ntasks * KS);
+    }
+    attr[0].val.clusterDim.x = KS;
+    unsigned long long* tr = nullptr;
+    const int seq = (int)(c.launches & 0xFFFFFF);
+    if (c.trace_on && c.trace && (size_t)c.trace_rows + cfg.gridDim.x <= c.trace_cap) {
+      tr = c.trace + 6ull * c.trace_rows;
+      c.trace_rows += (int)cfg.gridDim.x;
+    }
+#define Z2_LAUNCH(F, K)                                                                                         \
+  do {                                                                                                          \
+    cfg.blockDim = dim3(F::THREADS);                                                                            \
+    cfg.dynamicSmemBytes = F::SMEM;                                                                             \
+    cudaLaunchKernelEx(&cfg, K, (const MmaTask*)m.tasks, m.ntasks, (const MmaCol*)m.cols, A, srcA, srcB, zeros, \
+                       e, c.n, R, KS, tr, seq);                                                                 \
+  } while (0)
+    if (m.kind == 2 && m.bn == 64) Z2_LAUNCH(Z2Cols64, Z2K_COLS64);
+    else if (m.kind == 2) Z2_LAUNCH(Z2Cols32, Z2K_COLS32);
+    else if (m.bn == 64) Z2_LAUNCH(Z2Slab64, Z2K_SLAB64);
+    else Z2_LAUNCH(Z2Slab32, Z2K_SLAB32);
+#undef Z2_LAUNCH
+    return;
+  }
+  // split K over a cluster when the step has too few tasks to fill the GPU
+  const int minK = m.minK;
+  int KS = 1;
+  static int ks_max = getenv("HS_ZMMA_KS") ? atoi(getenv("HS_ZMMA_KS")) : 4;
+  static int min_chunks = getenv("HS_ZMMA_MINCH") ? atoi(getenv("HS_ZMMA_MINCH")) : 4;
+  while (KS < ks_max && (long long)m.ntasks * KS < 2LL * c.num_sms && minK / KC >= 2 * KS * min_chunks / 2) KS *= 2;
+  attr[0].val.clusterDim.x = KS;
+  cfg.gridDim = dim3(m.ntasks * KS);
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = kZmmaSmem;
   cudaLaunchKernelEx(&cfg, k_zmma, (const MmaTask*)m.tasks, (const MmaCol*)m.cols, A, srcA, srcB, e,
                      c.n, R, KS);
 }
@@ -652,6 +1159,10 @@ cudaError_t set_zmma_smem_limit() {
   cudaFuncSetAttribute(k_zmma_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kZmmaSmem);
   cudaFuncSetAttribute(k_zmma_fused_ks<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kZmmaSmem);
   cudaFuncSetAttribute(k_zmma_fused_ks<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kZmmaSmem);
+  cudaFuncSetAttribute(Z2K_SLAB64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Slab64::SMEM);
+  cudaFuncSetAttribute(Z2K_SLAB32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Slab32::SMEM);
+  cudaFuncSetAttribute(Z2K_COLS64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cols64::SMEM);
+  cudaFuncSetAttribute(Z2K_COLS32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cols32::SMEM);
   return cudaFuncSetAttribute(k_zmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kZmmaSmem);
 }
 

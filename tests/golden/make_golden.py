@@ -3,7 +3,8 @@
     PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py [--cfg3]
     python tests/golden/make_golden.py --check-cfg3   # shared-factor harness == cfg3 golden, bitwise
     python tests/golden/make_golden.py --cfg2-sweep   # cfg2 block counts p = 1, 2, 4, 8
-    python tests/golden/make_golden.py --cfg5         # headline config, ~1 h on 8 cores
+    python tests/golden/make_golden.py --cfg5         # headline config, ~32 min on 8 cores
+    python tests/golden/make_golden.py --cfg5-acc     # add the accurate-oracle terms to cfg5.npz
 
 Writes tests/golden/*.npz.  What is pinned:
   * lattice.npz   : m-order pair tables and reference windows for several lattices
@@ -247,15 +248,47 @@ def cfg5_fixture(workers):
     np.savez(os.path.join(HERE, "cfg5_partial.npz"), **out)
     _gmres_record(adap, out["b"], 8, 1e-6, out)
     adap.close()
-    prob, lat = oracle_from(c)
-    itf = Interface(prob, lat, backend="schur")
-    acc = gmres(itf.apply_A, Preconditioner(itf, "bsp", blocks=8), out["b"], tol=1e-6, maxit=1000)
-    out["acc_iters"] = acc.iterations
-    out["acc_dx"] = (acc.x - out["gm_x"]).astype(np.complex64)
     out["workers"] = adap.workers
+    out.update(cfg5_accurate_terms(out))
     np.savez_compressed(os.path.join(HERE, "cfg5.npz"), **out)
     os.remove(os.path.join(HERE, "cfg5_partial.npz"))
-    print(f"cfg5: done in {time.time() - t0:.1f}s; accurate oracle {acc.iterations} it", flush=True)
+    print(f"cfg5: done in {time.time() - t0:.1f}s; accurate oracle {int(out['acc_iters'])} it", flush=True)
+
+
+def cfg5_accurate_terms(G):
+    """The accurate (Dirichlet-eliminated Schur map) oracle on the golden's own
+    inputs, stored as complex64 differences from the reference values (the
+    differences are ~1e-10..1e-8 of the values, so complex64 keeps them to
+    ~1e-17 absolute): b, (I-S) g, BSP z and the GMRES solution from the
+    reference's b."""
+    from oracle import Interface
+    from oracle.schur import lifting_traces
+    c = CONFIGS[5]
+    prob, lat = oracle_from(c)
+    itf = Interface(prob, lat, backend="schur")
+    L = itf.size
+    home, tr = lifting_traces(prob, lat)
+    b = np.zeros(L, complex)
+    for f, j in lat.faces[home]:
+        m = lat.m_index(j, home)
+        b[(m - 1) * prob.n:m * prob.n] = tr[f]
+    out = {"acc_db": (b - G["b"]).astype(np.complex64),
+           "acc_dAg": (itf.apply_A(rng_vec(int(G["seed_g"]), L)) - G["Ag"]).astype(np.complex64),
+           "acc_dbsp": (Preconditioner(itf, "bsp", blocks=8)(rng_vec(int(G["seed_r"]), L)) - G["M_bsp8"]).astype(
+               np.complex64)}
+    acc = gmres(itf.apply_A, Preconditioner(itf, "bsp", blocks=8), G["b"], tol=1e-6, maxit=1000)
+    out["acc_iters"] = acc.iterations
+    out["acc_dx"] = (acc.x - G["gm_x"]).astype(np.complex64)
+    out["acc_hist"] = np.array(acc.history)
+    return out
+
+
+def cfg5_add_accurate():
+    """Add the accurate-oracle terms to an existing cfg5.npz (no reference rerun)."""
+    G = dict(np.load(os.path.join(HERE, "cfg5.npz")))
+    G.update(cfg5_accurate_terms(G))
+    np.savez_compressed(os.path.join(HERE, "cfg5.npz"), **G)
+    print("cfg5: accurate-oracle terms added", int(G["acc_iters"]), "it", flush=True)
 
 
 def oracle_from(c):
@@ -273,10 +306,11 @@ def main():
     ap.add_argument("--check-cfg3", action="store_true")
     ap.add_argument("--cfg2-sweep", action="store_true")
     ap.add_argument("--cfg5", action="store_true")
+    ap.add_argument("--cfg5-acc", action="store_true", help="add the accurate-oracle terms to cfg5.npz")
     ap.add_argument("--workers", type=int, default=None)
     ap.add_argument("--only", default=None)
     a = ap.parse_args()
-    if a.check_cfg3 or a.cfg2_sweep or a.cfg5:
+    if a.check_cfg3 or a.cfg2_sweep or a.cfg5 or a.cfg5_acc:
         sys.path.insert(0, HERE)
         if a.check_cfg3:
             check_cfg3(a.workers)
@@ -284,6 +318,8 @@ def main():
             cfg2_sweep(a.workers)
         if a.cfg5:
             cfg5_fixture(a.workers)
+        if a.cfg5_acc:
+            cfg5_add_accurate()
         return
     if a.only in (None, "lattice"):
         lattice_fixture()

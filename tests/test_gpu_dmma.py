@@ -36,14 +36,16 @@ def system(k, maps):
     return _S[key]
 
 
-@pytest.mark.parametrize("k", [1, 2])
-def test_multi_rhs_dmma_equals_single(k):
+@pytest.mark.parametrize("k,R", [(1, 40), (2, 40), (2, 16), (2, 64), (2, 100), (2, 128)])
+def test_multi_rhs_dmma_equals_single(k, R):
+    """R <= 32: 32-column tasks; R > 32: 64-column tasks (k_zmma2), partial
+    last chunks for R = 40, 100."""
     s = system(k, "subdomain")
     L = s.layout.size
-    X = cvec(3, L, 40)  # 40: a full and a partial 32-column chunk
+    X = cvec(3, L, R)
     Y = s.apply_interface_operator(X)
     Z = s.bsp_apply(X)
-    for r in (0, 17, 31, 32, 39):
+    for r in sorted({0, R // 2, 31 % R, min(32, R - 1), R - 1}):
         x = np.ascontiguousarray(X[:, r])
         assert relerr(Y[:, r], s.apply_interface_operator(x)) < 1e-14
         assert relerr(Z[:, r], s.bsp_apply(x)) < 1e-13
@@ -80,12 +82,22 @@ def test_shared_mode_vs_reference_golden_cfg2():
     assert relerr(res.solution, G["gm_x"]) < 1e-8
 
 
-def test_shared_mode_cfg5_gmres():
+def test_shared_mode_cfg5_vs_reference_golden():
+    """Shared class maps + DMMA at the headline config against the reference
+    golden (tests/golden/cfg5.npz) and the accurate oracle (see
+    test_gpu_scale.test_cfg5_vs_reference_golden for the floors)."""
+    G = golden("cfg5")
     s = system(5, "shared")
-    b = s.rhs()
-    res = s.gmres(b, "bsp", tol=1e-6, maxit=1000)
-    assert res.converged and 100 <= res.iterations <= 115
-    assert relerr(s.apply_interface_operator(res.solution), b) < 1e-6
+    L = s.layout.size
+    r = cvec(int(G["seed_r"]), L)
+    z = s.bsp_apply(r)
+    assert relerr(z, G["M_bsp8"]) < 2e-9
+    assert relerr(z, G["M_bsp8"] + G["acc_dbsp"]) < 1e-12
+    res = s.gmres(G["b"], "bsp", tol=1e-6, maxit=1000)
+    assert res.converged and abs(res.iterations - int(G["gm_iters"])) <= 1, res.iterations
+    assert relerr(res.solution, G["gm_x"]) < 1e-8
+    assert relerr(res.solution, G["gm_x"] + G["acc_dx"]) < 1e-11
+    assert relerr(s.apply_interface_operator(res.solution), G["b"]) < 1e-6
 
 
 def test_shared_mode_needs_n_multiple_of_32():

@@ -181,3 +181,17 @@ def test_cfg3_shared_factor_record():
     for k in ("b", "Ag", "M_bsp4", "gm_x", "gm_hist"):
         assert rep[k]["bitwise_equal"] and rep[k]["max_abs_diff"] == 0.0, k
     assert rep["gm_iters"]["golden"] == rep["gm_iters"]["shared"] == 67
+
+
+def test_cfg5_golden_reference_vs_accurate_oracle():
+    """The cfg5 golden (reference arithmetic, shared SuperLU factors) and the
+    accurate oracle's values on the same inputs agree within the reference's
+    scatterer-subdomain floor: same iteration count, x within
+    the north_star bar of 1e-8."""
+    G = golden("cfg5")
+    assert int(G["gm_iters"]) == int(G["acc_iters"]) == 107
+    x = G["gm_x"]
+    assert np.linalg.norm(G["acc_dx"]) / np.linalg.norm(x) < 5e-9
+    assert np.linalg.norm(G["acc_dAg"]) / np.linalg.norm(G["Ag"]) < 1e-9
+    assert np.linalg.norm(G["acc_dbsp"]) / np.linalg.norm(G["M_bsp8"]) < 2e-9
+    assert G["gm_hist"][-1] <= 1e-6 * G["gm_hist"][0] < G["gm_hist"][-2]
