@@ -233,6 +233,12 @@ int hs_schedule(const hs_ctx* ctx, int kind, int32_t* rec, int cap, int* count);
 int hs_exchange_plan(const hs_ctx* ctx, int kind, int peer, int recv, int32_t* triples, int cap,
                      int* count);
 
+/* The Arnoldi basis of the last hs_gmres call on this context: the first
+ * ncols basis vectors V[:, 0..ncols) as complex128, column after column, each
+ * L x R ([L][R] layout); *avail = vectors built (max iterations + 1).  out =
+ * NULL returns *avail only.  (max |V^H V - I| <= 1e-10; tests.) */
+int hs_gmres_basis(hs_ctx* ctx, double* out, int ncols, int* avail);
+
 /* Compact Schur map of subdomain (i1,i2) as a dense (k n) x (k n) complex
  * matrix, row-major (after hs_factor). */
 int hs_get_schur(hs_ctx* ctx, int i1, int i2, double* T);

@@ -29,6 +29,7 @@ class GmresOut:
     converged: bool
     history: list = field(default_factory=list)
     breakdown: bool = False
+    basis: list = field(default_factory=list)  # the Arnoldi vectors v_0 .. v_{iterations-1}
 
 
 def givens(a: complex, b: float):
@@ -86,4 +87,4 @@ def gmres(apply_A, apply_M, b, tol: float = 1e-6, maxit: int = 200) -> GmresOut:
         y[i] = (g[i] - H[i, i + 1:m] @ y[i + 1:m]) / H[i, i]
     u = sum(y[i] * V[i] for i in range(m))
     x = apply_M(u) if apply_M is not None else u
-    return GmresOut(np.asarray(x), m, conv, hist, brk)
+    return GmresOut(np.asarray(x), m, conv, hist, brk, V[:m])

@@ -2310,6 +2310,23 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
     if (iters) iters[r] = hi[R + r];
     if (converged) converged[r] = hi[2 * R + r];
   }
+  int itmax = 0;  // the basis of the reported iterations (a look-ahead step may have built one more)
+  for (int r = 0; r < R; ++r) itmax = std::max(itmax, hi[R + r]);
+  c->gm_basis = itmax > 0 ? std::min(kdone, itmax) + 1 : 0;
+  c->gm_LR = LR;
+  return 0;
+}
+
+int hs_gmres_basis(hs_ctx* c, double* out, int ncols, int* avail) {
+  if (!c || !avail) return fail(c, 1, "null argument");
+  DEV_SCOPE(c);
+  *avail = c->gm_basis;
+  if (!out) return 0;
+  if (ncols < 0 || ncols > c->gm_basis) return fail(c, 1, "ncols exceeds the basis of the last GMRES solve");
+  auto it = c->ws.find("V");
+  if (it == c->ws.end() || it->second.cap < (size_t)ncols * c->gm_LR) return fail(c, 1, "no GMRES basis");
+  CK(cudaStreamSynchronize(c->stream));
+  CK(cudaMemcpy(out, it->second.p, (size_t)ncols * c->gm_LR * sizeof(double2), cudaMemcpyDeviceToHost));
   return 0;
 }
 

@@ -336,6 +336,8 @@ struct Ctx {
   double2* recv_up = nullptr; double2* recv_dn = nullptr;
   size_t xbuf_cap = 0;
   void* nccl = nullptr;  // ncclComm_t
+  int gm_basis = 0;      // basis vectors built by the last hs_gmres (hs_gmres_basis)
+  long long gm_LR = 0;   // their length
   int gmres_mode = 0;    // 0 auto (cooperative MGS on one rank), 1 host-driven MGS over owned blocks
   int* h_flags = nullptr;             // pinned: GMRES active counts (2 slots)
   cudaEvent_t flag_ev[2] = {nullptr, nullptr};

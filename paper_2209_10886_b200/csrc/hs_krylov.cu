@@ -392,7 +392,7 @@ __global__ void k_combine(GmresDev G, int mmax, double2* u) {
 
 // k_mgs1 partials [2][6][kMgs1MaxGrid] followed by the grid-barrier counter
 // shared by k_mgs and k_mgs1 (same stream: launches never overlap).
-static constexpr int kGridScratch = 2 * 6 * 256 + 16;  // doubles
+static constexpr int kGridScratch = 2 * 20 * 256 + 16;  // doubles: k_mgs1 partials [2][20][256] + barrier counter
 cudaError_t ensure_grid_scratch(Ctx& c) {
   if (c.mgs1_slots) return cudaSuccess;
   cudaError_t e = cudaMalloc((void**)&c.mgs1_slots, (size_t)kGridScratch * sizeof(double));
@@ -400,7 +400,7 @@ cudaError_t ensure_grid_scratch(Ctx& c) {
   c.mgs1_bar = 0;
   return e;
 }
-static unsigned* grid_bar(Ctx& c) { return (unsigned*)(c.mgs1_slots + 2 * 6 * 256); }
+static unsigned* grid_bar(Ctx& c) { return (unsigned*)(c.mgs1_slots + 2 * 20 * 256); }
 
 static int pow2_floor(int x) {
   int p = 1;
@@ -793,18 +793,24 @@ static __device__ __forceinline__ void warp_sum3(double& a, double& b, double& c
   }
 }
 
-constexpr int kMgs1MaxGrid = 256;   // partials: [2 parities][6 components][kMgs1MaxGrid]
-constexpr int kMgs1Comp = 6;
+constexpr int kMgs1MaxGrid = 256;   // partials: [2 parities][kMgs1Comp components][kMgs1MaxGrid]
+constexpr int kMgs1MaxM = 4;        // MGS steps per grid barrier (blocks of M basis vectors)
+constexpr int kMgs1Comp = 2 * kMgs1MaxM + kMgs1MaxM * (kMgs1MaxM - 1);  // alpha (M complex) + gamma (M(M-1)/2 complex)
 static_assert(kGridScratch == 2 * kMgs1Comp * kMgs1MaxGrid + 16, "grid scratch layout");
 constexpr int kMgs1MaxBlock = 896;  // 72 registers per thread
 
-template <int E>
+template <int E, int M>
 __global__ void __launch_bounds__(kMgs1MaxBlock, 1) k_mgs1(GmresDev G, int k, int chunk, int nbuf, double* slots, unsigned* bar, unsigned bar_base) {
+  // M MGS steps per grid barrier (compile time: the block arrays stay in
+  // registers); nbuf = 2 M slices (the pending block and the next one), or
+  // 2 / 3 slices for M = 1
+  constexpr int NCM = M >= 2 ? 2 * M + M * (M - 1) : 3;  // components per barrier
+  static_assert(M == 1 || M == 2 || M == 4, "block size");
   extern __shared__ __align__(16) double2 sm1[];
   __shared__ double red[32][kMgs1Comp];
   __shared__ double red2[kMgs1Comp];
   const int BD = blockDim.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = BD >> 5;
-  auto buf = [&](int j) { return sm1 + (size_t)(j % nbuf) * chunk; };  // v_j (nbuf = 2, 3 or 4 slices)
+  auto buf = [&](int j) { return sm1 + (size_t)(j % nbuf) * chunk; };  // v_j (nbuf slices)
   double2* hs = sm1 + (size_t)nbuf * chunk;  // k + 2: the column (CTA 0)
   double2* sns = hs + (k + 2);     // k
   double* css = (double*)(sns + k);  // k
@@ -812,7 +818,6 @@ __global__ void __launch_bounds__(kMgs1MaxBlock, 1) k_mgs1(GmresDev G, int k, in
   const long long e0 = (long long)blockIdx.x * chunk;
   const long long eend = min(e0 + (long long)chunk, LR);
   const int nblk = gridDim.x;
-  const bool pairs = nbuf == 4;  // two MGS steps per grid barrier
   double2* w = G.V + (long long)(k + 1) * LR;
   double2 wr[E];
 #pragma unroll
@@ -831,72 +836,68 @@ __global__ void __launch_bounds__(kMgs1MaxBlock, 1) k_mgs1(GmresDev G, int k, in
     cpa_commit();
   };
   int step = 0;
-  // block sum, publish, grid barrier, collect: x[0..5] summed over the grid in
-  // a fixed order, returned identically to every thread of every CTA.
-  // Partials are stored component-major so the collecting warp's loads are
+  // block sum, publish, grid barrier, collect: x[0..nc) summed over the grid
+  // in a fixed order, returned identically to every thread of every CTA.
+  // Partials are stored component-major so the collecting warps' loads are
   // fully coalesced (a CTA-major layout is 3.5x slower: 7 vs 2 us per step,
-  // tools/allreduce_bench.cu).  pf0 / pf1 >= 0: basis vectors to prefetch.
-  auto reduce = [&](double (&x)[kMgs1Comp], int pf0, int pf1) {
+  // tools/allreduce_bench.cu).  Basis vectors [pf, pf + npf) are prefetched
+  // while the CTA waits at the barrier.
+  auto reduce = [&](double (&x)[NCM], int nc, int pf, int npf) {
     double* P = slots + (size_t)(step & 1) * kMgs1Comp * kMgs1MaxGrid;
-    warp_sum3(x[0], x[1], x[2]);
-    warp_sum3(x[3], x[4], x[5]);
+#pragma unroll
+    for (int q = 0; q < NCM; ++q)
+      if (q < nc)
+#pragma unroll
+        for (int o = 16; o; o >>= 1) x[q] += __shfl_xor_sync(0xffffffffu, x[q], o);
     if (lane == 0)
 #pragma unroll
-      for (int q = 0; q < kMgs1Comp; ++q) red[wid][q] = x[q];
+      for (int q = 0; q < NCM; ++q)
+        if (q < nc) red[wid][q] = x[q];
     __syncthreads();
-    if (wid == 0) {
+    for (int q = wid; q < nc; q += nw) {  // warp q: component q over the CTA's warps
+      double v = lane < nw ? red[lane][q] : 0.0;
 #pragma unroll
-      for (int q = 0; q < kMgs1Comp; ++q) x[q] = lane < nw ? red[lane][q] : 0.0;
-      warp_sum3(x[0], x[1], x[2]);
-      warp_sum3(x[3], x[4], x[5]);
-      if (lane == 0)
-#pragma unroll
-        for (int q = 0; q < kMgs1Comp; ++q) P[q * kMgs1MaxGrid + blockIdx.x] = x[q];
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) P[q * kMgs1MaxGrid + blockIdx.x] = v;
     }
     // a basis vector issued here streams while the CTA waits at the barrier;
     // issued after the barrier its loads would queue ahead of the partials
-    if (pf0 >= 0) prefetch(pf0);
-    if (pf1 >= 0) prefetch(pf1);
+    for (int j = pf; j < pf + npf; ++j) prefetch(j);
     grid_barrier(bar, bar_base + (unsigned)(step + 1) * (unsigned)nblk);
-    if (wid == 0) {
-      const int nc = pairs ? kMgs1Comp : 3;  // one step per barrier publishes 3 components
+    for (int q = wid; q < nc; q += nw) {  // warp q collects component q (fixed order)
+      double xs[kMgs1MaxGrid / 32];
 #pragma unroll
-      for (int q = 0; q < kMgs1Comp; ++q) {
-        if (q >= nc) {
-          x[q] = 0.0;
-          continue;
-        }
-        double xs[kMgs1MaxGrid / 32];
-#pragma unroll
-        for (int u = 0; u < kMgs1MaxGrid / 32; ++u) {
-          const int t = lane + 32 * u;
-          xs[u] = t < nblk ? __ldcg(P + q * kMgs1MaxGrid + t) : 0.0;
-        }
-        double a = 0.0;
-#pragma unroll
-        for (int u = 0; u < kMgs1MaxGrid / 32; ++u) a += xs[u];
-        x[q] = a;
+      for (int u = 0; u < kMgs1MaxGrid / 32; ++u) {
+        const int t = lane + 32 * u;
+        xs[u] = t < nblk ? __ldcg(P + q * kMgs1MaxGrid + t) : 0.0;
       }
-      warp_sum3(x[0], x[1], x[2]);
-      warp_sum3(x[3], x[4], x[5]);
-      if (lane == 0)
+      double v = 0.0;
 #pragma unroll
-        for (int q = 0; q < kMgs1Comp; ++q) red2[q] = x[q];
+      for (int u = 0; u < kMgs1MaxGrid / 32; ++u) v += xs[u];
+#pragma unroll
+      for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0) red2[q] = v;
     }
     __syncthreads();
     ++step;
 #pragma unroll
-    for (int q = 0; q < kMgs1Comp; ++q) x[q] = red2[q];
+    for (int q = 0; q < NCM; ++q) x[q] = q < nc ? red2[q] : 0.0;
   };
-  double x[kMgs1Comp];
-  // initial lead: v_0..v_{nbuf-1} (pairs: v_0..v_2, each pass then fetches the pair after next)
-  const int lead = pairs ? 3 : nbuf;
+  double x[NCM];
+  // initial lead: v_0 and the first block v_1..v_M (one step per barrier: v_0..v_{nbuf-1})
+  const int lead = M >= 2 ? M + 1 : nbuf;
   for (int j = 0; j < lead && j <= k; ++j) prefetch(j);
   if (blockIdx.x == 0)
     for (int j = tid; j < k; j += BD) { css[j] = G.cs[j]; sns[j] = G.sn[j]; }
   {  // v_0 landed: the groups issued after it may still be in flight
     const int later = min(lead, k + 1) - 1;
-    if (later >= 2) cpa_wait<2>(); else if (later == 1) cpa_wait<1>(); else cpa_wait<0>();
+    switch (later >= 4 ? 4 : later) {
+      case 4: cpa_wait<4>(); break;
+      case 3: cpa_wait<3>(); break;
+      case 2: cpa_wait<2>(); break;
+      case 1: cpa_wait<1>(); break;
+      default: cpa_wait<0>(); break;
+    }
   }
   // j = 0: <v_0, w> and ||w||^2 before orthogonalisation
   {
@@ -909,8 +910,10 @@ __global__ void __launch_bounds__(kMgs1MaxBlock, 1) k_mgs1(GmresDev G, int k, in
         cfma_conj(acc, v0[tid + i * BD], wr[i]);
         nrm += wr[i].x * wr[i].x + wr[i].y * wr[i].y;
       }
-    x[0] = acc.x; x[1] = acc.y; x[2] = nrm; x[3] = x[4] = x[5] = 0.0;
-    reduce(x, -1, -1);
+#pragma unroll
+    for (int q = 0; q < NCM; ++q) x[q] = 0.0;
+    x[0] = acc.x; x[1] = acc.y; x[2] = nrm;
+    reduce(x, 3, 0, 0);
   }
   double2 h = make_double2(x[0], x[1]);
   if (blockIdx.x == 0 && tid == 0) {
@@ -918,57 +921,88 @@ __global__ void __launch_bounds__(kMgs1MaxBlock, 1) k_mgs1(GmresDev G, int k, in
     hs[0] = h;
   }
   double hn2 = 0;
-  if (pairs) {
-    // Two MGS steps per barrier.  With the pending update w -= h_p v_p (p =
-    // the previous pair) applied, one pass forms alpha = <v_a, w>, beta =
-    // <v_b, w> and gamma = <v_b, v_a> for the next pair (a, b = a + 1); then
-    // h_a = alpha and h_b = <v_b, w - h_a v_a> = beta - h_a gamma, exactly
-    // the MGS coefficients (rounding differs only at the 1e-16 level).
-    int p0 = 0, p1 = -1;
-    double2 hp0 = h, hp1 = make_double2(0, 0);
-    for (int a = 1;; a += 2) {
-      const int bb = a + 1;
-      const bool ha = a <= k, hb = bb <= k;
-      cpa_wait<0>();  // v_a, v_b (issued before the previous barrier)
-      const double2* vp0 = buf(p0);
-      const double2* vp1 = p1 >= 0 ? buf(p1) : vp0;
-      const double2* va = buf(a);
-      const double2* vb = buf(bb);
-      double2 al = make_double2(0, 0), be = al, ga = al;
+  if constexpr (M >= 2) {
+    // M MGS steps per barrier.  With the pending update w -= sum_p h_p v_p
+    // (the previous block) applied, one pass forms alpha_q = <v_{a+q}, w> and
+    // gamma_qr = <v_{a+q}, v_{a+r}> (r < q) for the next block; then
+    //   h_{a+q} = <v_{a+q}, w - sum_{r<q} h_{a+r} v_{a+r}> = alpha_q - sum_{r<q} h_{a+r} gamma_qr,
+    // exactly the MGS coefficients (rounding differs at the 1e-16 level).  The
+    // last pass (no vectors left) applies the final update and forms ||w||^2.
+    int pb0 = 0, pbn = 1;
+    double2 hp[M];
+    hp[0] = h;
+#pragma unroll
+    for (int q = 1; q < M; ++q) hp[q] = make_double2(0, 0);
+    for (int a = 1;; a += M) {
+      const int mb = max(0, min(M, k + 1 - a));
+      cpa_wait<0>();  // the block (issued before the previous barrier)
+      double2 al[M], ga[M * (M - 1) / 2];
+#pragma unroll
+      for (int q = 0; q < M; ++q) al[q] = make_double2(0, 0);
+#pragma unroll
+      for (int q = 0; q < M * (M - 1) / 2; ++q) ga[q] = make_double2(0, 0);
       double nrm = 0;
 #pragma unroll
       for (int i = 0; i < E; ++i)
         if (e0 + tid + (long long)i * BD < eend) {
           const int o = tid + i * BD;
-          wr[i] = csub(wr[i], cmul(hp0, vp0[o]));
-          if (p1 >= 0) wr[i] = csub(wr[i], cmul(hp1, vp1[o]));
-          if (ha) {
-            const double2 xa = va[o];
-            cfma_conj(al, xa, wr[i]);
-            if (hb) {
-              const double2 xb = vb[o];
-              cfma_conj(be, xb, wr[i]);
-              cfma_conj(ga, xb, xa);
-            }
+#pragma unroll
+          for (int p = 0; p < M; ++p)
+            if (p < pbn) wr[i] = csub(wr[i], cmul(hp[p], buf(pb0 + p)[o]));
+          if (mb > 0) {
+            double2 xv[M];
+#pragma unroll
+            for (int q = 0; q < M; ++q) xv[q] = q < mb ? buf(a + q)[o] : make_double2(0, 0);
+#pragma unroll
+            for (int q = 0; q < M; ++q)
+              if (q < mb) cfma_conj(al[q], xv[q], wr[i]);
+#pragma unroll
+            for (int q = 1; q < M; ++q)
+#pragma unroll
+              for (int r = 0; r < q; ++r)
+                if (q < mb) cfma_conj(ga[q * (q - 1) / 2 + r], xv[q], xv[r]);
           } else {
             nrm += wr[i].x * wr[i].x + wr[i].y * wr[i].y;
           }
         }
-      x[0] = al.x; x[1] = al.y; x[2] = ha ? be.x : nrm; x[3] = be.y; x[4] = ga.x; x[5] = ga.y;
-      // the pending pair's slices are free: the pair after (a, b) goes into them
-      reduce(x, bb + 1 <= k ? bb + 1 : -1, bb + 2 <= k ? bb + 2 : -1);
-      if (!ha) {
-        hn2 = x[2];
+      int nc;
+      if (mb > 0) {
+#pragma unroll
+        for (int q = 0; q < M; ++q) x[2 * q] = al[q].x, x[2 * q + 1] = al[q].y;
+#pragma unroll
+        for (int q = 0; q < M * (M - 1) / 2; ++q)
+          x[2 * M + 2 * q] = ga[q].x, x[2 * M + 2 * q + 1] = ga[q].y;
+        nc = NCM;
+      } else {
+#pragma unroll
+        for (int q = 0; q < NCM; ++q) x[q] = 0.0;
+        x[0] = nrm;
+        nc = 1;
+      }
+      // the pending block's slices are free: the block after (a..) goes into them
+      const int pf = a + M, npf = max(0, min(M, k + 1 - pf));
+      reduce(x, nc, pf, npf);
+      if (mb == 0) {
+        hn2 = x[0];
         break;
       }
-      const double2 h_a = make_double2(x[0], x[1]);
-      const double2 h_b = csub(make_double2(x[2], x[3]), cmul(h_a, make_double2(x[4], x[5])));
-      if (blockIdx.x == 0 && tid == 0) {
-        hs[a] = h_a;
-        if (hb) hs[bb] = h_b;
+      double2 hb[M];
+#pragma unroll
+      for (int q = 0; q < M; ++q) {
+        double2 v = make_double2(x[2 * q], x[2 * q + 1]);
+#pragma unroll
+        for (int r = 0; r < q; ++r) {
+          const int g = 2 * M + 2 * (q * (q - 1) / 2 + r);
+          v = csub(v, cmul(hb[r], make_double2(x[g], x[g + 1])));
+        }
+        hb[q] = q < mb ? v : make_double2(0, 0);
       }
-      p0 = a; hp0 = h_a;
-      p1 = hb ? bb : -1; hp1 = h_b;
+      if (blockIdx.x == 0 && tid == 0)
+        for (int q = 0; q < mb; ++q) hs[a + q] = hb[q];
+      pb0 = a;
+      pbn = mb;
+#pragma unroll
+      for (int q = 0; q < M; ++q) hp[q] = hb[q];
     }
   } else {
     for (int j = 0; j <= k; ++j) {
@@ -988,8 +1022,10 @@ __global__ void __launch_bounds__(kMgs1MaxBlock, 1) k_mgs1(GmresDev G, int k, in
           else nrm += wr[i].x * wr[i].x + wr[i].y * wr[i].y;
         }
       // v_j's slice is free: the vector nbuf steps ahead goes into it
-      x[0] = acc.x; x[1] = acc.y; x[2] = nrm; x[3] = x[4] = x[5] = 0.0;
-      reduce(x, j + nbuf <= k ? j + nbuf : -1, -1);
+#pragma unroll
+      for (int q = 0; q < NCM; ++q) x[q] = 0.0;
+      x[0] = acc.x; x[1] = acc.y; x[2] = nrm;
+      reduce(x, 3, j + nbuf, j + nbuf <= k ? 1 : 0);
       if (more) {
         h = make_double2(x[0], x[1]);
         if (blockIdx.x == 0 && tid == 0) hs[j + 1] = h;
@@ -1040,7 +1076,9 @@ int gmres_mgs1_plan(Ctx& c, long long LR, int R, int maxit, int* chunk, int* E, 
 cudaError_t gmres_arnoldi1(Ctx& c, GmresDev& G, int k, int grid, int chunk, int E, int bd) {
   static cudaError_t attr = [] {
     cudaError_t e = cudaSuccess;
-    for (const void* f : {(const void*)k_mgs1<1>, (const void*)k_mgs1<2>, (const void*)k_mgs1<4>, (const void*)k_mgs1<8>})
+    for (const void* f : {(const void*)k_mgs1<1, 1>, (const void*)k_mgs1<2, 1>, (const void*)k_mgs1<4, 1>, (const void*)k_mgs1<8, 1>,
+                          (const void*)k_mgs1<1, 2>, (const void*)k_mgs1<2, 2>, (const void*)k_mgs1<4, 2>, (const void*)k_mgs1<8, 2>,
+                          (const void*)k_mgs1<1, 4>, (const void*)k_mgs1<2, 4>, (const void*)k_mgs1<4, 4>, (const void*)k_mgs1<8, 4>})
       if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMgs1SmemMax);
     return e;
   }();
@@ -1050,19 +1088,29 @@ cudaError_t gmres_arnoldi1(Ctx& c, GmresDev& G, int k, int grid, int chunk, int 
   double* slots = (double*)c.mgs1_slots;
   unsigned* bar = grid_bar(c);
   unsigned bar_base = c.mgs1_bar;  // counter value before this launch (wraps modulo 2^32)
-  // four basis slices: two MGS steps per grid barrier (the pending pair and the
-  // next one); else two slices, one step per barrier (three measured no faster)
-  static const bool pairs_ok = [] {
-    const char* e = getenv("HS_MGS1_PAIRS");
-    return !e || atoi(e) != 0;
+  // 2 M basis slices: M MGS steps per grid barrier (the pending block and the
+  // next one), M = 4 where the slices fit in shared memory (L <= ~250k), else
+  // 2; M = 1: two slices, one step per barrier (three measured no faster).
+  // HS_MGS1_BLOCK = 1 | 2 | 4 caps M (HS_MGS1_PAIRS=0: M = 1).
+  static const int mcap = [] {
+    const char* p = getenv("HS_MGS1_PAIRS");
+    if (p && atoi(p) == 0) return 1;
+    const char* e = getenv("HS_MGS1_BLOCK");
+    return e ? std::max(1, std::min(kMgs1MaxM, atoi(e))) : kMgs1MaxM;
   }();
-  int nbuf = pairs_ok && mgs1_smem(chunk, k, 4) <= kMgs1SmemMax ? 4 : 2;
-  const unsigned nbar = nbuf == 4 ? (unsigned)((k + 1) / 2 + 2) : (unsigned)(k + 2);
+  int M = 1;
+  for (int m = mcap; m >= 2; m /= 2)
+    if (mgs1_smem(chunk, k, 2 * m) <= kMgs1SmemMax) { M = m; break; }
+  int nbuf = M >= 2 ? 2 * M : 2;
+  const unsigned nbar = M >= 2 ? (unsigned)((k + M - 1) / M + 2) : (unsigned)(k + 2);
   c.mgs1_bar += nbar * (unsigned)grid;
   void* args[] = {(void*)&G, (void*)&k, (void*)&chunk, (void*)&nbuf, (void*)&slots, (void*)&bar, (void*)&bar_base};
   const size_t smem = mgs1_smem(chunk, k, nbuf);
-  const void* fn = E == 1 ? (const void*)k_mgs1<1> : E == 2 ? (const void*)k_mgs1<2>
-                 : E == 4 ? (const void*)k_mgs1<4> : (const void*)k_mgs1<8>;
+  static const void* fns[3][4] = {
+      {(const void*)k_mgs1<1, 1>, (const void*)k_mgs1<2, 1>, (const void*)k_mgs1<4, 1>, (const void*)k_mgs1<8, 1>},
+      {(const void*)k_mgs1<1, 2>, (const void*)k_mgs1<2, 2>, (const void*)k_mgs1<4, 2>, (const void*)k_mgs1<8, 2>},
+      {(const void*)k_mgs1<1, 4>, (const void*)k_mgs1<2, 4>, (const void*)k_mgs1<4, 4>, (const void*)k_mgs1<8, 4>}};
+  const void* fn = fns[M == 4 ? 2 : M == 2 ? 1 : 0][E == 1 ? 0 : E == 2 ? 1 : E == 4 ? 2 : 3];
   return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(bd), args, smem, c.stream);
 }
 

@@ -162,6 +162,8 @@ def gather_peer_handles(handle: bytes, rank: int, nranks: int) -> bytes:
 class GpuInterfaceSystem:
     """Subdomain Schur maps + matrix-free S on one GPU (or one row band)."""
 
+    _last_R = 1  # right-hand sides of the last gmres call (gmres_basis)
+
     def __init__(self, spec, partition: Partition, imp: ImpedanceSpec | None = None, workers: int = 1,
                  device: int = 0, rank: int = 0, nranks: int = 1, nccl_id: bytes | None = None,
                  sweep: SweepConfig | None = None, maps: str = "subdomain", fused: bool | int | str = True):
@@ -454,6 +456,7 @@ class GpuInterfaceSystem:
         v = _Vec(self.layout.check(b), self.layout.size)
         out, optr = v.empty()
         R = v.R
+        self._last_R = R
         iters = np.zeros(R, dtype=np.int32)
         conv = np.zeros(R, dtype=np.int32)
         hist = np.zeros((maxit + 1, R), dtype=np.float64)
@@ -466,6 +469,20 @@ class GpuInterfaceSystem:
             return GmresResult(v.wrap(out), h, int(iters[0]), bool(conv[0]), wall)
         return GmresResult(v.wrap(out), [list(hist[:iters[r] + 1, r]) for r in range(R)], iters.tolist(),
                            conv.astype(bool).tolist(), wall)
+
+
+    def gmres_basis(self, ncols: int | None = None) -> np.ndarray:
+        """The Arnoldi basis of the last gmres call, (L, ncols) complex128 for one
+        right-hand side ((L, R, ncols) for R): SPEC.md:412's orthonormality
+        invariant is checked on it (tests)."""
+        avail = C.c_int(0)
+        self.ctx.call("hs_gmres_basis", None, 0, C.byref(avail))
+        ncols = avail.value if ncols is None else int(ncols)
+        L = self.layout.size
+        out = np.empty(ncols * self._last_R * L, dtype=np.complex128)
+        self.ctx.call("hs_gmres_basis", C.c_void_p(out.ctypes.data), ncols, C.byref(avail))
+        V = out.reshape(ncols, L, self._last_R)
+        return V[:, :, 0].T.copy() if self._last_R == 1 else np.moveaxis(V, 0, -1).copy()
 
 
 InterfaceSystem = GpuInterfaceSystem
