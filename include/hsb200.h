@@ -213,6 +213,14 @@ int hs_map_once_plan(const hs_ctx* ctx, int which, int32_t* out, int cap, int* c
 int hs_set_trace(hs_ctx* ctx, int on);
 int hs_get_trace(hs_ctx* ctx, uint64_t* out, int cap, int* rows);
 
+/* Test hook of the peer-memory all-reduce that replaces ncclAllReduce for the
+ * sharded Arnoldi's inner products once hs_peer_open has mapped the ranks'
+ * regions (HS_PEER_ALLREDUCE=0 keeps NCCL): G ranks emulated by G co-resident
+ * CTAs on this GPU run `repeats` back-to-back reductions of `count` doubles
+ * (in/out: repeats x G x count, rank-major per reduction).  Every rank's
+ * result must be the rank-order sum, bitwise. */
+int hs_test_peer_allreduce(hs_ctx* ctx, int G, int count, int repeats, const double* in, double* out);
+
 /* ---- introspection (plan-only contexts too) ---------------------------- */
 /* Sizes: L (= 2 N_e n), number of subdomains, number of groups, 2 N_e. */
 int hs_sizes(const hs_ctx* ctx, int64_t* L, int* nsub, int* ngroups, int* npairs);

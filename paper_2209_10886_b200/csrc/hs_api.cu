@@ -24,8 +24,25 @@ using namespace hs;
 struct hs_ctx : public Ctx {};
 
 namespace hs {
-// One in-place sum over the ranks of the context (GMRES inner products).
+// One in-place sum over the ranks of the context (GMRES inner products): the
+// peer-memory all-reduce when the ranks' regions are mapped (hs_peer_open) --
+// one kernel, fixed rank order, no host call -- else ncclAllReduce.
 cudaError_t allreduce_sum_doubles(Ctx& c, double* buf, size_t count, void* comm) {
+  PeerRanks& p = c.peer;
+  if (p.G > 1 && p.red_on && count <= (size_t)kPeerRedCap) {
+    PeerRedArgs a;
+    a.G = p.G;
+    a.self = c.plan.rank;
+    a.count = (int)count;
+    a.epoch = ++p.red_epoch;
+    for (int g = 0; g < p.G; ++g) {
+      a.data[g] = p.red_data[g];
+      a.flag[g] = p.red_flag[g];
+      a.consumed[g] = p.red_consumed[g];
+    }
+    a.buf[0] = buf;
+    return launch_peer_allreduce(c, a);
+  }
   ncclResult_t r = ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, (ncclComm_t)comm, c.stream);
   if (r != ncclSuccess) {
     c.err = std::string("ncclAllReduce: ") + ncclGetErrorString(r);
@@ -2562,6 +2579,13 @@ int hs_get_trace(hs_ctx* c, uint64_t* out, int cap, int* rows) {
   return 0;
 }
 
+// The reduction area at the tail of a rank's exported region (256-aligned).
+static size_t peer_red_offset(const Ctx* c) {
+  const size_t L = (size_t)c->plan.L;
+  const size_t head = FV_N * L * sizeof(double2) + (size_t)(2 * c->plan.npairs + 2) * sizeof(int);
+  return (head + 255) / 256 * 256;
+}
+
 int hs_peer_export(hs_ctx* c, uint8_t handle[64]) {
   if (!c || !handle) return fail(c, 1, "null argument");
   DEV_SCOPE(c);
@@ -2570,7 +2594,7 @@ int hs_peer_export(hs_ctx* c, uint8_t handle[64]) {
   const size_t L = (size_t)c->plan.L;
   // FV_N vectors, npairs completion counters, the ticket, the inputs-posted
   // epoch flag, npairs wout-write counters
-  const size_t need = FV_N * L * sizeof(double2) + (size_t)(2 * c->plan.npairs + 2) * sizeof(int);
+  const size_t need = peer_red_offset(c) + kPeerRedBytes;
   if (!p.own || p.bytes != need) {
     dfree(c, p.own, 0);
     p.own = nullptr;
@@ -2618,7 +2642,13 @@ int hs_peer_open(hs_ctx* c, const uint8_t* handles, int nranks) {
     p.counters[g] = (int*)(base + FV_N * L * sizeof(double2));
     p.inflag[g] = p.counters[g] + c->plan.npairs + 1;
     p.wdone[g] = p.inflag[g] + 1;
+    char* red = base + peer_red_offset(c);
+    p.red_data[g] = (double*)red;
+    p.red_flag[g] = (unsigned*)(red + 2 * kPeerRedCap * sizeof(double));
+    p.red_consumed[g] = p.red_flag[g] + 2;
   }
+  p.red_epoch = 0;
+  p.red_on = !(getenv("HS_PEER_ALLREDUCE") && atoi(getenv("HS_PEER_ALLREDUCE")) == 0);
   std::vector<int> br(c->plan.npairs), own;
   for (int b = 0; b < c->plan.npairs; ++b) {
     br[b] = c->plan.subs[c->plan.block_sub[b]].rank;
@@ -2683,6 +2713,47 @@ int hs_fused_plan(const hs_ctx* cc, int ims, int rank, int32_t* out, int cap, in
   if (!out) return 0;
   if (cap < (int)v.size()) return fail(c, 1, "plan buffer too small");
   std::copy(v.begin(), v.end(), out);
+  return 0;
+}
+
+int hs_test_peer_allreduce(hs_ctx* c, int G, int count, int repeats, const double* in, double* out) {
+  if (!c || !in || !out) return fail(c, 1, "null argument");
+  DEV_SCOPE(c);
+  NEED_GPU(c);
+  if (G < 1 || G > kMaxRanks || count < 1 || count > kPeerRedCap || repeats < 1)
+    return fail(c, 1, "peer all-reduce test: 1 <= G <= 8, 1 <= count <= 4096, repeats >= 1");
+  // G emulated ranks' areas (zeroed: flags and counters start at epoch 0) and
+  // per-epoch buffers, every reduction launched back to back on the stream
+  const size_t area = kPeerRedBytes, nbuf = (size_t)repeats * G * count;
+  char* d = nullptr;
+  double* bufs = nullptr;
+  CK(cudaMalloc((void**)&d, area * G));
+  CK(cudaMemsetAsync(d, 0, area * G, c->stream));
+  CK(cudaMalloc((void**)&bufs, nbuf * sizeof(double)));
+  CK(cudaMemcpyAsync(bufs, in, nbuf * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  PeerRedArgs a;
+  a.G = G;
+  a.self = -1;
+  a.count = count;
+  for (int g = 0; g < G; ++g) {
+    char* red = d + area * g;
+    a.data[g] = (double*)red;
+    a.flag[g] = (unsigned*)(red + 2 * kPeerRedCap * sizeof(double));
+    a.consumed[g] = a.flag[g] + 2;
+  }
+  // one launch, every CTA running all the reductions: a fast rank races into
+  // the next epoch while others still read this one (the parity / consumed
+  // protocol is what keeps it correct)
+  a.epoch = 1;
+  a.repeats = repeats;
+  a.stride = (long long)G * count;
+  for (int g = 0; g < G; ++g) a.buf[g] = bufs + (size_t)g * count;
+  cudaError_t e = launch_peer_allreduce(*c, a);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(out, bufs, nbuf * sizeof(double), cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  cudaFree(d);
+  cudaFree(bufs);
+  CK(e);
   return 0;
 }
 

@@ -268,6 +268,33 @@ struct PeerRanks {
   unsigned epoch = 0;                 // applies run so far (epoch protocol)
   bool epochs = true;                 // false: two NCCL barriers per apply (HS_PEER_BARRIERS=1)
   double2* bar = nullptr;             // one-element NCCL barrier buffer
+  // GMRES inner-product all-reduce over the same mappings (region tail):
+  // per rank [2 parities][kPeerRedCap] partials, 2 published-epoch flags and a
+  // consumed-epoch counter; one kernel per reduction, no NCCL call
+  double* red_data[kMaxRanks] = {};
+  unsigned* red_flag[kMaxRanks] = {};
+  unsigned* red_consumed[kMaxRanks] = {};
+  unsigned red_epoch = 0;
+  bool red_on = true;                 // HS_PEER_ALLREDUCE=0: NCCL all-reduce instead
+};
+
+constexpr int kPeerRedCap = 4096;     // doubles per parity (CGS2: 2 (k + 2) <= 4096)
+// bytes of the reduction area at the tail of a rank's exported region
+constexpr size_t kPeerRedBytes = 2 * kPeerRedCap * sizeof(double) + 64;
+
+// The peer all-reduce (hs_krylov.cu): G ranks, every rank publishes its count
+// partials in its own area and sums all ranks' in rank order (bitwise the
+// same result on every rank).  self >= 0: this GPU's rank (one CTA); self < 0:
+// CTA r emulates rank r on one GPU (buf[r] per rank, tests).
+struct PeerRedArgs {
+  int G = 1, self = 0, count = 0;
+  unsigned epoch = 0;         // of the first reduction
+  int repeats = 1;            // reductions in this launch (tests: ranks race across epochs)
+  long long stride = 0;       // buffer offset between consecutive reductions
+  double* data[kMaxRanks] = {};
+  unsigned* flag[kMaxRanks] = {};
+  unsigned* consumed[kMaxRanks] = {};
+  double* buf[kMaxRanks] = {};
 };
 
 // One distinct subdomain operator (Dirichlet mask) and its factor.

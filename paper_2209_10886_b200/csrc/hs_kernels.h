@@ -113,5 +113,6 @@ cudaError_t gmres_arnoldi_cgs2(Ctx& c, GmresDev& G, int k, const int* blocks, in
                                double2* hbuf, void* nccl_comm);
 // in-place sum over ranks (implemented next to the NCCL calls in hs_api.cu)
 cudaError_t allreduce_sum_doubles(Ctx& c, double* buf, size_t count, void* nccl_comm);
+cudaError_t launch_peer_allreduce(Ctx& c, const PeerRedArgs& a);
 
 }  // namespace hs

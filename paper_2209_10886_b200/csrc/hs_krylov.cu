@@ -690,11 +690,17 @@ __global__ void k_cgs_update(GmresDev G, const int* __restrict__ blocks, int nb,
   }
 }
 
+// nrm2 = [h'_0 .. h'_k, |w'|^2] (pyth = 1: |w''|^2 = |w'|^2 - |h'|^2, the
+// second pass's coefficients being O(eps) |w'| -- no cancellation) or
+// [|w''|^2] (pyth = 0: a third reduction formed it directly)
 __global__ void k_cgs_normalize(GmresDev G, const int* __restrict__ blocks, int nb, int n, int k,
-                                const double2* nrm2) {
+                                const double2* nrm2, int pyth) {
   const long long LR = G.LR;
   double2* w = G.V + (long long)(k + 1) * LR;
-  const double hn = sqrt(nrm2[0].x);
+  double q = pyth ? nrm2[k + 1].x : nrm2[0].x;
+  if (pyth)
+    for (int j = 0; j <= k; ++j) q -= nrm2[j].x * nrm2[j].x + nrm2[j].y * nrm2[j].y;
+  const double hn = sqrt(q > 0 ? q : 0.0);
   const long long total = (long long)nb * n;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
@@ -714,21 +720,26 @@ cudaError_t gmres_arnoldi_cgs2(Ctx& c, GmresDev& G, int k, const int* blocks, in
     return allreduce_sum_doubles(c, (double*)hbuf, 2 * (size_t)cnt, nccl_comm);
   };
   const int ug = std::min(grid * 4, std::max(1, (int)(((long long)nb * c.n + 255) / 256)));
-  // pass 0 (+ |w|^2 before orthogonalisation), pass 1
+  // Two reductions per iteration: pass 0 forms h and |w|^2 (breakdown test),
+  // pass 1 h' and |w'|^2, and the new norm follows by Pythagoras.
+  // HS_CGS2_DIRECT=1: a third reduction forms |w''|^2 directly.
+  static const bool direct = getenv("HS_CGS2_DIRECT") && atoi(getenv("HS_CGS2_DIRECT")) != 0;
   for (int pass = 0; pass < 2; ++pass) {
-    const int cnt = kp1 + (pass == 0 ? 1 : 0);
+    const int cnt = kp1 + (pass == 0 || !direct ? 1 : 0);
     c.launches += 3;
     k_cgs_dots<<<grid, 256, 0, c.stream>>>(G, blocks, nb, c.n, k, 0, cnt, part);
     k_cgs_reduce<<<(cnt + 127) / 128, 128, 0, c.stream>>>(part, grid, kp1 + 1, cnt, hbuf);
     if (cudaError_t e = allreduce(cnt)) return e;
     k_cgs_update<<<ug, 256, 0, c.stream>>>(G, blocks, nb, c.n, k, hbuf, pass);
   }
-  // |w|^2 -> normalise
-  c.launches += 3;
-  k_cgs_dots<<<grid, 256, 0, c.stream>>>(G, blocks, nb, c.n, k, kp1, kp1 + 1, part);
-  k_cgs_reduce<<<1, 32, 0, c.stream>>>(part + kp1, grid, kp1 + 1, 1, hbuf);
-  if (cudaError_t e = allreduce(1)) return e;
-  k_cgs_normalize<<<ug, 256, 0, c.stream>>>(G, blocks, nb, c.n, k, hbuf);
+  if (direct) {  // |w|^2 -> normalise
+    c.launches += 2;
+    k_cgs_dots<<<grid, 256, 0, c.stream>>>(G, blocks, nb, c.n, k, kp1, kp1 + 1, part);
+    k_cgs_reduce<<<1, 32, 0, c.stream>>>(part + kp1, grid, kp1 + 1, 1, hbuf);
+    if (cudaError_t e = allreduce(1)) return e;
+  }
+  c.launches++;
+  k_cgs_normalize<<<ug, 256, 0, c.stream>>>(G, blocks, nb, c.n, k, hbuf, direct ? 0 : 1);
   return cudaGetLastError();
 }
 
@@ -1398,4 +1409,73 @@ cudaError_t gmres_finish(Ctx& c, GmresDev& G, int mmax, double2* u) {
   return cudaGetLastError();
 }
 
+}  // namespace hs
+
+namespace hs {
+// ---------------------------------------------------------------------------
+// Peer-memory all-reduce of the sharded Arnoldi's inner products (replaces the
+// ncclAllReduce calls: one kernel, no host involvement, fixed rank order).
+// Rank r: (1) wait until every peer has consumed epoch - 2 (the previous use
+// of this parity of r's area); (2) write its partials into its own area; (3)
+// release-publish the epoch on its flag (system scope); (4) acquire every
+// rank's flag >= epoch; (5) sum the G areas in rank order 0..G-1 -- the same
+// additions on every rank, so all ranks hold bitwise the same sums; (6)
+// release its consumed counter.  Peers are reached through the CUDA-IPC
+// mappings of hs_peer_open (NVLink loads); the areas sit at the tail of the
+// exported region.
+static __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+static __device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(256) k_peer_allreduce(PeerRedArgs a) {
+  const int r = a.self >= 0 ? a.self : (int)blockIdx.x;
+  for (int it = 0; it < a.repeats; ++it) {
+    const unsigned e = a.epoch + (unsigned)it;
+    const int par = (int)(e & 1);
+    double* mine = a.data[r] + (size_t)par * kPeerRedCap;
+    double* buf = a.buf[a.self >= 0 ? 0 : r] + (long long)it * a.stride;
+    if (threadIdx.x == 0 && e >= 2)
+      for (int g = 0; g < a.G; ++g)
+        if (g != r)
+          while (ld_acquire_sys(a.consumed[g]) < e - 2) __nanosleep(64);
+    __syncthreads();
+    for (int j = threadIdx.x; j < a.count; j += blockDim.x) mine[j] = buf[j];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      st_release_sys(a.flag[r] + par, e);
+      for (int g = 0; g < a.G; ++g)
+        while (ld_acquire_sys(a.flag[g] + par) < e) __nanosleep(32);
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < a.count; j += blockDim.x) {
+      double s = 0.0;
+      for (int g = 0; g < a.G; ++g) s += __ldcv(a.data[g] + (size_t)par * kPeerRedCap + j);
+      buf[j] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      st_release_sys(a.consumed[r], e);
+    }
+  }
+}
+
+cudaError_t launch_peer_allreduce(Ctx& c, const PeerRedArgs& a) {
+  if (a.count > kPeerRedCap || a.G < 1 || a.G > kMaxRanks) return cudaErrorInvalidValue;
+  c.launches++;
+  if (a.self >= 0) {
+    k_peer_allreduce<<<1, 256, 0, c.stream>>>(a);
+    return cudaGetLastError();
+  }
+  // emulation: the G CTAs wait on one another -> a cooperative launch keeps them co-resident
+  PeerRedArgs aa = a;
+  void* args[] = {(void*)&aa};
+  return cudaLaunchCooperativeKernel((const void*)k_peer_allreduce, dim3(a.G), dim3(256), args, 0, c.stream);
+}
 }  // namespace hs

@@ -57,6 +57,7 @@ _SIGS = {
     "hs_exchange_plan": (_I, [_P, _I, _I, _I, _pI32, _I, C.POINTER(_I)]),
     "hs_get_schur": (_I, [_P, _I, _I, _P]),
     "hs_gmres_basis": (_I, [_P, _P, _I, C.POINTER(_I)]),
+    "hs_test_peer_allreduce": (_I, [_P, _I, _I, _I, _P, _P]),
     "hs_set_schur": (_I, [_P, _I, _I, _P]),
     "hs_set_async": (_I, [_P, _I]),
     "hs_sync": (_I, [_P]),
