@@ -60,11 +60,11 @@ def load_peaks():
     return 6650.0, "fallback"
 
 
-def problem(cfgno):
-    from paper_2209_10886_b200.configs import CONFIGS
+def problem(cfgno, blocks=None):
+    from paper_2209_10886_b200.configs import CONFIGS, with_blocks
     from paper_2209_10886_b200.discretization import ProblemSpec, Scatterer
     from paper_2209_10886_b200.indexing import Partition
-    c = CONFIGS[cfgno]
+    c = CONFIGS[cfgno] if blocks is None else with_blocks(CONFIGS[cfgno], blocks)
     ang = c["angle"] if c["angle"] is not None else 0.0
     spec = ProblemSpec(kappa=c["kappa"], cells_per_side=c["n"], subdomain_side=c["side"],
                        scatterer=Scatterer(tuple(c["center"]), c["radius"]),
@@ -167,17 +167,19 @@ def host_info():
                     "each S application run in forked processes, one BLAS thread each"}
 
 
-def reference_iterations(cfgno):
+def reference_iterations(cfgno, blocks=None):
     """GMRES iterations of the reference arithmetic on this config, from its golden
-    run (tests/golden/cfg*.npz; config 4 = config 2's geometry, per angle)."""
+    run (tests/golden/cfg*.npz; config 4 = config 2's geometry, per angle; config
+    2 with another block count: the gm_iters_p{p} keys of the sweep golden)."""
     name = {4: "cfg2"}.get(cfgno, f"cfg{cfgno}")
     p = os.path.join(ROOT, "tests", "golden", f"{name}.npz")
     if not os.path.exists(p):
         return None, None
+    sfx = f"_p{blocks}" if blocks is not None else ""
     with np.load(p) as G:
-        if "gm_iters" not in G.files:
+        if f"gm_iters{sfx}" not in G.files:
             return None, None
-        return int(G["gm_iters"]), (float(G["gm_time"]) if "gm_time" in G.files else None)
+        return int(G[f"gm_iters{sfx}"]), (float(G[f"gm_time{sfx}"]) if f"gm_time{sfx}" in G.files else None)
 
 
 class ReferenceCPU:
@@ -190,10 +192,11 @@ class ReferenceCPU:
     of an S application spread over `workers` forked processes
     (oracle/parallel.py).  No product code is imported."""
 
-    def __init__(self, cfgno, workers=None):
+    def __init__(self, cfgno, workers=None, blocks=None):
         from oracle import Interface, Lattice, Preconditioner, Problem
         from oracle.parallel import ParInterface
-        c = load_configs().CONFIGS[cfgno]
+        cm = load_configs()
+        c = cm.CONFIGS[cfgno] if blocks is None else cm.with_blocks(cm.CONFIGS[cfgno], blocks)
         self.c = c
         ang = c["angle"] if c["angle"] is not None else 0.0
         prob = Problem(kappa=c["kappa"], n=c["n"], side=c["side"], center=tuple(c["center"]), radius=c["radius"],
@@ -241,16 +244,16 @@ class ReferenceCPU:
         return self.P.solves - s0, time.perf_counter() - t0
 
 
-def cpu_baseline(cfgno):
+def cpu_baseline(cfgno, blocks=None):
     """The reference arithmetic on all host cores, bounded sample: one full BSP
     apply and one (I-S) apply after the shared-factor setup (~10-30 s at cfg5)."""
-    ref = ReferenceCPU(cfgno)
+    ref = ReferenceCPU(cfgno, blocks=blocks)
     try:
         t_bsp, ns = ref.time_apply()
         t_ims = ref.time_ims()
     finally:
         ref.close()
-    its, _ = reference_iterations(cfgno)
+    its, _ = reference_iterations(cfgno, blocks)
     per = t_bsp * ref.R
     out = {"value": 1.0 / per, "unit": "applies/s", "cores": ref.workers, "kind": "port",
            "sample": f"one full BSP apply ({ns} subdomain SuperLU solves + outgoing traces through the reference "
@@ -269,7 +272,7 @@ def run_reference(args):
     rank, world = env_int("RANK", 0), env_int("WORLD_SIZE", 1)
     if rank != 0:
         return 0
-    ref = ReferenceCPU(args.config)
+    ref = ReferenceCPU(args.config, blocks=args.blocks)
     try:
         t_apply, ns = ref.time_apply()  # the first (warm-up) apply also sizes the samples
         t_ims = ref.time_ims()
@@ -291,7 +294,7 @@ def run_reference(args):
         ref.close()
     wall = sum(times)
     value = (done / (ns * ref.R)) / wall
-    its, t_golden = reference_iterations(args.config)
+    its, t_golden = reference_iterations(args.config, args.blocks)
     c = ref.c
     cpu = {"value": value, "unit": "applies/s", "cores": ref.workers, "kind": "port",
            "sample": (f"each step: {'one full BSP apply' if frac >= 1.0 else f'{quota} of the {ns} subdomain solves of a BSP apply'}"
@@ -321,6 +324,8 @@ def main():
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--blocks", type=int, default=None,
+                    help="sweep block count p (BASELINE config 2 varies p over 1, 2, 4, 8; SURVEY.md §8d window rule)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-gmres", action="store_true")
@@ -348,7 +353,7 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
 
-    c, spec, part = problem(args.config)
+    c, spec, part = problem(args.config, args.blocks)
     R = int(c["nrhs"])
     sweep = SweepConfig(blocks=c["blocks"])
     torch.zeros(1, device=f"cuda:{local}")  # CUDA context up before the setup clock starts
@@ -585,7 +590,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_baseline(args.config)
+            cpu = cpu_baseline(args.config, args.blocks)
         except Exception as e:  # report, do not fail the bench
             cpu = {"value": None, "unit": "applies/s", "cores": 1, "kind": "port", "sample": f"failed: {e}"}
 

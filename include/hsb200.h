@@ -221,6 +221,19 @@ int hs_get_trace(hs_ctx* ctx, uint64_t* out, int cap, int* rows);
  * result must be the rank-order sum, bitwise. */
 int hs_test_peer_allreduce(hs_ctx* ctx, int G, int count, int repeats, const double* in, double* out);
 
+/* Device-side checks (the debug library libhsb200_debug.so, built with
+ * -DHS_DEVICE_CHECKS; HS_LIB=debug loads it): bounds asserts on every table,
+ * map and vector access of the dataflow kernels and a watchdog on every
+ * cross-CTA spin-wait.  Synchronises the context's stream and returns in
+ * *first the first failure since the last call -- (unit << 48) | (source line
+ * << 8) | tag, unit 1 hs_apply.cu, 2 hs_zmma.cu, 3 hs_krylov.cu, 4
+ * hs_schur.cu; tag = DbgTag (hs_common.cuh) -- or 0; *enabled = 1 in the
+ * debug library, 0 in the release one (which checks nothing). */
+int hs_debug_check(hs_ctx* ctx, uint64_t* first, int* enabled);
+/* Launch one deliberately failing check (unit 1, tag 1): the debug library
+ * then reports it through hs_debug_check; the release library reports 0. */
+int hs_debug_selftest(hs_ctx* ctx);
+
 /* ---- introspection (plan-only contexts too) ---------------------------- */
 /* Sizes: L (= 2 N_e n), number of subdomains, number of groups, 2 N_e. */
 int hs_sizes(const hs_ctx* ctx, int64_t* L, int* nsub, int* ngroups, int* npairs);

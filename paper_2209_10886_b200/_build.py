@@ -53,17 +53,21 @@ def _needs(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, debug: bool = False) -> str:
+    """debug = True: libhsb200_debug.so, the device-checks build (-DHS_DEVICE_CHECKS:
+    bounds asserts + spin watchdogs, hs_debug_check; HS_LIB=debug loads it)."""
     os.makedirs(OUT_DIR, exist_ok=True)
-    os.makedirs(BUILD, exist_ok=True)
+    build_dir = BUILD + ("_debug" if debug else "")
+    lib_out = LIB.replace("libhsb200.so", "libhsb200_debug.so") if debug else LIB
+    os.makedirs(build_dir, exist_ok=True)
     inc, lib = nccl_paths()
     common = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-I", inc, "-I", os.path.join(ROOT, "include"),
-              "--expt-relaxed-constexpr"]
+              "--expt-relaxed-constexpr"] + (["-DHS_DEVICE_CHECKS"] if debug else [])
     hdrs = headers()
     jobs = []
     objs = []
     for src in sources():
-        obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+        obj = os.path.join(build_dir, os.path.basename(src) + ".o")
         objs.append(obj)
         if force or _needs(obj, [src] + hdrs):
             cmd = [NVCC] + ARCH + common + ["-Xptxas", "-v" if verbose else "-O3", "-c", src, "-o", obj]
@@ -81,15 +85,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 sys.stderr.write(" ".join(cmd) + "\n" + p.stdout + p.stderr)
             if p.returncode:
                 raise RuntimeError(f"nvcc failed for {cmd[-3]}")
-    if force or jobs or _needs(LIB, objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + [
+    if force or jobs or _needs(lib_out, objs):
+        cmd = [NVCC] + ARCH + ["-shared", "-o", lib_out] + objs + [
             "-L", lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + lib]
         p = subprocess.run(cmd, capture_output=True, text=True)
         if p.returncode:
             sys.stderr.write(" ".join(cmd) + "\n" + p.stdout + p.stderr)
             raise RuntimeError("link failed")
-    return LIB
+    return lib_out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, debug="--debug" in sys.argv))

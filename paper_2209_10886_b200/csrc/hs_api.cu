@@ -2716,6 +2716,33 @@ int hs_fused_plan(const hs_ctx* cc, int ims, int rank, int32_t* out, int cap, in
   return 0;
 }
 
+int hs_debug_check(hs_ctx* c, uint64_t* first, int* enabled) {
+  if (!c || !first) return fail(c, 1, "null argument");
+  DEV_SCOPE(c);
+#ifdef HS_DEVICE_CHECKS
+  if (enabled) *enabled = 1;
+#else
+  if (enabled) *enabled = 0;
+#endif
+  *first = 0;
+  if (c->device < 0) return 0;
+  CK(cudaStreamSynchronize(c->stream));
+  unsigned long long (*take[4])() = {hs_dbg_take_apply, hs_dbg_take_zmma, hs_dbg_take_krylov, hs_dbg_take_schur};
+  for (int u = 0; u < 4; ++u) {
+    const unsigned long long v = take[u]();
+    if (v && !*first) *first = (v & ((1ull << 48) - 1)) | ((unsigned long long)(u + 1) << 48);
+  }
+  return 0;
+}
+
+int hs_debug_selftest(hs_ctx* c) {
+  if (!c) return fail(nullptr, 1, "null context");
+  DEV_SCOPE(c);
+  NEED_GPU(c);
+  CK(launch_dbg_selftest(*c));
+  return 0;
+}
+
 int hs_test_peer_allreduce(hs_ctx* c, int G, int count, int repeats, const double* in, double* out) {
   if (!c || !in || !out) return fail(c, 1, "null argument");
   DEV_SCOPE(c);

@@ -133,6 +133,8 @@ struct FusedArgs {
   double2* split_buf;         // split-K partial sums [pair][half][32 rows][2]
   int* split_cnt;             // split-K arrivals per pair (odd arrival combines)
   MultiRankArgs mr;
+  long long L = 0, T_elems = 0;  // bounds of the device checks (debug library)
+  int nitems = 0, nsub = 0, npairs = 0;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -409,12 +411,18 @@ __global__ void __launch_bounds__(NW * 32, RT == 1 ? 6 : 1) k_bsp_fused(FusedArg
     unsigned long long* tr = (a.trace && !MR) ? a.trace + 6ll * t : nullptr;
     if (tr && threadIdx.x == 0) tr[0] = tr[1] = gtimer();
     const FusedTile ft = tiles[t];
+    HS_DCHECK(ft.item >= 0 && ft.item < a.nitems, DBG_INDEX);
     const DevItem it = a.items[ft.item];
+    HS_DCHECK(it.s >= 0 && it.s < a.nsub, DBG_INDEX);
     const DevSub sb = a.subs[it.s];
+    HS_DCHECK(sb.T_off >= 0 && sb.T_off + (long long)sb.k * n * ((sb.k * n + kRowTile - 1) / kRowTile * kRowTile) <= a.T_elems,
+              DBG_MAP);
+    HS_DCHECK(sb.in_off >= 0 && sb.in_off + (long long)sb.k * n <= a.L, DBG_VEC);
     for (int d = threadIdx.x; d < ft.ndep; d += blockDim.x) {
       const FusedDep dp = a.deps[ft.dep0 + d];
+      HS_DCHECK(dp.block >= 0 && dp.block < a.npairs, DBG_COUNTER);
       const volatile int* p = rv.done(dp.block);
-      while (*p < rv.target(dp)) __nanosleep(32);
+      HS_WAIT(*p < rv.target(dp), 32, DBG_DEPWAIT);
     }
     rv.fence();  // acquire: the producers' stores before this CTA's reads
     __syncthreads();
@@ -471,6 +479,7 @@ __global__ void __launch_bounds__(NW * 32, RT == 1 ? 6 : 1) k_bsp_fused(FusedArg
       if (row >= it.rlo && row < it.rhi) {
         const int f = row / n, p = row - f * n;
         const long long off = (long long)sb.tgt[f] + p;
+        HS_DCHECK(f < sb.k && off >= 0 && off < a.L, DBG_VEC);
         const int o = rv.owner(sb.tgt[f] / n);  // the output block's rank
         const bool low = f < sb.nlow, zr = (ft.rmask >> (4 + f)) & 1;
         double2 e1 = make_double2(0, 0), e2 = e1, e3 = e1;
@@ -535,10 +544,19 @@ __device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
 }
 __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
   unsigned ok = 0;
+#ifdef HS_DEVICE_CHECKS
+  unsigned long long spins = 0;
+#endif
   do {
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
+#ifdef HS_DEVICE_CHECKS
+    if (!ok && ++spins > (1ull << 28)) {
+      hs_dbg_fail(DBG_MBAR, __LINE__);
+      break;
+    }
+#endif
   } while (!ok);
 }
 // Map chunks are read exactly once per apply: evict them from L2 first, so the
@@ -605,8 +623,13 @@ __global__ void __maxnreg__(96) k_bsp_tma(FusedArgs a) {  // 96: two 10-warp CTA
         if (a.trace) td.claimed = gtimer();
         if (td.t < rv.ntiles()) {
           const FusedTile ft = rv.tiles()[td.t];
+          HS_DCHECK(ft.item >= 0 && ft.item < a.nitems, DBG_INDEX);
           const DevItem it = a.items[ft.item];
+          HS_DCHECK(it.s >= 0 && it.s < a.nsub, DBG_INDEX);
           const DevSub sb = a.subs[it.s];
+          HS_DCHECK(sb.T_off >= 0 && sb.T_off + (long long)(ft.tile + 1) * sb.k * a.n * kRowTile <= a.T_elems, DBG_MAP);
+          HS_DCHECK(sb.in_off >= 0 && sb.in_off + (long long)sb.k * a.n <= a.L, DBG_VEC);
+          HS_DCHECK(ft.c0 >= 0 && ft.c0 <= ft.c1 && ft.c1 <= sb.k * a.n, DBG_INDEX);
           td.K = sb.k * a.n;
           td.row0 = ft.tile * kRowTile;
           td.map_off = sb.T_off + (long long)ft.tile * td.K * kRowTile;
@@ -659,8 +682,9 @@ __global__ void __maxnreg__(96) k_bsp_tma(FusedArgs a) {  // 96: two 10-warp CTA
     }
     for (int i = threadIdx.x; i < td.ndep; i += NT) {
       const FusedDep dp = a.deps[td.dep0 + i];
+      HS_DCHECK(dp.block >= 0 && dp.block < a.npairs, DBG_COUNTER);
       const volatile int* p = rv.done(dp.block);
-      while (*p < rv.target(dp)) __nanosleep(32);
+      HS_WAIT(*p < rv.target(dp), 32, DBG_DEPWAIT);
     }
     rv.fence();  // acquire: the producers' stores before this CTA's reads
     consumers_sync(NT);
@@ -671,6 +695,7 @@ __global__ void __maxnreg__(96) k_bsp_tma(FusedArgs a) {  // 96: two 10-warp CTA
     const bool erow_ok = warp == 0 && erow >= td.rlo && erow < td.rhi;
     const int ef = erow / n;
     const long long eoff = erow_ok ? (long long)td.tgt[ef] + (erow - ef * n) : 0;
+    HS_DCHECK(!erow_ok || (ef < 4 && eoff >= 0 && eoff < a.L), DBG_VEC);
     const int eo = erow_ok ? rv.owner(td.tgt[ef] / n) : cr;  // the output block's rank
     const bool elow = ef < td.nlow;
     double2 e1 = make_double2(0, 0), e2 = e1, e3 = e1;
@@ -1000,6 +1025,7 @@ cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double
     a.r = r; a.zL = zL; a.rp = rp; a.w = w; a.z = z; a.wout = wout;
     a.done = f.counters; a.ticket = f.counters + c.plan.npairs;
     a.ntiles = f.ntiles; a.n = c.n; a.maxK = f.maxK; a.nv = f.nv;
+  a.L = c.plan.L; a.T_elems = (long long)c.T_elems; a.nitems = f.nitems; a.nsub = c.plan.nsub; a.npairs = c.plan.npairs;
     a.direct_signal = f.direct_signal;
     a.split_buf = f.split_buf; a.split_cnt = f.split_cnt;
     a.map_keep = c.map_mode == 2;
@@ -1026,6 +1052,7 @@ cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double
   a.r = r; a.zL = zL; a.rp = rp; a.w = w; a.z = z; a.wout = wout;
   a.done = f.counters; a.ticket = f.counters + c.plan.npairs;
   a.ntiles = f.ntiles; a.n = c.n; a.maxK = f.maxK; a.nv = f.nv;
+  a.L = c.plan.L; a.T_elems = (long long)c.T_elems; a.nitems = f.nitems; a.nsub = c.plan.nsub; a.npairs = c.plan.npairs;
     a.trace = (c.trace_on && c.trace && c.trace_cap >= (size_t)f.ntiles) ? c.trace : nullptr;
     if (a.trace) c.trace_rows = f.ntiles;
   const int grid = std::max(1, std::min(f.ntiles, per_sm[var] * c.num_sms));
@@ -1060,6 +1087,7 @@ cudaError_t launch_bsp_fused_ranks(Ctx& c, const DevFused& f, const MultiRankArg
   a.r = nullptr; a.zL = a.rp = a.w = a.z = a.wout = nullptr;
   a.done = nullptr; a.ticket = nullptr;
   a.ntiles = 0; a.n = c.n; a.maxK = f.maxK; a.nv = f.nv; a.trace = nullptr;
+  a.L = c.plan.L; a.T_elems = (long long)c.T_elems; a.nitems = f.nitems; a.nsub = c.plan.nsub; a.npairs = c.plan.npairs;
   a.direct_signal = f.direct_signal;
   a.split_buf = f.split_buf; a.split_cnt = f.split_cnt;
   a.map_keep = c.map_mode == 2;
@@ -1081,5 +1109,17 @@ cudaError_t launch_bsp_fused_ranks(Ctx& c, const DevFused& f, const MultiRankArg
   k_bsp_fused<8, 1, true><<<grid, 256, smem, c.stream>>>(a);
   return cudaGetLastError();
 }
+
+// A deliberately failing check (hs_debug_selftest): proves that the debug
+// library's instrumentation reports (and the release library's is compiled out).
+__global__ void k_dbg_selftest(int n) { HS_DCHECK(n < 0, DBG_INDEX); }
+
+cudaError_t launch_dbg_selftest(Ctx& c) {
+  c.launches++;
+  k_dbg_selftest<<<1, 32, 0, c.stream>>>(1);
+  return cudaGetLastError();
+}
+
+HS_DBG_ACCESSOR(hs_dbg_take_apply)
 
 }  // namespace hs

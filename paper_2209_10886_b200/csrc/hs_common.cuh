@@ -6,6 +6,56 @@
 
 namespace hs {
 
+// ---- device-side checks (the debug library, -DHS_DEVICE_CHECKS:
+// libhsb200_debug.so; compute-sanitizer is unavailable on this GPU pool).
+// HS_DCHECK: index / range asserts on every table and vector access of the
+// dataflow kernels; HS_WAIT: every spin-wait of a cross-CTA protocol (block
+// completion counters, grid barriers, mbarrier rings, peer flags) with a
+// watchdog (~2 s) so a protocol bug reports instead of hanging.  The first
+// failure of a translation unit is kept as (line << 8 | tag); hs_debug_check
+// collects them.  In the release library both macros are the plain code.
+enum DbgTag { DBG_INDEX = 1, DBG_MAP = 2, DBG_VEC = 3, DBG_COUNTER = 4, DBG_DEPWAIT = 5, DBG_MBAR = 6,
+              DBG_GRIDBAR = 7, DBG_PEER = 8, DBG_SMEM = 9 };
+#ifdef HS_DEVICE_CHECKS
+static __device__ unsigned long long g_hs_dbg;
+static __device__ __noinline__ void hs_dbg_fail(unsigned tag, unsigned line) {
+  atomicCAS(&g_hs_dbg, 0ull, (1ull << 63) | ((unsigned long long)line << 8) | tag);
+}
+#define HS_DCHECK(cond, tag)                     \
+  do {                                           \
+    if (!(cond)) ::hs::hs_dbg_fail((tag), __LINE__); \
+  } while (0)
+#define HS_WAIT(still_waiting, ns, tag)                        \
+  do {                                                         \
+    unsigned long long hs_n_ = 0;                              \
+    while (still_waiting) {                                    \
+      __nanosleep(ns);                                         \
+      if (++hs_n_ > (1ull << 26)) {                            \
+        ::hs::hs_dbg_fail((tag), __LINE__);                    \
+        break;                                                 \
+      }                                                        \
+    }                                                          \
+  } while (0)
+// one accessor per translation unit: the first failure, then cleared
+#define HS_DBG_ACCESSOR(name)                                             \
+  unsigned long long name() {                                             \
+    unsigned long long v = 0, z = 0;                                      \
+    cudaMemcpyFromSymbol(&v, ::hs::g_hs_dbg, sizeof(v));                  \
+    cudaMemcpyToSymbol(::hs::g_hs_dbg, &z, sizeof(z));                    \
+    return v;                                                             \
+  }
+#else
+#define HS_DCHECK(cond, tag) \
+  do {                       \
+  } while (0)
+#define HS_WAIT(still_waiting, ns, tag) \
+  do {                                  \
+    while (still_waiting) __nanosleep(ns); \
+  } while (0)
+#define HS_DBG_ACCESSOR(name) \
+  unsigned long long name() { return 0; }
+#endif
+
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {

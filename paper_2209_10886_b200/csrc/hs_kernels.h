@@ -114,5 +114,11 @@ cudaError_t gmres_arnoldi_cgs2(Ctx& c, GmresDev& G, int k, const int* blocks, in
 // in-place sum over ranks (implemented next to the NCCL calls in hs_api.cu)
 cudaError_t allreduce_sum_doubles(Ctx& c, double* buf, size_t count, void* nccl_comm);
 cudaError_t launch_peer_allreduce(Ctx& c, const PeerRedArgs& a);
+// first device-check failure of each translation unit (0: none; debug library only)
+unsigned long long hs_dbg_take_apply();
+cudaError_t launch_dbg_selftest(Ctx& c);
+unsigned long long hs_dbg_take_zmma();
+unsigned long long hs_dbg_take_krylov();
+unsigned long long hs_dbg_take_schur();
 
 }  // namespace hs

@@ -38,8 +38,17 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
     __threadfence();
     atomicAdd(bar, 1u);
     unsigned v;
+#ifdef HS_DEVICE_CHECKS
+    unsigned long long spins = 0;
+#endif
     do {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+#ifdef HS_DEVICE_CHECKS
+      if ((int)(v - target) < 0 && ++spins > (1ull << 28)) {
+        hs_dbg_fail(DBG_GRIDBAR, __LINE__);
+        break;
+      }
+#endif
     } while ((int)(v - target) < 0);
   }
   __syncthreads();
@@ -1441,16 +1450,14 @@ __global__ void __launch_bounds__(256) k_peer_allreduce(PeerRedArgs a) {
     double* buf = a.buf[a.self >= 0 ? 0 : r] + (long long)it * a.stride;
     if (threadIdx.x == 0 && e >= 2)
       for (int g = 0; g < a.G; ++g)
-        if (g != r)
-          while (ld_acquire_sys(a.consumed[g]) < e - 2) __nanosleep(64);
+        if (g != r) HS_WAIT(ld_acquire_sys(a.consumed[g]) < e - 2, 64, DBG_PEER);
     __syncthreads();
     for (int j = threadIdx.x; j < a.count; j += blockDim.x) mine[j] = buf[j];
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence_system();
       st_release_sys(a.flag[r] + par, e);
-      for (int g = 0; g < a.G; ++g)
-        while (ld_acquire_sys(a.flag[g] + par) < e) __nanosleep(32);
+      for (int g = 0; g < a.G; ++g) HS_WAIT(ld_acquire_sys(a.flag[g] + par) < e, 32, DBG_PEER);
     }
     __syncthreads();
     for (int j = threadIdx.x; j < a.count; j += blockDim.x) {
@@ -1478,4 +1485,6 @@ cudaError_t launch_peer_allreduce(Ctx& c, const PeerRedArgs& a) {
   void* args[] = {(void*)&aa};
   return cudaLaunchCooperativeKernel((const void*)k_peer_allreduce, dim3(a.G), dim3(256), args, 0, c.stream);
 }
+HS_DBG_ACCESSOR(hs_dbg_take_krylov)
+
 }  // namespace hs

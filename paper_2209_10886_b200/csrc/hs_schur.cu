@@ -690,4 +690,6 @@ void launch_lift_b(Ctx& c, double2* b, const double2* G, int Rtot, int col0, int
   k_lift_b<<<4 * c.n, th, 0, c.stream>>>(b, G, Rtot, col0, nrhs, c.n, face_tgt, coef);
 }
 
+HS_DBG_ACCESSOR(hs_dbg_take_schur)
+
 }  // namespace hs

@@ -412,7 +412,16 @@ __device__ __forceinline__ void z2_arrive(unsigned long long* b) {
 }
 __device__ __forceinline__ void z2_wait(unsigned long long* b, unsigned parity) {
   unsigned ok = 0;
+#ifdef HS_DEVICE_CHECKS
+  unsigned long long spins = 0;
+#endif
   do {
+#ifdef HS_DEVICE_CHECKS
+    if (++spins > (1ull << 28)) {
+      hs_dbg_fail(DBG_MBAR, __LINE__);
+      break;
+    }
+#endif
     asm volatile(
         "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(ok)
@@ -477,7 +486,8 @@ template <int BN, int TM, int TN, bool NMAJ, int S, bool PERS, int KG>
 __global__ void __launch_bounds__(Z2<BN, TM, TN, NMAJ, S, PERS, KG>::THREADS, 1)
     k_zmma2(const MmaTask* __restrict__ tasks, int ntasks, const MmaCol* __restrict__ cols,
             const double2* __restrict__ A, const double2* srcA, const double2* srcB,
-            const double2* __restrict__ zeros, Epi e, int n, int R, int KS, unsigned long long* tr, int seq) {
+            const double2* __restrict__ zeros, Epi e, int n, int R, int KS, unsigned long long* tr, int seq,
+            long long Aelems, long long LR) {
   using F = Z2<BN, TM, TN, NMAJ, S, PERS, KG>;
   extern __shared__ __align__(128) double2 sm[];
   __shared__ __align__(8) unsigned long long full[S], empty[S], dfull[2], dempty[2];
@@ -534,6 +544,8 @@ __global__ void __launch_bounds__(Z2<BN, TM, TN, NMAJ, S, PERS, KG>::THREADS, 1)
       const int d = PERS ? (it & 1) : 0;
       ZCols2<BN>& zc = zcs[d];
       const MmaTask tk = tasks[t];
+      HS_DCHECK(tk.a_off >= 0 && tk.a_off + (long long)tk.K * 32 <= Aelems && tk.K % Z2KC == 0, DBG_MAP);
+      HS_DCHECK(tk.ncols >= 1 && tk.ncols <= BN, DBG_INDEX);
       if (PERS) {
         z2_wait(&dempty[d], (unsigned)((it >> 1) & 1) ^ 1);
         if (lane == 0) zc.tk = tk;
@@ -557,11 +569,13 @@ __global__ void __launch_bounds__(Z2<BN, TM, TN, NMAJ, S, PERS, KG>::THREADS, 1)
         if (NMAJ) {
           for (int j = lane; j < BN; j += 32) {
             const long long off = zc.in[j][q];
+            HS_DCHECK(off < 0 || off + (long long)(p0 + 31) * R < LR, DBG_VEC);
             const double2* src = off >= 0 ? (zc.alt[j] ? srcB : srcA) + off + (long long)p0 * R : zeros;
             z2_copy(sb + j * F::SB, src, 32 * sizeof(double2), &full[st]);
           }
         } else {
           // one slab: positions k0.. of the compact faces are consecutive rows of R
+          HS_DCHECK(zc.in[0][0] >= 0 && zc.in[0][0] + (long long)(k0 + Z2KC - 1) * R + tk.ncols - 1 < LR, DBG_VEC);
           const double2* base = (zc.alt[0] ? srcB : srcA) + zc.in[0][0] + (long long)k0 * R;
           for (int r = lane; r < Z2KC; r += 32)
             z2_copy(sb + r * F::SB, base + (long long)r * R, tk.ncols * sizeof(double2), &full[st]);
@@ -754,6 +768,7 @@ __global__ void __launch_bounds__(Z2<BN, TM, TN, NMAJ, S, PERS, KG>::THREADS, 1)
           }
         }
         toff[u] = t;
+        HS_DCHECK(t < LR, DBG_VEC);
         if (t >= 0) xin[u] = epi_load(e, t);
       }
 #pragma unroll
@@ -1075,6 +1090,8 @@ void launch_zmma(Ctx& c, const DevMma& m, const double2* A, const double2* srcA,
       cfg.gridDim = dim3(m.ntasks * KS);
     }
     attr[0].val.clusterDim.x = KS;
+    const long long Aelems = (long long)(A == c.Tcls ? c.Tcls_elems : c.T_elems);
+    const long long LR = c.plan.L * (long long)R;
     unsigned long long* tr = nullptr;
     const int seq = (int)(c.launches & 0xFFFFFF);
     if (c.trace_on && c.trace && (size_t)c.trace_rows + cfg.gridDim.x <= c.trace_cap) {
@@ -1086,7 +1103,7 @@ void launch_zmma(Ctx& c, const DevMma& m, const double2* A, const double2* srcA,
     cfg.blockDim = dim3(F::THREADS);                                                                            \
     cfg.dynamicSmemBytes = F::SMEM;                                                                             \
     cudaLaunchKernelEx(&cfg, K, (const MmaTask*)m.tasks, m.ntasks, (const MmaCol*)m.cols, A, srcA, srcB, zeros, \
-                       e, c.n, R, KS, tr, seq);                                                                 \
+                       e, c.n, R, KS, tr, seq, Aelems, LR);                                                     \
   } while (0)
     if (m.kind == 2 && m.bn == 64) Z2_LAUNCH(Z2Cols64, Z2K_COLS64);
     else if (m.kind == 2) Z2_LAUNCH(Z2Cols32, Z2K_COLS32);
@@ -1185,5 +1202,7 @@ void launch_pack_strips(Ctx& c, const double2* T4, double2* out, int rows, int c
   c.launches++;
   k_pack_strips<<<4 * c.num_sms, 256, 0, c.stream>>>(T4, out, rows, cols);
 }
+
+HS_DBG_ACCESSOR(hs_dbg_take_zmma)
 
 }  // namespace hs

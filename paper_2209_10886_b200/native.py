@@ -15,7 +15,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libhsb200.so")
+# HS_LIB=debug: the device-checks build (bounds asserts + spin watchdogs,
+# include/hsb200.h hs_debug_check); same ABI, same arithmetic
+LIB_PATH = os.path.join(_HERE, "_lib", "libhsb200_debug.so" if os.environ.get("HS_LIB") == "debug" else "libhsb200.so")
 
 HS_MEM_HOST, HS_MEM_DEVICE = 0, 1
 HS_APPLY_S, HS_APPLY_IMS = 0, 1
@@ -58,6 +60,8 @@ _SIGS = {
     "hs_get_schur": (_I, [_P, _I, _I, _P]),
     "hs_gmres_basis": (_I, [_P, _P, _I, C.POINTER(_I)]),
     "hs_test_peer_allreduce": (_I, [_P, _I, _I, _I, _P, _P]),
+    "hs_debug_check": (_I, [_P, C.POINTER(C.c_uint64), C.POINTER(_I)]),
+    "hs_debug_selftest": (_I, [_P]),
     "hs_set_schur": (_I, [_P, _I, _I, _P]),
     "hs_set_async": (_I, [_P, _I]),
     "hs_sync": (_I, [_P]),
