@@ -173,8 +173,11 @@ int hs_set_emulated_ranks(hs_ctx* ctx, int ranks);
  * clear; otherwise the map-once plan computes the same z with every map row
  * read about once per apply (the intermediate residual vanishes inside the
  * forward windows and shares the backward steps' map reads),
- * equal to the step sequence to rounding.  Bit 1 (default off): the fused
- * launch for the DMMA contraction (R RHS or shared maps). */
+ * equal to the step sequence to rounding.  Bit 1 (default on): R right-hand
+ * sides on the per-subdomain maps run as one dataflow launch on the DMMA
+ * contraction (k_zmma2_df: the step sequence's arithmetic, list-scheduled
+ * tickets); bit 3 (default off) also the shared class maps (k_zmma_fused).
+ * Default mask 3. */
 int hs_set_fused(hs_ctx* ctx, int mask);
 
 /* Row-band ranks on separate GPUs (one process per GPU, nranks > 1 and

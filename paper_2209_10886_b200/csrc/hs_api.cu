@@ -10,6 +10,7 @@
 #include <cstring>
 #include <map>
 #include <queue>
+#include <type_traits>
 #include <tuple>
 #include <set>
 #include <string>
@@ -346,8 +347,15 @@ void free_fused_mma(Ctx* c) {
   dfree(c, f.deps, f.ndeps * sizeof(FusedDep));
   dfree(c, f.incs, f.nincs * sizeof(int));
   dfree(c, f.counters, (f.ncounters + 1) * sizeof(int));
+  dfree(c, f.split_buf, 0);
+  dfree(c, f.split_cnt, 0);
   f = DevFusedMma();
 }
+
+template <class Tile>
+std::vector<Tile> list_schedule(const std::vector<Tile>& tiles, const std::vector<FusedDep>& deps,
+                                const std::vector<std::vector<int>>& tile_inc, const std::vector<double>& cost,
+                                int nblocks, int workers, double fixed, double rate);
 
 // Dataflow plan of one BSP apply on the DMMA contraction: every task of the
 // forward steps, the residual and the backward steps in schedule order, with
@@ -400,6 +408,46 @@ int build_fused_mma(Ctx* c, int R, bool shared) {
   for (auto& st : c->fwd) add(st, 0);
   add(c->full, 1);
   for (auto& st : c->bwd) add(st, 2);
+  // k_zmma2_df split-K (opt-in, HS_ZMMA2_SPLIT=1): the sweep steps' tasks (the
+  // dependency chain) in two K halves on two CTAs; the later arrival adds the
+  // halves in half order and finishes the task.  Measured slower at cfg4
+  // (0.272 vs 0.239 ms per apply): the partial exchange and the extra tickets
+  // cost more than the halved contraction saves.  Not for the shared maps.
+  static const bool split = getenv("HS_ZMMA2_SPLIT") && atoi(getenv("HS_ZMMA2_SPLIT")) != 0;
+  int npairs = 0;
+  if (split && !shared) {
+    std::vector<FusedMmaTask> sp;
+    sp.reserve(ftasks.size() * 2);
+    for (const FusedMmaTask& ft : ftasks) {
+      if (ft.phase == 1 || ft.task.K / 32 < 4) {
+        sp.push_back(ft);
+        continue;
+      }
+      FusedMmaTask h = ft;
+      h.pair = npairs++;
+      h.ks = 0;
+      sp.push_back(h);
+      h.ks = 1;
+      sp.push_back(h);
+    }
+    ftasks.swap(sp);
+  }
+  {
+    // ticket order: list-scheduled on one CTA per SM (HS_FUSED_ORDER=0: plan
+    // order); a task costs ~1 us per 32-column k chunk + ~3 us of latency
+    static const bool reorder = !(getenv("HS_FUSED_ORDER") && atoi(getenv("HS_FUSED_ORDER")) == 0);
+    if (reorder) {
+      std::vector<std::vector<int>> tinc(ftasks.size());
+      std::vector<double> cost(ftasks.size());
+      for (size_t t = 0; t < ftasks.size(); ++t) {
+        // a pair's completions are its second arrival's: counted once, on half 1
+        if (ftasks[t].ks != 0)
+          tinc[t].assign(incs.begin() + ftasks[t].inc0, incs.begin() + ftasks[t].inc0 + ftasks[t].ninc);
+        cost[t] = ftasks[t].task.K / 32 / (ftasks[t].ks >= 0 ? 2 : 1);
+      }
+      ftasks = list_schedule(ftasks, deps, tinc, cost, ncnt, c->num_sms, 3e-6, 1e6);
+    }
+  }
   {
     std::vector<MmaTask> plain;
     for (auto& ft : ftasks) plain.push_back(ft.task);
@@ -409,6 +457,12 @@ int build_fused_mma(Ctx* c, int R, bool shared) {
       upload(c, &f.incs, incs))
     return -1;
   CK(dalloc(c, (void**)&f.counters, (ncnt + 1) * sizeof(int)));
+  f.npairs_split = npairs;
+  if (npairs > 0) {
+    CK(dalloc(c, (void**)&f.split_buf, (size_t)npairs * 2 * 32 * 32 * sizeof(double2)));
+    CK(dalloc(c, (void**)&f.split_cnt, (size_t)npairs * sizeof(int)));
+    CK(cudaMemsetAsync(f.split_cnt, 0, (size_t)npairs * sizeof(int), c->stream));
+  }
   f.ntasks = (int)ftasks.size();
   f.ncols = (int)cols.size();
   f.ndeps = (int)deps.size();
@@ -484,9 +538,27 @@ void free_fused(Ctx* c) {
 // result is a topological order of the dependency graph (a tile's
 // predecessors are the first `count` writers of each block it waits on), so
 // any such order keeps the plan deadlock-free and the arithmetic unchanged.
+// Ticket order of a dataflow plan: list-schedule the dependency graph on
+// `workers` resident CTAs, greedy by the longest path to the end (bottom
+// level), and return the tasks in the order they would start.  Any
+// topological order is deadlock-free; every writer of a block depends on the
+// block's earlier writers, so the per-block completion counts keep their
+// meaning.  dur[t] = fixed + cost[t] / rate.
+template <class Tile>
+std::vector<Tile> list_schedule(const std::vector<Tile>& tiles, const std::vector<FusedDep>& deps,
+                                const std::vector<std::vector<int>>& tile_inc, const std::vector<double>& cost,
+                                int nblocks, int workers, double fixed, double rate);
+
 std::vector<FusedTile> schedule_tickets(const std::vector<FusedTile>& tiles, const std::vector<FusedDep>& deps,
                                         const std::vector<std::vector<int>>& tile_inc,
                                         const std::vector<double>& cost, int nblocks, int workers) {
+  return list_schedule(tiles, deps, tile_inc, cost, nblocks, workers, 3e-6, 6.5e12 / std::max(1, workers));
+}
+
+template <class Tile>
+std::vector<Tile> list_schedule(const std::vector<Tile>& tiles, const std::vector<FusedDep>& deps,
+                                const std::vector<std::vector<int>>& tile_inc, const std::vector<double>& cost,
+                                int nblocks, int workers, double fixed, double rate) {
   const int T = (int)tiles.size();
   std::vector<std::vector<int>> writers(nblocks);
   for (int t = 0; t < T; ++t)
@@ -499,17 +571,18 @@ std::vector<FusedTile> schedule_tickets(const std::vector<FusedTile>& tiles, con
       const FusedDep& dp = deps[tiles[t].dep0 + d];
       for (int i = 0; i < dp.count; ++i) pre.push_back(writers[dp.block][i]);
     }
-    // split-K: half 1 (the pair's writer in `writers`) finishes after half 0
+    // split-K: half 1 (the pair's writer in `writers`) goes after half 0, so
+    // every successor of the pair gets a later ticket than BOTH halves (the
+    // completion is signalled by whichever half arrives second; a successor
+    // ticketed before half 0 could spin on a counter no running CTA will bump)
     if (tiles[t].ks == 1 && t > 0 && tiles[t - 1].pair == tiles[t].pair) pre.push_back(t - 1);
     std::sort(pre.begin(), pre.end());
     pre.erase(std::unique(pre.begin(), pre.end()), pre.end());
     npred[t] = (int)pre.size();
     for (int p : pre) succ[p].push_back(t);
   }
-  const double bw = 6.5e12 / std::max(1, workers);  // bytes/s per CTA
-  const double fixed = 3e-6;                         // ticket, waits, slab, epilogue
   std::vector<double> dur(T), bl(T, 0.0), ready(T, 0.0);
-  for (int t = 0; t < T; ++t) dur[t] = fixed + cost[t] / bw;
+  for (int t = 0; t < T; ++t) dur[t] = fixed + cost[t] / rate;
   for (int t = T - 1; t >= 0; --t) {  // successors come later in plan order
     double m = 0;
     for (int s : succ[t]) m = std::max(m, bl[s]);
@@ -521,7 +594,7 @@ std::vector<FusedTile> schedule_tickets(const std::vector<FusedTile>& tiles, con
   for (int w = 0; w < workers; ++w) freew.push({0.0, w});
   for (int t = 0; t < T; ++t)
     if (npred[t] == 0) waiting.push({0.0, t});
-  std::vector<FusedTile> out;
+  std::vector<Tile> out;
   out.reserve(T);
   while ((int)out.size() < T) {
     const double tau = freew.top().first;
@@ -1378,7 +1451,11 @@ int do_precond_ims(Ctx* c, const double2* r, double2* z, double2* wout) {
 // The per-step BSP in map-once form (dedup seams, intermediate residual, not
 // the literal-arithmetic mask bit 2).
 bool mma_fused_path(const Ctx* c, int R) {
-  return (c->fused_mode & 2) && (R > 1 || c->map_mode == 1) && c->n % 32 == 0 && c->plan.nranks == 1 && c->inter &&
+  // R right-hand sides on the per-subdomain maps: k_zmma2_df (bit 1, default
+  // on); the shared class maps: k_zmma_fused only on request (bit 3), the
+  // per-step k_zmma2 measured faster there
+  return (c->fused_mode & 2) && ((R > 1 && c->map_mode != 1) || (c->map_mode == 1 && (c->fused_mode & 8))) &&
+         c->n % 32 == 0 && c->plan.nranks == 1 && c->inter &&
          c->seam == HS_SEAM_DEDUP && c->full.nitems > 0;
 }
 
@@ -2543,7 +2620,7 @@ int hs_stream(hs_ctx* c, uint64_t* s) {
 int hs_set_fused(hs_ctx* c, int mask) {
   if (!c) return fail(nullptr, 1, "null context");
   DEV_SCOPE(c);
-  if (mask < 0 || mask > 7) return fail(c, 1, "fused mask must be 0..7");
+  if (mask < 0 || mask > 15) return fail(c, 1, "fused mask must be 0..15");
   if ((mask ^ c->fused_mode) & 4) {  // plan kind changed: rebuild the fused plans
     free_fused(c);
     free_emu(c);

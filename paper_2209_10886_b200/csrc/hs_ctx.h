@@ -168,6 +168,8 @@ struct FusedMmaTask {
   int phase;       // 0 forward, 1 residual, 2 backward
   int dep0, ndep;  // waits: counters[block * nchunk + chunk] >= count
   int inc0, ninc;  // counters this task completes
+  int ks = -1;     // k_zmma2_df split-K: half 0 / 1 of pair `pair` (-1: whole K)
+  int pair = -1;
 };
 
 struct DevFusedMma {
@@ -182,6 +184,9 @@ struct DevFusedMma {
   double flops = 0;
   int R = 0;
   bool shared = false, built = false;
+  int npairs_split = 0;          // split-K pairs (k_zmma2_df)
+  double2* split_buf = nullptr;  // [pair][half][32 x 32] partial tiles
+  int* split_cnt = nullptr;      // [pair] arrivals (never reset: the odd arrival combines)
 };
 
 struct FusedMmaArgs {
@@ -198,6 +203,9 @@ struct FusedMmaArgs {
   int* done;
   int* ticket;
   int ntasks, n, R;
+  unsigned long long* trace = nullptr;  // k_zmma2_df, per ticket: claimed, inputs met, first chunk, contracted, signalled, info
+  double2* split_buf = nullptr;
+  int* split_cnt = nullptr;
 };
 
 // Row-band ranks of the fused apply (multi-rank kernel instantiations): every
@@ -352,7 +360,7 @@ struct Ctx {
   EmuRanks emu;          // emulated row-band ranks for the fused apply (tests)
   PeerRanks peer;        // row-band ranks on separate GPUs (fused apply over CUDA IPC)
   DevFusedMma fused_mma; // the same on the DMMA contraction (R RHS or shared maps)
-  int fused_mode = 1;    // 1: use the fused kernel when applicable, 0: one launch per step
+  int fused_mode = 3;    // bit 0: 1-RHS dataflow apply, bit 1: R-RHS DMMA dataflow apply (hs_set_fused)
   std::vector<std::vector<int>> seam_blocks;  // [dir] blocks of seam groups (literal mode)
   int* d_seam[2] = {nullptr, nullptr};
   int n_seam[2] = {0, 0};

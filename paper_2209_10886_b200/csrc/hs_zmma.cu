@@ -1126,12 +1126,342 @@ void launch_zmma(Ctx& c, const DevMma& m, const double2* A, const double2* srcA,
                      c.n, R, KS);
 }
 
+// ---------------------------------------------------------------------------
+// k_zmma2_df: the whole R-RHS BSP apply as ONE persistent dataflow launch on
+// the k_zmma2 core.  The plan is build_fused_mma's: every 32-row x 32-RHS task
+// of the forward steps (phase 0), the residual step (1) and the backward steps
+// (2) in schedule order (a topological order), with per-(block, 32-RHS chunk)
+// completion counters it waits for / completes.  One CTA per SM: a producer
+// warp claims tickets, stages the task's column table (double-buffered),
+// streams the map chunks -- the first S before the task's dependencies are
+// met, since maps depend on nothing -- waits for the dependencies, then
+// streams the slab rows (after fence.proxy.async: generic-proxy stores of
+// other CTAs, async-proxy reads here).  Two groups of 4 consumer warps split
+// each chunk's k range; the tile goes through shared memory to a coalesced
+// epilogue; one thread then releases the task's completion counters.  A task
+// waits only for lower tickets, held by running CTAs: deadlock-free with every
+// CTA resident (grid <= #SMs).  Phase arithmetic (k_zmma_fused's):
+//   0 forward   y = T (zL | r):  zL += y
+//   1 residual  y = T zL:        v = r - (zL - y); rp = w = v; z = zL + v
+//   2 backward  y = T (w | rp):  w += y; z += y
+constexpr int kDfStages = 4;
+struct DfCols {
+  ZCols2<32> c;
+  int phase, inc0, ninc, stop, ks, pair;
+  unsigned long long* tr;
+};
+
+template <int S>
+__global__ void __launch_bounds__(Z2<32, 2, 2, false, S, false, 2>::THREADS, 1) k_zmma2_df(FusedMmaArgs a) {
+  using F = Z2<32, 2, 2, false, S, false, 2>;
+  extern __shared__ __align__(128) double2 sm[];
+  __shared__ __align__(8) unsigned long long full[S], empty[S], dfull[2], dempty[2];
+  __shared__ DfCols zcs[2];
+  double2* ys = sm + F::RING;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int n = a.n, R = a.R;
+  if (warp == F::NWC && lane == 0) {
+    for (int i = 0; i < S; ++i) z2_bar_init(&full[i], 1), z2_bar_init(&empty[i], F::NWC);
+    for (int i = 0; i < 2; ++i) z2_bar_init(&dfull[i], 1), z2_bar_init(&dempty[i], F::NWC);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == F::NWC) {  // ---------------- producer
+    long long g = 0;
+    for (int it = 0;; ++it) {
+      const int d = it & 1;
+      DfCols& zd = zcs[d];
+      z2_wait(&dempty[d], (unsigned)((it >> 1) & 1) ^ 1);
+      int t = 0;
+      if (lane == 0) t = atomicAdd(a.ticket, 1);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      if (t >= a.ntasks) {
+        if (lane == 0) {
+          zd.stop = 1;
+          z2_arrive(&dfull[d]);
+        }
+        break;
+      }
+      unsigned long long* tr = a.trace ? a.trace + 6ull * t : nullptr;
+      if (tr && lane == 0) tr[0] = z2_gtimer();
+      const FusedMmaTask ft = a.tasks[t];
+      const MmaTask tk = ft.task;
+      HS_DCHECK(tk.ncols >= 1 && tk.ncols <= 32 && tk.K % Z2KC == 0, DBG_INDEX);
+      for (int j = lane; j < 32; j += 32) {
+        if (j < tk.ncols) {
+          const MmaCol c = a.cols[tk.col0 + j];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) zd.c.in[j][q] = c.in[q], zd.c.out[j][q] = c.out[q], zd.c.slot[j][q] = c.slot[q];
+          zd.c.r[j] = c.r;
+          zd.c.alt[j] = c.alt;
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) zd.c.in[j][q] = zd.c.out[j][q] = -1, zd.c.slot[j][q] = -1;
+          zd.c.r[j] = 0;
+          zd.c.alt[j] = 0;
+        }
+      }
+      if (lane == 0) {
+        zd.c.tk = tk;
+        zd.phase = ft.phase;
+        zd.inc0 = ft.inc0;
+        zd.ninc = ft.ninc;
+        zd.stop = 0;
+        zd.tr = tr;
+        zd.ks = ft.ks;
+        zd.pair = ft.pair;
+      }
+      __syncwarp();
+      if (lane == 0) z2_arrive(&dfull[d]);  // release: the table is visible to the consumers
+      const double2* srcA = ft.phase == 0 ? a.zL : (ft.phase == 1 ? a.zL : a.w);
+      const double2* srcB = ft.phase == 0 ? a.r : (ft.phase == 1 ? a.zL : a.rp);
+      const int nkall = tk.K / Z2KC;
+      const int kc0 = ft.ks == 1 ? nkall / 2 : 0;
+      const int nk = ft.ks == 0 ? nkall / 2 : nkall - kc0;
+      const unsigned bytes = (unsigned)(Z2KC * 32 * sizeof(double2)) + (unsigned)(Z2KC * tk.ncols * sizeof(double2));
+      const double2* Ab = a.A + tk.a_off;
+      const double2* base = (zd.c.alt[0] ? srcB : srcA) + zd.c.in[0][0];
+      auto issueA = [&](int st, int kc) {
+        if (lane == 0)
+          z2_copy(sm + (size_t)st * F::STAGE, Ab + (long long)kc * Z2KC * 32, Z2KC * 32 * sizeof(double2), &full[st]);
+      };
+      auto issueB = [&](int st, int kc) {
+        double2* sb = sm + (size_t)st * F::STAGE + Z2KC * F::SA;
+        const double2* b0 = base + (long long)kc * Z2KC * R;
+        for (int r = lane; r < Z2KC; r += 32)
+          z2_copy(sb + r * F::SB, b0 + (long long)r * R, tk.ncols * sizeof(double2), &full[st]);
+      };
+      // the map chunks of the first stages stream while the dependencies settle
+      const int pre = nk < S ? nk : S;
+      const long long g0 = g;
+      for (int i = 0; i < pre; ++i, ++g) {
+        const int st = (int)(g % S);
+        if (g >= S) z2_wait(&empty[st], (unsigned)((g / S) & 1) ^ 1);
+        if (lane == 0) z2_expect_tx(&full[st], bytes);
+        __syncwarp();
+        issueA(st, kc0 + i);
+      }
+      for (int q = lane; q < ft.ndep; q += 32) {
+        const FusedDep dp = a.deps[ft.dep0 + q];
+        const volatile int* pc = a.done + dp.block;
+        HS_WAIT(*pc < dp.count, 32, DBG_DEPWAIT);
+      }
+      __syncwarp();
+      __threadfence();
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      if (tr && lane == 0) tr[1] = z2_gtimer();
+      for (int i = 0; i < pre; ++i) issueB((int)((g0 + i) % S), kc0 + i);
+      for (int i = pre; i < nk; ++i, ++g) {
+        const int st = (int)(g % S);
+        z2_wait(&empty[st], (unsigned)((g / S) & 1) ^ 1);
+        if (lane == 0) z2_expect_tx(&full[st], bytes);
+        __syncwarp();
+        issueA(st, kc0 + i);
+        issueB(st, kc0 + i);
+      }
+    }
+    return;
+  }
+  // ---------------- consumers (warps 0 .. 7: two groups of 4 quadrant warps)
+  const int kg = warp / F::NWQ, wq = warp % F::NWQ;
+  const int wm = wq / F::WN, wn = wq % F::WN;
+  const int gid = lane >> 2, tig = lane & 3;
+  constexpr int KH = Z2KC / 2;
+  constexpr int NT = 2 * 2 * 2;
+  long long g = 0;
+  for (int it = 0;; ++it) {
+    const int d = it & 1;
+    z2_wait(&dfull[d], (unsigned)((it >> 1) & 1));
+    const DfCols& zd = zcs[d];
+    if (zd.stop) break;
+    const MmaTask tk = zd.c.tk;
+    const int phase = zd.phase, ks = zd.ks;
+    const int nk = ks == 0 ? tk.K / Z2KC / 2 : (ks == 1 ? tk.K / Z2KC - tk.K / Z2KC / 2 : tk.K / Z2KC);
+    double cr[2][2][2], ci[2][2][2], p3[2][2][2];
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int y = 0; y < 2; ++y)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) cr[x][y][c] = ci[x][y][c] = p3[x][y][c] = 0.0;
+    unsigned long long* tr = zd.tr;
+    long long toff[F::EPT];
+    double2 u1[F::EPT], u2[F::EPT];
+    for (int i = 0; i < nk; ++i, ++g) {
+      const int st = (int)(g % S);
+      z2_wait(&full[st], (unsigned)((g / S) & 1));
+      if (i == 0) {
+        if (tr && tid == 0) tr[2] = z2_gtimer();
+        // the first chunk landed, so the producer saw every dependency met: the
+        // epilogue operands are final -- fetch them now, in the contraction's shadow
+#pragma unroll
+        for (int u = 0; u < F::EPT; ++u) {
+          const int el = u * F::NWC * 32 + tid;
+          const int rr = el / 32, j = el % 32;
+          const int row = tk.r0 + rr;
+          long long t = -1;
+          if (row >= tk.rlo && row < tk.rhi && j < tk.ncols) {
+            const int q = row / n, p = row - q * n;
+            const long long off = zd.c.out[j][q];
+            if (off >= 0) t = off + (long long)p * R;
+          }
+          toff[u] = t;
+          if (t >= 0) {
+            if (phase == 0) u1[u] = __ldcg(a.zL + t);
+            else if (phase == 1) { u1[u] = __ldcg(a.r + t); u2[u] = __ldcg(a.zL + t); }
+            else { u1[u] = __ldcg(a.w + t); u2[u] = __ldcg(a.z + t); }
+          }
+        }
+      }
+      const double2* sa = sm + (size_t)st * F::STAGE;
+      const double2* sb = sa + Z2KC * F::SA;
+#pragma unroll
+      for (int kk = 0; kk < KH; kk += 4) {
+        const int k4 = kg * KH + kk;
+        double2 av[2], bv[2];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) av[mt] = sa[(k4 + tig) * F::SA + (wm * 2 + mt) * 8 + gid];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) bv[nt] = sb[(k4 + tig) * F::SB + (wn * 2 + nt) * 8 + gid];
+        double s_b[2];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) s_b[nt] = bv[nt].x + bv[nt].y;
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          const double s_a = av[mt].x + av[mt].y;
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) dmma(cr[mt][nt][0], cr[mt][nt][1], av[mt].x, bv[nt].x);
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) dmma(ci[mt][nt][0], ci[mt][nt][1], av[mt].y, bv[nt].y);
+#pragma unroll
+          for (int nt = 0; nt < 2; ++nt) dmma(p3[mt][nt][0], p3[mt][nt][1], s_a, s_b[nt]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) z2_arrive(&empty[st]);
+    }
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int y = 0; y < 2; ++y)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const double s1 = cr[x][y][c], s2 = ci[x][y][c];
+          cr[x][y][c] = s1 - s2;
+          ci[x][y][c] = p3[x][y][c] - s1 - s2;
+        }
+    if (tr && tid == 0) tr[3] = z2_gtimer();
+    // group 1 hands its partial tile to group 0 through the output-tile buffer's
+    // tail; group 0 adds it and writes the tile
+    double2* red = ys + 32 * F::YS;
+    consumers_bar<F::NWC * 32>();  // the previous task's tile readers are done
+    if (kg == 1) {
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < 2; ++y)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) red[(wq * NT + (x * 2 + y) * 2 + c) * 32 + lane] = make_double2(cr[x][y][c], ci[x][y][c]);
+    }
+    consumers_bar<F::NWC * 32>();
+    if (kg == 0) {
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < 2; ++y)
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const double2 o = red[(wq * NT + (x * 2 + y) * 2 + c) * 32 + lane];
+            ys[((wm * 2 + x) * 8 + gid) * F::YS + (wn * 2 + y) * 8 + 2 * tig + c] =
+                make_double2(cr[x][y][c] + o.x, ci[x][y][c] + o.y);
+          }
+    }
+    consumers_bar<F::NWC * 32>();
+    bool finish = true;
+    const double2* other = nullptr;
+    if (ks >= 0) {
+      // split-K: publish this half's tile; the pair's second arrival adds the
+      // halves in half order (deterministic) and finishes the task
+      __shared__ int s_old;
+      double2* mine = a.split_buf + ((size_t)zd.pair * 2 + ks) * 1024;
+#pragma unroll
+      for (int u = 0; u < F::EPT; ++u) {
+        const int el = u * F::NWC * 32 + tid;
+        mine[el] = ys[(el / 32) * F::YS + (el % 32)];
+      }
+      consumers_bar<F::NWC * 32>();
+      if (tid == 0) {
+        __threadfence();
+        s_old = atomicAdd(a.split_cnt + zd.pair, 1);
+        __threadfence();
+      }
+      consumers_bar<F::NWC * 32>();
+      finish = s_old & 1;
+      other = a.split_buf + ((size_t)zd.pair * 2 + (1 - ks)) * 1024;
+    }
+    // coalesced epilogue: element el = row * 32 + column (consecutive RHS)
+#pragma unroll
+    for (int u = 0; u < F::EPT; ++u) {
+      const long long t = toff[u];
+      if (t < 0 || !finish) continue;
+      const int el = u * F::NWC * 32 + tid;
+      double2 y = ys[(el / 32) * F::YS + (el % 32)];
+      if (ks >= 0) {
+        const double2 o = __ldcg(other + el);
+        y = ks == 0 ? cadd(y, o) : cadd(o, y);
+      }
+      if (phase == 0) {
+        a.zL[t] = cadd(u1[u], y);
+      } else if (phase == 1) {
+        const double2 v = csub(u1[u], csub(u2[u], y));
+        a.rp[t] = v;
+        a.w[t] = v;
+        a.z[t] = cadd(u2[u], v);
+      } else {
+        a.w[t] = cadd(u1[u], y);
+        a.z[t] = cadd(u2[u], y);
+      }
+    }
+    consumers_bar<F::NWC * 32>();  // every epilogue store of the task issued
+    if (tid == 0 && finish) {
+      __threadfence();  // release the task's outputs, then count them done
+      for (int i = 0; i < zd.ninc; ++i) atomicAdd(a.done + a.incs[zd.inc0 + i], 1);
+      if (tr) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        tr[4] = z2_gtimer();
+        tr[5] = ((unsigned long long)smid << 32) | ((unsigned long long)blockIdx.x << 8) | (unsigned)phase;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) z2_arrive(&dempty[d]);
+  }
+}
+
 cudaError_t launch_zmma_fused(Ctx& c, const DevFusedMma& f, FusedMmaArgs a) {
   cudaError_t e = cudaMemsetAsync(f.counters, 0, (f.ncounters + 1) * sizeof(int), c.stream);
   if (e != cudaSuccess) return e;
   a.tasks = f.tasks; a.cols = f.cols; a.deps = f.deps; a.incs = f.incs;
+  a.split_buf = f.split_buf; a.split_cnt = f.split_cnt;
   a.done = f.counters; a.ticket = f.counters + f.ncounters;
   a.ntasks = f.ntasks; a.n = c.n;
+  // the k_zmma2 core for per-subdomain slabs (32-column tasks of consecutive
+  // right-hand sides); HS_ZMMA2=0 keeps k_zmma_fused
+  static const bool z2 = !(getenv("HS_ZMMA2") && atoi(getenv("HS_ZMMA2")) == 0);
+  if (z2 && !f.shared) {
+    using F = Z2<32, 2, 2, false, kDfStages, false, 2>;
+    constexpr size_t smem = F::SMEM + sizeof(double2) * 32 * F::YS + sizeof(double2) * F::NWQ * 8 * 32;
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(k_zmma2_df<kDfStages>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (attr != cudaSuccess) return attr;
+    c.launches++;
+    if (c.trace_on && c.trace && (size_t)f.ntasks <= c.trace_cap) {
+      a.trace = c.trace;
+      c.trace_rows = f.ntasks;
+    }
+    k_zmma2_df<kDfStages><<<std::min(f.ntasks, c.num_sms), F::THREADS, smem, c.stream>>>(a);
+    return cudaGetLastError();
+  }
   // K split over a cluster: KS ranks each keep >= 2 K chunks (HS_ZMMA_FUSED_KS overrides)
   static const int ks_env = getenv("HS_ZMMA_FUSED_KS") ? atoi(getenv("HS_ZMMA_FUSED_KS")) : 0;
   int KS = ks_env > 0 ? ks_env : 1;

@@ -200,15 +200,16 @@ class GpuInterfaceSystem:
         # map-once plan (each map row read ~once per apply; equal to the step
         # sequence to rounding); fused=False one launch per step, also in
         # map-once form; fused="steps" / "literal" the literal SPEC arithmetic
-        # as one launch / per step (bitwise equal to each other); fused=3 also
-        # fuses the DMMA contraction paths (opt-in); an int is the raw
-        # hs_set_fused mask
+        # as one launch / per step (bitwise equal to each other); R
+        # right-hand sides run the DMMA dataflow launch (k_zmma2_df) under
+        # fused=True too; an int is the raw hs_set_fused mask (8: the shared
+        # maps' fused DMMA launch as well)
         if isinstance(fused, str):
             if fused not in ("steps", "literal"):
                 raise ValueError(f"fused must be a bool, an int mask, 'steps' or 'literal', got {fused!r}")
             mask = 5 if fused == "steps" else 4
         elif isinstance(fused, bool):
-            mask = 1 if fused else 0
+            mask = 3 if fused else 0
         else:
             mask = int(fused)
         self.ctx.call("hs_set_fused", mask)

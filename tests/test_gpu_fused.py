@@ -68,7 +68,8 @@ def test_fused_gmres_bitwise_equals_steps(name, c, blocks):
 def test_fused_dmma_equals_steps(name, c, R, maps):
     spec, part = product_problem(c)
     a = GpuInterfaceSystem(spec, part, fused=False, maps=maps, sweep=SweepConfig(blocks=c["blocks"]))
-    b = GpuInterfaceSystem(spec, part, fused=3, maps=maps, sweep=SweepConfig(blocks=c["blocks"]))
+    b = GpuInterfaceSystem(spec, part, fused=11 if maps == "shared" else 3, maps=maps,
+                           sweep=SweepConfig(blocks=c["blocks"]))
     g = cvec(17, a.layout.size, None if R == 1 else R)
     za = a.bsp_apply(g)
     zb = b.bsp_apply(g)
