@@ -315,7 +315,10 @@ int make_mma(Ctx* c, DevStep& st, int R, bool shared, DevMma** out) {
   else if (z2 && shared && R == 1) kind = 2, bn = 64;
   build_mma_host(c, st.host, R, shared, tasks, cols, flops, bn);
   static const int bn_env = getenv("HS_ZMMA2_BN") ? atoi(getenv("HS_ZMMA2_BN")) : 0;  // 32 / 64: fixed
-  if (bn == 64 && (bn_env == 32 || (bn_env != 64 && (int)tasks.size() < c->num_sms))) {
+  // shared maps: 32-column tasks (finer tasks balance the persistent residual
+  // step; the n-major 64-column tile is copy-bound); slabs: 32 when a step
+  // has fewer 64-column tasks than SMs
+  if (bn == 64 && (bn_env == 32 || (bn_env != 64 && (kind == 2 || (int)tasks.size() < c->num_sms)))) {
     // a step with fewer 64-column tasks than SMs: 32-column tasks, twice the CTAs
     tasks.clear(); cols.clear(); flops = 0; bn = 32;
     build_mma_host(c, st.host, R, shared, tasks, cols, flops, bn);
@@ -1767,6 +1770,7 @@ int hs_destroy(hs_ctx* c) {
       if (e) cudaEventDestroy(e);
     if (c->aux_fork) cudaEventDestroy(c->aux_fork);
     if (c->aux_join) cudaEventDestroy(c->aux_join);
+    if (c->z2_tickets) cudaFree(c->z2_tickets);
     if (c->aux) cudaStreamDestroy(c->aux);
     if (c->copy_in) cudaStreamDestroy(c->copy_in);
     if (c->copy_out) cudaStreamDestroy(c->copy_out);

@@ -12,7 +12,8 @@
 
 namespace hs {
 
-constexpr int kRowTile = 32;  // rows per tile of the tile-major map layout
+constexpr int kRowTile = 32;
+constexpr int kZ2TicketSlots = 64;  // k_zmma2 persistent launches' ticket counters (a ring)  // rows per tile of the tile-major map layout
 // Every 1-RHS step kernel (k_step1, k_bsp_fused, k_bsp_tma) splits a row's map
 // columns the same way -- column c into partial sum (c % 32) / (32 / kSumWarps),
 // accumulator c & 1, partials added in order -- so their results are bitwise
@@ -399,6 +400,9 @@ struct Ctx {
   int num_sms = 148;
   int coop_ok = 0;
   double2* zeros = nullptr;  // 64 zero elements: the source of absent faces in bulk-copied operands
+  unsigned* z2_tickets = nullptr;        // k_zmma2 persistent launches: a ring of ticket counters
+  unsigned z2_base[64] = {};             // per slot: claims so far (the next launch's first ticket)
+  unsigned long long z2_seq = 0;
 };
 
 }  // namespace hs

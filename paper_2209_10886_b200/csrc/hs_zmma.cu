@@ -360,7 +360,7 @@ struct Z2 {
   // pipe needs to stay busy (tools/zcore_bench.cu: 4 warps x 12 reach ~0.4)
   static constexpr int WM = 32 / (8 * TM), WN = BN / (8 * TN), NWQ = WM * WN, NWC = NWQ * KG,
                        THREADS = (NWC + 1) * 32;
-  static_assert(KG == 1 || !PERS, "the persistent form keeps one warp group");
+
   // A: the chunk's 32 k rows x 32 map rows are one contiguous 16 KB run of the
   // strip-major layout -> ONE bulk copy, unpadded (a small copy costs the TMA
   // unit ~60 cycles whatever its size, so 32 padded row copies made the
@@ -374,7 +374,11 @@ struct Z2 {
   static constexpr int RING = S * STAGE;
   // persistent: a separate output tile (the ring already holds the next task's
   // chunks); one task per CTA: the drained ring holds it
-  static constexpr size_t SMEM = sizeof(double2) * (RING + (PERS ? 32 * YS : 0));
+  static constexpr int NTR = TM * TN * 2;  // accumulator pairs per lane
+  // persistent: a separate output tile and warp-group reduction area (the ring
+  // already holds the next task's chunks); one task per CTA: the drained ring
+  static constexpr size_t SMEM =
+      sizeof(double2) * (RING + (PERS ? 32 * YS + (KG > 1 ? NWQ * NTR * 32 : 0) : 0));
   static constexpr int ND = PERS ? 2 : 1;  // task descriptor buffers
   static constexpr int EPT = 32 * BN / (NWC * 32);  // epilogue elements per consumer thread
   static_assert(WM * TM * 8 == 32 && WN * TN * 8 == BN, "tile split");
@@ -384,6 +388,7 @@ struct Z2 {
 template <int BN>
 struct ZCols2 {
   MmaTask tk;
+  int stop;  // persistent form: no more tickets
   long long in[BN][4];
   long long out[BN][4];
   int slot[BN][4];
@@ -487,7 +492,7 @@ __global__ void __launch_bounds__(Z2<BN, TM, TN, NMAJ, S, PERS, KG>::THREADS, 1)
     k_zmma2(const MmaTask* __restrict__ tasks, int ntasks, const MmaCol* __restrict__ cols,
             const double2* __restrict__ A, const double2* srcA, const double2* srcB,
             const double2* __restrict__ zeros, Epi e, int n, int R, int KS, unsigned long long* tr, int seq,
-            long long Aelems, long long LR) {
+            long long Aelems, long long LR, unsigned* ticket, unsigned tbase) {
   using F = Z2<BN, TM, TN, NMAJ, S, PERS, KG>;
   extern __shared__ __align__(128) double2 sm[];
   __shared__ __align__(8) unsigned long long full[S], empty[S], dfull[2], dempty[2];
@@ -496,8 +501,11 @@ __global__ void __launch_bounds__(Z2<BN, TM, TN, NMAJ, S, PERS, KG>::THREADS, 1)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int rank = (!PERS && KS > 1) ? (int)cg::this_cluster().block_rank() : 0;
-  const int t0 = PERS ? (int)blockIdx.x : (int)blockIdx.x / KS;
-  const int tstep = PERS ? (int)gridDim.x : ntasks;
+  // persistent form: tasks claimed from a ticket counter (this launch's slot
+  // of a ring of counters, never reset: tickets tbase, tbase + 1, ...), so
+  // CTAs that start late -- the previous step's CTAs still hold their SMs --
+  // take fewer tasks; one task per CTA otherwise
+  const int t0 = PERS ? 0 : (int)blockIdx.x / KS;
   // trace row (hs_set_trace): start, setup done, first chunk landed, contraction
   // done, end, (seq << 40 | smid << 32 | block)
   unsigned long long* trow = tr ? tr + 6ull * blockIdx.x : nullptr;
@@ -540,15 +548,28 @@ __global__ void __launch_bounds__(Z2<BN, TM, TN, NMAJ, S, PERS, KG>::THREADS, 1)
   if (trow && tid == 0) trow[1] = z2_gtimer();
   if (warp == F::NWC) {  // ---------------- producer
     long long g = 0;
-    for (int t = t0, it = 0; t < ntasks; t += tstep, ++it) {
+    for (int it = 0; PERS || it == 0; ++it) {
       const int d = PERS ? (it & 1) : 0;
       ZCols2<BN>& zc = zcs[d];
+      int t = t0;
+      if (PERS) {
+        z2_wait(&dempty[d], (unsigned)((it >> 1) & 1) ^ 1);
+        unsigned raw = 0;
+        if (lane == 0) raw = atomicAdd(ticket, 1u);
+        t = (int)(__shfl_sync(0xffffffffu, raw, 0) - tbase);
+        if (t >= ntasks) {
+          if (lane == 0) {
+            zc.stop = 1;
+            z2_arrive(&dfull[d]);
+          }
+          break;
+        }
+      }
       const MmaTask tk = tasks[t];
       HS_DCHECK(tk.a_off >= 0 && tk.a_off + (long long)tk.K * 32 <= Aelems && tk.K % Z2KC == 0, DBG_MAP);
       HS_DCHECK(tk.ncols >= 1 && tk.ncols <= BN, DBG_INDEX);
       if (PERS) {
-        z2_wait(&dempty[d], (unsigned)((it >> 1) & 1) ^ 1);
-        if (lane == 0) zc.tk = tk;
+        if (lane == 0) zc.tk = tk, zc.stop = 0;
         stage_cols(zc, tk, lane, 32);
         __syncwarp();
         if (lane == 0) z2_arrive(&dfull[d]);  // release: the table is visible to the consumers
@@ -612,10 +633,11 @@ __global__ void __launch_bounds__(Z2<BN, TM, TN, NMAJ, S, PERS, KG>::THREADS, 1)
     const int ctid = tid;  // consumers are warps 0 .. NWC - 1
     constexpr int KH = Z2KC / KG;  // k rows of a chunk per warp group
     long long g = 0;
-    for (int t = t0, it = 0; t < ntasks; t += tstep, ++it) {
+    for (int it = 0; PERS || it == 0; ++it) {
       const int d = PERS ? (it & 1) : 0;
       if (PERS) z2_wait(&dfull[d], (unsigned)((it >> 1) & 1));
       const ZCols2<BN>& zc = zcs[d];
+      if (PERS && zc.stop) break;
       const MmaTask tk = zc.tk;
       int kc0, nk;
       kslice(tk, kc0, nk);
@@ -672,7 +694,9 @@ __global__ void __launch_bounds__(Z2<BN, TM, TN, NMAJ, S, PERS, KG>::THREADS, 1)
       if (trow && tid == 0 && it == 0) trow[3] = z2_gtimer();
       constexpr int NT = TM * TN * 2;  // accumulator pairs per lane
       if (KG > 1) {
-        // group g > 0 hands its partial tile to group 0 (the drained ring holds it)
+        // group g > 0 hands its partial tile to group 0 (the drained ring holds
+        // it; the persistent form has its own area past the output tile)
+        double2* gred = PERS ? ys + 32 * F::YS : sm;
         consumers_bar<F::NWC * 32>();
         if (kg > 0) {
 #pragma unroll
@@ -681,7 +705,7 @@ __global__ void __launch_bounds__(Z2<BN, TM, TN, NMAJ, S, PERS, KG>::THREADS, 1)
             for (int b = 0; b < TN; ++b)
 #pragma unroll
               for (int c = 0; c < 2; ++c)
-                sm[((warp - F::NWQ) * NT + (a * TN + b) * 2 + c) * 32 + lane] = make_double2(cr[a][b][c], ci[a][b][c]);
+                gred[((warp - F::NWQ) * NT + (a * TN + b) * 2 + c) * 32 + lane] = make_double2(cr[a][b][c], ci[a][b][c]);
         }
         consumers_bar<F::NWC * 32>();
         if (kg == 0) {
@@ -691,7 +715,7 @@ __global__ void __launch_bounds__(Z2<BN, TM, TN, NMAJ, S, PERS, KG>::THREADS, 1)
             for (int b = 0; b < TN; ++b)
 #pragma unroll
               for (int c = 0; c < 2; ++c) {
-                const double2 o = sm[(warp * NT + (a * TN + b) * 2 + c) * 32 + lane];
+                const double2 o = gred[(warp * NT + (a * TN + b) * 2 + c) * 32 + lane];
                 cr[a][b][c] += o.x;
                 ci[a][b][c] += o.y;
               }
@@ -1058,10 +1082,12 @@ using Z2Slab64 = Z2<64, 2, 2, false, 3, true>;
 using Z2Slab32 = Z2<32, 2, 2, false, 4, false, 2>;
 using Z2Cols64 = Z2<64, 2, 2, true, 3, true>;
 using Z2Cols32 = Z2<32, 2, 2, true, 4, false, 2>;
+using Z2Cols32P = Z2<32, 2, 2, true, 4, true, 2>;
 #define Z2K_SLAB64 k_zmma2<64, 2, 2, false, 3, true, 1>
 #define Z2K_SLAB32 k_zmma2<32, 2, 2, false, 4, false, 2>
 #define Z2K_COLS64 k_zmma2<64, 2, 2, true, 3, true, 1>
 #define Z2K_COLS32 k_zmma2<32, 2, 2, true, 4, false, 2>
+#define Z2K_COLS32P k_zmma2<32, 2, 2, true, 4, true, 2>
 
 void launch_zmma(Ctx& c, const DevMma& m, const double2* A, const double2* srcA, const double2* srcB,
                  const double2* zeros, const Epi& e, int R) {
@@ -1080,7 +1106,10 @@ void launch_zmma(Ctx& c, const DevMma& m, const double2* A, const double2* srcA,
   c.launches++;
   if (m.kind != 0) {
     int KS = 1;
-    if (m.bn == 64) {
+    // persistent: 64-column slab tasks, or 32-column shared-map tasks when the
+    // step has at least one per SM
+    const bool pers = m.bn == 64 || (m.kind == 2 && m.ntasks >= c.num_sms);
+    if (pers) {
       cfg.gridDim = dim3(std::min(m.ntasks, c.num_sms));
     } else {
       // split K over a cluster while the step's tasks leave SMs idle and every
@@ -1090,6 +1119,20 @@ void launch_zmma(Ctx& c, const DevMma& m, const double2* A, const double2* srcA,
       cfg.gridDim = dim3(m.ntasks * KS);
     }
     attr[0].val.clusterDim.x = KS;
+    // ticket slot of a persistent launch (a ring: consecutive, possibly
+    // overlapping launches never share a counter); its claims = tasks + grid
+    unsigned* ticket = nullptr;
+    unsigned tbase = 0;
+    if (pers) {
+      if (!c.z2_tickets) {
+        if (cudaMalloc((void**)&c.z2_tickets, kZ2TicketSlots * sizeof(unsigned)) != cudaSuccess) return;
+        cudaMemsetAsync(c.z2_tickets, 0, kZ2TicketSlots * sizeof(unsigned), c.stream);
+      }
+      const int slot = (int)(c.z2_seq++ % kZ2TicketSlots);
+      ticket = c.z2_tickets + slot;
+      tbase = c.z2_base[slot];
+      c.z2_base[slot] += (unsigned)(m.ntasks + (int)cfg.gridDim.x);
+    }
     const long long Aelems = (long long)(A == c.Tcls ? c.Tcls_elems : c.T_elems);
     const long long LR = c.plan.L * (long long)R;
     unsigned long long* tr = nullptr;
@@ -1103,9 +1146,10 @@ void launch_zmma(Ctx& c, const DevMma& m, const double2* A, const double2* srcA,
     cfg.blockDim = dim3(F::THREADS);                                                                            \
     cfg.dynamicSmemBytes = F::SMEM;                                                                             \
     cudaLaunchKernelEx(&cfg, K, (const MmaTask*)m.tasks, m.ntasks, (const MmaCol*)m.cols, A, srcA, srcB, zeros, \
-                       e, c.n, R, KS, tr, seq, Aelems, LR);                                                     \
+                       e, c.n, R, KS, tr, seq, Aelems, LR, ticket, tbase);                                      \
   } while (0)
     if (m.kind == 2 && m.bn == 64) Z2_LAUNCH(Z2Cols64, Z2K_COLS64);
+    else if (m.kind == 2 && pers) Z2_LAUNCH(Z2Cols32P, Z2K_COLS32P);
     else if (m.kind == 2) Z2_LAUNCH(Z2Cols32, Z2K_COLS32);
     else if (m.bn == 64) Z2_LAUNCH(Z2Slab64, Z2K_SLAB64);
     else Z2_LAUNCH(Z2Slab32, Z2K_SLAB32);
@@ -1510,6 +1554,7 @@ cudaError_t set_zmma_smem_limit() {
   cudaFuncSetAttribute(Z2K_SLAB32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Slab32::SMEM);
   cudaFuncSetAttribute(Z2K_COLS64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cols64::SMEM);
   cudaFuncSetAttribute(Z2K_COLS32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cols32::SMEM);
+  cudaFuncSetAttribute(Z2K_COLS32P, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cols32P::SMEM);
   return cudaFuncSetAttribute(k_zmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kZmmaSmem);
 }
 
