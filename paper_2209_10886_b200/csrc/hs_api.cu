@@ -558,6 +558,55 @@ std::vector<FusedTile> schedule_tickets(const std::vector<FusedTile>& tiles, con
   return list_schedule(tiles, deps, tile_inc, cost, nblocks, workers, 3e-6, 6.5e12 / std::max(1, workers));
 }
 
+// Predecessor lists of a plan in plan order (a dependency (block, count) =
+// the block's first `count` writers).
+static std::vector<std::vector<int>> plan_preds(const std::vector<FusedTile>& tiles, const std::vector<FusedDep>& deps,
+                                                const std::vector<std::vector<int>>& tile_inc, int nblocks) {
+  const int T = (int)tiles.size();
+  std::vector<std::vector<int>> writers(nblocks), pre(T);
+  for (int t = 0; t < T; ++t)
+    for (int b : tile_inc[t]) writers[b].push_back(t);
+  for (int t = 0; t < T; ++t) {
+    for (int d = 0; d < tiles[t].ndep; ++d) {
+      const FusedDep& dp = deps[tiles[t].dep0 + d];
+      for (int i = 0; i < dp.count && i < (int)writers[dp.block].size(); ++i) pre[t].push_back(writers[dp.block][i]);
+    }
+    std::sort(pre[t].begin(), pre[t].end());
+    pre[t].erase(std::unique(pre[t].begin(), pre[t].end()), pre[t].end());
+  }
+  return pre;
+}
+
+// Longest modelled path from a tile to the end (including it) / from the start
+// to it (excluding it); dur = fixed + cost / rate.
+std::vector<double> bottom_levels(const std::vector<FusedTile>& tiles, const std::vector<FusedDep>& deps,
+                                  const std::vector<std::vector<int>>& tile_inc, const std::vector<double>& cost,
+                                  int nblocks, double fixed, double rate) {
+  const auto pre = plan_preds(tiles, deps, tile_inc, nblocks);
+  const int T = (int)tiles.size();
+  std::vector<double> bl(T, 0.0);
+  std::vector<std::vector<int>> succ(T);
+  for (int t = 0; t < T; ++t)
+    for (int p : pre[t]) succ[p].push_back(t);
+  for (int t = T - 1; t >= 0; --t) {
+    double m = 0;
+    for (int q : succ[t]) m = std::max(m, bl[q]);
+    bl[t] = fixed + cost[t] / rate + m;
+  }
+  return bl;
+}
+
+std::vector<double> top_levels(const std::vector<FusedTile>& tiles, const std::vector<FusedDep>& deps,
+                               const std::vector<std::vector<int>>& tile_inc, const std::vector<double>& cost,
+                               int nblocks, double fixed, double rate) {
+  const auto pre = plan_preds(tiles, deps, tile_inc, nblocks);
+  const int T = (int)tiles.size();
+  std::vector<double> tl(T, 0.0);
+  for (int t = 0; t < T; ++t)
+    for (int p : pre[t]) tl[t] = std::max(tl[t], tl[p] + fixed + cost[p] / rate);
+  return tl;
+}
+
 template <class Tile>
 std::vector<Tile> list_schedule(const std::vector<Tile>& tiles, const std::vector<FusedDep>& deps,
                                 const std::vector<std::vector<int>>& tile_inc, const std::vector<double>& cost,
@@ -574,11 +623,6 @@ std::vector<Tile> list_schedule(const std::vector<Tile>& tiles, const std::vecto
       const FusedDep& dp = deps[tiles[t].dep0 + d];
       for (int i = 0; i < dp.count; ++i) pre.push_back(writers[dp.block][i]);
     }
-    // split-K: half 1 (the pair's writer in `writers`) goes after half 0, so
-    // every successor of the pair gets a later ticket than BOTH halves (the
-    // completion is signalled by whichever half arrives second; a successor
-    // ticketed before half 0 could spin on a counter no running CTA will bump)
-    if (tiles[t].ks == 1 && t > 0 && tiles[t - 1].pair == tiles[t].pair) pre.push_back(t - 1);
     std::sort(pre.begin(), pre.end());
     pre.erase(std::unique(pre.begin(), pre.end()), pre.end());
     npred[t] = (int)pre.size();
@@ -597,8 +641,27 @@ std::vector<Tile> list_schedule(const std::vector<Tile>& tiles, const std::vecto
   for (int w = 0; w < workers; ++w) freew.push({0.0, w});
   for (int t = 0; t < T; ++t)
     if (npred[t] == 0) waiting.push({0.0, t});
+  // split-K pairs (ks = 0 / 1, adjacent in plan order, the same
+  // dependencies): emitted together -- consecutive tickets, so both halves
+  // stream at once -- and every successor (it depends on half 1, the pair's
+  // writer) gets a later ticket than BOTH halves: the completion is signalled
+  // by whichever half arrives second, and a successor ticketed before a half
+  // could spin on a counter no running CTA will bump.
+  std::vector<char> emitted(T, 0);
   std::vector<Tile> out;
   out.reserve(T);
+  auto partner = [&](int t) -> int {
+    if (tiles[t].ks == 0 && t + 1 < T && tiles[t + 1].ks == 1 && tiles[t + 1].pair == tiles[t].pair) return t + 1;
+    if (tiles[t].ks == 1 && t > 0 && tiles[t - 1].ks == 0 && tiles[t - 1].pair == tiles[t].pair) return t - 1;
+    return -1;
+  };
+  auto finish = [&](int t, double fin) {
+    freew.push({fin, 0});
+    for (int s : succ[t]) {
+      ready[s] = std::max(ready[s], fin);
+      if (--npred[s] == 0) waiting.push({ready[s], s});
+    }
+  };
   while ((int)out.size() < T) {
     const double tau = freew.top().first;
     freew.pop();
@@ -606,21 +669,37 @@ std::vector<Tile> list_schedule(const std::vector<Tile>& tiles, const std::vecto
       avail.push({bl[waiting.top().second], waiting.top().second});
       waiting.pop();
     }
-    int t;
-    if (!avail.empty()) {
-      t = avail.top().second;
+    int t = -1;
+    while (t < 0 && !avail.empty()) {
+      if (!emitted[avail.top().second]) t = avail.top().second;
       avail.pop();
-    } else {
-      t = waiting.top().second;
+    }
+    while (t < 0 && !waiting.empty()) {
+      if (!emitted[waiting.top().second]) t = waiting.top().second;
       waiting.pop();
     }
-    const double fin = std::max(tau, ready[t]) + dur[t];
-    out.push_back(tiles[t]);
-    freew.push({fin, 0});
-    for (int s : succ[t]) {
-      ready[s] = std::max(ready[s], fin);
-      if (--npred[s] == 0) waiting.push({ready[s], s});
+    if (t < 0) {  // everything left is a partner already emitted
+      freew.push({tau, 0});
+      continue;
     }
+    const int q = partner(t);
+    const int first = q >= 0 ? std::min(t, q) : t;
+    const double fin = std::max(tau, ready[t]) + dur[t];
+    emitted[t] = 1;
+    if (q < 0) {
+      out.push_back(tiles[t]);
+      finish(t, fin);
+      continue;
+    }
+    // the pair: half 0 first, the partner on the next free CTA
+    const double tau2 = freew.top().first;
+    freew.pop();
+    const double fin2 = std::max(tau2, ready[q]) + dur[q];
+    emitted[q] = 1;
+    out.push_back(tiles[first]);
+    out.push_back(tiles[first == t ? q : t]);
+    finish(t, fin);
+    finish(q, fin2);
   }
   return out;
 }
@@ -854,18 +933,34 @@ int fused_plan_host(const Ctx* c, const Plan& P, const std::vector<StepTable>& f
   // ms), but the doubled per-tile cost measured on one GPU (cfg5 1.30 -> 1.50
   // ms, cfg3 0.207 -> 0.274 ms) is far above the model's, so it stays off until
   // it can be measured on real row bands.
+  // HS_SPLITK=2: only the tiles on (or within 15 % of) the modelled critical
+  // path are split -- the chain links of a critical-path-bound plan (cfg3's 8 +
+  // 8 window steps) stream at two CTAs' rate while the throughput-bound rest
+  // keeps one tile per strip.
   {
-    bool split = false;
-    if (const char* e = getenv("HS_SPLITK")) split = f.tma && atoi(e) != 0;
+    int split_mode = 0;
+    if (const char* e = getenv("HS_SPLITK")) split_mode = f.tma ? atoi(e) : 0;
     f.npairs_split = 0;
-    if (split) {
+    std::vector<char> crit(tiles.size(), 1);
+    if (split_mode == 2) {
+      const int workers = (f.stages == 12 ? 1 : 2) * c->num_sms;
+      const std::vector<double> bl =
+          bottom_levels(tiles, deps, tile_inc, tile_cost, P.npairs, 3e-6, 6.5e12 / std::max(1, workers));
+      const double mx = bl.empty() ? 0.0 : *std::max_element(bl.begin(), bl.end());
+      // a tile is critical when its bottom level plus the longest path into it
+      // is within 15 % of the plan's critical path (top levels: forward pass)
+      const std::vector<double> tl =
+          top_levels(tiles, deps, tile_inc, tile_cost, P.npairs, 3e-6, 6.5e12 / std::max(1, workers));
+      for (size_t i = 0; i < tiles.size(); ++i) crit[i] = tl[i] + bl[i] >= 0.85 * mx;
+    }
+    if (split_mode != 0) {
       std::vector<FusedTile> t2;
       std::vector<std::vector<int>> inc2;
       std::vector<double> cost2;
       for (size_t i = 0; i < tiles.size(); ++i) {
         const FusedTile& t = tiles[i];
         const int nch = (t.c1 + 31) / 32 - t.c0 / 32;
-        if (nch < 8) {
+        if (nch < 8 || !crit[i]) {
           t2.push_back(t); inc2.push_back(tile_inc[i]); cost2.push_back(tile_cost[i]);
           continue;
         }
