@@ -154,8 +154,11 @@ int hs_gmres(hs_ctx* ctx, int pc_kind, const double* b, double* x, int nrhs, dou
  * host-driven MGS (single-GPU test of the sharded algorithm), 2 = force the
  * generic grid-wide cooperative kernel (k_mgs + k_givens),
  * 3 = CGS2 (classical Gram-Schmidt + one reorthogonalisation; one RHS): two
- * reductions per iteration instead of k+1 -- one allreduce each across row
- * bands; same iteration counts as MGS within +-1. */
+ * reductions per iteration instead of k+1 -- one all-reduce each across row
+ * bands; same iteration counts as MGS within +-1;
+ * 4 = CGS2 with the reorthogonalisation done on the coefficients through the
+ * device-kept Gram matrix V^H V: ONE reduction per iteration (the row-band
+ * default for one RHS; HS_ARNOLDI_BANDS=cgs2 selects mode 3 there). */
 int hs_set_gmres_mode(hs_ctx* ctx, int mode);
 
 /* Test hook for the multi-GPU path: run the fused 1-RHS BSP

@@ -2359,9 +2359,14 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
   // instead of one per inner product (k + 1), which would dominate the sharded
   // iteration (54 small all-reduces per iteration on average at cfg5);
   // iterations within +-1 of MGS (tests).
-  const bool cgs2 = c->gmres_mode == 3 || (c->gmres_mode == 0 && c->plan.nranks > 1 && R == 1);
-  if (cgs2 && R != 1) return fail(c, 1, "CGS2 Arnoldi supports one right-hand side");
-  const bool dist = c->plan.nranks > 1 || c->gmres_mode == 1 || cgs2;
+  // Row bands, one RHS, auto mode: CGS2 with the Gram correction -- ONE
+  // reduction per iteration (HS_ARNOLDI_BANDS=cgs2: the two-reduction CGS2)
+  static const bool bands_cgs2 = getenv("HS_ARNOLDI_BANDS") && std::string(getenv("HS_ARNOLDI_BANDS")) == "cgs2";
+  const bool auto_bands = c->gmres_mode == 0 && c->plan.nranks > 1 && R == 1;
+  const bool cgs2 = c->gmres_mode == 3 || (auto_bands && bands_cgs2);
+  const bool cgsg = c->gmres_mode == 4 || (auto_bands && !bands_cgs2);
+  if ((cgs2 || cgsg) && R != 1) return fail(c, 1, "CGS2 Arnoldi supports one right-hand side");
+  const bool dist = c->plan.nranks > 1 || c->gmres_mode == 1 || cgs2 || cgsg;
   const long long LR = LRof(c, R);
   if (LR == 0) {  // empty interface system (1 x 1 lattice): 0 iterations
     for (int r = 0; r < R; ++r) {
@@ -2378,7 +2383,7 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
   int chunk = 0;
   int grid = dist ? 2 * c->num_sms : gmres_coop_grid(*c, LR, R, &chunk);
   if (grid <= 0) return fail(c, 3, "interface vector too large for the cooperative Arnoldi kernel");
-  double2 *part2 = nullptr, *mgsout = nullptr, *part3 = nullptr, *hbuf = nullptr;
+  double2 *part2 = nullptr, *mgsout = nullptr, *part3 = nullptr, *hbuf = nullptr, *gram = nullptr;
   if (dist) {
     if (!c->d_owned) {
       std::vector<int> owned;
@@ -2389,6 +2394,10 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
     }
     if (ws_get(c, "part2", (size_t)grid * 2 * R, &part2) || ws_get(c, "mgsout", (size_t)2 * R, &mgsout)) return -1;
     if (cgs2 && (ws_get(c, "part3", (size_t)grid * (maxit + 2), &part3) || ws_get(c, "hbuf", (size_t)maxit + 2, &hbuf)))
+      return -1;
+    if (cgsg && (ws_get(c, "part3", (size_t)grid * (2 * maxit + 3), &part3) ||
+                 ws_get(c, "hbuf", (size_t)3 * maxit + 6, &hbuf) ||
+                 ws_get(c, "gram", (size_t)(maxit + 1) * (maxit + 1), &gram)))
       return -1;
   }
   GmresDev G;
@@ -2457,7 +2466,10 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
         if (int e_ = do_apply(c, HS_APPLY_IMS, zin, w, R)) return e_;
       }
     }
-    if (cgs2) {
+    if (cgsg) {
+      CK(gmres_arnoldi_cgsg(*c, G, k, c->d_owned, c->n_owned, part3, hbuf, gram, maxit + 1, c->nccl));
+      CK(gmres_givens(*c, G, k));
+    } else if (cgs2) {
       CK(gmres_arnoldi_cgs2(*c, G, k, c->d_owned, c->n_owned, part3, hbuf, c->nccl));
       CK(gmres_givens(*c, G, k));
     } else if (dist) {
@@ -2974,8 +2986,8 @@ int hs_set_emulated_ranks(hs_ctx* c, int ranks) {
 int hs_set_gmres_mode(hs_ctx* c, int mode) {
   if (!c) return fail(nullptr, 1, "null context");
   DEV_SCOPE(c);
-  if (mode < 0 || mode > 3)
-    return fail(c, 1, "gmres mode must be 0 (auto), 1 (host-driven MGS), 2 (grid-wide MGS) or 3 (CGS2)");
+  if (mode < 0 || mode > 4)
+    return fail(c, 1, "gmres mode must be 0 (auto), 1 (host-driven MGS), 2 (grid-wide MGS), 3 (CGS2) or 4 (CGS2, Gram-corrected, one reduction)");
   c->gmres_mode = mode;
   return 0;
 }

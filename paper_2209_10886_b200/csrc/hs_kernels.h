@@ -112,6 +112,8 @@ cudaError_t gmres_init_dist(Ctx& c, GmresDev& G, const double2* b, const int* bl
 cudaError_t gmres_arnoldi_cgs2(Ctx& c, GmresDev& G, int k, const int* blocks, int nb, double2* part,
                                double2* hbuf, void* nccl_comm);
 // in-place sum over ranks (implemented next to the NCCL calls in hs_api.cu)
+cudaError_t gmres_arnoldi_cgsg(Ctx& c, GmresDev& G, int k, const int* blocks, int nb, double2* part,
+                               double2* red, double2* Gm, int ldg, void* nccl_comm);
 cudaError_t allreduce_sum_doubles(Ctx& c, double* buf, size_t count, void* nccl_comm);
 cudaError_t launch_peer_allreduce(Ctx& c, const PeerRedArgs& a);
 // first device-check failure of each translation unit (0: none; debug library only)

@@ -720,6 +720,165 @@ __global__ void k_cgs_normalize(GmresDev G, const int* __restrict__ blocks, int 
   if (blockIdx.x == 0 && threadIdx.x == 0) G.H[hoff(k, 1) + k + 1] = make_double2(hn, 0);
 }
 
+// ---------------------------------------------------------------------------
+// CGS2 with ONE reduction per iteration (arnoldi "cgs2g", the row-band
+// default): pass 0's inner products also give the new Gram row, and the
+// reorthogonalisation is done on the coefficients instead of a second pass,
+//   h  = V^H w,  g_k = V^H v_k (the Gram row of the newest basis vector),
+//   h' = V^H (w - V h) = h - G h,   c = h + h' = 2 h - G h,
+//   w'' = w - V c,  ||w''||^2 = ||w||^2 - 2 Re(c^H h) + c^H G c,
+// with G = V^H V kept on the device (rows added as the basis grows).  In exact
+// arithmetic this is CGS2; the second pass's re-projection of w's rounding
+// error (O(eps ||w||)) is what it omits.  One reduction of 2 (k + 1) + 1
+// values, one pass over V for the products and one for the update (+ the
+// normalisation, whose norm is already known).
+// part: [grid][2 (k+1) + 1]: h_j, g_kj, then ||w||^2
+__global__ void k_cgsg_dots(GmresDev G, const int* __restrict__ blocks, int nb, int n, int k, double2* part,
+                            int stride) {
+  extern __shared__ double2 sw[];  // this CTA's slice of w and v_k
+  const long long LR = G.LR;
+  const double2* w = G.V + (long long)(k + 1) * LR;
+  const double2* vk = G.V + (long long)k * LR;
+  const long long total = (long long)nb * n;
+  const long long per = (total + gridDim.x - 1) / gridDim.x;
+  const long long i0 = blockIdx.x * per, i1 = min(total, i0 + per);
+  const int cnt = (int)max(0ll, i1 - i0);
+  double2* sws = sw;
+  double2* svk = sw + per;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+    const long long gi = i0 + i;
+    const long long e = (long long)blocks[gi / n] * n + gi % n;
+    sws[i] = w[e];
+    svk[i] = vk[e];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int kp1 = k + 1;
+  for (int j = warp; j <= kp1; j += nw) {  // j = k + 1: ||w||^2
+    double2 a = make_double2(0, 0), b = make_double2(0, 0);
+    if (j < kp1) {
+      const double2* v = G.V + (long long)j * LR;
+      for (int i = lane; i < cnt; i += 32) {
+        const long long gi = i0 + i;
+        const double2 x = v[(long long)blocks[gi / n] * n + gi % n];
+        cfma_conj(a, x, sws[i]);
+        cfma_conj(b, x, svk[i]);
+      }
+    } else {
+      for (int i = lane; i < cnt; i += 32) a.x += sws[i].x * sws[i].x + sws[i].y * sws[i].y;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a.x += __shfl_down_sync(0xffffffffu, a.x, o);
+      a.y += __shfl_down_sync(0xffffffffu, a.y, o);
+      b.x += __shfl_down_sync(0xffffffffu, b.x, o);
+      b.y += __shfl_down_sync(0xffffffffu, b.y, o);
+    }
+    if (lane == 0) {
+      double2* P = part + (long long)blockIdx.x * stride;
+      if (j < kp1) {
+        P[j] = a;
+        P[kp1 + j] = b;
+      } else {
+        P[2 * kp1] = a;
+      }
+    }
+  }
+}
+
+// One CTA: the new Gram row, the coefficients c = 2 h - G h, the new norm by
+// expansion, H[:, k] and ||w|| (breakdown test); k_givens follows.
+// red = [h_0..h_k, g_k0..g_kk, ||w||^2] (reduced over CTAs / ranks); Gm is the
+// (maxit + 1)^2 lower triangle of V^H V: Gm[i (maxit + 1) + j] = <v_j, v_i>, j <= i.
+__global__ void k_cgsg_coef(GmresDev G, int k, const double2* red, double2* Gm, int ldg, double2* cbuf) {
+  extern __shared__ double2 sh[];  // h (k+1), Gh (k+1), c (k+1), then 2 (k+1) doubles of terms
+  const int kp1 = k + 1;
+  double2* h = sh;
+  double2* gh = sh + kp1;
+  double2* cc = sh + 2 * kp1;
+  double* t1 = (double*)(sh + 3 * kp1);  // per-i terms, summed in index order (deterministic)
+  double* t2 = t1 + kp1;
+  for (int j = threadIdx.x; j < kp1; j += blockDim.x) {
+    h[j] = red[j];
+    Gm[(long long)k * ldg + j] = red[kp1 + j];  // <v_j, v_k> = v_j^H v_k
+  }
+  __syncthreads();
+  // Gm[i][j] = v_j^H v_i (j <= i); Gel(i, j) = v_j^H v_i = G[j][i] for any i, j <= k
+  auto Gel = [&](int i, int j) -> double2 {
+    if (j <= i) return Gm[(long long)i * ldg + j];
+    const double2 t = Gm[(long long)j * ldg + i];
+    return make_double2(t.x, -t.y);
+  };
+  for (int i = threadIdx.x; i < kp1; i += blockDim.x) {  // (G h)_i = sum_j G[i][j] h_j
+    double2 acc = make_double2(0, 0);
+    for (int j = 0; j < kp1; ++j) acc = cadd(acc, cmul(Gel(j, i), h[j]));
+    gh[i] = acc;
+    cc[i] = csub(make_double2(2.0 * h[i].x, 2.0 * h[i].y), acc);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kp1; i += blockDim.x) {  // Re(c^H h), c^H G c termwise
+    double2 gc = make_double2(0, 0);
+    for (int j = 0; j < kp1; ++j) gc = cadd(gc, cmul(Gel(j, i), cc[j]));
+    t1[i] = cc[i].x * h[i].x + cc[i].y * h[i].y;
+    t2[i] = cc[i].x * gc.x + cc[i].y * gc.y;
+  }
+  __syncthreads();
+  double2* Hk = G.H + hoff(k, 1);
+  if (threadIdx.x == 0) {
+    double s1 = 0.0, s2 = 0.0;
+    for (int i = 0; i < kp1; ++i) s1 += t1[i], s2 += t2[i];
+    const double w2 = red[2 * kp1].x;
+    const double q = w2 - 2.0 * s1 + s2;
+    const double hn = sqrt(q > 0 ? q : 0.0);
+    G.wnorm0[0] = sqrt(w2);
+    Hk[k + 1] = make_double2(hn, 0);
+    cbuf[kp1] = make_double2(hn, 0);
+  }
+  for (int j = threadIdx.x; j < kp1; j += blockDim.x) {
+    Hk[j] = cc[j];
+    cbuf[j] = cc[j];
+  }
+}
+
+// w'' = (w - V c) / ||w''|| over the owned elements
+__global__ void k_cgsg_update(GmresDev G, const int* __restrict__ blocks, int nb, int n, int k, const double2* cbuf) {
+  const long long LR = G.LR;
+  double2* w = G.V + (long long)(k + 1) * LR;
+  const double hn = cbuf[k + 1].x;
+  const long long total = (long long)nb * n;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long e = (long long)blocks[i / n] * n + i % n;
+    double2 x = w[e];
+    for (int j = 0; j <= k; ++j) x = csub(x, cmul(cbuf[j], G.V[(long long)j * LR + e]));
+    w[e] = hn > 0 ? make_double2(x.x / hn, x.y / hn) : make_double2(0, 0);
+  }
+}
+
+cudaError_t gmres_arnoldi_cgsg(Ctx& c, GmresDev& G, int k, const int* blocks, int nb, double2* part,
+                               double2* red, double2* Gm, int ldg, void* nccl_comm) {
+  const int grid = 2 * c.num_sms;
+  const int kp1 = k + 1;
+  const int cnt = 2 * kp1 + 1;
+  const long long total = (long long)nb * c.n;
+  const long long per = (total + grid - 1) / grid;
+  const size_t smem = (size_t)2 * per * sizeof(double2);
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  static cudaError_t attr = cudaFuncSetAttribute(k_cgsg_dots, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if (attr != cudaSuccess) return attr;
+  c.launches += 4;
+  k_cgsg_dots<<<grid, 256, smem, c.stream>>>(G, blocks, nb, c.n, k, part, cnt);
+  k_cgs_reduce<<<(cnt + 127) / 128, 128, 0, c.stream>>>(part, grid, cnt, cnt, red);
+  if (nccl_comm) {
+    if (cudaError_t e = allreduce_sum_doubles(c, (double*)red, 2 * (size_t)cnt, nccl_comm)) return e;
+  }
+  double2* cbuf = red + cnt;  // c (k+1) + ||w''||
+  k_cgsg_coef<<<1, 256, (size_t)4 * kp1 * sizeof(double2), c.stream>>>(G, k, red, Gm, ldg, cbuf);
+  const int ug = std::min(grid * 4, std::max(1, (int)((total + 255) / 256)));
+  k_cgsg_update<<<ug, 256, 0, c.stream>>>(G, blocks, nb, c.n, k, cbuf);
+  return cudaGetLastError();
+}
+
 cudaError_t gmres_arnoldi_cgs2(Ctx& c, GmresDev& G, int k, const int* blocks, int nb, double2* part,
                                double2* hbuf, void* nccl_comm) {
   const int grid = 2 * c.num_sms;

@@ -446,11 +446,13 @@ class GpuInterfaceSystem:
         side -- two allreduces per iteration instead of one per inner product --
         and host-driven MGS with an allreduce per inner product for several),
         "hostloop" (force the sharded MGS on one GPU or across bands), "grid"
-        (force the grid-wide cooperative kernel) or "cgs2" (classical
+        (force the grid-wide cooperative kernel), "cgs2" (classical
         Gram-Schmidt with one reorthogonalisation, iterations within +-1 of
-        MGS)."""
+        MGS) or "cgs2g" (CGS2 with the reorthogonalisation done on the
+        coefficients through the device-kept Gram matrix: ONE reduction per
+        iteration, the row-band default)."""
         kind = self.sweep.kind if kind is None else kind
-        modes = {"auto": 0, "hostloop": 1, "grid": 2, "cgs2": 3}
+        modes = {"auto": 0, "hostloop": 1, "grid": 2, "cgs2": 3, "cgs2g": 4}
         if arnoldi not in modes:
             raise ValueError(f"arnoldi must be one of {sorted(modes)}, got {arnoldi!r}")
         self.ctx.call("hs_set_gmres_mode", modes[arnoldi])

@@ -263,6 +263,64 @@ class Band:
         return self.bsp(u), k_done
 
 
+    def gmres_cgs2g(self, b, tol=1e-6, maxit=200):
+        """The row-band default Arnoldi (gmres_arnoldi_cgsg): CGS2 with the
+        reorthogonalisation done on the coefficients through the Gram matrix
+        G = V^H V -- ONE all-reduce per iteration of [V^H w, V^H v_k, ||w||^2]
+        over the owned blocks; c = 2h - G h, w'' = w - V c, ||w''||^2 =
+        ||w||^2 - 2 Re(c^H h) + c^H G c.  Returns (x, iterations, all-reduces)."""
+        from oracle.gmres import givens
+        m = self.owned_mask()
+        nred = [0]
+
+        def allreduce(vec):
+            t = torch.view_as_real(torch.tensor(np.asarray(vec, complex))).contiguous()
+            dist.all_reduce(t)
+            nred[0] += 1
+            return t[:, 0].numpy() + 1j * t[:, 1].numpy()
+
+        beta = abs(allreduce([np.vdot(b[m], b[m])])[0]) ** 0.5
+        V = [np.where(m, b / beta, 0)]
+        Gm = np.zeros((maxit + 1, maxit + 1), complex)
+        H = np.zeros((maxit + 1, maxit), complex)
+        cs, sn = np.zeros(maxit), np.zeros(maxit, complex)
+        g = np.zeros(maxit + 1, complex)
+        g[0] = beta
+        k_done = 0
+        for k in range(maxit):
+            w = np.where(m, self.apply_A(self.bsp(V[k])), 0)
+            loc = [np.vdot(V[j][m], w[m]) for j in range(k + 1)] + \
+                  [np.vdot(V[j][m], V[k][m]) for j in range(k + 1)] + [np.vdot(w[m], w[m])]
+            red = allreduce(loc)
+            h, gk, w2 = red[:k + 1], red[k + 1:2 * k + 2], red[-1].real
+            Gm[k, :k + 1] = gk                       # <v_j, v_k>
+            L = np.tril(Gm[:k + 1, :k + 1])          # L[i][j] = v_j^H v_i, j <= i
+            Gfull = np.conj(L) + np.tril(L, -1).T    # G[i][j] = v_i^H v_j
+            c = 2 * h - Gfull @ h
+            q = w2 - 2 * np.real(np.vdot(c, h)) + np.real(np.vdot(c, Gfull @ c))
+            hn = max(q, 0.0) ** 0.5
+            w = w - sum(c[j] * V[j] for j in range(k + 1))
+            H[:k + 1, k] = c
+            H[k + 1, k] = hn
+            for j in range(k):
+                t = cs[j] * H[j, k] + sn[j] * H[j + 1, k]
+                H[j + 1, k] = -np.conj(sn[j]) * H[j, k] + cs[j] * H[j + 1, k]
+                H[j, k] = t
+            c_, s_ = givens(H[k, k], H[k + 1, k].real)
+            cs[k], sn[k] = c_, s_
+            H[k, k] = c_ * H[k, k] + s_ * H[k + 1, k]
+            H[k + 1, k] = 0
+            g[k + 1] = -np.conj(s_) * g[k]
+            g[k] = c_ * g[k]
+            k_done = k + 1
+            if abs(g[k + 1]) / beta <= tol:
+                break
+            V.append(w / hn)
+        y = np.linalg.solve(np.triu(H[:k_done, :k_done]), g[:k_done])
+        u = sum(y[i] * V[i] for i in range(k_done))
+        return self.bsp(u), k_done, nred[0]
+
+
 def _worker(rank, world, port, case, blocks, q, with_gmres=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -289,6 +347,8 @@ def _worker(rank, world, port, case, blocks, q, with_gmres=False):
             x, its = band.gmres(b)
             ref = gmres(ref_itf.apply_A, Preconditioner(ref_itf, "bsp", blocks=blocks), b, tol=1e-6, maxit=200)
             res += [its, ref.iterations, float(np.abs(x[m] - ref.x[m]).max() / np.abs(ref.x).max())]
+            xg, itg, nred = band.gmres_cgs2g(b)
+            res += [itg, nred, float(np.abs(xg[m] - ref.x[m]).max() / np.abs(ref.x).max())]
         q.put(tuple(res))
     finally:
         dist.destroy_process_group()
@@ -334,6 +394,12 @@ def test_sharded_gmres_matches_single_process(world):
         its, ref_its, ex = r[4], r[5], r[6]
         assert its == ref_its, (its, ref_its)
         assert ex < 1e-10, ex
+        # the row-band default (CGS2, Gram-corrected): one all-reduce per
+        # iteration (+ the initial norm), the same iterations and x
+        itg, nred, exg = r[7], r[8], r[9]
+        assert itg == ref_its, (itg, ref_its)
+        assert nred == itg + 1, (nred, itg)
+        assert exg < 1e-10, exg
 
 
 # ---- the multi-GPU peer-memory protocol, emulated by processes -------------
