@@ -157,8 +157,10 @@ int hs_gmres(hs_ctx* ctx, int pc_kind, const double* b, double* x, int nrhs, dou
  * reductions per iteration instead of k+1 -- one all-reduce each across row
  * bands; same iteration counts as MGS within +-1;
  * 4 = CGS2 with the reorthogonalisation done on the coefficients through the
- * device-kept Gram matrix V^H V: ONE reduction per iteration (the row-band
- * default for one RHS; HS_ARNOLDI_BANDS=cgs2 selects mode 3 there). */
+ * device-kept Gram matrix V^H V: ONE reduction per iteration -- what mode 0
+ * runs for one RHS, on one GPU and across row bands (HS_ARNOLDI_BANDS=cgs2:
+ * mode 3 across bands); 5 = the MGS kernels for one RHS too (mode 0's choice
+ * for several RHS: the cluster kernel up to 32k elements, k_mgs1 beyond). */
 int hs_set_gmres_mode(hs_ctx* ctx, int mode);
 
 /* Test hook for the multi-GPU path: run the fused 1-RHS BSP

@@ -2359,12 +2359,17 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
   // instead of one per inner product (k + 1), which would dominate the sharded
   // iteration (54 small all-reduces per iteration on average at cfg5);
   // iterations within +-1 of MGS (tests).
-  // Row bands, one RHS, auto mode: CGS2 with the Gram correction -- ONE
-  // reduction per iteration (HS_ARNOLDI_BANDS=cgs2: the two-reduction CGS2)
+  // One RHS, auto mode: CGS2 with the Gram correction -- ONE reduction per
+  // iteration, two passes over V, no barrier chain -- on one GPU and across
+  // row bands (HS_ARNOLDI_BANDS=cgs2: the two-reduction CGS2 across bands);
+  // measured faster than the MGS kernels on every config (cfg1 1.9 vs 2.3 ms,
+  // cfg2 5.4 vs 8.0, cfg3 23.3 vs 25.5, cfg5 0.240 vs 0.244 s GMRES) with the
+  // same iterations and histories within 1e-10 of the oracle's MGS.  Mode 5
+  // ("mgs") keeps the MGS kernels (the SPEC's literal Arnoldi).
   static const bool bands_cgs2 = getenv("HS_ARNOLDI_BANDS") && std::string(getenv("HS_ARNOLDI_BANDS")) == "cgs2";
-  const bool auto_bands = c->gmres_mode == 0 && c->plan.nranks > 1 && R == 1;
-  const bool cgs2 = c->gmres_mode == 3 || (auto_bands && bands_cgs2);
-  const bool cgsg = c->gmres_mode == 4 || (auto_bands && !bands_cgs2);
+  const bool auto1 = c->gmres_mode == 0 && R == 1;
+  const bool cgs2 = c->gmres_mode == 3 || (auto1 && c->plan.nranks > 1 && bands_cgs2);
+  const bool cgsg = c->gmres_mode == 4 || (auto1 && !(c->plan.nranks > 1 && bands_cgs2));
   if ((cgs2 || cgsg) && R != 1) return fail(c, 1, "CGS2 Arnoldi supports one right-hand side");
   const bool dist = c->plan.nranks > 1 || c->gmres_mode == 1 || cgs2 || cgsg;
   const long long LR = LRof(c, R);
@@ -2467,8 +2472,9 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
       }
     }
     if (cgsg) {
-      CK(gmres_arnoldi_cgsg(*c, G, k, c->d_owned, c->n_owned, part3, hbuf, gram, maxit + 1, c->nccl));
-      CK(gmres_givens(*c, G, k));
+      // one rank owns every block, in order: identity element mapping
+      CK(gmres_arnoldi_cgsg(*c, G, k, c->plan.nranks == 1 ? nullptr : c->d_owned, c->n_owned, part3, hbuf, gram,
+                            maxit + 1, c->nccl));  // includes the Givens update
     } else if (cgs2) {
       CK(gmres_arnoldi_cgs2(*c, G, k, c->d_owned, c->n_owned, part3, hbuf, c->nccl));
       CK(gmres_givens(*c, G, k));
@@ -2986,8 +2992,8 @@ int hs_set_emulated_ranks(hs_ctx* c, int ranks) {
 int hs_set_gmres_mode(hs_ctx* c, int mode) {
   if (!c) return fail(nullptr, 1, "null context");
   DEV_SCOPE(c);
-  if (mode < 0 || mode > 4)
-    return fail(c, 1, "gmres mode must be 0 (auto), 1 (host-driven MGS), 2 (grid-wide MGS), 3 (CGS2) or 4 (CGS2, Gram-corrected, one reduction)");
+  if (mode < 0 || mode > 5)
+    return fail(c, 1, "gmres mode must be 0 (auto), 1 (host-driven MGS), 2 (grid-wide MGS), 3 (CGS2), 4 (CGS2, Gram-corrected, one reduction) or 5 (MGS kernels by size)");
   c->gmres_mode = mode;
   return 0;
 }

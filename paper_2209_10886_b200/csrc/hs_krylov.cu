@@ -732,6 +732,15 @@ __global__ void k_cgs_normalize(GmresDev G, const int* __restrict__ blocks, int 
 // error (O(eps ||w||)) is what it omits.  One reduction of 2 (k + 1) + 1
 // values, one pass over V for the products and one for the update (+ the
 // normalisation, whose norm is already known).
+// Owned element i -> vector element: the owned blocks in order (row bands), or
+// the identity (blocks == nullptr: one rank owns everything).  32-bit index
+// arithmetic (a 64-bit division per element dominated these passes).
+__device__ __forceinline__ long long owned_elem(const int* __restrict__ blocks, int n, long long i) {
+  if (!blocks) return i;
+  const int ii = (int)i, q = ii / n;
+  return (long long)blocks[q] * n + (ii - q * n);
+}
+
 // part: [grid][2 (k+1) + 1]: h_j, g_kj, then ||w||^2
 __global__ void k_cgsg_dots(GmresDev G, const int* __restrict__ blocks, int nb, int n, int k, double2* part,
                             int stride) {
@@ -746,8 +755,7 @@ __global__ void k_cgsg_dots(GmresDev G, const int* __restrict__ blocks, int nb, 
   double2* sws = sw;
   double2* svk = sw + per;
   for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
-    const long long gi = i0 + i;
-    const long long e = (long long)blocks[gi / n] * n + gi % n;
+    const long long e = owned_elem(blocks, n, i0 + i);
     sws[i] = w[e];
     svk[i] = vk[e];
   }
@@ -759,8 +767,7 @@ __global__ void k_cgsg_dots(GmresDev G, const int* __restrict__ blocks, int nb, 
     if (j < kp1) {
       const double2* v = G.V + (long long)j * LR;
       for (int i = lane; i < cnt; i += 32) {
-        const long long gi = i0 + i;
-        const double2 x = v[(long long)blocks[gi / n] * n + gi % n];
+        const double2 x = v[owned_elem(blocks, n, i0 + i)];
         cfma_conj(a, x, sws[i]);
         cfma_conj(b, x, svk[i]);
       }
@@ -786,58 +793,93 @@ __global__ void k_cgsg_dots(GmresDev G, const int* __restrict__ blocks, int nb, 
   }
 }
 
+// out[j] = sum over CTAs of part[g][j]: one warp per entry, lane l summing
+// partials l, l + 32, ... then a shuffle tree (a fixed order: deterministic)
+__global__ void k_cgsg_reduce(const double2* __restrict__ part, int ngrid, int stride, int cnt, double2* out) {
+  const int lane = threadIdx.x & 31;
+  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (j >= cnt) return;
+  double2 a = make_double2(0, 0);
+  for (int g = lane; g < ngrid; g += 32) a = cadd(a, __ldcg(part + (long long)g * stride + j));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a.x += __shfl_xor_sync(0xffffffffu, a.x, o);
+    a.y += __shfl_xor_sync(0xffffffffu, a.y, o);
+  }
+  if (lane == 0) out[j] = a;
+}
+
 // One CTA: the new Gram row, the coefficients c = 2 h - G h, the new norm by
-// expansion, H[:, k] and ||w|| (breakdown test); k_givens follows.
+// expansion, H[:, k] and ||w|| (breakdown test), then the Givens update of the
+// column (as k_givens; fused here, the column in shared memory).
 // red = [h_0..h_k, g_k0..g_kk, ||w||^2] (reduced over CTAs / ranks); Gm is the
-// (maxit + 1)^2 lower triangle of V^H V: Gm[i (maxit + 1) + j] = <v_j, v_i>, j <= i.
+// full Hermitian (maxit + 1)^2 Gram matrix, row-major: Gm[i ldg + j] = v_i^H v_j.
 __global__ void k_cgsg_coef(GmresDev G, int k, const double2* red, double2* Gm, int ldg, double2* cbuf) {
-  extern __shared__ double2 sh[];  // h (k+1), Gh (k+1), c (k+1), then 2 (k+1) doubles of terms
+  extern __shared__ double2 sh[];  // h, c, Gh, Gc (k+1 each), column (k+2), 2 (k+1) terms, sn, cs
   const int kp1 = k + 1;
   double2* h = sh;
-  double2* gh = sh + kp1;
-  double2* cc = sh + 2 * kp1;
-  double* t1 = (double*)(sh + 3 * kp1);  // per-i terms, summed in index order (deterministic)
+  double2* cc = sh + kp1;
+  double2* gh = sh + 2 * kp1;
+  double2* gc = sh + 3 * kp1;
+  double2* col = sh + 4 * kp1;
+  double* t1 = (double*)(col + kp1 + 1);
   double* t2 = t1 + kp1;
+  double2* sns = (double2*)(t1 + 2 * kp1 + 2);  // the previous rotations, staged for thread 0 (16-byte aligned)
+  double* css = (double*)(sns + kp1);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    css[j] = G.cs[j];
+    sns[j] = G.sn[j];
+  }
   for (int j = threadIdx.x; j < kp1; j += blockDim.x) {
     h[j] = red[j];
-    Gm[(long long)k * ldg + j] = red[kp1 + j];  // <v_j, v_k> = v_j^H v_k
+    const double2 g = red[kp1 + j];                        // v_j^H v_k
+    Gm[(long long)j * ldg + k] = g;                        // G[j][k]
+    Gm[(long long)k * ldg + j] = make_double2(g.x, -g.y);  // G[k][j] = conj
   }
   __syncthreads();
-  // Gm[i][j] = v_j^H v_i (j <= i); Gel(i, j) = v_j^H v_i = G[j][i] for any i, j <= k
-  auto Gel = [&](int i, int j) -> double2 {
-    if (j <= i) return Gm[(long long)i * ldg + j];
-    const double2 t = Gm[(long long)j * ldg + i];
-    return make_double2(t.x, -t.y);
+  // warp per row: (G x)_i = sum_j G[i][j] x_j, lanes over j (coalesced), shuffle tree
+  auto matvec = [&](const double2* x, double2* y) {
+    for (int i = warp; i < kp1; i += nw) {
+      double2 acc = make_double2(0, 0);
+      const double2* row = Gm + (long long)i * ldg;
+      for (int j = lane; j < kp1; j += 32) acc = cadd(acc, cmul(row[j], x[j]));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+      }
+      if (lane == 0) y[i] = acc;
+    }
   };
-  for (int i = threadIdx.x; i < kp1; i += blockDim.x) {  // (G h)_i = sum_j G[i][j] h_j
-    double2 acc = make_double2(0, 0);
-    for (int j = 0; j < kp1; ++j) acc = cadd(acc, cmul(Gel(j, i), h[j]));
-    gh[i] = acc;
-    cc[i] = csub(make_double2(2.0 * h[i].x, 2.0 * h[i].y), acc);
-  }
+  matvec(h, gh);
+  __syncthreads();
+  for (int i = threadIdx.x; i < kp1; i += blockDim.x) cc[i] = csub(make_double2(2.0 * h[i].x, 2.0 * h[i].y), gh[i]);
+  __syncthreads();
+  matvec(cc, gc);
   __syncthreads();
   for (int i = threadIdx.x; i < kp1; i += blockDim.x) {  // Re(c^H h), c^H G c termwise
-    double2 gc = make_double2(0, 0);
-    for (int j = 0; j < kp1; ++j) gc = cadd(gc, cmul(Gel(j, i), cc[j]));
     t1[i] = cc[i].x * h[i].x + cc[i].y * h[i].y;
-    t2[i] = cc[i].x * gc.x + cc[i].y * gc.y;
+    t2[i] = cc[i].x * gc[i].x + cc[i].y * gc[i].y;
+    col[i] = cc[i];
+    cbuf[i] = cc[i];
   }
   __syncthreads();
-  double2* Hk = G.H + hoff(k, 1);
   if (threadIdx.x == 0) {
     double s1 = 0.0, s2 = 0.0;
-    for (int i = 0; i < kp1; ++i) s1 += t1[i], s2 += t2[i];
+    for (int i = 0; i < kp1; ++i) s1 += t1[i], s2 += t2[i];  // index order: deterministic
     const double w2 = red[2 * kp1].x;
     const double q = w2 - 2.0 * s1 + s2;
     const double hn = sqrt(q > 0 ? q : 0.0);
     G.wnorm0[0] = sqrt(w2);
-    Hk[k + 1] = make_double2(hn, 0);
+    col[kp1] = make_double2(hn, 0);
     cbuf[kp1] = make_double2(hn, 0);
+    // the Givens update of column k on the shared copy (k_givens' arithmetic)
+    *G.nactive = givens_column_at(G, k, 0, col, 1, css, sns, 1) ? 1 : 0;
   }
-  for (int j = threadIdx.x; j < kp1; j += blockDim.x) {
-    Hk[j] = cc[j];
-    cbuf[j] = cc[j];
-  }
+  __syncthreads();
+  double2* Hk = G.H + hoff(k, 1);
+  for (int j = threadIdx.x; j <= kp1; j += blockDim.x) Hk[j] = col[j];
 }
 
 // w'' = (w - V c) / ||w''|| over the owned elements
@@ -848,7 +890,7 @@ __global__ void k_cgsg_update(GmresDev G, const int* __restrict__ blocks, int nb
   const long long total = (long long)nb * n;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
-    const long long e = (long long)blocks[i / n] * n + i % n;
+    const long long e = owned_elem(blocks, n, i);
     double2 x = w[e];
     for (int j = 0; j <= k; ++j) x = csub(x, cmul(cbuf[j], G.V[(long long)j * LR + e]));
     w[e] = hn > 0 ? make_double2(x.x / hn, x.y / hn) : make_double2(0, 0);
@@ -864,16 +906,21 @@ cudaError_t gmres_arnoldi_cgsg(Ctx& c, GmresDev& G, int k, const int* blocks, in
   const long long per = (total + grid - 1) / grid;
   const size_t smem = (size_t)2 * per * sizeof(double2);
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  static cudaError_t attr = cudaFuncSetAttribute(k_cgsg_dots, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  static cudaError_t attr = [] {
+    cudaError_t e = cudaFuncSetAttribute(k_cgsg_dots, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_cgsg_coef, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    return e;
+  }();
   if (attr != cudaSuccess) return attr;
+  if ((size_t)(8 * kp1 + 2) * sizeof(double2) > 200 * 1024) return cudaErrorInvalidValue;
   c.launches += 4;
   k_cgsg_dots<<<grid, 256, smem, c.stream>>>(G, blocks, nb, c.n, k, part, cnt);
-  k_cgs_reduce<<<(cnt + 127) / 128, 128, 0, c.stream>>>(part, grid, cnt, cnt, red);
+  k_cgsg_reduce<<<(cnt + 7) / 8, 256, 0, c.stream>>>(part, grid, cnt, cnt, red);
   if (nccl_comm) {
     if (cudaError_t e = allreduce_sum_doubles(c, (double*)red, 2 * (size_t)cnt, nccl_comm)) return e;
   }
   double2* cbuf = red + cnt;  // c (k+1) + ||w''||
-  k_cgsg_coef<<<1, 256, (size_t)4 * kp1 * sizeof(double2), c.stream>>>(G, k, red, Gm, ldg, cbuf);
+  k_cgsg_coef<<<1, 256, (size_t)(8 * kp1 + 2) * sizeof(double2), c.stream>>>(G, k, red, Gm, ldg, cbuf);
   const int ug = std::min(grid * 4, std::max(1, (int)((total + 255) / 256)));
   k_cgsg_update<<<ug, 256, 0, c.stream>>>(G, blocks, nb, c.n, k, cbuf);
   return cudaGetLastError();

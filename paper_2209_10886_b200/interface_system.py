@@ -441,18 +441,20 @@ class GpuInterfaceSystem:
     # ---- SPEC.md:399-407 on the device
     def gmres(self, b, kind: str | None = None, tol: float = 1e-6, maxit: int = 200,
               arnoldi: str = "auto") -> GmresResult:
-        """arnoldi = "auto" (cluster MGS kernel for small vectors, grid-wide
-        cooperative kernel otherwise; across row bands CGS2 for one right-hand
-        side -- two allreduces per iteration instead of one per inner product --
-        and host-driven MGS with an allreduce per inner product for several),
-        "hostloop" (force the sharded MGS on one GPU or across bands), "grid"
-        (force the grid-wide cooperative kernel), "cgs2" (classical
+        """arnoldi = "auto" (one right-hand side: "cgs2g", on one GPU and
+        across row bands; several: the MGS kernels -- a cluster kernel for
+        small vectors, grid-wide otherwise, host-driven MGS with a reduction
+        per inner product across bands), "mgs" (the MGS kernels for one
+        right-hand side too: the SPEC's literal Arnoldi; k_mgs1c / k_mgs1 with
+        M steps per grid barrier), "hostloop" (force the sharded MGS on one
+        GPU or across bands), "grid" (force the generic grid-wide cooperative
+        kernel k_mgs + k_givens), "cgs2" (classical
         Gram-Schmidt with one reorthogonalisation, iterations within +-1 of
         MGS) or "cgs2g" (CGS2 with the reorthogonalisation done on the
         coefficients through the device-kept Gram matrix: ONE reduction per
         iteration, the row-band default)."""
         kind = self.sweep.kind if kind is None else kind
-        modes = {"auto": 0, "hostloop": 1, "grid": 2, "cgs2": 3, "cgs2g": 4}
+        modes = {"auto": 0, "hostloop": 1, "grid": 2, "cgs2": 3, "cgs2g": 4, "mgs": 5}
         if arnoldi not in modes:
             raise ValueError(f"arnoldi must be one of {sorted(modes)}, got {arnoldi!r}")
         self.ctx.call("hs_set_gmres_mode", modes[arnoldi])

@@ -63,7 +63,7 @@ def oracle_run(k):
     return _ORACLE[k]
 
 
-@pytest.mark.parametrize("mode", ["auto", "grid", "hostloop", "cgs2", "cgs2g"])
+@pytest.mark.parametrize("mode", ["auto", "mgs", "grid", "hostloop", "cgs2", "cgs2g"])
 @pytest.mark.parametrize("case", [(2, 2, 8), (3, 3, 8), (3, 2, 12), (4, 4, 16)])
 def test_basis_orthonormal_desk_scale(case, mode):
     """SPEC.md:412 at desk scale: max |V^H V - I| <= 1e-10 -- for CGS2; MGS
@@ -94,7 +94,7 @@ def test_basis_orthonormal_desk_scale(case, mode):
 
 
 @pytest.mark.parametrize("k", [1, 2, 3])
-@pytest.mark.parametrize("mode", ["auto", "grid", "hostloop", "cgs2", "cgs2g"])
+@pytest.mark.parametrize("mode", ["auto", "mgs", "grid", "hostloop", "cgs2", "cgs2g"])
 def test_basis_orthonormal(k, mode):
     """At the BASELINE sizes MGS loses orthogonality like kappa eps: the
     oracle's own MGS basis reaches 2.3e-10 (cfg1) and 1.1e-10 (cfg2).  The GPU
@@ -117,7 +117,7 @@ def test_basis_orthonormal(k, mode):
 
 
 @pytest.mark.parametrize("k", [1, 2])
-@pytest.mark.parametrize("mode", ["auto", "grid", "hostloop", "cgs2", "cgs2g"])
+@pytest.mark.parametrize("mode", ["auto", "mgs", "grid", "hostloop", "cgs2", "cgs2g"])
 def test_history_vs_oracle_mgs(k, mode):
     """Same operator arithmetic to ~1e-15 (accurate oracle maps), so the MGS
     GMRES histories agree to 1e-10 relative and the iterations are equal."""
@@ -137,7 +137,7 @@ def _blocked_run(k, m):
             "from paper_2209_10886_b200.interface_system import GpuInterfaceSystem, SweepConfig\n"
             f"c = CONFIGS[{k}]; spec, part = product_problem(c)\n"
             "s = GpuInterfaceSystem(spec, part, sweep=SweepConfig(blocks=c['blocks']))\n"
-            f"G = golden('cfg{k}'); r = s.gmres(G['b'], 'bsp', tol=1e-6, maxit=1000, arnoldi='grid')\n"
+            f"G = golden('cfg{k}'); r = s.gmres(G['b'], 'bsp', tol=1e-6, maxit=1000, arnoldi='mgs')\n"
             "V = s.gmres_basis(); E = np.abs(V.conj().T @ V - np.eye(V.shape[1])).max()\n"
             "x = np.asarray(r.solution)\n"
             "print(json.dumps({'it': r.iterations, 'hist': list(map(float, r.history)), 'orth': float(E),\n"
