@@ -329,6 +329,10 @@ int make_mma(Ctx* c, DevStep& st, int R, bool shared, DevMma** out) {
     CK(dalloc(c, (void**)&c->zeros, 64 * sizeof(double2)));
     CK(cudaMemsetAsync(c->zeros, 0, 64 * sizeof(double2), c->stream));
   }
+  if (kind != 0 && !c->z2_tickets) {  // k_zmma2 persistent launches' ticket counters (never reset)
+    CK(dalloc(c, (void**)&c->z2_tickets, kZ2TicketSlots * sizeof(unsigned)));
+    CK(cudaMemsetAsync(c->z2_tickets, 0, kZ2TicketSlots * sizeof(unsigned), c->stream));
+  }
   DevMma m;
   m.kind = kind;
   m.bn = bn;
@@ -1865,7 +1869,6 @@ int hs_destroy(hs_ctx* c) {
       if (e) cudaEventDestroy(e);
     if (c->aux_fork) cudaEventDestroy(c->aux_fork);
     if (c->aux_join) cudaEventDestroy(c->aux_join);
-    if (c->z2_tickets) cudaFree(c->z2_tickets);
     if (c->aux) cudaStreamDestroy(c->aux);
     if (c->copy_in) cudaStreamDestroy(c->copy_in);
     if (c->copy_out) cudaStreamDestroy(c->copy_out);

@@ -1123,11 +1123,7 @@ void launch_zmma(Ctx& c, const DevMma& m, const double2* A, const double2* srcA,
     // overlapping launches never share a counter); its claims = tasks + grid
     unsigned* ticket = nullptr;
     unsigned tbase = 0;
-    if (pers) {
-      if (!c.z2_tickets) {
-        if (cudaMalloc((void**)&c.z2_tickets, kZ2TicketSlots * sizeof(unsigned)) != cudaSuccess) return;
-        cudaMemsetAsync(c.z2_tickets, 0, kZ2TicketSlots * sizeof(unsigned), c.stream);
-      }
+    if (pers) {  // the counters are allocated (zeroed) with the contraction tables (make_mma)
       const int slot = (int)(c.z2_seq++ % kZ2TicketSlots);
       ticket = c.z2_tickets + slot;
       tbase = c.z2_base[slot];
