@@ -13,7 +13,15 @@ bounded below by its bytes / HBM bandwidth.  The constants are calibrated on
 the one-GPU traces (profiles/r01/fused_trace_cfg*.json): stream rate from
 stream_us, fixed cost from wait + epilogue.
 
-  python tools/scaling_model.py CFG [G ...]
+  python tools/scaling_model.py CFG [G ...] [--gmres ITERS]
+
+--gmres ITERS adds the modelled GMRES time-to-solution: ITERS x the replayed
+A M v plan (hs_fused_plan ims = 1) + the one-reduction CGS2 Arnoldi per
+iteration k: two passes over the rank's V slice (2 (k+1) L/G x 16 B at the
+HBM rate) + its fixed cost (calibrated on the one-GPU launch list,
+profiles/r02/gmres_launches_cfg5.csv: 23 ms of Arnoldi for 107 iterations =
+14 ms of streaming + ~80 us per iteration of launches / coefficients) + one
+peer-memory all-reduce across ranks (~8 us: two NVLink latencies + a kernel).
 """
 import bisect
 import ctypes as C
@@ -40,7 +48,7 @@ def parse(v):
     return out
 
 
-def plans(cfg, G):
+def plans(cfg, G, ims=0):
     c = CONFIGS[cfg]
     n = c["n"]
     out = []
@@ -51,9 +59,9 @@ def plans(cfg, G):
             lo, hi = native.i32([a for a, _ in w]), native.i32([b for _, b in w])
             ctx.call("hs_set_windows", k, native.iptr(lo), native.iptr(hi), len(w))
         cnt = C.c_int(0)
-        ctx.call("hs_fused_plan", 0, g, None, 0, C.byref(cnt))
+        ctx.call("hs_fused_plan", ims, g, None, 0, C.byref(cnt))
         buf = (C.c_int32 * cnt.value)()
-        ctx.call("hs_fused_plan", 0, g, buf, cnt.value, C.byref(cnt))
+        ctx.call("hs_fused_plan", ims, g, buf, cnt.value, C.byref(cnt))
         owner = ctx.block_owner()
         out.append(parse(np.frombuffer(buf, dtype=np.int32)))
     return out, owner, c
@@ -102,12 +110,12 @@ def critical_tiles(cfg, frac, rate=31.6e9, fixed=3.0e-6):
 
 
 def simulate(cfg, G, ctas=296, rate=31.6e9, fixed=3.0e-6, lat=3.0e-6, hbm=6.9e12, rate_max=None, split=False,
-             split_set=None):
+             split_set=None, ims=0):
     """rate: per-CTA stream rate under full load (calibrated); rate_max: the
     ring-latency limit of one CTA (5 x 16 KB in flight) when fewer CTAs share
     the HBM -- the rate of a tile is then min(rate_max, hbm / CTAs streaming at
     its start)."""
-    pl, owner, c = plans(cfg, G)
+    pl, owner, c = plans(cfg, G, ims)
     lat_ = lattice_maps(c)
     n = c["n"]
     # global ticket order = merge of the rank lists by their global position: the
@@ -201,15 +209,31 @@ def main():
     for a in sys.argv:
         if a.startswith("--split-critical="):
             calib = dict(calib, split_set=critical_tiles(cfg, float(a.split("=")[1])))
+    iters = None
+    if "--gmres" in sys.argv:
+        iters = int(sys.argv[sys.argv.index("--gmres") + 1])
+        Gs = [G for G in Gs if G != iters]
     rows = []
     t1 = None
+    g1 = None
+    from oracle.lattice import Lattice
+    L = Lattice(c["n1"], c["n2"]).n_pairs * c["n"]
     for G in Gs:
         if G > c["n2"]:
             continue
         T, per, by = simulate(cfg, G, **calib)
         t1 = T if G == 1 else t1
-        rows.append({"G": G, "apply_ms": round(T * 1e3, 4), "per_rank_ms": [round(x * 1e3, 4) for x in per],
-                     "efficiency": round(t1 / (G * T), 3) if t1 else None})
+        row = {"G": G, "apply_ms": round(T * 1e3, 4), "per_rank_ms": [round(x * 1e3, 4) for x in per],
+               "efficiency": round(t1 / (G * T), 3) if t1 else None}
+        if iters:
+            Tamv, _, _ = simulate(cfg, G, ims=1, **calib)
+            hbm = 6.5e12
+            arn = sum(2.0 * (k + 1) * (L / G) * 16.0 / hbm + 80e-6 + (8e-6 if G > 1 else 0.0) for k in range(iters))
+            gm = iters * Tamv + arn
+            g1 = gm if G == 1 else g1
+            row.update({"amv_ms": round(Tamv * 1e3, 4), "arnoldi_ms": round(arn * 1e3, 2),
+                        "gmres_ms": round(gm * 1e3, 2), "gmres_efficiency": round(g1 / (G * gm), 3) if g1 else None})
+        rows.append(row)
     print(json.dumps({"config": cfg, "model": "tools/scaling_model.py (calibrated on the 1-GPU traces)",
                       "rows": rows}))
 
