@@ -814,7 +814,7 @@ __global__ void k_cgsg_reduce(const double2* __restrict__ part, int ngrid, int s
 // column (as k_givens; fused here, the column in shared memory).
 // red = [h_0..h_k, g_k0..g_kk, ||w||^2] (reduced over CTAs / ranks); Gm is the
 // full Hermitian (maxit + 1)^2 Gram matrix, row-major: Gm[i ldg + j] = v_i^H v_j.
-__global__ void k_cgsg_coef(GmresDev G, int k, const double2* red, double2* Gm, int ldg, double2* cbuf) {
+__global__ void __launch_bounds__(1024) k_cgsg_coef(GmresDev G, int k, const double2* red, double2* Gm, int ldg, double2* cbuf) {
   extern __shared__ double2 sh[];  // h, c, Gh, Gc (k+1 each), column (k+2), 2 (k+1) terms, sn, cs
   const int kp1 = k + 1;
   double2* h = sh;
@@ -920,7 +920,7 @@ cudaError_t gmres_arnoldi_cgsg(Ctx& c, GmresDev& G, int k, const int* blocks, in
     if (cudaError_t e = allreduce_sum_doubles(c, (double*)red, 2 * (size_t)cnt, nccl_comm)) return e;
   }
   double2* cbuf = red + cnt;  // c (k+1) + ||w''||
-  k_cgsg_coef<<<1, 256, (size_t)(8 * kp1 + 2) * sizeof(double2), c.stream>>>(G, k, red, Gm, ldg, cbuf);
+  k_cgsg_coef<<<1, 1024, (size_t)(8 * kp1 + 2) * sizeof(double2), c.stream>>>(G, k, red, Gm, ldg, cbuf);
   const int ug = std::min(grid * 4, std::max(1, (int)((total + 255) / 256)));
   k_cgsg_update<<<ug, 256, 0, c.stream>>>(G, blocks, nb, c.n, k, cbuf);
   return cudaGetLastError();
