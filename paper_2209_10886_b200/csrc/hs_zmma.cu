@@ -434,8 +434,12 @@ __device__ __forceinline__ void z2_wait(unsigned long long* b, unsigned parity) 
         : "memory");
   } while (!ok);
 }
+// CTA-local destination and mbarrier (.shared::cta).  The .shared::cluster
+// form with shared::cta-window addresses gave wrong blocks in cluster launches
+// (even of cluster size 1) once two CTAs shared an SM (round 2,
+// tools/zmma_check.py); the CTA-window form is the one these addresses denote.
 __device__ __forceinline__ void z2_copy(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+  asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    z2_smem(dst)),
                "l"(src), "r"(bytes), "r"(z2_smem(bar))
                : "memory");
@@ -488,7 +492,7 @@ __device__ __forceinline__ void epi_store(const Epi& e, long long t, double2 y, 
 // coalesced accesses (k-major: consecutive right-hand sides of a row are
 // consecutive elements; n-major: consecutive rows of a column are).
 template <int BN, int TM, int TN, bool NMAJ, int S, bool PERS, int KG>
-__global__ void __launch_bounds__(Z2<BN, TM, TN, NMAJ, S, PERS, KG>::THREADS, 1)
+__global__ void __launch_bounds__(Z2<BN, TM, TN, NMAJ, S, PERS, KG>::THREADS, (!PERS && KG == 1 && BN == 32) ? 2 : 1)
     k_zmma2(const MmaTask* __restrict__ tasks, int ntasks, const MmaCol* __restrict__ cols,
             const double2* __restrict__ A, const double2* srcA, const double2* srcB,
             const double2* __restrict__ zeros, Epi e, int n, int R, int KS, unsigned long long* tr, int seq,
@@ -1119,6 +1123,11 @@ void launch_zmma(Ctx& c, const DevMma& m, const double2* A, const double2* srcA,
       cfg.gridDim = dim3(m.ntasks * KS);
     }
     attr[0].val.clusterDim.x = KS;
+    static const int test2 = getenv("HS_ZMMA2_TEST2CTA") ? atoi(getenv("HS_ZMMA2_TEST2CTA")) : 0;
+    if (KS == 1 && test2 != 2) {  // no cluster launch at all when K is not split
+      cfg.attrs = attr + 1;
+      cfg.numAttrs = pdl ? 1 : 0;
+    }
     // ticket slot of a persistent launch (a ring: consecutive, possibly
     // overlapping launches never share a counter); its claims = tasks + grid
     unsigned* ticket = nullptr;
@@ -1144,6 +1153,14 @@ void launch_zmma(Ctx& c, const DevMma& m, const double2* A, const double2* srcA,
     cudaLaunchKernelEx(&cfg, K, (const MmaTask*)m.tasks, m.ntasks, (const MmaCol*)m.cols, A, srcA, srcB, zeros, \
                        e, c.n, R, KS, tr, seq, Aelems, LR, ticket, tbase);                                      \
   } while (0)
+    if (test2 && m.kind == 1 && m.bn == 32 && !pers) {  // diagnostics: the 2-CTA-per-SM form of round 2's first version
+      using FT = Z2<32, 1, 2, false, 3, false, 1>;
+      static const cudaError_t at = cudaFuncSetAttribute(k_zmma2<32, 1, 2, false, 3, false, 1>,
+                                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FT::SMEM);
+      (void)at;
+      Z2_LAUNCH(FT, (k_zmma2<32, 1, 2, false, 3, false, 1>));
+      return;
+    }
     if (m.kind == 2 && m.bn == 64) Z2_LAUNCH(Z2Cols64, Z2K_COLS64);
     else if (m.kind == 2 && pers) Z2_LAUNCH(Z2Cols32P, Z2K_COLS32P);
     else if (m.kind == 2) Z2_LAUNCH(Z2Cols32, Z2K_COLS32);
