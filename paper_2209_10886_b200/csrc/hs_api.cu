@@ -2370,10 +2370,13 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
   // same iterations and histories within 1e-10 of the oracle's MGS.  Mode 5
   // ("mgs") keeps the MGS kernels (the SPEC's literal Arnoldi).
   static const bool bands_cgs2 = getenv("HS_ARNOLDI_BANDS") && std::string(getenv("HS_ARNOLDI_BANDS")) == "cgs2";
-  const bool auto1 = c->gmres_mode == 0 && R == 1;
+  // (the coefficient kernel keeps ~8 (k + 1) complex values in shared memory
+  // and the Gram matrix is (maxit + 1)^2: beyond 1500 iterations the MGS kernels)
+  const bool auto1 = c->gmres_mode == 0 && R == 1 && maxit <= 1500;
   const bool cgs2 = c->gmres_mode == 3 || (auto1 && c->plan.nranks > 1 && bands_cgs2);
   const bool cgsg = c->gmres_mode == 4 || (auto1 && !(c->plan.nranks > 1 && bands_cgs2));
   if ((cgs2 || cgsg) && R != 1) return fail(c, 1, "CGS2 Arnoldi supports one right-hand side");
+  if (cgsg && maxit > 1500) return fail(c, 1, "the Gram-corrected CGS2 Arnoldi supports maxit <= 1500");
   const bool dist = c->plan.nranks > 1 || c->gmres_mode == 1 || cgs2 || cgsg;
   const long long LR = LRof(c, R);
   if (LR == 0) {  // empty interface system (1 x 1 lattice): 0 iterations
@@ -2951,10 +2954,15 @@ int hs_test_peer_allreduce(hs_ctx* c, int G, int count, int repeats, const doubl
   const size_t area = kPeerRedBytes, nbuf = (size_t)repeats * G * count;
   char* d = nullptr;
   double* bufs = nullptr;
-  CK(cudaMalloc((void**)&d, area * G));
-  CK(cudaMemsetAsync(d, 0, area * G, c->stream));
-  CK(cudaMalloc((void**)&bufs, nbuf * sizeof(double)));
-  CK(cudaMemcpyAsync(bufs, in, nbuf * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+  cudaError_t ea = cudaMalloc((void**)&d, area * G);
+  if (ea == cudaSuccess) ea = cudaMalloc((void**)&bufs, nbuf * sizeof(double));
+  if (ea == cudaSuccess) ea = cudaMemsetAsync(d, 0, area * G, c->stream);
+  if (ea == cudaSuccess) ea = cudaMemcpyAsync(bufs, in, nbuf * sizeof(double), cudaMemcpyHostToDevice, c->stream);
+  if (ea != cudaSuccess) {
+    if (d) cudaFree(d);
+    if (bufs) cudaFree(bufs);
+    CK(ea);
+  }
   PeerRedArgs a;
   a.G = G;
   a.self = -1;

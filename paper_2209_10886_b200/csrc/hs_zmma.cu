@@ -561,7 +561,8 @@ __global__ void __launch_bounds__(Z2<BN, TM, TN, NMAJ, S, PERS, KG>::THREADS, (!
         unsigned raw = 0;
         if (lane == 0) raw = atomicAdd(ticket, 1u);
         t = (int)(__shfl_sync(0xffffffffu, raw, 0) - tbase);
-        if (t >= ntasks) {
+        HS_DCHECK(t >= 0, DBG_INDEX);
+        if (t >= ntasks || t < 0) {
           if (lane == 0) {
             zc.stop = 1;
             z2_arrive(&dfull[d]);
@@ -1136,7 +1137,6 @@ void launch_zmma(Ctx& c, const DevMma& m, const double2* A, const double2* srcA,
       const int slot = (int)(c.z2_seq++ % kZ2TicketSlots);
       ticket = c.z2_tickets + slot;
       tbase = c.z2_base[slot];
-      c.z2_base[slot] += (unsigned)(m.ntasks + (int)cfg.gridDim.x);
     }
     const long long Aelems = (long long)(A == c.Tcls ? c.Tcls_elems : c.T_elems);
     const long long LR = c.plan.L * (long long)R;
@@ -1153,6 +1153,17 @@ void launch_zmma(Ctx& c, const DevMma& m, const double2* A, const double2* srcA,
     cudaLaunchKernelEx(&cfg, K, (const MmaTask*)m.tasks, m.ntasks, (const MmaCol*)m.cols, A, srcA, srcB, zeros, \
                        e, c.n, R, KS, tr, seq, Aelems, LR, ticket, tbase);                                      \
   } while (0)
+    // a persistent launch's claims are tasks + grid (every CTA's last claim
+    // fails); counted only when the launch was accepted, so a failed launch
+    // cannot shift the next launch's ticket base on this slot
+    struct Claims {
+      Ctx& c;
+      bool pers;
+      int slot, claims;
+      ~Claims() {
+        if (pers && cudaPeekAtLastError() == cudaSuccess) c.z2_base[slot] += (unsigned)claims;
+      }
+    } claims_{c, pers, (int)((c.z2_seq + kZ2TicketSlots - 1) % kZ2TicketSlots), m.ntasks + (int)cfg.gridDim.x};
     if (test2 && m.kind == 1 && m.bn == 32 && !pers) {  // diagnostics: the 2-CTA-per-SM form of round 2's first version
       using FT = Z2<32, 1, 2, false, 3, false, 1>;
       static const cudaError_t at = cudaFuncSetAttribute(k_zmma2<32, 1, 2, false, 3, false, 1>,

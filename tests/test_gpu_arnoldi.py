@@ -156,3 +156,14 @@ def test_blocked_mgs_variants_agree(k):
         assert r["orth"] <= 3e-10, (m, r["orth"])
         np.testing.assert_allclose(r["hist"], runs[1]["hist"], rtol=1e-12)
         np.testing.assert_allclose(r["x"], runs[1]["x"], rtol=1e-12)
+
+
+def test_auto_beyond_1500_iterations_uses_mgs():
+    """maxit > 1500: auto falls back to the MGS kernels (the Gram-corrected
+    CGS2 keeps O(maxit^2) state); the forced mode refuses with ValueError."""
+    s = system(1)
+    G = golden("cfg1")
+    r = s.gmres(G["b"], "bsp", tol=1e-6, maxit=2000)
+    assert r.iterations == int(G["gm_iters"]) and r.converged
+    with pytest.raises(ValueError):
+        s.gmres(G["b"], "bsp", tol=1e-6, maxit=2000, arnoldi="cgs2g")
