@@ -352,8 +352,9 @@ __global__ void __launch_bounds__(THREADS) k_zmma(const MmaTask* __restrict__ ta
 // L2-resident operands (the cp.async core with 4 warps x 2 K halves: ~0.4).
 constexpr int Z2KC = 32;
 
-template <int BN, int TM, int TN, bool NMAJ, int S, bool PERS, int KG = 1>
+template <int BN, int TM, int TN, bool NMAJ, int S, bool PERS, int KG = 1, int KC_ = Z2KC>
 struct Z2 {
+  static constexpr int KC = KC_;  // k rows per chunk (64: the n-major shared-map form, half the copies per k)
   // KG warp groups split every chunk's k range (each group owns the whole tile;
   // group 1's partial is added to group 0's through shared memory): a 32 x 32
   // tile then keeps 8 warps x 12 accumulator chains in flight, which the DMMA
@@ -367,9 +368,9 @@ struct Z2 {
   // n-major contraction copy-bound; the 4-way bank conflicts of the unpadded
   // fragment loads are hidden behind the DMMAs, tools/zcore_bench.cu)
   static constexpr int SA = 32;
-  static constexpr int SB = NMAJ ? Z2KC + 4 : BN + 2;
-  static constexpr int BROWS = NMAJ ? BN : Z2KC;
-  static constexpr int STAGE = Z2KC * SA + BROWS * SB;
+  static constexpr int SB = NMAJ ? KC + 4 : BN + 2;
+  static constexpr int BROWS = NMAJ ? BN : KC;
+  static constexpr int STAGE = KC * SA + BROWS * SB;
   static constexpr int YS = BN + 1;  // output tile row stride (conflict-free fragment writes and row/column reads)
   static constexpr int RING = S * STAGE;
   // persistent: a separate output tile (the ring already holds the next task's
@@ -491,13 +492,14 @@ __device__ __forceinline__ void epi_store(const Epi& e, long long t, double2 y, 
 // goes through shared memory and is finished by all consumer threads with
 // coalesced accesses (k-major: consecutive right-hand sides of a row are
 // consecutive elements; n-major: consecutive rows of a column are).
-template <int BN, int TM, int TN, bool NMAJ, int S, bool PERS, int KG>
-__global__ void __launch_bounds__(Z2<BN, TM, TN, NMAJ, S, PERS, KG>::THREADS, (!PERS && KG == 1 && BN == 32) ? 2 : 1)
+template <int BN, int TM, int TN, bool NMAJ, int S, bool PERS, int KG, int KCT = Z2KC>
+__global__ void __launch_bounds__(Z2<BN, TM, TN, NMAJ, S, PERS, KG, KCT>::THREADS, (!PERS && KG == 1 && BN == 32) ? 2 : 1)
     k_zmma2(const MmaTask* __restrict__ tasks, int ntasks, const MmaCol* __restrict__ cols,
             const double2* __restrict__ A, const double2* srcA, const double2* srcB,
             const double2* __restrict__ zeros, Epi e, int n, int R, int KS, unsigned long long* tr, int seq,
             long long Aelems, long long LR, unsigned* ticket, unsigned tbase) {
-  using F = Z2<BN, TM, TN, NMAJ, S, PERS, KG>;
+  using F = Z2<BN, TM, TN, NMAJ, S, PERS, KG, KCT>;
+  constexpr int KC = F::KC;
   extern __shared__ __align__(128) double2 sm[];
   __shared__ __align__(8) unsigned long long full[S], empty[S], dfull[2], dempty[2];
   __shared__ ZCols2<BN> zcs[F::ND];
@@ -515,7 +517,7 @@ __global__ void __launch_bounds__(Z2<BN, TM, TN, NMAJ, S, PERS, KG>::THREADS, (!
   unsigned long long* trow = tr ? tr + 6ull * blockIdx.x : nullptr;
   if (trow && tid == 0) trow[0] = z2_gtimer();
   auto kslice = [&](const MmaTask& tk, int& kc0, int& nk) {
-    const int nk_all = tk.K / Z2KC;
+    const int nk_all = tk.K / KC;
     kc0 = (int)((long long)nk_all * rank / KS);
     nk = (int)((long long)nk_all * (rank + 1) / KS) - kc0;
   };
@@ -571,7 +573,7 @@ __global__ void __launch_bounds__(Z2<BN, TM, TN, NMAJ, S, PERS, KG>::THREADS, (!
         }
       }
       const MmaTask tk = tasks[t];
-      HS_DCHECK(tk.a_off >= 0 && tk.a_off + (long long)tk.K * 32 <= Aelems && tk.K % Z2KC == 0, DBG_MAP);
+      HS_DCHECK(tk.a_off >= 0 && tk.a_off + (long long)tk.K * 32 <= Aelems && tk.K % KC == 0, DBG_MAP);
       HS_DCHECK(tk.ncols >= 1 && tk.ncols <= BN, DBG_INDEX);
       if (PERS) {
         if (lane == 0) zc.tk = tk, zc.stop = 0;
@@ -582,28 +584,28 @@ __global__ void __launch_bounds__(Z2<BN, TM, TN, NMAJ, S, PERS, KG>::THREADS, (!
       int kc0, nk;
       kslice(tk, kc0, nk);
       const unsigned bytesB =
-          NMAJ ? (unsigned)(BN * 32 * sizeof(double2)) : (unsigned)(Z2KC * tk.ncols * sizeof(double2));
-      const unsigned bytes = (unsigned)(Z2KC * 32 * sizeof(double2)) + bytesB;
+          NMAJ ? (unsigned)(BN * KC * sizeof(double2)) : (unsigned)(KC * tk.ncols * sizeof(double2));
+      const unsigned bytes = (unsigned)(KC * 32 * sizeof(double2)) + bytesB;
       const double2* Ab = A + tk.a_off;
       auto issueA = [&](int st, int kc) {
         if (lane == 0)
-          z2_copy(sm + (size_t)st * F::STAGE, Ab + (long long)kc * Z2KC * 32, Z2KC * 32 * sizeof(double2), &full[st]);
+          z2_copy(sm + (size_t)st * F::STAGE, Ab + (long long)kc * KC * 32, KC * 32 * sizeof(double2), &full[st]);
       };
       auto issueB = [&](int st, int kc) {
-        double2* sb = sm + (size_t)st * F::STAGE + Z2KC * F::SA;
-        const int k0 = kc * Z2KC, q = k0 / n, p0 = k0 - q * n;
+        double2* sb = sm + (size_t)st * F::STAGE + KC * F::SA;
+        const int k0 = kc * KC, q = k0 / n, p0 = k0 - q * n;
         if (NMAJ) {
           for (int j = lane; j < BN; j += 32) {
             const long long off = zc.in[j][q];
-            HS_DCHECK(off < 0 || off + (long long)(p0 + 31) * R < LR, DBG_VEC);
+            HS_DCHECK(off < 0 || off + (long long)(p0 + KC - 1) * R < LR, DBG_VEC);
             const double2* src = off >= 0 ? (zc.alt[j] ? srcB : srcA) + off + (long long)p0 * R : zeros;
-            z2_copy(sb + j * F::SB, src, 32 * sizeof(double2), &full[st]);
+            z2_copy(sb + j * F::SB, src, KC * sizeof(double2), &full[st]);
           }
         } else {
           // one slab: positions k0.. of the compact faces are consecutive rows of R
-          HS_DCHECK(zc.in[0][0] >= 0 && zc.in[0][0] + (long long)(k0 + Z2KC - 1) * R + tk.ncols - 1 < LR, DBG_VEC);
+          HS_DCHECK(zc.in[0][0] >= 0 && zc.in[0][0] + (long long)(k0 + KC - 1) * R + tk.ncols - 1 < LR, DBG_VEC);
           const double2* base = (zc.alt[0] ? srcB : srcA) + zc.in[0][0] + (long long)k0 * R;
-          for (int r = lane; r < Z2KC; r += 32)
+          for (int r = lane; r < KC; r += 32)
             z2_copy(sb + r * F::SB, base + (long long)r * R, tk.ncols * sizeof(double2), &full[st]);
         }
       };
@@ -636,7 +638,7 @@ __global__ void __launch_bounds__(Z2<BN, TM, TN, NMAJ, S, PERS, KG>::THREADS, (!
     const int wm = wq / F::WN, wn = wq % F::WN;
     const int gid = lane >> 2, tig = lane & 3;
     const int ctid = tid;  // consumers are warps 0 .. NWC - 1
-    constexpr int KH = Z2KC / KG;  // k rows of a chunk per warp group
+    constexpr int KH = KC / KG;  // k rows of a chunk per warp group
     long long g = 0;
     for (int it = 0; PERS || it == 0; ++it) {
       const int d = PERS ? (it & 1) : 0;
@@ -658,7 +660,7 @@ __global__ void __launch_bounds__(Z2<BN, TM, TN, NMAJ, S, PERS, KG>::THREADS, (!
         z2_wait(&full[st], (unsigned)((g / S) & 1));
         if (trow && tid == 0 && g == 0) trow[2] = z2_gtimer();
         const double2* sa = sm + (size_t)st * F::STAGE;
-        const double2* sb = sa + Z2KC * F::SA;
+        const double2* sb = sa + KC * F::SA;
 #pragma unroll
         for (int kk = 0; kk < KH; kk += 4) {
           const int k4 = kg * KH + kk;
@@ -1088,11 +1090,18 @@ using Z2Slab32 = Z2<32, 2, 2, false, 4, false, 2>;
 using Z2Cols64 = Z2<64, 2, 2, true, 3, true>;
 using Z2Cols32 = Z2<32, 2, 2, true, 4, false, 2>;
 using Z2Cols32P = Z2<32, 2, 2, true, 4, true, 2>;
+// n-major with 64-row k chunks (n % 64 == 0): one 32 KB map copy + 32 column
+// copies of 1 KB per chunk, half the copies per k of the 32-row form (the
+// n-major contraction is bound by the TMA unit's per-copy cost otherwise)
+using Z2Cols32K = Z2<32, 2, 2, true, 2, false, 2, 64>;
+using Z2Cols32PK = Z2<32, 2, 2, true, 2, true, 2, 64>;
 #define Z2K_SLAB64 k_zmma2<64, 2, 2, false, 3, true, 1>
 #define Z2K_SLAB32 k_zmma2<32, 2, 2, false, 4, false, 2>
 #define Z2K_COLS64 k_zmma2<64, 2, 2, true, 3, true, 1>
 #define Z2K_COLS32 k_zmma2<32, 2, 2, true, 4, false, 2>
 #define Z2K_COLS32P k_zmma2<32, 2, 2, true, 4, true, 2>
+#define Z2K_COLS32K k_zmma2<32, 2, 2, true, 2, false, 2, 64>
+#define Z2K_COLS32PK k_zmma2<32, 2, 2, true, 2, true, 2, 64>
 
 void launch_zmma(Ctx& c, const DevMma& m, const double2* A, const double2* srcA, const double2* srcB,
                  const double2* zeros, const Epi& e, int R) {
@@ -1172,8 +1181,12 @@ void launch_zmma(Ctx& c, const DevMma& m, const double2* A, const double2* srcA,
       Z2_LAUNCH(FT, (k_zmma2<32, 1, 2, false, 3, false, 1>));
       return;
     }
+    static const bool kc64 = !(getenv("HS_ZMMA2_KC64") && atoi(getenv("HS_ZMMA2_KC64")) == 0);
+    const bool k64 = kc64 && m.kind == 2 && c.n % 64 == 0 && m.minK % 64 == 0;
     if (m.kind == 2 && m.bn == 64) Z2_LAUNCH(Z2Cols64, Z2K_COLS64);
+    else if (m.kind == 2 && pers && k64) Z2_LAUNCH(Z2Cols32PK, Z2K_COLS32PK);
     else if (m.kind == 2 && pers) Z2_LAUNCH(Z2Cols32P, Z2K_COLS32P);
+    else if (k64) Z2_LAUNCH(Z2Cols32K, Z2K_COLS32K);
     else if (m.kind == 2) Z2_LAUNCH(Z2Cols32, Z2K_COLS32);
     else if (m.bn == 64) Z2_LAUNCH(Z2Slab64, Z2K_SLAB64);
     else Z2_LAUNCH(Z2Slab32, Z2K_SLAB32);
@@ -1579,6 +1592,8 @@ cudaError_t set_zmma_smem_limit() {
   cudaFuncSetAttribute(Z2K_COLS64, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cols64::SMEM);
   cudaFuncSetAttribute(Z2K_COLS32, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cols32::SMEM);
   cudaFuncSetAttribute(Z2K_COLS32P, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cols32P::SMEM);
+  cudaFuncSetAttribute(Z2K_COLS32K, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cols32K::SMEM);
+  cudaFuncSetAttribute(Z2K_COLS32PK, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Z2Cols32PK::SMEM);
   return cudaFuncSetAttribute(k_zmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kZmmaSmem);
 }
 
