@@ -134,6 +134,7 @@ struct FusedArgs {
   int* split_cnt;             // split-K arrivals per pair (odd arrival combines)
   MultiRankArgs mr;
   long long L = 0, T_elems = 0;  // bounds of the device checks (debug library)
+  int prefetch = 0;              // k_bsp_tma: L2-prefetch each tile's chunks beyond the ring at its claim
   int nitems = 0, nsub = 0, npairs = 0;
 };
 
@@ -643,6 +644,22 @@ __global__ void __maxnreg__(96) k_bsp_tma(FusedArgs a) {  // 96: two 10-warp CTA
         if (td.t >= rv.ntiles()) break;
         const int nch = (td.c1 + 31) / 32;
         const double2* src = a.T + td.map_off;
+        if (a.prefetch) {
+          // the chunks beyond the ring stream into L2 now, while the consumers
+          // wait for the tile's dependencies: the bulk copies of those chunks
+          // then hit L2 (a critical-path tile streams at L2 rather than at its
+          // share of HBM bandwidth; the bytes from HBM are the same)
+          const int cp0 = td.c0 / 32 + S;
+          if (cp0 < nch) {
+            const long long e0 = (long long)cp0 * kChunk;
+            // prefetch = 1: the whole rest of the tile; 2: the next ring's worth
+            const int cp1 = a.prefetch == 2 ? min(nch, cp0 + S) : nch;
+            const long long e1 = (long long)min(td.K, 32 * cp1) * kRowTile;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + e0),
+                         "r"((unsigned)((e1 - e0) * sizeof(double2)))
+                         : "memory");
+          }
+        }
         for (int ch = td.c0 / 32; ch < nch; ++ch, ++g) {
           const int st = (int)(g % S);
           mbar_wait(&empty[st], (unsigned)((g / S) & 1) ^ 1);
@@ -1025,7 +1042,8 @@ cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double
     a.r = r; a.zL = zL; a.rp = rp; a.w = w; a.z = z; a.wout = wout;
     a.done = f.counters; a.ticket = f.counters + c.plan.npairs;
     a.ntiles = f.ntiles; a.n = c.n; a.maxK = f.maxK; a.nv = f.nv;
-  a.L = c.plan.L; a.T_elems = (long long)c.T_elems; a.nitems = f.nitems; a.nsub = c.plan.nsub; a.npairs = c.plan.npairs;
+  a.L = c.plan.L; a.T_elems = (long long)c.T_elems;
+  { static const int pf = getenv("HS_TMA_PREFETCH") ? atoi(getenv("HS_TMA_PREFETCH")) : 0; a.prefetch = pf; } a.nitems = f.nitems; a.nsub = c.plan.nsub; a.npairs = c.plan.npairs;
     a.direct_signal = f.direct_signal;
     a.split_buf = f.split_buf; a.split_cnt = f.split_cnt;
     a.map_keep = c.map_mode == 2;
@@ -1052,7 +1070,8 @@ cudaError_t launch_bsp_fused(Ctx& c, const DevFused& f, const double2* r, double
   a.r = r; a.zL = zL; a.rp = rp; a.w = w; a.z = z; a.wout = wout;
   a.done = f.counters; a.ticket = f.counters + c.plan.npairs;
   a.ntiles = f.ntiles; a.n = c.n; a.maxK = f.maxK; a.nv = f.nv;
-  a.L = c.plan.L; a.T_elems = (long long)c.T_elems; a.nitems = f.nitems; a.nsub = c.plan.nsub; a.npairs = c.plan.npairs;
+  a.L = c.plan.L; a.T_elems = (long long)c.T_elems;
+  { static const int pf = getenv("HS_TMA_PREFETCH") ? atoi(getenv("HS_TMA_PREFETCH")) : 0; a.prefetch = pf; } a.nitems = f.nitems; a.nsub = c.plan.nsub; a.npairs = c.plan.npairs;
     a.trace = (c.trace_on && c.trace && c.trace_cap >= (size_t)f.ntiles) ? c.trace : nullptr;
     if (a.trace) c.trace_rows = f.ntiles;
   const int grid = std::max(1, std::min(f.ntiles, per_sm[var] * c.num_sms));
@@ -1087,7 +1106,8 @@ cudaError_t launch_bsp_fused_ranks(Ctx& c, const DevFused& f, const MultiRankArg
   a.r = nullptr; a.zL = a.rp = a.w = a.z = a.wout = nullptr;
   a.done = nullptr; a.ticket = nullptr;
   a.ntiles = 0; a.n = c.n; a.maxK = f.maxK; a.nv = f.nv; a.trace = nullptr;
-  a.L = c.plan.L; a.T_elems = (long long)c.T_elems; a.nitems = f.nitems; a.nsub = c.plan.nsub; a.npairs = c.plan.npairs;
+  a.L = c.plan.L; a.T_elems = (long long)c.T_elems;
+  { static const int pf = getenv("HS_TMA_PREFETCH") ? atoi(getenv("HS_TMA_PREFETCH")) : 0; a.prefetch = pf; } a.nitems = f.nitems; a.nsub = c.plan.nsub; a.npairs = c.plan.npairs;
   a.direct_signal = f.direct_signal;
   a.split_buf = f.split_buf; a.split_cnt = f.split_cnt;
   a.map_keep = c.map_mode == 2;
