@@ -330,26 +330,29 @@ __global__ void __launch_bounds__(THREADS) k_zmma(const MmaTask* __restrict__ ta
 // ---------------------------------------------------------------------------
 // k_zmma2: the per-step contraction with bulk-copy (TMA) staging.
 //
-// One CTA = one task of 32 map rows x BN columns (64: all 64 right-hand sides
-// of a subdomain's slab, or 64 subdomain columns of a shared-map step), or a
-// 1/KS slice of its K range when the step has too few tasks to fill the GPU
-// (cluster split-K, partial tiles summed by rank 0 through DSMEM in rank
-// order -- deterministic).  A producer warp streams K in chunks of 32 through
-// an S-stage ring with cp.async.bulk copies (mbarrier complete_tx):
-//   A [k][m]  one 16 KB copy per chunk (unpadded, see Z2::SA);
+// One task = 32 map rows x BN columns (64: all 64 right-hand sides of a
+// subdomain's slab, or 64 subdomain columns of a shared-map step; 32 for
+// smaller steps).  A producer warp streams K in chunks of KC (32, or 64 for
+// the n-major form) through an S-stage ring with cp.async.bulk copies
+// (mbarrier complete_tx):
+//   A [k][m]  one copy per chunk (unpadded, see Z2::SA);
 //   B rows padded so the 128-bit fragment loads are conflict-free:
 //   B k-major [k][j] (R RHS of one slab: one contiguous row per position)
-//             stride BN + 2, the same argument;
-//   B n-major [j][k] (shared maps, one column per subdomain: its 32 positions
-//             of the chunk's face are one contiguous 512-byte run) stride 36:
+//             stride BN + 2: units 2 tig + gid (mod 8), distinct;
+//   B n-major [j][k] (shared maps, one column per subdomain: its KC positions
+//             of the chunk's face are one contiguous run) stride KC + 4:
 //             units 4 gid + tig (mod 8), distinct.
-// Absent faces read a zero buffer.  NWC consumer warps each own TM x TN 8x8
-// DMMA tiles of the output over the whole chunk (no intra-CTA K split), 3M
-// complex product.  The map chunks do not depend on the previous step, so the
-// producer issues the first S stages' map rows before griddepcontrol.wait
-// (programmatic dependent launch) and only the vector rows after it.
-// tools/zcore_bench.cu: this core sustains 0.80-0.86 of the DMMA peak on
-// L2-resident operands (the cp.async core with 4 warps x 2 K halves: ~0.4).
+// Absent faces read a zero buffer.  Consumer warps own TM x TN 8x8 DMMA tiles
+// of the output over the chunk (KG warp groups split the chunk's k range),
+// 3M complex product.  Launch forms (launch_zmma): one task per CTA, K split
+// over a thread-block cluster when the step leaves SMs idle (partial tiles
+// summed by rank 0 through DSMEM in rank order -- deterministic), or
+// persistent (PERS: tasks claimed from a ticket counter, the next task's
+// chunks streaming while the current one finishes).  The map chunks do not
+// depend on the previous step, so the producer issues the first stages' map
+// copies before griddepcontrol.wait (programmatic dependent launch) and the
+// vector rows after it.  tools/zcore_bench.cu: this core sustains 0.80-0.86
+// of the DMMA peak on L2-resident operands (the cp.async core: ~0.4).
 constexpr int Z2KC = 32;
 
 template <int BN, int TM, int TN, bool NMAJ, int S, bool PERS, int KG = 1, int KC_ = Z2KC>
@@ -373,8 +376,6 @@ struct Z2 {
   static constexpr int STAGE = KC * SA + BROWS * SB;
   static constexpr int YS = BN + 1;  // output tile row stride (conflict-free fragment writes and row/column reads)
   static constexpr int RING = S * STAGE;
-  // persistent: a separate output tile (the ring already holds the next task's
-  // chunks); one task per CTA: the drained ring holds it
   static constexpr int NTR = TM * TN * 2;  // accumulator pairs per lane
   // persistent: a separate output tile and warp-group reduction area (the ring
   // already holds the next task's chunks); one task per CTA: the drained ring
