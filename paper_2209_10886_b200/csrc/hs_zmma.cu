@@ -9,21 +9,20 @@
 //     Y = T4[rows, :] * [x_s1 ... x_sm] with missing faces read as zero and
 //     their outputs dropped -- FP64-bound with the map L2-resident.
 //
-// A task = 32 map rows x up to 32 columns.  A is read from the strip-major map
-// layout (a 32-row strip is contiguous, K x 32), B columns are gathered per
-// face from the vector (column descriptor: per-face element offset or -1,
-// stride R between consecutive face positions).  K is staged in chunks of 32
-// through a 3-stage cp.async pipeline.  8 warps: 4 output quadrants (16 x 16 =
-// 2 x 2 DMMA tiles; a complex MAC is 3 real DMMAs by the 3M (Gauss) product)
-// x 2 halves of every K chunk, reduced through shared memory.
-//
-// Two launch forms share that main loop:
-//   * k_zmma: one launch per sweep step; when a step has few tasks the K range
-//     is also split over a thread-block cluster of KS CTAs whose partial tiles
-//     rank 0 sums through distributed shared memory in rank order;
-//   * k_zmma_fused: the whole BSP apply as one persistent dataflow launch
-//     (tickets in schedule order + per-(block, 32-RHS chunk) completion
-//     counters), as k_bsp_fused does for one right-hand side.
+// Kernels (a complex MAC is 3 real DMMAs by the 3M (Gauss) product in all):
+//   * k_zmma2 (default, per step): bulk-copy (TMA) staged, producer warp +
+//     mbarrier ring, one task per CTA with cluster split-K or persistent;
+//   * k_zmma2_df (default for R right-hand sides): the whole BSP apply as one
+//     persistent dataflow launch on the same core (tickets, per-(block,
+//     32-RHS chunk) completion counters);
+//   * k_zmma / k_zmma_fused (round 1, cp.async core: tasks of 32 rows x 32
+//     columns, 4 output quadrants x 2 K halves): the shared maps with several
+//     right-hand sides (n-major columns of stride R are not bulk-copyable),
+//     HS_ZMMA2=0, and the fused shared-map launch (hs_set_fused bit 3);
+//   * k_zgemm_dmma: the factorisation's batched block solves.
+// A task's A operand is a 32-row strip of the strip-major map layout (K x 32,
+// contiguous); B columns come from the vector through column descriptors
+// (per-face element offset or -1, stride R between consecutive positions).
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
