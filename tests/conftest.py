@@ -52,3 +52,31 @@ def product_problem(c):
                        scatterer=None if c["center"] is None else Scatterer(tuple(c["center"]), c["radius"]),
                        incident_direction=(float(np.cos(ang)), float(np.sin(ang))))
     return spec, Partition(c["n1"], c["n2"])
+
+
+# HS_LIB=debug runs the whole GPU suite on the device-checks library: after
+# every GPU test the first bounds / watchdog failure since the previous test
+# (hs_debug_check) must be zero.  The check needs a context for its stream and
+# device; the failure records are per process, so one small context serves.
+_DBG = {}
+
+
+@pytest.fixture(autouse=True)
+def _device_checks(request):
+    yield
+    if os.environ.get("HS_LIB") != "debug" or request.node.get_closest_marker("gpu") is None:
+        return
+    import ctypes as C
+
+    import torch
+    if not torch.cuda.is_available():
+        return
+    if "sys" not in _DBG:
+        from paper_2209_10886_b200.configs import small_case
+        from paper_2209_10886_b200.interface_system import GpuInterfaceSystem
+        spec, part = product_problem(small_case(2, 2, 8))
+        _DBG["sys"] = GpuInterfaceSystem(spec, part)
+    first, en = C.c_uint64(0), C.c_int(0)
+    _DBG["sys"].ctx.call("hs_debug_check", C.byref(first), C.byref(en))
+    assert en.value == 1, "HS_LIB=debug but the release library is loaded"
+    assert first.value == 0, f"device check failed: unit {first.value >> 48}, line {(first.value >> 8) & 0xFFFFFFFF}, tag {first.value & 0xFF}"
