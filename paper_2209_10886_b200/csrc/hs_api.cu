@@ -367,6 +367,8 @@ std::vector<Tile> list_schedule(const std::vector<Tile>& tiles, const std::vecto
 // Dataflow plan of one BSP apply on the DMMA contraction: every task of the
 // forward steps, the residual and the backward steps in schedule order, with
 // per-(block, 32-RHS chunk) completion counts it waits for / completes.
+bool map_once_steps(const Ctx* c);
+
 int build_fused_mma(Ctx* c, int R, bool shared) {
   free_fused_mma(c);
   DevFusedMma& f = c->fused_mma;
@@ -380,6 +382,10 @@ int build_fused_mma(Ctx* c, int R, bool shared) {
   std::vector<int> written(ncnt, 0);
   double flops = 0;
   auto counter = [&](long long off, int r) { return (int)((off - r) / ((long long)n * R)) * nch + r / 32; };
+  // fill tasks and split-K pairs are k_zmma2_df's (launch_zmma_fused): not with
+  // HS_ZMMA2=0 or the shared maps with R > 1 (k_zmma_fused)
+  static const bool z2 = !(getenv("HS_ZMMA2") && atoi(getenv("HS_ZMMA2")) == 0);
+  const bool df = z2 && (!shared || R == 1);
   auto add = [&](const DevStep& st, int phase) {
     std::vector<MmaTask> tasks;
     std::vector<MmaCol> sc;
@@ -413,20 +419,50 @@ int build_fused_mma(Ctx* c, int R, bool shared) {
     for (int k2 : inc_step) written[k2]++;
   };
   for (auto& st : c->fwd) add(st, 0);
-  add(c->full, 1);
+  // map-once residual (as the per-step path, do_precond): the residual tasks
+  // cover only the rows where r' can be nonzero; fill tasks set rp = w = 0,
+  // z = zL on the other blocks (after the residual tasks in plan order, so no
+  // residual task waits on a fill).  HS_ZMMA2_DF_MO=0: the full residual step.
+  static const bool mo_env = !(getenv("HS_ZMMA2_DF_MO") && atoi(getenv("HS_ZMMA2_DF_MO")) == 0);
+  const bool mo = mo_env && df && map_once_steps(c);
+  if (mo) {
+    add(c->mo_resid, 1);
+    std::vector<int> fc;
+    for (int b : c->mo_zero_host)
+      for (int ch = 0; ch < nch; ++ch) fc.push_back(b * nch + ch);
+    // ~4k elements per fill task
+    const int per = std::max(1, 4096 / (n * std::min(R, 32)));
+    for (size_t i = 0; i < fc.size(); i += per) {
+      FusedMmaTask ft;
+      ft.task = MmaTask();
+      ft.task.a_off = 0; ft.task.K = 0; ft.task.ncols = 0; ft.task.col0 = 0;
+      ft.phase = 3;
+      ft.dep0 = (int)deps.size(); ft.ndep = 0;
+      ft.inc0 = (int)incs.size(); ft.ninc = 0;
+      for (size_t j = i; j < std::min(fc.size(), i + per); ++j) {
+        const int k2 = fc[j];
+        if (written[k2] > 0) { deps.push_back({k2, written[k2]}); ft.ndep++; }
+        incs.push_back(k2); ft.ninc++;
+      }
+      ftasks.push_back(ft);
+    }
+    for (int k2 : fc) written[k2]++;
+  } else {
+    add(c->full, 1);
+  }
   for (auto& st : c->bwd) add(st, 2);
   // k_zmma2_df split-K (opt-in, HS_ZMMA2_SPLIT=1): the sweep steps' tasks (the
   // dependency chain) in two K halves on two CTAs; the later arrival adds the
-  // halves in half order and finishes the task.  Measured slower at cfg4
-  // (0.272 vs 0.239 ms per apply): the partial exchange and the extra tickets
-  // cost more than the halved contraction saves.  Not for the shared maps.
+  // halves in half order and finishes the task.  cfg4: 0.208 ms either way
+  // (the chain's links shrink, the extra tickets and partial exchange eat it);
+  // the shared maps (K = 4n, 16 chunks per task): cfg5 0.490 -> 0.384 ms.
   static const bool split = getenv("HS_ZMMA2_SPLIT") && atoi(getenv("HS_ZMMA2_SPLIT")) != 0;
   int npairs = 0;
-  if (split && !shared) {
+  if (split && df) {
     std::vector<FusedMmaTask> sp;
     sp.reserve(ftasks.size() * 2);
     for (const FusedMmaTask& ft : ftasks) {
-      if (ft.phase == 1 || ft.task.K / 32 < 4) {
+      if (ft.phase == 1 || ft.phase == 3 || ft.task.K / 32 < 4) {
         sp.push_back(ft);
         continue;
       }
@@ -450,7 +486,7 @@ int build_fused_mma(Ctx* c, int R, bool shared) {
         // a pair's completions are its second arrival's: counted once, on half 1
         if (ftasks[t].ks != 0)
           tinc[t].assign(incs.begin() + ftasks[t].inc0, incs.begin() + ftasks[t].inc0 + ftasks[t].ninc);
-        cost[t] = ftasks[t].task.K / 32 / (ftasks[t].ks >= 0 ? 2 : 1);
+        cost[t] = ftasks[t].phase == 3 ? 0.5 : ftasks[t].task.K / 32 / (ftasks[t].ks >= 0 ? 2 : 1);
       }
       ftasks = list_schedule(ftasks, deps, tinc, cost, ncnt, c->num_sms, 3e-6, 1e6);
     }
@@ -464,6 +500,10 @@ int build_fused_mma(Ctx* c, int R, bool shared) {
       upload(c, &f.incs, incs))
     return -1;
   CK(dalloc(c, (void**)&f.counters, (ncnt + 1) * sizeof(int)));
+  if (shared && !c->zeros) {  // the n-major form's zero rows (absent faces, padding columns)
+    CK(dalloc(c, (void**)&c->zeros, 64 * sizeof(double2)));
+    CK(cudaMemsetAsync(c->zeros, 0, 64 * sizeof(double2), c->stream));
+  }
   f.npairs_split = npairs;
   if (npairs > 0) {
     CK(dalloc(c, (void**)&f.split_buf, (size_t)npairs * 2 * 32 * 32 * sizeof(double2)));
@@ -477,7 +517,8 @@ int build_fused_mma(Ctx* c, int R, bool shared) {
   f.ncounters = ncnt;
   f.flops = flops;
   f.minK = 1 << 30;
-  for (const auto& ft : ftasks) f.minK = std::min(f.minK, ft.task.K);
+  for (const auto& ft : ftasks)
+    if (ft.phase != 3) f.minK = std::min(f.minK, ft.task.K);
   f.R = R;
   f.shared = shared;
   f.built = true;
@@ -1094,7 +1135,7 @@ int build_steps(Ctx* c) {
   free_step(c, c->mo_resid);
   free_step(c, c->mo_ims_up);
   free_step(c, c->mo_ims_late);
-  dfree(c, c->mo_zero_blocks, 0); c->mo_zero_blocks = nullptr; c->n_mo_zero = 0;
+  dfree(c, c->mo_zero_blocks, 0); c->mo_zero_blocks = nullptr; c->n_mo_zero = 0; c->mo_zero_host.clear();
   dfree(c, c->mo_r_blocks, 0); c->mo_r_blocks = nullptr; c->n_mo_r = 0;
   Plan& P = c->plan;
   auto f = P.half_steps(0), b = P.half_steps(1);
@@ -1131,6 +1172,7 @@ int build_steps(Ctx* c) {
       return -1;
     if (upload(c, &c->mo_zero_blocks, zero) || upload(c, &c->mo_r_blocks, rfill)) return -1;
     c->n_mo_zero = (int)zero.size();
+    c->mo_zero_host = zero;
     c->n_mo_r = (int)rfill.size();
   }
   // seam blocks (literal mode): groups shared by consecutive windows
@@ -1554,8 +1596,10 @@ int do_precond_ims(Ctx* c, const double2* r, double2* z, double2* wout) {
 // the literal-arithmetic mask bit 2).
 bool mma_fused_path(const Ctx* c, int R) {
   // R right-hand sides on the per-subdomain maps: k_zmma2_df (bit 1, default
-  // on); the shared class maps: k_zmma_fused only on request (bit 3), the
-  // per-step k_zmma2 measured faster there
+  // on); the shared class maps only on request (bit 3: k_zmma2_df n-major for
+  // one right-hand side, else k_zmma_fused) -- the per-step k_zmma2 with
+  // cluster split-K measured faster there (cfg5 0.393 vs 0.490 ms, 0.384 with
+  // HS_ZMMA2_SPLIT=1; cfg3 0.198 vs 0.37 / 0.29)
   return (c->fused_mode & 2) && ((R > 1 && c->map_mode != 1) || (c->map_mode == 1 && (c->fused_mode & 8))) &&
          c->n % 32 == 0 && c->plan.nranks == 1 && c->inter &&
          c->seam == HS_SEAM_DEDUP && c->full.nitems > 0;
@@ -1621,9 +1665,6 @@ int do_precond(Ctx* c, int kind, const double2* r, double2* z, int R) {
     return 0;
   }
   const bool shared = c->map_mode == 1;
-  // opt-in (bit 1): measured slower than per-step cluster split-K launches at
-  // cfg4 / shared cfg5 -- without split-K each task serialises its K chunks and
-  // the step-to-step dependency chain grows
   if (mma_fused_path(c, R)) {
     // the whole apply on the DMMA contraction as one dataflow launch
     if (!c->fused_mma.built || c->fused_mma.R != R || c->fused_mma.shared != shared)

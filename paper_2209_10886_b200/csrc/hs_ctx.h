@@ -166,7 +166,7 @@ struct DevFused {
 // Fused BSP apply on the DMMA contraction (R right-hand sides or shared maps).
 struct FusedMmaTask {
   MmaTask task;
-  int phase;       // 0 forward, 1 residual, 2 backward
+  int phase;       // 0 forward, 1 residual, 2 backward, 3 fill (rp = w = 0, z = zL on the counters' elements)
   int dep0, ndep;  // waits: counters[block * nchunk + chunk] >= count
   int inc0, ninc;  // counters this task completes
   int ks = -1;     // k_zmma2_df split-K: half 0 / 1 of pair `pair` (-1: whole K)
@@ -207,6 +207,8 @@ struct FusedMmaArgs {
   unsigned long long* trace = nullptr;  // k_zmma2_df, per ticket: claimed, inputs met, first chunk, contracted, signalled, info
   double2* split_buf = nullptr;
   int* split_cnt = nullptr;
+  const double2* zeros = nullptr;  // n-major form: the rows of absent faces and padding columns
+  long long LR = 0;                // vector elements (bounds checks)
 };
 
 // Row-band ranks of the fused apply (multi-rank kernel instantiations): every
@@ -355,6 +357,7 @@ struct Ctx {
   // filled without a map read (device lists of own blocks)
   DevStep mo_resid, mo_ims_up, mo_ims_late;
   int* mo_zero_blocks = nullptr;  int n_mo_zero = 0;   // rp = w = 0, z = zL
+  std::vector<int> mo_zero_host;                      // the same blocks (dataflow plans)
   int* mo_r_blocks = nullptr;     int n_mo_r = 0;      // (I - S) z = r
   DevFused fused;        // BSP apply as one dataflow launch (1 RHS, per-subdomain maps, 1 rank)
   DevFused fused_ims;    // the same followed by (I - S) z: GMRES's A M v in one launch

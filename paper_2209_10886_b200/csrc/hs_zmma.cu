@@ -12,13 +12,14 @@
 // Kernels (a complex MAC is 3 real DMMAs by the 3M (Gauss) product in all):
 //   * k_zmma2 (default, per step): bulk-copy (TMA) staged, producer warp +
 //     mbarrier ring, one task per CTA with cluster split-K or persistent;
-//   * k_zmma2_df (default for R right-hand sides): the whole BSP apply as one
-//     persistent dataflow launch on the same core (tickets, per-(block,
-//     32-RHS chunk) completion counters);
+//   * k_zmma2_df (default for R right-hand sides; the shared maps with one
+//     right-hand side on request, hs_set_fused bit 3): the whole BSP apply as
+//     one persistent dataflow launch on the same core (tickets, per-(block,
+//     32-RHS chunk) completion counters, the map-once residual with fill tasks);
 //   * k_zmma / k_zmma_fused (round 1, cp.async core: tasks of 32 rows x 32
 //     columns, 4 output quadrants x 2 K halves): the shared maps with several
-//     right-hand sides (n-major columns of stride R are not bulk-copyable),
-//     HS_ZMMA2=0, and the fused shared-map launch (hs_set_fused bit 3);
+//     right-hand sides (n-major columns of stride R are not bulk-copyable) and
+//     HS_ZMMA2=0;
 //   * k_zgemm_dmma: the factorisation's batched block solves.
 // A task's A operand is a 32-row strip of the strip-major map layout (K x 32,
 // contiguous); B columns come from the vector through column descriptors
@@ -1209,9 +1210,13 @@ void launch_zmma(Ctx& c, const DevMma& m, const double2* A, const double2* srcA,
 
 // ---------------------------------------------------------------------------
 // k_zmma2_df: the whole R-RHS BSP apply as ONE persistent dataflow launch on
-// the k_zmma2 core.  The plan is build_fused_mma's: every 32-row x 32-RHS task
-// of the forward steps (phase 0), the residual step (1) and the backward steps
-// (2) in schedule order (a topological order), with per-(block, 32-RHS chunk)
+// the k_zmma2 core (k-major slabs of R right-hand sides, or NMAJ: the shared
+// class maps, one column per subdomain, KC = 64-row chunks where the faces
+// allow).  The plan is build_fused_mma's: every 32-row x 32-column task of
+// the forward steps (phase 0), the map-once residual step (1: only the rows
+// where r' can be nonzero, as the per-step path) with fill tasks (3: rp = w =
+// 0, z = zL on the other blocks; no contraction) and the backward steps (2)
+// in schedule order (a topological order), with per-(block, 32-RHS chunk)
 // completion counters it waits for / completes.  One CTA per SM: a producer
 // warp claims tickets, stages the task's column table (double-buffered),
 // streams the map chunks -- the first S before the task's dependencies are
@@ -1219,12 +1224,13 @@ void launch_zmma(Ctx& c, const DevMma& m, const double2* A, const double2* srcA,
 // streams the slab rows (after fence.proxy.async: generic-proxy stores of
 // other CTAs, async-proxy reads here).  Two groups of 4 consumer warps split
 // each chunk's k range; the tile goes through shared memory to a coalesced
-// epilogue; one thread then releases the task's completion counters.  A task
+// epilogue; warp 0 then releases the task's completion counters.  A task
 // waits only for lower tickets, held by running CTAs: deadlock-free with every
 // CTA resident (grid <= #SMs).  Phase arithmetic (k_zmma_fused's):
 //   0 forward   y = T (zL | r):  zL += y
 //   1 residual  y = T zL:        v = r - (zL - y); rp = w = v; z = zL + v
 //   2 backward  y = T (w | rp):  w += y; z += y
+//   3 fill      (no y):          rp = w = 0; z = zL
 constexpr int kDfStages = 4;
 struct DfCols {
   ZCols2<32> c;
@@ -1232,9 +1238,9 @@ struct DfCols {
   unsigned long long* tr;
 };
 
-template <int S>
-__global__ void __launch_bounds__(Z2<32, 2, 2, false, S, false, 2>::THREADS, 1) k_zmma2_df(FusedMmaArgs a) {
-  using F = Z2<32, 2, 2, false, S, false, 2>;
+template <int S, bool NMAJ, int KC>
+__global__ void __launch_bounds__(Z2<32, 2, 2, NMAJ, S, false, 2, KC>::THREADS, 1) k_zmma2_df(FusedMmaArgs a) {
+  using F = Z2<32, 2, 2, NMAJ, S, false, 2, KC>;
   extern __shared__ __align__(128) double2 sm[];
   __shared__ __align__(8) unsigned long long full[S], empty[S], dfull[2], dempty[2];
   __shared__ DfCols zcs[2];
@@ -1267,7 +1273,7 @@ __global__ void __launch_bounds__(Z2<32, 2, 2, false, S, false, 2>::THREADS, 1) 
       if (tr && lane == 0) tr[0] = z2_gtimer();
       const FusedMmaTask ft = a.tasks[t];
       const MmaTask tk = ft.task;
-      HS_DCHECK(tk.ncols >= 1 && tk.ncols <= 32 && tk.K % Z2KC == 0, DBG_INDEX);
+      HS_DCHECK(tk.ncols >= 1 && tk.ncols <= 32 && tk.K % KC == 0, DBG_INDEX);
       for (int j = lane; j < 32; j += 32) {
         if (j < tk.ncols) {
           const MmaCol c = a.cols[tk.col0 + j];
@@ -1292,25 +1298,53 @@ __global__ void __launch_bounds__(Z2<32, 2, 2, false, S, false, 2>::THREADS, 1) 
         zd.ks = ft.ks;
         zd.pair = ft.pair;
       }
+      if (ft.phase == 3) {
+        // fill task (map-once residual: rp = w = 0, z = zL on blocks the
+        // residual does not reach): no contraction, no ring; the consumers
+        // start it once its inputs are final
+        for (int q = lane; q < ft.ndep; q += 32) {
+          const FusedDep dp = a.deps[ft.dep0 + q];
+          const volatile int* pc = a.done + dp.block;
+          HS_WAIT(*pc < dp.count, 32, DBG_DEPWAIT);
+        }
+        __syncwarp();
+        __threadfence();
+        if (tr && lane == 0) tr[1] = tr[2] = z2_gtimer();
+        __syncwarp();
+        if (lane == 0) z2_arrive(&dfull[d]);
+        continue;
+      }
       __syncwarp();
       if (lane == 0) z2_arrive(&dfull[d]);  // release: the table is visible to the consumers
       const double2* srcA = ft.phase == 0 ? a.zL : (ft.phase == 1 ? a.zL : a.w);
       const double2* srcB = ft.phase == 0 ? a.r : (ft.phase == 1 ? a.zL : a.rp);
-      const int nkall = tk.K / Z2KC;
+      const int nkall = tk.K / KC;
       const int kc0 = ft.ks == 1 ? nkall / 2 : 0;
       const int nk = ft.ks == 0 ? nkall / 2 : nkall - kc0;
-      const unsigned bytes = (unsigned)(Z2KC * 32 * sizeof(double2)) + (unsigned)(Z2KC * tk.ncols * sizeof(double2));
+      // n-major: all 32 column rows (absent faces and padding columns read zeros)
+      const unsigned bytes = (unsigned)(KC * 32 * sizeof(double2)) +
+                             (unsigned)(KC * (NMAJ ? 32 : tk.ncols) * sizeof(double2));
       const double2* Ab = a.A + tk.a_off;
-      const double2* base = (zd.c.alt[0] ? srcB : srcA) + zd.c.in[0][0];
+      const double2* base = NMAJ ? nullptr : (zd.c.alt[0] ? srcB : srcA) + zd.c.in[0][0];
       auto issueA = [&](int st, int kc) {
         if (lane == 0)
-          z2_copy(sm + (size_t)st * F::STAGE, Ab + (long long)kc * Z2KC * 32, Z2KC * 32 * sizeof(double2), &full[st]);
+          z2_copy(sm + (size_t)st * F::STAGE, Ab + (long long)kc * KC * 32, KC * 32 * sizeof(double2), &full[st]);
       };
       auto issueB = [&](int st, int kc) {
-        double2* sb = sm + (size_t)st * F::STAGE + Z2KC * F::SA;
-        const double2* b0 = base + (long long)kc * Z2KC * R;
-        for (int r = lane; r < Z2KC; r += 32)
-          z2_copy(sb + r * F::SB, b0 + (long long)r * R, tk.ncols * sizeof(double2), &full[st]);
+        double2* sb = sm + (size_t)st * F::STAGE + KC * F::SA;
+        if (NMAJ) {
+          // column j (a subdomain): the chunk's KC positions of face q, one run
+          const int k0 = kc * KC, q = k0 / n, p0 = k0 - q * n;
+          const int j = lane;
+          const long long off = zd.c.in[j][q];
+          HS_DCHECK(off < 0 || off + (long long)(p0 + KC - 1) * R < a.LR, DBG_VEC);
+          const double2* src = off >= 0 ? (zd.c.alt[j] ? srcB : srcA) + off + (long long)p0 * R : a.zeros;
+          z2_copy(sb + j * F::SB, src, KC * sizeof(double2), &full[st]);
+        } else {
+          const double2* b0 = base + (long long)kc * KC * R;
+          for (int r = lane; r < KC; r += 32)
+            z2_copy(sb + r * F::SB, b0 + (long long)r * R, tk.ncols * sizeof(double2), &full[st]);
+        }
       };
       // the map chunks of the first stages stream while the dependencies settle
       const int pre = nk < S ? nk : S;
@@ -1347,8 +1381,12 @@ __global__ void __launch_bounds__(Z2<32, 2, 2, false, S, false, 2>::THREADS, 1) 
   const int kg = warp / F::NWQ, wq = warp % F::NWQ;
   const int wm = wq / F::WN, wn = wq % F::WN;
   const int gid = lane >> 2, tig = lane & 3;
-  constexpr int KH = Z2KC / 2;
+  constexpr int KH = KC / 2;
   constexpr int NT = 2 * 2 * 2;
+  // output element el of the 32 x 32 tile: k-major row-major (consecutive
+  // right-hand sides), n-major column-major (consecutive rows of a column)
+  auto el_rr = [](int el) { return NMAJ ? el % 32 : el / 32; };
+  auto el_j = [](int el) { return NMAJ ? el / 32 : el % 32; };
   long long g = 0;
   for (int it = 0;; ++it) {
     const int d = it & 1;
@@ -1357,7 +1395,42 @@ __global__ void __launch_bounds__(Z2<32, 2, 2, false, S, false, 2>::THREADS, 1) 
     if (zd.stop) break;
     const MmaTask tk = zd.c.tk;
     const int phase = zd.phase, ks = zd.ks;
-    const int nk = ks == 0 ? tk.K / Z2KC / 2 : (ks == 1 ? tk.K / Z2KC - tk.K / Z2KC / 2 : tk.K / Z2KC);
+    unsigned long long* tr = zd.tr;
+    if (phase == 3) {
+      // fill: counter k2 = block * nch + RHS chunk covers positions 0..n-1 of
+      // the block, right-hand sides 32 ch .. 32 ch + 31 (< R)
+      const int nch = (R + 31) / 32, cw = R < 32 ? R : 32;
+      const int per = n * cw;
+      for (int i = 0; i < zd.ninc; ++i) {
+        const int k2 = a.incs[zd.inc0 + i];
+        const int blk = k2 / nch, r0 = (k2 - blk * nch) * 32;
+        for (int e = tid; e < per; e += F::NWC * 32) {
+          const int p = e / cw, r = r0 + e - (e / cw) * cw;
+          if (r >= R) continue;
+          const long long t = ((long long)blk * n + p) * R + r;
+          HS_DCHECK(t < a.LR, DBG_VEC);
+          a.rp[t] = make_double2(0.0, 0.0);
+          a.w[t] = make_double2(0.0, 0.0);
+          a.z[t] = __ldcg(a.zL + t);
+        }
+      }
+      if (tr && tid == 0) tr[3] = z2_gtimer();
+      consumers_bar<F::NWC * 32>();  // every fill store issued
+      if (warp == 0) {
+        __threadfence();
+        for (int i = lane; i < zd.ninc; i += 32) atomicAdd(a.done + a.incs[zd.inc0 + i], 1);
+        if (tr && lane == 0) {
+          unsigned smid;
+          asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+          tr[4] = z2_gtimer();
+          tr[5] = ((unsigned long long)smid << 32) | ((unsigned long long)blockIdx.x << 8) | 3u;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) z2_arrive(&dempty[d]);
+      continue;
+    }
+    const int nk = ks == 0 ? tk.K / KC / 2 : (ks == 1 ? tk.K / KC - tk.K / KC / 2 : tk.K / KC);
     double cr[2][2][2], ci[2][2][2], p3[2][2][2];
 #pragma unroll
     for (int x = 0; x < 2; ++x)
@@ -1365,7 +1438,6 @@ __global__ void __launch_bounds__(Z2<32, 2, 2, false, S, false, 2>::THREADS, 1) 
       for (int y = 0; y < 2; ++y)
 #pragma unroll
         for (int c = 0; c < 2; ++c) cr[x][y][c] = ci[x][y][c] = p3[x][y][c] = 0.0;
-    unsigned long long* tr = zd.tr;
     long long toff[F::EPT];
     double2 u1[F::EPT], u2[F::EPT];
     for (int i = 0; i < nk; ++i, ++g) {
@@ -1378,7 +1450,7 @@ __global__ void __launch_bounds__(Z2<32, 2, 2, false, S, false, 2>::THREADS, 1) 
 #pragma unroll
         for (int u = 0; u < F::EPT; ++u) {
           const int el = u * F::NWC * 32 + tid;
-          const int rr = el / 32, j = el % 32;
+          const int rr = el_rr(el), j = el_j(el);
           const int row = tk.r0 + rr;
           long long t = -1;
           if (row >= tk.rlo && row < tk.rhi && j < tk.ncols) {
@@ -1395,7 +1467,7 @@ __global__ void __launch_bounds__(Z2<32, 2, 2, false, S, false, 2>::THREADS, 1) 
         }
       }
       const double2* sa = sm + (size_t)st * F::STAGE;
-      const double2* sb = sa + Z2KC * F::SA;
+      const double2* sb = sa + KC * F::SA;
 #pragma unroll
       for (int kk = 0; kk < KH; kk += 4) {
         const int k4 = kg * KH + kk;
@@ -1403,7 +1475,8 @@ __global__ void __launch_bounds__(Z2<32, 2, 2, false, S, false, 2>::THREADS, 1) 
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt) av[mt] = sa[(k4 + tig) * F::SA + (wm * 2 + mt) * 8 + gid];
 #pragma unroll
-        for (int nt = 0; nt < 2; ++nt) bv[nt] = sb[(k4 + tig) * F::SB + (wn * 2 + nt) * 8 + gid];
+        for (int nt = 0; nt < 2; ++nt)
+          bv[nt] = NMAJ ? sb[((wn * 2 + nt) * 8 + gid) * F::SB + k4 + tig] : sb[(k4 + tig) * F::SB + (wn * 2 + nt) * 8 + gid];
         double s_b[2];
 #pragma unroll
         for (int nt = 0; nt < 2; ++nt) s_b[nt] = bv[nt].x + bv[nt].y;
@@ -1468,7 +1541,7 @@ __global__ void __launch_bounds__(Z2<32, 2, 2, false, S, false, 2>::THREADS, 1) 
 #pragma unroll
       for (int u = 0; u < F::EPT; ++u) {
         const int el = u * F::NWC * 32 + tid;
-        mine[el] = ys[(el / 32) * F::YS + (el % 32)];
+        mine[el] = ys[el_rr(el) * F::YS + el_j(el)];
       }
       consumers_bar<F::NWC * 32>();
       if (tid == 0) {
@@ -1480,13 +1553,13 @@ __global__ void __launch_bounds__(Z2<32, 2, 2, false, S, false, 2>::THREADS, 1) 
       finish = s_old & 1;
       other = a.split_buf + ((size_t)zd.pair * 2 + (1 - ks)) * 1024;
     }
-    // coalesced epilogue: element el = row * 32 + column (consecutive RHS)
+    // coalesced epilogue (el_rr / el_j)
 #pragma unroll
     for (int u = 0; u < F::EPT; ++u) {
       const long long t = toff[u];
       if (t < 0 || !finish) continue;
       const int el = u * F::NWC * 32 + tid;
-      double2 y = ys[(el / 32) * F::YS + (el % 32)];
+      double2 y = ys[el_rr(el) * F::YS + el_j(el)];
       if (ks >= 0) {
         const double2 o = __ldcg(other + el);
         y = ks == 0 ? cadd(y, o) : cadd(o, y);
@@ -1504,10 +1577,15 @@ __global__ void __launch_bounds__(Z2<32, 2, 2, false, S, false, 2>::THREADS, 1) 
       }
     }
     consumers_bar<F::NWC * 32>();  // every epilogue store of the task issued
-    if (tid == 0 && finish) {
-      __threadfence();  // release the task's outputs, then count them done
-      for (int i = 0; i < zd.ninc; ++i) atomicAdd(a.done + a.incs[zd.inc0 + i], 1);
-      if (tr) {
+    if (warp == 0) {
+      // release the task's outputs, then count them done: one counter per lane
+      // (a shared-map task completes up to 32 blocks; one thread walking the
+      // list serialised a dependent load per counter, ~10 us per task)
+      if (finish) {
+        __threadfence();
+        for (int i = lane; i < zd.ninc; i += 32) atomicAdd(a.done + a.incs[zd.inc0 + i], 1);
+      }
+      if (tr && lane == 0) {
         unsigned smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         tr[4] = z2_gtimer();
@@ -1529,19 +1607,31 @@ cudaError_t launch_zmma_fused(Ctx& c, const DevFusedMma& f, FusedMmaArgs a) {
   // the k_zmma2 core for per-subdomain slabs (32-column tasks of consecutive
   // right-hand sides); HS_ZMMA2=0 keeps k_zmma_fused
   static const bool z2 = !(getenv("HS_ZMMA2") && atoi(getenv("HS_ZMMA2")) == 0);
-  if (z2 && !f.shared) {
-    using F = Z2<32, 2, 2, false, kDfStages, false, 2>;
-    constexpr size_t smem = F::SMEM + sizeof(double2) * 32 * F::YS + sizeof(double2) * F::NWQ * 8 * 32;
-    static const cudaError_t attr =
-        cudaFuncSetAttribute(k_zmma2_df<kDfStages>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (attr != cudaSuccess) return attr;
-    c.launches++;
+  // the shared class maps with one right-hand side: the n-major form (one
+  // column per subdomain), 64-row k chunks when the faces allow (half the
+  // bulk copies per k, two stages), else 32-row chunks in four stages
+  static const bool kc64 = !(getenv("HS_ZMMA2_KC64") && atoi(getenv("HS_ZMMA2_KC64")) == 0);
+  const bool nmaj = z2 && f.shared && f.R == 1 && c.zeros;
+  if (z2 && (!f.shared || nmaj)) {
     if (c.trace_on && c.trace && (size_t)f.ntasks <= c.trace_cap) {
       a.trace = c.trace;
       c.trace_rows = f.ntasks;
     }
-    k_zmma2_df<kDfStages><<<std::min(f.ntasks, c.num_sms), F::THREADS, smem, c.stream>>>(a);
-    return cudaGetLastError();
+    a.zeros = c.zeros;
+    a.LR = c.plan.L * (long long)f.R;
+    auto go = [&](auto kern, auto tag) -> cudaError_t {
+      using F = decltype(tag);
+      constexpr size_t smem = F::SMEM + sizeof(double2) * 32 * F::YS + sizeof(double2) * F::NWQ * 8 * 32;
+      const cudaError_t at = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (at != cudaSuccess) return at;
+      c.launches++;
+      kern<<<std::min(f.ntasks, c.num_sms), F::THREADS, smem, c.stream>>>(a);
+      return cudaGetLastError();
+    };
+    if (!nmaj) return go(k_zmma2_df<kDfStages, false, 32>, Z2<32, 2, 2, false, kDfStages, false, 2>());
+    if (kc64 && c.n % 64 == 0 && f.minK % 64 == 0)
+      return go(k_zmma2_df<2, true, 64>, Z2<32, 2, 2, true, 2, false, 2, 64>());
+    return go(k_zmma2_df<kDfStages, true, 32>, Z2<32, 2, 2, true, kDfStages, false, 2>());
   }
   // K split over a cluster: KS ranks each keep >= 2 K chunks (HS_ZMMA_FUSED_KS overrides)
   static const int ks_env = getenv("HS_ZMMA_FUSED_KS") ? atoi(getenv("HS_ZMMA_FUSED_KS")) : 0;

@@ -348,3 +348,41 @@ def test_kind_maps_bitwise(name, c, blocks):
     d = GpuInterfaceSystem(spec, part, maps="kinds", fused=False, sweep=SweepConfig(blocks=blocks))
     e = GpuInterfaceSystem(spec, part, fused=False, sweep=SweepConfig(blocks=blocks))
     assert np.array_equal(d.bsp_apply(g), e.bsp_apply(g))
+
+
+_DF_VARIANT_SCRIPT = """
+import numpy as np
+import sys
+sys.path[:0] = [".", "tests"]
+from conftest import cvec, product_problem, relerr
+from paper_2209_10886_b200.configs import CONFIGS
+from paper_2209_10886_b200.interface_system import GpuInterfaceSystem, SweepConfig
+for cfg, R, maps in ((2, 64, "subdomain"), (1, 40, "subdomain"), (2, 1, "shared"), (3, 1, "shared")):
+    c = CONFIGS[cfg]
+    spec, part = product_problem(c)
+    a = GpuInterfaceSystem(spec, part, fused=False, maps=maps, sweep=SweepConfig(blocks=c["blocks"]))
+    b = GpuInterfaceSystem(spec, part, fused=11 if maps == "shared" else 3, maps=maps,
+                           sweep=SweepConfig(blocks=c["blocks"]))
+    g = cvec(17, a.layout.size, None if R == 1 else R)
+    za, zb = a.bsp_apply(g), b.bsp_apply(g)
+    assert relerr(zb, za) < 1e-13, (cfg, R, maps, relerr(zb, za))
+    assert np.array_equal(b.bsp_apply(g), zb)
+    if maps == "shared":  # one right-hand side: GMRES runs the dataflow apply
+        rhs = a.rhs()
+        ra, rb = a.gmres(rhs, "bsp", tol=1e-8, maxit=300), b.gmres(rhs, "bsp", tol=1e-8, maxit=300)
+        assert ra.iterations == rb.iterations and relerr(rb.solution, ra.solution) < 1e-10
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("env", [{"HS_ZMMA2_SPLIT": "1"}, {"HS_ZMMA2_DF_MO": "0"},
+                                 {"HS_ZMMA2_SPLIT": "1", "HS_ZMMA2_KC64": "0"}])
+def test_dmma_dataflow_variants(env):
+    """k_zmma2_df variants against the per-step contraction: split-K pairs
+    (HS_ZMMA2_SPLIT=1, both halves summed in half order by the later arrival),
+    the full residual step instead of the map-once residual + fill tasks
+    (HS_ZMMA2_DF_MO=0), the n-major shared-map form on 32-row chunks
+    (HS_ZMMA2_KC64=0); apply to rounding, bitwise reproducible, GMRES
+    iterations equal."""
+    out = _run_variant_script(_DF_VARIANT_SCRIPT, env)
+    assert out.endswith("ok")

@@ -1,7 +1,7 @@
 """Per-task timeline of one dataflow DMMA apply (k_zmma2_df, hs_set_trace):
 per phase the mean wait for inputs, slab latency, contraction and
 epilogue+signal, the span, and how many CTAs contract at a time.
-    python tools/zmma_df_trace.py CFG R"""
+    python tools/zmma_df_trace.py CFG R [subdomain|shared]"""
 import ctypes as C
 import json
 import sys
@@ -15,9 +15,11 @@ from paper_2209_10886_b200.configs import CONFIGS  # noqa: E402
 from paper_2209_10886_b200.interface_system import GpuInterfaceSystem, SweepConfig  # noqa: E402
 
 cfg, R = int(sys.argv[1]), int(sys.argv[2])
+maps = sys.argv[3] if len(sys.argv) > 3 else "subdomain"
 c = CONFIGS[cfg]
 spec, part = product_problem(c)
-s = GpuInterfaceSystem(spec, part, fused=3, sweep=SweepConfig(blocks=c["blocks"]))
+s = GpuInterfaceSystem(spec, part, fused=11 if maps == "shared" else 3, maps=maps,
+                       sweep=SweepConfig(blocks=c["blocks"]))
 X = torch.from_numpy(cvec(5, s.layout.size, R)).cuda()
 for _ in range(3):
     s.bsp_apply(X)
@@ -34,7 +36,7 @@ tr = np.frombuffer(buf, dtype=np.uint64).reshape(-1, 6).astype(np.int64)
 t0 = tr[:, 0].min()
 claim, met, first, comp, sig = [(tr[:, i] - t0) / 1e3 for i in range(5)]
 phase = tr[:, 5] & 0xFF
-out = {"config": cfg, "R": R, "tasks": int(len(tr)), "span_us": round(float(sig.max()), 1), "phases": {}}
+out = {"config": cfg, "R": R, "maps": maps, "tasks": int(len(tr)), "span_us": round(float(sig.max()), 1), "phases": {}}
 for p in sorted(set(phase.tolist())):
     m = phase == p
     out["phases"][int(p)] = {"tasks": int(m.sum()), "wait_inputs": round(float(np.mean(met[m] - claim[m])), 2),
