@@ -1273,7 +1273,8 @@ __global__ void __launch_bounds__(Z2<32, 2, 2, NMAJ, S, false, 2, KC>::THREADS, 
       if (tr && lane == 0) tr[0] = z2_gtimer();
       const FusedMmaTask ft = a.tasks[t];
       const MmaTask tk = ft.task;
-      HS_DCHECK(tk.ncols >= 1 && tk.ncols <= 32 && tk.K % KC == 0, DBG_INDEX);
+      // fill tasks (phase 3) carry no columns and no contraction
+      HS_DCHECK(ft.phase == 3 ? tk.ncols == 0 && tk.K == 0 : tk.ncols >= 1 && tk.ncols <= 32 && tk.K % KC == 0, DBG_INDEX);
       for (int j = lane; j < 32; j += 32) {
         if (j < tk.ncols) {
           const MmaCol c = a.cols[tk.col0 + j];
