@@ -4,6 +4,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <complex>
 #include <cstdlib>
@@ -2015,8 +2016,9 @@ int hs_factor(hs_ctx* c) {
   c->ws["__X"].cap = (size_t)xstride * ncls;
   double2 *Rp, *Cp;
   const long long pstride = 32LL * n + 32 * 32;  // row/column panel + the panel inverse
-  CK(tmp.alloc(&Rp, (size_t)pstride * ncls * sizeof(double2)));
-  CK(tmp.alloc(&Cp, (size_t)pstride * ncls * sizeof(double2)));
+  // two slices each: the twisted elimination runs two chains at once
+  CK(tmp.alloc(&Rp, (size_t)pstride * ncls * 2 * sizeof(double2)));
+  CK(tmp.alloc(&Cp, (size_t)pstride * ncls * 2 * sizeof(double2)));
   int* dbad;
   CK(tmp.alloc(&dbad, sizeof(int)));
   CK(cudaMemsetAsync(dbad, 0, sizeof(int), c->stream));
@@ -2026,7 +2028,7 @@ int hs_factor(hs_ctx* c) {
   double2 *Y, *Bk, *G;
   const long long ystride = nn * R, bstride = (long long)n * R, gstride = 4LL * n * R;
   CK(tmp.alloc(&Y, (size_t)ystride * ncls * sizeof(double2)));
-  CK(tmp.alloc(&Bk, (size_t)bstride * ncls * sizeof(double2)));
+  CK(tmp.alloc(&Bk, (size_t)bstride * ncls * 2 * sizeof(double2)));
   CK(tmp.alloc(&G, (size_t)gstride * ncls * sizeof(double2)));
   std::vector<ExtraRHS> extras(ncls);
   for (int k = 0; k < ncls; ++k) {
@@ -2034,8 +2036,12 @@ int hs_factor(hs_ctx* c) {
     dirichlet_boundary_extras(c, c->classes[k], ex);
     if (upload_extras(c, ex, extras[k], tmp.p)) return -1;
   }
+  static const bool timing = getenv("HS_FACTOR_TIMING") && atoi(getenv("HS_FACTOR_TIMING")) != 0;
+  auto now = [] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  const double t_pre = now();
   CK(factor_and_solve_boundary(*c, X, xstride, dmasks, ncls, Rp, Cp, pstride, dbad, R, R, extras.data(), Y, ystride,
                                Bk, bstride, G, gstride));
+  const double t_fac = now();
   // T4 = -(s/d) I - (2 tau / (h^3 d^2)) G
   const std::complex<double> tau(c->tau_re, c->tau_im);
   const double h = c->h;
@@ -2089,17 +2095,16 @@ int hs_factor(hs_ctx* c) {
   } else if (n % 32 != 0) {
     return fail(c, 1, "shared-map mode needs cells_per_side divisible by 32");
   }
+  // finite check of the class maps, on the device (flag bit 1)
+  for (int k = 0; k < ncls; ++k) launch_finite_check(*c, c->classes[k].T4, 16 * nn, dbad);
   CK(cudaGetLastError());
   int bad = 0;
   CK(cudaMemcpyAsync(&bad, dbad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
-  // finite check of the class maps
-  for (int k = 0; k < ncls; ++k) {
-    std::vector<double2> h4((size_t)16 * nn);
-    CK(cudaMemcpy(h4.data(), c->classes[k].T4, h4.size() * sizeof(double2), cudaMemcpyDeviceToHost));
-    for (auto& v : h4)
-      if (!std::isfinite(v.x) || !std::isfinite(v.y)) { bad = 2; break; }
-  }
+  const double t_maps = now();
+  if (timing)
+    fprintf(stderr, "[hs_factor] host: elimination + boundary solves %.3f ms, maps + finite check %.3f ms\n", t_fac - t_pre,
+            t_maps - t_fac);
   for (auto& oc : c->classes) oc.factored = true;
   if (bad) return fail(c, -3, "singular or non-finite subdomain factorisation");
   c->factored = true;

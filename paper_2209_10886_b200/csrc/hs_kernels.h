@@ -40,8 +40,7 @@ cudaError_t launch_zmma_fused(Ctx& c, const DevFusedMma& f, FusedMmaArgs a);
 void launch_pack_strips(Ctx& c, const double2* T4, double2* out, int rows, int cols);
 
 // ---- factorisation (hs_schur.cu)
-cudaError_t factor_blocks(Ctx& c, double2* X, long long xstride, const uint8_t* dmasks, int ncls,
-                          double2* Rp, double2* Cp, long long pstride, int* dbad);
+// Rp / Cp / Bk: two slices each (2 * ncls), one per elimination chain
 cudaError_t factor_and_solve_boundary(Ctx& c, double2* X, long long xstride, const uint8_t* dmasks, int ncls,
                                       double2* Rp, double2* Cp, long long pstride, int* dbad, int R, int nunit,
                                       const ExtraRHS* extras, double2* Y, long long ystride, double2* Bk,
@@ -58,6 +57,7 @@ void zgemm(cudaStream_t st, int M, int N, int K, double2 alpha, const double2* A
            long long sa, const double2* B, int ldb, long long sb, double2 beta, double2* C, int ldc,
            long long sc, int batch);
 void launch_make_T4(Ctx& c, double2* T4, const double2* G, int R, double2 a, double2 b);
+void launch_finite_check(Ctx& c, const double2* v, long long count, int* flag);
 cudaError_t solve_fields(Ctx& c, const double2* X, const uint8_t* dmask, int R, const double2* g,
                          const int* face_off, double2 coeff, const ExtraRHS& extras, double2* Y, double2* Bk);
 void launch_scatter_field(Ctx& c, double2* field, int nx_total, const double2* Y, int R, const int* col_ab,
