@@ -188,3 +188,24 @@ def test_gmres_not_converged_is_data(fused):
     assert not res.converged and res.iterations == 7
     np.testing.assert_allclose(res.history[:8], G["gm_hist"][:8], rtol=1e-8, atol=1e-14)
     assert relerr(s.apply_interface_operator(res.solution), G["b"]) == pytest.approx(res.history[-1], rel=1e-6)
+
+
+@pytest.mark.parametrize("n", [4, 5, 7, 9, 33])
+def test_schur_maps_odd_sizes(n):
+    """The twisted elimination (rows above n/2 downwards, below upwards, row n/2
+    coupling them) at sizes where the halves are empty, unequal or not a panel
+    multiple: maps vs the accurate oracle."""
+    from oracle.schur import schur_maps_for
+    c = small_case(2, 2, n)
+    prob, lat = oracle_problem(c)
+    spec, part = product_problem(c)
+    s = GpuInterfaceSystem(spec, part)
+    ref = schur_maps_for(prob, lat, list(lat.subs))
+    for sub in lat.subs:
+        T = s.schur_map(sub)
+        assert T.shape == ref[sub].shape
+        assert relerr(T, ref[sub]) < 1e-11, (n, sub, relerr(T, ref[sub]))
+    g = torch.from_numpy(cvec(5, s.layout.size)).cuda()
+    from oracle import Interface
+    itf = Interface(prob, lat, backend="schur")
+    assert relerr(s.apply_interface_operator(g).cpu().numpy(), itf.apply_A(cvec(5, s.layout.size))) < 1e-11
