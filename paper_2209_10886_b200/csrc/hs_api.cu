@@ -2421,10 +2421,19 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
   const bool auto1 = c->gmres_mode == 0 && R == 1 && maxit <= 1500;
   const bool cgs2 = c->gmres_mode == 3 || (auto1 && c->plan.nranks > 1 && bands_cgs2);
   const bool cgsg = c->gmres_mode == 4 || (auto1 && !(c->plan.nranks > 1 && bands_cgs2));
-  if ((cgs2 || cgsg) && R != 1) return fail(c, 1, "CGS2 Arnoldi supports one right-hand side");
-  if (cgsg && maxit > 1500) return fail(c, 1, "the Gram-corrected CGS2 Arnoldi supports maxit <= 1500");
-  const bool dist = c->plan.nranks > 1 || c->gmres_mode == 1 || cgs2 || cgsg;
   const long long LR = LRof(c, R);
+  // R right-hand sides on one rank: the same one-reduction Arnoldi, column by
+  // column (auto mode, or forced "cgs2g"); HS_ARNOLDI_R=mgs keeps the
+  // cooperative MGS kernel
+  static const bool r_mgs = getenv("HS_ARNOLDI_R") && std::string(getenv("HS_ARNOLDI_R")) == "mgs";
+  const bool cgsgR = R > 1 && c->plan.nranks == 1 && LR > 0 && ((c->gmres_mode == 0 && !r_mgs) || c->gmres_mode == 4) &&
+                     gmres_cgsgR_ok(*c, LR, R, maxit);
+  if (cgs2 && R != 1) return fail(c, 1, "CGS2 Arnoldi supports one right-hand side");
+  if (cgsg && R != 1 && !cgsgR)
+    return fail(c, 1, "the Gram-corrected CGS2 Arnoldi with several right-hand sides needs one rank, R <= 128 and maxit "
+                      "small enough for the Gram matrices (2 GB)");
+  if (cgsg && R == 1 && maxit > 1500) return fail(c, 1, "the Gram-corrected CGS2 Arnoldi supports maxit <= 1500");
+  const bool dist = !cgsgR && (c->plan.nranks > 1 || c->gmres_mode == 1 || cgs2 || cgsg);
   if (LR == 0) {  // empty interface system (1 x 1 lattice): 0 iterations
     for (int r = 0; r < R; ++r) {
       if (iters) iters[r] = 0;
@@ -2439,6 +2448,7 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
   if (int e = dev_out(c, x, LR, mem, "gout", &dx)) return e;
   int chunk = 0;
   int grid = dist ? 2 * c->num_sms : gmres_coop_grid(*c, LR, R, &chunk);
+  if (grid <= 0 && cgsgR) grid = 1;  // the cooperative kernel is not used
   if (grid <= 0) return fail(c, 3, "interface vector too large for the cooperative Arnoldi kernel");
   double2 *part2 = nullptr, *mgsout = nullptr, *part3 = nullptr, *hbuf = nullptr, *gram = nullptr;
   if (dist) {
@@ -2455,6 +2465,12 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
     if (cgsg && (ws_get(c, "part3", (size_t)grid * (2 * maxit + 3), &part3) ||
                  ws_get(c, "hbuf", (size_t)3 * maxit + 6, &hbuf) ||
                  ws_get(c, "gram", (size_t)(maxit + 1) * (maxit + 1), &gram)))
+      return -1;
+  }
+  if (cgsgR) {
+    const size_t g2 = 2 * (size_t)c->num_sms;
+    if (ws_get(c, "part3", g2 * (2 * maxit + 3) * R, &part3) || ws_get(c, "hbuf", ((size_t)3 * maxit + 6) * R, &hbuf) ||
+        ws_get(c, "gram", (size_t)R * (maxit + 1) * (maxit + 1), &gram))
       return -1;
   }
   GmresDev G;
@@ -2523,7 +2539,10 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
         if (int e_ = do_apply(c, HS_APPLY_IMS, zin, w, R)) return e_;
       }
     }
-    if (cgsg) {
+    if (cgsgR) {
+      CK(gmres_arnoldi_cgsgR(*c, G, k, part3, hbuf, gram, maxit + 1));
+      CK(gmres_givens(*c, G, k));
+    } else if (cgsg) {
       // one rank owns every block, in order: identity element mapping
       CK(gmres_arnoldi_cgsg(*c, G, k, c->plan.nranks == 1 ? nullptr : c->d_owned, c->n_owned, part3, hbuf, gram,
                             maxit + 1, c->nccl));  // includes the Givens update

@@ -926,6 +926,241 @@ cudaError_t gmres_arnoldi_cgsg(Ctx& c, GmresDev& G, int k, const int* blocks, in
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------
+// The same Gram-corrected one-reduction CGS2 for R right-hand sides on one
+// rank (element e = position * R + r; every column r runs its own Arnoldi
+// process with its own Gram matrix Gm[r]).  It replaces the cooperative k_mgs
+// (one grid barrier, two block trees and a 148 x R partial read per CTA *per
+// basis vector*: ~12 us per j at cfg4, where the vector itself streams in 2 us)
+// by four launches per iteration: all inner products in one pass over V,
+// one reduction over the CTAs, the coefficients per right-hand side, one
+// update pass.  k_givens follows as after k_mgs.
+//   part: [grid][2 (k+1) + 1][R]   red: [2 (k+1) + 1][R]   cbuf: [k + 2][R]
+template <int NC>
+__global__ void __launch_bounds__(256) k_cgsgR_dots(GmresDev G, int k, long long npos, long long per, double2* part,
+                                                    int cnt) {
+  extern __shared__ double2 sw[];  // this CTA's positions of w and v_k, all R columns
+  const int R = G.R;
+  const long long LR = G.LR;
+  const double2* w = G.V + (long long)(k + 1) * LR;
+  const double2* vk = G.V + (long long)k * LR;
+  const long long p0 = blockIdx.x * per, p1 = min(npos, p0 + per);
+  const int np = (int)max(0ll, p1 - p0);
+  const int ne = np * R;
+  double2* sws = sw;
+  double2* svk = sw + per * R;
+  for (int i = threadIdx.x; i < ne; i += blockDim.x) {
+    sws[i] = w[p0 * R + i];
+    svk[i] = vk[p0 * R + i];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int kp1 = k + 1;
+  double2* P = part + (long long)blockIdx.x * cnt * R;
+  // a warp per basis vector; lane l owns columns l, l + 32, ...: no cross-lane
+  // reduction, positions summed in order (deterministic)
+  for (int j = warp; j <= kp1; j += nw) {  // j = k + 1: ||w||^2
+    double2 a[NC], b[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) a[c] = b[c] = make_double2(0, 0);
+    if (j < kp1) {
+      const double2* v = G.V + (long long)j * LR + p0 * R;
+      // PB positions' loads issued before their products: PB * NC 16-byte loads
+      // in flight per lane (the one-position loop ran at DRAM latency per step)
+      constexpr int PB = 8;
+      int rr[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) rr[c] = lane + 32 * c < R ? lane + 32 * c : -1;
+      for (int pq = 0; pq < np; pq += PB) {
+        double2 x[PB][NC];
+#pragma unroll
+        for (int u = 0; u < PB; ++u)
+#pragma unroll
+          for (int c = 0; c < NC; ++c)
+            x[u][c] = (pq + u < np && rr[c] >= 0) ? __ldg(v + (pq + u) * R + rr[c]) : make_double2(0, 0);
+#pragma unroll
+        for (int u = 0; u < PB; ++u) {
+          if (pq + u >= np) break;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            if (rr[c] < 0) continue;
+            cfma_conj(a[c], x[u][c], sws[(pq + u) * R + rr[c]]);
+            cfma_conj(b[c], x[u][c], svk[(pq + u) * R + rr[c]]);
+          }
+        }
+      }
+    } else {
+      for (int p = 0; p < np; ++p) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          const int r = lane + 32 * c;
+          if (r < R) {
+            const double2 x = sws[p * R + r];
+            a[c].x += x.x * x.x + x.y * x.y;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int r = lane + 32 * c;
+      if (r >= R) continue;
+      if (j < kp1) {
+        P[(long long)j * R + r] = a[c];
+        P[(long long)(kp1 + j) * R + r] = b[c];
+      } else {
+        P[(long long)2 * kp1 * R + r] = a[c];
+      }
+    }
+  }
+}
+
+// out[e] = sum over CTAs g of part[g][e], e < total: 32 consecutive entries per
+// block (coalesced), warp w sums CTAs w, w + 8, ... with four loads in flight,
+// the eight warp sums added in warp order (a fixed order: deterministic)
+__global__ void __launch_bounds__(256) k_cgsgR_reduce(const double2* __restrict__ part, int ngrid, long long total,
+                                                      double2* out) {
+  __shared__ double2 s[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long e = (long long)blockIdx.x * 32 + lane;
+  double2 a0 = make_double2(0, 0), a1 = a0, a2 = a0, a3 = a0;
+  if (e < total) {
+    int g = warp;
+    for (; g + 24 < ngrid; g += 32) {
+      a0 = cadd(a0, __ldcg(part + (long long)g * total + e));
+      a1 = cadd(a1, __ldcg(part + (long long)(g + 8) * total + e));
+      a2 = cadd(a2, __ldcg(part + (long long)(g + 16) * total + e));
+      a3 = cadd(a3, __ldcg(part + (long long)(g + 24) * total + e));
+    }
+    for (; g < ngrid; g += 8) a0 = cadd(a0, __ldcg(part + (long long)g * total + e));
+  }
+  s[warp][lane] = cadd(cadd(a0, a1), cadd(a2, a3));
+  __syncthreads();
+  if (warp == 0 && e < total) {
+    double2 t = s[0][lane];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) t = cadd(t, s[q][lane]);
+    out[e] = t;
+  }
+}
+
+// One CTA per right-hand side r: its new Gram row, c = 2 h - G h, the new norm
+// by expansion, H[:, k] and ||w|| (k_cgsg_coef's arithmetic; the Givens update
+// is k_givens').  Gm: R matrices of ldg x ldg, row-major, Hermitian.
+__global__ void __launch_bounds__(256) k_cgsgR_coef(GmresDev G, int k, const double2* red, double2* Gm, int ldg,
+                                                    double2* cbuf) {
+  extern __shared__ double2 sh[];  // h, c, Gh, Gc (k+1 each), 2 (k+1) terms
+  const int R = G.R, r = blockIdx.x;
+  const int kp1 = k + 1;
+  double2* h = sh;
+  double2* cc = sh + kp1;
+  double2* gh = sh + 2 * kp1;
+  double2* gc = sh + 3 * kp1;
+  double* t1 = (double*)(sh + 4 * kp1);
+  double* t2 = t1 + kp1;
+  double2* Gr = Gm + (long long)r * ldg * ldg;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int j = threadIdx.x; j < kp1; j += blockDim.x) {
+    h[j] = red[(long long)j * R + r];
+    const double2 g = red[(long long)(kp1 + j) * R + r];   // v_j^H v_k
+    Gr[(long long)j * ldg + k] = g;                        // G[j][k]
+    Gr[(long long)k * ldg + j] = make_double2(g.x, -g.y);  // G[k][j] = conj
+  }
+  __syncthreads();
+  auto matvec = [&](const double2* x, double2* y) {
+    for (int i = warp; i < kp1; i += nw) {
+      double2 acc = make_double2(0, 0);
+      const double2* row = Gr + (long long)i * ldg;
+      for (int j = lane; j < kp1; j += 32) acc = cadd(acc, cmul(row[j], x[j]));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+      }
+      if (lane == 0) y[i] = acc;
+    }
+  };
+  matvec(h, gh);
+  __syncthreads();
+  for (int i = threadIdx.x; i < kp1; i += blockDim.x) cc[i] = csub(make_double2(2.0 * h[i].x, 2.0 * h[i].y), gh[i]);
+  __syncthreads();
+  matvec(cc, gc);
+  __syncthreads();
+  double2* Hk = G.H + hoff(k, R);
+  for (int i = threadIdx.x; i < kp1; i += blockDim.x) {  // Re(c^H h), c^H G c termwise
+    t1[i] = cc[i].x * h[i].x + cc[i].y * h[i].y;
+    t2[i] = cc[i].x * gc[i].x + cc[i].y * gc[i].y;
+    cbuf[(long long)i * R + r] = cc[i];
+    Hk[(long long)i * R + r] = cc[i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s1 = 0.0, s2 = 0.0;
+    for (int i = 0; i < kp1; ++i) s1 += t1[i], s2 += t2[i];  // index order: deterministic
+    const double w2 = red[(long long)2 * kp1 * R + r].x;
+    const double q = w2 - 2.0 * s1 + s2;
+    const double hn = sqrt(q > 0 ? q : 0.0);
+    G.wnorm0[r] = sqrt(w2);
+    cbuf[(long long)kp1 * R + r] = make_double2(hn, 0);
+    Hk[(long long)kp1 * R + r] = make_double2(hn, 0);
+  }
+}
+
+// w'' = (w - V c) / ||w''||, column by column
+__global__ void __launch_bounds__(256) k_cgsgR_update(GmresDev G, int k, const double2* __restrict__ cbuf) {
+  const int R = G.R;
+  const long long LR = G.LR;
+  double2* w = G.V + (long long)(k + 1) * LR;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < LR; e += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(e % R);
+    double2 x = w[e];
+#pragma unroll 4
+    for (int j = 0; j <= k; ++j) x = csub(x, cmul(cbuf[(long long)j * R + r], G.V[(long long)j * LR + e]));
+    const double hn = cbuf[(long long)(k + 1) * R + r].x;
+    w[e] = hn > 0 ? make_double2(x.x / hn, x.y / hn) : make_double2(0, 0);
+  }
+}
+
+static int cgsgR_grid(Ctx& c) { return 2 * c.num_sms; }
+
+bool gmres_cgsgR_ok(Ctx& c, long long LR, int R, int maxit) {
+  if (R < 2 || R > 128 || LR % R) return false;
+  const long long npos = LR / R, per = (npos + cgsgR_grid(c) - 1) / cgsgR_grid(c);
+  if ((size_t)2 * per * R * sizeof(double2) > 200 * 1024) return false;
+  if ((size_t)(5 * (maxit + 1) + 2) * sizeof(double2) > 200 * 1024) return false;
+  return (double)R * (maxit + 1) * (maxit + 1) * sizeof(double2) <= 2e9;  // the Gram matrices
+}
+
+cudaError_t gmres_arnoldi_cgsgR(Ctx& c, GmresDev& G, int k, double2* part, double2* red, double2* Gm, int ldg) {
+  const int grid = cgsgR_grid(c), R = G.R;
+  const int kp1 = k + 1, cnt = 2 * kp1 + 1;
+  const long long npos = G.LR / R, per = (npos + grid - 1) / grid;
+  const size_t smem = (size_t)2 * per * R * sizeof(double2);
+  static cudaError_t attr = [] {
+    cudaError_t e = cudaFuncSetAttribute(k_cgsgR_dots<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_cgsgR_dots<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_cgsgR_dots<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_cgsgR_dots<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(k_cgsgR_coef, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    return e;
+  }();
+  if (attr != cudaSuccess) return attr;
+  c.launches += 4;
+  switch ((R + 31) / 32) {
+    case 1: k_cgsgR_dots<1><<<grid, 256, smem, c.stream>>>(G, k, npos, per, part, cnt); break;
+    case 2: k_cgsgR_dots<2><<<grid, 256, smem, c.stream>>>(G, k, npos, per, part, cnt); break;
+    case 3: k_cgsgR_dots<3><<<grid, 256, smem, c.stream>>>(G, k, npos, per, part, cnt); break;
+    default: k_cgsgR_dots<4><<<grid, 256, smem, c.stream>>>(G, k, npos, per, part, cnt); break;
+  }
+  const long long total = (long long)cnt * R;
+  k_cgsgR_reduce<<<(unsigned)((total + 31) / 32), 256, 0, c.stream>>>(part, grid, total, red);
+  double2* cbuf = red + total;  // c (k+1 rows of R) + ||w''||
+  k_cgsgR_coef<<<R, 256, (size_t)(5 * kp1 + 2) * sizeof(double2), c.stream>>>(G, k, red, Gm, ldg, cbuf);
+  const int ug = (int)std::min<long long>((long long)grid * 4, std::max<long long>(1, (G.LR + 255) / 256));
+  k_cgsgR_update<<<ug, 256, 0, c.stream>>>(G, k, cbuf);
+  return cudaGetLastError();
+}
+
 cudaError_t gmres_arnoldi_cgs2(Ctx& c, GmresDev& G, int k, const int* blocks, int nb, double2* part,
                                double2* hbuf, void* nccl_comm) {
   const int grid = 2 * c.num_sms;

@@ -442,9 +442,10 @@ class GpuInterfaceSystem:
     def gmres(self, b, kind: str | None = None, tol: float = 1e-6, maxit: int = 200,
               arnoldi: str = "auto") -> GmresResult:
         """arnoldi = "auto" (one right-hand side: "cgs2g", on one GPU and
-        across row bands; several: the MGS kernels -- a cluster kernel for
-        small vectors, grid-wide otherwise, host-driven MGS with a reduction
-        per inner product across bands), "mgs" (the MGS kernels for one
+        across row bands; several, up to 128, on one GPU: "cgs2g" column by
+        column; otherwise the MGS kernels -- a cluster kernel for small
+        vectors, grid-wide otherwise, host-driven MGS with a reduction per
+        inner product across bands), "mgs" (the MGS kernels for one
         right-hand side too: the SPEC's literal Arnoldi; k_mgs1c / k_mgs1 with
         M steps per grid barrier), "hostloop" (force the sharded MGS on one
         GPU or across bands), "grid" (force the generic grid-wide cooperative

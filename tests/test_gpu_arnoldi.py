@@ -169,3 +169,40 @@ def test_auto_beyond_1500_iterations_uses_mgs():
     assert r.iterations == int(G["gm_iters"]) and r.converged
     with pytest.raises(ValueError):
         s.gmres(G["b"], "bsp", tol=1e-6, maxit=2000, arnoldi="cgs2g")
+
+
+def _plane_waves(s, R):
+    return s.rhs(directions=[(float(np.cos(2 * np.pi * q / R)), float(np.sin(2 * np.pi * q / R))) for q in range(R)])
+
+
+@pytest.mark.parametrize("R", [3, 40, 64, 100])
+def test_multi_rhs_one_reduction_arnoldi(R):
+    """R right-hand sides on one rank: the column-wise one-reduction CGS2
+    (k_cgsgR_*: auto and "cgs2g") against the cooperative MGS kernels ("grid":
+    k_mgs + k_givens): iterations equal column by column, histories within
+    1e-10, solutions within 1e-10; a column equals its single-RHS solve."""
+    s = system(1)
+    b = _plane_waves(s, R)
+    auto = s.gmres(b, "bsp", tol=1e-6, maxit=200)
+    forced = s.gmres(b, "bsp", tol=1e-6, maxit=200, arnoldi="cgs2g")
+    mgs = s.gmres(b, "bsp", tol=1e-6, maxit=200, arnoldi="grid")
+    assert all(auto.converged) and list(auto.iterations) == list(mgs.iterations)
+    assert np.array_equal(np.asarray(auto.solution), np.asarray(forced.solution))  # the same kernels
+    for r in range(R):
+        np.testing.assert_allclose(auto.history[r], mgs.history[r], rtol=1e-10)
+    assert relerr(auto.solution, mgs.solution) < 1e-10
+    q = R // 2
+    one = s.gmres(np.ascontiguousarray(b[:, q]), "bsp", tol=1e-6, maxit=200)
+    assert one.iterations == auto.iterations[q]
+    assert relerr(np.asarray(auto.solution)[:, q], one.solution) < 1e-10
+
+
+def test_multi_rhs_beyond_128_columns_uses_mgs():
+    """More than 128 columns: auto keeps the cooperative MGS kernel; the forced
+    one-reduction mode refuses with ValueError."""
+    s = system(1)
+    b = _plane_waves(s, 130)
+    r = s.gmres(b, "bsp", tol=1e-6, maxit=200)
+    assert all(r.converged)
+    with pytest.raises(ValueError):
+        s.gmres(b, "bsp", tol=1e-6, maxit=200, arnoldi="cgs2g")
