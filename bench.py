@@ -501,7 +501,9 @@ def main():
         ach = (m["kflops"] / (m["kms"] * 1e-3)) / 1e12 if m["kms"] > 0 else None
         roof = {"bound": "fp64", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                 "frac": (ach / peak) if ach else None, "traffic": None,
-                "kernel": "k_zmma (FP64 DMMA complex contraction, per-subdomain maps x R RHS)",
+                "kernel": "k_zmma2_df (the whole R-RHS BSP apply as one persistent dataflow launch: FP64 DMMA m8n8k4, 3M "
+                          "complex product, map chunks staged by bulk copies into an mbarrier ring; flops counted "
+                          "as 8 per complex multiply-add)",
                 "peak_source": "measured DMMA m8n8k4 peak, profiles/fp64_peak_b200.json",
                 "launches": m["kl"], "kernel_ms_share_of_step": share,
                 "algorithmic_flops_per_apply": m["kflops"] / max(args.steps, 1)}
@@ -563,7 +565,8 @@ def main():
         fl = ms_sh["kflops"] / (ms_sh["kms"] * 1e-3) / 1e12 if ms_sh["kms"] > 0 else None
         variants["shared_maps"] = {
             "what": "generic subdomains share one 4n x 4n map (discretization.py:224-229); each sweep step is "
-                    "one FP64 DMMA contraction (k_zmma) with the map L2-resident",
+                    "one FP64 DMMA contraction (k_zmma2: bulk-copy staged, 3M product, flops counted as 8 per "
+                    "complex multiply-add) with the map L2-resident",
             "applies_per_s": 1e3 / ms_sh["ms_per"], "ms_per_apply": ms_sh["ms_per"],
             "roofline": {"bound": "fp64", "achieved": fl, "peak": fp64_peak(), "unit": "TFLOP/s",
                          "frac": fl / fp64_peak() if fl else None},
