@@ -374,7 +374,16 @@ int build_fused_mma(Ctx* c, int R, bool shared) {
   free_fused_mma(c);
   DevFusedMma& f = c->fused_mma;
   const int n = c->n;
-  const int nch = (R + 31) / 32;
+  // fill tasks and split-K pairs are k_zmma2_df's (launch_zmma_fused): not with
+  // HS_ZMMA2=0 or the shared maps with R > 1 (k_zmma_fused)
+  static const bool z2 = !(getenv("HS_ZMMA2") && atoi(getenv("HS_ZMMA2")) == 0);
+  const bool df = z2 && (!shared || R == 1);
+  // task / counter width in right-hand sides: 16 for the per-subdomain slabs
+  // (k_zmma2_df<.., 16>: the apply is bound by its dependency chain, so twice
+  // the tasks at half the contraction each; HS_ZMMA2_DF_BN=32: 32-column tasks)
+  static const int bn_env = getenv("HS_ZMMA2_DF_BN") ? atoi(getenv("HS_ZMMA2_DF_BN")) : 16;
+  const int cwd = (df && !shared && R > 16 && bn_env == 16) ? 16 : 32;
+  const int nch = (R + cwd - 1) / cwd;
   const int ncnt = c->plan.npairs * nch;
   std::vector<FusedMmaTask> ftasks;
   std::vector<MmaCol> cols;
@@ -382,15 +391,11 @@ int build_fused_mma(Ctx* c, int R, bool shared) {
   std::vector<int> incs;
   std::vector<int> written(ncnt, 0);
   double flops = 0;
-  auto counter = [&](long long off, int r) { return (int)((off - r) / ((long long)n * R)) * nch + r / 32; };
-  // fill tasks and split-K pairs are k_zmma2_df's (launch_zmma_fused): not with
-  // HS_ZMMA2=0 or the shared maps with R > 1 (k_zmma_fused)
-  static const bool z2 = !(getenv("HS_ZMMA2") && atoi(getenv("HS_ZMMA2")) == 0);
-  const bool df = z2 && (!shared || R == 1);
+  auto counter = [&](long long off, int r) { return (int)((off - r) / ((long long)n * R)) * nch + r / cwd; };
   auto add = [&](const DevStep& st, int phase) {
     std::vector<MmaTask> tasks;
     std::vector<MmaCol> sc;
-    build_mma_host(c, st.host, R, shared, tasks, sc, flops);
+    build_mma_host(c, st.host, R, shared, tasks, sc, flops, cwd);
     std::vector<int> inc_step;
     const int cbase = (int)cols.size();
     cols.insert(cols.end(), sc.begin(), sc.end());
@@ -432,7 +437,7 @@ int build_fused_mma(Ctx* c, int R, bool shared) {
     for (int b : c->mo_zero_host)
       for (int ch = 0; ch < nch; ++ch) fc.push_back(b * nch + ch);
     // ~4k elements per fill task
-    const int per = std::max(1, 4096 / (n * std::min(R, 32)));
+    const int per = std::max(1, 4096 / (n * std::min(R, cwd)));
     for (size_t i = 0; i < fc.size(); i += per) {
       FusedMmaTask ft;
       ft.task = MmaTask();
@@ -487,9 +492,14 @@ int build_fused_mma(Ctx* c, int R, bool shared) {
         // a pair's completions are its second arrival's: counted once, on half 1
         if (ftasks[t].ks != 0)
           tinc[t].assign(incs.begin() + ftasks[t].inc0, incs.begin() + ftasks[t].inc0 + ftasks[t].ninc);
-        cost[t] = ftasks[t].phase == 3 ? 0.5 : ftasks[t].task.K / 32 / (ftasks[t].ks >= 0 ? 2 : 1);
+        // us: a 32-position chunk of a 16-column task contracts in ~0.55 us, of a
+        // 32-column task in ~0.9 us (tensor-copy staged slabs; zmma_df_trace)
+        static const double us16 = getenv("HS_DF_COST16") ? atof(getenv("HS_DF_COST16")) : 0.55;
+        const double per_chunk = shared ? 1.0 : (cwd == 16 ? us16 : 0.9);
+        cost[t] = ftasks[t].phase == 3 ? 0.5 : per_chunk * (ftasks[t].task.K / 32) / (ftasks[t].ks >= 0 ? 2 : 1);
       }
-      ftasks = list_schedule(ftasks, deps, tinc, cost, ncnt, c->num_sms, 3e-6, 1e6);
+      static const double fixed_us = getenv("HS_DF_FIXED") ? atof(getenv("HS_DF_FIXED")) : 3.0;
+      ftasks = list_schedule(ftasks, deps, tinc, cost, ncnt, c->num_sms, fixed_us * 1e-6, 1e6);
     }
   }
   {
@@ -521,6 +531,7 @@ int build_fused_mma(Ctx* c, int R, bool shared) {
   for (const auto& ft : ftasks)
     if (ft.phase != 3) f.minK = std::min(f.minK, ft.task.K);
   f.R = R;
+  f.cw = cwd;
   f.shared = shared;
   f.built = true;
   return 0;

@@ -1,6 +1,7 @@
 // Context of one GPU (or plan-only) instance and the device data structures
 // shared by the kernels.  See include/hsb200.h for the C ABI.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -184,6 +185,7 @@ struct DevFusedMma {
   int minK = 0;             // smallest task K (split-K decision)
   double flops = 0;
   int R = 0;
+  int cw = 32;  // task / completion-counter width in right-hand sides (k_zmma2_df: 16 or 32)
   bool shared = false, built = false;
   int npairs_split = 0;          // split-K pairs (k_zmma2_df)
   double2* split_buf = nullptr;  // [pair][half][32 x 32] partial tiles
@@ -209,6 +211,10 @@ struct FusedMmaArgs {
   int* split_cnt = nullptr;
   const double2* zeros = nullptr;  // n-major form: the rows of absent faces and padding columns
   long long LR = 0;                // vector elements (bounds checks)
+  // k_zmma2_df, k-major slabs: the vectors zL, r, w, rp as [L][2 R] FP64 tensors,
+  // box (BN + 2 columns) x (32 positions): a chunk's slab rows in ONE tensor copy
+  int use_tm = 0;
+  alignas(64) CUtensorMap tm[4];
 };
 
 // Row-band ranks of the fused apply (multi-rank kernel instantiations): every

@@ -28,6 +28,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdint>
 #include <cstdlib>
 
 #include "hs_common.cuh"
@@ -1232,18 +1233,26 @@ void launch_zmma(Ctx& c, const DevMma& m, const double2* A, const double2* srcA,
 //   2 backward  y = T (w | rp):  w += y; z += y
 //   3 fill      (no y):          rp = w = 0; z = zL
 constexpr int kDfStages = 4;
+template <int BN>
 struct DfCols {
-  ZCols2<32> c;
+  ZCols2<BN> c;
   int phase, inc0, ninc, stop, ks, pair;
   unsigned long long* tr;
 };
 
-template <int S, bool NMAJ, int KC>
-__global__ void __launch_bounds__(Z2<32, 2, 2, NMAJ, S, false, 2, KC>::THREADS, 1) k_zmma2_df(FusedMmaArgs a) {
-  using F = Z2<32, 2, 2, NMAJ, S, false, 2, KC>;
+// BN = 16 (k-major slabs only): 32 x 16 tasks on four warp groups of two
+// quadrant warps (8 warps x 12 accumulator chains again), per-(block, 16-RHS
+// chunk) counters: twice the tasks at half the contraction each, for applies
+// that are bound by their dependency chain rather than by the flops.
+template <int S, bool NMAJ, int KC, int BN = 32>
+__global__ void __launch_bounds__(Z2<BN, 2, 2, NMAJ, S, false, 64 / BN, KC>::THREADS, 1)
+    k_zmma2_df(const __grid_constant__ FusedMmaArgs a) {
+  constexpr int KG = 64 / BN;  // warp groups splitting each chunk's k range
+  using F = Z2<BN, 2, 2, NMAJ, S, false, KG, KC>;
+  static_assert(BN == 32 || (BN == 16 && !NMAJ), "task width");
   extern __shared__ __align__(128) double2 sm[];
   __shared__ __align__(8) unsigned long long full[S], empty[S], dfull[2], dempty[2];
-  __shared__ DfCols zcs[2];
+  __shared__ DfCols<BN> zcs[2];
   double2* ys = sm + F::RING;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int n = a.n, R = a.R;
@@ -1257,7 +1266,7 @@ __global__ void __launch_bounds__(Z2<32, 2, 2, NMAJ, S, false, 2, KC>::THREADS, 
     long long g = 0;
     for (int it = 0;; ++it) {
       const int d = it & 1;
-      DfCols& zd = zcs[d];
+      DfCols<BN>& zd = zcs[d];
       z2_wait(&dempty[d], (unsigned)((it >> 1) & 1) ^ 1);
       int t = 0;
       if (lane == 0) t = atomicAdd(a.ticket, 1);
@@ -1274,8 +1283,8 @@ __global__ void __launch_bounds__(Z2<32, 2, 2, NMAJ, S, false, 2, KC>::THREADS, 
       const FusedMmaTask ft = a.tasks[t];
       const MmaTask tk = ft.task;
       // fill tasks (phase 3) carry no columns and no contraction
-      HS_DCHECK(ft.phase == 3 ? tk.ncols == 0 && tk.K == 0 : tk.ncols >= 1 && tk.ncols <= 32 && tk.K % KC == 0, DBG_INDEX);
-      for (int j = lane; j < 32; j += 32) {
+      HS_DCHECK(ft.phase == 3 ? tk.ncols == 0 && tk.K == 0 : tk.ncols >= 1 && tk.ncols <= BN && tk.K % KC == 0, DBG_INDEX);
+      for (int j = lane; j < BN; j += 32) {
         if (j < tk.ncols) {
           const MmaCol c = a.cols[tk.col0 + j];
 #pragma unroll
@@ -1323,10 +1332,16 @@ __global__ void __launch_bounds__(Z2<32, 2, 2, NMAJ, S, false, 2, KC>::THREADS, 
       const int kc0 = ft.ks == 1 ? nkall / 2 : 0;
       const int nk = ft.ks == 0 ? nkall / 2 : nkall - kc0;
       // n-major: all 32 column rows (absent faces and padding columns read zeros)
+      // (a tensor copy of the slab rows always delivers its whole box: BN + 2 columns)
+      const bool tmb = !NMAJ && a.use_tm;
       const unsigned bytes = (unsigned)(KC * 32 * sizeof(double2)) +
-                             (unsigned)(KC * (NMAJ ? 32 : tk.ncols) * sizeof(double2));
+                             (unsigned)(KC * (NMAJ ? 32 : (tmb ? BN + 2 : tk.ncols)) * sizeof(double2));
       const double2* Ab = a.A + tk.a_off;
       const double2* base = NMAJ ? nullptr : (zd.c.alt[0] ? srcB : srcA) + zd.c.in[0][0];
+      // tensor-copy coordinates of the slab: vector (zL, r, w, rp), first row, first column (in doubles)
+      const int tmi = ft.phase == 2 ? (zd.c.alt[0] ? 3 : 2) : ((ft.phase == 0 && zd.c.alt[0]) ? 1 : 0);
+      const int tmx = 2 * zd.c.r[0];
+      const int tmy = NMAJ ? 0 : (int)((zd.c.in[0][0] - zd.c.r[0]) / R);
       auto issueA = [&](int st, int kc) {
         if (lane == 0)
           z2_copy(sm + (size_t)st * F::STAGE, Ab + (long long)kc * KC * 32, KC * 32 * sizeof(double2), &full[st]);
@@ -1342,9 +1357,23 @@ __global__ void __launch_bounds__(Z2<32, 2, 2, NMAJ, S, false, 2, KC>::THREADS, 
           const double2* src = off >= 0 ? (zd.c.alt[j] ? srcB : srcA) + off + (long long)p0 * R : a.zeros;
           z2_copy(sb + j * F::SB, src, KC * sizeof(double2), &full[st]);
         } else {
-          const double2* b0 = base + (long long)kc * KC * R;
-          for (int r = lane; r < KC; r += 32)
-            z2_copy(sb + r * F::SB, b0 + (long long)r * R, tk.ncols * sizeof(double2), &full[st]);
+          if (tmb) {
+            // ONE tensor copy of the chunk's KC slab rows x (BN + 2) columns (the
+            // padded row stride of the fragment loads; columns past R read as
+            // zeros).  A bulk copy per row kept the TMA unit busy ~60 cycles per
+            // row, ~1 us per chunk: that, not the DMMAs, bounded a contraction.
+            HS_DCHECK(tmy >= 0 && (long long)(tmy + (kc + 1) * KC) * R <= a.LR, DBG_VEC);
+            if (lane == 0)
+              asm volatile(
+                  "cp.async.bulk.tensor.2d.shared::cta.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                      z2_smem(sb)),
+                  "l"(&a.tm[tmi]), "r"(tmx), "r"(tmy + kc * KC), "r"(z2_smem(&full[st]))
+                  : "memory");
+          } else {
+            const double2* b0 = base + (long long)kc * KC * R;
+            for (int r = lane; r < KC; r += 32)
+              z2_copy(sb + r * F::SB, b0 + (long long)r * R, tk.ncols * sizeof(double2), &full[st]);
+          }
         }
       };
       // the map chunks of the first stages stream while the dependencies settle
@@ -1382,29 +1411,29 @@ __global__ void __launch_bounds__(Z2<32, 2, 2, NMAJ, S, false, 2, KC>::THREADS, 
   const int kg = warp / F::NWQ, wq = warp % F::NWQ;
   const int wm = wq / F::WN, wn = wq % F::WN;
   const int gid = lane >> 2, tig = lane & 3;
-  constexpr int KH = KC / 2;
+  constexpr int KH = KC / KG;
   constexpr int NT = 2 * 2 * 2;
   // output element el of the 32 x 32 tile: k-major row-major (consecutive
   // right-hand sides), n-major column-major (consecutive rows of a column)
-  auto el_rr = [](int el) { return NMAJ ? el % 32 : el / 32; };
-  auto el_j = [](int el) { return NMAJ ? el / 32 : el % 32; };
+  auto el_rr = [](int el) { return NMAJ ? el % 32 : el / BN; };
+  auto el_j = [](int el) { return NMAJ ? el / 32 : el % BN; };
   long long g = 0;
   for (int it = 0;; ++it) {
     const int d = it & 1;
     z2_wait(&dfull[d], (unsigned)((it >> 1) & 1));
-    const DfCols& zd = zcs[d];
+    const DfCols<BN>& zd = zcs[d];
     if (zd.stop) break;
     const MmaTask tk = zd.c.tk;
     const int phase = zd.phase, ks = zd.ks;
     unsigned long long* tr = zd.tr;
     if (phase == 3) {
       // fill: counter k2 = block * nch + RHS chunk covers positions 0..n-1 of
-      // the block, right-hand sides 32 ch .. 32 ch + 31 (< R)
-      const int nch = (R + 31) / 32, cw = R < 32 ? R : 32;
+      // the block, right-hand sides BN ch .. BN ch + BN - 1 (< R)
+      const int nch = (R + BN - 1) / BN, cw = R < BN ? R : BN;
       const int per = n * cw;
       for (int i = 0; i < zd.ninc; ++i) {
         const int k2 = a.incs[zd.inc0 + i];
-        const int blk = k2 / nch, r0 = (k2 - blk * nch) * 32;
+        const int blk = k2 / nch, r0 = (k2 - blk * nch) * BN;
         for (int e = tid; e < per; e += F::NWC * 32) {
           const int p = e / cw, r = r0 + e - (e / cw) * cw;
           if (r >= R) continue;
@@ -1506,17 +1535,18 @@ __global__ void __launch_bounds__(Z2<32, 2, 2, NMAJ, S, false, 2, KC>::THREADS, 
           ci[x][y][c] = p3[x][y][c] - s1 - s2;
         }
     if (tr && tid == 0) tr[3] = z2_gtimer();
-    // group 1 hands its partial tile to group 0 through the output-tile buffer's
-    // tail; group 0 adds it and writes the tile
+    // groups 1 .. KG-1 hand their partial tiles to group 0 through the area past
+    // the output tile; group 0 adds them in group order and writes the tile
     double2* red = ys + 32 * F::YS;
     consumers_bar<F::NWC * 32>();  // the previous task's tile readers are done
-    if (kg == 1) {
+    if (kg > 0) {
+      double2* mine = red + (size_t)(kg - 1) * F::NWQ * NT * 32;
 #pragma unroll
       for (int x = 0; x < 2; ++x)
 #pragma unroll
         for (int y = 0; y < 2; ++y)
 #pragma unroll
-          for (int c = 0; c < 2; ++c) red[(wq * NT + (x * 2 + y) * 2 + c) * 32 + lane] = make_double2(cr[x][y][c], ci[x][y][c]);
+          for (int c = 0; c < 2; ++c) mine[(wq * NT + (x * 2 + y) * 2 + c) * 32 + lane] = make_double2(cr[x][y][c], ci[x][y][c]);
     }
     consumers_bar<F::NWC * 32>();
     if (kg == 0) {
@@ -1526,9 +1556,14 @@ __global__ void __launch_bounds__(Z2<32, 2, 2, NMAJ, S, false, 2, KC>::THREADS, 
         for (int y = 0; y < 2; ++y)
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
-            const double2 o = red[(wq * NT + (x * 2 + y) * 2 + c) * 32 + lane];
-            ys[((wm * 2 + x) * 8 + gid) * F::YS + (wn * 2 + y) * 8 + 2 * tig + c] =
-                make_double2(cr[x][y][c] + o.x, ci[x][y][c] + o.y);
+            double2 t = make_double2(cr[x][y][c], ci[x][y][c]);
+#pragma unroll
+            for (int g2 = 1; g2 < KG; ++g2) {
+              const double2 o = red[(size_t)(g2 - 1) * F::NWQ * NT * 32 + (wq * NT + (x * 2 + y) * 2 + c) * 32 + lane];
+              t.x += o.x;
+              t.y += o.y;
+            }
+            ys[((wm * 2 + x) * 8 + gid) * F::YS + (wn * 2 + y) * 8 + 2 * tig + c] = t;
           }
     }
     consumers_bar<F::NWC * 32>();
@@ -1598,6 +1633,30 @@ __global__ void __launch_bounds__(Z2<32, 2, 2, NMAJ, S, false, 2, KC>::THREADS, 
   }
 }
 
+// vec as a [L][2 R] FP64 tensor, box = (2 cols doubles) x rows; false when the
+// driver entry point or the encoding is not available (the caller falls back
+// to a bulk copy per row)
+static bool encode_slab_tensor(CUtensorMap* tm, const double2* vec, long long L, int R, int cols, int rows) {
+  typedef CUresult (*Encode)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                             const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                             CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode enc = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return (Encode)fn;
+  }();
+  if (!enc || ((uintptr_t)vec & 15) || L <= 0) return false;
+  const cuuint64_t gdim[2] = {(cuuint64_t)2 * R, (cuuint64_t)L};
+  const cuuint64_t gstr[1] = {(cuuint64_t)R * sizeof(double2)};
+  const cuuint32_t box[2] = {(cuuint32_t)2 * cols, (cuuint32_t)rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)vec, gdim, gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 cudaError_t launch_zmma_fused(Ctx& c, const DevFusedMma& f, FusedMmaArgs a) {
   cudaError_t e = cudaMemsetAsync(f.counters, 0, (f.ncounters + 1) * sizeof(int), c.stream);
   if (e != cudaSuccess) return e;
@@ -1620,15 +1679,25 @@ cudaError_t launch_zmma_fused(Ctx& c, const DevFusedMma& f, FusedMmaArgs a) {
     }
     a.zeros = c.zeros;
     a.LR = c.plan.L * (long long)f.R;
+    // the slab rows of the k-major form by tensor copies (HS_ZMMA2_DF_TM=0: a bulk copy per row)
+    static const bool tm_env = !(getenv("HS_ZMMA2_DF_TM") && atoi(getenv("HS_ZMMA2_DF_TM")) == 0);
+    if (!nmaj && tm_env && f.R >= f.cw + 2) {
+      const double2* vecs[4] = {a.zL, a.r, a.w, a.rp};
+      a.use_tm = 1;
+      for (int i = 0; i < 4 && a.use_tm; ++i)
+        if (!encode_slab_tensor(&a.tm[i], vecs[i], c.plan.L, f.R, f.cw + 2, 32)) a.use_tm = 0;
+    }
     auto go = [&](auto kern, auto tag) -> cudaError_t {
       using F = decltype(tag);
-      constexpr size_t smem = F::SMEM + sizeof(double2) * 32 * F::YS + sizeof(double2) * F::NWQ * 8 * 32;
+      constexpr size_t smem =
+          F::SMEM + sizeof(double2) * 32 * F::YS + sizeof(double2) * (F::NWC / F::NWQ - 1) * F::NWQ * 8 * 32;
       const cudaError_t at = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (at != cudaSuccess) return at;
       c.launches++;
       kern<<<std::min(f.ntasks, c.num_sms), F::THREADS, smem, c.stream>>>(a);
       return cudaGetLastError();
     };
+    if (!nmaj && f.cw == 16) return go(k_zmma2_df<kDfStages, false, 32, 16>, Z2<16, 2, 2, false, kDfStages, false, 4>());
     if (!nmaj) return go(k_zmma2_df<kDfStages, false, 32>, Z2<32, 2, 2, false, kDfStages, false, 2>());
     if (kc64 && c.n % 64 == 0 && f.minK % 64 == 0)
       return go(k_zmma2_df<2, true, 64>, Z2<32, 2, 2, true, 2, false, 2, 64>());
