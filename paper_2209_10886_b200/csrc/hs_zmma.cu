@@ -1681,7 +1681,7 @@ cudaError_t launch_zmma_fused(Ctx& c, const DevFusedMma& f, FusedMmaArgs a) {
     a.LR = c.plan.L * (long long)f.R;
     // the slab rows of the k-major form by tensor copies (HS_ZMMA2_DF_TM=0: a bulk copy per row)
     static const bool tm_env = !(getenv("HS_ZMMA2_DF_TM") && atoi(getenv("HS_ZMMA2_DF_TM")) == 0);
-    if (!nmaj && tm_env && f.R >= f.cw + 2) {
+    if (!nmaj && tm_env) {  // (a box wider than the R columns reads zeros past them: tests at R = 16)
       const double2* vecs[4] = {a.zL, a.r, a.w, a.rp};
       a.use_tm = 1;
       for (int i = 0; i < 4 && a.use_tm; ++i)
