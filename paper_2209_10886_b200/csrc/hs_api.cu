@@ -2480,9 +2480,11 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
   }
   if (cgsgR) {
     const size_t g2 = 2 * (size_t)c->num_sms;
-    if (ws_get(c, "part3", g2 * (2 * maxit + 3) * R, &part3) || ws_get(c, "hbuf", ((size_t)3 * maxit + 6) * R, &hbuf) ||
+    if (ws_get(c, "part3", g2 * (2 * maxit + 3) * R, &part3) || ws_get(c, "hbuf", ((size_t)3 * maxit + 6) * R + 1, &hbuf) ||
         ws_get(c, "gram", (size_t)R * (maxit + 1) * (maxit + 1), &gram))
       return -1;
+    // the coefficient kernels' active-count / ticket pair, past the buffer's data
+    CK(cudaMemsetAsync(hbuf + ((size_t)3 * maxit + 6) * R, 0, sizeof(double2), c->stream));
   }
   GmresDev G;
   G.LR = LR; G.R = R; G.tol = tol;
@@ -2551,8 +2553,8 @@ int hs_gmres(hs_ctx* c, int pc, const double* b, double* x, int R, double tol, i
       }
     }
     if (cgsgR) {
-      CK(gmres_arnoldi_cgsgR(*c, G, k, part3, hbuf, gram, maxit + 1));
-      CK(gmres_givens(*c, G, k));
+      CK(gmres_arnoldi_cgsgR(*c, G, k, part3, hbuf, gram, maxit + 1,
+                             (int*)(hbuf + ((size_t)3 * maxit + 6) * R)));  // includes the Givens update
     } else if (cgsg) {
       // one rank owns every block, in order: identity element mapping
       CK(gmres_arnoldi_cgsg(*c, G, k, c->plan.nranks == 1 ? nullptr : c->d_owned, c->n_owned, part3, hbuf, gram,

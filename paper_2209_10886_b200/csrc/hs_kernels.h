@@ -114,9 +114,10 @@ cudaError_t gmres_arnoldi_cgs2(Ctx& c, GmresDev& G, int k, const int* blocks, in
 // in-place sum over ranks (implemented next to the NCCL calls in hs_api.cu)
 cudaError_t gmres_arnoldi_cgsg(Ctx& c, GmresDev& G, int k, const int* blocks, int nb, double2* part,
                                double2* red, double2* Gm, int ldg, void* nccl_comm);
-// the same for R right-hand sides on one rank (k_givens follows); ok: sizes fit
+// the same for R right-hand sides on one rank (Givens included); ok: sizes fit
 bool gmres_cgsgR_ok(Ctx& c, long long LR, int R, int maxit);
-cudaError_t gmres_arnoldi_cgsgR(Ctx& c, GmresDev& G, int k, double2* part, double2* red, double2* Gm, int ldg);
+cudaError_t gmres_arnoldi_cgsgR(Ctx& c, GmresDev& G, int k, double2* part, double2* red, double2* Gm, int ldg,
+                                int* sync);  // sync: two zeroed ints
 cudaError_t allreduce_sum_doubles(Ctx& c, double* buf, size_t count, void* nccl_comm);
 cudaError_t launch_peer_allreduce(Ctx& c, const PeerRedArgs& a);
 // first device-check failure of each translation unit (0: none; debug library only)

@@ -934,7 +934,7 @@ cudaError_t gmres_arnoldi_cgsg(Ctx& c, GmresDev& G, int k, const int* blocks, in
 // basis vector*: ~12 us per j at cfg4, where the vector itself streams in 2 us)
 // by four launches per iteration: all inner products in one pass over V,
 // one reduction over the CTAs, the coefficients per right-hand side, one
-// update pass.  k_givens follows as after k_mgs.
+// update pass; the Givens update rides in the coefficient kernel.
 //   part: [grid][2 (k+1) + 1][R]   red: [2 (k+1) + 1][R]   cbuf: [k + 2][R]
 template <int NC>
 __global__ void __launch_bounds__(256) k_cgsgR_dots(GmresDev G, int k, long long npos, long long per, double2* part,
@@ -1047,8 +1047,12 @@ __global__ void __launch_bounds__(256) k_cgsgR_reduce(const double2* __restrict_
 // One CTA per right-hand side r: its new Gram row, c = 2 h - G h, the new norm
 // by expansion, H[:, k] and ||w|| (k_cgsg_coef's arithmetic; the Givens update
 // is k_givens').  Gm: R matrices of ldg x ldg, row-major, Hermitian.
+// The Givens update of the column follows in the same CTA (thread 0, as
+// k_givens does per column); the CTAs count the still-active right-hand sides
+// through sync[0] and a ticket sync[1] (the last one publishes the count and
+// resets both).
 __global__ void __launch_bounds__(256) k_cgsgR_coef(GmresDev G, int k, const double2* red, double2* Gm, int ldg,
-                                                    double2* cbuf) {
+                                                    double2* cbuf, int* sync) {
   extern __shared__ double2 sh[];  // h, c, Gh, Gc (k+1 each), 2 (k+1) terms
   const int R = G.R, r = blockIdx.x;
   const int kp1 = k + 1;
@@ -1103,6 +1107,15 @@ __global__ void __launch_bounds__(256) k_cgsgR_coef(GmresDev G, int k, const dou
     G.wnorm0[r] = sqrt(w2);
     cbuf[(long long)kp1 * R + r] = make_double2(hn, 0);
     Hk[(long long)kp1 * R + r] = make_double2(hn, 0);
+    // (the column's entries above were written by this CTA's other threads before the barrier)
+    const int act = givens_column(G, k, r) ? 1 : 0;
+    atomicAdd(&sync[0], act);
+    __threadfence();
+    if (atomicAdd(&sync[1], 1) == R - 1) {
+      *G.nactive = atomicAdd(&sync[0], 0);
+      sync[0] = 0;
+      sync[1] = 0;
+    }
   }
 }
 
@@ -1131,7 +1144,8 @@ bool gmres_cgsgR_ok(Ctx& c, long long LR, int R, int maxit) {
   return (double)R * (maxit + 1) * (maxit + 1) * sizeof(double2) <= 2e9;  // the Gram matrices
 }
 
-cudaError_t gmres_arnoldi_cgsgR(Ctx& c, GmresDev& G, int k, double2* part, double2* red, double2* Gm, int ldg) {
+cudaError_t gmres_arnoldi_cgsgR(Ctx& c, GmresDev& G, int k, double2* part, double2* red, double2* Gm, int ldg,
+                                int* sync) {
   const int grid = cgsgR_grid(c), R = G.R;
   const int kp1 = k + 1, cnt = 2 * kp1 + 1;
   const long long npos = G.LR / R, per = (npos + grid - 1) / grid;
@@ -1155,7 +1169,7 @@ cudaError_t gmres_arnoldi_cgsgR(Ctx& c, GmresDev& G, int k, double2* part, doubl
   const long long total = (long long)cnt * R;
   k_cgsgR_reduce<<<(unsigned)((total + 31) / 32), 256, 0, c.stream>>>(part, grid, total, red);
   double2* cbuf = red + total;  // c (k+1 rows of R) + ||w''||
-  k_cgsgR_coef<<<R, 256, (size_t)(5 * kp1 + 2) * sizeof(double2), c.stream>>>(G, k, red, Gm, ldg, cbuf);
+  k_cgsgR_coef<<<R, 256, (size_t)(5 * kp1 + 2) * sizeof(double2), c.stream>>>(G, k, red, Gm, ldg, cbuf, sync);
   const int ug = (int)std::min<long long>((long long)grid * 4, std::max<long long>(1, (G.LR + 255) / 256));
   k_cgsgR_update<<<ug, 256, 0, c.stream>>>(G, k, cbuf);
   return cudaGetLastError();
