@@ -144,13 +144,14 @@ constexpr int kGjCW = GJ_CW, kGjThreads = 32 / kGjCW * 32;
 //                the other CTAs copy the panels A[J, :] and A[:, J];
 //   k_gj_update: each 32 x 32 tile forms its row-panel tile P^{-1} A[J, cols]
 //                and applies the trailing update.
-// k_gj_inv keeps P in registers (in place: see the kernel): warp w owns columns
-// [8w, 8w + 8), lane = row.  The warp owning column p finds the pivot and
+// k_gj_inv keeps P in registers (in place: see the kernel): warp w owns kGjCW
+// columns, lane = row.  The warp owning column p finds the pivot and
 // publishes the column and the pivot's inverse (double-buffered by step
 // parity); every warp then scales the pivot row and eliminates its columns
 // with warp shuffles, one barrier per step (the shared-memory form had five
-// and took 57 us per panel, the augmented [P | I] register form 23).
-// grid (ncls), block 256
+// and took 57 us per panel, the augmented [P | I] register form 23, this one
+// ~16).
+// grid (1 + 8 copy CTAs, ncls), block kGjThreads
 __global__ void __launch_bounds__(kGjThreads) k_gj_inv(const double2* X, long long xstride, int k, int n, int j0,
                                                 int nb, double2* Pinv, double2* Bp, double2* Cp,
                                                 long long pstride, int* bad) {
@@ -183,12 +184,11 @@ __global__ void __launch_bounds__(kGjThreads) k_gj_inv(const double2* X, long lo
   // In-place Gauss-Jordan: warp w owns columns [CW w, CW w + CW) of P, lane =
   // row.  The identity column that the augmented form [P | I] would bring in at
   // step p (the pivot row's) takes the place of column p, which that step turns
-  // into a unit vector.  Few columns per warp and several warps per scheduler:
-  // a step's critical chain (publish -> update of the next pivot column ->
-  // search -> publish) is ~40 dependent instructions, and with 8 columns per
-  // warp on one warp per scheduler the other columns' updates sat in the same
-  // in-order stream (1100 cycles per step, ncu).  perm[u]: which column of
-  // P^{-1} the register column holds at the end.
+  // into a unit vector.  A step is a dependent chain (read the published
+  // pivot -> update the next pivot column -> reciprocal and search -> publish
+  // -> barrier) of ~470 ns whatever the columns per warp (tools/gjinv_bench.cu:
+  // 1, 2, 4, 8 columns within 10 %; 2 is the in-situ best by a little).
+  // perm[u]: which column of P^{-1} the register column holds at the end.
   constexpr int CW = kGjCW;
   double2 a[CW];
   int perm[CW];
