@@ -209,3 +209,17 @@ def test_schur_maps_odd_sizes(n):
     from oracle import Interface
     itf = Interface(prob, lat, backend="schur")
     assert relerr(s.apply_interface_operator(g).cpu().numpy(), itf.apply_A(cvec(5, s.layout.size))) < 1e-11
+
+
+def test_refactorisation_is_bitwise_reproducible():
+    """The factorisation runs its two elimination chains and their forward
+    solves on four streams: refactorising must give bitwise the same maps
+    (a missed cross-stream dependency would show up as a different map)."""
+    s = system("cfg2")
+    _, lat = oracle_problem(CASES["cfg2"])
+    picks = [lat.subs[0], lat.subs[len(lat.subs) // 2], lat.subs[-1]]
+    ref = [s.schur_map(q).copy() for q in picks]
+    for _ in range(5):
+        s.ctx.call("hs_factor")
+        for q, T in zip(picks, ref):
+            assert np.array_equal(s.schur_map(q), T)
