@@ -10,7 +10,10 @@
   iterations identical;
 * the blocked variants (M = 1, 2, 4; environment HS_MGS1_BLOCK, read once per
   process: run in subprocesses) give the same iterations and histories within
-  1e-12 of each other.
+  1e-12 of each other;
+* R right-hand sides: the column-wise one-reduction CGS2 (k_cgsgR_*, the
+  default for 2 <= R <= 128 on one GPU) against the cooperative MGS kernel and
+  against the single-RHS solve of a column.
 """
 
 import json
