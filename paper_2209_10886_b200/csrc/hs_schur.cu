@@ -690,9 +690,9 @@ struct Twist {
 // Four streams: one per chain for the panel steps (the chains are independent
 // until row m; high priority, so their small latency-bound kernels are not
 // queued behind full-grid GEMMs), and one per chain for the forward solve step
-// of row k (it only needs X_k) while the chain factors its next rows.  Row m, the backward sweeps
-// (again one stream per half) and the extraction follow.  Rp / Cp / Bk hold
-// two slices (2 * ncls classes' worth), one per chain.
+// of row k (it only needs X_k) while the chain factors its next rows.  Row m,
+// the backward sweeps (again one stream per half) and the extraction follow.
+// Rp / Cp / Bk hold two slices (2 * ncls classes' worth), one per chain.
 cudaError_t factor_and_solve_boundary(Ctx& c, double2* X, long long xstride, const uint8_t* dmasks, int ncls,
                                       double2* Rp, double2* Cp, long long pstride, int* dbad, int R, int nunit,
                                       const ExtraRHS* extras, double2* Y, long long ystride, double2* Bk,
